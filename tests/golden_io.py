@@ -1,0 +1,26 @@
+"""Loader for the committed golden fixtures (tests/golden, made by
+oracle/make_golden.py from the real reference)."""
+import json
+import os
+from functools import lru_cache
+
+import numpy as np
+
+GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+
+
+@lru_cache(maxsize=None)
+def manifest():
+    with open(os.path.join(GOLDEN, "manifest.json")) as fh:
+        return json.load(fh)
+
+
+def case(name):
+    """(arrays, meta) of one golden case."""
+    with np.load(os.path.join(GOLDEN, f"{name}.npz")) as z:
+        arrs = {k: z[k] for k in z.files}
+    return arrs, manifest()["cases"][name]
+
+
+def names(prefix):
+    return sorted(k for k in manifest()["cases"] if k.startswith(prefix))

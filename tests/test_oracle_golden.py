@@ -1,0 +1,196 @@
+"""Pin the CPU oracle against the real reference's outputs (CPU, no GPU).
+
+The golden fixtures were produced by ``oracle/make_golden.py`` running the
+unmodified reference (``pintlab``) in this container; the oracle must
+reproduce every one of them bit for bit.  This is what licenses using the
+oracle as the checker for the CUDA path on the GPU box, where the reference
+itself is absent.
+"""
+import numpy as np
+import pytest
+
+from oracle import pintlab_oracle as O
+from tests.golden_io import case, names
+
+
+def eq(a, b):
+    assert a.shape == b.shape
+    assert np.array_equal(a, b), f"max diff {np.max(np.abs(a - b))}"
+
+
+@pytest.mark.parametrize("name", names("apply_"))
+def test_apply_diag(name):
+    a, m = case(name)
+    op = O.Op(m["dim"], m["n"], m["nu"], m["order"], m.get("length", 1.0))
+    eq(O.heat_apply(op, a["u"]), a["f"])
+    eq(O.heat_diagonal(op), a["diag"])
+    if "au" in a:
+        eq(O.shifted_apply(op, m["sigma"], a["u"]), a["au"])
+        eq(O.shifted_diag(op, m["sigma"]), a["sdiag"])
+
+
+@pytest.mark.parametrize("name", names("transfer_"))
+def test_transfers(name):
+    a, _ = case(name)
+    eq(O.full_weighting(a["u"]), a["fw"])
+    eq(O.inject(a["u"]), a["inj"])
+    eq(O.interp_linear(a["c"]), a["lin"])
+    eq(O.interp_cubic(a["c"]), a["cub"])
+
+
+@pytest.mark.parametrize("name", names("cubic_1d_"))
+def test_cubic_matrix(name):
+    a, m = case(name)
+    eq(O.cubic_matrix(m["nf"]), a["mat"])
+    eq(O.interp_cubic(a["c"]), a["cub"])
+
+
+@pytest.mark.parametrize("name", names("mg_"))
+def test_smoothers_vcycle(name):
+    a, m = case(name)
+    op = O.Op(m["dim"], m["n"], 1.0, m["order"])
+    cfg = O.Mg(m["smoother"], m["omega"], m["pre"], m["post"])
+    eq(O.smooth(op, m["sigma"], a["u"], a["b"], cfg, 2), a["sm2"])
+    eq(O.v_cycle(op, m["sigma"], a["u"], a["b"], cfg), a["vc"])
+    eq(O.v_cycle(op, m["sigma"], np.zeros_like(a["b"]), a["b"], cfg), a["vc0"])
+
+
+@pytest.mark.parametrize("name", names("coarsest_"))
+def test_coarsest(name):
+    a, m = case(name)
+    op = O.Op(m["dim"], 4)
+    eq(O.v_cycle(op, m["sigma"], np.zeros_like(a["b"]), a["b"], O.Mg()), a["u"])
+
+
+@pytest.mark.parametrize("name", names("solve_"))
+def test_policies(name):
+    a, m = case(name)
+    op = O.Op(m["dim"], m["n"])
+    s = m["sigma"]
+    u, c, st = O.mg_solve(op, s, a["u0"], a["b"], O.Mg(), O.Fixed(2))
+    eq(u, a["fixed2"])
+    assert (c, st) == (2, "fixed")
+    u, c, st = O.mg_solve(op, s, a["u0"], a["b"], O.Mg(), O.ToTol(1e-12))
+    eq(u, a["tol"])
+    assert (c, st) == (m["tol_cycles"], m["tol_status"])
+    u, c, st = O.mg_solve(op, s, np.zeros_like(a["b"]), a["b"], O.Mg(pre_sweeps=0, post_sweeps=0),
+                          O.ToTol(1e-14))
+    eq(u, a["stall"])
+    assert (c, st) == (m["stall_cycles"], m["stall_status"])
+    with pytest.raises(O.MgCapError) as ei:
+        O.mg_solve(op, s, np.zeros_like(a["b"]), a["b"], O.Mg(),
+                   O.ToTol(1e-14, stall=1.0 - 1e-12, max_cycles=3))
+    assert ei.value.cycles == m["cap"]["cycles"]
+    assert ei.value.residual == m["cap"]["residual"]
+
+
+@pytest.mark.parametrize("name", names("sweep_"))
+def test_sweep_residual(name):
+    a, m = case(name)
+    op = O.Op(m["dim"], m["n"])
+    table = O.uniform_table(m["M"])
+    y = a["y"].copy()
+    st = O.States(table, y, np.stack([O.heat_apply(op, v) for v in y]))
+    pol = O.Fixed(1) if m["policy"] == "fixed1" else O.ToTol(1e-12)
+    log = []
+    cyc = O.sdc_sweep(st, a["y0"], m["dt"], op, O.Mg(), pol, tau=a.get("tau"), solve_log=log)
+    assert cyc == m["cycles"]
+    assert [[n, s, c, t] for n, s, c, t in log] == m["solves"]
+    eq(st.y, a["y_out"])
+    eq(st.f, a["f_out"])
+    assert O.residual(st, a["y0"], m["dt"], tau=a.get("tau")) == m["residual"]
+
+
+def _fas_levels(m):
+    return [O.Lvl(O.Op(m["dim"], n), O.uniform_table(M), O.Mg(), O.Fixed(1), m["interp"])
+            for n, M in zip(m["ns"], (4, 2, 1))]
+
+
+@pytest.mark.parametrize("name", names("fas_"))
+def test_fas(name):
+    a, m = case(name)
+    lv = _fas_levels(m)
+    f, c = lv[0], lv[1]
+    y = a["y"]
+    fst = O.States(f.table, y.copy(), np.stack([O.heat_apply(f.op, v) for v in y]))
+    rs = O.restrict_state(fst, f, c)
+    eq(rs.y, a["ry"])
+    eq(rs.f, a["rf"])
+    eq(O.compute_fas(fst, rs, f, c, m["dt"], fine_tau=a["ftau"]), a["tau"])
+    eq(O.compute_fas(fst, rs, f, c, m["dt"]), a["tau0"])
+    new = rs.copy()
+    new.y = a["newc"].copy()
+    cc = fst.copy()
+    O.coarse_correction(cc, rs, new, f, c)
+    eq(cc.y, a["cc_y"])
+    eq(cc.f, a["cc_f"])
+    # initialize_step + one 3-level MLSDC iteration (hierarchy.py:166-250)
+    ts = O.Step.spread(lv, a["u0"])
+    copies = [s.copy() for s in ts.states]
+    c0 = O.burn_in(ts, m["dt"], 1)
+    O.interpolate_up(ts, copies, exact_y0=a["u0"])
+    assert c0 == m["init_cycles"]
+    assert O.mlsdc_iteration(ts, m["dt"]) == m["it_cycles"]
+    assert O.residual(ts.states[0], ts.y0[0], m["dt"]) == m["residual"]
+    eq(ts.states[0].y, a["ml_y0"])
+    eq(ts.states[1].y, a["ml_y1"])
+    eq(ts.states[2].y, a["ml_y2"])
+    eq(ts.tau[1], a["ml_tau1"])
+    eq(ts.tau[2], a["ml_tau2"])
+
+
+def oracle_levels(m):
+    pol = O.Fixed(m["policy"][1]) if m["policy"][0] == "fixed" else \
+        O.ToTol(*m["policy"][1:])
+    orders = m.get("orders") or [2] * len(m["ns"])
+    return [O.Lvl(O.Op(m["d"], n, 1.0, o), O.uniform_table(k - 1),
+                  O.Mg(m["sm"], m["om"], m["pre"], m["post"]), pol, m.get("interp", 4))
+            for n, k, o in zip(m["ns"], m["nodes"], orders)]
+
+
+FAST_RUNS = ["run_cfg0", "run_cfg0_interp2", "run_cfg1", "run_cfg1_fc2", "run_same_n_3lvl",
+             "run_order4_small", "run_cfg4_small_tol", "run_cfg2_small"]
+SLOW_RUNS = ["run_cfg2_small_fc2", "run_cfg3_small", "run_cfg4_small"]
+
+
+@pytest.mark.parametrize("name", FAST_RUNS + [pytest.param(n, marks=pytest.mark.slow)
+                                              for n in SLOW_RUNS])
+def test_pfasst_runs(name):
+    a, m = case(name)
+    levels = oracle_levels(m)
+    t_end = m["dt"] * m["p"] * m["blocks"]
+    out = O.pfasst_run(levels, a["u0"], t_end, m["p"], m["blocks"], m["tol"], 20,
+                       record_final_values=True, log_solves=True)
+    assert out.rank_iterations == m["rank_iterations"]
+    assert out.rank_vcycles == m["rank_vcycles"]
+    assert out.converged == m["converged"]
+    assert [list(t) for t in out.trace] == m["trace"]
+    solves = [list(s) for blk in out.solve_log for s in blk]
+    assert solves == m["solves"]
+    eq(out.u, a["u"])
+    finals = out.final_values[-1][m["finals_kept_from"]:]
+    eq(np.stack(finals) if finals else np.zeros_like(a["finals"]), a["finals"])
+
+
+def test_serial_drivers():
+    a, m = case("serial_drivers")
+    lv = [O.Lvl(O.Op(1, n), O.uniform_table(k - 1), O.Mg(), O.Fixed(1), 4)
+          for n, k in ((64, 3), (32, 2))]
+    ml = O.run_mlsdc(lv, a["u0"], 0.25, 4, 1e-10, 20)
+    assert ml["iterations"] == m["ml_iterations"]
+    assert ml["residuals"] == m["ml_residuals"]
+    assert ml["vcycles"] == m["ml_vcycles"]
+    eq(ml["u"], a["ml_u"])
+    sd = O.run_sdc(lv[0].op, lv[0].table, a["u0"], 0.25, 4, 1e-10, 20, O.Mg(), O.Fixed(1))
+    assert sd["iterations"] == m["sdc_iterations"]
+    assert sd["residuals"] == m["sdc_residuals"]
+    assert sd["vcycles"] == m["sdc_vcycles"]
+    eq(sd["u"], a["sdc_u"])
+    p1 = O.pfasst_run(lv, a["u0"], 0.25 / 4, 1, tol=1e-10, max_iter=20)
+    eq(p1.u, a["p1_u"])
+    assert p1.rank_iterations == m["p1_iterations"]
+
+
+def test_seeded_field_matches_fixture():
+    a, _ = case("run_cfg2_small")
+    eq(O.seeded_field(2, 64), a["u0"])
