@@ -1,0 +1,153 @@
+"""ctypes binding of include/pintlab_b200.h (lib/libpintlab_b200.so).
+
+The product path has no fallback: if the library is missing this module
+raises on first use, and every CUDA failure surfaces as an exception.
+Status codes map to the reference's exception types (multigrid.py:77-83,
+sdc.py:75-81): PL_ERR_MGCAP -> MultigridError, negative -> ValueError /
+NotImplementedError, PL_ERR_CUDA -> RuntimeError.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+
+from ._build import LIB
+
+PL_OK, PL_ERR_MGCAP, PL_ERR_CUDA = 0, 1, 2
+PL_ERR_ARG, PL_ERR_UNSUPPORTED, PL_ERR_STATE = -1, -2, -3
+PL_MAX_NODES = 17
+SMOOTHERS = {"jacobi": 0, "gauss-seidel": 1, "jor-rb": 2}
+RESTRICT = {"full-weighting": 0, "inject": 1, "copy": 2}
+STATUS = {0: "fixed", 1: "converged", 2: "stalled"}
+NUM_KINDS = 16
+
+_lib = None
+_lock = threading.Lock()
+
+dp = C.POINTER(C.c_double)
+ip = C.POINTER(C.c_int)
+vp = C.c_void_p
+i32, i64, f64, sz = C.c_int, C.c_longlong, C.c_double, C.c_size_t
+
+
+class SweepDesc(C.Structure):
+    _fields_ = [("m", C.c_int),
+                ("qdelta", C.c_double * (PL_MAX_NODES * PL_MAX_NODES)),
+                ("gammas", C.c_double * PL_MAX_NODES),
+                ("policy", C.c_int),
+                ("fixed_cycles", C.c_int),
+                ("tol", C.c_double),
+                ("stall", C.c_double),
+                ("max_cycles", C.c_int)]
+
+
+_SIGS = {
+    "pl_abi_version": (i32, []),
+    "pl_last_error": (C.c_char_p, []),
+    "pl_heat_apply": (i32, [vp, vp, i32, i32, f64, f64, i32, vp]),
+    "pl_heat_diagonal": (i32, [vp, i32, i32, f64, f64, i32, f64, i32, vp]),
+    "pl_shifted_apply": (i32, [vp, vp, i32, i32, f64, f64, i32, f64, vp]),
+    "pl_full_weighting": (i32, [vp, vp, i32, i32, vp]),
+    "pl_inject": (i32, [vp, vp, i32, i32, vp]),
+    "pl_interp_linear": (i32, [vp, vp, i32, i32, i32, vp]),
+    "pl_interp_cubic_scratch_bytes": (sz, [i32, i32]),
+    "pl_interp_cubic": (i32, [vp, vp, i32, i32, i32, vp, vp]),
+    "pl_mg_workspace_bytes": (sz, [i32, i32, i32]),
+    "pl_mg_plan_create": (i32, [C.POINTER(vp), i32, i32, f64, f64, i32, i32, f64, i32, i32,
+                                i32, vp, sz]),
+    "pl_mg_plan_destroy": (i32, [vp]),
+    "pl_mg_prepare": (i32, [vp, f64, vp]),
+    "pl_mg_smooth": (i32, [vp, vp, vp, f64, i32, vp]),
+    "pl_mg_vcycles": (i32, [vp, vp, vp, f64, i32, i32, vp]),
+    "pl_mg_solve_tol": (i32, [vp, vp, vp, f64, f64, f64, i32, ip, ip, dp, vp]),
+    "pl_sweep_workspace_bytes": (sz, [i32, i32, i32]),
+    "pl_sdc_sweep": (i32, [vp, C.POINTER(SweepDesc), vp, vp, vp, vp, f64, vp, sz, ip, ip, dp,
+                           ip, vp]),
+    "pl_sdc_residual": (i32, [vp, vp, vp, vp, dp, i32, f64, i64, vp, vp]),
+    "pl_restrict_state": (i32, [vp, ip, i32, vp, vp, i32, i32, i32, i32, f64, f64, i32, vp]),
+    "pl_compute_fas": (i32, [vp, vp, i32, dp, ip, i32, vp, dp, i32, f64, vp, vp, i32, i32, i32,
+                             i32, vp]),
+    "pl_compute_fas_scratch_bytes": (sz, [i32, i32, i32]),
+    "pl_coarse_correction": (i32, [vp, vp, i32, vp, vp, i32, dp, i32, i32, i32, i32, f64, f64,
+                                   i32, vp, vp]),
+    "pl_coarse_correction_scratch_bytes": (sz, [i32, i32, i32, i32, i32]),
+    "pl_stats_reset": (i32, []),
+    "pl_stats_get": (i32, [C.POINTER(i64), dp, i32]),
+    "pl_timing_enable": (i32, [i32]),
+    "pl_timing_collect": (i32, [C.POINTER(i64), dp, dp]),
+    "pl_kind_name": (C.c_char_p, [i32]),
+}
+
+EXPORTED = tuple(_SIGS)
+
+
+def lib():
+    """Load the shared library (raises if it was not built)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    with _lock:
+        if _lib is None:
+            if not os.path.exists(LIB):
+                raise RuntimeError(
+                    f"CUDA library {LIB} is missing: run __graft_entry__.build() "
+                    "(there is no CPU fallback)")
+            h = C.CDLL(LIB)
+            for name, (res, args) in _SIGS.items():
+                fn = getattr(h, name)
+                fn.restype = res
+                fn.argtypes = args
+            if h.pl_abi_version() != 1:
+                raise RuntimeError("ABI version mismatch")
+            _lib = h
+    return _lib
+
+
+class MultigridErrorBase(RuntimeError):
+    pass
+
+
+def last_error():
+    return lib().pl_last_error().decode(errors="replace")
+
+
+def check(rc, what=""):
+    if rc == PL_OK:
+        return
+    msg = f"{what}: {last_error()}" if what else last_error()
+    if rc == PL_ERR_UNSUPPORTED:
+        raise NotImplementedError(msg)
+    if rc < 0:
+        raise ValueError(msg)
+    raise RuntimeError(msg)
+
+
+def stats():
+    """(launches, alg_bytes) per kernel kind since the last reset."""
+    n = (i64 * NUM_KINDS)()
+    b = (f64 * NUM_KINDS)()
+    lib().pl_stats_get(n, b, NUM_KINDS)
+    names = [lib().pl_kind_name(k).decode() for k in range(NUM_KINDS)]
+    return {names[k]: (int(n[k]), float(b[k])) for k in range(NUM_KINDS)}
+
+
+def stats_reset():
+    lib().pl_stats_reset()
+
+
+def kind_index(name):
+    for k in range(NUM_KINDS):
+        if lib().pl_kind_name(k).decode() == name:
+            return k
+    raise KeyError(name)
+
+
+def timing_enable(name):
+    lib().pl_timing_enable(-1 if name is None else kind_index(name))
+
+
+def timing_collect():
+    n, t, b = i64(0), f64(0), f64(0)
+    check(lib().pl_timing_collect(C.byref(n), C.byref(t), C.byref(b)))
+    return int(n.value), float(t.value), float(b.value)

@@ -1,0 +1,631 @@
+// Geometric multigrid V-cycle (multigrid.py:211-288) on B200.
+//
+// Levels whose whole remaining hierarchy fits in one SM's shared memory run
+// as ONE single-CTA "tail" kernel (smoothers, residual, full weighting,
+// dense LU on the coarsest grid, prolongation, post-smoothing) -- these
+// levels are latency-bound, and folding them into one launch removes ~7
+// launches per level.  Larger levels use the grid-wide HBM-streaming kernels
+// of stencil.cu / transfer.cu.  Both paths evaluate the same device
+// arithmetic (common.cuh / transfer_dev.cuh), so where a level runs does not
+// change a single bit of the result.
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <vector>
+
+#include "kernels.cuh"
+#include "mg.h"
+#include "transfer_dev.cuh"
+
+namespace pl {
+
+// ---------------------------------------------------------------------------
+// operator constants (heat.py:114, 148-152) computed with the same libm pow
+// the reference's Python floats use
+
+OpC make_opc(int n, double length, double nu, int order) {
+  static double (*volatile powp)(double, double) = std::pow;
+  OpC c;
+  volatile double dx = length / (double)n;
+  c.dx2 = powp(dx, 2.0);
+  int e;
+  double mant = std::frexp(c.dx2, &e);
+  c.pow2 = (mant == 0.5);
+  c.inv_dx2 = 1.0 / c.dx2;
+  c.d12 = 12.0 * c.dx2;
+  c.nu = nu;
+  c.order = order;
+  c.d1_edge = -2.0 / c.dx2;
+  c.d1_int = order == 2 ? -2.0 / c.dx2 : -30.0 / (12.0 * c.dx2);
+  return c;
+}
+
+// ---------------------------------------------------------------------------
+// single-CTA tail
+
+namespace {
+
+constexpr int TAIL_THREADS = 1024;
+constexpr int MAX_LEVELS = 16;
+constexpr size_t TAIL_SMEM_BUDGET = 200 * 1024;
+
+struct TailLevel {
+  Geo g;
+  OpC c;
+  int off_u, off_b, off_t;   // offsets (doubles) into shared memory
+  int coarsest;
+};
+
+struct TailArgs {
+  int nlev;
+  TailLevel lv[MAX_LEVELS];
+  int smoother, pre, post;
+  double omega, sigma;
+  const double* lu;   // m*m factors + m pivots (global, L1-cached)
+  int m;
+};
+
+#define PL_FOR_SM_POINTS(g)                                                  \
+  for (long long p = threadIdx.x; p < (g).npts; p += blockDim.x)
+
+__device__ __forceinline__ void decode(const Geo& g, long long p, int& x, int& y, int& z) {
+  x = (int)(p % g.nx);
+  long long r = p / g.nx;
+  y = (int)(r % g.ny);
+  z = (int)(r / g.ny);
+}
+
+// `count` sweeps on shared-memory level L; result ends in u.
+template <int DIM>
+__device__ void tail_smooth(const TailArgs& a, const TailLevel& L, double* sm, int count,
+                            bool zero) {
+  double* u = sm + L.off_u;
+  double* b = sm + L.off_b;
+  double* t = sm + L.off_t;
+  if (count == 0) {
+    if (zero) {
+      PL_FOR_SM_POINTS(L.g) u[p] = 0.0;
+      __syncthreads();
+    }
+    return;
+  }
+  if (a.smoother == SM_JACOBI) {
+    for (int k = 0; k < count; ++k) {
+      bool z0 = zero && k == 0;
+      PL_FOR_SM_POINTS(L.g) {
+        int x, y, z;
+        decode(L.g, p, x, y, z);
+        double d = shifted_diag<DIM>(L.g, L.c, a.sigma, x, y, z);
+        if (z0) {
+          t[p] = 0.0 + ((a.omega * b[p]) / d);
+        } else {
+          double au = shifted_point<DIM>(u, L.g, L.c, a.sigma, x, y, z, p);
+          t[p] = u[p] + ((a.omega * (b[p] - au)) / d);
+        }
+      }
+      __syncthreads();
+      PL_FOR_SM_POINTS(L.g) u[p] = t[p];
+      __syncthreads();
+    }
+    return;
+  }
+  // jor-rb: red then black per sweep; out of place (t) so that order-4
+  // same-colour neighbours read pre-update values like the reference.
+  if (zero) {
+    PL_FOR_SM_POINTS(L.g) u[p] = 0.0;
+    __syncthreads();
+  }
+  for (int k = 0; k < count; ++k) {
+    for (int colour = 1; colour >= 0; --colour) {
+      PL_FOR_SM_POINTS(L.g) {
+        int x, y, z;
+        decode(L.g, p, x, y, z);
+        if (is_red<DIM>(x, y, z) == (colour == 1)) {
+          double d = shifted_diag<DIM>(L.g, L.c, a.sigma, x, y, z);
+          double r = b[p] - shifted_point<DIM>(u, L.g, L.c, a.sigma, x, y, z, p);
+          t[p] = u[p] + ((a.omega * r) / d);
+        } else {
+          t[p] = u[p];
+        }
+      }
+      __syncthreads();
+      PL_FOR_SM_POINTS(L.g) u[p] = t[p];
+      __syncthreads();
+    }
+  }
+}
+
+// dense LU solve on the coarsest grid: b (smem) -> u (smem), one warp.
+// LAPACK getrs order: row interchanges, unit-lower forward, upper backward.
+__device__ void tail_lu(const TailArgs& a, const double* b, double* u) {
+  const int m = a.m;
+  const double* A = a.lu;
+  const double* piv = a.lu + (size_t)m * m;
+  if (threadIdx.x < 32) {
+    for (int i = threadIdx.x; i < m; i += 32) u[i] = b[i];
+    __syncwarp();
+    if (threadIdx.x == 0) {
+      for (int i = 0; i < m; ++i) {
+        int pi = (int)piv[i];
+        if (pi != i) {
+          double tmp = u[i];
+          u[i] = u[pi];
+          u[pi] = tmp;
+        }
+      }
+    }
+    __syncwarp();
+    for (int j = 0; j < m; ++j) {            // L y = Pb, column oriented
+      double yj = u[j];
+      __syncwarp();
+      for (int i = j + 1 + threadIdx.x; i < m; i += 32) u[i] = u[i] - A[i * m + j] * yj;
+      __syncwarp();
+    }
+    for (int j = m - 1; j >= 0; --j) {       // U x = y
+      if (threadIdx.x == 0) u[j] = u[j] / A[j * m + j];
+      __syncwarp();
+      double xj = u[j];
+      for (int i = threadIdx.x; i < j; i += 32) u[i] = u[i] - A[i * m + j] * xj;
+      __syncwarp();
+    }
+  }
+  __syncthreads();
+}
+
+template <int DIM>
+__global__ void __launch_bounds__(TAIL_THREADS) k_tail(TailArgs a,
+                                                       const double* __restrict__ b_in,
+                                                       double* u_io, int zero_guess,
+                                                       int ncycles) {
+  extern __shared__ double sm[];
+  const TailLevel& L0 = a.lv[0];
+  PL_FOR_SM_POINTS(L0.g) {
+    sm[L0.off_b + p] = b_in[p];
+    if (!zero_guess) sm[L0.off_u + p] = u_io[p];
+  }
+  __syncthreads();
+  for (int cyc = 0; cyc < ncycles; ++cyc) {
+    bool zero0 = zero_guess && cyc == 0;
+    int l = 0;
+    // ---- down: pre-smooth, residual, full weighting
+    for (; !a.lv[l].coarsest; ++l) {
+      const TailLevel& L = a.lv[l];
+      const TailLevel& C = a.lv[l + 1];
+      tail_smooth<DIM>(a, L, sm, a.pre, l == 0 ? zero0 : true);
+      double* u = sm + L.off_u;
+      double* b = sm + L.off_b;
+      double* t = sm + L.off_t;
+      PL_FOR_SM_POINTS(L.g) {
+        int x, y, z;
+        decode(L.g, p, x, y, z);
+        t[p] = b[p] - shifted_point<DIM>(u, L.g, L.c, a.sigma, x, y, z, p);
+      }
+      __syncthreads();
+      double* bc = sm + C.off_b;
+      PL_FOR_SM_POINTS(C.g) {
+        int x, y, z;
+        decode(C.g, p, x, y, z);
+        bc[p] = fw_point<DIM>(t, L.g, x, y, z);
+      }
+      __syncthreads();
+    }
+    // ---- coarsest: dense LU (ignores the initial guess, multigrid.py:240-243)
+    tail_lu(a, sm + a.lv[l].off_b, sm + a.lv[l].off_u);
+    // ---- up: prolongate, correct, post-smooth
+    for (--l; l >= 0; --l) {
+      const TailLevel& L = a.lv[l];
+      const TailLevel& C = a.lv[l + 1];
+      double* u = sm + L.off_u;
+      const double* ec = sm + C.off_u;
+      PL_FOR_SM_POINTS(L.g) {
+        int x, y, z;
+        decode(L.g, p, x, y, z);
+        u[p] = u[p] + lin_point<DIM>(ec, C.g, x, y, z);
+      }
+      __syncthreads();
+      tail_smooth<DIM>(a, L, sm, a.post, false);
+    }
+  }
+  PL_FOR_SM_POINTS(L0.g) u_io[p] = sm[L0.off_u + p];
+}
+
+}  // namespace
+
+static int launch_tail(MgPlan* P, int l0, double* u, const double* b, double sigma,
+                       int zero_guess, int ncycles, cudaStream_t s) {
+  TailArgs a;
+  std::memset(&a, 0, sizeof(a));
+  a.smoother = P->smoother;
+  a.pre = P->pre;
+  a.post = P->post;
+  a.omega = P->omega;
+  a.sigma = sigma;
+  a.m = P->m_lu;
+  auto it = P->lu.find(*(unsigned long long*)&sigma);
+  if (it == P->lu.end()) {
+    set_error("coarsest LU for sigma=%.17g not prepared", sigma);
+    return -3;
+  }
+  a.lu = it->second.dev;
+  int off = 0;
+  a.nlev = (int)P->lv.size() - l0;
+  for (int i = 0; i < a.nlev; ++i) {
+    const MgLevel& L = P->lv[l0 + i];
+    TailLevel& T = a.lv[i];
+    T.g = L.g;
+    T.c = L.c;
+    T.coarsest = L.coarsest;
+    int np = (int)L.g.npts;
+    T.off_u = off; off += np;
+    T.off_b = off; off += np;
+    T.off_t = off; off += np;
+  }
+  size_t smem = sizeof(double) * off;
+  void (*kern)(TailArgs, const double*, double*, int, int) =
+      P->dim == 1 ? k_tail<1> : (P->dim == 2 ? k_tail<2> : k_tail<3>);
+  static bool attr_set[4] = {false, false, false, false};
+  if (!attr_set[P->dim]) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)TAIL_SMEM_BUDGET + 8192);
+    attr_set[P->dim] = true;
+  }
+  PL_PRE(K_TAIL);
+  kern<<<1, TAIL_THREADS, smem, s>>>(a, b, u, zero_guess, ncycles);
+  double bytes = 8.0 * P->lv[l0].g.npts * (zero_guess ? 2 : 3);
+  PL_CHECK_LAUNCH(K_TAIL, bytes);
+  return 0;
+}
+
+// ---------------------------------------------------------------------------
+// plan
+
+static std::vector<int> level_ns(int n, int coarsest_n) {
+  std::vector<int> ns;
+  int m = n;
+  while (true) {
+    ns.push_back(m);
+    if (m <= coarsest_n || m < 4) break;
+    m /= 2;
+  }
+  return ns;
+}
+
+size_t mg_workspace_bytes(int dim, int n, int coarsest_n) {
+  std::vector<int> ns = level_ns(n, coarsest_n);
+  size_t total = 0;
+  for (size_t l = 0; l < ns.size(); ++l) {
+    Geo g = make_geo(dim, ns[l]);
+    size_t per = (l == 0 ? 1 : 3) * (size_t)g.npts;   // fine: t only; coarse: u, b, t
+    total += ((per * 8 + 255) / 256) * 256;
+  }
+  return total;
+}
+
+int mg_plan_create(MgPlan** out, int dim, int n, double length, double nu, int order,
+                   int smoother, double omega, int pre, int post, int coarsest_n, void* ws,
+                   size_t ws_bytes) {
+  if (dim < 1 || dim > 3 || n < 2 || (n & (n - 1))) {
+    set_error("bad grid dim=%d n=%d", dim, n);
+    return -1;
+  }
+  if (order != 2 && order != 4) {
+    set_error("stencil order must be 2 or 4");
+    return -1;
+  }
+  if (smoother != SM_JACOBI && smoother != SM_RB) {
+    set_error("smoother %d is not implemented on the GPU path", smoother);
+    return -2;
+  }
+  if (pre < 0 || post < 0 || coarsest_n < 2) {
+    set_error("bad MG configuration");
+    return -1;
+  }
+  size_t need = mg_workspace_bytes(dim, n, coarsest_n);
+  if (ws_bytes < need) {
+    set_error("MG workspace too small: %zu < %zu", ws_bytes, need);
+    return -1;
+  }
+  MgPlan* P = new MgPlan();
+  P->dim = dim; P->n = n; P->order = order; P->smoother = smoother;
+  P->pre = pre; P->post = post; P->coarsest_n = coarsest_n;
+  P->length = length; P->nu = nu; P->omega = omega;
+  P->ws = (char*)ws; P->ws_bytes = ws_bytes;
+  std::vector<int> ns = level_ns(n, coarsest_n);
+  char* cur = (char*)ws;
+  for (size_t l = 0; l < ns.size(); ++l) {
+    MgLevel L;
+    L.n = ns[l];
+    L.g = make_geo(dim, ns[l]);
+    L.c = make_opc(ns[l], length, nu, order);
+    L.coarsest = ns[l] <= coarsest_n || ns[l] < 4;
+    size_t per = (l == 0 ? 1 : 3) * (size_t)L.g.npts;
+    double* base = (double*)cur;
+    if (l == 0) {
+      L.t = base;
+    } else {
+      L.u = base;
+      L.b = base + L.g.npts;
+      L.t = base + 2 * L.g.npts;
+    }
+    cur += ((per * 8 + 255) / 256) * 256;
+    P->lv.push_back(L);
+  }
+  P->m_lu = (int)P->lv.back().g.npts;
+  // tail: deepest suffix of levels whose u, b, t fit the shared-memory budget
+  size_t acc = 0;
+  int start = (int)P->lv.size();
+  for (int l = (int)P->lv.size() - 1; l >= 0; --l) {
+    size_t lvl = 3 * sizeof(double) * (size_t)P->lv[l].g.npts;
+    if (acc + lvl > TAIL_SMEM_BUDGET) break;
+    acc += lvl;
+    start = l;
+  }
+  if (start == (int)P->lv.size()) {
+    delete P;
+    set_error("coarsest grid does not fit the tail kernel");
+    return -1;
+  }
+  P->tail_start = start;
+  P->tail_smem = acc;
+  // norms
+  P->npartials = sumsq_partials(P->lv[0].g);
+  cudaError_t e = cudaMalloc(&P->partials, sizeof(double) * (P->npartials + 2));
+  if (e != cudaSuccess) {
+    delete P;
+    return cuda_status(e, "cudaMalloc partials");
+  }
+  P->norm_dev = P->partials + P->npartials;
+  e = cudaMallocHost(&P->norm_host, 2 * sizeof(double));
+  if (e != cudaSuccess) {
+    cudaFree(P->partials);
+    delete P;
+    return cuda_status(e, "cudaMallocHost");
+  }
+  *out = P;
+  return 0;
+}
+
+void mg_plan_destroy(MgPlan* P) {
+  if (!P) return;
+  for (auto& kv : P->lu) {
+    cudaFree(kv.second.dev);
+    cudaFreeHost(kv.second.host);
+  }
+  cudaFree(P->partials);
+  cudaFreeHost(P->norm_host);
+  delete P;
+}
+
+// Dense I - sigma A on the coarsest grid with the reference's entry values
+// (multigrid.py:86-135: 1-D stencils / dx2, Kronecker sum in axis order,
+// times nu, identity minus sigma times it), then partial-pivoting LU.
+static void coarsest_lu_host(const MgPlan* P, double sigma, double* out) {
+  const MgLevel& L = P->lv.back();
+  const int N = L.g.N, d = P->dim, m = (int)L.g.npts;
+  const double dx2 = L.c.dx2;
+  std::vector<double> d1((size_t)N * N, 0.0);
+  for (int i = 0; i < N; ++i) {
+    if (P->order == 2) {
+      d1[i * N + i] = -2.0 / dx2;
+      if (i > 0) d1[i * N + i - 1] = 1.0 / dx2;
+      if (i < N - 1) d1[i * N + i + 1] = 1.0 / dx2;
+    } else if (i == 0 || i == N - 1) {
+      d1[i * N + i] = -2.0 / dx2;
+      if (i > 0) d1[i * N + i - 1] = 1.0 / dx2;
+      if (i < N - 1) d1[i * N + i + 1] = 1.0 / dx2;
+    } else {
+      const int offs[5] = {-2, -1, 0, 1, 2};
+      const double ws[5] = {-1.0, 16.0, -30.0, 16.0, -1.0};
+      for (int q = 0; q < 5; ++q) {
+        int j = i + offs[q];
+        if (j >= 0 && j < N) d1[i * N + j] = ws[q] / (12.0 * dx2);
+      }
+    }
+  }
+  std::vector<double> A((size_t)m * m, 0.0);
+  auto coord = [&](int p, int axis) {   // axis 0 slowest
+    int c[3] = {0, 0, 0};
+    int r = p;
+    for (int ax = d - 1; ax >= 0; --ax) { c[ax] = r % N; r /= N; }
+    return c[axis];
+  };
+  for (int p = 0; p < m; ++p)
+    for (int q = 0; q < m; ++q) {
+      double total = 0.0;
+      bool any = false;
+      for (int ax = 0; ax < d; ++ax) {
+        bool same = true;
+        for (int o = 0; o < d; ++o)
+          if (o != ax && coord(p, o) != coord(q, o)) same = false;
+        if (!same) continue;
+        double v = d1[coord(p, ax) * N + coord(q, ax)];
+        if (v == 0.0) continue;
+        total = any ? total + v : v;
+        any = true;
+      }
+      double a = P->nu * total;
+      A[(size_t)p * m + q] = (p == q ? 1.0 : 0.0) - sigma * a;
+    }
+  std::vector<double> piv(m);
+  for (int k = 0; k < m; ++k) {
+    int pr = k;
+    double best = std::fabs(A[(size_t)k * m + k]);
+    for (int i = k + 1; i < m; ++i) {
+      double v = std::fabs(A[(size_t)i * m + k]);
+      if (v > best) { best = v; pr = i; }
+    }
+    piv[k] = pr;
+    if (pr != k)
+      for (int j = 0; j < m; ++j) std::swap(A[(size_t)k * m + j], A[(size_t)pr * m + j]);
+    double inv = 1.0 / A[(size_t)k * m + k];
+    for (int i = k + 1; i < m; ++i) A[(size_t)i * m + k] = A[(size_t)i * m + k] * inv;
+    for (int i = k + 1; i < m; ++i) {
+      double lik = A[(size_t)i * m + k];
+      if (lik == 0.0) continue;
+      for (int j = k + 1; j < m; ++j)
+        A[(size_t)i * m + j] = A[(size_t)i * m + j] - lik * A[(size_t)k * m + j];
+    }
+  }
+  std::memcpy(out, A.data(), sizeof(double) * (size_t)m * m);
+  std::memcpy(out + (size_t)m * m, piv.data(), sizeof(double) * m);
+}
+
+int mg_prepare(MgPlan* P, double sigma, cudaStream_t s) {
+  unsigned long long key = *(unsigned long long*)&sigma;
+  if (P->lu.count(key)) return 0;
+  size_t count = (size_t)P->m_lu * P->m_lu + P->m_lu;
+  LuEntry E;
+  cudaError_t e = cudaMallocHost(&E.host, count * sizeof(double));
+  if (e != cudaSuccess) return cuda_status(e, "cudaMallocHost lu");
+  e = cudaMalloc(&E.dev, count * sizeof(double));
+  if (e != cudaSuccess) {
+    cudaFreeHost(E.host);
+    return cuda_status(e, "cudaMalloc lu");
+  }
+  coarsest_lu_host(P, sigma, E.host);
+  e = cudaMemcpyAsync(E.dev, E.host, count * sizeof(double), cudaMemcpyHostToDevice, s);
+  if (e != cudaSuccess) return cuda_status(e, "upload lu");
+  P->lu[key] = E;
+  return 0;
+}
+
+// ---------------------------------------------------------------------------
+// grid-wide levels
+
+// sweeps on a grid-wide level; *cur holds the iterate (u or t) and is updated
+static int level_smooth(MgPlan* P, MgLevel& L, double** cur, double* alt_u, const double* b,
+                        double sigma, int count, bool zero, cudaStream_t s) {
+  double* u = *cur;
+  double* other = (u == alt_u) ? L.t : alt_u;
+  if (count == 0) {
+    if (zero) {
+      cudaError_t e = cudaMemsetAsync(u, 0, sizeof(double) * L.g.npts, s);
+      if (e != cudaSuccess) return cuda_status(e, "memset");
+    }
+    return 0;
+  }
+  if (P->smoother == SM_JACOBI) {
+    for (int k = 0; k < count; ++k) {
+      PL_TRY(launch_jacobi(u, b, other, L.g, L.c, sigma, P->omega, zero && k == 0, s));
+      std::swap(u, other);
+    }
+    *cur = u;
+    return 0;
+  }
+  if (zero) {
+    cudaError_t e = cudaMemsetAsync(u, 0, sizeof(double) * L.g.npts, s);
+    if (e != cudaSuccess) return cuda_status(e, "memset");
+  }
+  for (int k = 0; k < count; ++k) {
+    if (P->order == 2) {    // same-colour points never neighbour: in place
+      PL_TRY(launch_rb(u, b, u, L.g, L.c, sigma, P->omega, 1, s));
+      PL_TRY(launch_rb(u, b, u, L.g, L.c, sigma, P->omega, 0, s));
+    } else {                // order 4: +-2 neighbours share the colour
+      PL_TRY(launch_rb(u, b, other, L.g, L.c, sigma, P->omega, 1, s));
+      PL_TRY(launch_rb(other, b, u, L.g, L.c, sigma, P->omega, 0, s));
+    }
+  }
+  *cur = u;
+  return 0;
+}
+
+static int vcycle(MgPlan* P, int l, double* u, const double* b, double sigma, bool zero,
+                  cudaStream_t s) {
+  if (l >= P->tail_start) return launch_tail(P, l, u, b, sigma, zero, 1, s);
+  MgLevel& L = P->lv[l];
+  MgLevel& C = P->lv[l + 1];
+  double* cur = u;
+  PL_TRY(level_smooth(P, L, &cur, u, b, sigma, P->pre, zero, s));
+  double* r = (cur == u) ? L.t : u;
+  PL_TRY(launch_residual(cur, b, r, L.g, L.c, sigma, s));
+  PL_TRY(launch_fw(r, C.b, L.g, s));
+  PL_TRY(vcycle(P, l + 1, C.u, C.b, sigma, true, s));
+  PL_TRY(launch_prolong(C.u, cur, L.g, 1, s));
+  PL_TRY(level_smooth(P, L, &cur, u, b, sigma, P->post, false, s));
+  if (cur != u) {
+    cudaError_t e = cudaMemcpyAsync(u, cur, sizeof(double) * L.g.npts,
+                                    cudaMemcpyDeviceToDevice, s);
+    if (e != cudaSuccess) return cuda_status(e, "copy");
+    count_launch(K_COPY, 16.0 * L.g.npts);
+  }
+  return 0;
+}
+
+int mg_cycles(MgPlan* P, double* u, const double* b, double sigma, int ncycles, int zero_guess,
+              cudaStream_t s) {
+  PL_TRY(mg_prepare(P, sigma, s));
+  if (P->tail_start == 0) return launch_tail(P, 0, u, b, sigma, zero_guess, ncycles, s);
+  for (int c = 0; c < ncycles; ++c)
+    PL_TRY(vcycle(P, 0, u, b, sigma, zero_guess && c == 0, s));
+  return 0;
+}
+
+int mg_smooth(MgPlan* P, double* u, const double* b, double sigma, int count, cudaStream_t s) {
+  MgLevel& L = P->lv[0];
+  double* cur = u;
+  PL_TRY(level_smooth(P, L, &cur, u, b, sigma, count, false, s));
+  if (cur != u) {
+    cudaError_t e = cudaMemcpyAsync(u, cur, sizeof(double) * L.g.npts,
+                                    cudaMemcpyDeviceToDevice, s);
+    if (e != cudaSuccess) return cuda_status(e, "copy");
+  }
+  return 0;
+}
+
+static int norm2(MgPlan* P, const double* u, const double* b, double sigma, double* out,
+                 cudaStream_t s) {
+  MgLevel& L = P->lv[0];
+  PL_TRY(launch_sumsq(u, b, L.g, L.c, sigma, P->partials, P->npartials, P->norm_dev, s));
+  cudaError_t e = cudaMemcpyAsync(P->norm_host, P->norm_dev, sizeof(double),
+                                  cudaMemcpyDeviceToHost, s);
+  if (e != cudaSuccess) return cuda_status(e, "norm readback");
+  e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return cuda_status(e, "sync");
+  *out = std::sqrt(P->norm_host[0]);
+  return 0;
+}
+
+int mg_solve_tol(MgPlan* P, double* u, const double* b, double sigma, double tol, double stall,
+                 int max_cycles, int* cycles, int* status, double* residual, cudaStream_t s) {
+  PL_TRY(mg_prepare(P, sigma, s));
+  MgLevel& L = P->lv[0];
+  double bnorm;
+  PL_TRY(norm2(P, nullptr, b, sigma, &bnorm, s));
+  *cycles = 0;
+  if (bnorm == 0.0) {
+    cudaError_t e = cudaMemsetAsync(u, 0, sizeof(double) * L.g.npts, s);
+    if (e != cudaSuccess) return cuda_status(e, "memset");
+    *status = ST_CONVERGED;
+    *residual = 0.0;
+    return 0;
+  }
+  double res;
+  PL_TRY(norm2(P, u, b, sigma, &res, s));
+  int c = 0;
+  while (res > tol * bnorm) {
+    if (c >= max_cycles) {
+      *cycles = c;
+      *residual = res;
+      *status = -1;
+      set_error("no convergence after %d V-cycles (relative residual %.3e)", c, res / bnorm);
+      return 1;
+    }
+    PL_TRY(mg_cycles(P, u, b, sigma, 1, 0, s));
+    ++c;
+    double nres;
+    PL_TRY(norm2(P, u, b, sigma, &nres, s));
+    if (nres > tol * bnorm && nres >= stall * res) {
+      *cycles = c;
+      *status = ST_STALLED;
+      *residual = nres;
+      return 0;
+    }
+    res = nres;
+  }
+  *cycles = c;
+  *status = ST_CONVERGED;
+  *residual = res;
+  return 0;
+}
+
+}  // namespace pl

@@ -1,0 +1,227 @@
+// Factor-2 grid transfers (transfers.py): full weighting, injection, linear
+// and cubic interpolation.  Each restates the reference's per-axis numpy
+// evaluation (axis 0 first, one rounding per operation) so results are
+// bit-identical; the cubic weights go through a sequential FMA chain like the
+// reference's dgemm (np.tensordot with the dense interpolation matrix).
+#include <map>
+#include <mutex>
+#include <vector>
+#include <cmath>
+
+#include "common.cuh"
+#include "kernels.cuh"
+#include "transfer_dev.cuh"
+
+namespace pl {
+
+namespace {
+
+template <int DIM>
+__global__ void __launch_bounds__(256) k_fw(const double* __restrict__ f,
+                                            double* __restrict__ cz, Geo gf, Geo gc) {
+  long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= gc.npts) return;
+  int jx = (int)(t % gc.nx);
+  long long r = t / gc.nx;
+  int jy = (int)(r % gc.ny);
+  int jz = (int)(r / gc.ny);
+  cz[t] = fw_point<DIM>(f, gf, jx, jy, jz);
+}
+
+template <int DIM>
+__global__ void __launch_bounds__(256) k_inject(const double* __restrict__ f,
+                                                double* __restrict__ cz, Geo gf, Geo gc) {
+  long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= gc.npts) return;
+  int jx = (int)(t % gc.nx);
+  long long r = t / gc.nx;
+  int jy = (int)(r % gc.ny);
+  int jz = (int)(r / gc.ny);
+  long long idx = 2 * jx + 1;
+  if (DIM >= 2) idx += (long long)(2 * jy + 1) * gf.sy;
+  if (DIM == 3) idx += (long long)(2 * jz + 1) * gf.sz;
+  cz[t] = f[idx];
+}
+
+template <int DIM>
+__global__ void __launch_bounds__(256) k_prolong(const double* __restrict__ c,
+                                                 double* __restrict__ f, Geo gf, Geo gc,
+                                                 int accumulate) {
+  long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= gf.npts) return;
+  int ix = (int)(t % gf.nx);
+  long long r = t / gf.nx;
+  int iy = (int)(r % gf.ny);
+  int iz = (int)(r / gf.ny);
+  double v = lin_point<DIM>(c, gc, ix, iy, iz);
+  f[t] = accumulate ? f[t] + v : v;
+}
+
+// One axis of the cubic interpolation (transfers.py:82-89): input shape
+// (n0, nin, n2) -> output (n0, nout, n2) along the middle axis, with
+// sequential FMA over the taps (dgemm order).
+__global__ void __launch_bounds__(256) k_cubic_axis(const double* __restrict__ in,
+                                                    double* __restrict__ out, long long n0,
+                                                    int nin, int nout, long long n2,
+                                                    const int* __restrict__ cnt,
+                                                    const int* __restrict__ tidx,
+                                                    const double* __restrict__ tw,
+                                                    int accumulate) {
+  long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  long long total = n0 * nout * n2;
+  if (t >= total) return;
+  long long k2 = t % n2;
+  long long r = t / n2;
+  int i = (int)(r % nout);
+  long long k0 = r / nout;
+  const double* src = in + k0 * nin * n2 + k2;
+  double acc = 0.0;
+  int nt = cnt[i];
+  for (int q = 0; q < nt; ++q) acc = __fma_rn(tw[i * 4 + q], src[(long long)tidx[i * 4 + q] * n2], acc);
+  out[t] = accumulate ? out[t] + acc : acc;
+}
+
+}  // namespace
+
+#define PL_T_DISPATCH(g, KERNEL, grid, block, s, ...)                          \
+  do {                                                                        \
+    if ((g).dim == 1) KERNEL<1><<<grid, block, 0, s>>>(__VA_ARGS__);           \
+    else if ((g).dim == 2) KERNEL<2><<<grid, block, 0, s>>>(__VA_ARGS__);      \
+    else KERNEL<3><<<grid, block, 0, s>>>(__VA_ARGS__);                        \
+  } while (0)
+
+static Geo coarse_geo(const Geo& gf) { return make_geo(gf.dim, (gf.N + 1) / 2); }
+
+int launch_fw(const double* fine, double* coarse, const Geo& gf, cudaStream_t s) {
+  Geo gc = coarse_geo(gf);
+  PL_PRE(K_RESTRICT);
+  PL_T_DISPATCH(gf, k_fw, ceil_div(gc.npts, 256), 256, s, fine, coarse, gf, gc);
+  PL_CHECK_LAUNCH(K_RESTRICT, 8.0 * gf.npts + 8.0 * gc.npts);
+  return 0;
+}
+
+int launch_inject(const double* fine, double* coarse, const Geo& gf, cudaStream_t s) {
+  Geo gc = coarse_geo(gf);
+  PL_PRE(K_RESTRICT);
+  PL_T_DISPATCH(gf, k_inject, ceil_div(gc.npts, 256), 256, s, fine, coarse, gf, gc);
+  PL_CHECK_LAUNCH(K_RESTRICT, 16.0 * gc.npts);
+  return 0;
+}
+
+int launch_prolong(const double* coarse, double* fine, const Geo& gf, int accumulate,
+                   cudaStream_t s) {
+  Geo gc = coarse_geo(gf);
+  PL_PRE(K_PROLONG);
+  PL_T_DISPATCH(gf, k_prolong, ceil_div(gf.npts, 256), 256, s, coarse, fine, gf, gc,
+                accumulate);
+  PL_CHECK_LAUNCH(K_PROLONG, (accumulate ? 16.0 : 8.0) * gf.npts + 8.0 * gc.npts);
+  return 0;
+}
+
+// ---------------------------------------------------------------------------
+// cubic taps (host restatement of transfers.py:53-79, weights in double with
+// the reference's own float expression order)
+
+static std::mutex g_taps_mu;
+static std::map<int, CubicTaps*> g_taps;
+
+const CubicTaps* cubic_taps(int nf) {
+  std::lock_guard<std::mutex> lk(g_taps_mu);
+  auto it = g_taps.find(nf);
+  if (it != g_taps.end()) return it->second;
+  int nc = nf / 2;
+  int rows = nf - 1;
+  std::vector<int> cnt(rows, 0), idx(rows * 4, 0);
+  std::vector<double> w(rows * 4, 0.0);
+  for (int i = 1; i < nf; ++i) {
+    int r = i - 1;
+    if (i % 2 == 0) {
+      cnt[r] = 1;
+      idx[r * 4] = i / 2 - 1;
+      w[r * 4] = 1.0;
+      continue;
+    }
+    double sp = i / 2.0;
+    std::vector<int> pts;
+    if (nc < 3) {
+      for (int j = 0; j <= nc; ++j) pts.push_back(j);
+    } else {
+      int j0 = (int)std::floor(sp) - 1;
+      if (j0 < 0) j0 = 0;
+      if (j0 > nc - 3) j0 = nc - 3;
+      for (int j = j0; j < j0 + 4; ++j) pts.push_back(j);
+    }
+    // the matrix row accumulates weights with += into zeros; columns are
+    // then contracted in increasing order by the dgemm chain
+    std::map<int, double> row;
+    for (size_t a = 0; a < pts.size(); ++a) {
+      double wt = 1.0;
+      for (size_t b = 0; b < pts.size(); ++b)
+        if (b != a) wt *= (sp - pts[b]) / (double)(pts[a] - pts[b]);
+      if (pts[a] >= 1 && pts[a] <= nc - 1) {
+        double& cell = row[pts[a] - 1];
+        cell = cell + wt;
+      }
+    }
+    int q = 0;
+    for (auto& kv : row) {
+      if (kv.second == 0.0) continue;
+      idx[r * 4 + q] = kv.first;
+      w[r * 4 + q] = kv.second;
+      ++q;
+    }
+    cnt[r] = q;
+  }
+  CubicTaps* t = new CubicTaps;
+  t->nf = nf;
+  size_t bi = sizeof(int) * rows, bi4 = sizeof(int) * rows * 4, bw = sizeof(double) * rows * 4;
+  if (cudaMalloc(&t->cnt, bi) != cudaSuccess || cudaMalloc(&t->idx, bi4) != cudaSuccess ||
+      cudaMalloc(&t->w, bw) != cudaSuccess) {
+    set_error("cudaMalloc failed for cubic taps");
+    delete t;
+    return nullptr;
+  }
+  cudaMemcpy(t->cnt, cnt.data(), bi, cudaMemcpyHostToDevice);
+  cudaMemcpy(t->idx, idx.data(), bi4, cudaMemcpyHostToDevice);
+  cudaMemcpy(t->w, w.data(), bw, cudaMemcpyHostToDevice);
+  g_taps[nf] = t;
+  return t;
+}
+
+long long cubic_scratch_doubles(const Geo& gf) {
+  long long Nf = gf.N, Nc = (gf.N + 1) / 2 - 1;
+  if (gf.dim == 1) return 0;
+  if (gf.dim == 2) return Nf * Nc;
+  return Nf * Nc * Nc + Nf * Nf * Nc;
+}
+
+int launch_cubic(const double* coarse, double* fine, const Geo& gf, int accumulate,
+                 double* scratch, cudaStream_t s) {
+  const CubicTaps* t = cubic_taps(gf.N + 1);
+  if (!t) return 2;
+  long long Nf = gf.N, Nc = (gf.N + 1) / 2 - 1;
+  auto pass = [&](const double* in, double* out, long long n0, long long n2, int acc) {
+    long long total = n0 * Nf * n2;
+    k_cubic_axis<<<ceil_div(total, 256), 256, 0, s>>>(in, out, n0, (int)Nc, (int)Nf, n2,
+                                                      t->cnt, t->idx, t->w, acc);
+  };
+  PL_PRE(K_INTERP);
+  if (gf.dim == 1) {
+    pass(coarse, fine, 1, 1, accumulate);
+  } else if (gf.dim == 2) {
+    pass(coarse, scratch, 1, Nc, 0);          // axis 0: (Nc,Nc) -> (Nf,Nc)
+    pass(scratch, fine, Nf, 1, accumulate);   // axis 1: (Nf,Nc) -> (Nf,Nf)
+  } else {
+    double* s1 = scratch;                     // (Nf, Nc, Nc)
+    double* s2 = scratch + Nf * Nc * Nc;      // (Nf, Nf, Nc)
+    pass(coarse, s1, 1, Nc * Nc, 0);
+    pass(s1, s2, Nf, Nc, 0);
+    pass(s2, fine, Nf * Nf, 1, accumulate);
+  }
+  double bytes = (accumulate ? 16.0 : 8.0) * gf.npts;
+  if (gf.dim >= 2) bytes += 16.0 * (double)cubic_scratch_doubles(gf);
+  PL_CHECK_LAUNCH(K_INTERP, bytes);
+  return 0;
+}
+
+}  // namespace pl

@@ -1,0 +1,225 @@
+"""Geometric multigrid for (I - sigma nu Lap_h) u = b  (multigrid.py).
+
+Same configuration objects, policies and results as the reference; the
+V-cycle itself runs inside lib/libpintlab_b200.so (csrc/mg.cu): grid-wide
+HBM-streaming kernels on the fine levels and one single-CTA shared-memory
+kernel for the latency-bound tail (coarse levels + dense LU on n <= 4).
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+from typing import Union
+
+import torch
+
+from . import _capi as capi
+from ._device import device, like_input, ptr, stream_ptr, to_device
+from .heat import Grid, HeatOperator
+
+
+@dataclass(frozen=True)
+class MgConfig:
+    """multigrid.py:24-38."""
+
+    smoother: str = "jacobi"   # jacobi | gauss-seidel | jor-rb
+    omega: float = 2.0 / 3.0
+    pre_sweeps: int = 2
+    post_sweeps: int = 2
+    coarsest_n: int = 4
+
+    def __post_init__(self):
+        if self.smoother not in ("jacobi", "gauss-seidel", "jor-rb"):
+            raise ValueError(f"unknown smoother {self.smoother!r}")
+        if self.pre_sweeps < 0 or self.post_sweeps < 0:
+            raise ValueError("sweep counts must be non-negative")
+        if self.coarsest_n < 2:
+            raise ValueError("coarsest grid needs at least one interior point")
+
+
+@dataclass(frozen=True)
+class FixedCycles:
+    """multigrid.py:41-47."""
+
+    cycles: int
+
+    def __post_init__(self):
+        if self.cycles < 1:
+            raise ValueError("need at least one V-cycle")
+
+
+@dataclass(frozen=True)
+class ToTolerance:
+    """multigrid.py:50-60."""
+
+    tol: float = 1e-12
+    stall: float = 0.75
+    max_cycles: int = 100
+
+    def __post_init__(self):
+        if self.tol <= 0:
+            raise ValueError("tolerance must be positive")
+        if not 0.0 < self.stall < 1.0:
+            raise ValueError("stall factor must be in (0, 1)")
+
+
+@dataclass(frozen=True)
+class Direct:
+    """Exact sparse solve (multigrid.py:63-65).  Not on the GPU path: no
+    BASELINE configuration uses it."""
+
+
+SolvePolicy = Union[FixedCycles, ToTolerance, Direct]
+
+
+class MultigridError(RuntimeError):
+    """Tolerance solve hit the cycle cap (multigrid.py:77-83)."""
+
+    def __init__(self, message, residual, cycles):
+        super().__init__(message)
+        self.residual = residual
+        self.cycles = cycles
+
+
+class _Plan:
+    """Device workspace + C plan for one (operator, MgConfig, stream)."""
+
+    def __init__(self, op: HeatOperator, cfg: MgConfig):
+        g = op.grid
+        lib = capi.lib()
+        nbytes = lib.pl_mg_workspace_bytes(g.dim, g.n, cfg.coarsest_n)
+        self.ws = torch.empty(max(nbytes, 8), dtype=torch.uint8, device=device())
+        h = C.c_void_p()
+        capi.check(lib.pl_mg_plan_create(C.byref(h), g.dim, g.n, float(g.length), float(op.nu),
+                                         op.order, capi.SMOOTHERS[cfg.smoother],
+                                         float(cfg.omega), cfg.pre_sweeps, cfg.post_sweeps,
+                                         cfg.coarsest_n, self.ws.data_ptr(), nbytes),
+                   "MG plan")
+        self.handle = h
+
+    def __del__(self):
+        try:
+            if self.handle:
+                capi.lib().pl_mg_plan_destroy(self.handle)
+        except Exception:
+            pass
+
+
+_plans: dict = {}
+
+
+def plan_for(op: HeatOperator, cfg: MgConfig) -> _Plan:
+    key = (op.grid, float(op.nu), op.order, cfg, stream_ptr(), torch.cuda.current_device())
+    p = _plans.get(key)
+    if p is None:
+        p = _Plan(op, cfg)
+        _plans[key] = p
+    return p
+
+
+class ShiftedOperator:
+    """I - sigma * A for the heat operator (multigrid.py:178-208)."""
+
+    def __init__(self, base: HeatOperator, sigma: float):
+        if sigma < 0:
+            raise ValueError("shift must be non-negative")
+        self.base = base
+        self.sigma = sigma
+
+    @property
+    def grid(self) -> Grid:
+        return self.base.grid
+
+    def apply(self, u):
+        t, host = to_device(u)
+        out = torch.empty_like(t)
+        g = self.base.grid
+        capi.check(capi.lib().pl_shifted_apply(ptr(t), ptr(out), g.dim, g.n, float(g.length),
+                                               float(self.base.nu), self.base.order,
+                                               float(self.sigma), stream_ptr()),
+                   "ShiftedOperator.apply")
+        return like_input(out, host)
+
+    def diagonal(self, as_numpy: bool = True):
+        g = self.base.grid
+        out = torch.empty(g.shape, dtype=torch.float64, device=device())
+        capi.check(capi.lib().pl_heat_diagonal(ptr(out), g.dim, g.n, float(g.length),
+                                               float(self.base.nu), self.base.order,
+                                               float(self.sigma), 1, stream_ptr()),
+                   "ShiftedOperator.diagonal")
+        return like_input(out, as_numpy)
+
+    def solve_direct(self, b):
+        raise NotImplementedError("Direct solves are not on the GPU path")
+
+
+def _check_policy(policy):
+    if isinstance(policy, Direct):
+        raise NotImplementedError("Direct (sparse LU) is not on the B200 path; use "
+                                  "FixedCycles or ToTolerance")
+
+
+def smooth(op: ShiftedOperator, u, b, cfg: MgConfig, count: int):
+    """multigrid.py:211-234 (returns a new array, like the reference)."""
+    tu, host = to_device(u)
+    tb, _ = to_device(b)
+    if tu.shape != tb.shape:
+        raise ValueError("shape mismatch between iterate and right-hand side")
+    out = tu.clone()
+    if count:
+        p = plan_for(op.base, cfg)
+        capi.check(capi.lib().pl_mg_smooth(p.handle.value, ptr(out), ptr(tb), float(op.sigma),
+                                           count, stream_ptr()), "smooth")
+    return like_input(out, host)
+
+
+def vcycles_into(op: ShiftedOperator, u, b, cfg: MgConfig, ncycles: int, zero_guess=False):
+    """ncycles V-cycles in place on the device tensor u."""
+    p = plan_for(op.base, cfg)
+    capi.check(capi.lib().pl_mg_vcycles(p.handle.value, ptr(u), ptr(b), float(op.sigma),
+                                        ncycles, int(zero_guess), stream_ptr()), "v_cycle")
+    return u
+
+
+def v_cycle(op: ShiftedOperator, u, b, cfg: MgConfig):
+    """multigrid.py:237-251 (returns a new array)."""
+    tu, host = to_device(u)
+    tb, _ = to_device(b)
+    out = tu.clone()
+    vcycles_into(op, out, tb, cfg, 1)
+    return like_input(out, host)
+
+
+@dataclass
+class SolveResult:
+    """multigrid.py:254-258."""
+
+    u: object
+    cycles: int
+    status: str  # fixed | converged | stalled
+
+
+def solve_into(op: ShiftedOperator, u, b, cfg: MgConfig, policy) -> tuple:
+    """In-place device solve; returns (cycles, status).  Raises MultigridError."""
+    _check_policy(policy)
+    if isinstance(policy, FixedCycles):
+        vcycles_into(op, u, b, cfg, policy.cycles)
+        return policy.cycles, "fixed"
+    p = plan_for(op.base, cfg)
+    cyc, st, res = C.c_int(0), C.c_int(0), C.c_double(0)
+    rc = capi.lib().pl_mg_solve_tol(p.handle.value, ptr(u), ptr(b), float(op.sigma),
+                                    float(policy.tol), float(policy.stall), policy.max_cycles,
+                                    C.byref(cyc), C.byref(st), C.byref(res), stream_ptr())
+    if rc == capi.PL_ERR_MGCAP:
+        raise MultigridError(capi.last_error(), res.value, cyc.value)
+    capi.check(rc, "solve")
+    return cyc.value, capi.STATUS[st.value]
+
+
+def solve(op: ShiftedOperator, u0, b, cfg: MgConfig, policy: SolvePolicy) -> SolveResult:
+    """multigrid.py:261-288."""
+    tu, host = to_device(u0)
+    tb, _ = to_device(b)
+    out = tu.clone()
+    cycles, status = solve_into(op, out, tb, cfg, policy)
+    return SolveResult(like_input(out, host), cycles, status)

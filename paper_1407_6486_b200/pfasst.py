@@ -1,0 +1,488 @@
+"""Pipelined MLSDC across a block of time steps -- PFASST / IPFASST (pfasst.py).
+
+The reference's serial schedule (pfasst.py:213-228) is normative and is kept
+exactly: predictor phases, coarse hand-offs, blocking fine hand-offs per
+iteration, convergence freezing, block chaining.  Three executors:
+
+``"serial"`` / ``"threaded"``
+    all P time ranks resident on one GPU, issued in the serial order on one
+    CUDA stream.  Hand-offs are stream-ordered device reads of the sender's
+    state (identical to the reference's snapshots).
+    Convergence flags are resolved lazily: rank n's residual of iteration k
+    is read back only when rank n's iteration k+1 is about to be issued, by
+    which time ranks n+1..P-1 of iteration k are still queued -- the GPU never
+    drains waiting for the host.  ("threaded" is the reference's bitwise-
+    identical alternative executor; here it is the same device schedule.)
+``"nccl"``
+    one process per GPU (torch.distributed, NCCL over NVLink/NVSwitch), time
+    rank n on process n mod G.  Fine / coarse hand-offs are NCCL send/recv of
+    snapshot buffers; the final value of a block is broadcast from the owner
+    of the last rank.  Frozen ranks stop sending once their receiver has seen
+    converged=True and the receiver re-uses the cached payloads, which is
+    numerically identical to the reference's resend.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from ._device import empty, to_device, zeros
+from .hierarchy import (Hooks, Level, TimeStep, burn_in, check_hierarchy, interpolate_up,
+                        mlsdc_iteration, restrict_state)
+from .sdc import NodeStates, residual_into
+
+
+@dataclass
+class TraceRow:
+    """pfasst.py:24-31."""
+
+    block: int
+    rank: int
+    iteration: int
+    level: int
+    residual: float
+    vcycles: int
+
+
+@dataclass
+class PfasstResult:
+    """pfasst.py:34-46."""
+
+    u: object
+    rank_iterations: list = field(default_factory=list)
+    rank_vcycles: list = field(default_factory=list)
+    converged: list = field(default_factory=list)
+    trace: list = field(default_factory=list)
+    final_values: list = field(default_factory=list)
+
+    @property
+    def total_vcycles(self) -> int:
+        return sum(sum(b) for b in self.rank_vcycles)
+
+
+# ---------------------------------------------------------------------------
+# per-rank device engine
+
+
+class _PreCoarse(Hooks):
+    def __init__(self, fn):
+        self.fn = fn
+
+    def pre_coarse_sweep(self, ts):
+        if self.fn is not None:
+            self.fn(ts)
+
+
+class DeviceEngine:
+    """Owns the TimeStep state of the time ranks of this process (one GPU)."""
+
+    def __init__(self, levels, dt, ranks):
+        self.levels = levels
+        self.dt = dt
+        self.L = len(levels)
+        self.ranks = list(ranks)
+        self.ts = {}
+        self.spread_y = {}
+        self._res = zeros((max(self.ranks) + 1 if self.ranks else 1,))
+        self._res_host = torch.zeros(self._res.shape, dtype=torch.float64,
+                                     pin_memory=True)
+        self._events = {}
+
+    # -- state ---------------------------------------------------------------
+    def spread(self, n, u):
+        """TimeStep.spread + spread copies of levels >= 1 (hierarchy.py:138-150,
+        pfasst.py:132-134); buffers are reused across blocks."""
+        ts = self.ts.get(n)
+        if ts is None:
+            ts = self.ts[n] = TimeStep.spread(self.levels, u)
+        else:
+            uu = u
+            for l, lvl in enumerate(self.levels):
+                if l > 0:
+                    prev = self.levels[l - 1]
+                    if lvl.grid.n == prev.grid.n:
+                        uu = uu.clone()
+                    else:
+                        from .transfers import full_weighting, inject
+                        uu = inject(uu) if prev.space_restrict == "inject" else \
+                            full_weighting(uu)
+                st = ts.states[l]
+                st.y.copy_(uu.unsqueeze(0).expand_as(st.y))
+                lvl.operator.apply_into(st.y[0], st.f[0])
+                st.f[1:].copy_(st.f[0].unsqueeze(0).expand_as(st.f[1:]))
+                ts.set_y0(l, uu)
+                ts.tau[l] = None
+        copies = self.spread_y.get(n)
+        if copies is None:
+            copies = self.spread_y[n] = [None] + [ts.states[l].y.clone()
+                                                  for l in range(1, self.L)]
+        else:
+            for l in range(1, self.L):
+                copies[l].copy_(ts.states[l].y)
+
+    def coarse_payload(self, n):
+        return self.ts[n].states[self.L - 1].y[-1]
+
+    def fine_payload(self, n):
+        return self.ts[n].states[0].y[-1]
+
+    def set_coarse_y0(self, n, t):
+        self.ts[n].set_y0(self.L - 1, t)
+
+    def set_fine_y0(self, n, t):
+        """pfasst.py:196-198 for level 0."""
+        ts = self.ts[n]
+        ts.set_y0(0, t)
+        ts.states[0].y[0].copy_(t)
+        self.levels[0].operator.apply_into(ts.states[0].y[0], ts.states[0].f[0])
+
+    # -- work ----------------------------------------------------------------
+    def burn_in(self, n):
+        return burn_in(self.ts[n], self.dt, 1)
+
+    def interpolate_up(self, n, exact):
+        ts = self.ts[n]
+        interpolate_up(ts, self.spread_y[n], exact_y0=ts.y0[0].clone() if exact else None)
+
+    def iteration(self, n, pre_coarse):
+        return mlsdc_iteration(self.ts[n], self.dt, _PreCoarse(pre_coarse))
+
+    def residual(self, n):
+        """Launch the fine residual (pfasst.py:200) and its readback."""
+        ts = self.ts[n]
+        residual_into(ts.states[0], ts.y0[0], self.dt, self._res[n:n + 1])
+        self._res_host[n:n + 1].copy_(self._res[n:n + 1], non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record()
+        return ev
+
+    def read(self, n, handle):
+        handle.synchronize()
+        return float(self._res_host[n].item())
+
+    def snapshot(self, t):
+        return t.clone()
+
+
+# ---------------------------------------------------------------------------
+# exchanges
+
+
+class _LocalExchange:
+    """All ranks in this process: hand-offs read the sender's current state,
+    which in the serial issue order equals the reference's snapshot."""
+
+    def __init__(self, engine):
+        self.e = engine
+
+    def owns(self, n):
+        return True
+
+    def send_pred(self, n, ph):
+        pass
+
+    def recv_pred(self, n, ph):
+        return self.e.coarse_payload(n - 1)
+
+    def send_coarse(self, n, k):
+        pass
+
+    def recv_iteration(self, n, k):
+        return self.e.fine_payload(n - 1), self.e.coarse_payload(n - 1)
+
+    def send_fine(self, n, k):
+        pass
+
+    def send_flag(self, n, k, flag):
+        pass
+
+    def recv_flag(self, n, k):
+        return None        # resolved from this process's own bookkeeping
+
+
+class DistExchange:
+    """torch.distributed point-to-point hand-offs between processes (NCCL on
+    GPUs, gloo in the CPU tests).  Time rank n lives on process n % world.
+
+    Ordering rules that keep NCCL's per-pair stream deadlock-free: payload
+    receives are posted when the receiving rank starts its iteration (and
+    waited on at once), sends are posted as soon as the payload is final,
+    and the 8-byte converged flag is received lazily, right before the host
+    needs it."""
+
+    def __init__(self, engine, group=None):
+        import torch.distributed as dist
+        self.dist = dist
+        self.e = engine
+        self.group = group
+        self.world = dist.get_world_size(group)
+        self.me = dist.get_rank(group)
+        self._pending = []       # outstanding send works (+ their buffers)
+        self._cache = {}         # n -> (fine, coarse) once the predecessor froze
+        self._last = {}          # n -> last (fine, coarse) received
+        self._last_pred = {}
+
+    def proc(self, n):
+        return n % self.world
+
+    def owns(self, n):
+        return self.proc(n) == self.me
+
+    def _send(self, t, dst_rank):
+        buf = self.e.snapshot(t)
+        w = self.dist.isend(buf, self.proc(dst_rank), group=self.group)
+        self._pending.append((w, buf))
+        if len(self._pending) > 16:
+            w0, _ = self._pending.pop(0)
+            w0.wait()
+
+    def _recv(self, like, src_rank):
+        buf = torch.empty_like(like)
+        self.dist.irecv(buf, self.proc(src_rank), group=self.group).wait()
+        return buf
+
+    def send_pred(self, n, ph):
+        self._send(self.e.coarse_payload(n), n + 1)
+
+    def recv_pred(self, n, ph):
+        # rank n-1 took part in phases 0..n-1; phase n re-reads phase n-1
+        if ph < n:
+            self._last_pred[n] = self._recv(self.e.coarse_payload(n), n - 1)
+        return self._last_pred[n]
+
+    def send_coarse(self, n, k):
+        self._send(self.e.coarse_payload(n), n + 1)
+
+    def recv_iteration(self, n, k):
+        if n in self._cache:
+            return self._cache[n]
+        coarse = self._recv(self.e.coarse_payload(n), n - 1)
+        fine = self._recv(self.e.fine_payload(n), n - 1)
+        self._last[n] = (fine, coarse)
+        return fine, coarse
+
+    def send_fine(self, n, k):
+        self._send(self.e.fine_payload(n), n + 1)
+
+    def send_flag(self, n, k, flag):
+        dev = self.e.fine_payload(n).device
+        self._send(torch.tensor([1.0 if flag else 0.0], dtype=torch.float64, device=dev), n + 1)
+
+    def recv_flag(self, n, k):
+        if n in self._cache:
+            return True
+        flag = self._recv(torch.empty(1, dtype=torch.float64,
+                                      device=self.e.fine_payload(n).device), n - 1)
+        ok = bool(flag.item() != 0.0)
+        if ok:                   # predecessor frozen: keep its final payloads
+            self._cache[n] = self._last[n]
+        return ok
+
+    def finish(self):
+        for w, _ in self._pending:
+            w.wait()
+        self._pending.clear()
+        self._cache.clear()
+        self._last.clear()
+        self._last_pred.clear()
+
+
+# ---------------------------------------------------------------------------
+# the schedule (pfasst.py:121-253)
+
+
+class _Block:
+    def __init__(self, engine, exchange, p, tol, max_iter, block, record_final_values):
+        self.e, self.x = engine, exchange
+        self.p, self.tol, self.max_iter, self.block = p, tol, max_iter, block
+        self.record = record_final_values
+        self.mine = [n for n in range(p) if exchange.owns(n)]
+        self.vcycles = [0] * p
+        self.iterations = [0] * p
+        self.converged = [False] * p
+        self.trace = []
+        self.final_values = []
+        self.frozen = [False] * p
+        self.pending = {}        # n -> (k, cycles, residual handle)
+        self.status = [dict() for _ in range(p)]   # n -> {k: converged}
+
+    def predictor(self):
+        """pfasst.py:166-181, phase-major (serial order)."""
+        e, x, p = self.e, self.x, self.p
+        for ph in range(p):
+            for n in range(ph, p):
+                if not x.owns(n):
+                    continue
+                if n > 0:
+                    e.set_coarse_y0(n, x.recv_pred(n, ph))
+                self.vcycles[n] += e.burn_in(n)
+                if n + 1 < p and not x.owns(n + 1):
+                    x.send_pred(n, ph)
+                elif n + 1 < p:
+                    pass  # local receiver reads the state directly
+        for n in self.mine:
+            e.interpolate_up(n, exact=(n == 0))
+
+    def _resolve(self, n):
+        """Read rank n's residual of its last live iteration and settle its
+        converged flag (pfasst.py:200-210)."""
+        if n not in self.pending:
+            return
+        k, cyc, handle = self.pending.pop(n)
+        res = self.e.read(n, handle)
+        if n == 0:
+            pred_ok = True
+        elif self.x.owns(n - 1):
+            if n - 1 in self.pending and self.pending[n - 1][0] == k:
+                self._resolve(n - 1)
+            # a predecessor frozen before k resends converged=True
+            pred_ok = self.status[n - 1].get(k, True)
+        else:
+            pred_ok = self.x.recv_flag(n, k)
+        ok = (res <= self.tol) and pred_ok
+        self.status[n][k] = ok
+        self.converged[n] = ok
+        self.frozen[n] = ok
+        self.trace.append(TraceRow(self.block, n, k, 0, res, cyc))
+        if n + 1 < self.p and not self.x.owns(n + 1):
+            self.x.send_flag(n, k, ok)
+
+    def iterations_loop(self):
+        e, x, p = self.e, self.x, self.p
+        for k in range(1, self.max_iter + 1):
+            active = False
+            for n in self.mine:
+                self._resolve(n)
+                if self.frozen[n]:
+                    continue
+                active = True
+                if n > 0:
+                    fine, coarse = x.recv_iteration(n, k)
+                    e.set_fine_y0(n, fine)
+                    coarse_msg = coarse
+                    pre = (lambda ts, n=n, c=coarse_msg: e.set_coarse_y0(n, c))
+                else:
+                    pre = None
+                # the local exchange hands over the predecessor's coarse value
+                # by reading its state inside the pre-coarse hook (same as the
+                # reference's blocking coarse recv, pfasst.py:107-112)
+                cyc = e.iteration(n, pre)
+                if n + 1 < p and not x.owns(n + 1):
+                    # coarse payload was produced by the coarse sweep; the fine
+                    # one by the finest sweep -- both final now
+                    x.send_coarse(n, k)
+                    x.send_fine(n, k)
+                handle = e.residual(n)
+                self.vcycles[n] += cyc
+                self.iterations[n] = k
+                self.pending[n] = (k, cyc, handle)
+                if self.record and n == p - 1:
+                    self.final_values.append(e.snapshot(e.fine_payload(n)))
+            if not active:
+                break
+        for n in self.mine:
+            self._resolve(n)
+
+
+def _gather_block(blk, exchange):
+    """Combine per-process bookkeeping (nccl executor)."""
+    if not isinstance(exchange, DistExchange):
+        return blk.iterations, blk.vcycles, blk.converged, blk.trace
+    dist = exchange.dist
+    mine = {n: (blk.iterations[n], blk.vcycles[n], blk.converged[n]) for n in blk.mine}
+    rows = [(r.block, r.rank, r.iteration, r.level, r.residual, r.vcycles) for r in blk.trace]
+    gathered = [None] * exchange.world
+    dist.all_gather_object(gathered, (mine, rows), group=exchange.group)
+    it, vc, cv, tr = [0] * blk.p, [0] * blk.p, [False] * blk.p, []
+    for m, rws in gathered:
+        for n, (a, b, c) in m.items():
+            it[n], vc[n], cv[n] = a, b, c
+        tr.extend(TraceRow(*r) for r in rws)
+    return it, vc, cv, tr
+
+
+def _world(group):
+    import torch.distributed as dist
+    return dist.get_world_size(group) if dist.is_initialized() else 1
+
+
+def pfasst_run(levels, u0, t_end: float, p: int, blocks: int = 1, tol: float = 1e-9,
+               max_iter: int = 20, executor: str = "serial", record_final_values: bool = False,
+               engine_factory=None, group=None) -> PfasstResult:
+    """Run PFASST / IPFASST over ``blocks`` windows of ``p`` steps (pfasst.py:256-287).
+
+    ``u0`` may be a numpy array (result returned on the host, drop-in) or an
+    fp64 CUDA tensor (result stays on the device)."""
+    check_hierarchy(levels)
+    if executor not in ("serial", "threaded", "nccl"):
+        raise ValueError(f"unknown executor {executor!r}")
+    if p < 1 or blocks < 1:
+        raise ValueError("need at least one rank and one block")
+    dt = t_end / (p * blocks)
+    if engine_factory is None:
+        u, host = to_device(u0)
+        engine_factory = DeviceEngine
+    else:                       # test hook: alternative engines (CPU oracle)
+        u, host = u0, False
+    result = PfasstResult(u=u0)
+    engine = None
+    for block in range(blocks):
+        if executor == "nccl" and _world(group) > 1:
+            import torch.distributed as dist
+            world = dist.get_world_size(group)
+            me = dist.get_rank(group)
+            ranks = [n for n in range(p) if n % world == me]
+            if engine is None:
+                engine = engine_factory(levels, dt, ranks)
+            exchange = DistExchange(engine, group)
+        else:
+            if engine is None:
+                engine = engine_factory(levels, dt, range(p))
+            exchange = _LocalExchange(engine)
+        for n in range(p):
+            if exchange.owns(n):
+                engine.spread(n, u)
+        blk = _Block(engine, exchange, p, tol, max_iter, block, record_final_values)
+        blk.predictor()
+        blk.iterations_loop()
+        if isinstance(exchange, DistExchange):
+            exchange.finish()
+            last = (p - 1) % exchange.world
+            if exchange.owns(p - 1):
+                u = engine.snapshot(engine.fine_payload(p - 1))
+            else:
+                u = torch.empty_like(u)
+            exchange.dist.broadcast(u, last, group=group)
+            if record_final_values:
+                fv = [v.cpu().numpy() for v in blk.final_values] \
+                    if exchange.owns(p - 1) else None
+                holder = [fv]
+                exchange.dist.broadcast_object_list(holder, last, group=group)
+                blk.final_values = holder[0]
+        else:
+            u = engine.snapshot(engine.fine_payload(p - 1))
+        it, vc, cv, tr = _gather_block(blk, exchange)
+        result.rank_iterations.append(list(it))
+        result.rank_vcycles.append(list(vc))
+        result.converged.append(list(cv))
+        result.trace.extend(sorted(tr, key=lambda r: (r.iteration, r.rank, r.level)))
+        result.final_values.append([v.cpu().numpy() if host and isinstance(v, torch.Tensor)
+                                    else v for v in blk.final_values])
+    result.u = u.cpu().numpy() if host else u
+    return result
+
+
+def predictor_sweep_counts(p: int) -> list:
+    """pfasst.py:290-292."""
+    return [n + 1 for n in range(p)]
+
+
+def write_trace_csv(rows, path: str) -> None:
+    """pfasst.py:295-300 (byte-identical format)."""
+    with open(path, "w") as fh:
+        fh.write("block,rank,iter,level,residual,vcycles\n")
+        for r in rows:
+            fh.write(f"{r.block},{r.rank},{r.iteration},{r.level},"
+                     f"{r.residual:.16e},{r.vcycles}\n")

@@ -1,0 +1,293 @@
+"""Parity of the CUDA path against the reference's golden vectors (GPU).
+
+Golden fixtures come from the real reference (oracle/make_golden.py).  The
+bar (BASELINE.json north_star):
+  * element-wise kernels (stencil, diagonal, smoothers, transfers, FW) are
+    bit-identical -- the kernels restate numpy's expression trees with FMA
+    contraction disabled;
+  * anything downstream of the coarsest-grid LU or the BLAS contractions is
+    within 1e-10 relative L-inf (tolerances stated per test, tighter where
+    the arithmetic allows);
+  * iteration counts, V-cycle counts (per run and per sub-step solve) and
+    convergence flags are identical.
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+from paper_1407_6486_b200 import heat, hierarchy, multigrid as mg, pfasst, quadrature, sdc  # noqa: E402
+from paper_1407_6486_b200 import transfers  # noqa: E402
+from paper_1407_6486_b200 import _capi  # noqa: E402
+from tests.golden_io import case, names  # noqa: E402
+
+REL = 1e-10
+
+
+def bitwise(a, b):
+    a = a.cpu().numpy() if hasattr(a, "cpu") else np.asarray(a)
+    assert a.shape == b.shape
+    if not np.array_equal(a, b):
+        d = np.max(np.abs(a - b))
+        raise AssertionError(f"not bit-identical: max |diff| {d:.3e}")
+
+
+def close(a, b, rel=REL):
+    a = a.cpu().numpy() if hasattr(a, "cpu") else np.asarray(a)
+    assert a.shape == b.shape
+    scale = max(np.max(np.abs(b)), 1e-300)
+    err = np.max(np.abs(a - b)) / scale
+    assert err <= rel, f"relative L-inf error {err:.3e} > {rel:.1e}"
+    return err
+
+
+def dev(x):
+    return torch.from_numpy(np.ascontiguousarray(x)).cuda()
+
+
+@pytest.fixture(autouse=True)
+def _sync():
+    yield
+    torch.cuda.synchronize()
+
+
+# ---------------------------------------------------------------- L1: stencil
+@pytest.mark.parametrize("name", names("apply_"))
+def test_apply_diag_bitwise(name):
+    a, m = case(name)
+    op = heat.HeatOperator(heat.Grid(m["dim"], m["n"], m.get("length", 1.0)), m["nu"],
+                           m["order"])
+    bitwise(op.apply(dev(a["u"])), a["f"])
+    bitwise(op.diagonal(), a["diag"])
+    if "au" in a:
+        sop = mg.ShiftedOperator(op, m["sigma"])
+        bitwise(sop.apply(dev(a["u"])), a["au"])
+        bitwise(sop.diagonal(), a["sdiag"])
+
+
+def test_apply_numpy_in_numpy_out():
+    a, m = case("apply_d2_o2_nu1.0")
+    op = heat.HeatOperator(heat.Grid(2, m["n"]), 1.0, 2)
+    out = op.apply(a["u"])
+    assert isinstance(out, np.ndarray)
+    bitwise(out, a["f"])
+    with pytest.raises(ValueError):
+        op.apply(np.zeros((3, 3)))
+
+
+# ------------------------------------------------------------- transfers
+@pytest.mark.parametrize("name", names("transfer_"))
+def test_transfers_bitwise(name):
+    a, _ = case(name)
+    bitwise(transfers.full_weighting(dev(a["u"])), a["fw"])
+    bitwise(transfers.inject(dev(a["u"])), a["inj"])
+    bitwise(transfers.interp_linear(dev(a["c"])), a["lin"])
+    bitwise(transfers.interp_cubic(dev(a["c"])), a["cub"])
+
+
+@pytest.mark.parametrize("name", names("cubic_1d_"))
+def test_cubic_small_windows(name):
+    a, _ = case(name)
+    bitwise(transfers.interp_cubic(dev(a["c"])), a["cub"])
+
+
+# ------------------------------------------------------- smoothers, V-cycle
+@pytest.mark.parametrize("name", names("mg_"))
+def test_smoother_bitwise_vcycle_close(name):
+    a, m = case(name)
+    op = mg.ShiftedOperator(heat.HeatOperator(heat.Grid(m["dim"], m["n"]), 1.0, m["order"]),
+                            m["sigma"])
+    cfg = mg.MgConfig(smoother=m["smoother"], omega=m["omega"], pre_sweeps=m["pre"],
+                      post_sweeps=m["post"])
+    bitwise(mg.smooth(op, dev(a["u"]), dev(a["b"]), cfg, 2), a["sm2"])
+    # the coarsest-grid LU is the only non-element-wise step: 1e-13
+    close(mg.v_cycle(op, dev(a["u"]), dev(a["b"]), cfg), a["vc"], 1e-13)
+    close(mg.v_cycle(op, dev(np.zeros_like(a["b"])), dev(a["b"]), cfg), a["vc0"], 1e-13)
+
+
+@pytest.mark.parametrize("name", names("coarsest_"))
+def test_coarsest_direct(name):
+    a, m = case(name)
+    op = mg.ShiftedOperator(heat.HeatOperator(heat.Grid(m["dim"], 4)), m["sigma"])
+    close(mg.v_cycle(op, dev(np.zeros_like(a["b"])), dev(a["b"]), mg.MgConfig()), a["u"], 1e-14)
+
+
+@pytest.mark.parametrize("name", names("solve_"))
+def test_solve_policies(name):
+    a, m = case(name)
+    op = mg.ShiftedOperator(heat.HeatOperator(heat.Grid(m["dim"], m["n"])), m["sigma"])
+    r = mg.solve(op, dev(a["u0"]), dev(a["b"]), mg.MgConfig(), mg.FixedCycles(2))
+    assert (r.cycles, r.status) == (2, "fixed")
+    close(r.u, a["fixed2"], 1e-12)
+    r = mg.solve(op, dev(a["u0"]), dev(a["b"]), mg.MgConfig(), mg.ToTolerance(1e-12))
+    assert (r.cycles, r.status) == (m["tol_cycles"], m["tol_status"])
+    close(r.u, a["tol"], 1e-10)
+    r = mg.solve(op, dev(np.zeros_like(a["b"])), dev(a["b"]),
+                 mg.MgConfig(pre_sweeps=0, post_sweeps=0), mg.ToTolerance(1e-14))
+    assert (r.cycles, r.status) == (m["stall_cycles"], m["stall_status"])
+    close(r.u, a["stall"], 1e-10)
+    with pytest.raises(mg.MultigridError) as ei:
+        mg.solve(op, dev(np.zeros_like(a["b"])), dev(a["b"]), mg.MgConfig(),
+                 mg.ToTolerance(1e-14, stall=1.0 - 1e-12, max_cycles=3))
+    assert ei.value.cycles == m["cap"]["cycles"]
+    assert abs(ei.value.residual - m["cap"]["residual"]) <= 1e-10 * m["cap"]["residual"]
+
+
+def test_zero_rhs_tolerance_solve():
+    op = mg.ShiftedOperator(heat.HeatOperator(heat.Grid(1, 32)), 0.1)
+    r = mg.solve(op, dev(np.ones(31)), dev(np.zeros(31)), mg.MgConfig(), mg.ToTolerance(1e-12))
+    assert (r.cycles, r.status) == (0, "converged")
+    assert torch.count_nonzero(r.u).item() == 0
+
+
+# ----------------------------------------------------------------- SDC sweep
+@pytest.mark.parametrize("name", names("sweep_"))
+def test_sweep_and_residual(name):
+    a, m = case(name)
+    op = heat.HeatOperator(heat.Grid(m["dim"], m["n"]))
+    table = quadrature.uniform_table(m["M"])
+    y = dev(a["y"])
+    f = torch.stack([op.apply(v) for v in y])
+    st = sdc.NodeStates(table, y, f)
+    pol = mg.FixedCycles(1) if m["policy"] == "fixed1" else mg.ToTolerance(1e-12)
+    tau = dev(a["tau"]) if "tau" in a else None
+    cyc = sdc.sdc_sweep(st, dev(a["y0"]), m["dt"], op, mg.MgConfig(), pol, tau=tau)
+    assert cyc == m["cycles"]
+    close(st.y, a["y_out"], 1e-12)
+    close(st.f, a["f_out"], 1e-10)
+    res = sdc.residual(st, dev(a["y0"]), m["dt"], tau=tau)
+    assert abs(res - m["residual"]) <= 1e-10 * max(m["residual"], 1e-6)
+
+
+def test_sweep_substep_error():
+    op = heat.HeatOperator(heat.Grid(1, 32))
+    table = quadrature.uniform_table(2)
+    rng = np.random.default_rng(3)
+    st = sdc.NodeStates.spread(op, table, dev(rng.standard_normal(31)))
+    with pytest.raises(sdc.SubStepError) as ei:
+        sdc.sdc_sweep(st, st.y[0].clone(), 0.05, op, mg.MgConfig(),
+                      mg.ToTolerance(1e-15, stall=1.0 - 1e-12, max_cycles=1))
+    assert ei.value.substep == 1
+    assert isinstance(ei.value.cause, mg.MultigridError)
+
+
+# ------------------------------------------------------------------ FAS
+def _fas_levels(m):
+    return [hierarchy.Level(heat.HeatOperator(heat.Grid(m["dim"], n)),
+                            quadrature.uniform_table(M), mg.MgConfig(), mg.FixedCycles(1),
+                            space_interp_order=m["interp"])
+            for n, M in zip(m["ns"], (4, 2, 1))]
+
+
+@pytest.mark.parametrize("name", names("fas_"))
+def test_fas_machinery(name):
+    a, m = case(name)
+    lv = _fas_levels(m)
+    f, c = lv[0], lv[1]
+    y = dev(a["y"])
+    fst = sdc.NodeStates(f.table, y.clone(), torch.stack([f.operator.apply(v) for v in y]))
+    rs = hierarchy.restrict_state(fst, f, c)
+    bitwise(rs.y, a["ry"])
+    bitwise(rs.f, a["rf"])
+    close(hierarchy.compute_fas(fst, rs, f, c, m["dt"], fine_tau=dev(a["ftau"])), a["tau"], 1e-12)
+    close(hierarchy.compute_fas(fst, rs, f, c, m["dt"]), a["tau0"], 1e-12)
+    new = sdc.NodeStates(c.table, dev(a["newc"]), rs.f.clone())
+    cc = fst.copy()
+    hierarchy.coarse_correction(cc, rs, new, f, c)
+    close(cc.y, a["cc_y"], 1e-14)
+    close(cc.f, a["cc_f"], 1e-12)
+    ts, c0 = hierarchy.initialize_step(lv, dev(a["u0"]), m["dt"])
+    assert c0 == m["init_cycles"]
+    assert hierarchy.mlsdc_iteration(ts, m["dt"]) == m["it_cycles"]
+    res = sdc.residual(ts.states[0], ts.y0[0], m["dt"])
+    assert abs(res - m["residual"]) <= 1e-10 * max(m["residual"], 1e-6)
+    close(ts.states[0].y, a["ml_y0"], 1e-11)
+    close(ts.states[1].y, a["ml_y1"], 1e-11)
+    close(ts.states[2].y, a["ml_y2"], 1e-11)
+
+
+# ------------------------------------------------------------- PFASST runs
+def levels_from(m):
+    pol = mg.FixedCycles(m["policy"][1]) if m["policy"][0] == "fixed" else \
+        mg.ToTolerance(*m["policy"][1:])
+    orders = m.get("orders") or [2] * len(m["ns"])
+    return [hierarchy.Level(heat.HeatOperator(heat.Grid(m["d"], n), 1.0, o),
+                            quadrature.uniform_table(k - 1),
+                            mg.MgConfig(m["sm"], m["om"], m["pre"], m["post"]), pol,
+                            space_interp_order=m.get("interp", 4))
+            for n, k, o in zip(m["ns"], m["nodes"], orders)]
+
+
+RUNS = ["run_cfg0", "run_cfg0_interp2", "run_cfg1", "run_cfg1_fc2", "run_cfg2_small",
+        "run_cfg2_small_fc2", "run_cfg3_small", "run_cfg4_small", "run_cfg4_small_tol",
+        "run_order4_small", "run_same_n_3lvl"]
+
+
+@pytest.mark.parametrize("name", RUNS)
+def test_pfasst_run_parity(name):
+    a, m = case(name)
+    levels = levels_from(m)
+    t_end = m["dt"] * m["p"] * m["blocks"]
+    res = pfasst.pfasst_run(levels, dev(a["u0"]), t_end, m["p"], blocks=m["blocks"],
+                            tol=m["tol"], max_iter=20, record_final_values=True)
+    assert res.rank_iterations == m["rank_iterations"]
+    assert res.rank_vcycles == m["rank_vcycles"]
+    assert res.converged == m["converged"]
+    got = [(t.block, t.rank, t.iteration, t.level, t.vcycles) for t in res.trace]
+    assert got == [(r[0], r[1], r[2], r[3], r[5]) for r in m["trace"]]
+    u0max = np.max(np.abs(a["u0"]))
+    for t, r in zip(res.trace, m["trace"]):
+        assert abs(t.residual - r[4]) <= 1e-10 * max(abs(r[4]), u0max * 1e-6)
+    close(res.u, a["u"], REL)
+    fv = res.final_values[-1][m["finals_kept_from"]:]
+    for got_v, ref_v in zip(fv, a["finals"]):
+        close(got_v, ref_v, REL)
+
+
+def test_pfasst_numpy_drop_in_and_executors():
+    a, m = case("run_cfg1")
+    levels = levels_from(m)
+    t_end = m["dt"] * m["p"]
+    r1 = pfasst.pfasst_run(levels, a["u0"], t_end, m["p"], tol=m["tol"], executor="serial")
+    r2 = pfasst.pfasst_run(levels, a["u0"], t_end, m["p"], tol=m["tol"], executor="threaded")
+    assert isinstance(r1.u, np.ndarray)
+    assert np.array_equal(r1.u, r2.u)
+    assert r1.rank_iterations == r2.rank_iterations == m["rank_iterations"]
+    assert [t.residual for t in r1.trace] == [t.residual for t in r2.trace]
+    with pytest.raises(ValueError):
+        pfasst.pfasst_run(levels, a["u0"], t_end, 2, executor="mpi")
+    with pytest.raises(ValueError):
+        pfasst.pfasst_run(levels, a["u0"], t_end, 0)
+
+
+def test_serial_drivers_and_p1_equivalence():
+    a, m = case("serial_drivers")
+    lv = [hierarchy.Level(heat.HeatOperator(heat.Grid(1, n)), quadrature.uniform_table(k - 1),
+                          mg.MgConfig(), mg.FixedCycles(1), space_interp_order=4)
+          for n, k in ((64, 3), (32, 2))]
+    ml = hierarchy.run_mlsdc(lv, a["u0"], 0.25, 4, 1e-10, 20)
+    assert ml.iterations == m["ml_iterations"] and ml.vcycles == m["ml_vcycles"]
+    close(ml.u, a["ml_u"], REL)
+    sd = sdc.run_sdc(lv[0].operator, lv[0].table, a["u0"], 0.25, 4, 1e-10, 20, mg.MgConfig(),
+                     mg.FixedCycles(1))
+    assert sd.iterations == m["sdc_iterations"] and sd.vcycles == m["sdc_vcycles"]
+    close(sd.u, a["sdc_u"], REL)
+    p1 = pfasst.pfasst_run(lv, a["u0"], 0.25 / 4, 1, tol=1e-10, max_iter=20)
+    assert p1.rank_iterations == m["p1_iterations"]
+    close(p1.u, a["p1_u"], REL)
+    # P = 1 PFASST is bitwise the serial MLSDC on the GPU too (test_pfasst.py:30-35)
+    ml1 = hierarchy.run_mlsdc(lv, a["u0"], 0.25 / 4, 1, 1e-10, 20)
+    assert np.array_equal(ml1.u, p1.u)
+
+
+def test_launch_stats_count_native_kernels():
+    _capi.stats_reset()
+    op = heat.HeatOperator(heat.Grid(3, 16))
+    op.apply(dev(np.ones((15, 15, 15))))
+    torch.cuda.synchronize()
+    st = _capi.stats()
+    assert st["apply"][0] == 1 and st["apply"][1] == 16.0 * 15 ** 3
