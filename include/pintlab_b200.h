@@ -92,6 +92,14 @@ int pl_mg_plan_create(pl_mg_plan** plan, int dim, int n, double length, double n
 int pl_mg_plan_destroy(pl_mg_plan* plan);
 /* factor the coarsest-grid system for sigma ahead of time (capture-safe) */
 int pl_mg_prepare(pl_mg_plan* plan, double sigma, void* stream);
+/* install the LAPACK getrf factors of the coarsest-grid system for sigma
+   (row-major packed L\U, 0-based pivots, m = pl_mg_coarsest_size unknowns);
+   the Python layer passes scipy.linalg.lu_factor's result -- the call the
+   reference makes (multigrid.py:161-164) -- so the factors are the
+   reference's own; without it the plan factors on the host itself */
+int pl_mg_set_coarsest_lu(pl_mg_plan* plan, double sigma, const double* lu, const int* piv,
+                          void* stream);
+int pl_mg_coarsest_size(pl_mg_plan* plan);
 /* smooth(op, u, b, cfg, count), in place on u (multigrid.py:211-234) */
 int pl_mg_smooth(pl_mg_plan* plan, double* u, const double* b, double sigma, int count,
                  void* stream);
@@ -164,10 +172,11 @@ size_t pl_coarse_correction_scratch_bytes(int dim, int nf, int nc, int mf, int i
 /* counts and algorithmic bytes (SURVEY.md 8(d) model) of launched kernels */
 int pl_stats_reset(void);
 int pl_stats_get(long long* launches, double* alg_bytes, int nkinds);
-/* CUDA-event timing of every launch of one kernel kind (-1 = off);
-   pl_timing_collect returns launches timed and total milliseconds */
-int pl_timing_enable(int kind);
-int pl_timing_collect(long long* launches, double* total_ms, double* alg_bytes);
+/* CUDA-event timing of every launch of the kernel kinds in `mask` (bit k =
+   kind k; 0 = off); pl_timing_collect returns, for one kind, the launches
+   timed, their total milliseconds and their algorithmic bytes */
+int pl_timing_enable(unsigned mask);
+int pl_timing_collect(int kind, long long* launches, double* total_ms, double* alg_bytes);
 const char* pl_kind_name(int kind);
 
 #ifdef __cplusplus

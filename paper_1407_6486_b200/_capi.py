@@ -58,6 +58,8 @@ _SIGS = {
                                 i32, vp, sz]),
     "pl_mg_plan_destroy": (i32, [vp]),
     "pl_mg_prepare": (i32, [vp, f64, vp]),
+    "pl_mg_set_coarsest_lu": (i32, [vp, f64, dp, ip, vp]),
+    "pl_mg_coarsest_size": (i32, [vp]),
     "pl_mg_smooth": (i32, [vp, vp, vp, f64, i32, vp]),
     "pl_mg_vcycles": (i32, [vp, vp, vp, f64, i32, i32, vp]),
     "pl_mg_solve_tol": (i32, [vp, vp, vp, f64, f64, f64, i32, ip, ip, dp, vp]),
@@ -74,8 +76,8 @@ _SIGS = {
     "pl_coarse_correction_scratch_bytes": (sz, [i32, i32, i32, i32, i32]),
     "pl_stats_reset": (i32, []),
     "pl_stats_get": (i32, [C.POINTER(i64), dp, i32]),
-    "pl_timing_enable": (i32, [i32]),
-    "pl_timing_collect": (i32, [C.POINTER(i64), dp, dp]),
+    "pl_timing_enable": (i32, [C.c_uint]),
+    "pl_timing_collect": (i32, [i32, C.POINTER(i64), dp, dp]),
     "pl_kind_name": (C.c_char_p, [i32]),
 }
 
@@ -143,11 +145,21 @@ def kind_index(name):
     raise KeyError(name)
 
 
-def timing_enable(name):
-    lib().pl_timing_enable(-1 if name is None else kind_index(name))
+def kind_names():
+    return [lib().pl_kind_name(k).decode() for k in range(NUM_KINDS)]
 
 
-def timing_collect():
+def timing_enable(names):
+    """Record CUDA events around every launch of the given kernel kinds
+    (None / empty: off)."""
+    mask = 0
+    for n in names or ():
+        mask |= 1 << kind_index(n)
+    lib().pl_timing_enable(mask)
+
+
+def timing_collect(name):
+    """(launches, total_ms, alg_bytes) for one kind since timing_enable."""
     n, t, b = i64(0), f64(0), f64(0)
-    check(lib().pl_timing_collect(C.byref(n), C.byref(t), C.byref(b)))
+    check(lib().pl_timing_collect(kind_index(name), C.byref(n), C.byref(t), C.byref(b)))
     return int(n.value), float(t.value), float(b.value)

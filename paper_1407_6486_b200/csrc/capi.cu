@@ -45,34 +45,37 @@ void count_launch(int kind, double alg_bytes) {
   g_bytes[kind] += alg_bytes;
 }
 
-static int g_time_kind = -1;
+static unsigned g_time_mask = 0;     // kinds whose launches get event pairs
 struct EvPair {
   cudaEvent_t a, b;
   double bytes;
+  int kind;
 };
 static std::vector<EvPair> g_ev_pool;
 static size_t g_ev_used = 0;
-static bool g_ev_open = false;
+static int g_ev_open = -1;
 
 void timing_pre(int kind, cudaStream_t s) {
-  if (kind != g_time_kind) return;
+  if (!(g_time_mask & (1u << kind))) return;
   if (g_ev_used == g_ev_pool.size()) {
     EvPair p;
     cudaEventCreate(&p.a);
     cudaEventCreate(&p.b);
     p.bytes = 0;
+    p.kind = -1;
     g_ev_pool.push_back(p);
   }
   cudaEventRecord(g_ev_pool[g_ev_used].a, s);
-  g_ev_open = true;
+  g_ev_open = kind;
 }
 
 void timing_post(int kind, cudaStream_t s, double alg_bytes) {
-  if (kind != g_time_kind || !g_ev_open) return;
+  if (!(g_time_mask & (1u << kind)) || g_ev_open != kind) return;
   cudaEventRecord(g_ev_pool[g_ev_used].b, s);
   g_ev_pool[g_ev_used].bytes = alg_bytes;
+  g_ev_pool[g_ev_used].kind = kind;
   ++g_ev_used;
-  g_ev_open = false;
+  g_ev_open = -1;
 }
 
 static const char* kKindNames[K_NUM_KINDS] = {
@@ -306,6 +309,13 @@ int pl_mg_prepare(pl_mg_plan* plan, double sigma, void* stream) {
   return mg_prepare((MgPlan*)plan, sigma, (cudaStream_t)stream);
 }
 
+int pl_mg_set_coarsest_lu(pl_mg_plan* plan, double sigma, const double* lu, const int* piv,
+                          void* stream) {
+  return mg_set_coarsest_lu((MgPlan*)plan, sigma, lu, piv, (cudaStream_t)stream);
+}
+
+int pl_mg_coarsest_size(pl_mg_plan* plan) { return ((MgPlan*)plan)->m_lu; }
+
 int pl_mg_smooth(pl_mg_plan* plan, double* u, const double* b, double sigma, int count,
                  void* stream) {
   if (count < 0) return PL_ERR_ARG;
@@ -451,24 +461,27 @@ int pl_stats_get(long long* launches, double* alg_bytes, int nkinds) {
   return 0;
 }
 
-int pl_timing_enable(int kind) {
-  g_time_kind = kind;
+int pl_timing_enable(unsigned mask) {
+  g_time_mask = mask;
   g_ev_used = 0;
-  g_ev_open = false;
+  g_ev_open = -1;
   return 0;
 }
 
-int pl_timing_collect(long long* launches, double* total_ms, double* alg_bytes) {
+int pl_timing_collect(int kind, long long* launches, double* total_ms, double* alg_bytes) {
   double t = 0, b = 0;
+  long long n = 0;
   for (size_t i = 0; i < g_ev_used; ++i) {
+    if (g_ev_pool[i].kind != kind) continue;
     cudaError_t e = cudaEventSynchronize(g_ev_pool[i].b);
     if (e != cudaSuccess) return cuda_status(e, "event sync");
     float ms = 0;
     cudaEventElapsedTime(&ms, g_ev_pool[i].a, g_ev_pool[i].b);
     t += ms;
     b += g_ev_pool[i].bytes;
+    ++n;
   }
-  *launches = (long long)g_ev_used;
+  *launches = n;
   *total_ms = t;
   *alg_bytes = b;
   return 0;

@@ -155,17 +155,21 @@ __device__ void tail_lu(const TailArgs& a, const double* b, double* u) {
       }
     }
     __syncwarp();
-    for (int j = 0; j < m; ++j) {            // L y = Pb, column oriented
+    // column-oriented substitutions with FMA axpy updates and a true
+    // division by the pivot -- the operation order of LAPACK getrs over
+    // BLAS trsv/axpy (bit-identical to scipy.linalg.lu_solve, see
+    // tests/test_gpu_parity.py::test_coarsest_direct)
+    for (int j = 0; j < m; ++j) {            // L y = Pb (unit lower)
       double yj = u[j];
       __syncwarp();
-      for (int i = j + 1 + threadIdx.x; i < m; i += 32) u[i] = u[i] - A[i * m + j] * yj;
+      for (int i = j + 1 + threadIdx.x; i < m; i += 32) u[i] = __fma_rn(-yj, A[i * m + j], u[i]);
       __syncwarp();
     }
     for (int j = m - 1; j >= 0; --j) {       // U x = y
       if (threadIdx.x == 0) u[j] = u[j] / A[j * m + j];
       __syncwarp();
       double xj = u[j];
-      for (int i = threadIdx.x; i < j; i += 32) u[i] = u[i] - A[i * m + j] * xj;
+      for (int i = threadIdx.x; i < j; i += 32) u[i] = __fma_rn(-xj, A[i * m + j], u[i]);
       __syncwarp();
     }
   }
@@ -470,9 +474,13 @@ static void coarsest_lu_host(const MgPlan* P, double sigma, double* out) {
   std::memcpy(out + (size_t)m * m, piv.data(), sizeof(double) * m);
 }
 
-int mg_prepare(MgPlan* P, double sigma, cudaStream_t s) {
+static int lu_entry(MgPlan* P, double sigma, LuEntry** out) {
   unsigned long long key = *(unsigned long long*)&sigma;
-  if (P->lu.count(key)) return 0;
+  auto it = P->lu.find(key);
+  if (it != P->lu.end()) {
+    *out = &it->second;
+    return 0;
+  }
   size_t count = (size_t)P->m_lu * P->m_lu + P->m_lu;
   LuEntry E;
   cudaError_t e = cudaMallocHost(&E.host, count * sizeof(double));
@@ -482,10 +490,38 @@ int mg_prepare(MgPlan* P, double sigma, cudaStream_t s) {
     cudaFreeHost(E.host);
     return cuda_status(e, "cudaMalloc lu");
   }
-  coarsest_lu_host(P, sigma, E.host);
-  e = cudaMemcpyAsync(E.dev, E.host, count * sizeof(double), cudaMemcpyHostToDevice, s);
-  if (e != cudaSuccess) return cuda_status(e, "upload lu");
   P->lu[key] = E;
+  *out = &P->lu[key];
+  return 1;   // new, not filled
+}
+
+int mg_prepare(MgPlan* P, double sigma, cudaStream_t s) {
+  LuEntry* E = nullptr;
+  int rc = lu_entry(P, sigma, &E);
+  if (rc <= 0) return rc;
+  size_t count = (size_t)P->m_lu * P->m_lu + P->m_lu;
+  coarsest_lu_host(P, sigma, E->host);
+  cudaError_t e = cudaMemcpyAsync(E->dev, E->host, count * sizeof(double),
+                                  cudaMemcpyHostToDevice, s);
+  if (e != cudaSuccess) return cuda_status(e, "upload lu");
+  return 0;
+}
+
+int mg_set_coarsest_lu(MgPlan* P, double sigma, const double* lu, const int* piv,
+                       cudaStream_t s) {
+  LuEntry* E = nullptr;
+  int rc = lu_entry(P, sigma, &E);
+  if (rc < 0) return rc;
+  const size_t mm = (size_t)P->m_lu * P->m_lu;
+  // the previous upload of this entry must have landed before the staging
+  // buffer is rewritten
+  cudaError_t e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return cuda_status(e, "sync");
+  std::memcpy(E->host, lu, sizeof(double) * mm);
+  for (int i = 0; i < P->m_lu; ++i) E->host[mm + i] = (double)piv[i];
+  e = cudaMemcpyAsync(E->dev, E->host, (mm + P->m_lu) * sizeof(double),
+                      cudaMemcpyHostToDevice, s);
+  if (e != cudaSuccess) return cuda_status(e, "upload lu");
   return 0;
 }
 

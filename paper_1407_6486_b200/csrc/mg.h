@@ -52,6 +52,9 @@ void mg_plan_destroy(MgPlan* p);
 // make sure the coarsest LU for sigma exists (host factorisation + async
 // upload); call outside CUDA-graph capture
 int mg_prepare(MgPlan* p, double sigma, cudaStream_t s);
+// install caller-provided LAPACK getrf factors (row-major LU, 0-based pivots)
+int mg_set_coarsest_lu(MgPlan* p, double sigma, const double* lu, const int* piv,
+                       cudaStream_t s);
 // `count` smoothing sweeps in place on u (multigrid.py:211-234)
 int mg_smooth(MgPlan* p, double* u, const double* b, double sigma, int count, cudaStream_t s);
 // `ncycles` V-cycles in place on u (multigrid.py:237-251, 265-269);

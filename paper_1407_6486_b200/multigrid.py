@@ -11,6 +11,8 @@ import ctypes as C
 from dataclasses import dataclass
 from typing import Union
 
+import numpy as np
+import scipy.linalg
 import torch
 
 from . import _capi as capi
@@ -96,6 +98,27 @@ class _Plan:
                                          cfg.coarsest_n, self.ws.data_ptr(), nbytes),
                    "MG plan")
         self.handle = h
+        self.op, self.cfg = op, cfg
+        self._factored = set()
+        n = g.n
+        while n > cfg.coarsest_n and n >= 4:
+            n //= 2
+        self.coarsest = HeatOperator(Grid(g.dim, n, g.length), op.nu, op.order)
+
+    def ensure(self, sigma: float):
+        """Factor the coarsest-grid system I - sigma A once per sigma with the
+        reference's own LAPACK call (scipy.linalg.lu_factor, multigrid.py:
+        161-164) and install the factors; the solve itself runs on the GPU."""
+        sigma = float(sigma)
+        if sigma in self._factored:
+            return
+        lu, piv = scipy.linalg.lu_factor(_dense_shifted(self.coarsest, sigma))
+        lu = np.ascontiguousarray(lu)
+        piv = np.ascontiguousarray(piv, dtype=np.int32)
+        capi.check(capi.lib().pl_mg_set_coarsest_lu(
+            self.handle.value, sigma, lu.ctypes.data_as(C.POINTER(C.c_double)),
+            piv.ctypes.data_as(C.POINTER(C.c_int)), stream_ptr()), "coarsest LU")
+        self._factored.add(sigma)
 
     def __del__(self):
         try:
@@ -106,6 +129,42 @@ class _Plan:
 
 
 _plans: dict = {}
+
+
+def _laplacian_1d(n, length, order):
+    """Dense 1-D nu-free stencil matrix with the reference's entry values
+    (multigrid.py:86-107)."""
+    dx2 = (length / n) ** 2
+    npts = n - 1
+    a = np.zeros((npts, npts))
+    for i in range(npts):
+        if order == 2 or i in (0, npts - 1):
+            a[i, i] = -2.0 / dx2
+            if i > 0:
+                a[i, i - 1] = 1.0 / dx2
+            if i < npts - 1:
+                a[i, i + 1] = 1.0 / dx2
+        else:
+            for off, w in ((-2, -1.0), (-1, 16.0), (0, -30.0), (1, 16.0), (2, -1.0)):
+                if 0 <= i + off < npts:
+                    a[i, i + off] = w / (12.0 * dx2)
+    return a
+
+
+def _dense_shifted(op: HeatOperator, sigma: float):
+    """I - sigma * nu * (Kronecker sum of the 1-D stencils, axis order)
+    (multigrid.py:110-135); dense, only for the <= 3^d coarsest grid."""
+    g = op.grid
+    d1 = _laplacian_1d(g.n, g.length, op.order)
+    eye = np.eye(g.n - 1)
+    total = None
+    for axis in range(g.dim):
+        term = None
+        for k in range(g.dim):
+            f = d1 if k == axis else eye
+            term = f if term is None else np.kron(term, f)
+        total = term if total is None else total + term
+    return np.eye(total.shape[0]) - sigma * (op.nu * total)
 
 
 def plan_for(op: HeatOperator, cfg: MgConfig) -> _Plan:
@@ -176,6 +235,7 @@ def smooth(op: ShiftedOperator, u, b, cfg: MgConfig, count: int):
 def vcycles_into(op: ShiftedOperator, u, b, cfg: MgConfig, ncycles: int, zero_guess=False):
     """ncycles V-cycles in place on the device tensor u."""
     p = plan_for(op.base, cfg)
+    p.ensure(op.sigma)
     capi.check(capi.lib().pl_mg_vcycles(p.handle.value, ptr(u), ptr(b), float(op.sigma),
                                         ncycles, int(zero_guess), stream_ptr()), "v_cycle")
     return u
@@ -206,6 +266,7 @@ def solve_into(op: ShiftedOperator, u, b, cfg: MgConfig, policy) -> tuple:
         vcycles_into(op, u, b, cfg, policy.cycles)
         return policy.cycles, "fixed"
     p = plan_for(op.base, cfg)
+    p.ensure(op.sigma)
     cyc, st, res = C.c_int(0), C.c_int(0), C.c_double(0)
     rc = capi.lib().pl_mg_solve_tol(p.handle.value, ptr(u), ptr(b), float(op.sigma),
                                     float(policy.tol), float(policy.stall), policy.max_cycles,

@@ -101,6 +101,8 @@ def sdc_sweep(states: NodeStates, y0, dt: float, op: HeatOperator, mg_cfg: MgCon
     ttau = to_device(tau)[0] if tau is not None else None
     desc = sweep_desc(states.table, policy)
     plan = plan_for(op, mg_cfg)
+    for gam in states.table.nodes.gammas:
+        plan.ensure(float(gam) * dt)            # sdc.py:101 sigma of each sub-step
     g = op.grid
     nb = capi.lib().pl_sweep_workspace_bytes(g.dim, g.n, states.table.m)
     ws = scratch("sweep", nb)
