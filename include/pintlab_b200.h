@@ -59,6 +59,10 @@ typedef struct pl_mg_plan pl_mg_plan;
 int pl_abi_version(void);
 const char* pl_last_error(void);
 
+/* runtime options (A/B testing of kernel variants; results are bit-identical) */
+#define PL_OPT_ZMARCH 0 /* 1 (default): cp.async z-marching + fused sweeps for 3-D order 2 */
+int pl_set_option(int key, int value);
+
 /* ---- heat operator (heat.py) ------------------------------------------- */
 /* f = nu * Lap_h u, order 2 or 4 (HeatOperator.apply, heat.py:111-142) */
 int pl_heat_apply(const double* u, double* f, int dim, int n, double length, double nu,

@@ -279,6 +279,26 @@ def main():
                            "p1_iterations": p1.rank_iterations},
         u0=u0, ml_u=ml.u, sdc_u=isdc.u, p1_u=p1.u)
 
+    # ---- 3-D n = 32 cases (exercise the z-marching / fused-sweep kernels,
+    # which engage from 31^3 up); appended last so earlier draws are unchanged
+    rng2 = np.random.default_rng(4242)
+    op32 = HeatOperator(Grid(3, 32), 1.0, 2)
+    u = rng2.standard_normal(op32.grid.shape)
+    b = rng2.standard_normal(op32.grid.shape)
+    sop = mg.ShiftedOperator(op32, 1.0 / 256)
+    meta = {"dim": 3, "n": 32, "sigma": 1.0 / 256}
+    arr = {"u": u, "b": b, "f": op32.apply(u), "r": b - sop.apply(u)}
+    for sm, om in (("jacobi", 2.0 / 3.0), ("jor-rb", 1.0), ("jor-rb", 0.8)):
+        cfg = mg.MgConfig(smoother=sm, omega=om, pre_sweeps=2, post_sweeps=2)
+        tag = f"{sm}_{om:.3f}"
+        for cnt in (1, 2, 3):
+            arr[f"sm{cnt}_{tag}"] = mg.smooth(sop, u, b, cfg, cnt)
+        arr[f"vc22_{tag}"] = mg.v_cycle(sop, u, b, cfg)
+        arr[f"vc22z_{tag}"] = mg.v_cycle(sop, np.zeros_like(b), b, cfg)
+        cfg11 = mg.MgConfig(smoother=sm, omega=om, pre_sweeps=1, post_sweeps=1)
+        arr[f"vc11_{tag}"] = mg.v_cycle(sop, u, b, cfg11)
+    put("mg32_d3", meta, **arr)
+
     for case, arr in arrays.items():
         np.savez_compressed(OUT / f"{case}.npz", **arr)
     with open(OUT / "manifest.json", "w") as fh:

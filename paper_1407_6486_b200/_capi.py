@@ -45,6 +45,7 @@ class SweepDesc(C.Structure):
 _SIGS = {
     "pl_abi_version": (i32, []),
     "pl_last_error": (C.c_char_p, []),
+    "pl_set_option": (i32, [i32, i32]),
     "pl_heat_apply": (i32, [vp, vp, i32, i32, f64, f64, i32, vp]),
     "pl_heat_diagonal": (i32, [vp, i32, i32, f64, f64, i32, f64, i32, vp]),
     "pl_shifted_apply": (i32, [vp, vp, i32, i32, f64, f64, i32, f64, vp]),
@@ -108,6 +109,13 @@ def lib():
 
 class MultigridErrorBase(RuntimeError):
     pass
+
+
+OPT_ZMARCH = 0
+
+
+def set_option(key, value):
+    check(lib().pl_set_option(key, int(value)), "set_option")
 
 
 def last_error():

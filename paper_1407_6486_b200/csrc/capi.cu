@@ -213,9 +213,22 @@ __global__ void k_shifted_apply(const double* __restrict__ u, double* __restrict
 }
 }  // namespace
 
+namespace pl {
+extern int g_zmarch_enabled;
+}
+
 extern "C" {
 
 int pl_abi_version(void) { return PL_ABI_VERSION; }
+
+int pl_set_option(int key, int value) {
+  if (key == PL_OPT_ZMARCH) {
+    g_zmarch_enabled = value != 0;
+    return 0;
+  }
+  set_error("unknown option %d", key);
+  return PL_ERR_ARG;
+}
 const char* pl_last_error(void) { return g_err; }
 
 int pl_heat_apply(const double* u, double* f, int dim, int n, double length, double nu,

@@ -24,6 +24,20 @@ int launch_sumsq(const double* u, const double* b, const Geo& g, const OpC& c, d
                  double* partials, int npartials, double* out, cudaStream_t s);
 int sumsq_partials(const Geo& g);
 
+// ---- zmarch.cu: cp.async-pipelined 3-D order-2 versions (zmarch_ok) -------
+bool zmarch_ok(const Geo& g, const OpC& c);
+int zlaunch_apply(const double* u, double* f, const Geo& g, const OpC& c, cudaStream_t s);
+int zlaunch_residual(const double* u, const double* b, double* r, const Geo& g, const OpC& c,
+                     double sigma, cudaStream_t s);
+int zlaunch_jacobi(const double* u, const double* b, double* out, const Geo& g, const OpC& c,
+                   double sigma, double omega, int zero_in, cudaStream_t s);
+// two fused Jacobi sweeps u -> out (out != u)
+int zlaunch_jacobi2(const double* u, const double* b, double* out, const Geo& g, const OpC& c,
+                    double sigma, double omega, int zero_in, cudaStream_t s);
+// one fused red+black jor-rb sweep u -> out (out != u)
+int zlaunch_rb(const double* u, const double* b, double* out, const Geo& g, const OpC& c,
+               double sigma, double omega, cudaStream_t s);
+
 // ---- transfer.cu -----------------------------------------------------------
 // coarse = FW(fine) (transfers.py:27-34); fine geometry gf
 int launch_fw(const double* fine, double* coarse, const Geo& gf, cudaStream_t s);

@@ -540,8 +540,16 @@ static int level_smooth(MgPlan* P, MgLevel& L, double** cur, double* alt_u, cons
     }
     return 0;
   }
+  const bool fused = zmarch_ok(L.g, L.c);
   if (P->smoother == SM_JACOBI) {
-    for (int k = 0; k < count; ++k) {
+    int k = 0;
+    if (fused) {             // pairs of sweeps in one pass (temporal blocking)
+      for (; k + 1 < count; k += 2) {
+        PL_TRY(zlaunch_jacobi2(u, b, other, L.g, L.c, sigma, P->omega, zero && k == 0, s));
+        std::swap(u, other);
+      }
+    }
+    for (; k < count; ++k) {
       PL_TRY(launch_jacobi(u, b, other, L.g, L.c, sigma, P->omega, zero && k == 0, s));
       std::swap(u, other);
     }
@@ -553,7 +561,10 @@ static int level_smooth(MgPlan* P, MgLevel& L, double** cur, double* alt_u, cons
     if (e != cudaSuccess) return cuda_status(e, "memset");
   }
   for (int k = 0; k < count; ++k) {
-    if (P->order == 2) {    // same-colour points never neighbour: in place
+    if (fused) {            // red and black in one pass, out of place
+      PL_TRY(zlaunch_rb(u, b, other, L.g, L.c, sigma, P->omega, s));
+      std::swap(u, other);
+    } else if (P->order == 2) {    // same-colour points never neighbour: in place
       PL_TRY(launch_rb(u, b, u, L.g, L.c, sigma, P->omega, 1, s));
       PL_TRY(launch_rb(u, b, u, L.g, L.c, sigma, P->omega, 0, s));
     } else {                // order 4: +-2 neighbours share the colour

@@ -157,6 +157,7 @@ __global__ void k_sum_final(const double* __restrict__ partials, int n, double* 
   } while (0)
 
 int launch_apply(const double* u, double* f, const Geo& g, const OpC& c, cudaStream_t s) {
+  if (zmarch_ok(g, c)) return zlaunch_apply(u, f, g, c, s);
   Launch L = plan_launch(g);
   PL_PRE(K_APPLY);
   PL_DISPATCH_DIM(g, k_apply, L, s, u, f, g, c);
@@ -166,6 +167,7 @@ int launch_apply(const double* u, double* f, const Geo& g, const OpC& c, cudaStr
 
 int launch_residual(const double* u, const double* b, double* r, const Geo& g, const OpC& c,
                     double sigma, cudaStream_t s) {
+  if (zmarch_ok(g, c)) return zlaunch_residual(u, b, r, g, c, sigma, s);
   Launch L = plan_launch(g);
   PL_PRE(K_RESID);
   PL_DISPATCH_DIM(g, k_residual, L, s, u, b, r, g, c, sigma);
@@ -175,6 +177,7 @@ int launch_residual(const double* u, const double* b, double* r, const Geo& g, c
 
 int launch_jacobi(const double* u, const double* b, double* out, const Geo& g, const OpC& c,
                   double sigma, double omega, int zero_in, cudaStream_t s) {
+  if (zmarch_ok(g, c)) return zlaunch_jacobi(u, b, out, g, c, sigma, omega, zero_in, s);
   Launch L = plan_launch(g);
   PL_PRE(K_JACOBI);
   PL_DISPATCH_DIM(g, k_jacobi, L, s, u, b, out, g, c, sigma, omega, zero_in);
