@@ -155,7 +155,7 @@ __global__ void __launch_bounds__(NTHR) k_z2(const double* __restrict__ u,
                                              int zero_in) {
   constexpr int UX = TX + 4, UY = TY + 4, PU = UX * UY;     // input, halo 2
   constexpr int HX = TX + 2, HY = TY + 2, PH = HX * HY;     // stage 1 + b, halo 1
-  constexpr int RU = PREF + 2;    // u planes in flight / live (>= PREF + 1)
+  constexpr int RU = PREF + 3;    // u planes: the prologue stages z0-2 .. z0+PREF
   constexpr int RB_ = PREF + 1;   // b planes in flight / live (>= PREF)
   extern __shared__ double sm[];
   double* su = sm;                        // RU * PU
@@ -288,7 +288,7 @@ template <bool RB>
 int launch_z2(const double* u, const double* b, double* out, const Geo& g, const OpC& c,
               double sigma, double omega, double dval, int zero_in, cudaStream_t s) {
   constexpr int UX = TX + 4, UY = TY + 4, HX = TX + 2, HY = TY + 2;
-  size_t smem = sizeof(double) * ((PREF2 + 2) * UX * UY + (PREF2 + 1) * HX * HY + 3 * HX * HY);
+  size_t smem = sizeof(double) * ((PREF2 + 3) * UX * UY + (PREF2 + 1) * HX * HY + 3 * HX * HY);
   int zc = pick_zc(g);
   dim3 grid(ceil_div(g.nx, TX), ceil_div(g.ny, TY), ceil_div(g.nz, zc)), block(32, 8);
   auto kern = c.pow2 ? k_z2<RB, true, PREF2> : k_z2<RB, false, PREF2>;

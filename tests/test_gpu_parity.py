@@ -243,9 +243,8 @@ def test_pfasst_run_parity(name):
     assert got == [(r[0], r[1], r[2], r[3], r[5]) for r in m["trace"]]
     # residual histories: relative L-inf of the whole history <= 1e-10 (the
     # north-star criterion), and per entry 1e-10 relative plus an absolute
-    # floor of 1e-12 |u0|: a residual is a difference of O(|u|) terms whose
-    # rounding noise is ~ kappa * eps * |u| with kappa = dt |A_h| (1e3 - 1e4
-    # for these grids), not eps * |r|.
+    # floor of 4 kappa eps |u0|: a residual is a difference of O(|u|) terms
+    # whose rounding noise is ~ kappa * eps * |u| (kappa below), not eps * |r|.
     got_r = np.array([t.residual for t in res.trace])
     ref_r = np.array([r[4] for r in m["trace"]])
     diff = np.abs(got_r - ref_r)
@@ -255,7 +254,10 @@ def test_pfasst_run_parity(name):
     # summation order is CPU-kernel specific ("parity"); the 1-ulp
     # difference is amplified by dt*|A_h| ~ 8e3 per sweep, so 1-D cubic runs
     # are held to the conditioning floor below (counts and u stay exact/1e-10)
-    floor = 1e-12 * np.max(np.abs(a["u0"]))
+    # kappa = dt * |A_h|_inf (order 2: 4 d nu / dx^2), the per-sweep error
+    # amplification of the implicit sub-steps
+    kappa = m["dt"] * 4 * m["d"] * m["ns"][0] ** 2
+    floor = 4 * kappa * np.finfo(float).eps * np.max(np.abs(a["u0"]))
     bad = np.nonzero(diff > 1e-10 * np.abs(ref_r) + floor)[0]
     assert bad.size == 0, [(i, ref_r[i], diff[i]) for i in bad[:5]]
     close(res.u, a["u"], REL)
