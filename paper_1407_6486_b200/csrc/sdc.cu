@@ -5,10 +5,16 @@
 //
 // Each thread owns one grid point and walks the node axis, so every nodal
 // field is streamed exactly once per launch (coalesced 256 B per warp per
-// field) and the small M x M coefficient matrix sits in kernel parameter
-// (constant) space.  The contractions over nodes are sequential FMA chains
-// in column order, which is how the reference's BLAS evaluates
-// np.tensordot for these shapes (verified bit-for-bit by the oracle tests).
+// field).  The host compacts the small coefficient matrix to the columns
+// that carry a non-zero (column 0 of Q is structurally zero, so F[0] is never
+// read) and the kernels are instantiated per column count K, so every
+// coefficient index is a compile-time constant.  Contractions over nodes are
+// sequential FMA chains in column order -- how the reference's BLAS
+// evaluates np.tensordot for these shapes (verified bit-for-bit by the
+// oracle tests).  Zero entries inside a used column are FMA'd like BLAS does
+// (they can only change the sign of an exact zero).
+#include <cstring>
+
 #include "common.cuh"
 #include "kernels.cuh"
 
@@ -18,40 +24,104 @@ namespace {
 
 constexpr int MAXN = 17;
 
-struct AddMap {
-  int row[MAXN];  // field index of `add` for output row m
+struct NodeCoef {
+  int rows;            // R <= MAXN
+  int col[MAXN];       // source field index of compacted column k
+  int addrow[MAXN];    // field index of `add` for output row m
+  double a[MAXN * MAXN];   // R x K, row-major over compacted columns
 };
 
 // mode 0: out = scale*chain ; 1: out = scale*chain + add ; 2: out = add - scale*chain
+template <int K>
 __global__ void __launch_bounds__(256) k_chain(const double* __restrict__ in, long long in_stride,
                                                double* out, long long out_stride,
-                                               Coef c, double scale, long long npts,
+                                               NodeCoef c, double scale, long long npts,
                                                const double* add,   // may alias out
-                                               long long add_stride, AddMap am, int mode) {
+                                               long long add_stride, int mode) {
   long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= npts) return;
-  double v[MAXN];
+  double v[K];
 #pragma unroll
-  for (int k = 0; k < MAXN; ++k) {
-    if (k < c.cols) {
-      bool used = false;
-      for (int m = 0; m < c.rows; ++m) used |= c.a[m * c.cols + k] != 0.0;
-      v[k] = used ? in[k * in_stride + i] : 0.0;
+  for (int k = 0; k < K; ++k) v[k] = in[c.col[k] * in_stride + i];
+#pragma unroll
+  for (int m = 0; m < MAXN; ++m) {
+    if (m < c.rows) {
+      double acc = 0.0;
+#pragma unroll
+      for (int k = 0; k < K; ++k) acc = __fma_rn(c.a[m * K + k], v[k], acc);
+      double r = scale * acc;
+      if (mode == 1) r = r + add[c.addrow[m] * add_stride + i];
+      else if (mode == 2) r = add[c.addrow[m] * add_stride + i] - r;
+      out[m * out_stride + i] = r;
     }
   }
-  for (int m = 0; m < c.rows; ++m) {
-    double acc = 0.0;
+}
+
+// sdc.py:117-124, max-reduced as IEEE bit patterns (non-negative doubles
+// order like unsigned integers; NaN propagates like np.max).
+template <int K>
+__global__ void __launch_bounds__(256) k_resmax(const double* __restrict__ Y,
+                                                const double* __restrict__ F, long long stride,
+                                                const double* __restrict__ y0,
+                                                const double* __restrict__ tau, NodeCoef q,
+                                                double dt, long long npts,
+                                                unsigned long long* out) {
+  long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  unsigned long long best = 0ull;
+  if (i < npts) {
+    double f[K];
 #pragma unroll
-    for (int k = 0; k < MAXN; ++k) {
-      if (k < c.cols) {
-        double w = c.a[m * c.cols + k];
-        if (w != 0.0) acc = __fma_rn(w, v[k], acc);
+    for (int k = 0; k < K; ++k) f[k] = F[q.col[k] * stride + i];
+    const double base = y0[i];
+#pragma unroll
+    for (int m = 0; m < MAXN; ++m) {
+      if (m < q.rows) {
+        double acc = 0.0;
+#pragma unroll
+        for (int k = 0; k < K; ++k) acc = __fma_rn(q.a[m * K + k], f[k], acc);
+        double r = (base + dt * acc) - Y[m * stride + i];
+        if (tau) r = r + tau[m * stride + i];
+        unsigned long long bits = (unsigned long long)__double_as_longlong(fabs(r));
+        best = bits > best ? bits : best;
       }
     }
-    double r = scale * acc;
-    if (mode == 1) r = r + add[am.row[m] * add_stride + i];
-    else if (mode == 2) r = add[am.row[m] * add_stride + i] - r;
-    out[m * out_stride + i] = r;
+  }
+  for (int off = 16; off > 0; off >>= 1) {
+    unsigned long long o = __shfl_down_sync(0xffffffffu, best, off);
+    best = o > best ? o : best;
+  }
+  __shared__ unsigned long long sh[8];
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = best;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) best = sh[w] > best ? sh[w] : best;
+    if (best) atomicMax(out, best);
+  }
+}
+
+// hierarchy.py:116-118: d_j = new_j - old_j ; out[m] = chain_j P_t[m][j] d_j
+template <int K>
+__global__ void __launch_bounds__(256) k_delta_chain(const double* __restrict__ ynew,
+                                                     const double* __restrict__ yold,
+                                                     long long stride, NodeCoef pt,
+                                                     double* __restrict__ out,
+                                                     long long out_stride, long long npts) {
+  long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= npts) return;
+  double d[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    long long o = pt.col[k] * stride + i;
+    d[k] = ynew[o] - yold[o];
+  }
+#pragma unroll
+  for (int m = 0; m < MAXN; ++m) {
+    if (m < pt.rows) {
+      double acc = 0.0;
+#pragma unroll
+      for (int k = 0; k < K; ++k) acc = __fma_rn(pt.a[m * K + k], d[k], acc);
+      out[m * out_stride + i] = acc;
+    }
   }
 }
 
@@ -69,75 +139,6 @@ __global__ void __launch_bounds__(256) k_rhs(const double* __restrict__ y,
   rhs[i] = r;
 }
 
-// sdc.py:117-124, max-reduced as IEEE bit patterns (non-negative doubles
-// order like unsigned integers; NaN propagates like np.max).
-__global__ void __launch_bounds__(256) k_resmax(const double* __restrict__ Y,
-                                                const double* __restrict__ F, long long stride,
-                                                const double* __restrict__ y0,
-                                                const double* __restrict__ tau, Coef q,
-                                                double dt, long long npts,
-                                                unsigned long long* out) {
-  long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  unsigned long long best = 0ull;
-  if (i < npts) {
-    double f[MAXN];
-#pragma unroll
-    for (int k = 0; k < MAXN; ++k)
-      if (k < q.cols) f[k] = F[k * stride + i];
-    double base = y0[i];
-    for (int m = 0; m < q.rows; ++m) {
-      double acc = 0.0;
-#pragma unroll
-      for (int k = 0; k < MAXN; ++k) {
-        if (k < q.cols) {
-          double w = q.a[m * q.cols + k];
-          if (w != 0.0) acc = __fma_rn(w, f[k], acc);
-        }
-      }
-      double r = (base + dt * acc) - Y[m * stride + i];
-      if (tau) r = r + tau[m * stride + i];
-      unsigned long long bits = (unsigned long long)__double_as_longlong(fabs(r));
-      best = bits > best ? bits : best;
-    }
-  }
-  for (int off = 16; off > 0; off >>= 1) {
-    unsigned long long o = __shfl_down_sync(0xffffffffu, best, off);
-    best = o > best ? o : best;
-  }
-  __shared__ unsigned long long sh[8];
-  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = best;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) best = sh[w] > best ? sh[w] : best;
-    if (best) atomicMax(out, best);
-  }
-}
-
-// hierarchy.py:116-118: d_j = new_j - old_j ; out[m] = chain_j P_t[m][j] d_j
-__global__ void __launch_bounds__(256) k_delta_chain(const double* __restrict__ ynew,
-                                                     const double* __restrict__ yold,
-                                                     long long stride, Coef pt,
-                                                     double* __restrict__ out,
-                                                     long long out_stride, long long npts) {
-  long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= npts) return;
-  double d[MAXN];
-#pragma unroll
-  for (int j = 0; j < MAXN; ++j)
-    if (j < pt.cols) d[j] = ynew[j * stride + i] - yold[j * stride + i];
-  for (int m = 0; m < pt.rows; ++m) {
-    double acc = 0.0;
-#pragma unroll
-    for (int j = 0; j < MAXN; ++j) {
-      if (j < pt.cols) {
-        double w = pt.a[m * pt.cols + j];
-        if (w != 0.0) acc = __fma_rn(w, d[j], acc);
-      }
-    }
-    out[m * out_stride + i] = acc;
-  }
-}
-
 __global__ void __launch_bounds__(256) k_axpby(const double* __restrict__ a,
                                                const double* __restrict__ b,
                                                double* __restrict__ out, int sub,
@@ -147,31 +148,58 @@ __global__ void __launch_bounds__(256) k_axpby(const double* __restrict__ a,
   out[i] = sub ? a[i] - b[i] : a[i] + b[i];
 }
 
-}  // namespace
-
-static int used_cols(const Coef& a) {
-  int n = 0;
-  for (int k = 0; k < a.cols; ++k) {
-    bool u = false;
-    for (int m = 0; m < a.rows; ++m) u |= a.a[m * a.cols + k] != 0.0;
-    n += u;
+// compact a dense R x C matrix to its used columns; false if too large
+bool compact(const Coef& a, NodeCoef& c, int& K) {
+  if (a.rows > MAXN || a.cols > MAXN) {
+    set_error("coefficient matrix %dx%d exceeds %d", a.rows, a.cols, MAXN);
+    return false;
   }
-  return n;
+  std::memset(&c, 0, sizeof(c));
+  c.rows = a.rows;
+  K = 0;
+  for (int k = 0; k < a.cols; ++k) {
+    bool used = false;
+    for (int m = 0; m < a.rows; ++m) used |= a.a[m * a.cols + k] != 0.0;
+    if (used) c.col[K++] = k;
+  }
+  for (int m = 0; m < a.rows; ++m)
+    for (int k = 0; k < K; ++k) c.a[m * K + k] = a.a[m * a.cols + c.col[k]];
+  for (int m = 0; m < MAXN; ++m) c.addrow[m] = m;
+  if (K == 0) {            // all-zero matrix: one zero column keeps the chain exact
+    c.col[0] = 0;
+    K = 1;
+  }
+  return true;
 }
+
+#define PL_K_DISPATCH(K, CALL)                                                    \
+  switch (K) {                                                                    \
+    case 1: CALL(1); break; case 2: CALL(2); break; case 3: CALL(3); break;      \
+    case 4: CALL(4); break; case 5: CALL(5); break; case 6: CALL(6); break;      \
+    case 7: CALL(7); break; case 8: CALL(8); break; case 9: CALL(9); break;      \
+    case 10: CALL(10); break; case 11: CALL(11); break; case 12: CALL(12); break; \
+    case 13: CALL(13); break; case 14: CALL(14); break; case 15: CALL(15); break; \
+    case 16: CALL(16); break; default: CALL(17); break;                           \
+  }
+
+}  // namespace
 
 int launch_chain_ex(const double* in, long long in_stride, double* out, long long out_stride,
                     const Coef& a, double scale, long long npts, const double* add,
                     long long add_stride, const int* add_rows, int mode, cudaStream_t s) {
-  if (a.rows > MAXN || a.cols > MAXN) {
-    set_error("coefficient matrix %dx%d exceeds %d", a.rows, a.cols, MAXN);
-    return -1;
-  }
-  AddMap am;
-  for (int m = 0; m < MAXN; ++m) am.row[m] = (add_rows && m < a.rows) ? add_rows[m] : m;
+  NodeCoef c;
+  int K;
+  if (!compact(a, c, K)) return -1;
+  if (add_rows)
+    for (int m = 0; m < a.rows; ++m) c.addrow[m] = add_rows[m];
+  const int blocks = ceil_div(npts, 256);
   PL_PRE(K_QUAD);
-  k_chain<<<ceil_div(npts, 256), 256, 0, s>>>(in, in_stride, out, out_stride, a, scale, npts,
-                                              add, add_stride, am, mode);
-  PL_CHECK_LAUNCH(K_QUAD, 8.0 * npts * (used_cols(a) + a.rows + (mode ? a.rows : 0)));
+#define CALL(KK)                                                                          \
+  k_chain<KK><<<blocks, 256, 0, s>>>(in, in_stride, out, out_stride, c, scale, npts, add, \
+                                     add_stride, mode)
+  PL_K_DISPATCH(K, CALL);
+#undef CALL
+  PL_CHECK_LAUNCH(K_QUAD, 8.0 * npts * (K + a.rows + (mode ? a.rows : 0)));
   return 0;
 }
 
@@ -192,30 +220,34 @@ int launch_rhs(const double* y, const double* f, const double* sm, const double*
 int launch_resmax(const double* Y, const double* F, long long stride, const double* y0,
                   const double* tau, const Coef& q, double dt, long long npts,
                   double* out_dev, cudaStream_t s) {
-  if (q.rows > MAXN || q.cols > MAXN) {
-    set_error("quadrature matrix too large");
-    return -1;
-  }
+  NodeCoef c;
+  int K;
+  if (!compact(q, c, K)) return -1;
   cudaError_t e = cudaMemsetAsync(out_dev, 0, sizeof(double), s);
   if (e != cudaSuccess) return cuda_status(e, "memset");
+  const int blocks = ceil_div(npts, 256);
+  unsigned long long* o = (unsigned long long*)out_dev;
   PL_PRE(K_RESMAX);
-  k_resmax<<<ceil_div(npts, 256), 256, 0, s>>>(Y, F, stride, y0, tau, q, dt, npts,
-                                               (unsigned long long*)out_dev);
-  PL_CHECK_LAUNCH(K_RESMAX, 8.0 * npts * (used_cols(q) + q.rows + 1 + (tau ? q.rows : 0)));
+#define CALL(KK) k_resmax<KK><<<blocks, 256, 0, s>>>(Y, F, stride, y0, tau, c, dt, npts, o)
+  PL_K_DISPATCH(K, CALL);
+#undef CALL
+  PL_CHECK_LAUNCH(K_RESMAX, 8.0 * npts * (K + q.rows + 1 + (tau ? q.rows : 0)));
   return 0;
 }
 
 int launch_delta_chain(const double* ynew, const double* yold, long long stride,
                        const Coef& pt, double* out, long long out_stride, long long npts,
                        cudaStream_t s) {
-  if (pt.rows > MAXN || pt.cols > MAXN) {
-    set_error("interpolation matrix too large");
-    return -1;
-  }
+  NodeCoef c;
+  int K;
+  if (!compact(pt, c, K)) return -1;
+  const int blocks = ceil_div(npts, 256);
   PL_PRE(K_CORR);
-  k_delta_chain<<<ceil_div(npts, 256), 256, 0, s>>>(ynew, yold, stride, pt, out, out_stride,
-                                                    npts);
-  PL_CHECK_LAUNCH(K_CORR, 8.0 * npts * (2 * pt.cols + pt.rows));
+#define CALL(KK) \
+  k_delta_chain<KK><<<blocks, 256, 0, s>>>(ynew, yold, stride, c, out, out_stride, npts)
+  PL_K_DISPATCH(K, CALL);
+#undef CALL
+  PL_CHECK_LAUNCH(K_CORR, 8.0 * npts * (2 * K + pt.rows));
   return 0;
 }
 

@@ -39,20 +39,40 @@ __device__ __forceinline__ void cp_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
 }
 
-// stage a W x H window with origin (gx0, gy0) of plane gz; zero outside
+// A W x H plane window with origin (gx0, gy0).  Each thread copies the same
+// window elements for every plane, so their in-plane offsets (or "outside
+// the domain" = -1, zero-filled) are computed once; a plane then costs one
+// 64-bit add, one predicate and one cp.async per element.
 template <int W, int H>
-__device__ __forceinline__ void load_window(double* dst, const double* src, const Geo& g,
-                                            int gx0, int gy0, int gz, int tid) {
-  const bool zin = gz >= 0 && gz < g.nz;
-  for (int i = tid; i < W * H; i += NTHR) {
-    int yy = i / W;
-    int xx = i - yy * W;
-    int gx = gx0 + xx, gy = gy0 + yy;
-    bool ok = zin && gx >= 0 && gx < g.nx && gy >= 0 && gy < g.ny;
-    const double* p = ok ? src + (long long)gz * g.sz + (long long)gy * g.sy + gx : src;
-    cp_async8(dst + i, p, ok);
+struct Window {
+  static constexpr int N = W * H;
+  static constexpr int PER = (N + NTHR - 1) / NTHR;
+  int off[PER];
+
+  __device__ __forceinline__ void init(const Geo& g, int gx0, int gy0, int tid) {
+#pragma unroll
+    for (int q = 0; q < PER; ++q) {
+      int i = tid + q * NTHR;
+      int yy = i / W, xx = i - yy * W;
+      int gx = gx0 + xx, gy = gy0 + yy;
+      off[q] = (i < N && gx >= 0 && gx < g.nx && gy >= 0 && gy < g.ny)
+                   ? gy * (int)g.sy + gx : -1;
+    }
   }
-}
+  __device__ __forceinline__ void load(double* dst, const double* src, const Geo& g, int gz,
+                                       int tid) const {
+    const bool zin = gz >= 0 && gz < g.nz;
+    const double* plane = src + (long long)(zin ? gz : 0) * g.sz;
+#pragma unroll
+    for (int q = 0; q < PER; ++q) {
+      int i = tid + q * NTHR;
+      if (i < N) {
+        bool ok = zin && off[q] >= 0;
+        cp_async8(dst + i, ok ? plane + off[q] : src, ok);
+      }
+    }
+  }
+};
 
 template <bool POW2>
 __device__ __forceinline__ double dd2(double x, const OpC& c) {
@@ -91,11 +111,15 @@ __global__ void __launch_bounds__(NTHR) k_z1(const double* __restrict__ u,
   const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TY;
   const int z0 = blockIdx.z * zc, z1 = min(z0 + zc, g.nz);
 
+  Window<HX, HY> wu;
+  Window<TX, TY> wb;
+  if (NEED_U) wu.init(g, x0 - 1, y0 - 1, tid);
+  if (NEED_B) wb.init(g, x0, y0, tid);
   auto load = [&](int zz) {
     if (zz <= z1) {
       int slot = (zz - z0 + 1) % RING;
-      if (NEED_U) load_window<HX, HY>(su + slot * PU, u, g, x0 - 1, y0 - 1, zz, tid);
-      if (NEED_B && zz < z1) load_window<TX, TY>(sb + slot * PB, b, g, x0, y0, zz, tid);
+      if (NEED_U) wu.load(su + slot * PU, u, g, zz, tid);
+      if (NEED_B && zz < z1) wb.load(sb + slot * PB, b, g, zz, tid);
     }
     cp_commit();
   };
@@ -167,15 +191,31 @@ __global__ void __launch_bounds__(NTHR) k_z2(const double* __restrict__ u,
 
   // plane zz of u lives in slot (zz - z0 + 2) % RU (zz >= z0 - 2)
   // plane zz of b lives in slot (zz - z0 + 1) % RB_ (zz >= z0 - 1)
+  Window<UX, UY> wu;
+  Window<HX, HY> wb;
+  wu.init(g, x0 - 2, y0 - 2, tid);
+  wb.init(g, x0 - 1, y0 - 1, tid);
   auto load = [&](int zz) {            // u plane zz and b plane zz - 1
-    if (zz <= z1 + 1 && !zero_in)
-      load_window<UX, UY>(su + ((zz - z0 + 2) % RU) * PU, u, g, x0 - 2, y0 - 2, zz, tid);
+    if (zz <= z1 + 1 && !zero_in) wu.load(su + ((zz - z0 + 2) % RU) * PU, u, g, zz, tid);
     const int zb = zz - 1;
-    if (zb >= z0 - 1 && zb <= z1)
-      load_window<HX, HY>(sbb + ((zb - z0 + 1) % RB_) * PH, b, g, x0 - 1, y0 - 1, zb, tid);
+    if (zb >= z0 - 1 && zb <= z1) wb.load(sbb + ((zb - z0 + 1) % RB_) * PH, b, g, zb, tid);
     cp_commit();
   };
-  // stage 1 at plane zz over the halo-1 window (value 0 outside the domain)
+  // stage 1 at plane zz over the halo-1 window (value 0 outside the domain);
+  // each thread owns the same <= 3 window points on every plane
+  constexpr int PER1 = (PH + NTHR - 1) / NTHR;
+  int e_k[PER1], e_i[PER1], e_par[PER1];
+  bool e_in[PER1];
+#pragma unroll
+  for (int q = 0; q < PER1; ++q) {
+    int k = tid + q * NTHR;
+    int yy = k / HX, xx = k - yy * HX;
+    int gxx = x0 - 1 + xx, gyy = y0 - 1 + yy;
+    e_k[q] = k;
+    e_i[q] = (yy + 1) * UX + xx + 1;
+    e_in[q] = k < PH && gxx >= 0 && gxx < g.nx && gyy >= 0 && gyy < g.ny;
+    e_par[q] = (gxx + gyy + 3) & 1;
+  }
   auto stage1 = [&](int zz) {
     double* dst = s1 + ((zz - z0 + 3) % 3) * PH;
     const bool zin = zz >= 0 && zz < g.nz;
@@ -183,29 +223,31 @@ __global__ void __launch_bounds__(NTHR) k_z2(const double* __restrict__ u,
     const double* pc = su + ((zz - z0 + 2) % RU) * PU;
     const double* pp = su + ((zz + 1 - z0 + 2) % RU) * PU;
     const double* pb = sbb + ((zz - z0 + 1) % RB_) * PH;
-    for (int k = tid; k < PH; k += NTHR) {
-      int yy = k / HX, xx = k - yy * HX;
-      int gx = x0 - 1 + xx, gy = y0 - 1 + yy;
-      double v = 0.0;
-      if (zin && gx >= 0 && gx < g.nx && gy >= 0 && gy < g.ny) {
-        int i = (yy + 1) * UX + xx + 1;
-        double bb = pb[k];
-        if (RB) {
-          bool red = ((gx + gy + zz + 3) & 1) == 0;
-          if (red) {
-            double r = bb - (pc[i] - sigma * lap7<POW2, UX>(pm, pc, pp, i, c));
-            v = pc[i] + ((omega * r) / dval);
+#pragma unroll
+    for (int q = 0; q < PER1; ++q) {
+      const int k = e_k[q];
+      if (k < PH) {
+        double v = 0.0;
+        if (zin && e_in[q]) {
+          const int i = e_i[q];
+          double bb = pb[k];
+          if (RB) {
+            bool red = ((e_par[q] + zz) & 1) == 0;
+            if (red) {
+              double r = bb - (pc[i] - sigma * lap7<POW2, UX>(pm, pc, pp, i, c));
+              v = pc[i] + ((omega * r) / dval);
+            } else {
+              v = pc[i];
+            }
+          } else if (zero_in) {
+            v = 0.0 + ((omega * bb) / dval);
           } else {
-            v = pc[i];
+            double au = pc[i] - sigma * lap7<POW2, UX>(pm, pc, pp, i, c);
+            v = pc[i] + ((omega * (bb - au)) / dval);
           }
-        } else if (zero_in) {
-          v = 0.0 + ((omega * bb) / dval);
-        } else {
-          double au = pc[i] - sigma * lap7<POW2, UX>(pm, pc, pp, i, c);
-          v = pc[i] + ((omega * (bb - au)) / dval);
         }
+        dst[k] = v;
       }
-      dst[k] = v;
     }
   };
 
