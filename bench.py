@@ -127,10 +127,11 @@ def alg_bytes_of_one_substep(w):
     from paper_1407_6486_b200 import _capi
     from paper_1407_6486_b200.heat import Grid, HeatOperator, seeded_field
     from paper_1407_6486_b200.multigrid import MgConfig, ShiftedOperator, vcycles_into
+    from paper_1407_6486_b200._device import clone_field, to_device
     g = Grid(w["dim"], w["ns"][0])
     op = HeatOperator(g)
-    u = torch.from_numpy(seeded_field(g)).cuda()
-    b = u.clone()
+    u = to_device(seeded_field(g))[0]
+    b = clone_field(u)
     cfg = MgConfig(w["smoother"], w["omega"], w["pre"], w["post"])
     sop = ShiftedOperator(op, w["dt"] / (w["nodes"][0] - 1))
     vcycles_into(sop, u, b, cfg, w["cycles"])        # warm (plans, LU)
@@ -157,8 +158,9 @@ def run_ours(args, w):
     executor = "nccl" if world > 1 else "serial"
     levels = build_levels(w)
     p, dt = w["p"], w["dt"]
+    from paper_1407_6486_b200._device import to_device
     u0_host = seeded_field(Grid(w["dim"], w["ns"][0]))
-    u0_dev = torch.from_numpy(u0_host).cuda()
+    u0_dev = to_device(u0_host)[0]            # device field in the library layout
     u0_pinned = torch.from_numpy(u0_host).pin_memory()
 
     def step(u0):
@@ -274,9 +276,10 @@ def vcycle_rate(w, reps=10):
     from paper_1407_6486_b200 import _capi
     from paper_1407_6486_b200.heat import Grid, HeatOperator, seeded_field
     from paper_1407_6486_b200.multigrid import MgConfig, ShiftedOperator, vcycles_into
+    from paper_1407_6486_b200._device import clone_field, to_device
     g = Grid(w["dim"], w["ns"][0])
-    u = torch.from_numpy(seeded_field(g)).cuda()
-    b = u.clone()
+    u = to_device(seeded_field(g))[0]
+    b = clone_field(u)
     cfg = MgConfig(w["smoother"], w["omega"], w["pre"], w["post"])
     sop = ShiftedOperator(HeatOperator(g), w["dt"] / (w["nodes"][0] - 1))
     for _ in range(3):

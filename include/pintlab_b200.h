@@ -11,7 +11,11 @@
  * Conventions
  *  - All arrays are fp64, C order, interior points only, x fastest
  *    (heat.py:1-6): a grid with n cells per axis holds (n-1)^dim values.
- *    Nodal arrays (M+1 fields) are contiguous with stride (n-1)^dim.
+ *    Device layout: for dim >= 2 each x-row of n-1 values is stored with a
+ *    pitch of n doubles (one zero pad per row, 16-byte aligned rows for TMA);
+ *    1-D fields are one unpadded row.  pl_field_elems(dim, n) is the storage
+ *    size of one field; nodal arrays (M+1 fields) are contiguous with that
+ *    stride.  Pads must hold zeros.
  *  - Device buffers are allocated and owned by the caller; the library owns
  *    only plans (level descriptors, coarsest-grid LU factors, norm scratch).
  *  - Every call is asynchronous on `stream` (a cudaStream_t, NULL = legacy
@@ -62,6 +66,9 @@ const char* pl_last_error(void);
 /* runtime options (A/B testing of kernel variants; results are bit-identical) */
 #define PL_OPT_ZMARCH 0 /* 1 (default): cp.async z-marching + fused sweeps for 3-D order 2 */
 int pl_set_option(int key, int value);
+
+/* storage elements of one field (incl. row pads) */
+long long pl_field_elems(int dim, int n);
 
 /* ---- heat operator (heat.py) ------------------------------------------- */
 /* f = nu * Lap_h u, order 2 or 4 (HeatOperator.apply, heat.py:111-142) */
@@ -144,7 +151,7 @@ int pl_sdc_sweep(pl_mg_plan* plan, const pl_sweep_desc* desc, double* Y, double*
 /* residual(states, y0, dt, tau) (sdc.py:117-124): max-norm into out_dev
    (device double, asynchronous).  q is (M+1)x(M+1) row-major (host). */
 int pl_sdc_residual(const double* Y, const double* F, const double* y0, const double* tau,
-                    const double* q, int m, double dt, long long npts, double* out_dev,
+                    const double* q, int m, double dt, int dim, int n, double* out_dev,
                     void* stream);
 
 /* ---- FAS machinery (hierarchy.py) ---------------------------------------- */

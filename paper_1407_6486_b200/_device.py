@@ -1,4 +1,13 @@
-"""Device plumbing: fp64 CUDA tensors, the current stream, scratch caches.
+"""Device plumbing: fp64 CUDA fields in the library's layout, the current
+stream, scratch caches.
+
+Device layout (include/pintlab_b200.h): a grid field of shape (N,)*d with
+N = n-1 is stored with an x-row pitch of n doubles for d >= 2 (one zero pad
+per row, 16-byte aligned rows for TMA); 1-D fields are unpadded.  Public
+objects expose *strided views* of the logical shape, so ``states.y[m][i, j]``
+indexes exactly like the reference's numpy arrays.  Nodal arrays (M+1 fields)
+are one allocation with a field stride of the padded field size.  All
+storage is zero-initialised and every kernel maps pad zeros to zeros.
 
 PyTorch is used only for allocation, streams and host<->device copies; every
 computation on the path is a kernel of lib/libpintlab_b200.so.
@@ -22,28 +31,105 @@ def stream_ptr():
     return torch.cuda.current_stream().cuda_stream
 
 
-def to_device(x):
-    """(tensor, was_host): fp64 contiguous CUDA tensor for x (numpy / torch)."""
+def _layout(grid_shape):
+    """(field strides, storage elements) of one grid field."""
+    d = len(grid_shape)
+    N = grid_shape[-1]
+    pitch = N + 1 if d >= 2 else N
+    if d == 1:
+        return (1,), N
+    if d == 2:
+        return (pitch, 1), N * pitch
+    return (N * pitch, pitch, 1), N * N * pitch
+
+
+def field_elems(grid_shape):
+    return _layout(tuple(grid_shape))[1]
+
+
+def new_field(grid_shape, lead=()):
+    """Zeroed device field(s) in the library layout; returns the strided view
+    of logical shape lead + grid_shape."""
+    grid_shape = tuple(grid_shape)
+    lead = tuple(lead)
+    strides, ns = _layout(grid_shape)
+    count = int(np.prod(lead)) if lead else 1
+    store = torch.zeros(count * ns, dtype=torch.float64, device=device())
+    lead_strides = []
+    acc = ns
+    for dim in reversed(lead):
+        lead_strides.insert(0, acc)
+        acc *= dim
+    return torch.as_strided(store, lead + grid_shape, tuple(lead_strides) + strides)
+
+
+def is_field(t, grid_dim):
+    """True when t is an fp64 CUDA view in the library layout."""
+    if not (isinstance(t, torch.Tensor) and t.is_cuda and t.dtype == torch.float64):
+        return False
+    shape = tuple(t.shape)
+    if len(shape) < grid_dim:
+        return False
+    gshape = shape[len(shape) - grid_dim:]
+    if len(set(gshape)) != 1:
+        return False
+    strides, ns = _layout(gshape)
+    want = list(strides)
+    acc = ns
+    for dim in reversed(shape[:len(shape) - grid_dim]):
+        want.insert(0, acc)
+        acc *= dim
+    got = list(t.stride())
+    return all(g == w or s == 1 for g, w, s in zip(got, want, shape))
+
+
+def to_device(x, grid_dim=None):
+    """(field, was_host): x as a device field in the library layout (copied
+    unless it already is one).  grid_dim defaults to x.ndim."""
+    if grid_dim is None:
+        grid_dim = np.ndim(x) if not isinstance(x, torch.Tensor) else x.dim()
+    if is_field(x, grid_dim):
+        return x, False
+    host = not (isinstance(x, torch.Tensor) and x.is_cuda)
     if isinstance(x, torch.Tensor):
-        if x.is_cuda and x.dtype == torch.float64 and x.is_contiguous():
-            return x, False
-        host = not x.is_cuda
-        return x.to(device=device(), dtype=torch.float64).contiguous(), host
-    arr = np.ascontiguousarray(np.asarray(x, dtype=np.float64))
-    return torch.from_numpy(arr).to(device()), True
+        src = x.detach().to(dtype=torch.float64)
+    else:
+        src = torch.from_numpy(np.ascontiguousarray(np.asarray(x, dtype=np.float64)))
+    shape = tuple(src.shape)
+    out = new_field(shape[len(shape) - grid_dim:], shape[:len(shape) - grid_dim])
+    out.copy_(src, non_blocking=src.is_pinned() if not src.is_cuda else False)
+    return out, host
+
+
+def clone_field(t, grid_dim=None):
+    """Copy of a device field, in the library layout."""
+    if grid_dim is None:
+        grid_dim = t.dim()
+    shape = tuple(t.shape)
+    out = new_field(shape[len(shape) - grid_dim:], shape[:len(shape) - grid_dim])
+    out.copy_(t)
+    return out
+
+
+def flat_storage(t):
+    """Contiguous 1-D view of one field's storage (pads included): the wire
+    format of the time-rank hand-offs."""
+    return torch.as_strided(t, (field_elems(tuple(t.shape)),), (1,), t.storage_offset())
+
+
+def field_from_flat(flat, grid_shape):
+    """Field view over a flat storage buffer (inverse of flat_storage)."""
+    strides, ns = _layout(tuple(grid_shape))
+    return torch.as_strided(flat, tuple(grid_shape), strides, flat.storage_offset())
 
 
 def like_input(t, was_host):
-    """Return t as numpy when the caller passed host data (drop-in behaviour)."""
-    return t.cpu().numpy() if was_host else t
+    """Return t as a dense numpy array when the caller passed host data."""
+    return t.contiguous().cpu().numpy() if was_host else t
 
 
 def ptr(t):
     return None if t is None else t.data_ptr()
-
-
-def empty(shape):
-    return torch.empty(shape, dtype=torch.float64, device=device())
 
 
 def zeros(shape):
@@ -51,11 +137,12 @@ def zeros(shape):
 
 
 def scratch(tag, nbytes):
-    """Stream-ordered scratch buffer reused across calls (keyed per stream)."""
+    """Zeroed, stream-ordered scratch buffer reused across calls (per stream);
+    zero pads stay zero because every kernel maps zeros to zeros."""
     key = (tag, stream_ptr(), torch.cuda.current_device())
     buf = _scratch.get(key)
     if buf is None or buf.numel() < nbytes:
-        buf = torch.empty(max(int(nbytes), 8), dtype=torch.uint8, device=device())
+        buf = torch.zeros(max(int(nbytes), 8), dtype=torch.uint8, device=device())
         _scratch[key] = buf
     return buf
 

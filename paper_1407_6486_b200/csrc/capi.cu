@@ -99,7 +99,7 @@ static int sdc_sweep(MgPlan* P, const pl_sweep_desc* d, double* Y, double* F, co
                      const double* tau, double dt, double* ws, size_t ws_bytes, int* cycles,
                      int* failed, double* fres, int* fcyc, cudaStream_t s) {
   const MgLevel& L = P->lv[0];
-  const long long np = L.g.npts;
+  const long long np = L.g.nstore;     // field stride / point-wise extent
   const int M = d->m;
   if (M < 1 || M + 1 > PL_MAX_NODES) {
     set_error("sweep needs 1 <= M <= %d", PL_MAX_NODES - 1);
@@ -124,7 +124,7 @@ static int sdc_sweep(MgPlan* P, const pl_sweep_desc* d, double* Y, double* F, co
   if (Y != y0) {
     cudaError_t e = cudaMemcpyAsync(Y, y0, sizeof(double) * np, cudaMemcpyDeviceToDevice, s);
     if (e != cudaSuccess) return cuda_status(e, "y0 copy");
-    count_launch(K_COPY, 16.0 * np);
+    count_launch(K_COPY, 16.0 * L.g.npts);
   }
   PL_TRY(launch_apply(Y, F, L.g, L.c, s));
   int total = 0;
@@ -163,7 +163,7 @@ static int sdc_sweep(MgPlan* P, const pl_sweep_desc* d, double* Y, double* F, co
 static int restrict_field(const double* f, double* c, const Geo& gf, int kind, cudaStream_t s) {
   if (kind == PL_RESTRICT_FULL_WEIGHTING) return launch_fw(f, c, gf, s);
   if (kind == PL_RESTRICT_INJECT) return launch_inject(f, c, gf, s);
-  cudaError_t e = cudaMemcpyAsync(c, f, sizeof(double) * gf.npts, cudaMemcpyDeviceToDevice, s);
+  cudaError_t e = cudaMemcpyAsync(c, f, sizeof(double) * gf.nstore, cudaMemcpyDeviceToDevice, s);
   if (e != cudaSuccess) return cuda_status(e, "copy");
   count_launch(K_COPY, 16.0 * gf.npts);
   return 0;
@@ -184,12 +184,11 @@ static bool check_grid(int dim, int n) {
 namespace {
 template <int DIM>
 __global__ void k_diag(double* out, Geo g, OpC c, double sigma, int shifted) {
-  long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (p >= g.npts) return;
-  int x = (int)(p % g.nx);
-  long long r = p / g.nx;
-  int y = (int)(r % g.ny);
-  int z = (int)(r / g.ny);
+  long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= g.npts) return;
+  int x, y, z;
+  decode_point(g, t, x, y, z);
+  const long long p = g.at(x, y, z);
   if (shifted) {
     out[p] = shifted_diag<DIM>(g, c, sigma, x, y, z);
   } else {
@@ -203,12 +202,11 @@ __global__ void k_diag(double* out, Geo g, OpC c, double sigma, int shifted) {
 template <int DIM>
 __global__ void k_shifted_apply(const double* __restrict__ u, double* __restrict__ out, Geo g,
                                 OpC c, double sigma) {
-  long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (p >= g.npts) return;
-  int x = (int)(p % g.nx);
-  long long r = p / g.nx;
-  int y = (int)(r % g.ny);
-  int z = (int)(r / g.ny);
+  long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= g.npts) return;
+  int x, y, z;
+  decode_point(g, t, x, y, z);
+  const long long p = g.at(x, y, z);
   out[p] = shifted_point<DIM>(u, g, c, sigma, x, y, z, p);
 }
 }  // namespace
@@ -351,9 +349,14 @@ int pl_mg_solve_tol(pl_mg_plan* plan, double* u, const double* b, double sigma, 
                       residual, (cudaStream_t)stream);
 }
 
+long long pl_field_elems(int dim, int n) {
+  if (!check_grid(dim, n)) return 0;
+  return make_geo(dim, n).nstore;
+}
+
 size_t pl_sweep_workspace_bytes(int dim, int n, int m) {
   if (!check_grid(dim, n)) return 0;
-  return sizeof(double) * (size_t)make_geo(dim, n).npts * (m + 1);
+  return sizeof(double) * (size_t)make_geo(dim, n).nstore * (m + 1);
 }
 
 int pl_sdc_sweep(pl_mg_plan* plan, const pl_sweep_desc* desc, double* Y, double* F,
@@ -366,11 +369,12 @@ int pl_sdc_sweep(pl_mg_plan* plan, const pl_sweep_desc* desc, double* Y, double*
 }
 
 int pl_sdc_residual(const double* Y, const double* F, const double* y0, const double* tau,
-                    const double* q, int m, double dt, long long npts, double* out_dev,
+                    const double* q, int m, double dt, int dim, int n, double* out_dev,
                     void* stream) {
-  if (m < 1 || m + 1 > PL_MAX_NODES) return PL_ERR_ARG;
+  if (m < 1 || m + 1 > PL_MAX_NODES || !check_grid(dim, n)) return PL_ERR_ARG;
   Coef c = coef_from(q, m + 1, m + 1);
-  return launch_resmax(Y, F, npts, y0, tau, c, dt, npts, out_dev, (cudaStream_t)stream);
+  const long long ns = make_geo(dim, n).nstore;
+  return launch_resmax(Y, F, ns, y0, tau, c, dt, ns, out_dev, (cudaStream_t)stream);
 }
 
 int pl_restrict_state(const double* fineY, const int* idx, int nsel, double* coarseY,
@@ -386,16 +390,16 @@ int pl_restrict_state(const double* fineY, const int* idx, int nsel, double* coa
   Geo gf = make_geo(dim, nf), gc = make_geo(dim, nc);
   OpC cc = make_opc(nc, length, nu_c, order_c);
   for (int j = 0; j < nsel; ++j) {
-    double* cy = coarseY + (size_t)j * gc.npts;
-    PL_TRY(restrict_field(fineY + (size_t)idx[j] * gf.npts, cy, gf, restrict_kind, s));
-    PL_TRY(launch_apply(cy, coarseF + (size_t)j * gc.npts, gc, cc, s));
+    double* cy = coarseY + (size_t)j * gc.nstore;
+    PL_TRY(restrict_field(fineY + (size_t)idx[j] * gf.nstore, cy, gf, restrict_kind, s));
+    PL_TRY(launch_apply(cy, coarseF + (size_t)j * gc.nstore, gc, cc, s));
   }
   return 0;
 }
 
 size_t pl_compute_fas_scratch_bytes(int dim, int nf, int nsel) {
   if (!check_grid(dim, nf)) return 0;
-  return sizeof(double) * (size_t)make_geo(dim, nf).npts * nsel;
+  return sizeof(double) * (size_t)make_geo(dim, nf).nstore * nsel;
 }
 
 int pl_compute_fas(const double* fineF, const double* fine_tau, int mf, const double* qf_rows,
@@ -409,21 +413,21 @@ int pl_compute_fas(const double* fineF, const double* fine_tau, int mf, const do
   Geo gf = make_geo(dim, nf), gc = make_geo(dim, nc);
   // fine integrals at the selected nodes: dt * (Q_f F_f)[idx] (+ tau_f[idx])
   Coef qf = coef_from(qf_rows, nsel, mf + 1);
-  PL_TRY(launch_chain_ex(fineF, gf.npts, scratch, gf.npts, qf, dt, gf.npts, fine_tau, gf.npts,
-                         idx, fine_tau ? 1 : 0, s));
+  PL_TRY(launch_chain_ex(fineF, gf.nstore, scratch, gf.nstore, qf, dt, gf.nstore, fine_tau,
+                         gf.nstore, idx, fine_tau ? 1 : 0, s));
   // restrict each into tau_c (temporarily), then tau_c = R - dt (Q_c F_c)
   for (int j = 0; j < nsel; ++j)
-    PL_TRY(restrict_field(scratch + (size_t)j * gf.npts, tau_c + (size_t)j * gc.npts, gf,
+    PL_TRY(restrict_field(scratch + (size_t)j * gf.nstore, tau_c + (size_t)j * gc.nstore, gf,
                           restrict_kind, s));
   Coef q = coef_from(qc, mc + 1, mc + 1);
-  PL_TRY(launch_chain_ex(coarseF, gc.npts, tau_c, gc.npts, q, dt, gc.npts, tau_c, gc.npts,
-                         nullptr, 2, s));
+  PL_TRY(launch_chain_ex(coarseF, gc.nstore, tau_c, gc.nstore, q, dt, gc.nstore, tau_c,
+                         gc.nstore, nullptr, 2, s));
   return 0;
 }
 
 size_t pl_coarse_correction_scratch_bytes(int dim, int nf, int nc, int mf, int interp_order) {
   if (!check_grid(dim, nf) || !check_grid(dim, nc)) return 0;
-  size_t n = (size_t)make_geo(dim, nc).npts * (mf + 1);
+  size_t n = (size_t)make_geo(dim, nc).nstore * (mf + 1);
   if (nc != nf && interp_order == 4) n += cubic_scratch_doubles(make_geo(dim, nf));
   return sizeof(double) * n;
 }
@@ -439,19 +443,20 @@ int pl_coarse_correction(double* fineY, double* fineF, int mf, const double* coa
   OpC cf = make_opc(nf, length, nu_f, order_f);
   Coef p = coef_from(pt, mf + 1, mc + 1);
   double* dt_fields = scratch;   // (Mf+1) coarse fields
-  PL_TRY(launch_delta_chain(coarse_new, coarse_old, gc.npts, p, dt_fields, gc.npts, gc.npts, s));
-  double* cub = scratch + (size_t)gc.npts * (mf + 1);
+  PL_TRY(launch_delta_chain(coarse_new, coarse_old, gc.nstore, p, dt_fields, gc.nstore, gc.nstore,
+                            s));
+  double* cub = scratch + (size_t)gc.nstore * (mf + 1);
   for (int m = 0; m <= mf; ++m) {
-    double* y = fineY + (size_t)m * gf.npts;
-    const double* d = dt_fields + (size_t)m * gc.npts;
+    double* y = fineY + (size_t)m * gf.nstore;
+    const double* d = dt_fields + (size_t)m * gc.nstore;
     if (nc == nf) {
-      PL_TRY(launch_axpby(y, d, y, 0, gf.npts, s));
+      PL_TRY(launch_axpby(y, d, y, 0, gf.nstore, s));
     } else if (interp_order == 2) {
       PL_TRY(launch_prolong(d, y, gf, 1, s));
     } else {
       PL_TRY(launch_cubic(d, y, gf, 1, cub, s));
     }
-    PL_TRY(launch_apply(y, fineF + (size_t)m * gf.npts, gf, cf, s));
+    PL_TRY(launch_apply(y, fineF + (size_t)m * gf.nstore, gf, cf, s));
   }
   return 0;
 }

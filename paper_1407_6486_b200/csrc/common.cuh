@@ -50,27 +50,50 @@ enum KernelKind {
 };
 
 // ---------------------------------------------------------------------------
-// geometry: interior-only Dirichlet grid, C order, x fastest (heat.py:1-6)
+// geometry: interior-only Dirichlet grid, C order, x fastest (heat.py:1-6).
+//
+// Device layout: for dim >= 2 every row of N = n-1 interior values is stored
+// with a pitch of n doubles (one zero pad per row), so rows start 16-byte
+// aligned and TMA tensor maps (strides must be multiples of 16 B) can address
+// the field; the pad is outside the tensor map's extent and is never read as
+// data.  1-D fields are a single unpadded row.  Pads hold zeros: buffers are
+// zero-initialised and every point-wise kernel maps zeros to zeros.
 
 struct Geo {
   int dim;        // 1, 2, 3
   int N;          // interior points per axis = n - 1
   int nx, ny, nz; // nz = ny = 1 for lower dims
-  long long sy, sz;
-  long long npts;
+  long long sy, sz;   // storage strides in elements
+  long long npts;     // logical points (n-1)^dim
+  long long nstore;   // storage elements per field (incl. pads)
+  __host__ __device__ long long at(int x, int y, int z) const { return z * sz + y * sy + x; }
 };
 
-inline Geo make_geo(int dim, int n) {
+inline Geo make_geo_pitch(int dim, int n, int pitch) {
   Geo g;
   g.dim = dim;
   g.N = n - 1;
   g.nx = g.N;
   g.ny = dim >= 2 ? g.N : 1;
   g.nz = dim >= 3 ? g.N : 1;
-  g.sy = g.nx;
-  g.sz = (long long)g.nx * g.ny;
-  g.npts = g.sz * g.nz;
+  g.sy = pitch;
+  g.sz = (long long)pitch * g.ny;
+  g.npts = (long long)g.nx * g.ny * g.nz;
+  g.nstore = g.sz * g.nz;
   return g;
+}
+
+// the device (storage) layout of a grid with n cells per axis
+inline Geo make_geo(int dim, int n) { return make_geo_pitch(dim, n, dim >= 2 ? n : n - 1); }
+// dense layout (shared-memory tiles, scratch)
+inline Geo make_geo_compact(int dim, int n) { return make_geo_pitch(dim, n, n - 1); }
+
+// logical linear index -> (x, y, z)
+__host__ __device__ inline void decode_point(const Geo& g, long long t, int& x, int& y, int& z) {
+  x = (int)(t % g.nx);
+  long long r = t / g.nx;
+  y = (int)(r % g.ny);
+  z = (int)(r / g.ny);
 }
 
 // Operator constants, all computed on the host with the reference's own

@@ -57,6 +57,7 @@ struct TailLevel {
 };
 
 struct TailArgs {
+  Geo g0;             // global (storage) geometry of the first tail level
   int nlev;
   TailLevel lv[MAX_LEVELS];
   int smoother, pre, post;
@@ -184,8 +185,11 @@ __global__ void __launch_bounds__(TAIL_THREADS) k_tail(TailArgs a,
   extern __shared__ double sm[];
   const TailLevel& L0 = a.lv[0];
   PL_FOR_SM_POINTS(L0.g) {
-    sm[L0.off_b + p] = b_in[p];
-    if (!zero_guess) sm[L0.off_u + p] = u_io[p];
+    int x, y, z;
+    decode(L0.g, p, x, y, z);
+    const long long gi = a.g0.at(x, y, z);
+    sm[L0.off_b + p] = b_in[gi];
+    if (!zero_guess) sm[L0.off_u + p] = u_io[gi];
   }
   __syncthreads();
   for (int cyc = 0; cyc < ncycles; ++cyc) {
@@ -230,7 +234,11 @@ __global__ void __launch_bounds__(TAIL_THREADS) k_tail(TailArgs a,
       tail_smooth<DIM>(a, L, sm, a.post, false);
     }
   }
-  PL_FOR_SM_POINTS(L0.g) u_io[p] = sm[L0.off_u + p];
+  PL_FOR_SM_POINTS(L0.g) {
+    int x, y, z;
+    decode(L0.g, p, x, y, z);
+    u_io[a.g0.at(x, y, z)] = sm[L0.off_u + p];
+  }
 }
 
 }  // namespace
@@ -253,10 +261,11 @@ static int launch_tail(MgPlan* P, int l0, double* u, const double* b, double sig
   a.lu = it->second.dev;
   int off = 0;
   a.nlev = (int)P->lv.size() - l0;
+  a.g0 = P->lv[l0].g;
   for (int i = 0; i < a.nlev; ++i) {
     const MgLevel& L = P->lv[l0 + i];
     TailLevel& T = a.lv[i];
-    T.g = L.g;
+    T.g = make_geo_compact(P->dim, L.n);     // shared memory is dense
     T.c = L.c;
     T.coarsest = L.coarsest;
     int np = (int)L.g.npts;
@@ -299,7 +308,7 @@ size_t mg_workspace_bytes(int dim, int n, int coarsest_n) {
   size_t total = 0;
   for (size_t l = 0; l < ns.size(); ++l) {
     Geo g = make_geo(dim, ns[l]);
-    size_t per = (l == 0 ? 1 : 3) * (size_t)g.npts;   // fine: t only; coarse: u, b, t
+    size_t per = (l == 0 ? 1 : 3) * (size_t)g.nstore;   // fine: t only; coarse: u, b, t
     total += ((per * 8 + 255) / 256) * 256;
   }
   return total;
@@ -342,14 +351,14 @@ int mg_plan_create(MgPlan** out, int dim, int n, double length, double nu, int o
     L.g = make_geo(dim, ns[l]);
     L.c = make_opc(ns[l], length, nu, order);
     L.coarsest = ns[l] <= coarsest_n || ns[l] < 4;
-    size_t per = (l == 0 ? 1 : 3) * (size_t)L.g.npts;
+    size_t per = (l == 0 ? 1 : 3) * (size_t)L.g.nstore;
     double* base = (double*)cur;
     if (l == 0) {
       L.t = base;
     } else {
       L.u = base;
-      L.b = base + L.g.npts;
-      L.t = base + 2 * L.g.npts;
+      L.b = base + L.g.nstore;
+      L.t = base + 2 * L.g.nstore;
     }
     cur += ((per * 8 + 255) / 256) * 256;
     P->lv.push_back(L);
@@ -535,7 +544,7 @@ static int level_smooth(MgPlan* P, MgLevel& L, double** cur, double* alt_u, cons
   double* other = (u == alt_u) ? L.t : alt_u;
   if (count == 0) {
     if (zero) {
-      cudaError_t e = cudaMemsetAsync(u, 0, sizeof(double) * L.g.npts, s);
+      cudaError_t e = cudaMemsetAsync(u, 0, sizeof(double) * L.g.nstore, s);
       if (e != cudaSuccess) return cuda_status(e, "memset");
     }
     return 0;
@@ -557,7 +566,7 @@ static int level_smooth(MgPlan* P, MgLevel& L, double** cur, double* alt_u, cons
     return 0;
   }
   if (zero) {
-    cudaError_t e = cudaMemsetAsync(u, 0, sizeof(double) * L.g.npts, s);
+    cudaError_t e = cudaMemsetAsync(u, 0, sizeof(double) * L.g.nstore, s);
     if (e != cudaSuccess) return cuda_status(e, "memset");
   }
   for (int k = 0; k < count; ++k) {
@@ -590,7 +599,7 @@ static int vcycle(MgPlan* P, int l, double* u, const double* b, double sigma, bo
   PL_TRY(launch_prolong(C.u, cur, L.g, 1, s));
   PL_TRY(level_smooth(P, L, &cur, u, b, sigma, P->post, false, s));
   if (cur != u) {
-    cudaError_t e = cudaMemcpyAsync(u, cur, sizeof(double) * L.g.npts,
+    cudaError_t e = cudaMemcpyAsync(u, cur, sizeof(double) * L.g.nstore,
                                     cudaMemcpyDeviceToDevice, s);
     if (e != cudaSuccess) return cuda_status(e, "copy");
     count_launch(K_COPY, 16.0 * L.g.npts);
@@ -612,7 +621,7 @@ int mg_smooth(MgPlan* P, double* u, const double* b, double sigma, int count, cu
   double* cur = u;
   PL_TRY(level_smooth(P, L, &cur, u, b, sigma, count, false, s));
   if (cur != u) {
-    cudaError_t e = cudaMemcpyAsync(u, cur, sizeof(double) * L.g.npts,
+    cudaError_t e = cudaMemcpyAsync(u, cur, sizeof(double) * L.g.nstore,
                                     cudaMemcpyDeviceToDevice, s);
     if (e != cudaSuccess) return cuda_status(e, "copy");
   }
@@ -640,7 +649,7 @@ int mg_solve_tol(MgPlan* P, double* u, const double* b, double sigma, double tol
   PL_TRY(norm2(P, nullptr, b, sigma, &bnorm, s));
   *cycles = 0;
   if (bnorm == 0.0) {
-    cudaError_t e = cudaMemsetAsync(u, 0, sizeof(double) * L.g.npts, s);
+    cudaError_t e = cudaMemsetAsync(u, 0, sizeof(double) * L.g.nstore, s);
     if (e != cudaSuccess) return cuda_status(e, "memset");
     *status = ST_CONVERGED;
     *residual = 0.0;

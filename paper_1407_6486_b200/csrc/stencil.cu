@@ -108,14 +108,13 @@ __global__ void __launch_bounds__(NORM_THREADS) k_sumsq(const double* __restrict
                                                         double* __restrict__ partials) {
   double acc = 0.0;
   const long long stride = (long long)gridDim.x * blockDim.x;
-  for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < g.npts;
-       idx += stride) {
+  for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < g.npts;
+       t += stride) {
+    int x, y, z;
+    decode_point(g, t, x, y, z);
+    const long long idx = g.at(x, y, z);
     double v;
     if (u) {
-      int x = (int)(idx % g.nx);
-      long long t = idx / g.nx;
-      int y = (int)(t % g.ny);
-      int z = (int)(t / g.ny);
       v = b[idx] - shifted_point<DIM>(u, g, c, sigma, x, y, z, idx);
     } else {
       v = b[idx];

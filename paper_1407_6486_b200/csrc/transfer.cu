@@ -21,11 +21,9 @@ __global__ void __launch_bounds__(256) k_fw(const double* __restrict__ f,
                                             double* __restrict__ cz, Geo gf, Geo gc) {
   long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= gc.npts) return;
-  int jx = (int)(t % gc.nx);
-  long long r = t / gc.nx;
-  int jy = (int)(r % gc.ny);
-  int jz = (int)(r / gc.ny);
-  cz[t] = fw_point<DIM>(f, gf, jx, jy, jz);
+  int jx, jy, jz;
+  decode_point(gc, t, jx, jy, jz);
+  cz[gc.at(jx, jy, jz)] = fw_point<DIM>(f, gf, jx, jy, jz);
 }
 
 template <int DIM>
@@ -33,14 +31,12 @@ __global__ void __launch_bounds__(256) k_inject(const double* __restrict__ f,
                                                 double* __restrict__ cz, Geo gf, Geo gc) {
   long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= gc.npts) return;
-  int jx = (int)(t % gc.nx);
-  long long r = t / gc.nx;
-  int jy = (int)(r % gc.ny);
-  int jz = (int)(r / gc.ny);
+  int jx, jy, jz;
+  decode_point(gc, t, jx, jy, jz);
   long long idx = 2 * jx + 1;
   if (DIM >= 2) idx += (long long)(2 * jy + 1) * gf.sy;
   if (DIM == 3) idx += (long long)(2 * jz + 1) * gf.sz;
-  cz[t] = f[idx];
+  cz[gc.at(jx, jy, jz)] = f[idx];
 }
 
 template <int DIM>
@@ -49,36 +45,38 @@ __global__ void __launch_bounds__(256) k_prolong(const double* __restrict__ c,
                                                  int accumulate) {
   long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= gf.npts) return;
-  int ix = (int)(t % gf.nx);
-  long long r = t / gf.nx;
-  int iy = (int)(r % gf.ny);
-  int iz = (int)(r / gf.ny);
+  int ix, iy, iz;
+  decode_point(gf, t, ix, iy, iz);
+  const long long o = gf.at(ix, iy, iz);
   double v = lin_point<DIM>(c, gc, ix, iy, iz);
-  f[t] = accumulate ? f[t] + v : v;
+  f[o] = accumulate ? f[o] + v : v;
 }
 
-// One axis of the cubic interpolation (transfers.py:82-89): input shape
-// (n0, nin, n2) -> output (n0, nout, n2) along the middle axis, with
-// sequential FMA over the taps (dgemm order).
+// One axis of the cubic interpolation (transfers.py:82-89): input viewed as
+// (A, Bin, C) with strides (ia, ib, 1) -> output (A, Bout, C) with strides
+// (oa, ob, 1), interpolating along B with sequential FMA over the taps
+// (dgemm order).  Padded rows are processed whole (their zeros map to zeros).
 __global__ void __launch_bounds__(256) k_cubic_axis(const double* __restrict__ in,
-                                                    double* __restrict__ out, long long n0,
-                                                    int nin, int nout, long long n2,
+                                                    double* __restrict__ out, long long A,
+                                                    int bout, long long C, long long ia,
+                                                    long long ib, long long oa, long long ob,
                                                     const int* __restrict__ cnt,
                                                     const int* __restrict__ tidx,
                                                     const double* __restrict__ tw,
                                                     int accumulate) {
   long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  long long total = n0 * nout * n2;
-  if (t >= total) return;
-  long long k2 = t % n2;
-  long long r = t / n2;
-  int i = (int)(r % nout);
-  long long k0 = r / nout;
-  const double* src = in + k0 * nin * n2 + k2;
+  if (t >= A * bout * C) return;
+  long long cc = t % C;
+  long long r = t / C;
+  int i = (int)(r % bout);
+  long long a = r / bout;
+  const double* src = in + a * ia + cc;
   double acc = 0.0;
   int nt = cnt[i];
-  for (int q = 0; q < nt; ++q) acc = __fma_rn(tw[i * 4 + q], src[(long long)tidx[i * 4 + q] * n2], acc);
-  out[t] = accumulate ? out[t] + acc : acc;
+  for (int q = 0; q < nt; ++q)
+    acc = __fma_rn(tw[i * 4 + q], src[(long long)tidx[i * 4 + q] * ib], acc);
+  double* dst = out + a * oa + (long long)i * ob + cc;
+  *dst = accumulate ? *dst + acc : acc;
 }
 
 }  // namespace
@@ -189,34 +187,38 @@ const CubicTaps* cubic_taps(int nf) {
 }
 
 long long cubic_scratch_doubles(const Geo& gf) {
-  long long Nf = gf.N, Nc = (gf.N + 1) / 2 - 1;
+  Geo gc = make_geo(gf.dim, (gf.N + 1) / 2);
+  long long Nf = gf.N, Nc = gc.N;
   if (gf.dim == 1) return 0;
-  if (gf.dim == 2) return Nf * Nc;
-  return Nf * Nc * Nc + Nf * Nf * Nc;
+  if (gf.dim == 2) return Nf * gc.sy;
+  return Nf * Nc * gc.sy + Nf * Nf * gc.sy;
 }
 
 int launch_cubic(const double* coarse, double* fine, const Geo& gf, int accumulate,
                  double* scratch, cudaStream_t s) {
   const CubicTaps* t = cubic_taps(gf.N + 1);
   if (!t) return 2;
-  long long Nf = gf.N, Nc = (gf.N + 1) / 2 - 1;
-  auto pass = [&](const double* in, double* out, long long n0, long long n2, int acc) {
-    long long total = n0 * Nf * n2;
-    k_cubic_axis<<<ceil_div(total, 256), 256, 0, s>>>(in, out, n0, (int)Nc, (int)Nf, n2,
+  Geo gc = make_geo(gf.dim, (gf.N + 1) / 2);
+  const long long Nf = gf.N, Nc = gc.N, pc = gc.sy, pf = gf.sy;
+  auto pass = [&](const double* in, double* out, long long A, long long C, long long ia,
+                  long long ib, long long oa, long long ob, int acc) {
+    long long total = A * Nf * C;
+    k_cubic_axis<<<ceil_div(total, 256), 256, 0, s>>>(in, out, A, (int)Nf, C, ia, ib, oa, ob,
                                                       t->cnt, t->idx, t->w, acc);
   };
   PL_PRE(K_INTERP);
   if (gf.dim == 1) {
-    pass(coarse, fine, 1, 1, accumulate);
+    pass(coarse, fine, 1, 1, 0, 1, 0, 1, accumulate);
   } else if (gf.dim == 2) {
-    pass(coarse, scratch, 1, Nc, 0);          // axis 0: (Nc,Nc) -> (Nf,Nc)
-    pass(scratch, fine, Nf, 1, accumulate);   // axis 1: (Nf,Nc) -> (Nf,Nf)
+    // axis 0 (y): (Nc, pc) -> scratch (Nf, pc); axis 1 (x): rows of pc -> fine rows
+    pass(coarse, scratch, 1, pc, 0, pc, 0, pc, 0);
+    pass(scratch, fine, Nf, 1, pc, 1, pf, 1, accumulate);
   } else {
-    double* s1 = scratch;                     // (Nf, Nc, Nc)
-    double* s2 = scratch + Nf * Nc * Nc;      // (Nf, Nf, Nc)
-    pass(coarse, s1, 1, Nc * Nc, 0);
-    pass(s1, s2, Nf, Nc, 0);
-    pass(s2, fine, Nf * Nf, 1, accumulate);
+    double* s1 = scratch;                     // (Nf, Nc, pc)
+    double* s2 = scratch + Nf * Nc * pc;      // (Nf, Nf, pc)
+    pass(coarse, s1, 1, Nc * pc, 0, Nc * pc, 0, Nc * pc, 0);   // axis 0 (z)
+    pass(s1, s2, Nf, pc, Nc * pc, pc, Nf * pc, pc, 0);         // axis 1 (y)
+    pass(s2, fine, Nf * Nf, 1, pc, 1, pf, 1, accumulate);     // axis 2 (x)
   }
   double bytes = (accumulate ? 16.0 : 8.0) * gf.npts;
   if (gf.dim >= 2) bytes += 16.0 * (double)cubic_scratch_doubles(gf);

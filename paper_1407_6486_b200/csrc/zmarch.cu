@@ -1,23 +1,28 @@
-// 3-D order-2 stencil kernels with a cp.async plane pipeline ("z-marching").
+// 3-D order-2 stencil kernels fed by TMA ("z-marching").
 //
 // A CTA owns a 32 x 16 (x, y) tile and marches through a chunk of z planes.
-// Each plane tile (with its 1- or 2-point halo; Dirichlet ghosts are the
-// zero-fill of out-of-domain cp.async copies) is staged into a shared-memory
-// ring PREF planes ahead of the plane being computed, so every SM keeps tens
-// of KB of loads in flight (the naive one-point-per-thread kernels were
-// latency-bound: <0.5 eligible warps per scheduler, see profiles/).  z
-// neighbours come from the ring, x/y neighbours from the same smem plane;
-// DRAM sees each input field once and each output field once.
+// Each plane window (tile plus a 1- or 2-point halo) arrives in shared memory
+// through one cp.async.bulk.tensor copy issued by a single thread; the
+// tensor map covers only the interior points, so out-of-domain halo points
+// -- the homogeneous Dirichlet ghosts -- are zero-filled by the TMA unit and
+// the padded rows of the device layout are never read.  Copies run PREF
+// planes ahead of the plane being computed and complete on per-slot
+// mbarriers; no SM instruction is spent on address arithmetic for loads.
 //
 // Fused sweeps (temporal blocking) run two dependent stages in one pass:
-//   k_zrb   one full jor-rb sweep (red on plane z+1, black on plane z)
-//   k_zjac2 two Jacobi sweeps (sweep 1 on plane z+1 over the halo-1 region,
-//           sweep 2 on plane z over the tile)
-// They read u and b once and write u once: 24 B/DOF for the whole fused
-// pass instead of 24 B/DOF per stage.  Arithmetic is the reference's
-// expression tree (common.cuh), so results are bit-identical to the
-// unfused kernels.  Out-of-domain halo points are zero and stay zero: every
-// stage forces its value to 0 outside the domain.
+//   k_z2<RB>  one full jor-rb sweep (red on plane z+1 over the halo-1 window,
+//             black on plane z over the tile)
+//   k_z2<Jac> two Jacobi sweeps (sweep 1 on plane z+1 over the halo-1 window,
+//             sweep 2 on plane z)
+// They read u and b once and write u once per pass.  Arithmetic is the
+// reference's expression tree (common.cuh), bit-identical to the unfused
+// kernels; out-of-domain stage-1 points are forced to zero.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <cstring>
+#include <mutex>
+
 #include "common.cuh"
 #include "kernels.cuh"
 
@@ -28,51 +33,46 @@ namespace {
 constexpr int TX = 32, TY = 16;           // output tile
 constexpr int NTHR = 256;                 // 32 x 8 threads, 2 rows each
 
-__device__ __forceinline__ void cp_async8(double* smem, const double* gmem, bool valid) {
-  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-  int n = valid ? 8 : 0;
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem), "r"(n));
+// ---- TMA / mbarrier primitives --------------------------------------------
+
+__device__ __forceinline__ unsigned saddr(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
 }
-__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-template <int N>
-__device__ __forceinline__ void cp_wait() {
-  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+__device__ __forceinline__ void mbar_init(unsigned long long* b, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(saddr(b)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect(unsigned long long* b, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(saddr(b)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(unsigned long long* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(saddr(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(saddr(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma3(void* dst, const CUtensorMap* map, int x, int y, int z,
+                                     unsigned long long* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4}], [%5];\n" ::"r"(saddr(dst)),
+      "l"(map), "r"(x), "r"(y), "r"(z), "r"(saddr(bar))
+      : "memory");
+}
+__device__ __forceinline__ void fence_barrier_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
 }
 
-// A W x H plane window with origin (gx0, gy0).  Each thread copies the same
-// window elements for every plane, so their in-plane offsets (or "outside
-// the domain" = -1, zero-filled) are computed once; a plane then costs one
-// 64-bit add, one predicate and one cp.async per element.
-template <int W, int H>
-struct Window {
-  static constexpr int N = W * H;
-  static constexpr int PER = (N + NTHR - 1) / NTHR;
-  int off[PER];
-
-  __device__ __forceinline__ void init(const Geo& g, int gx0, int gy0, int tid) {
-#pragma unroll
-    for (int q = 0; q < PER; ++q) {
-      int i = tid + q * NTHR;
-      int yy = i / W, xx = i - yy * W;
-      int gx = gx0 + xx, gy = gy0 + yy;
-      off[q] = (i < N && gx >= 0 && gx < g.nx && gy >= 0 && gy < g.ny)
-                   ? gy * (int)g.sy + gx : -1;
-    }
-  }
-  __device__ __forceinline__ void load(double* dst, const double* src, const Geo& g, int gz,
-                                       int tid) const {
-    const bool zin = gz >= 0 && gz < g.nz;
-    const double* plane = src + (long long)(zin ? gz : 0) * g.sz;
-#pragma unroll
-    for (int q = 0; q < PER; ++q) {
-      int i = tid + q * NTHR;
-      if (i < N) {
-        bool ok = zin && off[q] >= 0;
-        cp_async8(dst + i, ok ? plane + off[q] : src, ok);
-      }
-    }
-  }
-};
+__host__ __device__ constexpr int align16(int n) { return (n + 15) / 16 * 16; }  // doubles -> 128 B
 
 template <bool POW2>
 __device__ __forceinline__ double dd2(double x, const OpC& c) {
@@ -97,42 +97,52 @@ enum { Z_APPLY = 0, Z_RESID = 1, Z_JAC = 2, Z_JAC0 = 3 };
 // single-stage kernels: apply, residual, one Jacobi sweep
 
 template <int OP, bool POW2, int PREF>
-__global__ void __launch_bounds__(NTHR) k_z1(const double* __restrict__ u,
-                                             const double* __restrict__ b,
+__global__ void __launch_bounds__(NTHR) k_z1(const __grid_constant__ CUtensorMap mu,
+                                             const __grid_constant__ CUtensorMap mb,
                                              double* __restrict__ out, Geo g, OpC c,
                                              double sigma, double omega, double dval, int zc) {
-  constexpr int HX = TX + 2, HY = TY + 2, PU = HX * HY, PB = TX * TY, RING = PREF + 3;
+  constexpr int HX = TX + 2, HY = TY + 2, PU = align16(HX * HY), PB = align16(TX * TY);
+  constexpr int RING = PREF + 3;
   constexpr bool NEED_U = OP != Z_JAC0;
   constexpr bool NEED_B = OP != Z_APPLY;
-  extern __shared__ double sm[];
+  extern __shared__ __align__(128) double sm[];
   double* su = sm;
   double* sb = sm + (NEED_U ? RING * PU : 0);
+  unsigned long long* bar = (unsigned long long*)(sb + (NEED_B ? RING * PB : 0));
   const int tid = threadIdx.y * 32 + threadIdx.x;
   const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TY;
   const int z0 = blockIdx.z * zc, z1 = min(z0 + zc, g.nz);
-
-  Window<HX, HY> wu;
-  Window<TX, TY> wb;
-  if (NEED_U) wu.init(g, x0 - 1, y0 - 1, tid);
-  if (NEED_B) wb.init(g, x0, y0, tid);
-  auto load = [&](int zz) {
-    if (zz <= z1) {
-      int slot = (zz - z0 + 1) % RING;
-      if (NEED_U) wu.load(su + slot * PU, u, g, zz, tid);
-      if (NEED_B && zz < z1) wb.load(sb + slot * PB, b, g, zz, tid);
-    }
-    cp_commit();
-  };
-  if (NEED_U) {
-    for (int k = -1; k <= PREF; ++k) load(z0 + k);
-  } else {
-    cp_commit();
-    for (int k = 0; k <= PREF; ++k) load(z0 + k);
+  if (tid == 0) {
+    for (int i = 0; i < RING; ++i) mbar_init(bar + i, 1);
+    fence_barrier_init();
   }
+  __syncthreads();
+  // plane p (z0-1 <= p <= z1) uses slot (p - z0 + 1) % RING, its k-th use
+  // waits on parity k & 1.  Every plane in range arrives exactly once.
+  auto issue = [&](int p) {
+    if (p > z1) return;
+    const int slot = (p - z0 + 1) % RING;
+    const bool wu = NEED_U;
+    const bool wb = NEED_B && p >= z0 && p < z1;
+    if (!wu && !wb) {
+      mbar_arrive(bar + slot);
+      return;
+    }
+    mbar_expect(bar + slot, (wu ? HX * HY * 8u : 0u) + (wb ? TX * TY * 8u : 0u));
+    if (wu) tma3(su + slot * PU, &mu, x0 - 1, y0 - 1, p, bar + slot);
+    if (wb) tma3(sb + slot * PB, &mb, x0, y0, p, bar + slot);
+  };
+  auto wait = [&](int p) {
+    const int k = p - z0 + 1;
+    mbar_wait(bar + k % RING, (unsigned)((k / RING) & 1));
+  };
+  if (tid == 0)
+    for (int p = z0 - 1; p <= z0 + PREF; ++p) issue(p);
+  wait(z0 - 1);
+  wait(z0);
   const int gx = x0 + threadIdx.x;
   for (int z = z0; z < z1; ++z) {
-    cp_wait<PREF - 1>();
-    __syncthreads();
+    wait(z + 1);
     const int sc = (z - z0 + 1) % RING;
     const double* pc = su + sc * PU;
     const double* pm = su + ((z - z0) % RING) * PU;
@@ -143,7 +153,6 @@ __global__ void __launch_bounds__(NTHR) k_z1(const double* __restrict__ u,
       const int ly = threadIdx.y + 8 * r;
       const int gy = y0 + ly;
       if (gx < g.nx && gy < g.ny) {
-        const long long gi = (long long)z * g.sz + (long long)gy * g.sy + gx;
         const int i = (ly + 1) * HX + threadIdx.x + 1;
         double v;
         if (OP == Z_JAC0) {
@@ -158,52 +167,73 @@ __global__ void __launch_bounds__(NTHR) k_z1(const double* __restrict__ u,
             v = OP == Z_RESID ? bb - au : pc[i] + ((omega * (bb - au)) / dval);
           }
         }
-        out[gi] = v;
+        out[g.at(gx, gy, z)] = v;
       }
     }
-    __syncthreads();
-    load(z + PREF + 1);
+    __syncthreads();   // slot of plane z-1 is free
+    if (tid == 0) issue(z + PREF + 1);
   }
-  cp_wait<0>();
 }
 
 // ---------------------------------------------------------------------------
-// fused two-stage kernels.  Input u window has halo 2, the intermediate stage
-// (red-updated / once-smoothed u) halo 1.
+// fused two-stage kernels.  Input u window has halo 2, stage 1 and b halo 1.
 
 template <bool RB, bool POW2, int PREF>
-__global__ void __launch_bounds__(NTHR) k_z2(const double* __restrict__ u,
-                                             const double* __restrict__ b,
+__global__ void __launch_bounds__(NTHR) k_z2(const __grid_constant__ CUtensorMap mu,
+                                             const __grid_constant__ CUtensorMap mb,
                                              double* __restrict__ out, Geo g, OpC c,
                                              double sigma, double omega, double dval, int zc,
                                              int zero_in) {
-  constexpr int UX = TX + 4, UY = TY + 4, PU = UX * UY;     // input, halo 2
-  constexpr int HX = TX + 2, HY = TY + 2, PH = HX * HY;     // stage 1 + b, halo 1
-  constexpr int RU = PREF + 3;    // u planes: the prologue stages z0-2 .. z0+PREF
-  constexpr int RB_ = PREF + 1;   // b planes in flight / live (>= PREF)
-  extern __shared__ double sm[];
+  constexpr int UX = TX + 4, UY = TY + 4, PU = align16(UX * UY);    // input, halo 2
+  constexpr int HX = TX + 2, HY = TY + 2, PH = align16(HX * HY);    // stage 1 + b, halo 1
+  constexpr int NH = HX * HY;
+  constexpr int RU = PREF + 3;    // u planes z0-2 .. z0+PREF staged in the prologue
+  constexpr int RBB = PREF + 1;   // b planes
+  extern __shared__ __align__(128) double sm[];
   double* su = sm;                        // RU * PU
-  double* sbb = su + RU * PU;             // RB_ * PH
-  double* s1 = sbb + RB_ * PH;            // 3 * PH  stage-1 planes z-1, z, z+1
+  double* sbb = su + RU * PU;             // RBB * PH
+  double* s1 = sbb + RBB * PH;            // 3 * PH  stage-1 planes z-1, z, z+1
+  unsigned long long* bu = (unsigned long long*)(s1 + 3 * PH);
+  unsigned long long* bbar = bu + RU;
   const int tid = threadIdx.y * 32 + threadIdx.x;
   const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TY;
   const int z0 = blockIdx.z * zc, z1 = min(z0 + zc, g.nz);
-
-  // plane zz of u lives in slot (zz - z0 + 2) % RU (zz >= z0 - 2)
-  // plane zz of b lives in slot (zz - z0 + 1) % RB_ (zz >= z0 - 1)
-  Window<UX, UY> wu;
-  Window<HX, HY> wb;
-  wu.init(g, x0 - 2, y0 - 2, tid);
-  wb.init(g, x0 - 1, y0 - 1, tid);
-  auto load = [&](int zz) {            // u plane zz and b plane zz - 1
-    if (zz <= z1 + 1 && !zero_in) wu.load(su + ((zz - z0 + 2) % RU) * PU, u, g, zz, tid);
-    const int zb = zz - 1;
-    if (zb >= z0 - 1 && zb <= z1) wb.load(sbb + ((zb - z0 + 1) % RB_) * PH, b, g, zb, tid);
-    cp_commit();
+  if (tid == 0) {
+    for (int i = 0; i < RU; ++i) mbar_init(bu + i, 1);
+    for (int i = 0; i < RBB; ++i) mbar_init(bbar + i, 1);
+    fence_barrier_init();
+  }
+  __syncthreads();
+  // u plane p (z0-2 <= p <= z1+1): slot (p - z0 + 2) % RU
+  // b plane q (z0-1 <= q <= z1):   slot (q - z0 + 1) % RBB
+  auto issue = [&](int p) {          // u plane p and b plane p - 1
+    if (p <= z1 + 1) {
+      const int k = p - z0 + 2;
+      if (zero_in) {
+        mbar_arrive(bu + k % RU);
+      } else {
+        mbar_expect(bu + k % RU, UX * UY * 8u);
+        tma3(su + (k % RU) * PU, &mu, x0 - 2, y0 - 2, p, bu + k % RU);
+      }
+    }
+    const int q = p - 1;
+    if (q >= z0 - 1 && q <= z1) {
+      const int k = q - z0 + 1;
+      mbar_expect(bbar + k % RBB, HX * HY * 8u);
+      tma3(sbb + (k % RBB) * PH, &mb, x0 - 1, y0 - 1, q, bbar + k % RBB);
+    }
   };
-  // stage 1 at plane zz over the halo-1 window (value 0 outside the domain);
-  // each thread owns the same <= 3 window points on every plane
-  constexpr int PER1 = (PH + NTHR - 1) / NTHR;
+  auto wait_u = [&](int p) {
+    const int k = p - z0 + 2;
+    mbar_wait(bu + k % RU, (unsigned)((k / RU) & 1));
+  };
+  auto wait_b = [&](int q) {
+    const int k = q - z0 + 1;
+    mbar_wait(bbar + k % RBB, (unsigned)((k / RBB) & 1));
+  };
+
+  // each thread owns the same <= 3 stage-1 window points on every plane
+  constexpr int PER1 = (NH + NTHR - 1) / NTHR;
   int e_k[PER1], e_i[PER1], e_par[PER1];
   bool e_in[PER1];
 #pragma unroll
@@ -213,7 +243,7 @@ __global__ void __launch_bounds__(NTHR) k_z2(const double* __restrict__ u,
     int gxx = x0 - 1 + xx, gyy = y0 - 1 + yy;
     e_k[q] = k;
     e_i[q] = (yy + 1) * UX + xx + 1;
-    e_in[q] = k < PH && gxx >= 0 && gxx < g.nx && gyy >= 0 && gyy < g.ny;
+    e_in[q] = k < NH && gxx >= 0 && gxx < g.nx && gyy >= 0 && gyy < g.ny;
     e_par[q] = (gxx + gyy + 3) & 1;
   }
   auto stage1 = [&](int zz) {
@@ -222,28 +252,28 @@ __global__ void __launch_bounds__(NTHR) k_z2(const double* __restrict__ u,
     const double* pm = su + ((zz - 1 - z0 + 2 + RU) % RU) * PU;
     const double* pc = su + ((zz - z0 + 2) % RU) * PU;
     const double* pp = su + ((zz + 1 - z0 + 2) % RU) * PU;
-    const double* pb = sbb + ((zz - z0 + 1) % RB_) * PH;
+    const double* pb = sbb + ((zz - z0 + 1) % RBB) * PH;
 #pragma unroll
     for (int q = 0; q < PER1; ++q) {
       const int k = e_k[q];
-      if (k < PH) {
+      if (k < NH) {
         double v = 0.0;
         if (zin && e_in[q]) {
           const int i = e_i[q];
-          double bb = pb[k];
+          double b = pb[k];
           if (RB) {
             bool red = ((e_par[q] + zz) & 1) == 0;
             if (red) {
-              double r = bb - (pc[i] - sigma * lap7<POW2, UX>(pm, pc, pp, i, c));
+              double r = b - (pc[i] - sigma * lap7<POW2, UX>(pm, pc, pp, i, c));
               v = pc[i] + ((omega * r) / dval);
             } else {
               v = pc[i];
             }
           } else if (zero_in) {
-            v = 0.0 + ((omega * bb) / dval);
+            v = 0.0 + ((omega * b) / dval);
           } else {
             double au = pc[i] - sigma * lap7<POW2, UX>(pm, pc, pp, i, c);
-            v = pc[i] + ((omega * (bb - au)) / dval);
+            v = pc[i] + ((omega * (b - au)) / dval);
           }
         }
         dst[k] = v;
@@ -251,23 +281,24 @@ __global__ void __launch_bounds__(NTHR) k_z2(const double* __restrict__ u,
     }
   };
 
-  for (int k = -2; k <= PREF; ++k) load(z0 + k);     // u: z0-2..z0+PREF
-  // prologue: stage-1 planes z0-1 and z0 need u up to z0+1 and b up to z0
-  cp_wait<PREF - 1>();
-  __syncthreads();
+  if (tid == 0)
+    for (int p = z0 - 2; p <= z0 + PREF; ++p) issue(p);
+  // prologue: stage-1 planes z0-1, z0 need u z0-2 .. z0+1 and b z0-1, z0
+  for (int p = z0 - 2; p <= z0 + 1; ++p) wait_u(p);
+  wait_b(z0 - 1);
+  wait_b(z0);
   stage1(z0 - 1);
   stage1(z0);
   const int gx = x0 + threadIdx.x;
   for (int z = z0; z < z1; ++z) {
-    // stage 1 at z+1 needs u plane z+2 and b plane z+1: groups up to z+2
-    cp_wait<PREF - 2>();
-    __syncthreads();
+    wait_u(z + 2);
+    wait_b(z + 1);
     stage1(z + 1);
     __syncthreads();
     const double* qm = s1 + ((z - 1 - z0 + 3) % 3) * PH;
     const double* qc = s1 + ((z - z0 + 3) % 3) * PH;
     const double* qp = s1 + ((z + 1 - z0 + 3) % 3) * PH;
-    const double* pb = sbb + ((z - z0 + 1) % RB_) * PH;
+    const double* pb = sbb + ((z - z0 + 1) % RBB) * PH;
 #pragma unroll
     for (int r = 0; r < 2; ++r) {
       const int ly = threadIdx.y + 8 * r;
@@ -287,17 +318,52 @@ __global__ void __launch_bounds__(NTHR) k_z2(const double* __restrict__ u,
           double au = qc[i] - sigma * lap7<POW2, HX>(qm, qc, qp, i, c);
           v = qc[i] + ((omega * (pb[i] - au)) / dval);
         }
-        out[(long long)z * g.sz + (long long)gy * g.sy + gx] = v;
+        out[g.at(gx, gy, z)] = v;
       }
     }
-    __syncthreads();
-    load(z + PREF + 1);
+    __syncthreads();   // u plane z, b plane z and stage-1 plane z-1 are free
+    if (tid == 0) issue(z + PREF + 1);
   }
-  cp_wait<0>();
 }
 
 constexpr int PREF1 = 3;
 constexpr int PREF2 = 3;
+
+// ---- host: tensor maps -----------------------------------------------------
+
+PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+std::mutex g_encode_mu;
+
+int get_encode() {
+  std::lock_guard<std::mutex> lk(g_encode_mu);
+  if (g_encode) return 0;
+  void* fn = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  cudaError_t e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q);
+  if (e != cudaSuccess || q != cudaDriverEntryPointSuccess || !fn) {
+    set_error("cuTensorMapEncodeTiled unavailable");
+    return 2;
+  }
+  g_encode = (PFN_cuTensorMapEncodeTiled_v12000)fn;
+  return 0;
+}
+
+int make_map(CUtensorMap* m, const double* base, const Geo& g, int bw, int bh) {
+  PL_TRY(get_encode());
+  cuuint64_t dims[3] = {(cuuint64_t)g.nx, (cuuint64_t)g.ny, (cuuint64_t)g.nz};
+  cuuint64_t strides[2] = {(cuuint64_t)g.sy * 8, (cuuint64_t)g.sz * 8};
+  cuuint32_t box[3] = {(cuuint32_t)bw, (cuuint32_t)bh, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, (void*)base, dims, strides, box,
+                        estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error("cuTensorMapEncodeTiled failed (%d): base %p pitch %lld", (int)r, (void*)base,
+              (long long)g.sy);
+    return 2;
+  }
+  return 0;
+}
 
 int pick_zc(const Geo& g) {
   // enough CTAs for several waves on 148 SMs; chunk halo planes cost
@@ -312,8 +378,15 @@ template <int OP>
 int launch_z1(const double* u, const double* b, double* out, const Geo& g, const OpC& c,
               double sigma, double omega, double dval, cudaStream_t s) {
   constexpr int HX = TX + 2, HY = TY + 2, RING = PREF1 + 3;
+  CUtensorMap mu, mb;
+  std::memset(&mu, 0, sizeof(mu));
+  std::memset(&mb, 0, sizeof(mb));
+  if (OP != Z_JAC0) PL_TRY(make_map(&mu, u, g, HX, HY));
+  if (OP != Z_APPLY) PL_TRY(make_map(&mb, b, g, TX, TY));
   size_t smem = sizeof(double) * RING *
-                ((OP != Z_JAC0 ? HX * HY : 0) + (OP != Z_APPLY ? TX * TY : 0));
+                    ((OP != Z_JAC0 ? align16(HX * HY) : 0) +
+                     (OP != Z_APPLY ? align16(TX * TY) : 0)) +
+                8 * RING;
   int zc = pick_zc(g);
   dim3 grid(ceil_div(g.nx, TX), ceil_div(g.ny, TY), ceil_div(g.nz, zc)), block(32, 8);
   auto kern = c.pow2 ? k_z1<OP, true, PREF1> : k_z1<OP, false, PREF1>;
@@ -322,7 +395,7 @@ int launch_z1(const double* u, const double* b, double* out, const Geo& g, const
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
     set[c.pow2] = true;
   }
-  kern<<<grid, block, smem, s>>>(u, b, out, g, c, sigma, omega, dval, zc);
+  kern<<<grid, block, smem, s>>>(mu, mb, out, g, c, sigma, omega, dval, zc);
   return 0;
 }
 
@@ -330,7 +403,13 @@ template <bool RB>
 int launch_z2(const double* u, const double* b, double* out, const Geo& g, const OpC& c,
               double sigma, double omega, double dval, int zero_in, cudaStream_t s) {
   constexpr int UX = TX + 4, UY = TY + 4, HX = TX + 2, HY = TY + 2;
-  size_t smem = sizeof(double) * ((PREF2 + 3) * UX * UY + (PREF2 + 1) * HX * HY + 3 * HX * HY);
+  CUtensorMap mu, mb;
+  std::memset(&mu, 0, sizeof(mu));
+  if (!zero_in) PL_TRY(make_map(&mu, u, g, UX, UY));
+  PL_TRY(make_map(&mb, b, g, HX, HY));
+  size_t smem = sizeof(double) * ((PREF2 + 3) * align16(UX * UY) +
+                                  (PREF2 + 1) * align16(HX * HY) + 3 * align16(HX * HY)) +
+                8 * ((PREF2 + 3) + (PREF2 + 1));
   int zc = pick_zc(g);
   dim3 grid(ceil_div(g.nx, TX), ceil_div(g.ny, TY), ceil_div(g.nz, zc)), block(32, 8);
   auto kern = c.pow2 ? k_z2<RB, true, PREF2> : k_z2<RB, false, PREF2>;
@@ -339,7 +418,7 @@ int launch_z2(const double* u, const double* b, double* out, const Geo& g, const
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
     set[c.pow2] = true;
   }
-  kern<<<grid, block, smem, s>>>(u, b, out, g, c, sigma, omega, dval, zc, zero_in);
+  kern<<<grid, block, smem, s>>>(mu, mb, out, g, c, sigma, omega, dval, zc, zero_in);
   return 0;
 }
 
@@ -357,12 +436,13 @@ double zdiag(const OpC& c, double sigma) {
 int g_zmarch_enabled = 1;   // runtime knob (pl_set_option), for A/B tests
 
 bool zmarch_ok(const Geo& g, const OpC& c) {
-  return g_zmarch_enabled && g.dim == 3 && c.order == 2 && g.N >= 31;
+  // TMA needs 16-byte row and plane strides: the padded device layout
+  return g_zmarch_enabled && g.dim == 3 && c.order == 2 && g.N >= 31 && (g.sy % 2) == 0;
 }
 
 int zlaunch_apply(const double* u, double* f, const Geo& g, const OpC& c, cudaStream_t s) {
   PL_PRE(K_APPLY);
-  launch_z1<Z_APPLY>(u, nullptr, f, g, c, 0.0, 0.0, 1.0, s);
+  PL_TRY(launch_z1<Z_APPLY>(u, nullptr, f, g, c, 0.0, 0.0, 1.0, s));
   PL_CHECK_LAUNCH(K_APPLY, 16.0 * g.npts);
   return 0;
 }
@@ -370,7 +450,7 @@ int zlaunch_apply(const double* u, double* f, const Geo& g, const OpC& c, cudaSt
 int zlaunch_residual(const double* u, const double* b, double* r, const Geo& g, const OpC& c,
                      double sigma, cudaStream_t s) {
   PL_PRE(K_RESID);
-  launch_z1<Z_RESID>(u, b, r, g, c, sigma, 0.0, 1.0, s);
+  PL_TRY(launch_z1<Z_RESID>(u, b, r, g, c, sigma, 0.0, 1.0, s));
   PL_CHECK_LAUNCH(K_RESID, 24.0 * g.npts);
   return 0;
 }
@@ -379,8 +459,8 @@ int zlaunch_jacobi(const double* u, const double* b, double* out, const Geo& g, 
                    double sigma, double omega, int zero_in, cudaStream_t s) {
   double dval = zdiag(c, sigma);
   PL_PRE(K_JACOBI);
-  if (zero_in) launch_z1<Z_JAC0>(u, b, out, g, c, sigma, omega, dval, s);
-  else launch_z1<Z_JAC>(u, b, out, g, c, sigma, omega, dval, s);
+  if (zero_in) PL_TRY(launch_z1<Z_JAC0>(u, b, out, g, c, sigma, omega, dval, s));
+  else PL_TRY(launch_z1<Z_JAC>(u, b, out, g, c, sigma, omega, dval, s));
   PL_CHECK_LAUNCH(K_JACOBI, (zero_in ? 16.0 : 24.0) * g.npts);
   return 0;
 }
@@ -389,7 +469,7 @@ int zlaunch_jacobi2(const double* u, const double* b, double* out, const Geo& g,
                     double sigma, double omega, int zero_in, cudaStream_t s) {
   double dval = zdiag(c, sigma);
   PL_PRE(K_JACOBI);
-  launch_z2<false>(u, b, out, g, c, sigma, omega, dval, zero_in, s);
+  PL_TRY(launch_z2<false>(u, b, out, g, c, sigma, omega, dval, zero_in, s));
   // algorithmic bytes of the two unfused sweeps it replaces
   PL_CHECK_LAUNCH(K_JACOBI, (zero_in ? 40.0 : 48.0) * g.npts);
   return 0;
@@ -399,7 +479,7 @@ int zlaunch_rb(const double* u, const double* b, double* out, const Geo& g, cons
                double sigma, double omega, cudaStream_t s) {
   double dval = zdiag(c, sigma);
   PL_PRE(K_RB);
-  launch_z2<true>(u, b, out, g, c, sigma, omega, dval, 0, s);
+  PL_TRY(launch_z2<true>(u, b, out, g, c, sigma, omega, dval, 0, s));
   PL_CHECK_LAUNCH(K_RB, 24.0 * g.npts);
   return 0;
 }

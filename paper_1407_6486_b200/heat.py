@@ -12,7 +12,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import _capi as capi
-from ._device import empty, like_input, ptr, stream_ptr, to_device
+from ._device import like_input, new_field, ptr, stream_ptr, to_device
 
 
 @dataclass(frozen=True)
@@ -125,15 +125,15 @@ class HeatOperator:
         return out
 
     def apply(self, u):
-        t, host = to_device(u)
-        if tuple(t.shape) != self.grid.shape:
-            raise ValueError(f"expected shape {self.grid.shape}, got {tuple(t.shape)}")
-        out = empty(self.grid.shape)
+        if tuple(np.shape(u)) != self.grid.shape:
+            raise ValueError(f"expected shape {self.grid.shape}, got {tuple(np.shape(u))}")
+        t, host = to_device(u, self.grid.dim)
+        out = new_field(self.grid.shape)
         self.apply_into(t, out)
         return like_input(out, host)
 
     def diagonal(self, as_numpy: bool = True):
-        out = empty(self.grid.shape)
+        out = new_field(self.grid.shape)
         capi.check(capi.lib().pl_heat_diagonal(ptr(out), *self._args(), 0.0, 0, stream_ptr()),
                    "HeatOperator.diagonal")
         return like_input(out, as_numpy)

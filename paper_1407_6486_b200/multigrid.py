@@ -16,7 +16,7 @@ import scipy.linalg
 import torch
 
 from . import _capi as capi
-from ._device import device, like_input, ptr, stream_ptr, to_device
+from ._device import clone_field, device, like_input, new_field, ptr, stream_ptr, to_device
 from .heat import Grid, HeatOperator
 
 
@@ -90,7 +90,7 @@ class _Plan:
         g = op.grid
         lib = capi.lib()
         nbytes = lib.pl_mg_workspace_bytes(g.dim, g.n, cfg.coarsest_n)
-        self.ws = torch.empty(max(nbytes, 8), dtype=torch.uint8, device=device())
+        self.ws = torch.zeros(max(nbytes, 8), dtype=torch.uint8, device=device())
         h = C.c_void_p()
         capi.check(lib.pl_mg_plan_create(C.byref(h), g.dim, g.n, float(g.length), float(op.nu),
                                          op.order, capi.SMOOTHERS[cfg.smoother],
@@ -190,9 +190,9 @@ class ShiftedOperator:
         return self.base.grid
 
     def apply(self, u):
-        t, host = to_device(u)
-        out = torch.empty_like(t)
         g = self.base.grid
+        t, host = to_device(u, g.dim)
+        out = new_field(g.shape)
         capi.check(capi.lib().pl_shifted_apply(ptr(t), ptr(out), g.dim, g.n, float(g.length),
                                                float(self.base.nu), self.base.order,
                                                float(self.sigma), stream_ptr()),
@@ -201,7 +201,7 @@ class ShiftedOperator:
 
     def diagonal(self, as_numpy: bool = True):
         g = self.base.grid
-        out = torch.empty(g.shape, dtype=torch.float64, device=device())
+        out = new_field(g.shape)
         capi.check(capi.lib().pl_heat_diagonal(ptr(out), g.dim, g.n, float(g.length),
                                                float(self.base.nu), self.base.order,
                                                float(self.sigma), 1, stream_ptr()),
@@ -220,11 +220,12 @@ def _check_policy(policy):
 
 def smooth(op: ShiftedOperator, u, b, cfg: MgConfig, count: int):
     """multigrid.py:211-234 (returns a new array, like the reference)."""
-    tu, host = to_device(u)
-    tb, _ = to_device(b)
-    if tu.shape != tb.shape:
+    if tuple(np.shape(u)) != tuple(np.shape(b)):
         raise ValueError("shape mismatch between iterate and right-hand side")
-    out = tu.clone()
+    d = op.grid.dim
+    tu, host = to_device(u, d)
+    tb, _ = to_device(b, d)
+    out = clone_field(tu)
     if count:
         p = plan_for(op.base, cfg)
         capi.check(capi.lib().pl_mg_smooth(p.handle.value, ptr(out), ptr(tb), float(op.sigma),
@@ -243,9 +244,10 @@ def vcycles_into(op: ShiftedOperator, u, b, cfg: MgConfig, ncycles: int, zero_gu
 
 def v_cycle(op: ShiftedOperator, u, b, cfg: MgConfig):
     """multigrid.py:237-251 (returns a new array)."""
-    tu, host = to_device(u)
-    tb, _ = to_device(b)
-    out = tu.clone()
+    d = op.grid.dim
+    tu, host = to_device(u, d)
+    tb, _ = to_device(b, d)
+    out = clone_field(tu)
     vcycles_into(op, out, tb, cfg, 1)
     return like_input(out, host)
 
@@ -279,8 +281,9 @@ def solve_into(op: ShiftedOperator, u, b, cfg: MgConfig, policy) -> tuple:
 
 def solve(op: ShiftedOperator, u0, b, cfg: MgConfig, policy: SolvePolicy) -> SolveResult:
     """multigrid.py:261-288."""
-    tu, host = to_device(u0)
-    tb, _ = to_device(b)
-    out = tu.clone()
+    d = op.grid.dim
+    tu, host = to_device(u0, d)
+    tb, _ = to_device(b, d)
+    out = clone_field(tu)
     cycles, status = solve_into(op, out, tb, cfg, policy)
     return SolveResult(like_input(out, host), cycles, status)

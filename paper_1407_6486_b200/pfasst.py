@@ -28,7 +28,8 @@ from dataclasses import dataclass, field
 import numpy as np
 import torch
 
-from ._device import empty, to_device, zeros
+from ._device import (clone_field, field_elems, field_from_flat, flat_storage, like_input,
+                      to_device, zeros)
 from .hierarchy import (Hooks, Level, TimeStep, burn_in, check_hierarchy, interpolate_up,
                         mlsdc_iteration, restrict_state)
 from .sdc import NodeStates, residual_into
@@ -103,7 +104,7 @@ class DeviceEngine:
                 if l > 0:
                     prev = self.levels[l - 1]
                     if lvl.grid.n == prev.grid.n:
-                        uu = uu.clone()
+                        uu = clone_field(uu)
                     else:
                         from .transfers import full_weighting, inject
                         uu = inject(uu) if prev.space_restrict == "inject" else \
@@ -116,8 +117,9 @@ class DeviceEngine:
                 ts.tau[l] = None
         copies = self.spread_y.get(n)
         if copies is None:
-            copies = self.spread_y[n] = [None] + [ts.states[l].y.clone()
-                                                  for l in range(1, self.L)]
+            copies = self.spread_y[n] = [None] + [clone_field(ts.states[l].y, lvl_d)
+                                                  for l in range(1, self.L)
+                                                  for lvl_d in [self.levels[l].grid.dim]]
         else:
             for l in range(1, self.L):
                 copies[l].copy_(ts.states[l].y)
@@ -144,7 +146,7 @@ class DeviceEngine:
 
     def interpolate_up(self, n, exact):
         ts = self.ts[n]
-        interpolate_up(ts, self.spread_y[n], exact_y0=ts.y0[0].clone() if exact else None)
+        interpolate_up(ts, self.spread_y[n], exact_y0=clone_field(ts.y0[0]) if exact else None)
 
     def iteration(self, n, pre_coarse):
         return mlsdc_iteration(self.ts[n], self.dt, _PreCoarse(pre_coarse))
@@ -163,7 +165,18 @@ class DeviceEngine:
         return float(self._res_host[n].item())
 
     def snapshot(self, t):
-        return t.clone()
+        return clone_field(t)
+
+    # wire format of the NCCL hand-offs: the field's flat padded storage
+    def to_wire(self, t):
+        return flat_storage(t).clone()
+
+    def wire_buffer(self, like):
+        return torch.empty(field_elems(tuple(like.shape)), dtype=torch.float64,
+                           device=like.device)
+
+    def from_wire(self, buf, like):
+        return field_from_flat(buf, tuple(like.shape))
 
 
 # ---------------------------------------------------------------------------
@@ -231,7 +244,7 @@ class DistExchange:
         return self.proc(n) == self.me
 
     def _send(self, t, dst_rank):
-        buf = self.e.snapshot(t)
+        buf = self.e.to_wire(t)
         w = self.dist.isend(buf, self.proc(dst_rank), group=self.group)
         self._pending.append((w, buf))
         if len(self._pending) > 16:
@@ -239,9 +252,9 @@ class DistExchange:
             w0.wait()
 
     def _recv(self, like, src_rank):
-        buf = torch.empty_like(like)
+        buf = self.e.wire_buffer(like)
         self.dist.irecv(buf, self.proc(src_rank), group=self.group).wait()
-        return buf
+        return self.e.from_wire(buf, like)
 
     def send_pred(self, n, ph):
         self._send(self.e.coarse_payload(n), n + 1)
@@ -268,13 +281,15 @@ class DistExchange:
 
     def send_flag(self, n, k, flag):
         dev = self.e.fine_payload(n).device
-        self._send(torch.tensor([1.0 if flag else 0.0], dtype=torch.float64, device=dev), n + 1)
+        buf = torch.tensor([1.0 if flag else 0.0], dtype=torch.float64, device=dev)
+        w = self.dist.isend(buf, self.proc(n + 1), group=self.group)
+        self._pending.append((w, buf))
 
     def recv_flag(self, n, k):
         if n in self._cache:
             return True
-        flag = self._recv(torch.empty(1, dtype=torch.float64,
-                                      device=self.e.fine_payload(n).device), n - 1)
+        flag = torch.empty(1, dtype=torch.float64, device=self.e.fine_payload(n).device)
+        self.dist.irecv(flag, self.proc(n - 1), group=self.group).wait()
         ok = bool(flag.item() != 0.0)
         if ok:                   # predecessor frozen: keep its final payloads
             self._cache[n] = self._last[n]
@@ -422,7 +437,7 @@ def pfasst_run(levels, u0, t_end: float, p: int, blocks: int = 1, tol: float = 1
         raise ValueError("need at least one rank and one block")
     dt = t_end / (p * blocks)
     if engine_factory is None:
-        u, host = to_device(u0)
+        u, host = to_device(u0, levels[0].grid.dim)
         engine_factory = DeviceEngine
     else:                       # test hook: alternative engines (CPU oracle)
         u, host = u0, False
@@ -450,13 +465,13 @@ def pfasst_run(levels, u0, t_end: float, p: int, blocks: int = 1, tol: float = 1
         if isinstance(exchange, DistExchange):
             exchange.finish()
             last = (p - 1) % exchange.world
-            if exchange.owns(p - 1):
-                u = engine.snapshot(engine.fine_payload(p - 1))
-            else:
-                u = torch.empty_like(u)
-            exchange.dist.broadcast(u, last, group=group)
+            like = engine.fine_payload(engine.ranks[0]) if engine.ranks else u
+            wire = engine.to_wire(engine.fine_payload(p - 1)) if exchange.owns(p - 1) \
+                else engine.wire_buffer(like)
+            exchange.dist.broadcast(wire, last, group=group)
+            u = engine.from_wire(wire, like)
             if record_final_values:
-                fv = [v.cpu().numpy() for v in blk.final_values] \
+                fv = [v.contiguous().cpu().numpy() for v in blk.final_values] \
                     if exchange.owns(p - 1) else None
                 holder = [fv]
                 exchange.dist.broadcast_object_list(holder, last, group=group)
@@ -468,9 +483,9 @@ def pfasst_run(levels, u0, t_end: float, p: int, blocks: int = 1, tol: float = 1
         result.rank_vcycles.append(list(vc))
         result.converged.append(list(cv))
         result.trace.extend(sorted(tr, key=lambda r: (r.iteration, r.rank, r.level)))
-        result.final_values.append([v.cpu().numpy() if host and isinstance(v, torch.Tensor)
+        result.final_values.append([like_input(v, host) if isinstance(v, torch.Tensor)
                                     else v for v in blk.final_values])
-    result.u = u.cpu().numpy() if host else u
+    result.u = like_input(u, host)
     return result
 
 

@@ -14,7 +14,7 @@ import numpy as np
 import torch
 
 from . import _capi as capi
-from ._device import empty, ptr, scratch, stream_ptr, to_device, zeros
+from ._device import clone_field, new_field, ptr, scratch, stream_ptr, to_device, zeros
 from .heat import HeatOperator
 from .multigrid import (Direct, FixedCycles, MgConfig, MultigridError, SolvePolicy,
                         ToTolerance, _check_policy, plan_for)
@@ -29,25 +29,29 @@ class NodeStates:
 
     def __init__(self, table: QuadratureTable, y, f):
         self.table = table
-        self.y = to_device(y)[0]
-        self.f = to_device(f)[0]
+        self.y = to_device(y, np.ndim(y) - 1)[0]
+        self.f = to_device(f, np.ndim(f) - 1)[0]
 
     @classmethod
     def spread(cls, op: HeatOperator, table: QuadratureTable, y0) -> "NodeStates":
-        t, _ = to_device(y0)
-        y = t.unsqueeze(0).repeat((table.m + 1,) + (1,) * t.dim())
-        f0 = empty(tuple(t.shape))
+        t, _ = to_device(y0, op.grid.dim)
+        shape = tuple(t.shape)
+        y = new_field(shape, (table.m + 1,))
+        y.copy_(t.unsqueeze(0).expand_as(y))
+        f0 = new_field(shape)
         op.apply_into(t, f0)
-        f = f0.unsqueeze(0).repeat((table.m + 1,) + (1,) * t.dim())
+        f = new_field(shape, (table.m + 1,))
+        f.copy_(f0.unsqueeze(0).expand_as(f))
         return cls(table, y, f)
 
     @classmethod
     def empty(cls, op: HeatOperator, table: QuadratureTable) -> "NodeStates":
-        shape = (table.m + 1,) + op.grid.shape
-        return cls(table, empty(shape), empty(shape))
+        lead = (table.m + 1,)
+        return cls(table, new_field(op.grid.shape, lead), new_field(op.grid.shape, lead))
 
     def copy(self) -> "NodeStates":
-        return NodeStates(self.table, self.y.clone(), self.f.clone())
+        d = self.y.dim() - 1
+        return NodeStates(self.table, clone_field(self.y, d), clone_field(self.f, d))
 
     def refresh(self, op: HeatOperator) -> None:
         for m in range(self.table.m + 1):
@@ -97,8 +101,9 @@ def sdc_sweep(states: NodeStates, y0, dt: float, op: HeatOperator, mg_cfg: MgCon
     """One sweep through the sub-steps, in place; returns V-cycles used
     (sdc.py:84-114)."""
     _check_policy(policy)
-    ty0, _ = to_device(y0)
-    ttau = to_device(tau)[0] if tau is not None else None
+    d = op.grid.dim
+    ty0, _ = to_device(y0, d)
+    ttau = to_device(tau, d)[0] if tau is not None else None
     desc = sweep_desc(states.table, policy)
     plan = plan_for(op, mg_cfg)
     for gam in states.table.nodes.gammas:
@@ -122,17 +127,19 @@ def residual_into(states: NodeStates, y0, dt: float, out, tau=None):
     """Device-side residual (asynchronous) into the 0-d/1-element tensor out."""
     m = states.table.m
     q = (C.c_double * ((m + 1) * (m + 1)))(*[float(v) for v in states.table.q.ravel()])
-    npts = states.y[0].numel()
+    d = states.y.dim() - 1
+    n = states.y.shape[-1] + 1
     capi.check(capi.lib().pl_sdc_residual(ptr(states.y), ptr(states.f), ptr(y0), ptr(tau), q,
-                                          m, float(dt), npts, ptr(out), stream_ptr()),
+                                          m, float(dt), d, n, ptr(out), stream_ptr()),
                "residual")
     return out
 
 
 def residual(states: NodeStates, y0, dt: float, tau=None) -> float:
     """Max over nodes of the max-norm of the collocation residual (sdc.py:117-124)."""
-    ty0, _ = to_device(y0)
-    ttau = to_device(tau)[0] if tau is not None else None
+    d = states.y.dim() - 1
+    ty0, _ = to_device(y0, d)
+    ttau = to_device(tau, d)[0] if tau is not None else None
     out = zeros((1,))
     residual_into(states, ty0, dt, out, ttau)
     return float(out.item())
@@ -155,7 +162,7 @@ def run_sdc(op: HeatOperator, table: QuadratureTable, u0, t_end: float, n_steps:
     if n_steps < 1:
         raise ValueError("need at least one time step")
     dt = t_end / n_steps
-    u, host = to_device(u0)
+    u, host = to_device(u0, op.grid.dim)
     result = RunResult(u=u0)
     for step in range(n_steps):
         states = NodeStates.spread(op, table, u)
@@ -172,6 +179,6 @@ def run_sdc(op: HeatOperator, table: QuadratureTable, u0, t_end: float, n_steps:
             result.exhausted_steps.append(step)
         result.iterations.append(sweeps)
         result.residuals.append(history)
-        u = states.y[-1].clone()
-    result.u = u.cpu().numpy() if host else u
+        u = clone_field(states.y[-1])
+    result.u = u.contiguous().cpu().numpy() if host else u
     return result

@@ -6,7 +6,7 @@ at fine index 2j.  All four run as sm_100a kernels (csrc/transfer.cu).
 from __future__ import annotations
 
 from . import _capi as capi
-from ._device import empty, like_input, ptr, scratch, stream_ptr, to_device
+from ._device import like_input, new_field, ptr, scratch, stream_ptr, to_device
 
 
 def _fine_n(shape):
@@ -21,7 +21,7 @@ def _restrict(u, fn):
     nf = _fine_n(tuple(t.shape))
     if nf < 4:
         raise ValueError("grid too small to coarsen")
-    out = empty((nf // 2 - 1,) * t.dim())
+    out = new_field((nf // 2 - 1,) * t.dim())
     capi.check(fn(ptr(t), ptr(out), t.dim(), nf, stream_ptr()))
     return like_input(out, host)
 
@@ -56,7 +56,7 @@ def interp_cubic_into(coarse, fine, accumulate):
 def _interp(u, fn):
     t, host = to_device(u)
     nf = 2 * (t.shape[0] + 1)
-    out = empty((nf - 1,) * t.dim())
+    out = new_field((nf - 1,) * t.dim())
     fn(t, out, False)
     return like_input(out, host)
 

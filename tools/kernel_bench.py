@@ -18,6 +18,7 @@ import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
 from paper_1407_6486_b200 import _capi, transfers  # noqa: E402
+from paper_1407_6486_b200._device import new_field, to_device  # noqa: E402
 from paper_1407_6486_b200.heat import Grid, HeatOperator  # noqa: E402
 from paper_1407_6486_b200.multigrid import MgConfig, ShiftedOperator, plan_for, vcycles_into  # noqa: E402
 from paper_1407_6486_b200.quadrature import uniform_table  # noqa: E402
@@ -50,9 +51,9 @@ def main():
     g = Grid(args.dim, args.n)
     N = g.dof
     rng = np.random.default_rng(0)
-    u = torch.from_numpy(rng.standard_normal(g.shape)).cuda()
-    b = torch.from_numpy(rng.standard_normal(g.shape)).cuda()
-    out = torch.empty_like(u)
+    u = to_device(rng.standard_normal(g.shape))[0]
+    b = to_device(rng.standard_normal(g.shape))[0]
+    out = new_field(g.shape)
     op = HeatOperator(g)
     lib = _capi.lib()
     s = torch.cuda.current_stream().cuda_stream
@@ -82,7 +83,7 @@ def main():
         (24.0 * 4 + 32 + 16 / 2 ** args.dim) / (1 - 2.0 ** -args.dim) * N)
     run("residual", lambda: lib.pl_shifted_apply(u.data_ptr(), out.data_ptr(), g.dim, g.n,
                                                  1.0, 1.0, 2, sig, s), 16.0 * N)
-    c = torch.empty((g.n // 2 - 1,) * g.dim, dtype=torch.float64, device="cuda")
+    c = new_field((g.n // 2 - 1,) * g.dim)
     run("full_weighting", lambda: lib.pl_full_weighting(u.data_ptr(), c.data_ptr(), g.dim,
                                                         g.n, s), 8.0 * N * (1 + 2.0 ** -g.dim))
     run("prolong_add", lambda: lib.pl_interp_linear(c.data_ptr(), u.data_ptr(), g.dim, g.n, 1,
@@ -92,7 +93,7 @@ def main():
     for M in (4, 8):
         table = uniform_table(M)
         st = NodeStates.spread(op, table, u)
-        y0 = u.clone()
+        y0 = to_device(u.cpu().numpy())[0]
         r = torch.zeros(1, dtype=torch.float64, device="cuda")
         run(f"residual_max_M{M}", lambda st=st, y0=y0, r=r: residual_into(st, y0, 0.01, r),
             8.0 * N * (2 * M + 2))
