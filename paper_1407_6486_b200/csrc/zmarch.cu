@@ -101,7 +101,9 @@ __global__ void __launch_bounds__(NTHR) k_z1(const __grid_constant__ CUtensorMap
                                              const __grid_constant__ CUtensorMap mb,
                                              double* __restrict__ out, Geo g, OpC c,
                                              double sigma, double omega, double dval, int zc) {
-  constexpr int HX = TX + 2, HY = TY + 2, PU = align16(HX * HY), PB = align16(TX * TY);
+  // TMA needs the innermost box start 16-byte aligned: windows start at the
+  // even column x0-2 (one extra column on the left, unused)
+  constexpr int HX = TX + 4, HY = TY + 2, PU = align16(HX * HY), PB = align16(TX * TY);
   constexpr int RING = PREF + 3;
   constexpr bool NEED_U = OP != Z_JAC0;
   constexpr bool NEED_B = OP != Z_APPLY;
@@ -129,7 +131,7 @@ __global__ void __launch_bounds__(NTHR) k_z1(const __grid_constant__ CUtensorMap
       return;
     }
     mbar_expect(bar + slot, (wu ? HX * HY * 8u : 0u) + (wb ? TX * TY * 8u : 0u));
-    if (wu) tma3(su + slot * PU, &mu, x0 - 1, y0 - 1, p, bar + slot);
+    if (wu) tma3(su + slot * PU, &mu, x0 - 2, y0 - 1, p, bar + slot);
     if (wb) tma3(sb + slot * PB, &mb, x0, y0, p, bar + slot);
   };
   auto wait = [&](int p) {
@@ -153,7 +155,7 @@ __global__ void __launch_bounds__(NTHR) k_z1(const __grid_constant__ CUtensorMap
       const int ly = threadIdx.y + 8 * r;
       const int gy = y0 + ly;
       if (gx < g.nx && gy < g.ny) {
-        const int i = (ly + 1) * HX + threadIdx.x + 1;
+        const int i = (ly + 1) * HX + threadIdx.x + 2;
         double v;
         if (OP == Z_JAC0) {
           v = 0.0 + ((omega * pb[ly * TX + threadIdx.x]) / dval);
@@ -185,14 +187,15 @@ __global__ void __launch_bounds__(NTHR) k_z2(const __grid_constant__ CUtensorMap
                                              double sigma, double omega, double dval, int zc,
                                              int zero_in) {
   constexpr int UX = TX + 4, UY = TY + 4, PU = align16(UX * UY);    // input, halo 2
-  constexpr int HX = TX + 2, HY = TY + 2, PH = align16(HX * HY);    // stage 1 + b, halo 1
+  constexpr int HX = TX + 2, HY = TY + 2, PH = align16(HX * HY);    // stage 1, halo 1
   constexpr int NH = HX * HY;
+  constexpr int BW = TX + 4, PBW = align16(BW * HY);   // b window from the even column x0-2
   constexpr int RU = PREF + 3;    // u planes z0-2 .. z0+PREF staged in the prologue
   constexpr int RBB = PREF + 1;   // b planes
   extern __shared__ __align__(128) double sm[];
   double* su = sm;                        // RU * PU
-  double* sbb = su + RU * PU;             // RBB * PH
-  double* s1 = sbb + RBB * PH;            // 3 * PH  stage-1 planes z-1, z, z+1
+  double* sbb = su + RU * PU;             // RBB * PBW
+  double* s1 = sbb + RBB * PBW;           // 3 * PH  stage-1 planes z-1, z, z+1
   unsigned long long* bu = (unsigned long long*)(s1 + 3 * PH);
   unsigned long long* bbar = bu + RU;
   const int tid = threadIdx.y * 32 + threadIdx.x;
@@ -219,8 +222,8 @@ __global__ void __launch_bounds__(NTHR) k_z2(const __grid_constant__ CUtensorMap
     const int q = p - 1;
     if (q >= z0 - 1 && q <= z1) {
       const int k = q - z0 + 1;
-      mbar_expect(bbar + k % RBB, HX * HY * 8u);
-      tma3(sbb + (k % RBB) * PH, &mb, x0 - 1, y0 - 1, q, bbar + k % RBB);
+      mbar_expect(bbar + k % RBB, BW * HY * 8u);
+      tma3(sbb + (k % RBB) * PBW, &mb, x0 - 2, y0 - 1, q, bbar + k % RBB);
     }
   };
   auto wait_u = [&](int p) {
@@ -234,7 +237,7 @@ __global__ void __launch_bounds__(NTHR) k_z2(const __grid_constant__ CUtensorMap
 
   // each thread owns the same <= 3 stage-1 window points on every plane
   constexpr int PER1 = (NH + NTHR - 1) / NTHR;
-  int e_k[PER1], e_i[PER1], e_par[PER1];
+  int e_k[PER1], e_i[PER1], e_b[PER1], e_par[PER1];
   bool e_in[PER1];
 #pragma unroll
   for (int q = 0; q < PER1; ++q) {
@@ -243,6 +246,7 @@ __global__ void __launch_bounds__(NTHR) k_z2(const __grid_constant__ CUtensorMap
     int gxx = x0 - 1 + xx, gyy = y0 - 1 + yy;
     e_k[q] = k;
     e_i[q] = (yy + 1) * UX + xx + 1;
+    e_b[q] = yy * BW + xx + 1;
     e_in[q] = k < NH && gxx >= 0 && gxx < g.nx && gyy >= 0 && gyy < g.ny;
     e_par[q] = (gxx + gyy + 3) & 1;
   }
@@ -252,7 +256,7 @@ __global__ void __launch_bounds__(NTHR) k_z2(const __grid_constant__ CUtensorMap
     const double* pm = su + ((zz - 1 - z0 + 2 + RU) % RU) * PU;
     const double* pc = su + ((zz - z0 + 2) % RU) * PU;
     const double* pp = su + ((zz + 1 - z0 + 2) % RU) * PU;
-    const double* pb = sbb + ((zz - z0 + 1) % RBB) * PH;
+    const double* pb = sbb + ((zz - z0 + 1) % RBB) * PBW;
 #pragma unroll
     for (int q = 0; q < PER1; ++q) {
       const int k = e_k[q];
@@ -260,7 +264,7 @@ __global__ void __launch_bounds__(NTHR) k_z2(const __grid_constant__ CUtensorMap
         double v = 0.0;
         if (zin && e_in[q]) {
           const int i = e_i[q];
-          double b = pb[k];
+          double b = pb[e_b[q]];
           if (RB) {
             bool red = ((e_par[q] + zz) & 1) == 0;
             if (red) {
@@ -298,30 +302,157 @@ __global__ void __launch_bounds__(NTHR) k_z2(const __grid_constant__ CUtensorMap
     const double* qm = s1 + ((z - 1 - z0 + 3) % 3) * PH;
     const double* qc = s1 + ((z - z0 + 3) % 3) * PH;
     const double* qp = s1 + ((z + 1 - z0 + 3) % 3) * PH;
-    const double* pb = sbb + ((z - z0 + 1) % RBB) * PH;
+    const double* pb = sbb + ((z - z0 + 1) % RBB) * PBW;
 #pragma unroll
     for (int r = 0; r < 2; ++r) {
       const int ly = threadIdx.y + 8 * r;
       const int gy = y0 + ly;
       if (gx < g.nx && gy < g.ny) {
         const int i = (ly + 1) * HX + threadIdx.x + 1;
+        const int ib = (ly + 1) * BW + threadIdx.x + 2;
         double v;
         if (RB) {
           bool red = ((gx + gy + z + 3) & 1) == 0;
           if (red) {
             v = qc[i];
           } else {
-            double rr = pb[i] - (qc[i] - sigma * lap7<POW2, HX>(qm, qc, qp, i, c));
+            double rr = pb[ib] - (qc[i] - sigma * lap7<POW2, HX>(qm, qc, qp, i, c));
             v = qc[i] + ((omega * rr) / dval);
           }
         } else {
           double au = qc[i] - sigma * lap7<POW2, HX>(qm, qc, qp, i, c);
-          v = qc[i] + ((omega * (pb[i] - au)) / dval);
+          v = qc[i] + ((omega * (pb[ib] - au)) / dval);
         }
         out[g.at(gx, gy, z)] = v;
       }
     }
     __syncthreads();   // u plane z, b plane z and stage-1 plane z-1 are free
+    if (tid == 0) issue(z + PREF + 1);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// one full jor-rb sweep in one pass, divergence-free.  With the 7-point
+// stencil a red point reads only black neighbours and its own old value, so
+// the red update of plane z+1 is done IN PLACE in the staged u window (no
+// copy of black points); the black update of plane z then reads the updated
+// red neighbours straight from the window.  Red work is a dense list of the
+// window's red points (17 per row); black work gives every thread one
+// (black, red) x-pair of a tile row, so no warp branches on colour.
+
+template <bool POW2, int PREF>
+__global__ void __launch_bounds__(NTHR) k_zrb(const __grid_constant__ CUtensorMap mu,
+                                              const __grid_constant__ CUtensorMap mb,
+                                              double* __restrict__ out, Geo g, OpC c,
+                                              double sigma, double omega, double dval, int zc) {
+  constexpr int UX = TX + 4, UY = TY + 4, PU = align16(UX * UY);    // u window, halo 2
+  constexpr int BW = TX + 4, BH = TY + 2, PB = align16(BW * BH);    // b window, halo 1
+  constexpr int RU = PREF + 3, RBB = PREF + 1;
+  constexpr int NRED = (TX + 2) / 2 * (TY + 2);                     // red points of halo-1
+  constexpr int PERR = (NRED + NTHR - 1) / NTHR;
+  extern __shared__ __align__(128) double sm[];
+  double* su = sm;
+  double* sbb = su + RU * PU;
+  unsigned long long* bu = (unsigned long long*)(sbb + RBB * PB);
+  unsigned long long* bbar = bu + RU;
+  const int tid = threadIdx.y * 32 + threadIdx.x;
+  const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TY;
+  const int z0 = blockIdx.z * zc, z1 = min(z0 + zc, g.nz);
+  if (tid == 0) {
+    for (int i = 0; i < RU; ++i) mbar_init(bu + i, 1);
+    for (int i = 0; i < RBB; ++i) mbar_init(bbar + i, 1);
+    fence_barrier_init();
+  }
+  __syncthreads();
+  auto issue = [&](int p) {          // u plane p and b plane p - 1
+    if (p <= z1 + 1) {
+      const int k = p - z0 + 2;
+      mbar_expect(bu + k % RU, UX * UY * 8u);
+      tma3(su + (k % RU) * PU, &mu, x0 - 2, y0 - 2, p, bu + k % RU);
+    }
+    const int q = p - 1;
+    if (q >= z0 - 1 && q <= z1) {
+      const int k = q - z0 + 1;
+      mbar_expect(bbar + k % RBB, BW * BH * 8u);
+      tma3(sbb + (k % RBB) * PB, &mb, x0 - 2, y0 - 1, q, bbar + k % RBB);
+    }
+  };
+  auto wait_u = [&](int p) {
+    const int k = p - z0 + 2;
+    mbar_wait(bu + k % RU, (unsigned)((k / RU) & 1));
+  };
+  auto wait_b = [&](int q) {
+    const int k = q - z0 + 1;
+    mbar_wait(bbar + k % RBB, (unsigned)((k / RBB) & 1));
+  };
+  // red list: window point j -> (yy, xx) with xx = 2 (j % 17) + ((yy + zz + 1) & 1)
+  // (x0, y0 even); per plane parity: u-window index, b-window index, in-domain
+  int r_iu[2][PERR], r_ib[2][PERR];
+  bool r_in[2][PERR];
+#pragma unroll
+  for (int par = 0; par < 2; ++par)
+#pragma unroll
+    for (int q = 0; q < PERR; ++q) {
+      int j = tid + q * NTHR;
+      int yy = j / ((TX + 2) / 2), xr = j - yy * ((TX + 2) / 2);
+      int xx = 2 * xr + ((yy + par + 1) & 1);
+      int gx = x0 - 1 + xx, gy = y0 - 1 + yy;
+      r_iu[par][q] = (yy + 1) * UX + xx + 1;
+      r_ib[par][q] = yy * BW + xx + 1;
+      r_in[par][q] = j < NRED && gx >= 0 && gx < g.nx && gy >= 0 && gy < g.ny;
+    }
+  // black pair: tile row `row`, x = 2 px + {0, 1}; black x has (x + row + z) even
+  const int px = tid & 15, row = tid >> 4;
+  const int gy = y0 + row;
+  auto red_update = [&](int zz) {
+    if (zz < 0 || zz >= g.nz) return;       // ghost planes stay zero
+    const int par = zz & 1;
+    double* pc = su + ((zz - z0 + 2) % RU) * PU;
+    const double* pm = su + ((zz - 1 - z0 + 2 + RU) % RU) * PU;
+    const double* pp = su + ((zz + 1 - z0 + 2) % RU) * PU;
+    const double* pb = sbb + ((zz - z0 + 1) % RBB) * PB;
+#pragma unroll
+    for (int q = 0; q < PERR; ++q) {
+      if (r_in[par][q]) {
+        const int i = r_iu[par][q];
+        const double r = pb[r_ib[par][q]] - (pc[i] - sigma * lap7<POW2, UX>(pm, pc, pp, i, c));
+        pc[i] = pc[i] + ((omega * r) / dval);
+      }
+    }
+  };
+
+  if (tid == 0)
+    for (int p = z0 - 2; p <= z0 + PREF; ++p) issue(p);
+  // prologue: red planes z0-1 (needs u z0-2..z0, b z0-1) and z0
+  for (int p = z0 - 2; p <= z0 + 1; ++p) wait_u(p);
+  wait_b(z0 - 1);
+  wait_b(z0);
+  red_update(z0 - 1);
+  __syncthreads();
+  red_update(z0);
+  for (int z = z0; z < z1; ++z) {
+    wait_u(z + 2);
+    wait_b(z + 1);
+    __syncthreads();                          // red planes <= z complete
+    red_update(z + 1);
+    __syncthreads();
+    const int par = (row + z) & 1;
+    const int xb = 2 * px + par, xr = 2 * px + 1 - par;
+    const double* pm = su + ((z - 1 - z0 + 2 + RU) % RU) * PU;
+    const double* pc = su + ((z - z0 + 2) % RU) * PU;
+    const double* pp = su + ((z + 1 - z0 + 2) % RU) * PU;
+    const double* pb = sbb + ((z - z0 + 1) % RBB) * PB;
+    if (gy < g.ny) {
+      const int gxb = x0 + xb, gxr = x0 + xr;
+      const int ib = (row + 2) * UX + xb + 2;
+      if (gxb < g.nx) {
+        const double rr =
+            pb[(row + 1) * BW + xb + 2] - (pc[ib] - sigma * lap7<POW2, UX>(pm, pc, pp, ib, c));
+        out[g.at(gxb, gy, z)] = pc[ib] + ((omega * rr) / dval);
+      }
+      if (gxr < g.nx) out[g.at(gxr, gy, z)] = pc[(row + 2) * UX + xr + 2];
+    }
+    __syncthreads();   // u plane z-1 and b plane z are free
     if (tid == 0) issue(z + PREF + 1);
   }
 }
@@ -377,7 +508,7 @@ int pick_zc(const Geo& g) {
 template <int OP>
 int launch_z1(const double* u, const double* b, double* out, const Geo& g, const OpC& c,
               double sigma, double omega, double dval, cudaStream_t s) {
-  constexpr int HX = TX + 2, HY = TY + 2, RING = PREF1 + 3;
+  constexpr int HX = TX + 4, HY = TY + 2, RING = PREF1 + 3;
   CUtensorMap mu, mb;
   std::memset(&mu, 0, sizeof(mu));
   std::memset(&mb, 0, sizeof(mb));
@@ -402,13 +533,13 @@ int launch_z1(const double* u, const double* b, double* out, const Geo& g, const
 template <bool RB>
 int launch_z2(const double* u, const double* b, double* out, const Geo& g, const OpC& c,
               double sigma, double omega, double dval, int zero_in, cudaStream_t s) {
-  constexpr int UX = TX + 4, UY = TY + 4, HX = TX + 2, HY = TY + 2;
+  constexpr int UX = TX + 4, UY = TY + 4, HX = TX + 2, HY = TY + 2, BW = TX + 4;
   CUtensorMap mu, mb;
   std::memset(&mu, 0, sizeof(mu));
   if (!zero_in) PL_TRY(make_map(&mu, u, g, UX, UY));
-  PL_TRY(make_map(&mb, b, g, HX, HY));
+  PL_TRY(make_map(&mb, b, g, BW, HY));
   size_t smem = sizeof(double) * ((PREF2 + 3) * align16(UX * UY) +
-                                  (PREF2 + 1) * align16(HX * HY) + 3 * align16(HX * HY)) +
+                                  (PREF2 + 1) * align16(BW * HY) + 3 * align16(HX * HY)) +
                 8 * ((PREF2 + 3) + (PREF2 + 1));
   int zc = pick_zc(g);
   dim3 grid(ceil_div(g.nx, TX), ceil_div(g.ny, TY), ceil_div(g.nz, zc)), block(32, 8);
@@ -419,6 +550,26 @@ int launch_z2(const double* u, const double* b, double* out, const Geo& g, const
     set[c.pow2] = true;
   }
   kern<<<grid, block, smem, s>>>(mu, mb, out, g, c, sigma, omega, dval, zc, zero_in);
+  return 0;
+}
+
+int launch_zrb(const double* u, const double* b, double* out, const Geo& g, const OpC& c,
+               double sigma, double omega, double dval, cudaStream_t s) {
+  constexpr int UX = TX + 4, UY = TY + 4, BW = TX + 4, BH = TY + 2;
+  CUtensorMap mu, mb;
+  PL_TRY(make_map(&mu, u, g, UX, UY));
+  PL_TRY(make_map(&mb, b, g, BW, BH));
+  size_t smem = sizeof(double) * ((PREF2 + 3) * align16(UX * UY) + (PREF2 + 1) * align16(BW * BH)) +
+                8 * ((PREF2 + 3) + (PREF2 + 1));
+  int zc = pick_zc(g);
+  dim3 grid(ceil_div(g.nx, TX), ceil_div(g.ny, TY), ceil_div(g.nz, zc)), block(32, 8);
+  auto kern = c.pow2 ? k_zrb<true, PREF2> : k_zrb<false, PREF2>;
+  static bool set[2] = {false, false};
+  if (!set[c.pow2]) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+    set[c.pow2] = true;
+  }
+  kern<<<grid, block, smem, s>>>(mu, mb, out, g, c, sigma, omega, dval, zc);
   return 0;
 }
 
@@ -479,7 +630,7 @@ int zlaunch_rb(const double* u, const double* b, double* out, const Geo& g, cons
                double sigma, double omega, cudaStream_t s) {
   double dval = zdiag(c, sigma);
   PL_PRE(K_RB);
-  PL_TRY(launch_z2<true>(u, b, out, g, c, sigma, omega, dval, 0, s));
+  PL_TRY(launch_zrb(u, b, out, g, c, sigma, omega, dval, s));
   PL_CHECK_LAUNCH(K_RB, 24.0 * g.npts);
   return 0;
 }
