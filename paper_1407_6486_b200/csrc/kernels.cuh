@@ -31,12 +31,12 @@ int zlaunch_residual(const double* u, const double* b, double* r, const Geo& g, 
                      double sigma, cudaStream_t s);
 int zlaunch_jacobi(const double* u, const double* b, double* out, const Geo& g, const OpC& c,
                    double sigma, double omega, int zero_in, cudaStream_t s);
-// two fused Jacobi sweeps u -> out (out != u)
+// two fused Jacobi sweeps u -> out (out != u); e non-null: u + P_lin e first
 int zlaunch_jacobi2(const double* u, const double* b, double* out, const Geo& g, const OpC& c,
-                    double sigma, double omega, int zero_in, cudaStream_t s);
-// one fused red+black jor-rb sweep u -> out (out != u)
+                    double sigma, double omega, int zero_in, const double* e, cudaStream_t s);
+// one fused red+black jor-rb sweep u -> out (out != u); e non-null: u + P_lin e first
 int zlaunch_rb(const double* u, const double* b, double* out, const Geo& g, const OpC& c,
-               double sigma, double omega, cudaStream_t s);
+               double sigma, double omega, const double* e, cudaStream_t s);
 
 // ---- transfer.cu -----------------------------------------------------------
 // coarse = FW(fine) (transfers.py:27-34); fine geometry gf

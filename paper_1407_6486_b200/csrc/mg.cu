@@ -554,7 +554,8 @@ static int level_smooth(MgPlan* P, MgLevel& L, double** cur, double* alt_u, cons
     int k = 0;
     if (fused) {             // pairs of sweeps in one pass (temporal blocking)
       for (; k + 1 < count; k += 2) {
-        PL_TRY(zlaunch_jacobi2(u, b, other, L.g, L.c, sigma, P->omega, zero && k == 0, s));
+        PL_TRY(zlaunch_jacobi2(u, b, other, L.g, L.c, sigma, P->omega, zero && k == 0, nullptr,
+                               s));
         std::swap(u, other);
       }
     }
@@ -571,7 +572,7 @@ static int level_smooth(MgPlan* P, MgLevel& L, double** cur, double* alt_u, cons
   }
   for (int k = 0; k < count; ++k) {
     if (fused) {            // red and black in one pass, out of place
-      PL_TRY(zlaunch_rb(u, b, other, L.g, L.c, sigma, P->omega, s));
+      PL_TRY(zlaunch_rb(u, b, other, L.g, L.c, sigma, P->omega, nullptr, s));
       std::swap(u, other);
     } else if (P->order == 2) {    // same-colour points never neighbour: in place
       PL_TRY(launch_rb(u, b, u, L.g, L.c, sigma, P->omega, 1, s));
@@ -596,8 +597,23 @@ static int vcycle(MgPlan* P, int l, double* u, const double* b, double sigma, bo
   PL_TRY(launch_residual(cur, b, r, L.g, L.c, sigma, s));
   PL_TRY(launch_fw(r, C.b, L.g, s));
   PL_TRY(vcycle(P, l + 1, C.u, C.b, sigma, true, s));
-  PL_TRY(launch_prolong(C.u, cur, L.g, 1, s));
-  PL_TRY(level_smooth(P, L, &cur, u, b, sigma, P->post, false, s));
+  // u += P e_c, then post-smoothing; fused into the first post-sweep pass
+  // when the TMA kernels cover this level (multigrid.py:250-251)
+  int post = P->post;
+  if (zmarch_ok(L.g, L.c) && P->smoother == SM_RB && post >= 1) {
+    double* other = (cur == u) ? L.t : u;
+    PL_TRY(zlaunch_rb(cur, b, other, L.g, L.c, sigma, P->omega, C.u, s));
+    cur = other;
+    post -= 1;
+  } else if (zmarch_ok(L.g, L.c) && P->smoother == SM_JACOBI && post >= 2) {
+    double* other = (cur == u) ? L.t : u;
+    PL_TRY(zlaunch_jacobi2(cur, b, other, L.g, L.c, sigma, P->omega, 0, C.u, s));
+    cur = other;
+    post -= 2;
+  } else {
+    PL_TRY(launch_prolong(C.u, cur, L.g, 1, s));
+  }
+  PL_TRY(level_smooth(P, L, &cur, u, b, sigma, post, false, s));
   if (cur != u) {
     cudaError_t e = cudaMemcpyAsync(u, cur, sizeof(double) * L.g.nstore,
                                     cudaMemcpyDeviceToDevice, s);

@@ -1,22 +1,28 @@
 // 3-D order-2 stencil kernels fed by TMA ("z-marching").
 //
 // A CTA owns a 32 x 16 (x, y) tile and marches through a chunk of z planes.
-// Each plane window (tile plus a 1- or 2-point halo) arrives in shared memory
-// through one cp.async.bulk.tensor copy issued by a single thread; the
-// tensor map covers only the interior points, so out-of-domain halo points
-// -- the homogeneous Dirichlet ghosts -- are zero-filled by the TMA unit and
-// the padded rows of the device layout are never read.  Copies run PREF
-// planes ahead of the plane being computed and complete on per-slot
-// mbarriers; no SM instruction is spent on address arithmetic for loads.
+// Each plane window (tile plus halo) arrives in shared memory through one
+// cp.async.bulk.tensor copy issued by a single thread; the tensor map covers
+// only the interior points, so out-of-domain halo points -- the homogeneous
+// Dirichlet ghosts -- are zero-filled by the TMA unit and the padded rows of
+// the device layout are never read.  Copies run PREF planes ahead of the
+// plane being computed and complete on per-slot mbarriers.  TMA requires the
+// innermost box start to be 16-byte aligned, so every window starts at the
+// even column x0-2.
 //
-// Fused sweeps (temporal blocking) run two dependent stages in one pass:
-//   k_z2<RB>  one full jor-rb sweep (red on plane z+1 over the halo-1 window,
-//             black on plane z over the tile)
-//   k_z2<Jac> two Jacobi sweeps (sweep 1 on plane z+1 over the halo-1 window,
-//             sweep 2 on plane z)
-// They read u and b once and write u once per pass.  Arithmetic is the
-// reference's expression tree (common.cuh), bit-identical to the unfused
-// kernels; out-of-domain stage-1 points are forced to zero.
+// Kernels
+//   k_z1<op>     one stage: heat apply, residual, or one Jacobi sweep
+//   k_z2<PRO>    two fused Jacobi sweeps (sweep 1 on plane z+1 over the halo-1
+//                window, sweep 2 on plane z)
+//   k_zrb<PRO>   one fused jor-rb sweep: red points of plane z+1 are updated
+//                in place in the staged window (a red point reads only black
+//                neighbours and itself), black points of plane z then read
+//                the updated reds -- no colour divergence inside a warp
+// With PRO (prolongation fused, multigrid.py:250) every staged u plane first
+// receives u += P_lin e_c in shared memory, the coarse correction planes
+// arriving by TMA on the same barriers, so the post-smoother replaces the
+// separate prolongation pass.  Arithmetic is the reference's expression tree
+// (common.cuh / transfer_dev.cuh), bit-identical to the unfused kernels.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -31,7 +37,8 @@ namespace pl {
 namespace {
 
 constexpr int TX = 32, TY = 16;           // output tile
-constexpr int NTHR = 256;                 // 32 x 8 threads, 2 rows each
+constexpr int NTHR = 256;                 // k_z1 / k_z2: 32 x 8 threads, 2 rows each
+constexpr int NTHR_RB = 320;              // k_zrb: one red point of the halo-1 window each
 
 // ---- TMA / mbarrier primitives --------------------------------------------
 
@@ -72,7 +79,7 @@ __device__ __forceinline__ void fence_barrier_init() {
   asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
 }
 
-__host__ __device__ constexpr int align16(int n) { return (n + 15) / 16 * 16; }  // doubles -> 128 B
+__host__ __device__ constexpr int align16(int n) { return (n + 15) / 16 * 16; }  // 128 B
 
 template <bool POW2>
 __device__ __forceinline__ double dd2(double x, const OpC& c) {
@@ -93,24 +100,121 @@ __device__ __forceinline__ double lap7(const double* pm, const double* pc, const
 
 enum { Z_APPLY = 0, Z_RESID = 1, Z_JAC = 2, Z_JAC0 = 3 };
 
+// ---- shared machinery of the halo-2 kernels -------------------------------
+
+constexpr int UX = TX + 4, UY = TY + 4, PU = align16(UX * UY);   // u window (halo 2)
+constexpr int BW = TX + 4, BH = TY + 2, PB = align16(BW * BH);   // b window (halo 1)
+constexpr int CW = TX / 2 + 4, CH = TY / 2 + 3, PC = align16(CW * CH);   // coarse e window
+constexpr int RC = 6;                                                    // coarse ring
+
+// linear interpolation tap along one axis for fine index i (transfers.py:40-45)
+__device__ __forceinline__ void ltap(int i, int& j0, int& j1, bool& two) {
+  if (i & 1) {
+    j0 = (i - 1) >> 1; j1 = j0; two = false;
+  } else {
+    j0 = (i >> 1) - 1; j1 = i >> 1; two = true;
+  }
+}
+__device__ __forceinline__ double lcomb(double a, double b, bool two) {
+  return two ? 0.5 * (a + b) : a;
+}
+
+// u += P_lin e on a staged window plane, separably and in the tree order of
+// transfer_dev.cuh::lin_point (z, then y, then x):
+//   pass B: Y(yy, cx) = lcomb(Z(jy0, cx), Z(jy1, cx), yt(gy)) with
+//           Z(jy, cx) = lcomb(c0[jy][cx], c1[jy][cx], zt)   for the 20 window rows
+//   pass C: w(yy, xx) += lcomb(Y(yy, jx0), Y(yy, jx1), xt(gx))
+// Each thread owns fixed window entries (the (x, y) geometry does not change
+// between planes), precomputed once by ProlongGeo::init.
+constexpr int NYC = UY * CW;      // pass-B entries (fine window rows x coarse window cols)
+
+template <int NT>
+struct ProlongGeo {
+  static constexpr int PB_ = (NYC + NT - 1) / NT;
+  static constexpr int PC_ = (UX * UY + NT - 1) / NT;
+  short b_row[PB_], b_c0[PB_], b_c1[PB_], b_k[PB_];   // Y entry, Z rows (local)
+  bool b_two[PB_], b_ok[PB_];
+  short c_k[PC_], c_y[PC_], c_x0[PC_], c_x1[PC_];
+  bool c_two[PC_], c_ok[PC_];
+
+  __device__ __forceinline__ void init(const Geo& g, int x0, int y0, int cy0, int cx0, int tid) {
+#pragma unroll
+    for (int q = 0; q < PB_; ++q) {
+      const int k = tid + q * NT;
+      const int yy = k / CW;
+      const int gy = y0 - 2 + yy;
+      int j0, j1;
+      bool two;
+      ltap(gy, j0, j1, two);
+      b_k[q] = (short)k;
+      b_row[q] = (short)yy;
+      b_c0[q] = (short)(j0 - cy0);
+      b_c1[q] = (short)(j1 - cy0);
+      b_two[q] = two;
+      b_ok[q] = k < NYC && gy >= 0 && gy < g.ny;
+    }
+#pragma unroll
+    for (int q = 0; q < PC_; ++q) {
+      const int k = tid + q * NT;
+      const int yy = k / UX, xx = k - yy * UX;
+      const int gx = x0 - 2 + xx, gy = y0 - 2 + yy;
+      int j0, j1;
+      bool two;
+      ltap(gx, j0, j1, two);
+      c_k[q] = (short)k;
+      c_y[q] = (short)yy;
+      c_x0[q] = (short)(j0 - cx0);
+      c_x1[q] = (short)(j1 - cx0);
+      c_two[q] = two;
+      c_ok[q] = k < UX * UY && gx >= 0 && gx < g.nx && gy >= 0 && gy < g.ny;
+    }
+  }
+
+  // two passes with a barrier between; the caller syncs after
+  __device__ __forceinline__ void apply(double* w, double* ybuf, const double* c0,
+                                        const double* c1, bool zt) const {
+#pragma unroll
+    for (int q = 0; q < PB_; ++q) {
+      if (b_k[q] < NYC) {
+        double v = 0.0;
+        if (b_ok[q]) {
+          const int cx = b_k[q] - b_row[q] * CW;
+          const int i0 = b_c0[q] * CW + cx, i1 = b_c1[q] * CW + cx;
+          const double z0 = lcomb(c0[i0], zt ? c1[i0] : 0.0, zt);
+          const double z1 = b_two[q] ? lcomb(c0[i1], zt ? c1[i1] : 0.0, zt) : 0.0;
+          v = lcomb(z0, z1, b_two[q]);
+        }
+        ybuf[b_k[q]] = v;
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < PC_; ++q) {
+      if (c_ok[q]) {
+        const double* yr = ybuf + c_y[q] * CW;
+        const double v = lcomb(yr[c_x0[q]], c_two[q] ? yr[c_x1[q]] : 0.0, c_two[q]);
+        w[c_k[q]] = w[c_k[q]] + v;
+      }
+    }
+  }
+};
+
 // ---------------------------------------------------------------------------
-// single-stage kernels: apply, residual, one Jacobi sweep
+// single-stage kernels: apply, residual, one Jacobi sweep (halo-1 window)
 
 template <int OP, bool POW2, int PREF>
 __global__ void __launch_bounds__(NTHR) k_z1(const __grid_constant__ CUtensorMap mu,
                                              const __grid_constant__ CUtensorMap mb,
                                              double* __restrict__ out, Geo g, OpC c,
                                              double sigma, double omega, double dval, int zc) {
-  // TMA needs the innermost box start 16-byte aligned: windows start at the
-  // even column x0-2 (one extra column on the left, unused)
-  constexpr int HX = TX + 4, HY = TY + 2, PU = align16(HX * HY), PB = align16(TX * TY);
+  constexpr int HX = TX + 4, HY = TY + 2, P1 = align16(HX * HY), P0 = align16(TX * TY);
   constexpr int RING = PREF + 3;
   constexpr bool NEED_U = OP != Z_JAC0;
   constexpr bool NEED_B = OP != Z_APPLY;
   extern __shared__ __align__(128) double sm[];
   double* su = sm;
-  double* sb = sm + (NEED_U ? RING * PU : 0);
-  unsigned long long* bar = (unsigned long long*)(sb + (NEED_B ? RING * PB : 0));
+  double* sb = sm + (NEED_U ? RING * P1 : 0);
+  unsigned long long* bar = (unsigned long long*)(sb + (NEED_B ? RING * P0 : 0));
   const int tid = threadIdx.y * 32 + threadIdx.x;
   const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TY;
   const int z0 = blockIdx.z * zc, z1 = min(z0 + zc, g.nz);
@@ -131,8 +235,8 @@ __global__ void __launch_bounds__(NTHR) k_z1(const __grid_constant__ CUtensorMap
       return;
     }
     mbar_expect(bar + slot, (wu ? HX * HY * 8u : 0u) + (wb ? TX * TY * 8u : 0u));
-    if (wu) tma3(su + slot * PU, &mu, x0 - 2, y0 - 1, p, bar + slot);
-    if (wb) tma3(sb + slot * PB, &mb, x0, y0, p, bar + slot);
+    if (wu) tma3(su + slot * P1, &mu, x0 - 2, y0 - 1, p, bar + slot);
+    if (wb) tma3(sb + slot * P0, &mb, x0, y0, p, bar + slot);
   };
   auto wait = [&](int p) {
     const int k = p - z0 + 1;
@@ -146,10 +250,10 @@ __global__ void __launch_bounds__(NTHR) k_z1(const __grid_constant__ CUtensorMap
   for (int z = z0; z < z1; ++z) {
     wait(z + 1);
     const int sc = (z - z0 + 1) % RING;
-    const double* pc = su + sc * PU;
-    const double* pm = su + ((z - z0) % RING) * PU;
-    const double* pp = su + ((z - z0 + 2) % RING) * PU;
-    const double* pb = sb + sc * PB;
+    const double* pc = su + sc * P1;
+    const double* pm = su + ((z - z0) % RING) * P1;
+    const double* pp = su + ((z - z0 + 2) % RING) * P1;
+    const double* pb = sb + sc * P0;
 #pragma unroll
     for (int r = 0; r < 2; ++r) {
       const int ly = threadIdx.y + 8 * r;
@@ -178,66 +282,125 @@ __global__ void __launch_bounds__(NTHR) k_z1(const __grid_constant__ CUtensorMap
 }
 
 // ---------------------------------------------------------------------------
-// fused two-stage kernels.  Input u window has halo 2, stage 1 and b halo 1.
+// fused two-stage kernels (halo-2 u window, halo-1 b window)
+//
+// u plane p (z0-2 <= p <= z1+1): slot (p - z0 + 2) % RU
+// b plane q (z0-1 <= q <= z1):   slot (q - z0 + 1) % RBB, arrives with u plane q+1
+// coarse plane j: slot (j - jlo) % RC, arrives with u plane 2j (and the
+//                 first plane z0-2 also brings j = jlo = (z0-2)/2 - 1)
 
-template <bool RB, bool POW2, int PREF>
-__global__ void __launch_bounds__(NTHR) k_z2(const __grid_constant__ CUtensorMap mu,
-                                             const __grid_constant__ CUtensorMap mb,
-                                             double* __restrict__ out, Geo g, OpC c,
-                                             double sigma, double omega, double dval, int zc,
-                                             int zero_in) {
-  constexpr int UX = TX + 4, UY = TY + 4, PU = align16(UX * UY);    // input, halo 2
-  constexpr int HX = TX + 2, HY = TY + 2, PH = align16(HX * HY);    // stage 1, halo 1
-  constexpr int NH = HX * HY;
-  constexpr int BW = TX + 4, PBW = align16(BW * HY);   // b window from the even column x0-2
-  constexpr int RU = PREF + 3;    // u planes z0-2 .. z0+PREF staged in the prologue
-  constexpr int RBB = PREF + 1;   // b planes
-  extern __shared__ __align__(128) double sm[];
-  double* su = sm;                        // RU * PU
-  double* sbb = su + RU * PU;             // RBB * PBW
-  double* s1 = sbb + RBB * PBW;           // 3 * PH  stage-1 planes z-1, z, z+1
-  unsigned long long* bu = (unsigned long long*)(s1 + 3 * PH);
-  unsigned long long* bbar = bu + RU;
-  const int tid = threadIdx.y * 32 + threadIdx.x;
-  const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TY;
-  const int z0 = blockIdx.z * zc, z1 = min(z0 + zc, g.nz);
-  if (tid == 0) {
-    for (int i = 0; i < RU; ++i) mbar_init(bu + i, 1);
-    for (int i = 0; i < RBB; ++i) mbar_init(bbar + i, 1);
-    fence_barrier_init();
+template <int NT, bool PRO, int PREF>
+struct Stager {
+  static constexpr int RU = PREF + 3, RBB = PREF + 1;
+  double *su, *sbb, *se, *ybuf;
+  ProlongGeo<NT> pg;
+  unsigned long long *bu, *bbar;
+  const CUtensorMap *mu, *mb, *me;
+  int x0, y0, z0, z1, jlo, cx0, cy0;
+
+  __device__ __forceinline__ void setup(double* sm, const CUtensorMap* mu_,
+                                        const CUtensorMap* mb_, const CUtensorMap* me_, int zc,
+                                        const Geo& g, int tid) {
+    su = sm;
+    sbb = su + RU * PU;
+    se = sbb + RBB * PB;
+    ybuf = se + (PRO ? RC * PC : 0);
+    bu = (unsigned long long*)(ybuf + (PRO ? align16(NYC) : 0));
+    bbar = bu + RU;
+    mu = mu_;
+    mb = mb_;
+    me = me_;
+    x0 = blockIdx.x * TX;
+    y0 = blockIdx.y * TY;
+    z0 = blockIdx.z * zc;
+    z1 = min(z0 + zc, g.nz);
+    jlo = (z0 - 2) / 2 - 1;    // z0 is even: exact
+    cx0 = x0 / 2 - 2;
+    cy0 = y0 / 2 - 2;
+    if (PRO) pg.init(g, x0, y0, cy0, cx0, tid);
+    if (tid == 0) {
+      for (int i = 0; i < RU; ++i) mbar_init(bu + i, 1);
+      for (int i = 0; i < RBB; ++i) mbar_init(bbar + i, 1);
+      fence_barrier_init();
+    }
+    __syncthreads();
   }
-  __syncthreads();
-  // u plane p (z0-2 <= p <= z1+1): slot (p - z0 + 2) % RU
-  // b plane q (z0-1 <= q <= z1):   slot (q - z0 + 1) % RBB
-  auto issue = [&](int p) {          // u plane p and b plane p - 1
+  __device__ __forceinline__ double* uplane(int p) const { return su + ((p - z0 + 2) % RU) * PU; }
+  __device__ __forceinline__ const double* bplane(int q) const {
+    return sbb + ((q - z0 + 1) % RBB) * PB;
+  }
+  __device__ __forceinline__ const double* eplane(int j) const {
+    return se + ((j - jlo) % RC) * PC;
+  }
+  __device__ __forceinline__ void issue(int p, bool zero_u) {   // thread 0 only
     if (p <= z1 + 1) {
       const int k = p - z0 + 2;
-      if (zero_in) {
+      unsigned bytes = zero_u ? 0u : UX * UY * 8u;
+      int ne = 0, js[2];
+      if (PRO && !zero_u && (p & 1) == 0) {
+        if (p == z0 - 2) js[ne++] = jlo;
+        js[ne++] = p / 2;
+        bytes += ne * CW * CH * 8u;
+      }
+      if (bytes == 0) {
         mbar_arrive(bu + k % RU);
       } else {
-        mbar_expect(bu + k % RU, UX * UY * 8u);
-        tma3(su + (k % RU) * PU, &mu, x0 - 2, y0 - 2, p, bu + k % RU);
+        mbar_expect(bu + k % RU, bytes);
+        if (!zero_u) tma3(su + (k % RU) * PU, mu, x0 - 2, y0 - 2, p, bu + k % RU);
+        for (int e = 0; e < ne; ++e)
+          tma3(se + ((js[e] - jlo) % RC) * PC, me, cx0, cy0, js[e], bu + k % RU);
       }
     }
     const int q = p - 1;
     if (q >= z0 - 1 && q <= z1) {
       const int k = q - z0 + 1;
-      mbar_expect(bbar + k % RBB, BW * HY * 8u);
-      tma3(sbb + (k % RBB) * PBW, &mb, x0 - 2, y0 - 1, q, bbar + k % RBB);
+      mbar_expect(bbar + k % RBB, BW * BH * 8u);
+      tma3(sbb + (k % RBB) * PB, mb, x0 - 2, y0 - 1, q, bbar + k % RBB);
     }
-  };
-  auto wait_u = [&](int p) {
+  }
+  __device__ __forceinline__ void wait_u(int p) const {
     const int k = p - z0 + 2;
     mbar_wait(bu + k % RU, (unsigned)((k / RU) & 1));
-  };
-  auto wait_b = [&](int q) {
+  }
+  __device__ __forceinline__ void wait_b(int q) const {
     const int k = q - z0 + 1;
     mbar_wait(bbar + k % RBB, (unsigned)((k / RBB) & 1));
-  };
+  }
+  // prolongation of staged u plane p (after wait_u(p), before any use)
+  // prolongation of staged u plane p (after wait_u(p), before any use); all
+  // threads, contains a barrier -- the plane is usable after the next one
+  __device__ __forceinline__ void prolong(int p, const Geo& g) {
+    if (!PRO || p < 0 || p >= g.nz) return;
+    int jz0, jz1;
+    bool zt;
+    ltap(p, jz0, jz1, zt);
+    pg.apply(uplane(p), ybuf, eplane(jz0), eplane(jz1), zt);
+  }
+  __host__ __device__ static constexpr size_t smem_doubles() {
+    return (size_t)RU * PU + RBB * PB + (PRO ? RC * PC + align16(NYC) : 0);
+  }
+  __host__ __device__ static constexpr size_t smem_bytes() { return smem_doubles() * 8 + 8 * (RU + RBB); }
+};
 
-  // each thread owns the same <= 3 stage-1 window points on every plane
+// two fused Jacobi sweeps (optionally after the prolongation)
+template <bool POW2, bool PRO, int PREF>
+__global__ void __launch_bounds__(NTHR) k_z2(const __grid_constant__ CUtensorMap mu,
+                                             const __grid_constant__ CUtensorMap mb,
+                                             const __grid_constant__ CUtensorMap me,
+                                             double* __restrict__ out, Geo g, OpC c,
+                                             double sigma, double omega, double dval, int zc,
+                                             int zero_in) {
+  constexpr int HX = TX + 2, HY = TY + 2, PH = align16(HX * HY), NH = HX * HY;
+  using S = Stager<NTHR, PRO, PREF>;
+  extern __shared__ __align__(128) double sm[];
+  const int tid = threadIdx.y * 32 + threadIdx.x;
+  S st;
+  st.setup(sm, &mu, &mb, &me, zc, g, tid);
+  double* s1 = sm + S::smem_doubles() + 16;     // after the (<= 16) barriers
+  const int x0 = st.x0, y0 = st.y0, z0 = st.z0, z1 = st.z1;
+
   constexpr int PER1 = (NH + NTHR - 1) / NTHR;
-  int e_k[PER1], e_i[PER1], e_b[PER1], e_par[PER1];
+  int e_k[PER1], e_i[PER1], e_b[PER1];
   bool e_in[PER1];
 #pragma unroll
   for (int q = 0; q < PER1; ++q) {
@@ -248,15 +411,15 @@ __global__ void __launch_bounds__(NTHR) k_z2(const __grid_constant__ CUtensorMap
     e_i[q] = (yy + 1) * UX + xx + 1;
     e_b[q] = yy * BW + xx + 1;
     e_in[q] = k < NH && gxx >= 0 && gxx < g.nx && gyy >= 0 && gyy < g.ny;
-    e_par[q] = (gxx + gyy + 3) & 1;
   }
+  // sweep 1 at plane zz over the halo-1 window (0 outside the domain)
   auto stage1 = [&](int zz) {
     double* dst = s1 + ((zz - z0 + 3) % 3) * PH;
     const bool zin = zz >= 0 && zz < g.nz;
-    const double* pm = su + ((zz - 1 - z0 + 2 + RU) % RU) * PU;
-    const double* pc = su + ((zz - z0 + 2) % RU) * PU;
-    const double* pp = su + ((zz + 1 - z0 + 2) % RU) * PU;
-    const double* pb = sbb + ((zz - z0 + 1) % RBB) * PBW;
+    const double* pm = st.uplane(zz - 1);
+    const double* pc = st.uplane(zz);
+    const double* pp = st.uplane(zz + 1);
+    const double* pb = st.bplane(zz);
 #pragma unroll
     for (int q = 0; q < PER1; ++q) {
       const int k = e_k[q];
@@ -264,16 +427,8 @@ __global__ void __launch_bounds__(NTHR) k_z2(const __grid_constant__ CUtensorMap
         double v = 0.0;
         if (zin && e_in[q]) {
           const int i = e_i[q];
-          double b = pb[e_b[q]];
-          if (RB) {
-            bool red = ((e_par[q] + zz) & 1) == 0;
-            if (red) {
-              double r = b - (pc[i] - sigma * lap7<POW2, UX>(pm, pc, pp, i, c));
-              v = pc[i] + ((omega * r) / dval);
-            } else {
-              v = pc[i];
-            }
-          } else if (zero_in) {
+          const double b = pb[e_b[q]];
+          if (zero_in) {
             v = 0.0 + ((omega * b) / dval);
           } else {
             double au = pc[i] - sigma * lap7<POW2, UX>(pm, pc, pp, i, c);
@@ -286,23 +441,31 @@ __global__ void __launch_bounds__(NTHR) k_z2(const __grid_constant__ CUtensorMap
   };
 
   if (tid == 0)
-    for (int p = z0 - 2; p <= z0 + PREF; ++p) issue(p);
-  // prologue: stage-1 planes z0-1, z0 need u z0-2 .. z0+1 and b z0-1, z0
-  for (int p = z0 - 2; p <= z0 + 1; ++p) wait_u(p);
-  wait_b(z0 - 1);
-  wait_b(z0);
+    for (int p = z0 - 2; p <= z0 + PREF; ++p) st.issue(p, zero_in);
+  for (int p = z0 - 2; p <= z0 + 1; ++p) {
+    st.wait_u(p);
+    __syncthreads();
+    st.prolong(p, g);
+  }
+  st.wait_b(z0 - 1);
+  st.wait_b(z0);
+  __syncthreads();
   stage1(z0 - 1);
   stage1(z0);
   const int gx = x0 + threadIdx.x;
   for (int z = z0; z < z1; ++z) {
-    wait_u(z + 2);
-    wait_b(z + 1);
+    st.wait_u(z + 2);
+    st.wait_b(z + 1);
+    if (PRO) {
+      st.prolong(z + 2, g);
+      __syncthreads();
+    }
     stage1(z + 1);
     __syncthreads();
     const double* qm = s1 + ((z - 1 - z0 + 3) % 3) * PH;
     const double* qc = s1 + ((z - z0 + 3) % 3) * PH;
     const double* qp = s1 + ((z + 1 - z0 + 3) % 3) * PH;
-    const double* pb = sbb + ((z - z0 + 1) % RBB) * PBW;
+    const double* pb = st.bplane(z);
 #pragma unroll
     for (int r = 0; r < 2; ++r) {
       const int ly = threadIdx.y + 8 * r;
@@ -310,81 +473,31 @@ __global__ void __launch_bounds__(NTHR) k_z2(const __grid_constant__ CUtensorMap
       if (gx < g.nx && gy < g.ny) {
         const int i = (ly + 1) * HX + threadIdx.x + 1;
         const int ib = (ly + 1) * BW + threadIdx.x + 2;
-        double v;
-        if (RB) {
-          bool red = ((gx + gy + z + 3) & 1) == 0;
-          if (red) {
-            v = qc[i];
-          } else {
-            double rr = pb[ib] - (qc[i] - sigma * lap7<POW2, HX>(qm, qc, qp, i, c));
-            v = qc[i] + ((omega * rr) / dval);
-          }
-        } else {
-          double au = qc[i] - sigma * lap7<POW2, HX>(qm, qc, qp, i, c);
-          v = qc[i] + ((omega * (pb[ib] - au)) / dval);
-        }
-        out[g.at(gx, gy, z)] = v;
+        double au = qc[i] - sigma * lap7<POW2, HX>(qm, qc, qp, i, c);
+        out[g.at(gx, gy, z)] = qc[i] + ((omega * (pb[ib] - au)) / dval);
       }
     }
-    __syncthreads();   // u plane z, b plane z and stage-1 plane z-1 are free
-    if (tid == 0) issue(z + PREF + 1);
+    __syncthreads();   // u plane z-1, b plane z and stage-1 plane z-1 are free
+    if (tid == 0) st.issue(z + PREF + 1, zero_in);
   }
 }
 
-// ---------------------------------------------------------------------------
-// one full jor-rb sweep in one pass, divergence-free.  With the 7-point
-// stencil a red point reads only black neighbours and its own old value, so
-// the red update of plane z+1 is done IN PLACE in the staged u window (no
-// copy of black points); the black update of plane z then reads the updated
-// red neighbours straight from the window.  Red work is a dense list of the
-// window's red points (17 per row); black work gives every thread one
-// (black, red) x-pair of a tile row, so no warp branches on colour.
-
-template <bool POW2, int PREF>
-__global__ void __launch_bounds__(NTHR) k_zrb(const __grid_constant__ CUtensorMap mu,
-                                              const __grid_constant__ CUtensorMap mb,
-                                              double* __restrict__ out, Geo g, OpC c,
-                                              double sigma, double omega, double dval, int zc) {
-  constexpr int UX = TX + 4, UY = TY + 4, PU = align16(UX * UY);    // u window, halo 2
-  constexpr int BW = TX + 4, BH = TY + 2, PB = align16(BW * BH);    // b window, halo 1
-  constexpr int RU = PREF + 3, RBB = PREF + 1;
+// one fused jor-rb sweep (optionally after the prolongation)
+template <bool POW2, bool PRO, int PREF>
+__global__ void __launch_bounds__(NTHR_RB) k_zrb(const __grid_constant__ CUtensorMap mu,
+                                                 const __grid_constant__ CUtensorMap mb,
+                                                 const __grid_constant__ CUtensorMap me,
+                                                 double* __restrict__ out, Geo g, OpC c,
+                                                 double sigma, double omega, double dval,
+                                                 int zc) {
+  using S = Stager<NTHR_RB, PRO, PREF>;
   constexpr int NRED = (TX + 2) / 2 * (TY + 2);                     // red points of halo-1
-  constexpr int PERR = (NRED + NTHR - 1) / NTHR;
+  constexpr int PERR = (NRED + NTHR_RB - 1) / NTHR_RB;
   extern __shared__ __align__(128) double sm[];
-  double* su = sm;
-  double* sbb = su + RU * PU;
-  unsigned long long* bu = (unsigned long long*)(sbb + RBB * PB);
-  unsigned long long* bbar = bu + RU;
-  const int tid = threadIdx.y * 32 + threadIdx.x;
-  const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TY;
-  const int z0 = blockIdx.z * zc, z1 = min(z0 + zc, g.nz);
-  if (tid == 0) {
-    for (int i = 0; i < RU; ++i) mbar_init(bu + i, 1);
-    for (int i = 0; i < RBB; ++i) mbar_init(bbar + i, 1);
-    fence_barrier_init();
-  }
-  __syncthreads();
-  auto issue = [&](int p) {          // u plane p and b plane p - 1
-    if (p <= z1 + 1) {
-      const int k = p - z0 + 2;
-      mbar_expect(bu + k % RU, UX * UY * 8u);
-      tma3(su + (k % RU) * PU, &mu, x0 - 2, y0 - 2, p, bu + k % RU);
-    }
-    const int q = p - 1;
-    if (q >= z0 - 1 && q <= z1) {
-      const int k = q - z0 + 1;
-      mbar_expect(bbar + k % RBB, BW * BH * 8u);
-      tma3(sbb + (k % RBB) * PB, &mb, x0 - 2, y0 - 1, q, bbar + k % RBB);
-    }
-  };
-  auto wait_u = [&](int p) {
-    const int k = p - z0 + 2;
-    mbar_wait(bu + k % RU, (unsigned)((k / RU) & 1));
-  };
-  auto wait_b = [&](int q) {
-    const int k = q - z0 + 1;
-    mbar_wait(bbar + k % RBB, (unsigned)((k / RBB) & 1));
-  };
+  const int tid = threadIdx.x;
+  S st;
+  st.setup(sm, &mu, &mb, &me, zc, g, tid);
+  const int x0 = st.x0, y0 = st.y0, z0 = st.z0, z1 = st.z1;
   // red list: window point j -> (yy, xx) with xx = 2 (j % 17) + ((yy + zz + 1) & 1)
   // (x0, y0 even); per plane parity: u-window index, b-window index, in-domain
   int r_iu[2][PERR], r_ib[2][PERR];
@@ -393,7 +506,7 @@ __global__ void __launch_bounds__(NTHR) k_zrb(const __grid_constant__ CUtensorMa
   for (int par = 0; par < 2; ++par)
 #pragma unroll
     for (int q = 0; q < PERR; ++q) {
-      int j = tid + q * NTHR;
+      int j = tid + q * NTHR_RB;
       int yy = j / ((TX + 2) / 2), xr = j - yy * ((TX + 2) / 2);
       int xx = 2 * xr + ((yy + par + 1) & 1);
       int gx = x0 - 1 + xx, gy = y0 - 1 + yy;
@@ -407,10 +520,10 @@ __global__ void __launch_bounds__(NTHR) k_zrb(const __grid_constant__ CUtensorMa
   auto red_update = [&](int zz) {
     if (zz < 0 || zz >= g.nz) return;       // ghost planes stay zero
     const int par = zz & 1;
-    double* pc = su + ((zz - z0 + 2) % RU) * PU;
-    const double* pm = su + ((zz - 1 - z0 + 2 + RU) % RU) * PU;
-    const double* pp = su + ((zz + 1 - z0 + 2) % RU) * PU;
-    const double* pb = sbb + ((zz - z0 + 1) % RBB) * PB;
+    double* pc = st.uplane(zz);
+    const double* pm = st.uplane(zz - 1);
+    const double* pp = st.uplane(zz + 1);
+    const double* pb = st.bplane(zz);
 #pragma unroll
     for (int q = 0; q < PERR; ++q) {
       if (r_in[par][q]) {
@@ -422,27 +535,35 @@ __global__ void __launch_bounds__(NTHR) k_zrb(const __grid_constant__ CUtensorMa
   };
 
   if (tid == 0)
-    for (int p = z0 - 2; p <= z0 + PREF; ++p) issue(p);
-  // prologue: red planes z0-1 (needs u z0-2..z0, b z0-1) and z0
-  for (int p = z0 - 2; p <= z0 + 1; ++p) wait_u(p);
-  wait_b(z0 - 1);
-  wait_b(z0);
+    for (int p = z0 - 2; p <= z0 + PREF; ++p) st.issue(p, false);
+  for (int p = z0 - 2; p <= z0 + 1; ++p) {
+    st.wait_u(p);
+    __syncthreads();
+    st.prolong(p, g);
+  }
+  st.wait_b(z0 - 1);
+  st.wait_b(z0);
+  __syncthreads();
   red_update(z0 - 1);
   __syncthreads();
   red_update(z0);
   for (int z = z0; z < z1; ++z) {
-    wait_u(z + 2);
-    wait_b(z + 1);
-    __syncthreads();                          // red planes <= z complete
+    st.wait_u(z + 2);
+    st.wait_b(z + 1);
+    if (PRO) {
+      st.prolong(z + 2, g);
+      __syncthreads();
+    }
+    // red(z+1) reads only black points of planes z..z+2 and its own centre
     red_update(z + 1);
     __syncthreads();
     const int par = (row + z) & 1;
     const int xb = 2 * px + par, xr = 2 * px + 1 - par;
-    const double* pm = su + ((z - 1 - z0 + 2 + RU) % RU) * PU;
-    const double* pc = su + ((z - z0 + 2) % RU) * PU;
-    const double* pp = su + ((z + 1 - z0 + 2) % RU) * PU;
-    const double* pb = sbb + ((z - z0 + 1) % RBB) * PB;
-    if (gy < g.ny) {
+    const double* pm = st.uplane(z - 1);
+    const double* pc = st.uplane(z);
+    const double* pp = st.uplane(z + 1);
+    const double* pb = st.bplane(z);
+    if (tid < 16 * TY && gy < g.ny) {
       const int gxb = x0 + xb, gxr = x0 + xr;
       const int ib = (row + 2) * UX + xb + 2;
       if (gxb < g.nx) {
@@ -453,7 +574,7 @@ __global__ void __launch_bounds__(NTHR) k_zrb(const __grid_constant__ CUtensorMa
       if (gxr < g.nx) out[g.at(gxr, gy, z)] = pc[(row + 2) * UX + xr + 2];
     }
     __syncthreads();   // u plane z-1 and b plane z are free
-    if (tid == 0) issue(z + PREF + 1);
+    if (tid == 0) st.issue(z + PREF + 1, false);
   }
 }
 
@@ -498,11 +619,16 @@ int make_map(CUtensorMap* m, const double* base, const Geo& g, int bw, int bh) {
 
 int pick_zc(const Geo& g) {
   // enough CTAs for several waves on 148 SMs; chunk halo planes cost
-  // (2 or 4)/zc extra L2 reads
+  // (2 or 4)/zc extra L2 reads; zc even (the prolongation pairs planes)
   long long tiles = (long long)ceil_div(g.nx, TX) * ceil_div(g.ny, TY);
   int zc = 64;
   while (zc > 16 && tiles * ceil_div(g.nz, zc) < 148 * 8) zc /= 2;
   return zc;
+}
+
+template <typename K>
+void raise_smem(K kern, size_t bytes) {
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
 }
 
 template <int OP>
@@ -521,55 +647,63 @@ int launch_z1(const double* u, const double* b, double* out, const Geo& g, const
   int zc = pick_zc(g);
   dim3 grid(ceil_div(g.nx, TX), ceil_div(g.ny, TY), ceil_div(g.nz, zc)), block(32, 8);
   auto kern = c.pow2 ? k_z1<OP, true, PREF1> : k_z1<OP, false, PREF1>;
-  static bool set[2] = {false, false};
-  if (!set[c.pow2]) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
-    set[c.pow2] = true;
-  }
+  raise_smem(kern, smem);
   kern<<<grid, block, smem, s>>>(mu, mb, out, g, c, sigma, omega, dval, zc);
   return 0;
 }
 
-template <bool RB>
-int launch_z2(const double* u, const double* b, double* out, const Geo& g, const OpC& c,
-              double sigma, double omega, double dval, int zero_in, cudaStream_t s) {
-  constexpr int UX = TX + 4, UY = TY + 4, HX = TX + 2, HY = TY + 2, BW = TX + 4;
-  CUtensorMap mu, mb;
+// e (coarse correction, geometry gc) non-null: prolongation fused
+int launch_z2(const double* u, const double* b, const double* e, const Geo& gc, double* out,
+              const Geo& g, const OpC& c, double sigma, double omega, double dval, int zero_in,
+              cudaStream_t s) {
+  constexpr int HX = TX + 2, HY = TY + 2;
+  CUtensorMap mu, mb, me;
   std::memset(&mu, 0, sizeof(mu));
+  std::memset(&me, 0, sizeof(me));
   if (!zero_in) PL_TRY(make_map(&mu, u, g, UX, UY));
-  PL_TRY(make_map(&mb, b, g, BW, HY));
-  size_t smem = sizeof(double) * ((PREF2 + 3) * align16(UX * UY) +
-                                  (PREF2 + 1) * align16(BW * HY) + 3 * align16(HX * HY)) +
-                8 * ((PREF2 + 3) + (PREF2 + 1));
+  PL_TRY(make_map(&mb, b, g, BW, BH));
+  if (e) PL_TRY(make_map(&me, e, gc, CW, CH));
   int zc = pick_zc(g);
   dim3 grid(ceil_div(g.nx, TX), ceil_div(g.ny, TY), ceil_div(g.nz, zc)), block(32, 8);
-  auto kern = c.pow2 ? k_z2<RB, true, PREF2> : k_z2<RB, false, PREF2>;
-  static bool set[2] = {false, false};
-  if (!set[c.pow2]) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
-    set[c.pow2] = true;
+#define PL_Z2(P2, PRO)                                                                  \
+  do {                                                                                 \
+    size_t smem = (Stager<NTHR, PRO, PREF2>::smem_doubles() + 16 + 3 * align16(HX * HY)) * 8; \
+    auto kern = k_z2<P2, PRO, PREF2>;                                                  \
+    raise_smem(kern, smem);                                                            \
+    kern<<<grid, block, smem, s>>>(mu, mb, me, out, g, c, sigma, omega, dval, zc, zero_in); \
+  } while (0)
+  if (c.pow2) {
+    if (e) PL_Z2(true, true); else PL_Z2(true, false);
+  } else {
+    if (e) PL_Z2(false, true); else PL_Z2(false, false);
   }
-  kern<<<grid, block, smem, s>>>(mu, mb, out, g, c, sigma, omega, dval, zc, zero_in);
+#undef PL_Z2
   return 0;
 }
 
-int launch_zrb(const double* u, const double* b, double* out, const Geo& g, const OpC& c,
-               double sigma, double omega, double dval, cudaStream_t s) {
-  constexpr int UX = TX + 4, UY = TY + 4, BW = TX + 4, BH = TY + 2;
-  CUtensorMap mu, mb;
+int launch_zrb(const double* u, const double* b, const double* e, const Geo& gc, double* out,
+               const Geo& g, const OpC& c, double sigma, double omega, double dval,
+               cudaStream_t s) {
+  CUtensorMap mu, mb, me;
+  std::memset(&me, 0, sizeof(me));
   PL_TRY(make_map(&mu, u, g, UX, UY));
   PL_TRY(make_map(&mb, b, g, BW, BH));
-  size_t smem = sizeof(double) * ((PREF2 + 3) * align16(UX * UY) + (PREF2 + 1) * align16(BW * BH)) +
-                8 * ((PREF2 + 3) + (PREF2 + 1));
+  if (e) PL_TRY(make_map(&me, e, gc, CW, CH));
   int zc = pick_zc(g);
-  dim3 grid(ceil_div(g.nx, TX), ceil_div(g.ny, TY), ceil_div(g.nz, zc)), block(32, 8);
-  auto kern = c.pow2 ? k_zrb<true, PREF2> : k_zrb<false, PREF2>;
-  static bool set[2] = {false, false};
-  if (!set[c.pow2]) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
-    set[c.pow2] = true;
+  dim3 grid(ceil_div(g.nx, TX), ceil_div(g.ny, TY), ceil_div(g.nz, zc));
+#define PL_ZRB(P2, PRO)                                                             \
+  do {                                                                             \
+    size_t smem = Stager<NTHR_RB, PRO, PREF2>::smem_bytes();                       \
+    auto kern = k_zrb<P2, PRO, PREF2>;                                             \
+    raise_smem(kern, smem);                                                        \
+    kern<<<grid, dim3(NTHR_RB), smem, s>>>(mu, mb, me, out, g, c, sigma, omega, dval, zc); \
+  } while (0)
+  if (c.pow2) {
+    if (e) PL_ZRB(true, true); else PL_ZRB(true, false);
+  } else {
+    if (e) PL_ZRB(false, true); else PL_ZRB(false, false);
   }
-  kern<<<grid, block, smem, s>>>(mu, mb, out, g, c, sigma, omega, dval, zc);
+#undef PL_ZRB
   return 0;
 }
 
@@ -617,21 +751,24 @@ int zlaunch_jacobi(const double* u, const double* b, double* out, const Geo& g, 
 }
 
 int zlaunch_jacobi2(const double* u, const double* b, double* out, const Geo& g, const OpC& c,
-                    double sigma, double omega, int zero_in, cudaStream_t s) {
+                    double sigma, double omega, int zero_in, const double* e, cudaStream_t s) {
   double dval = zdiag(c, sigma);
+  Geo gc = make_geo(3, (g.N + 1) / 2);
   PL_PRE(K_JACOBI);
-  PL_TRY(launch_z2<false>(u, b, out, g, c, sigma, omega, dval, zero_in, s));
-  // algorithmic bytes of the two unfused sweeps it replaces
-  PL_CHECK_LAUNCH(K_JACOBI, (zero_in ? 40.0 : 48.0) * g.npts);
+  PL_TRY(launch_z2(u, b, e, gc, out, g, c, sigma, omega, dval, zero_in, s));
+  // algorithmic bytes of the unfused passes it replaces (two sweeps, prolongation)
+  PL_CHECK_LAUNCH(K_JACOBI, (zero_in ? 40.0 : 48.0) * g.npts +
+                                (e ? 16.0 * g.npts + 8.0 * gc.npts : 0.0));
   return 0;
 }
 
 int zlaunch_rb(const double* u, const double* b, double* out, const Geo& g, const OpC& c,
-               double sigma, double omega, cudaStream_t s) {
+               double sigma, double omega, const double* e, cudaStream_t s) {
   double dval = zdiag(c, sigma);
+  Geo gc = make_geo(3, (g.N + 1) / 2);
   PL_PRE(K_RB);
-  PL_TRY(launch_zrb(u, b, out, g, c, sigma, omega, dval, s));
-  PL_CHECK_LAUNCH(K_RB, 24.0 * g.npts);
+  PL_TRY(launch_zrb(u, b, e, gc, out, g, c, sigma, omega, dval, s));
+  PL_CHECK_LAUNCH(K_RB, 24.0 * g.npts + (e ? 16.0 * g.npts + 8.0 * gc.npts : 0.0));
   return 0;
 }
 
