@@ -26,6 +26,7 @@ int sumsq_partials(const Geo& g);
 
 // ---- zmarch.cu: cp.async-pipelined 3-D order-2 versions (zmarch_ok) -------
 bool zmarch_ok(const Geo& g, const OpC& c);
+bool zmarch_enabled();
 int zlaunch_apply(const double* u, double* f, const Geo& g, const OpC& c, cudaStream_t s);
 int zlaunch_residual(const double* u, const double* b, double* r, const Geo& g, const OpC& c,
                      double sigma, cudaStream_t s);
@@ -37,6 +38,10 @@ int zlaunch_jacobi2(const double* u, const double* b, double* out, const Geo& g,
 // one fused red+black jor-rb sweep u -> out (out != u); e non-null: u + P_lin e first
 int zlaunch_rb(const double* u, const double* b, double* out, const Geo& g, const OpC& c,
                double sigma, double omega, const double* e, cudaStream_t s);
+
+// fine (+)= P_cubic coarse, 3-D, TMA-staged coarse planes (taps of cubic_taps)
+int zlaunch_cubic(const double* coarse, double* fine, const Geo& gf, const int* cnt,
+                  const int* idx, const double* w, int accumulate, cudaStream_t s);
 
 // ---- transfer.cu -----------------------------------------------------------
 // coarse = FW(fine) (transfers.py:27-34); fine geometry gf

@@ -578,6 +578,133 @@ __global__ void __launch_bounds__(NTHR_RB) k_zrb(const __grid_constant__ CUtenso
   }
 }
 
+// ---------------------------------------------------------------------------
+// fine (+)= P_cubic coarse for 3-D (transfers.py:82-89).  The coarse planes a
+// fine plane needs arrive by TMA (20 x 12 windows); per fine plane three
+// separable passes in shared memory -- z taps over the coarse window, y taps
+// onto the tile rows, x taps onto the tile -- each a sequential FMA chain in
+// increasing tap order, exactly the per-axis dgemm order of the reference.
+
+constexpr int QW = TX / 2 + 4, QH = TY / 2 + 4, PQ = align16(QW * QH);   // coarse window
+constexpr int RQ = 6;                                                     // coarse ring
+
+__global__ void __launch_bounds__(NTHR) k_cubic3(const double* __restrict__ coarse, Geo gc,
+                                                 double* __restrict__ fine, Geo gf,
+                                                 const int* __restrict__ tcnt,
+                                                 const int* __restrict__ tidx,
+                                                 const double* __restrict__ tw, int zc,
+                                                 int accumulate) {
+  extern __shared__ __align__(128) double sm[];
+  double* sc = sm;                       // RQ * PQ coarse planes
+  double* zb = sc + RQ * PQ;             // QH x QW  z-interpolated window
+  double* yb = zb + align16(QW * QH);    // TY x QW  y-interpolated rows
+  const int tid = threadIdx.y * 32 + threadIdx.x;
+  const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TY;
+  const int z0 = blockIdx.z * zc, z1 = min(z0 + zc, gf.nz);
+  const int cx0 = x0 / 2 - 2, cy0 = y0 / 2 - 2;
+  const int jlo = tidx[z0 * 4];
+  int loaded = jlo;      // coarse planes [jlo, loaded) are staged
+  // coarse window element (per thread fixed): in-plane offset or -1 (zero)
+  constexpr int PERQ = (QW * QH + NTHR - 1) / NTHR;
+  int qoff[PERQ];
+#pragma unroll
+  for (int q = 0; q < PERQ; ++q) {
+    const int k = tid + q * NTHR;
+    const int yy = k / QW, xx = k - yy * QW;
+    const int cx = cx0 + xx, cy = cy0 + yy;
+    qoff[q] = (k < QW * QH && cx >= 0 && cx < gc.nx && cy >= 0 && cy < gc.ny)
+                  ? cy * (int)gc.sy + cx : -1;
+  }
+  // per-thread tap registers: x taps of the thread's column, y taps of its
+  // pass-y entries (the (x, y) geometry is the same on every plane)
+  const int gx = x0 + threadIdx.x;
+  int xn = 0, xi[4] = {0, 0, 0, 0};
+  double xw[4] = {0.0, 0.0, 0.0, 0.0};
+  if (gx < gf.nx) {
+    xn = tcnt[gx];
+#pragma unroll
+    for (int t = 0; t < 4; ++t)
+      if (t < xn) { xi[t] = tidx[gx * 4 + t] - cx0; xw[t] = tw[gx * 4 + t]; }
+  }
+  constexpr int PERY = (TY * QW + NTHR - 1) / NTHR;
+  int yn[PERY], yk[PERY], yi[PERY][4];
+  double yw[PERY][4];
+#pragma unroll
+  for (int q = 0; q < PERY; ++q) {
+    const int k = tid + q * NTHR;
+    const int fy = k / QW, cx = k - fy * QW;
+    const int gy = y0 + fy;
+    yk[q] = k;
+    yn[q] = (k < TY * QW && gy < gf.ny) ? tcnt[gy] : 0;
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      yi[q][t] = 0;
+      yw[q][t] = 0.0;
+      if (t < yn[q]) { yi[q][t] = (tidx[gy * 4 + t] - cy0) * QW + cx; yw[q][t] = tw[gy * 4 + t]; }
+    }
+  }
+  for (int iz = z0; iz < z1; ++iz) {
+    const int nt = tcnt[iz];
+    int zs[4] = {0, 0, 0, 0};
+    double zw[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+    for (int t = 0; t < 4; ++t)
+      if (t < nt) { zs[t] = ((tidx[iz * 4 + t] - jlo) % RQ) * PQ; zw[t] = tw[iz * 4 + t]; }
+    const int jmax = tidx[iz * 4 + nt - 1];
+    // stage the coarse planes this fine plane adds (planes below its first
+    // tap are dead; the ring holds RQ >= 4 live planes)
+    for (; loaded <= jmax; ++loaded) {
+      double* dst = sc + ((loaded - jlo) % RQ) * PQ;
+      const double* src = coarse + (long long)loaded * gc.sz;
+#pragma unroll
+      for (int q = 0; q < PERQ; ++q) {
+        const int k = tid + q * NTHR;
+        if (k < QW * QH) dst[k] = qoff[q] >= 0 ? __ldg(src + qoff[q]) : 0.0;
+      }
+    }
+    __syncthreads();
+    // pass z over the coarse window
+    for (int k = tid; k < QW * QH; k += NTHR) {
+      double acc = 0.0;
+#pragma unroll
+      for (int t = 0; t < 4; ++t)
+        if (t < nt) acc = __fma_rn(zw[t], sc[zs[t] + k], acc);
+      zb[k] = acc;
+    }
+    __syncthreads();
+    // pass y onto the tile rows
+#pragma unroll
+    for (int q = 0; q < PERY; ++q) {
+      if (yk[q] < TY * QW) {
+        double acc = 0.0;
+#pragma unroll
+        for (int t = 0; t < 4; ++t)
+          if (t < yn[q]) acc = __fma_rn(yw[q][t], zb[yi[q][t]], acc);
+        yb[yk[q]] = acc;
+      }
+    }
+    __syncthreads();
+    // pass x onto the tile, accumulate into the fine field
+    if (gx < gf.nx) {
+#pragma unroll
+      for (int r = 0; r < 2; ++r) {
+        const int fy = threadIdx.y + 8 * r;
+        const int gy = y0 + fy;
+        if (gy < gf.ny) {
+          const double* row = yb + fy * QW;
+          double acc = 0.0;
+#pragma unroll
+          for (int t = 0; t < 4; ++t)
+            if (t < xn) acc = __fma_rn(xw[t], row[xi[t]], acc);
+          const long long o = gf.at(gx, gy, iz);
+          fine[o] = accumulate ? fine[o] + acc : acc;
+        }
+      }
+    }
+    __syncthreads();
+  }
+}
+
 constexpr int PREF1 = 3;
 constexpr int PREF2 = 3;
 
@@ -707,7 +834,27 @@ int launch_zrb(const double* u, const double* b, const double* e, const Geo& gc,
   return 0;
 }
 
+int launch_cubic3(const double* coarse, double* fine, const Geo& gf, const int* cnt,
+                  const int* idx, const double* w, int accumulate, cudaStream_t s) {
+  Geo gc = make_geo(3, (gf.N + 1) / 2);
+  const int zc = pick_zc(gf);
+  dim3 grid(ceil_div(gf.nx, TX), ceil_div(gf.ny, TY), ceil_div(gf.nz, zc)), block(32, 8);
+  size_t smem = sizeof(double) * (RQ * PQ + align16(QW * QH) + align16(QW * TY));
+  raise_smem(k_cubic3, smem);
+  k_cubic3<<<grid, block, smem, s>>>(coarse, gc, fine, gf, cnt, idx, w, zc, accumulate);
+  return 0;
+}
+
 }  // namespace
+
+int zlaunch_cubic(const double* coarse, double* fine, const Geo& gf, const int* cnt,
+                  const int* idx, const double* w, int accumulate, cudaStream_t s) {
+  PL_PRE(K_INTERP);
+  PL_TRY(launch_cubic3(coarse, fine, gf, cnt, idx, w, accumulate, s));
+  Geo gc = make_geo(3, (gf.N + 1) / 2);
+  PL_CHECK_LAUNCH(K_INTERP, (accumulate ? 16.0 : 8.0) * gf.npts + 8.0 * gc.npts);
+  return 0;
+}
 
 // host value of 1 - sigma * (nu * ((0 + d) + d + d)) for order 2 (constant)
 double zdiag(const OpC& c, double sigma) {
@@ -719,6 +866,7 @@ double zdiag(const OpC& c, double sigma) {
 }
 
 int g_zmarch_enabled = 1;   // runtime knob (pl_set_option), for A/B tests
+bool zmarch_enabled() { return g_zmarch_enabled != 0; }
 
 bool zmarch_ok(const Geo& g, const OpC& c) {
   // TMA needs 16-byte row and plane strides: the padded device layout

@@ -354,3 +354,17 @@ def test_fused_equals_unfused_at_127(sm, om, pre, post):
         outs.append(mg.v_cycle(sop, u, b, cfg))
     _capi.set_option(_capi.OPT_ZMARCH, 1)
     assert torch.equal(outs[0], outs[1])
+
+
+@pytest.mark.parametrize("nf", [32, 64, 256])
+def test_cubic_zmarch_equals_pass_kernels(nf):
+    """The TMA-staged 3-D cubic interpolation equals the per-axis pass kernels
+    (which are pinned to the reference by test_transfers_bitwise) bit for bit."""
+    rng = np.random.default_rng(nf)
+    c = dev(rng.standard_normal((nf // 2 - 1,) * 3))
+    outs = []
+    for z in (1, 0):
+        _capi.set_option(_capi.OPT_ZMARCH, z)
+        outs.append(transfers.interp_cubic(c))
+    _capi.set_option(_capi.OPT_ZMARCH, 1)
+    assert torch.equal(outs[0], outs[1])
