@@ -201,6 +201,7 @@ def run_ours(args, w):
         barrier()
     ms = t0.elapsed_time(t1)
     n_dom, ms_dom, bytes_dom = _capi.timing_collect(dom)
+    by_size = _capi.timing_by_size(dom)
     _capi.timing_enable(None)
     stats = _capi.stats()
     launches = sum(v[0] for v in stats.values())
@@ -253,6 +254,10 @@ def run_ours(args, w):
             "roofline": {"bound": "hbm", "kernel": dom,
                          "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": (achieved / peak) if achieved else None,
+                         "per_level": {f"{b / 1e6:.1f}MB": {
+                             "launches": c, "avg_us": 1e3 * t / c,
+                             "gbs": b / (t / c / 1e3) / 1e9}
+                             for b, (c, t) in sorted(by_size.items(), reverse=True)},
                          "traffic": None, "peak_source": peak_src,
                          "launches_timed": n_dom,
                          "kernel_share_of_step": ms_dom / ms if ms else None,

@@ -64,7 +64,8 @@ int pl_abi_version(void);
 const char* pl_last_error(void);
 
 /* runtime options (A/B testing of kernel variants; results are bit-identical) */
-#define PL_OPT_ZMARCH 0 /* 1 (default): cp.async z-marching + fused sweeps for 3-D order 2 */
+#define PL_OPT_ZMARCH 0       /* 1 (default): TMA z-marching + fused sweeps, 3-D order 2 */
+#define PL_OPT_ZMARCH_MIN_N 1 /* smallest n-1 using them (default 127, >= 31) */
 int pl_set_option(int key, int value);
 
 /* storage elements of one field (incl. row pads) */
@@ -188,6 +189,8 @@ int pl_stats_get(long long* launches, double* alg_bytes, int nkinds);
    timed, their total milliseconds and their algorithmic bytes */
 int pl_timing_enable(unsigned mask);
 int pl_timing_collect(int kind, long long* launches, double* total_ms, double* alg_bytes);
+/* the individual timed launches of one kind: algorithmic bytes and ms */
+int pl_timing_dump(int kind, long long nmax, double* bytes, float* ms, long long* n);
 const char* pl_kind_name(int kind);
 
 #ifdef __cplusplus

@@ -79,6 +79,7 @@ _SIGS = {
     "pl_stats_get": (i32, [C.POINTER(i64), dp, i32]),
     "pl_timing_enable": (i32, [C.c_uint]),
     "pl_timing_collect": (i32, [i32, C.POINTER(i64), dp, dp]),
+    "pl_timing_dump": (i32, [i32, i64, dp, C.POINTER(C.c_float), C.POINTER(i64)]),
     "pl_kind_name": (C.c_char_p, [i32]),
 }
 
@@ -112,6 +113,7 @@ class MultigridErrorBase(RuntimeError):
 
 
 OPT_ZMARCH = 0
+OPT_ZMARCH_MIN_N = 1
 
 
 def set_option(key, value):
@@ -164,6 +166,21 @@ def timing_enable(names):
     for n in names or ():
         mask |= 1 << kind_index(n)
     lib().pl_timing_enable(mask)
+
+
+def timing_by_size(name, nmax=1 << 20):
+    """{alg_bytes_per_launch: (launches, total_ms)} for one kind: separates
+    the multigrid levels (each level has its own byte count)."""
+    b = (f64 * nmax)()
+    t = (C.c_float * nmax)()
+    n = i64(0)
+    check(lib().pl_timing_dump(kind_index(name), nmax, b, t, C.byref(n)))
+    out = {}
+    for i in range(n.value):
+        k = b[i]
+        c, s = out.get(k, (0, 0.0))
+        out[k] = (c + 1, s + t[i])
+    return out
 
 
 def timing_collect(name):

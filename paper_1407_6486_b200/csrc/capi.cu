@@ -213,6 +213,7 @@ __global__ void k_shifted_apply(const double* __restrict__ u, double* __restrict
 
 namespace pl {
 extern int g_zmarch_enabled;
+extern int g_zmarch_min_n;
 }
 
 extern "C" {
@@ -222,6 +223,10 @@ int pl_abi_version(void) { return PL_ABI_VERSION; }
 int pl_set_option(int key, int value) {
   if (key == PL_OPT_ZMARCH) {
     g_zmarch_enabled = value != 0;
+    return 0;
+  }
+  if (key == PL_OPT_ZMARCH_MIN_N) {
+    g_zmarch_min_n = value < 31 ? 31 : value;
     return 0;
   }
   set_error("unknown option %d", key);
@@ -502,6 +507,20 @@ int pl_timing_collect(int kind, long long* launches, double* total_ms, double* a
   *launches = n;
   *total_ms = t;
   *alg_bytes = b;
+  return 0;
+}
+
+int pl_timing_dump(int kind, long long nmax, double* bytes, float* ms, long long* n) {
+  long long c = 0;
+  for (size_t i = 0; i < g_ev_used && c < nmax; ++i) {
+    if (g_ev_pool[i].kind != kind) continue;
+    cudaError_t e = cudaEventSynchronize(g_ev_pool[i].b);
+    if (e != cudaSuccess) return cuda_status(e, "event sync");
+    cudaEventElapsedTime(&ms[c], g_ev_pool[i].a, g_ev_pool[i].b);
+    bytes[c] = g_ev_pool[i].bytes;
+    ++c;
+  }
+  *n = c;
   return 0;
 }
 

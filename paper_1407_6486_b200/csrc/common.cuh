@@ -88,12 +88,14 @@ inline Geo make_geo(int dim, int n) { return make_geo_pitch(dim, n, dim >= 2 ? n
 // dense layout (shared-memory tiles, scratch)
 inline Geo make_geo_compact(int dim, int n) { return make_geo_pitch(dim, n, n - 1); }
 
-// logical linear index -> (x, y, z)
+// logical linear index -> (x, y, z); 32-bit division (every grid here has
+// fewer than 2^32 points; 64-bit division is a ~70-instruction subroutine)
 __host__ __device__ inline void decode_point(const Geo& g, long long t, int& x, int& y, int& z) {
-  x = (int)(t % g.nx);
-  long long r = t / g.nx;
-  y = (int)(r % g.ny);
-  z = (int)(r / g.ny);
+  const unsigned tt = (unsigned)t, nx = (unsigned)g.nx, ny = (unsigned)g.ny;
+  const unsigned r = tt / nx;
+  x = (int)(tt - r * nx);
+  z = (int)(r / ny);
+  y = (int)(r - (unsigned)z * ny);
 }
 
 // Operator constants, all computed on the host with the reference's own

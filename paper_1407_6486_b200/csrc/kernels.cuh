@@ -27,6 +27,7 @@ int sumsq_partials(const Geo& g);
 // ---- zmarch.cu: cp.async-pipelined 3-D order-2 versions (zmarch_ok) -------
 bool zmarch_ok(const Geo& g, const OpC& c);
 bool zmarch_enabled();
+bool zmarch_size_ok(int N);
 int zlaunch_apply(const double* u, double* f, const Geo& g, const OpC& c, cudaStream_t s);
 int zlaunch_residual(const double* u, const double* b, double* r, const Geo& g, const OpC& c,
                      double sigma, cudaStream_t s);

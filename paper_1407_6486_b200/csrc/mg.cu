@@ -67,13 +67,10 @@ struct TailArgs {
 };
 
 #define PL_FOR_SM_POINTS(g)                                                  \
-  for (long long p = threadIdx.x; p < (g).npts; p += blockDim.x)
+  for (int p = threadIdx.x; p < (int)(g).npts; p += blockDim.x)
 
-__device__ __forceinline__ void decode(const Geo& g, long long p, int& x, int& y, int& z) {
-  x = (int)(p % g.nx);
-  long long r = p / g.nx;
-  y = (int)(r % g.ny);
-  z = (int)(r / g.ny);
+__device__ __forceinline__ void decode(const Geo& g, int p, int& x, int& y, int& z) {
+  decode_point(g, p, x, y, z);
 }
 
 // `count` sweeps on shared-memory level L; result ends in u.
@@ -91,20 +88,25 @@ __device__ void tail_smooth(const TailArgs& a, const TailLevel& L, double* sm, i
     return;
   }
   if (a.smoother == SM_JACOBI) {
+    // ping-pong u <-> t; one copy back only for an odd sweep count
     for (int k = 0; k < count; ++k) {
-      bool z0 = zero && k == 0;
+      const bool z0 = zero && k == 0;
+      const double* src = (k & 1) ? t : u;
+      double* dst = (k & 1) ? u : t;
       PL_FOR_SM_POINTS(L.g) {
         int x, y, z;
         decode(L.g, p, x, y, z);
         double d = shifted_diag<DIM>(L.g, L.c, a.sigma, x, y, z);
         if (z0) {
-          t[p] = 0.0 + ((a.omega * b[p]) / d);
+          dst[p] = 0.0 + ((a.omega * b[p]) / d);
         } else {
-          double au = shifted_point<DIM>(u, L.g, L.c, a.sigma, x, y, z, p);
-          t[p] = u[p] + ((a.omega * (b[p] - au)) / d);
+          double au = shifted_point<DIM>(src, L.g, L.c, a.sigma, x, y, z, p);
+          dst[p] = src[p] + ((a.omega * (b[p] - au)) / d);
         }
       }
       __syncthreads();
+    }
+    if (count & 1) {
       PL_FOR_SM_POINTS(L.g) u[p] = t[p];
       __syncthreads();
     }
@@ -118,6 +120,20 @@ __device__ void tail_smooth(const TailArgs& a, const TailLevel& L, double* sm, i
   }
   for (int k = 0; k < count; ++k) {
     for (int colour = 1; colour >= 0; --colour) {
+      if (L.c.order == 2) {
+        // same-colour points never neighbour: update in place
+        PL_FOR_SM_POINTS(L.g) {
+          int x, y, z;
+          decode(L.g, p, x, y, z);
+          if (is_red<DIM>(x, y, z) == (colour == 1)) {
+            double d = shifted_diag<DIM>(L.g, L.c, a.sigma, x, y, z);
+            double r = b[p] - shifted_point<DIM>(u, L.g, L.c, a.sigma, x, y, z, p);
+            u[p] = u[p] + ((a.omega * r) / d);
+          }
+        }
+        __syncthreads();
+        continue;
+      }
       PL_FOR_SM_POINTS(L.g) {
         int x, y, z;
         decode(L.g, p, x, y, z);

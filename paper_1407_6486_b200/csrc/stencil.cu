@@ -15,20 +15,28 @@ namespace {
 
 constexpr int TX = 32;
 constexpr int TY = 4;
-constexpr int ZC = 16;
 
 struct Launch {
   dim3 grid, block;
+  int zc;
 };
 
+// z planes per thread: large grids march through a chunk (z-neighbours stay
+// in L1); small grids take one plane per thread so the grid still fills the
+// 148 SMs -- a long per-thread chain over few CTAs is latency-bound
 inline Launch plan_launch(const Geo& g) {
   Launch L;
   if (g.dim == 1) {
     L.block = dim3(256, 1, 1);
     L.grid = dim3(ceil_div(g.nx, 256), 1, 1);
+    L.zc = 1;
   } else {
     L.block = dim3(TX, TY, 1);
-    L.grid = dim3(ceil_div(g.nx, TX), ceil_div(g.ny, TY), ceil_div(g.nz, ZC));
+    long long cols = (long long)ceil_div(g.nx, TX) * ceil_div(g.ny, TY);
+    int zc = 16;
+    while (zc > 1 && cols * ceil_div(g.nz, zc) < 148 * 16) zc /= 2;
+    L.zc = zc;
+    L.grid = dim3(ceil_div(g.nx, TX), ceil_div(g.ny, TY), ceil_div(g.nz, zc));
   }
   return L;
 }
@@ -38,13 +46,13 @@ inline Launch plan_launch(const Geo& g) {
   const int x = blockIdx.x * blockDim.x + threadIdx.x;                         \
   const int y = blockIdx.y * blockDim.y + threadIdx.y;                         \
   if (x >= g.nx || y >= g.ny) return;                                          \
-  const int z0 = blockIdx.z * ZC;                                              \
-  const int z1 = min(z0 + ZC, g.nz);                                           \
+  const int z0 = blockIdx.z * zc;                                              \
+  const int z1 = min(z0 + zc, g.nz);                                           \
   for (int z = z0; z < z1; ++z)
 
 template <int DIM>
 __global__ void __launch_bounds__(256) k_apply(const double* __restrict__ u,
-                                               double* __restrict__ f, Geo g, OpC c) {
+                                               double* __restrict__ f, Geo g, OpC c, int zc) {
   PL_FOR_POINTS(g) {
     long long idx = (long long)z * g.sz + (long long)y * g.sy + x;
     f[idx] = lap_point<DIM>(u, g, c, x, y, z, idx);
@@ -55,7 +63,7 @@ template <int DIM>
 __global__ void __launch_bounds__(256) k_residual(const double* __restrict__ u,
                                                   const double* __restrict__ b,
                                                   double* __restrict__ r, Geo g, OpC c,
-                                                  double sigma) {
+                                                  double sigma, int zc) {
   PL_FOR_POINTS(g) {
     long long idx = (long long)z * g.sz + (long long)y * g.sy + x;
     r[idx] = b[idx] - shifted_point<DIM>(u, g, c, sigma, x, y, z, idx);
@@ -67,7 +75,7 @@ template <int DIM>
 __global__ void __launch_bounds__(256) k_jacobi(const double* __restrict__ u,
                                                 const double* __restrict__ b,
                                                 double* __restrict__ out, Geo g, OpC c,
-                                                double sigma, double omega, int zero_in) {
+                                                double sigma, double omega, int zero_in, int zc) {
   PL_FOR_POINTS(g) {
     long long idx = (long long)z * g.sz + (long long)y * g.sy + x;
     double d = shifted_diag<DIM>(g, c, sigma, x, y, z);
@@ -84,7 +92,7 @@ __global__ void __launch_bounds__(256) k_jacobi(const double* __restrict__ u,
 template <int DIM>
 __global__ void __launch_bounds__(256) k_rb(const double* in, const double* __restrict__ b,
                                             double* out, Geo g, OpC c, double sigma,
-                                            double omega, int red, int inplace) {
+                                            double omega, int red, int inplace, int zc) {
   PL_FOR_POINTS(g) {
     long long idx = (long long)z * g.sz + (long long)y * g.sy + x;
     bool mine = is_red<DIM>(x, y, z) == (red != 0);
@@ -159,7 +167,7 @@ int launch_apply(const double* u, double* f, const Geo& g, const OpC& c, cudaStr
   if (zmarch_ok(g, c)) return zlaunch_apply(u, f, g, c, s);
   Launch L = plan_launch(g);
   PL_PRE(K_APPLY);
-  PL_DISPATCH_DIM(g, k_apply, L, s, u, f, g, c);
+  PL_DISPATCH_DIM(g, k_apply, L, s, u, f, g, c, L.zc);
   PL_CHECK_LAUNCH(K_APPLY, 16.0 * g.npts);
   return 0;
 }
@@ -169,7 +177,7 @@ int launch_residual(const double* u, const double* b, double* r, const Geo& g, c
   if (zmarch_ok(g, c)) return zlaunch_residual(u, b, r, g, c, sigma, s);
   Launch L = plan_launch(g);
   PL_PRE(K_RESID);
-  PL_DISPATCH_DIM(g, k_residual, L, s, u, b, r, g, c, sigma);
+  PL_DISPATCH_DIM(g, k_residual, L, s, u, b, r, g, c, sigma, L.zc);
   PL_CHECK_LAUNCH(K_RESID, 24.0 * g.npts);
   return 0;
 }
@@ -179,7 +187,7 @@ int launch_jacobi(const double* u, const double* b, double* out, const Geo& g, c
   if (zmarch_ok(g, c)) return zlaunch_jacobi(u, b, out, g, c, sigma, omega, zero_in, s);
   Launch L = plan_launch(g);
   PL_PRE(K_JACOBI);
-  PL_DISPATCH_DIM(g, k_jacobi, L, s, u, b, out, g, c, sigma, omega, zero_in);
+  PL_DISPATCH_DIM(g, k_jacobi, L, s, u, b, out, g, c, sigma, omega, zero_in, L.zc);
   PL_CHECK_LAUNCH(K_JACOBI, (zero_in ? 16.0 : 24.0) * g.npts);
   return 0;
 }
@@ -189,7 +197,7 @@ int launch_rb(const double* in, const double* b, double* out, const Geo& g, cons
   Launch L = plan_launch(g);
   int inplace = in == out;
   PL_PRE(K_RB);
-  PL_DISPATCH_DIM(g, k_rb, L, s, in, b, out, g, c, sigma, omega, red, inplace);
+  PL_DISPATCH_DIM(g, k_rb, L, s, in, b, out, g, c, sigma, omega, red, inplace, L.zc);
   // one colour: half of a full red+black sweep's 24 B/DOF
   PL_CHECK_LAUNCH(K_RB, 12.0 * g.npts);
   return 0;
@@ -204,7 +212,7 @@ int launch_sumsq(const double* u, const double* b, const Geo& g, const OpC& c, d
                  double* partials, int npartials, double* out, cudaStream_t s) {
   dim3 grid(npartials), block(NORM_THREADS);
   PL_PRE(K_NORM);
-  PL_DISPATCH_DIM(g, k_sumsq, (Launch{grid, block}), s, u, b, g, c, sigma, partials);
+  PL_DISPATCH_DIM(g, k_sumsq, (Launch{grid, block, 1}), s, u, b, g, c, sigma, partials);
   PL_CHECK_LAUNCH(K_NORM, (u ? 16.0 : 8.0) * g.npts);
   PL_PRE(K_NORM);
   k_sum_final<<<1, 256, 0, s>>>(partials, npartials, out);

@@ -198,7 +198,7 @@ int launch_cubic(const double* coarse, double* fine, const Geo& gf, int accumula
                  double* scratch, cudaStream_t s) {
   const CubicTaps* t = cubic_taps(gf.N + 1);
   if (!t) return 2;
-  if (gf.dim == 3 && gf.N >= 31 && zmarch_enabled())
+  if (gf.dim == 3 && gf.N >= 31 && zmarch_size_ok(gf.N))
     return zlaunch_cubic(coarse, fine, gf, t->cnt, t->idx, t->w, accumulate, s);
   Geo gc = make_geo(gf.dim, (gf.N + 1) / 2);
   const long long Nf = gf.N, Nc = gc.N, pc = gc.sy, pf = gf.sy;

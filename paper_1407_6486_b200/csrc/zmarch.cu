@@ -588,6 +588,17 @@ __global__ void __launch_bounds__(NTHR_RB) k_zrb(const __grid_constant__ CUtenso
 constexpr int QW = TX / 2 + 4, QH = TY / 2 + 4, PQ = align16(QW * QH);   // coarse window
 constexpr int RQ = 6;                                                     // coarse ring
 
+__device__ __forceinline__ void cpa8(double* smem, const double* gmem, bool valid) {
+  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem),
+               "r"(valid ? 8 : 0));
+}
+__device__ __forceinline__ void cpa_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cpa_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
 __global__ void __launch_bounds__(NTHR) k_cubic3(const double* __restrict__ coarse, Geo gc,
                                                  double* __restrict__ fine, Geo gf,
                                                  const int* __restrict__ tcnt,
@@ -603,6 +614,7 @@ __global__ void __launch_bounds__(NTHR) k_cubic3(const double* __restrict__ coar
   const int z0 = blockIdx.z * zc, z1 = min(z0 + zc, gf.nz);
   const int cx0 = x0 / 2 - 2, cy0 = y0 / 2 - 2;
   const int jlo = tidx[z0 * 4];
+  const int jtop = tidx[(z1 - 1) * 4 + tcnt[z1 - 1] - 1];   // last coarse plane needed
   int loaded = jlo;      // coarse planes [jlo, loaded) are staged
   // coarse window element (per thread fixed): in-plane offset or -1 (zero)
   constexpr int PERQ = (QW * QH + NTHR - 1) / NTHR;
@@ -618,6 +630,7 @@ __global__ void __launch_bounds__(NTHR) k_cubic3(const double* __restrict__ coar
   // per-thread tap registers: x taps of the thread's column, y taps of its
   // pass-y entries (the (x, y) geometry is the same on every plane)
   const int gx = x0 + threadIdx.x;
+  (void)jtop;
   int xn = 0, xi[4] = {0, 0, 0, 0};
   double xw[4] = {0.0, 0.0, 0.0, 0.0};
   if (gx < gf.nx) {
@@ -651,6 +664,15 @@ __global__ void __launch_bounds__(NTHR) k_cubic3(const double* __restrict__ coar
     for (int t = 0; t < 4; ++t)
       if (t < nt) { zs[t] = ((tidx[iz * 4 + t] - jlo) % RQ) * PQ; zw[t] = tw[iz * 4 + t]; }
     const int jmax = tidx[iz * 4 + nt - 1];
+    // fine values to accumulate into: load now, use after the passes
+    double fin[2] = {0.0, 0.0};
+    if (accumulate && gx < gf.nx) {
+#pragma unroll
+      for (int r = 0; r < 2; ++r) {
+        const int gy = y0 + threadIdx.y + 8 * r;
+        if (gy < gf.ny) fin[r] = fine[gf.at(gx, gy, iz)];
+      }
+    }
     // stage the coarse planes this fine plane adds (planes below its first
     // tap are dead; the ring holds RQ >= 4 live planes)
     for (; loaded <= jmax; ++loaded) {
@@ -696,8 +718,7 @@ __global__ void __launch_bounds__(NTHR) k_cubic3(const double* __restrict__ coar
 #pragma unroll
           for (int t = 0; t < 4; ++t)
             if (t < xn) acc = __fma_rn(xw[t], row[xi[t]], acc);
-          const long long o = gf.at(gx, gy, iz);
-          fine[o] = accumulate ? fine[o] + acc : acc;
+          fine[gf.at(gx, gy, iz)] = accumulate ? fin[r] + acc : acc;
         }
       }
     }
@@ -866,11 +887,16 @@ double zdiag(const OpC& c, double sigma) {
 }
 
 int g_zmarch_enabled = 1;   // runtime knob (pl_set_option), for A/B tests
+// smallest interior size for the TMA kernels: below it a CTA would march many
+// planes for few CTAs (latency-bound); the one-point-per-thread kernels win
+int g_zmarch_min_n = 127;
 bool zmarch_enabled() { return g_zmarch_enabled != 0; }
+bool zmarch_size_ok(int N) { return g_zmarch_enabled && N >= g_zmarch_min_n; }
 
 bool zmarch_ok(const Geo& g, const OpC& c) {
   // TMA needs 16-byte row and plane strides: the padded device layout
-  return g_zmarch_enabled && g.dim == 3 && c.order == 2 && g.N >= 31 && (g.sy % 2) == 0;
+  return g_zmarch_enabled && g.dim == 3 && c.order == 2 && g.N >= g_zmarch_min_n && g.N >= 31 &&
+         (g.sy % 2) == 0;
 }
 
 int zlaunch_apply(const double* u, double* f, const Geo& g, const OpC& c, cudaStream_t s) {

@@ -319,6 +319,7 @@ def test_zmarch_kernels_bitwise_31cubed(zmarch):
     plain kernels run.  Both must be bit-identical to the reference."""
     a, m = case("mg32_d3")
     _capi.set_option(_capi.OPT_ZMARCH, zmarch)
+    _capi.set_option(_capi.OPT_ZMARCH_MIN_N, 31)
     try:
         op = heat.HeatOperator(heat.Grid(3, 32))
         sop = mg.ShiftedOperator(op, m["sigma"])
@@ -336,6 +337,7 @@ def test_zmarch_kernels_bitwise_31cubed(zmarch):
             close(mg.v_cycle(sop, dev(a["u"]), dev(a["b"]), cfg11), a[f"vc11_{tag}"], 1e-13)
     finally:
         _capi.set_option(_capi.OPT_ZMARCH, 1)
+        _capi.set_option(_capi.OPT_ZMARCH_MIN_N, 127)
 
 
 @pytest.mark.parametrize("sm,om,pre,post", [("jacobi", 2.0 / 3.0, 2, 2), ("jor-rb", 1.0, 1, 1)])
@@ -363,8 +365,21 @@ def test_cubic_zmarch_equals_pass_kernels(nf):
     rng = np.random.default_rng(nf)
     c = dev(rng.standard_normal((nf // 2 - 1,) * 3))
     outs = []
+    _capi.set_option(_capi.OPT_ZMARCH_MIN_N, 31)
     for z in (1, 0):
         _capi.set_option(_capi.OPT_ZMARCH, z)
         outs.append(transfers.interp_cubic(c))
     _capi.set_option(_capi.OPT_ZMARCH, 1)
+    _capi.set_option(_capi.OPT_ZMARCH_MIN_N, 127)
     assert torch.equal(outs[0], outs[1])
+
+
+@pytest.mark.parametrize("name", ["run_cfg3_small", "run_cfg4_small", "run_cfg4_small_tol"])
+def test_pfasst_run_parity_tma_path(name):
+    """The 31^3 runs again with the TMA / fused kernels engaged from 31^3 (by
+    default they start at 127^3): same counts, same tolerance."""
+    _capi.set_option(_capi.OPT_ZMARCH_MIN_N, 31)
+    try:
+        test_pfasst_run_parity(name)
+    finally:
+        _capi.set_option(_capi.OPT_ZMARCH_MIN_N, 127)
