@@ -66,6 +66,7 @@ const char* pl_last_error(void);
 /* runtime options (A/B testing of kernel variants; results are bit-identical) */
 #define PL_OPT_ZMARCH 0       /* 1 (default): TMA z-marching + fused sweeps, 3-D order 2 */
 #define PL_OPT_ZMARCH_MIN_N 1 /* smallest n-1 using them (default 127, >= 31) */
+#define PL_OPT_GRAPHS 2       /* 1 (default): FixedCycles sweeps replay as CUDA graphs */
 int pl_set_option(int key, int value);
 
 /* storage elements of one field (incl. row pads) */

@@ -114,6 +114,7 @@ class MultigridErrorBase(RuntimeError):
 
 OPT_ZMARCH = 0
 OPT_ZMARCH_MIN_N = 1
+OPT_GRAPHS = 2
 
 
 def set_option(key, value):
