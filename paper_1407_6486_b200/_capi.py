@@ -115,6 +115,9 @@ class MultigridErrorBase(RuntimeError):
 OPT_ZMARCH = 0
 OPT_ZMARCH_MIN_N = 1
 OPT_GRAPHS = 2
+OPT_ZRB_VARIANT = 3
+OPT_FUSE_PROLONG = 4
+OPT_CUBIC_VARIANT = 5
 
 
 def set_option(key, value):

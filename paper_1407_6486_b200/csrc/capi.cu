@@ -218,6 +218,9 @@ extern "C" int g_graphs_enabled;
 namespace pl {
 extern int g_zmarch_enabled;
 extern int g_zmarch_min_n;
+extern int g_zrb_variant;
+extern int g_fuse_prolong;
+extern int g_cubic_variant;
 }
 
 extern "C" {
@@ -231,6 +234,22 @@ int pl_set_option(int key, int value) {
   }
   if (key == PL_OPT_GRAPHS) {
     g_graphs_enabled = value != 0;
+    return 0;
+  }
+  if (key == PL_OPT_ZRB_VARIANT) {
+    if (value < 0 || value > 4) {
+      set_error("zrb variant %d out of range", value);
+      return -1;
+    }
+    g_zrb_variant = value;
+    return 0;
+  }
+  if (key == PL_OPT_CUBIC_VARIANT) {
+    g_cubic_variant = value != 0;
+    return 0;
+  }
+  if (key == PL_OPT_FUSE_PROLONG) {
+    g_fuse_prolong = value != 0;
     return 0;
   }
   if (key == PL_OPT_ZMARCH_MIN_N) {

@@ -28,6 +28,7 @@ int sumsq_partials(const Geo& g);
 bool zmarch_ok(const Geo& g, const OpC& c);
 bool zmarch_enabled();
 bool zmarch_size_ok(int N);
+bool zmarch_fuse_prolong();   // PL_OPT_FUSE_PROLONG
 int zlaunch_apply(const double* u, double* f, const Geo& g, const OpC& c, cudaStream_t s);
 int zlaunch_residual(const double* u, const double* b, double* r, const Geo& g, const OpC& c,
                      double sigma, cudaStream_t s);

@@ -62,8 +62,9 @@ struct TailArgs {
   TailLevel lv[MAX_LEVELS];
   int smoother, pre, post;
   double omega, sigma;
-  const double* lu;   // m*m factors + m pivots (global, L1-cached)
+  const double* lu;   // m*m factors + m pivots (global)
   int m;
+  int lu_off;         // >= 0: factors staged in shared memory at this offset
 };
 
 #define PL_FOR_SM_POINTS(g)                                                  \
@@ -121,15 +122,21 @@ __device__ void tail_smooth(const TailArgs& a, const TailLevel& L, double* sm, i
   for (int k = 0; k < count; ++k) {
     for (int colour = 1; colour >= 0; --colour) {
       if (L.c.order == 2) {
-        // same-colour points never neighbour: update in place
-        PL_FOR_SM_POINTS(L.g) {
-          int x, y, z;
-          decode(L.g, p, x, y, z);
-          if (is_red<DIM>(x, y, z) == (colour == 1)) {
-            double d = shifted_diag<DIM>(L.g, L.c, a.sigma, x, y, z);
-            double r = b[p] - shifted_point<DIM>(u, L.g, L.c, a.sigma, x, y, z, p);
-            u[p] = u[p] + ((a.omega * r) / d);
-          }
+        // same-colour points never neighbour: update in place, visiting only
+        // this colour (x = 2h + s on each (y, z) row)
+        const int N = L.g.nx, H = (N + 1) / 2;
+        const int rows = (DIM >= 2 ? L.g.ny : 1) * (DIM == 3 ? L.g.nz : 1);
+        for (int t = threadIdx.x; t < H * rows; t += blockDim.x) {
+          const int row = t / H, h = t - row * H;
+          const int y = DIM >= 2 ? row % L.g.ny : 0;
+          const int z = DIM == 3 ? row / L.g.ny : 0;
+          // is_red: x + y + z + DIM even
+          const int x = 2 * h + (((y + z + DIM) & 1) ^ colour ^ 1);
+          if (x >= N) continue;
+          const int p = (z * L.g.ny + y) * N + x;
+          double d = shifted_diag<DIM>(L.g, L.c, a.sigma, x, y, z);
+          double r = b[p] - shifted_point<DIM>(u, L.g, L.c, a.sigma, x, y, z, p);
+          u[p] = u[p] + ((a.omega * r) / d);
         }
         __syncthreads();
         continue;
@@ -154,9 +161,9 @@ __device__ void tail_smooth(const TailArgs& a, const TailLevel& L, double* sm, i
 
 // dense LU solve on the coarsest grid: b (smem) -> u (smem), one warp.
 // LAPACK getrs order: row interchanges, unit-lower forward, upper backward.
-__device__ void tail_lu(const TailArgs& a, const double* b, double* u) {
+__device__ void tail_lu(const TailArgs& a, const double* lu, const double* b, double* u) {
   const int m = a.m;
-  const double* A = a.lu;
+  const double* A = lu;
   const double* piv = a.lu + (size_t)m * m;
   if (threadIdx.x < 32) {
     for (int i = threadIdx.x; i < m; i += 32) u[i] = b[i];
@@ -200,6 +207,8 @@ __global__ void __launch_bounds__(TAIL_THREADS) k_tail(TailArgs a,
                                                        int ncycles) {
   extern __shared__ double sm[];
   const TailLevel& L0 = a.lv[0];
+  if (a.lu_off >= 0)
+    for (int i = threadIdx.x; i < a.m * a.m + a.m; i += blockDim.x) sm[a.lu_off + i] = a.lu[i];
   PL_FOR_SM_POINTS(L0.g) {
     int x, y, z;
     decode(L0.g, p, x, y, z);
@@ -234,7 +243,7 @@ __global__ void __launch_bounds__(TAIL_THREADS) k_tail(TailArgs a,
       __syncthreads();
     }
     // ---- coarsest: dense LU (ignores the initial guess, multigrid.py:240-243)
-    tail_lu(a, sm + a.lv[l].off_b, sm + a.lv[l].off_u);
+    tail_lu(a, a.lu_off >= 0 ? sm + a.lu_off : a.lu, sm + a.lv[l].off_b, sm + a.lv[l].off_u);
     // ---- up: prolongate, correct, post-smooth
     for (--l; l >= 0; --l) {
       const TailLevel& L = a.lv[l];
@@ -288,6 +297,12 @@ static int launch_tail(MgPlan* P, int l0, double* u, const double* b, double sig
     T.off_u = off; off += np;
     T.off_b = off; off += np;
     T.off_t = off; off += np;
+  }
+  a.lu_off = -1;
+  const int lu_n = a.m * a.m + a.m;
+  if (sizeof(double) * (off + lu_n) <= TAIL_SMEM_BUDGET + 8192) {
+    a.lu_off = off;
+    off += lu_n;
   }
   size_t smem = sizeof(double) * off;
   void (*kern)(TailArgs, const double*, double*, int, int) =
@@ -616,12 +631,13 @@ static int vcycle(MgPlan* P, int l, double* u, const double* b, double sigma, bo
   // u += P e_c, then post-smoothing; fused into the first post-sweep pass
   // when the TMA kernels cover this level (multigrid.py:250-251)
   int post = P->post;
-  if (zmarch_ok(L.g, L.c) && P->smoother == SM_RB && post >= 1) {
+  if (zmarch_ok(L.g, L.c) && zmarch_fuse_prolong() && P->smoother == SM_RB && post >= 1) {
     double* other = (cur == u) ? L.t : u;
     PL_TRY(zlaunch_rb(cur, b, other, L.g, L.c, sigma, P->omega, C.u, s));
     cur = other;
     post -= 1;
-  } else if (zmarch_ok(L.g, L.c) && P->smoother == SM_JACOBI && post >= 2) {
+  } else if (zmarch_ok(L.g, L.c) && zmarch_fuse_prolong() && P->smoother == SM_JACOBI &&
+             post >= 2) {
     double* other = (cur == u) ? L.t : u;
     PL_TRY(zlaunch_jacobi2(cur, b, other, L.g, L.c, sigma, P->omega, 0, C.u, s));
     cur = other;

@@ -52,6 +52,64 @@ __global__ void __launch_bounds__(256) k_prolong(const double* __restrict__ c,
   f[o] = accumulate ? f[o] + v : v;
 }
 
+// 3-D prolongation by coarse cell: thread (jx, jy, jz), 0 <= j <= nc, owns
+// the fine points 2j and 2j+1 per axis (even: average of coarse j-1 and j;
+// odd: copy of coarse j; transfers.py:40-45), reads the 2x2x2 coarse corners
+// once (zero outside the domain) and moves fine x-pairs as 16-byte vectors.
+// Per fine point the tree is lin_point's: z taps, then y, then x.
+__global__ void __launch_bounds__(256) k_prolong3_cell(const double* __restrict__ c,
+                                                       double* __restrict__ f, Geo gf, Geo gc,
+                                                       int accumulate) {
+  const int jx = blockIdx.x * 32 + threadIdx.x;
+  const int jy = blockIdx.y * 8 + threadIdx.y;
+  const int jz = blockIdx.z;
+  const int nc = gc.nx;
+  if (jx > nc || jy > nc) return;
+  double cr[2][2][2];   // [z][y][x] corners at j-1, j
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int b = 0; b < 2; ++b)
+#pragma unroll
+      for (int d = 0; d < 2; ++d) {
+        const int z = jz - 1 + a, y = jy - 1 + b, x = jx - 1 + d;
+        cr[a][b][d] = (z >= 0 && z < nc && y >= 0 && y < nc && x >= 0 && x < nc)
+                          ? __ldg(c + (long long)z * gc.sz + (long long)y * gc.sy + x)
+                          : 0.0;
+      }
+  const bool xo = jx < nc;   // fine 2j+1 exists along x
+#pragma unroll
+  for (int pz = 0; pz < 2; ++pz) {
+    if (pz == 1 && jz >= nc) break;
+    double zc[2][2];
+#pragma unroll
+    for (int b = 0; b < 2; ++b)
+#pragma unroll
+      for (int d = 0; d < 2; ++d)
+        zc[b][d] = pz == 0 ? 0.5 * (cr[0][b][d] + cr[1][b][d]) : cr[1][b][d];
+#pragma unroll
+    for (int py = 0; py < 2; ++py) {
+      if (py == 1 && jy >= nc) break;
+      const double y0 = py == 0 ? 0.5 * (zc[0][0] + zc[1][0]) : zc[1][0];
+      const double y1 = py == 0 ? 0.5 * (zc[0][1] + zc[1][1]) : zc[1][1];
+      const double ve = 0.5 * (y0 + y1), vo = y1;
+      double* dst = f + (long long)(2 * jz + pz) * gf.sz + (long long)(2 * jy + py) * gf.sy +
+                    2 * jx;
+      if (xo) {
+        double2 w = make_double2(ve, vo);
+        if (accumulate) {
+          const double2 o = *reinterpret_cast<const double2*>(dst);
+          w.x = o.x + w.x;
+          w.y = o.y + w.y;
+        }
+        *reinterpret_cast<double2*>(dst) = w;
+      } else {
+        dst[0] = accumulate ? dst[0] + ve : ve;
+      }
+    }
+  }
+}
+
 // One axis of the cubic interpolation (transfers.py:82-89): input viewed as
 // (A, Bin, C) with strides (ia, ib, 1) -> output (A, Bout, C) with strides
 // (oa, ob, 1), interpolating along B with sequential FMA over the taps
@@ -110,8 +168,14 @@ int launch_prolong(const double* coarse, double* fine, const Geo& gf, int accumu
                    cudaStream_t s) {
   Geo gc = coarse_geo(gf);
   PL_PRE(K_PROLONG);
-  PL_T_DISPATCH(gf, k_prolong, ceil_div(gf.npts, 256), 256, s, coarse, fine, gf, gc,
-                accumulate);
+  if (gf.dim == 3 && (gf.sy % 2) == 0) {
+    const int nc = gc.nx;
+    dim3 grid(ceil_div(nc + 1, 32), ceil_div(nc + 1, 8), nc + 1);
+    k_prolong3_cell<<<grid, dim3(32, 8), 0, s>>>(coarse, fine, gf, gc, accumulate);
+  } else {
+    PL_T_DISPATCH(gf, k_prolong, ceil_div(gf.npts, 256), 256, s, coarse, fine, gf, gc,
+                  accumulate);
+  }
   PL_CHECK_LAUNCH(K_PROLONG, (accumulate ? 16.0 : 8.0) * gf.npts + 8.0 * gc.npts);
   return 0;
 }

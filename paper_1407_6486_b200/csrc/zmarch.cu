@@ -28,6 +28,7 @@
 
 #include <cstring>
 #include <mutex>
+#include <type_traits>
 
 #include "common.cuh"
 #include "kernels.cuh"
@@ -579,6 +580,529 @@ __global__ void __launch_bounds__(NTHR_RB) k_zrb(const __grid_constant__ CUtenso
 }
 
 // ---------------------------------------------------------------------------
+// one fused jor-rb sweep, ONE barrier per plane (k_zrb2)
+//
+// Phase z updates the red points of plane z+2 and the black points of plane
+// z.  A red point reads only black neighbours (old values) and its own
+// centre; a black point reads the red points of planes z-1..z+1, final since
+// phases z-3..z-1.  The two sets touch disjoint data, so one barrier per
+// plane suffices.  Thread (row, px) owns the point pair (x0+2px, x0+2px+1)
+// of tile row `row` on every plane and keeps that pair for planes z-1..z+3
+// (and b for z..z+2) in registers: each plane is read from shared memory
+// once by its owner, the centre and z-neighbours of both updates come from
+// registers, only the x/y neighbours are shared-memory loads.  The 50 red
+// points of the tile's halo ring are updated by threads 0..49.  The division
+// by the (constant) diagonal is the correctly rounded quotient computed from
+// the host's 1/d (div_const); everything else is the reference expression
+// tree (multigrid.py:225-233), so the result is bit-identical to k_zrb.
+
+constexpr int NTHR_RB2 = 256;
+
+// correctly rounded a / b given y = RN(1/b): q0 = RN(a y) is within 1.5 ulp,
+// one Markstein correction makes it faithful, the second exact (Markstein's
+// theorem: y within half an ulp of 1/b, q faithful, remainder exact by FMA).
+// Zeros (sign), subnormals, huge values and non-finite a take the IEEE
+// division.
+__device__ __noinline__ double div_slow(double a, double b) { return a / b; }
+__device__ __forceinline__ double div_const(double a, double b, double y) {
+  double q = a * y;
+  double r = __fma_rn(-b, q, a);
+  q = __fma_rn(r, y, q);
+  r = __fma_rn(-b, q, a);
+  q = __fma_rn(r, y, q);
+  const double aa = fabs(a);
+  if (__builtin_expect(!(aa >= 0x1p-960 && aa <= 0x1p960), 0)) q = div_slow(a, b);
+  return q;
+}
+
+__device__ __forceinline__ double2 lds2(const double* p) {
+  return *reinterpret_cast<const double2*>(p);
+}
+__device__ __forceinline__ double sel(bool hi, const double2& v) { return hi ? v.y : v.x; }
+
+template <bool POW2, int RU, int RB>
+__global__ void __launch_bounds__(NTHR_RB2) k_zrb2(const __grid_constant__ CUtensorMap mu,
+                                                   const __grid_constant__ CUtensorMap mb,
+                                                   double* __restrict__ out, Geo g, OpC c,
+                                                   double sigma, double omega, double dval,
+                                                   double dinv, int zc) {
+  static_assert(RU >= 5 && RB >= 3, "ring too small");
+  extern __shared__ __align__(128) double sm[];
+  double* su = sm;
+  double* sb = su + RU * PU;
+  unsigned long long* bu = (unsigned long long*)(sb + RB * PB);
+  unsigned long long* bbar = bu + RU;
+  const int tid = threadIdx.x;
+  const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TY;
+  const int z0 = blockIdx.z * zc, z1 = min(z0 + zc, g.nz);
+  const int R = min(z1, g.nz - 1);          // last plane whose reds are needed
+  const int uhi = R + 1, bhi = R;           // last u / b plane staged
+  if (tid == 0) {
+    for (int i = 0; i < RU; ++i) mbar_init(bu + i, 1);
+    for (int i = 0; i < RB; ++i) mbar_init(bbar + i, 1);
+    fence_barrier_init();
+  }
+  __syncthreads();
+  // u plane p (z0-2 <= p <= uhi): slot (p-z0+2) % RU; b plane q (z0-1..bhi):
+  // slot (q-z0+1) % RB; the k-th use of a slot waits on parity k & 1
+  auto uplane = [&](int p) { return su + ((p - z0 + 2) % RU) * PU; };
+  auto bplane = [&](int q) { return sb + ((q - z0 + 1) % RB) * PB; };
+  auto issue_u = [&](int p) {
+    if (p > uhi) return;
+    const int k = (p - z0 + 2) % RU;
+    mbar_expect(bu + k, UX * UY * 8u);
+    tma3(su + k * PU, &mu, x0 - 2, y0 - 2, p, bu + k);
+  };
+  auto issue_b = [&](int q) {
+    if (q > bhi) return;
+    const int k = (q - z0 + 1) % RB;
+    mbar_expect(bbar + k, BW * BH * 8u);
+    tma3(sb + k * PB, &mb, x0 - 2, y0 - 1, q, bbar + k);
+  };
+  auto wait_u = [&](int p) {
+    const int k = p - z0 + 2;
+    mbar_wait(bu + k % RU, (unsigned)((k / RU) & 1));
+  };
+  auto wait_b = [&](int q) {
+    const int k = q - z0 + 1;
+    mbar_wait(bbar + k % RB, (unsigned)((k / RB) & 1));
+  };
+  if (tid == 0) {
+    for (int p = z0 - 2; p < z0 - 2 + RU; ++p) issue_u(p);
+    for (int q = z0 - 1; q < z0 - 1 + RB; ++q) issue_b(q);
+  }
+
+  // ---- per-thread geometry (fixed for all planes)
+  const int row = tid >> 4, px = tid & 15;
+  const int gy = y0 + row, gxa = x0 + 2 * px;
+  const bool va = gy < g.ny && gxa < g.nx, vb = gy < g.ny && gxa + 1 < g.nx;
+  const int iu = (row + 2) * UX + 2 * px + 2;     // first pair member, u window
+  const int ib = (row + 1) * BW + 2 * px + 2;     // first pair member, b window
+  double* optr = out + (long long)gy * g.sy + gxa;
+  // halo ring red point h = tid < 50, per plane parity P
+  int hu[2], hb[2];
+  bool hv[2];
+#pragma unroll
+  for (int P = 0; P < 2; ++P) {
+    int xx, yy;   // window-relative (tile origin = 0)
+    if (tid < 17) { yy = -1; xx = -1 + 2 * tid + (1 - P); }
+    else if (tid < 34) { yy = TY; xx = -1 + 2 * (tid - 17) + P; }
+    else if (tid < 42) { xx = -1; yy = 2 * (tid - 34) + P; }
+    else { xx = TX; yy = 2 * (tid - 42) + (1 - P); }
+    hu[P] = (yy + 2) * UX + xx + 2;
+    hb[P] = (yy + 1) * BW + xx + 2;
+    hv[P] = tid < 50 && x0 + xx >= 0 && x0 + xx < g.nx && y0 + yy >= 0 && y0 + yy < g.ny;
+  }
+  const int hu0 = hu[0], hu1 = hu[1], hb0 = hb[0], hb1 = hb[1];
+  const bool hv0 = hv[0], hv1 = hv[1];
+
+  auto lap = [&](double zm, double zp, double ym, double yp, double xm, double xp, double cc) {
+    double acc = 0.0;
+    acc = acc + dd2<POW2>((zm - 2.0 * cc) + zp, c);
+    acc = acc + dd2<POW2>((ym - 2.0 * cc) + yp, c);
+    acc = acc + dd2<POW2>((xm - 2.0 * cc) + xp, c);
+    return c.nu * acc;
+  };
+  auto relax = [&](double cc, double bv, double lp) {
+    const double r = bv - (cc - sigma * lp);
+    return cc + div_const(omega * r, dval, dinv);
+  };
+  // interior red member of the own pair on plane q (registers um, uc, up, bq)
+  auto red_own = [&](double* pl, const double2& um, double2& uc, const double2& up,
+                     const double2& bq, int q) {
+    const bool o = ((gy + q) & 1) == 0;             // red member: x odd <=> o
+    const double cc = sel(o, uc);
+    const double xo = pl[o ? iu + 2 : iu - 1];
+    const double xm = o ? uc.x : xo, xp = o ? xo : uc.y;
+    const double lp = lap(sel(o, um), sel(o, up), pl[iu - UX + o], pl[iu + UX + o], xm, xp, cc);
+    const double v = relax(cc, sel(o, bq), lp);
+    if ((o ? vb : va) && q >= 0 && q <= R) {
+      pl[iu + o] = v;
+      if (o) uc.y = v; else uc.x = v;
+    }
+  };
+  // halo red point on plane q (shared memory only)
+  auto red_halo = [&](int q) {
+    if (tid >= 50 || q < 0 || q > R) return;
+    const bool P = q & 1;
+    if (!(P ? hv1 : hv0)) return;
+    const int i = P ? hu1 : hu0;
+    double* pl = uplane(q);
+    const double* pm = uplane(q - 1);
+    const double* pp = uplane(q + 1);
+    const double cc = pl[i];
+    const double lp = lap(pm[i], pp[i], pl[i - UX], pl[i + UX], pl[i - 1], pl[i + 1], cc);
+    pl[i] = relax(cc, bplane(q)[P ? hb1 : hb0], lp);
+  };
+
+  // ---- prologue: reds of planes z0-1, z0, z0+1
+  for (int p = z0 - 2; p <= min(z0 + 2, uhi); ++p) wait_u(p);
+  for (int q = z0 - 1; q <= min(z0 + 1, bhi); ++q) wait_b(q);
+  double2 Um2 = lds2(uplane(z0 - 2) + iu);
+  double2 U0 = lds2(uplane(z0 - 1) + iu);
+  double2 U1 = lds2(uplane(z0) + iu);
+  double2 U2 = lds2(uplane(z0 + 1) + iu);
+  double2 U3 = z0 + 2 <= uhi ? lds2(uplane(z0 + 2) + iu) : make_double2(0.0, 0.0);
+  double2 Bm1 = lds2(bplane(z0 - 1) + ib);
+  double2 B0 = lds2(bplane(z0) + ib);
+  double2 B1 = z0 + 1 <= bhi ? lds2(bplane(z0 + 1) + ib) : make_double2(0.0, 0.0);
+  red_own(uplane(z0 - 1), Um2, U0, U1, Bm1, z0 - 1);
+  red_own(uplane(z0), U0, U1, U2, B0, z0);
+  if (z0 + 1 <= R) red_own(uplane(z0 + 1), U1, U2, U3, B1, z0 + 1);
+  red_halo(z0 - 1);
+  red_halo(z0);
+  red_halo(z0 + 1);
+  __syncthreads();
+  if (tid == 0) {
+    issue_u(z0 - 2 + RU);
+    issue_b(z0 - 1 + RB);
+  }
+
+  // ---- main loop: U0..U4 = own pair on planes z-1..z+3, B0..B2 = b on z..z+2
+  for (int z = z0; z < z1; ++z) {
+    const int q = z + 2;
+    const bool red = q <= R;
+    double2 U4 = make_double2(0.0, 0.0), B2 = make_double2(0.0, 0.0);
+    if (red) {
+      wait_u(q + 1);
+      wait_b(q);
+      U4 = lds2(uplane(q + 1) + iu);
+      B2 = lds2(bplane(q) + ib);
+      red_own(uplane(q), U2, U3, U4, B2, q);
+    }
+    // black member of the own pair on plane z
+    {
+      double* pl = uplane(z);
+      const bool o = ((gy + z) & 1) != 0;           // black member: x odd <=> o
+      const double cc = sel(o, U1);
+      const double xo = pl[o ? iu + 2 : iu - 1];
+      const double xm = o ? U1.x : xo, xp = o ? xo : U1.y;
+      const double lp = lap(sel(o, U0), sel(o, U2), pl[iu - UX + o], pl[iu + UX + o], xm, xp, cc);
+      const double v = relax(cc, sel(o, B0), lp);
+      double* dst = optr + (long long)z * g.sz;
+      const double2 w = o ? make_double2(U1.x, v) : make_double2(v, U1.y);
+      if (va && vb) *reinterpret_cast<double2*>(dst) = w;
+      else if (va) dst[0] = w.x;
+    }
+    red_halo(q);
+    __syncthreads();   // u plane z-1 and b plane z are free
+    if (tid == 0) {
+      issue_u(z - 1 + RU);
+      issue_b(z + RB);
+    }
+    U0 = U1; U1 = U2; U2 = U3; U3 = U4;
+    B0 = B1; B1 = B2;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// k_zrb3: k_zrb2's schedule with the colour made warp-uniform.  Warp w owns
+// tile rows 4(w/2) + (w&1) and that + 2, so (y + z) has one parity per warp
+// and plane; the phase code is instantiated per parity (no selects), the main
+// loop is unrolled by two planes, rings are powers of two, and b is read
+// from shared memory once per plane (by its red phase) into registers.
+// u plane p is read from shared memory in phases p-3 .. p, b plane q in
+// phase q-2 only, so the rings recycle as soon as possible.
+
+struct RbCtx {
+  double* su;
+  double* sb;
+  int z0, R;
+  int iu, ib;           // own pair (first member) in the u / b windows
+  bool va, vb;          // pair members in the domain
+  double* optr;         // global address of the pair on plane 0
+  long long sz;
+  int hu0, hu1, hb0, hb1;   // halo red point per plane parity
+  bool hv0, hv1;
+  OpC c;
+  double sigma, omega, dval, dinv;
+};
+
+template <int RU>
+__device__ __forceinline__ double* rb_u(const RbCtx& k, int p) {
+  return k.su + ((p - k.z0 + 2) & (RU - 1)) * PU;
+}
+template <int RB>
+__device__ __forceinline__ double* rb_b(const RbCtx& k, int q) {
+  return k.sb + ((q - k.z0 + 1) & (RB - 1)) * PB;
+}
+template <int O>
+__device__ __forceinline__ double mem(const double2& v) { return O ? v.y : v.x; }
+template <int O>
+__device__ __forceinline__ void set_mem(double2& v, double x) {
+  if (O) v.y = x; else v.x = x;
+}
+template <bool POW2>
+__device__ __forceinline__ double rb_relax(const RbCtx& k, double zm, double zp, double ym,
+                                           double yp, double xm, double xp, double cc,
+                                           double bv) {
+  double acc = 0.0;
+  acc = acc + dd2<POW2>((zm - 2.0 * cc) + zp, k.c);
+  acc = acc + dd2<POW2>((ym - 2.0 * cc) + yp, k.c);
+  acc = acc + dd2<POW2>((xm - 2.0 * cc) + xp, k.c);
+  const double lp = k.c.nu * acc;
+  const double r = bv - (cc - k.sigma * lp);
+  return cc + div_const(k.omega * r, k.dval, k.dinv);
+}
+
+// branch-free part of a relaxation: a = omega * r and the Markstein quotient
+// (valid when in_range(a)); the caller finishes with cc + quotient
+struct Relax {
+  double cc, a, q;
+};
+template <bool POW2>
+__device__ __forceinline__ Relax rb_fast(const RbCtx& k, double zm, double zp, double ym,
+                                         double yp, double xm, double xp, double cc, double bv) {
+  double acc = 0.0;
+  acc = acc + dd2<POW2>((zm - 2.0 * cc) + zp, k.c);
+  acc = acc + dd2<POW2>((ym - 2.0 * cc) + yp, k.c);
+  acc = acc + dd2<POW2>((xm - 2.0 * cc) + xp, k.c);
+  const double lp = k.c.nu * acc;
+  const double r = bv - (cc - k.sigma * lp);
+  Relax o;
+  o.cc = cc;
+  o.a = k.omega * r;
+  double q = o.a * k.dinv;
+  double e = __fma_rn(-k.dval, q, o.a);
+  q = __fma_rn(e, k.dinv, q);
+  e = __fma_rn(-k.dval, q, o.a);
+  o.q = __fma_rn(e, k.dinv, q);
+  return o;
+}
+__device__ __forceinline__ bool quot_ok(double a) {
+  const double aa = fabs(a);
+  return aa >= 0x1p-960 && aa <= 0x1p960;
+}
+template <bool POW2, int O>
+__device__ __forceinline__ Relax rb_point_fast(const RbCtx& k, const double* pl,
+                                               const double2& um, const double2& uc,
+                                               const double2& up, const double2& bq) {
+  const double xm = O ? uc.x : pl[k.iu - 1];
+  const double xp = O ? pl[k.iu + 2] : uc.y;
+  return rb_fast<POW2>(k, mem<O>(um), mem<O>(up), pl[k.iu - UX + O], pl[k.iu + UX + O], xm, xp,
+                       mem<O>(uc), mem<O>(bq));
+}
+
+// update member O of the own pair on plane q (pl); um/uc/up = own pair on
+// planes q-1, q, q+1 (uc updated), bq = b pair on q.  Returns the new value.
+template <bool POW2, int O>
+__device__ __forceinline__ double rb_point(const RbCtx& k, const double* pl, const double2& um,
+                                           const double2& uc, const double2& up,
+                                           const double2& bq) {
+  const double xm = O ? uc.x : pl[k.iu - 1];
+  const double xp = O ? pl[k.iu + 2] : uc.y;
+  return rb_relax<POW2>(k, mem<O>(um), mem<O>(up), pl[k.iu - UX + O], pl[k.iu + UX + O], xm, xp,
+                        mem<O>(uc), mem<O>(bq));
+}
+
+// halo red point (threads < 50) on plane q of parity P, shared memory only
+template <bool POW2, int RU, int RB, int P>
+__device__ __forceinline__ void rb_halo(const RbCtx& k, int q) {
+  const bool hv = P ? k.hv1 : k.hv0;
+  if (!hv || q > k.R || q < 0) return;
+  const int i = P ? k.hu1 : k.hu0;
+  double* pl = rb_u<RU>(k, q);
+  const double* pm = rb_u<RU>(k, q - 1);
+  const double* pp = rb_u<RU>(k, q + 1);
+  pl[i] = rb_relax<POW2>(k, pm[i], pp[i], pl[i - UX], pl[i + UX], pl[i - 1], pl[i + 1], pl[i],
+                         rb_b<RB>(k, q)[P ? k.hb1 : k.hb0]);
+}
+
+// one phase: red of plane z+2 (if <= R), black of plane z.  PAR = (y + z) & 1
+// of this warp's rows: red member 1 - PAR, black member PAR.  Both updates
+// are evaluated branch-free (independent chains the scheduler interleaves);
+// one warp-wide test sends out-of-range quotients to the IEEE division.
+template <bool POW2, int RU, int RB, int PAR>
+__device__ __forceinline__ void rb_phase(const RbCtx& k, int z, const double2& U0, double2& U1,
+                                         const double2& U2, double2& U3, const double2& U4,
+                                         const double2& B0, const double2& B2) {
+  const int q = z + 2;
+  double* plr = rb_u<RU>(k, q);
+  const double* plb = rb_u<RU>(k, z);
+  Relax rr = rb_point_fast<POW2, 1 - PAR>(k, plr, U2, U3, U4, B2);
+  Relax rbk = rb_point_fast<POW2, PAR>(k, plb, U0, U1, U2, B0);
+  if (__builtin_expect(!(quot_ok(rr.a) && quot_ok(rbk.a)), 0)) {
+    if (!quot_ok(rr.a)) rr.q = div_slow(rr.a, k.dval);
+    if (!quot_ok(rbk.a)) rbk.q = div_slow(rbk.a, k.dval);
+  }
+  const double vr = rr.cc + rr.q, vb = rbk.cc + rbk.q;
+  if (q <= k.R && (PAR ? k.va : k.vb)) {
+    plr[k.iu + 1 - PAR] = vr;
+    set_mem<1 - PAR>(U3, vr);
+  }
+  double* dst = k.optr + (long long)z * k.sz;
+  const double2 w = PAR ? make_double2(U1.x, vb) : make_double2(vb, U1.y);
+  if (k.va && k.vb) *reinterpret_cast<double2*>(dst) = w;
+  else if (k.va) dst[0] = w.x;
+}
+
+template <bool POW2, int RU, int RB>
+__global__ void __launch_bounds__(NTHR_RB2, 3) k_zrb3(const __grid_constant__ CUtensorMap mu,
+                                                      const __grid_constant__ CUtensorMap mb,
+                                                      double* __restrict__ out, Geo g, OpC c,
+                                                      double sigma, double omega, double dval,
+                                                      double dinv, int zc) {
+  static_assert((RU & (RU - 1)) == 0 && (RB & (RB - 1)) == 0 && RU >= 8 && RB >= 4, "rings");
+  extern __shared__ __align__(128) double sm[];
+  RbCtx k;
+  k.su = sm;
+  k.sb = sm + RU * PU;
+  unsigned long long* bu = (unsigned long long*)(k.sb + RB * PB);
+  unsigned long long* bbar = bu + RU;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TY;
+  const int z0 = blockIdx.z * zc, z1 = min(z0 + zc, g.nz);
+  k.z0 = z0;
+  k.R = min(z1, g.nz - 1);
+  const int uhi = k.R + 1, bhi = k.R;
+  k.c = c;
+  k.sigma = sigma;
+  k.omega = omega;
+  k.dval = dval;
+  k.dinv = dinv;
+  if (tid == 0) {
+    for (int i = 0; i < RU; ++i) mbar_init(bu + i, 1);
+    for (int i = 0; i < RB; ++i) mbar_init(bbar + i, 1);
+    fence_barrier_init();
+  }
+  __syncthreads();
+  auto issue_u = [&](int p) {
+    if (p > uhi) return;
+    const int s = (p - z0 + 2) & (RU - 1);
+    mbar_expect(bu + s, UX * UY * 8u);
+    tma3(k.su + s * PU, &mu, x0 - 2, y0 - 2, p, bu + s);
+  };
+  auto issue_b = [&](int q) {
+    if (q > bhi) return;
+    const int s = (q - z0 + 1) & (RB - 1);
+    mbar_expect(bbar + s, BW * BH * 8u);
+    tma3(k.sb + s * PB, &mb, x0 - 2, y0 - 1, q, bbar + s);
+  };
+  auto wait_u = [&](int p) {
+    const int i = p - z0 + 2;
+    mbar_wait(bu + (i & (RU - 1)), (unsigned)((i / RU) & 1));
+  };
+  auto wait_b = [&](int q) {
+    const int i = q - z0 + 1;
+    mbar_wait(bbar + (i & (RB - 1)), (unsigned)((i / RB) & 1));
+  };
+  if (tid == 0) {
+    for (int p = z0 - 2; p < z0 - 2 + RU; ++p) issue_u(p);
+    for (int q = z0 - 1; q < z0 - 1 + RB; ++q) issue_b(q);
+  }
+  // rows 4(w/2) + (w&1) (lanes 0-15) and +2 (lanes 16-31): one parity per warp
+  const int row = 4 * (warp >> 1) + (warp & 1) + 2 * (lane >> 4), px = lane & 15;
+  const int gy = y0 + row, gxa = x0 + 2 * px;
+  k.va = gy < g.ny && gxa < g.nx;
+  k.vb = gy < g.ny && gxa + 1 < g.nx;
+  k.iu = (row + 2) * UX + 2 * px + 2;
+  k.ib = (row + 1) * BW + 2 * px + 2;
+  k.optr = out + (long long)gy * g.sy + gxa;
+  k.sz = g.sz;
+  {
+    int hu[2], hb[2];
+    bool hv[2];
+#pragma unroll
+    for (int P = 0; P < 2; ++P) {
+      int xx, yy;
+      if (tid < 17) { yy = -1; xx = -1 + 2 * tid + (1 - P); }
+      else if (tid < 34) { yy = TY; xx = -1 + 2 * (tid - 17) + P; }
+      else if (tid < 42) { xx = -1; yy = 2 * (tid - 34) + P; }
+      else { xx = TX; yy = 2 * (tid - 42) + (1 - P); }
+      hu[P] = (yy + 2) * UX + xx + 2;
+      hb[P] = (yy + 1) * BW + xx + 2;
+      hv[P] = tid < 50 && x0 + xx >= 0 && x0 + xx < g.nx && y0 + yy >= 0 && y0 + yy < g.ny;
+    }
+    k.hu0 = hu[0]; k.hu1 = hu[1]; k.hb0 = hb[0]; k.hb1 = hb[1];
+    k.hv0 = hv[0]; k.hv1 = hv[1];
+  }
+  const int wpar = (y0 + row) & 1;   // = warp & 1 (y0 even)
+
+  // ---- prologue: reds of planes z0-1 (if >= 0), z0, z0+1 (if <= R)
+  for (int p = z0 - 2; p <= min(z0 + 2, uhi); ++p) wait_u(p);
+  for (int q = z0 - 1; q <= min(z0 + 1, bhi); ++q) wait_b(q);
+  const double2 zero2 = make_double2(0.0, 0.0);
+  double2 Um2 = lds2(rb_u<RU>(k, z0 - 2) + k.iu);
+  double2 U0 = lds2(rb_u<RU>(k, z0 - 1) + k.iu);
+  double2 U1 = lds2(rb_u<RU>(k, z0) + k.iu);
+  double2 U2 = lds2(rb_u<RU>(k, z0 + 1) + k.iu);
+  double2 U3 = z0 + 2 <= uhi ? lds2(rb_u<RU>(k, z0 + 2) + k.iu) : zero2;
+  const double2 Bm1 = lds2(rb_b<RB>(k, z0 - 1) + k.ib);
+  double2 B0 = lds2(rb_b<RB>(k, z0) + k.ib);
+  double2 B1 = z0 + 1 <= bhi ? lds2(rb_b<RB>(k, z0 + 1) + k.ib) : zero2;
+  // plane p red member: 1 - ((y + p) & 1); z0 even, so plane z0 has parity wpar
+  auto pro_red = [&](int q, const double2& um, double2& uc, const double2& up,
+                     const double2& bq, int par) {
+    if (q < 0 || q > k.R) return;
+    double* pl = rb_u<RU>(k, q);
+    if (par) {
+      const double v = c.pow2 ? rb_point<true, 0>(k, pl, um, uc, up, bq)
+                              : rb_point<false, 0>(k, pl, um, uc, up, bq);
+      if (k.va) { pl[k.iu] = v; uc.x = v; }
+    } else {
+      const double v = c.pow2 ? rb_point<true, 1>(k, pl, um, uc, up, bq)
+                              : rb_point<false, 1>(k, pl, um, uc, up, bq);
+      if (k.vb) { pl[k.iu + 1] = v; uc.y = v; }
+    }
+  };
+  pro_red(z0 - 1, Um2, U0, U1, Bm1, 1 - wpar);
+  pro_red(z0, U0, U1, U2, B0, wpar);
+  pro_red(z0 + 1, U1, U2, U3, B1, 1 - wpar);
+  if (tid < 50) {
+    rb_halo<POW2, RU, RB, 1>(k, z0 - 1);
+    rb_halo<POW2, RU, RB, 0>(k, z0);
+    rb_halo<POW2, RU, RB, 1>(k, z0 + 1);
+  }
+  __syncthreads();
+  if (tid == 0) {       // u planes z0-2, z0-1 and b planes z0-1 .. z0+1 are dead
+    issue_u(z0 - 2 + RU);
+    issue_u(z0 - 1 + RU);
+    for (int q = z0 - 1; q <= z0 + 1; ++q) issue_b(q + RB);
+  }
+
+  // ---- main loop, two planes per trip: U0..U3 = own pair on z-1..z+2,
+  // B0, B1 = b pair on z, z+1
+  auto run = [&](auto par_tag) {
+    constexpr int PA = decltype(par_tag)::value, PB = 1 - PA;
+    for (int z = z0; z < z1; z += 2) {
+      // plane z (parity PA)
+      if (z + 2 <= k.R) {
+        wait_u(z + 3);
+        wait_b(z + 2);
+      }
+      double2 U4 = lds2(rb_u<RU>(k, z + 3) + k.iu);   // stale beyond R: unused
+      const double2 B2 = lds2(rb_b<RB>(k, z + 2) + k.ib);
+      rb_phase<POW2, RU, RB, PA>(k, z, U0, U1, U2, U3, U4, B0, B2);
+      if (tid < 50) rb_halo<POW2, RU, RB, 0>(k, z + 2);
+      __syncthreads();
+      if (tid == 0) {
+        issue_u(z + RU);
+        issue_b(z + 2 + RB);
+      }
+      if (z + 1 >= z1) break;
+      // plane z+1 (parity PB)
+      if (z + 3 <= k.R) {
+        wait_u(z + 4);
+        wait_b(z + 3);
+      }
+      double2 U5 = lds2(rb_u<RU>(k, z + 4) + k.iu);
+      const double2 B3 = lds2(rb_b<RB>(k, z + 3) + k.ib);
+      rb_phase<POW2, RU, RB, PB>(k, z + 1, U1, U2, U3, U4, U5, B1, B3);
+      if (tid < 50) rb_halo<POW2, RU, RB, 1>(k, z + 3);
+      __syncthreads();
+      if (tid == 0) {
+        issue_u(z + 1 + RU);
+        issue_b(z + 3 + RB);
+      }
+      U0 = U2; U1 = U3; U2 = U4; U3 = U5;
+      B0 = B2; B1 = B3;
+    }
+  };
+  if (wpar) run(std::integral_constant<int, 1>{});
+  else run(std::integral_constant<int, 0>{});
+}
+
+// ---------------------------------------------------------------------------
 // fine (+)= P_cubic coarse for 3-D (transfers.py:82-89).  The coarse planes a
 // fine plane needs arrive by TMA (20 x 12 windows); per fine plane three
 // separable passes in shared memory -- z taps over the coarse window, y taps
@@ -726,6 +1250,202 @@ __global__ void __launch_bounds__(NTHR) k_cubic3(const double* __restrict__ coar
   }
 }
 
+// k_cubic4: k_cubic3's arithmetic (same passes, same FMA chains) as a skewed
+// three-stage pipeline with one barrier per fine plane: phase t runs the z
+// pass of fine plane z0+t (coarse ring -> zb[t&1]), the y pass of plane
+// z0+t-1 (zb -> yb[(t-1)&1]) and the x pass of plane z0+t-2 (yb -> fine).
+// Coarse windows arrive by TMA (zero-filled outside the domain) into an
+// 8-slot ring, issued as soon as a slot's plane is no longer needed.  Shared
+// memory is static (compile-time addresses); every tap is loaded from a safe
+// index and accumulated by a predicated FMA, so the chains are branch-free
+// and skip absent taps exactly like the reference's sparse rows.
+constexpr int RQ4 = 8;
+constexpr int PY4 = align16(TY * QW);
+
+// acc = chain_{u < n} w[u] * v[u] in tap order (v loaded for every u)
+__device__ __forceinline__ double tap_chain(int n, const double (&w)[4], double v0, double v1,
+                                            double v2, double v3) {
+  double acc = __fma_rn(w[0], v0, 0.0);
+  if (n > 1) acc = __fma_rn(w[1], v1, acc);
+  if (n > 2) acc = __fma_rn(w[2], v2, acc);
+  if (n > 3) acc = __fma_rn(w[3], v3, acc);
+  return acc;
+}
+
+constexpr int RF4 = 8;                       // fine-tile ring (accumulate mode)
+constexpr int PF4 = TX * TY;
+
+__global__ void __launch_bounds__(NTHR, 3) k_cubic4(const __grid_constant__ CUtensorMap mc,
+                                                 const __grid_constant__ CUtensorMap mf,
+                                                 double* __restrict__ fine, Geo gf,
+                                                 const int* __restrict__ tcnt,
+                                                 const int* __restrict__ tidx,
+                                                 const double* __restrict__ tw, int zc,
+                                                 int accumulate) {
+  __shared__ __align__(128) double sc[RQ4 * PQ];
+  __shared__ __align__(128) double zb[2 * PQ];
+  __shared__ __align__(128) double yb[2 * PY4];
+  __shared__ __align__(8) unsigned long long bar[RQ4];
+  __shared__ __align__(8) unsigned long long fbar[RF4];
+  __shared__ double s_zw[64 * 4];        // z taps of the chunk's fine planes (zc <= 64)
+  __shared__ int s_zj[64 * 4], s_zn[64];
+  extern __shared__ __align__(128) double sfine[];   // RF4 fine tiles (accumulate)
+  const int tid = threadIdx.y * 32 + threadIdx.x;
+  const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TY;
+  const int z0 = blockIdx.z * zc, z1 = min(z0 + zc, gf.nz);
+  const int n = z1 - z0;
+  const int cx0 = x0 / 2 - 2, cy0 = y0 / 2 - 2;
+  // tap windows are not monotone in the fine index (an odd row reaches one
+  // coarse plane below the even row before it and one above the even row
+  // after it): bounds take the last two planes into account
+  auto first_tap = [&](int iz) { return __ldg(tidx + iz * 4); };
+  auto last_tap = [&](int iz) { return __ldg(tidx + iz * 4 + __ldg(tcnt + iz) - 1); };
+  const int jlo = n > 1 ? min(first_tap(z0), first_tap(z0 + 1)) : first_tap(z0);
+  const int jtop = n > 1 ? max(last_tap(z1 - 1), last_tap(z1 - 2)) : last_tap(z1 - 1);
+  if (tid == 0) {
+    for (int i = 0; i < RQ4; ++i) mbar_init(bar + i, 1);
+    for (int i = 0; i < RF4; ++i) mbar_init(fbar + i, 1);
+    fence_barrier_init();
+  }
+  if (tid < n) {
+    const int iz = z0 + tid, nt = __ldg(tcnt + iz);
+    s_zn[tid] = nt;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      s_zj[tid * 4 + u] = __ldg(tidx + iz * 4 + min(u, nt - 1));   // absent: last tap
+      s_zw[tid * 4 + u] = u < nt ? __ldg(tw + iz * 4 + u) : 0.0;
+    }
+  }
+  __syncthreads();
+  auto issue_fine = [&](int p) {   // thread 0
+    if (!accumulate || p >= z1) return;
+    const int sl = (p - z0) & (RF4 - 1);
+    mbar_expect(fbar + sl, PF4 * 8u);
+    tma3(sfine + sl * PF4, &mf, x0, y0, p, fbar + sl);
+  };
+  if (tid == 0)
+    for (int p = z0; p < z0 + RF4; ++p) issue_fine(p);
+  int issued = jlo;     // thread 0: next coarse plane to issue
+  auto issue_upto = [&](int live_lo) {   // thread 0
+    for (; issued <= jtop && issued < live_lo + RQ4; ++issued) {
+      const int sl = (issued - jlo) & (RQ4 - 1);
+      mbar_expect(bar + sl, QW * QH * 8u);
+      tma3(sc + sl * PQ, &mc, cx0, cy0, issued, bar + sl);
+    }
+  };
+  if (tid == 0) issue_upto(jlo);
+  int waited = jlo;     // all threads: coarse planes [jlo, waited) have landed
+  // ---- x taps of this thread's fine column
+  const int gx = x0 + threadIdx.x;
+  const bool xin = gx < gf.nx;
+  int xn = 1, xi[4] = {0, 0, 0, 0};
+  double xw[4] = {0.0, 0.0, 0.0, 0.0};
+  if (xin) {
+    xn = __ldg(tcnt + gx);
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (u < xn) { xi[u] = __ldg(tidx + gx * 4 + u) - cx0; xw[u] = __ldg(tw + gx * 4 + u); }
+#pragma unroll
+    for (int u = 1; u < 4; ++u)
+      if (u >= xn) xi[u] = xi[0];
+  }
+  // ---- y taps of this thread's (up to two) y-pass entries
+  constexpr int PERY = (TY * QW + NTHR - 1) / NTHR;
+  static_assert(PERY == 2, "y pass layout");
+  int yn[2], yk[2], yi[2][4];
+  double yw[2][4];
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    const int k = tid + q * NTHR;
+    const int fy = k / QW, cx = k - fy * QW;
+    const int gy = y0 + fy;
+    yk[q] = k < TY * QW ? k : -1;
+    const bool ok = k < TY * QW && gy < gf.ny;
+    yn[q] = ok ? __ldg(tcnt + gy) : 1;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      yi[q][u] = cx;
+      yw[q][u] = 0.0;
+      if (ok && u < yn[q]) {
+        yi[q][u] = (__ldg(tidx + gy * 4 + u) - cy0) * QW + cx;
+        yw[q][u] = __ldg(tw + gy * 4 + u);
+      }
+    }
+#pragma unroll
+    for (int u = 1; u < 4; ++u)
+      if (u >= yn[q]) yi[q][u] = yi[q][0];
+  }
+  const bool zent = tid < QW * QH;
+  const int fy0 = threadIdx.y, fy1 = threadIdx.y + 8;
+  const bool r0 = xin && y0 + fy0 < gf.ny, r1 = xin && y0 + fy1 < gf.ny;
+  // fine addresses of the x pass, advanced one plane per phase
+  double* f0 = fine + gf.at(xin ? gx : 0, r0 ? y0 + fy0 : 0, 0) + (long long)(z0 - 2) * gf.sz;
+  double* f1 = fine + gf.at(xin ? gx : 0, r1 ? y0 + fy1 : 0, 0) + (long long)(z0 - 2) * gf.sz;
+  for (int t = 0; t < n + 2; ++t, f0 += gf.sz, f1 += gf.sz) {
+    // ---- x pass of fine plane z0+t-2: fine values first
+    const int ixp = z0 + t - 2;
+    const bool xpass = t >= 2;
+    const double* ftile = sfine + ((ixp - z0) & (RF4 - 1)) * PF4;
+    if (xpass && accumulate) {
+      const int k = ixp - z0;
+      mbar_wait(fbar + (k & (RF4 - 1)), (unsigned)((k / RF4) & 1));
+    }
+    // ---- z pass of fine plane z0+t
+    if (t < n) {
+      const int zn = s_zn[t];
+      int zj[4];
+      double zw[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) { zj[u] = s_zj[t * 4 + u]; zw[u] = s_zw[t * 4 + u]; }
+      for (; waited <= zj[3]; ++waited) {     // zj[3] = last tap (clamped)
+        const int k = waited - jlo;
+        mbar_wait(bar + (k & (RQ4 - 1)), (unsigned)((k / RQ4) & 1));
+      }
+      if (zent) {
+        const double* s0 = sc + ((zj[0] - jlo) & (RQ4 - 1)) * PQ + tid;
+        const double* s1 = sc + ((zj[1] - jlo) & (RQ4 - 1)) * PQ + tid;
+        const double* s2 = sc + ((zj[2] - jlo) & (RQ4 - 1)) * PQ + tid;
+        const double* s3 = sc + ((zj[3] - jlo) & (RQ4 - 1)) * PQ + tid;
+        zb[(t & 1) * PQ + tid] = tap_chain(zn, zw, *s0, *s1, *s2, *s3);
+      }
+    }
+    // ---- y pass of fine plane z0+t-1
+    if (t >= 1 && t <= n) {
+      const double* zs = zb + ((t - 1) & 1) * PQ;
+      double* yd = yb + ((t - 1) & 1) * PY4;
+#pragma unroll
+      for (int q = 0; q < 2; ++q)
+        if (yk[q] >= 0)
+          yd[yk[q]] = tap_chain(yn[q], yw[q], zs[yi[q][0]], zs[yi[q][1]], zs[yi[q][2]],
+                                zs[yi[q][3]]);
+    }
+    // ---- x pass (finish)
+    if (xpass) {
+      const double* ys = yb + (t & 1) * PY4;      // (t - 2) & 1
+      const double* ya = ys + fy0 * QW;
+      const double* yc = ys + fy1 * QW;
+      const double a0 = tap_chain(xn, xw, ya[xi[0]], ya[xi[1]], ya[xi[2]], ya[xi[3]]);
+      const double a1 = tap_chain(xn, xw, yc[xi[0]], yc[xi[1]], yc[xi[2]], yc[xi[3]]);
+      if (accumulate) {
+        if (r0) *f0 = ftile[fy0 * TX + threadIdx.x] + a0;
+        if (r1) *f1 = ftile[fy1 * TX + threadIdx.x] + a1;
+      } else {
+        if (r0) *f0 = a0;
+        if (r1) *f1 = a1;
+      }
+    }
+    __syncthreads();
+    if (tid == 0 && t >= 2) issue_fine(ixp + RF4);   // x pass of ixp done: slot free
+    // coarse planes below the first taps of fine planes z0+t+1, z0+t+2 are dead
+    if (tid == 0) {
+      int lo = jtop + 1;
+      if (t + 1 < n) lo = min(lo, s_zj[(t + 1) * 4]);
+      if (t + 2 < n) lo = min(lo, s_zj[(t + 2) * 4]);
+      issue_upto(lo);
+    }
+  }
+}
+
 constexpr int PREF1 = 3;
 constexpr int PREF2 = 3;
 
@@ -855,11 +1575,57 @@ int launch_zrb(const double* u, const double* b, const double* e, const Geo& gc,
   return 0;
 }
 
+int launch_zrb2(const double* u, const double* b, double* out, const Geo& g, const OpC& c,
+                double sigma, double omega, double dval, int variant, cudaStream_t s) {
+  CUtensorMap mu, mb;
+  PL_TRY(make_map(&mu, u, g, UX, UY));
+  PL_TRY(make_map(&mb, b, g, BW, BH));
+  int zc = pick_zc(g);
+  dim3 grid(ceil_div(g.nx, TX), ceil_div(g.ny, TY), ceil_div(g.nz, zc));
+  const double dinv = 1.0 / dval;
+#define PL_ZRB2(P2, RU, RB)                                                          \
+  do {                                                                              \
+    size_t smem = ((size_t)RU * PU + (size_t)RB * PB) * 8 + 8 * (RU + RB);          \
+    auto kern = k_zrb2<P2, RU, RB>;                                                 \
+    raise_smem(kern, smem);                                                         \
+    kern<<<grid, dim3(NTHR_RB2), smem, s>>>(mu, mb, out, g, c, sigma, omega, dval, dinv, zc); \
+  } while (0)
+  if (variant == 4) {
+    size_t smem = ((size_t)8 * PU + (size_t)4 * PB) * 8 + 8 * (8 + 4);
+    auto kern = c.pow2 ? k_zrb3<true, 8, 4> : k_zrb3<false, 8, 4>;
+    raise_smem(kern, smem);
+    kern<<<grid, dim3(NTHR_RB2), smem, s>>>(mu, mb, out, g, c, sigma, omega, dval, dinv, zc);
+  } else if (variant == 2) {
+    if (c.pow2) PL_ZRB2(true, 8, 4); else PL_ZRB2(false, 8, 4);
+  } else if (variant == 3) {
+    if (c.pow2) PL_ZRB2(true, 8, 6); else PL_ZRB2(false, 8, 6);
+  } else {
+    if (c.pow2) PL_ZRB2(true, 6, 4); else PL_ZRB2(false, 6, 4);
+  }
+#undef PL_ZRB2
+  return 0;
+}
+
+}  // namespace
+int g_cubic_variant = 1;    // 0: k_cubic3, 1: k_cubic4 (TMA ring, one barrier per plane)
+namespace {
+
 int launch_cubic3(const double* coarse, double* fine, const Geo& gf, const int* cnt,
                   const int* idx, const double* w, int accumulate, cudaStream_t s) {
   Geo gc = make_geo(3, (gf.N + 1) / 2);
   const int zc = pick_zc(gf);
   dim3 grid(ceil_div(gf.nx, TX), ceil_div(gf.ny, TY), ceil_div(gf.nz, zc)), block(32, 8);
+  if (g_cubic_variant == 1) {
+    CUtensorMap mc;
+    PL_TRY(make_map(&mc, coarse, gc, QW, QH));
+    CUtensorMap mf;
+    std::memset(&mf, 0, sizeof(mf));
+    if (accumulate) PL_TRY(make_map(&mf, fine, gf, TX, TY));
+    size_t smem = accumulate ? sizeof(double) * RF4 * PF4 : 0;
+    raise_smem(k_cubic4, smem);
+    k_cubic4<<<grid, block, smem, s>>>(mc, mf, fine, gf, cnt, idx, w, zc, accumulate);
+    return 0;
+  }
   size_t smem = sizeof(double) * (RQ * PQ + align16(QW * QH) + align16(QW * TY));
   raise_smem(k_cubic3, smem);
   k_cubic3<<<grid, block, smem, s>>>(coarse, gc, fine, gf, cnt, idx, w, zc, accumulate);
@@ -887,6 +1653,9 @@ double zdiag(const OpC& c, double sigma) {
 }
 
 int g_zmarch_enabled = 1;   // runtime knob (pl_set_option), for A/B tests
+int g_zrb_variant = 4;      // 0: k_zrb (3 barriers / plane), 1-3: k_zrb2 rings, 4: k_zrb3
+int g_fuse_prolong = 0;     // prolongation fused into the first post-sweep (slower since k_zrb3)
+bool zmarch_fuse_prolong() { return g_fuse_prolong != 0; }
 // smallest interior size for the TMA kernels: below it a CTA would march many
 // planes for few CTAs (latency-bound); the one-point-per-thread kernels win
 int g_zmarch_min_n = 127;
@@ -941,7 +1710,8 @@ int zlaunch_rb(const double* u, const double* b, double* out, const Geo& g, cons
   double dval = zdiag(c, sigma);
   Geo gc = make_geo(3, (g.N + 1) / 2);
   PL_PRE(K_RB);
-  PL_TRY(launch_zrb(u, b, e, gc, out, g, c, sigma, omega, dval, s));
+  if (e || g_zrb_variant == 0) PL_TRY(launch_zrb(u, b, e, gc, out, g, c, sigma, omega, dval, s));
+  else PL_TRY(launch_zrb2(u, b, out, g, c, sigma, omega, dval, g_zrb_variant, s));
   PL_CHECK_LAUNCH(K_RB, 24.0 * g.npts + (e ? 16.0 * g.npts + 8.0 * gc.npts : 0.0));
   return 0;
 }

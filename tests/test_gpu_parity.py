@@ -364,14 +364,24 @@ def test_cubic_zmarch_equals_pass_kernels(nf):
     (which are pinned to the reference by test_transfers_bitwise) bit for bit."""
     rng = np.random.default_rng(nf)
     c = dev(rng.standard_normal((nf // 2 - 1,) * 3))
-    outs = []
+    f = dev(rng.standard_normal((nf - 1,) * 3))
     _capi.set_option(_capi.OPT_ZMARCH_MIN_N, 31)
-    for z in (1, 0):
-        _capi.set_option(_capi.OPT_ZMARCH, z)
-        outs.append(transfers.interp_cubic(c))
-    _capi.set_option(_capi.OPT_ZMARCH, 1)
-    _capi.set_option(_capi.OPT_ZMARCH_MIN_N, 127)
-    assert torch.equal(outs[0], outs[1])
+    try:
+        _capi.set_option(_capi.OPT_ZMARCH, 0)
+        ref = transfers.interp_cubic(c)
+        ref_acc = f.clone()
+        transfers.interp_cubic_into(c, ref_acc, True)
+        _capi.set_option(_capi.OPT_ZMARCH, 1)
+        for variant in (0, 1):
+            _capi.set_option(_capi.OPT_CUBIC_VARIANT, variant)
+            assert torch.equal(transfers.interp_cubic(c), ref), variant
+            acc = f.clone()
+            transfers.interp_cubic_into(c, acc, True)
+            assert torch.equal(acc, ref_acc), variant
+    finally:
+        _capi.set_option(_capi.OPT_CUBIC_VARIANT, 1)
+        _capi.set_option(_capi.OPT_ZMARCH, 1)
+        _capi.set_option(_capi.OPT_ZMARCH_MIN_N, 127)
 
 
 @pytest.mark.parametrize("name", ["run_cfg3_small", "run_cfg4_small", "run_cfg4_small_tol"])
@@ -383,3 +393,51 @@ def test_pfasst_run_parity_tma_path(name):
         test_pfasst_run_parity(name)
     finally:
         _capi.set_option(_capi.OPT_ZMARCH_MIN_N, 127)
+
+
+@pytest.mark.parametrize("variant", [0, 1, 2, 3, 4])
+def test_zrb_variants_bitwise_31cubed(variant):
+    """Every jor-rb TMA sweep variant (three barriers per plane, and the
+    register-pipelined one-barrier kernels with their ring sizes) reproduces
+    the reference's red-black sweeps bit for bit on the 31^3 golden case."""
+    a, m = case("mg32_d3")
+    _capi.set_option(_capi.OPT_ZMARCH_MIN_N, 31)
+    _capi.set_option(_capi.OPT_ZRB_VARIANT, variant)
+    try:
+        sop = mg.ShiftedOperator(heat.HeatOperator(heat.Grid(3, 32)), m["sigma"])
+        for om in (1.0, 0.8):
+            cfg = mg.MgConfig(smoother="jor-rb", omega=om, pre_sweeps=2, post_sweeps=2)
+            for cnt in (1, 2, 3):
+                bitwise(mg.smooth(sop, dev(a["u"]), dev(a["b"]), cfg, cnt),
+                        a[f"sm{cnt}_jor-rb_{om:.3f}"])
+    finally:
+        _capi.set_option(_capi.OPT_ZRB_VARIANT, 4)
+        _capi.set_option(_capi.OPT_ZMARCH_MIN_N, 127)
+
+
+@pytest.mark.parametrize("n,length,sigma", [(128, 1.0, 1.0 / 128), (256, 1.0, 0.37),
+                                            (128, 3.0, 0.01)])
+@pytest.mark.parametrize("fuse", [1, 0])
+def test_zrb_variants_equal_plain_kernels(n, length, sigma, fuse):
+    """At 127^3 / 255^3 (several z chunks, ragged last tiles, a non-power-of-two
+    dx^2) every sweep variant, with and without the fused prolongation, gives
+    the plain one-colour kernels' V-cycle bit for bit."""
+    rng = np.random.default_rng(n + int(length))
+    g = heat.Grid(3, n, length)
+    u = dev(rng.standard_normal(g.shape))
+    b = dev(rng.standard_normal(g.shape))
+    sop = mg.ShiftedOperator(heat.HeatOperator(g), sigma)
+    cfg = mg.MgConfig("jor-rb", 1.0, 1, 1)
+    _capi.set_option(_capi.OPT_ZMARCH, 0)
+    ref = mg.v_cycle(sop, u, b, cfg)
+    ref_s = mg.smooth(sop, u, b, cfg, 2)
+    _capi.set_option(_capi.OPT_ZMARCH, 1)
+    _capi.set_option(_capi.OPT_FUSE_PROLONG, fuse)
+    try:
+        for variant in (0, 1, 2, 3, 4):
+            _capi.set_option(_capi.OPT_ZRB_VARIANT, variant)
+            assert torch.equal(mg.v_cycle(sop, u, b, cfg), ref), variant
+            assert torch.equal(mg.smooth(sop, u, b, cfg, 2), ref_s), variant
+    finally:
+        _capi.set_option(_capi.OPT_ZRB_VARIANT, 4)
+        _capi.set_option(_capi.OPT_FUSE_PROLONG, 0)

@@ -47,7 +47,11 @@ def main():
     ap.add_argument("--n", type=int, default=256)
     ap.add_argument("--reps", type=int, default=20)
     ap.add_argument("--only", default="")
+    ap.add_argument("--opts", default="", help="pl_set_option pairs KEY=VAL,...")
     args = ap.parse_args()
+    for kv in filter(None, args.opts.split(",")):
+        k, v = kv.split("=")
+        _capi.set_option(int(k), int(v))
     g = Grid(args.dim, args.n)
     N = g.dof
     rng = np.random.default_rng(0)
@@ -100,7 +104,7 @@ def main():
         run(f"sweep_M{M}_jorrb_V11",
             lambda st=st, y0=y0: sdc_sweep(st, y0, 1 / 64, op, MgConfig("jor-rb", 1.0, 1, 1),
                                            FixedCycles(1)), None or 0.0)
-    print(json.dumps({"dim": g.dim, "n": g.n, "dof": N, "kernels": res}))
+    print(json.dumps({"dim": g.dim, "n": g.n, "dof": N, "opts": args.opts, "kernels": res}))
 
 
 if __name__ == "__main__":
