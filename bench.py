@@ -163,8 +163,11 @@ def run_ours(args, w):
     u0_dev = to_device(u0_host)[0]            # device field in the library layout
     u0_pinned = torch.from_numpy(u0_host).pin_memory()
 
-    def step(u0):
-        return pfasst_run(levels, u0, dt * p, p, tol=w["tol"], max_iter=20, executor=executor)
+    streams = not args.no_streams
+
+    def step(u0, streams=streams):
+        return pfasst_run(levels, u0, dt * p, p, tol=w["tol"], max_iter=20, executor=executor,
+                          streams=streams)
 
     def barrier():
         if world > 1:
@@ -179,7 +182,7 @@ def run_ours(args, w):
     # which kernel dominates?  one untimed profiling block with events on all
     names = _capi.kind_names()
     _capi.timing_enable(names)
-    step(u0_dev)
+    step(u0_dev, streams=False)       # per-launch events: no cross-rank overlap
     barrier()
     per_kind = {n: _capi.timing_collect(n) for n in names}
     _capi.timing_enable(None)
@@ -216,7 +219,7 @@ def run_ours(args, w):
     r1 = torch.cuda.Event(enable_timing=True)
     r0.record(stream)
     for _ in range(args.steps):
-        step(u0_dev)
+        step(u0_dev, streams=False)
     r1.record(stream)
     barrier()
     ms_instr = r0.elapsed_time(r1)
@@ -229,7 +232,7 @@ def run_ours(args, w):
     te0 = time.perf_counter()
     for _ in range(args.steps):
         r = pfasst_run(levels, u0_pinned, dt * p, p, tol=w["tol"], max_iter=20,
-                       executor=executor)
+                       executor=executor, streams=streams)
         _ = r.u if isinstance(r.u, np.ndarray) else r.u.cpu()
     barrier()
     e2e_s = time.perf_counter() - te0
@@ -256,6 +259,7 @@ def run_ours(args, w):
                        "omega": w["omega"], "sweeps": [w["pre"], w["post"]],
                        "vcycles_per_substep": w["cycles"], "time_ranks": p, "dt": dt,
                        "tol": w["tol"], "max_iter": 20, "executor": executor,
+                       "rank_streams": streams,
                        "parallelism": f"time{world}",
                        "l2": "fields (>=133 MB) exceed the 126 MB L2; no flush needed",
                        "rank_iterations": res.rank_iterations[0],
@@ -404,6 +408,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="cfg3", choices=sorted(WORKLOADS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-streams", action="store_true",
+                    help="issue all time ranks on one stream (A/B of the wavefront overlap)")
     args = ap.parse_args()
     w = WORKLOADS[args.workload]
     if args.impl == "reference":

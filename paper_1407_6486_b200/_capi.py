@@ -118,6 +118,9 @@ OPT_GRAPHS = 2
 OPT_ZRB_VARIANT = 3
 OPT_FUSE_PROLONG = 4
 OPT_CUBIC_VARIANT = 5
+OPT_MID = 6
+OPT_MID_TAIL_N = 7
+OPT_RFW = 8
 
 
 def set_option(key, value):

@@ -83,7 +83,7 @@ void timing_post(int kind, cudaStream_t s, double alg_bytes) {
 static const char* kKindNames[K_NUM_KINDS] = {
     "apply", "jacobi", "jor_rb", "residual", "restrict", "prolong", "mg_tail", "norm",
     "quadrature", "rhs", "residual_max", "fas", "correction_time", "interp_cubic", "copy",
-    "lu"};
+    "lu", "mg_mid"};
 
 // ---------------------------------------------------------------------------
 // SDC sweep (sdc.py:84-114)
@@ -221,6 +221,9 @@ extern int g_zmarch_min_n;
 extern int g_zrb_variant;
 extern int g_fuse_prolong;
 extern int g_cubic_variant;
+extern int g_mid_enabled;
+extern int g_mid_tail_n;
+extern int g_rfw_enabled;
 }
 
 extern "C" {
@@ -242,6 +245,18 @@ int pl_set_option(int key, int value) {
       return -1;
     }
     g_zrb_variant = value;
+    return 0;
+  }
+  if (key == PL_OPT_RFW) {
+    g_rfw_enabled = value != 0;
+    return 0;
+  }
+  if (key == PL_OPT_MID) {
+    g_mid_enabled = value != 0;
+    return 0;
+  }
+  if (key == PL_OPT_MID_TAIL_N) {
+    g_mid_tail_n = value;
     return 0;
   }
   if (key == PL_OPT_CUBIC_VARIANT) {

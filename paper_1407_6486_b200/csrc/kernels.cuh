@@ -41,6 +41,11 @@ int zlaunch_jacobi2(const double* u, const double* b, double* out, const Geo& g,
 int zlaunch_rb(const double* u, const double* b, double* out, const Geo& g, const OpC& c,
                double sigma, double omega, const double* e, cudaStream_t s);
 
+// coarse = FW(b - (I - sigma A) u) in one pass (residual never stored)
+bool zmarch_rfw();   // PL_OPT_RFW
+int zlaunch_rfw(const double* u, const double* b, double* coarse, const Geo& g, const OpC& c,
+                double sigma, cudaStream_t s);
+
 // fine (+)= P_cubic coarse, 3-D, TMA-staged coarse planes (taps of cubic_taps)
 int zlaunch_cubic(const double* coarse, double* fine, const Geo& gf, const int* cnt,
                   const int* idx, const double* w, int accumulate, cudaStream_t s);

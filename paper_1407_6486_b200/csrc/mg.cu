@@ -17,6 +17,9 @@
 #include "mg.h"
 #include "transfer_dev.cuh"
 
+#include <cooperative_groups.h>
+namespace cg = cooperative_groups;
+
 namespace pl {
 
 // ---------------------------------------------------------------------------
@@ -200,12 +203,10 @@ __device__ void tail_lu(const TailArgs& a, const double* lu, const double* b, do
   __syncthreads();
 }
 
+// the whole V-cycle of the tail levels by one CTA in shared memory
 template <int DIM>
-__global__ void __launch_bounds__(TAIL_THREADS) k_tail(TailArgs a,
-                                                       const double* __restrict__ b_in,
-                                                       double* u_io, int zero_guess,
-                                                       int ncycles) {
-  extern __shared__ double sm[];
+__device__ void tail_run(const TailArgs& a, const double* __restrict__ b_in, double* u_io,
+                         int zero_guess, int ncycles, double* sm) {
   const TailLevel& L0 = a.lv[0];
   if (a.lu_off >= 0)
     for (int i = threadIdx.x; i < a.m * a.m + a.m; i += blockDim.x) sm[a.lu_off + i] = a.lu[i];
@@ -266,11 +267,139 @@ __global__ void __launch_bounds__(TAIL_THREADS) k_tail(TailArgs a,
   }
 }
 
+template <int DIM>
+__global__ void __launch_bounds__(TAIL_THREADS) k_tail(TailArgs a,
+                                                       const double* __restrict__ b_in,
+                                                       double* u_io, int zero_guess,
+                                                       int ncycles) {
+  extern __shared__ double sm[];
+  tail_run<DIM>(a, b_in, u_io, zero_guess, ncycles, sm);
+}
+
+// ---------------------------------------------------------------------------
+// cooperative "mid" V-cycle: the grid-wide levels below the TMA threshold plus
+// the tail in ONE persistent launch.  Each former kernel becomes a phase of a
+// grid-stride loop separated by grid-wide barriers: per level and sweep one
+// red and one black phase (colour points only, in place), then residual and
+// full weighting on the way down; prolongation and the post-sweeps on the way
+// up; CTA 0 runs the tail levels (shared memory, dense LU) in between.  The
+// per-point arithmetic is that of k_rb / k_residual / fw_point / lin_point,
+// so results are bit-identical to the separate launches.
+
+constexpr int MID_THREADS = 1024;
+constexpr int MID_MAX = 8;
+
+struct MidLevel {
+  double* u;
+  double* b;
+  double* t;
+  Geo g;
+  OpC c;
+};
+
+struct MidArgs {
+  int nmid;                 // grid-wide levels 0 .. nmid-1; level nmid starts the tail
+  MidLevel lv[MID_MAX + 1];
+  int pre, post;
+  double omega, sigma;
+  int zero;                 // level 0 starts from a zero guess
+};
+
+// one colour of jor-rb, in place (k_rb arithmetic); zero: u == 0 on entry,
+// so red points get 0 + (omega b) / d and black points are set to 0
+template <int DIM>
+__device__ __forceinline__ void mid_colour(const MidLevel& L, const MidArgs& m, int red,
+                                           bool zero, long long gt, long long gs) {
+  const Geo& g = L.g;
+  if (zero) {
+    for (long long t = gt; t < g.npts; t += gs) {
+      int x, y, z;
+      decode_point(g, t, x, y, z);
+      const long long idx = g.at(x, y, z);
+      if (is_red<DIM>(x, y, z)) {
+        const double d = shifted_diag<DIM>(g, L.c, m.sigma, x, y, z);
+        L.u[idx] = 0.0 + ((m.omega * L.b[idx]) / d);
+      } else {
+        L.u[idx] = 0.0;
+      }
+    }
+    return;
+  }
+  const int N = g.nx, H = (N + 1) / 2;
+  const long long cnt = (long long)H * g.ny * g.nz;
+  for (long long t = gt; t < cnt; t += gs) {
+    const unsigned tt = (unsigned)t;
+    const unsigned row = tt / (unsigned)H;
+    const int h = (int)(tt - row * (unsigned)H);
+    const int z = (int)(row / (unsigned)g.ny);
+    const int y = (int)(row - (unsigned)z * (unsigned)g.ny);
+    const int x = 2 * h + (((y + z + DIM) & 1) ^ red ^ 1);
+    if (x >= N) continue;
+    const long long idx = g.at(x, y, z);
+    const double d = shifted_diag<DIM>(g, L.c, m.sigma, x, y, z);
+    const double r = L.b[idx] - shifted_point<DIM>(L.u, g, L.c, m.sigma, x, y, z, idx);
+    L.u[idx] = L.u[idx] + ((m.omega * r) / d);
+  }
+}
+
+template <int DIM>
+__global__ void __launch_bounds__(MID_THREADS) k_mid(MidArgs m, TailArgs ta) {
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ double sm[];
+  const long long gt = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long gs = (long long)gridDim.x * blockDim.x;
+  for (int l = 0; l < m.nmid; ++l) {
+    const MidLevel& L = m.lv[l];
+    const MidLevel& C = m.lv[l + 1];
+    const bool zero = l == 0 ? m.zero != 0 : true;
+    if (zero && m.pre == 0) {
+      for (long long t = gt; t < L.g.nstore; t += gs) L.u[t] = 0.0;
+      grid.sync();
+    }
+    for (int k = 0; k < m.pre; ++k) {
+      mid_colour<DIM>(L, m, 1, zero && k == 0, gt, gs);
+      grid.sync();
+      mid_colour<DIM>(L, m, 0, false, gt, gs);
+      grid.sync();
+    }
+    for (long long t = gt; t < L.g.npts; t += gs) {       // residual (k_residual)
+      int x, y, z;
+      decode_point(L.g, t, x, y, z);
+      const long long idx = L.g.at(x, y, z);
+      L.t[idx] = L.b[idx] - shifted_point<DIM>(L.u, L.g, L.c, m.sigma, x, y, z, idx);
+    }
+    grid.sync();
+    for (long long t = gt; t < C.g.npts; t += gs) {       // full weighting (k_fw)
+      int x, y, z;
+      decode_point(C.g, t, x, y, z);
+      C.b[C.g.at(x, y, z)] = fw_point<DIM>(L.t, L.g, x, y, z);
+    }
+    grid.sync();
+  }
+  if (blockIdx.x == 0) tail_run<DIM>(ta, m.lv[m.nmid].b, m.lv[m.nmid].u, 1, 1, sm);
+  grid.sync();
+  for (int l = m.nmid - 1; l >= 0; --l) {
+    const MidLevel& L = m.lv[l];
+    const MidLevel& C = m.lv[l + 1];
+    for (long long t = gt; t < L.g.npts; t += gs) {       // u += P_lin e (k_prolong)
+      int x, y, z;
+      decode_point(L.g, t, x, y, z);
+      const long long idx = L.g.at(x, y, z);
+      L.u[idx] = L.u[idx] + lin_point<DIM>(C.u, C.g, x, y, z);
+    }
+    grid.sync();
+    for (int k = 0; k < m.post; ++k) {
+      mid_colour<DIM>(L, m, 1, false, gt, gs);
+      grid.sync();
+      mid_colour<DIM>(L, m, 0, false, gt, gs);
+      if (l > 0 || k + 1 < m.post) grid.sync();
+    }
+  }
+}
+
 }  // namespace
 
-static int launch_tail(MgPlan* P, int l0, double* u, const double* b, double sigma,
-                       int zero_guess, int ncycles, cudaStream_t s) {
-  TailArgs a;
+static int tail_args(MgPlan* P, int l0, double sigma, TailArgs& a, size_t* smem_out) {
   std::memset(&a, 0, sizeof(a));
   a.smoother = P->smoother;
   a.pre = P->pre;
@@ -304,7 +433,15 @@ static int launch_tail(MgPlan* P, int l0, double* u, const double* b, double sig
     a.lu_off = off;
     off += lu_n;
   }
-  size_t smem = sizeof(double) * off;
+  *smem_out = sizeof(double) * off;
+  return 0;
+}
+
+static int launch_tail(MgPlan* P, int l0, double* u, const double* b, double sigma,
+                       int zero_guess, int ncycles, cudaStream_t s) {
+  TailArgs a;
+  size_t smem = 0;
+  PL_TRY(tail_args(P, l0, sigma, a, &smem));
   void (*kern)(TailArgs, const double*, double*, int, int) =
       P->dim == 1 ? k_tail<1> : (P->dim == 2 ? k_tail<2> : k_tail<3>);
   static bool attr_set[4] = {false, false, false, false};
@@ -317,6 +454,73 @@ static int launch_tail(MgPlan* P, int l0, double* u, const double* b, double sig
   kern<<<1, TAIL_THREADS, smem, s>>>(a, b, u, zero_guess, ncycles);
   double bytes = 8.0 * P->lv[l0].g.npts * (zero_guess ? 2 : 3);
   PL_CHECK_LAUNCH(K_TAIL, bytes);
+  return 0;
+}
+
+int g_mid_enabled = 1;      // PL_OPT_MID
+int g_mid_tail_n = 7;       // PL_OPT_MID_TAIL_N: largest N the mid kernel leaves to its tail
+
+// first tail level of the mid kernel (>= the plan's tail_start)
+static int mid_tail_level(const MgPlan* P) {
+  for (int l = 0; l < (int)P->lv.size(); ++l)
+    if (l >= P->tail_start && P->lv[l].g.N <= g_mid_tail_n) return l;
+  return P->tail_start;
+}
+
+static bool mid_applies(const MgPlan* P, int l) {
+  return g_mid_enabled && P->dim == 3 && P->order == 2 && P->smoother == SM_RB &&
+         l < mid_tail_level(P) && mid_tail_level(P) - l <= MID_MAX;
+}
+
+static int launch_mid(MgPlan* P, int l0, double* u, const double* b, double sigma, int zero,
+                      cudaStream_t s) {
+  const int lt = mid_tail_level(P);
+  MidArgs m;
+  std::memset(&m, 0, sizeof(m));
+  m.nmid = lt - l0;
+  m.pre = P->pre;
+  m.post = P->post;
+  m.omega = P->omega;
+  m.sigma = sigma;
+  m.zero = zero;
+  double bytes = 0.0;
+  for (int i = 0; i <= m.nmid; ++i) {
+    const MgLevel& L = P->lv[l0 + i];
+    MidLevel& M = m.lv[i];
+    M.u = i == 0 ? u : L.u;
+    M.b = i == 0 ? const_cast<double*>(b) : L.b;
+    M.t = L.t;
+    M.g = L.g;
+    M.c = L.c;
+    if (i < m.nmid) {   // the unfused kernels' algorithmic bytes
+      const double np = (double)L.g.npts, nc = (double)P->lv[l0 + i + 1].g.npts;
+      bytes += np * (24.0 * (P->pre + P->post) + 24.0 + 8.0 + 16.0) + nc * 16.0;
+    }
+  }
+  TailArgs ta;
+  size_t smem = 0;
+  PL_TRY(tail_args(P, lt, sigma, ta, &smem));
+  static int grid = 0;
+  if (grid == 0) {
+    int dev = 0, sms = 0, per = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaFuncSetAttribute(k_mid<3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)TAIL_SMEM_BUDGET + 8192);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_mid<3>, MID_THREADS,
+                                                  TAIL_SMEM_BUDGET + 8192);
+    grid = sms * (per > 0 ? 1 : 1);
+    if (per < 1) {
+      set_error("mid kernel does not fit one CTA per SM");
+      return 2;
+    }
+  }
+  void* args[] = {&m, &ta};
+  PL_PRE(K_MID);
+  cudaError_t e = cudaLaunchCooperativeKernel((void*)k_mid<3>, grid, MID_THREADS, args, smem, s);
+  if (e != cudaSuccess) return cuda_status(e, "cooperative mid launch");
+  bytes += 8.0 * P->lv[lt].g.npts * 3;
+  PL_CHECK_LAUNCH(K_MID, bytes);
   return 0;
 }
 
@@ -620,13 +824,19 @@ static int level_smooth(MgPlan* P, MgLevel& L, double** cur, double* alt_u, cons
 static int vcycle(MgPlan* P, int l, double* u, const double* b, double sigma, bool zero,
                   cudaStream_t s) {
   if (l >= P->tail_start) return launch_tail(P, l, u, b, sigma, zero, 1, s);
+  if (!zmarch_ok(P->lv[l].g, P->lv[l].c) && mid_applies(P, l))
+    return launch_mid(P, l, u, b, sigma, zero, s);
   MgLevel& L = P->lv[l];
   MgLevel& C = P->lv[l + 1];
   double* cur = u;
   PL_TRY(level_smooth(P, L, &cur, u, b, sigma, P->pre, zero, s));
-  double* r = (cur == u) ? L.t : u;
-  PL_TRY(launch_residual(cur, b, r, L.g, L.c, sigma, s));
-  PL_TRY(launch_fw(r, C.b, L.g, s));
+  if (zmarch_ok(L.g, L.c) && zmarch_rfw()) {
+    PL_TRY(zlaunch_rfw(cur, b, C.b, L.g, L.c, sigma, s));
+  } else {
+    double* r = (cur == u) ? L.t : u;
+    PL_TRY(launch_residual(cur, b, r, L.g, L.c, sigma, s));
+    PL_TRY(launch_fw(r, C.b, L.g, s));
+  }
   PL_TRY(vcycle(P, l + 1, C.u, C.b, sigma, true, s));
   // u += P e_c, then post-smoothing; fused into the first post-sweep pass
   // when the TMA kernels cover this level (multigrid.py:250-251)

@@ -32,6 +32,7 @@
 
 #include "common.cuh"
 #include "kernels.cuh"
+#include "transfer_dev.cuh"
 
 namespace pl {
 
@@ -1250,6 +1251,140 @@ __global__ void __launch_bounds__(NTHR) k_cubic3(const double* __restrict__ coar
   }
 }
 
+// k_rfw: coarse b = FW(b - (I - sigma A) u) in one pass (multigrid.py:245-246;
+// transfers.py:27-34).  A CTA owns a 16 x 8 coarse tile; each thread owns up
+// to three fine (x, y) points of the 33 x 17 residual window (fine x0..x0+32,
+// y0..y0+16).  Marching up the fine planes it evaluates its residuals from
+// TMA-staged u (halo 1) and b windows and folds them into the z weights in
+// registers in fw3's operation order (0.25 * ((a + 2 b) + c): a at plane 2jz,
+// t = a + 2 b at 2jz+1, 0.25 * (t + c) at 2jz+2, which is also the next
+// coarse plane's a).  The z-weighted plane goes to shared memory; the y pass
+// runs in the next phase and the x pass in the one after -- one barrier per
+// fine plane, and the fine residual is never stored.  Residual arithmetic is
+// k_z1<Z_RESID>'s and the weights fw_point's: the coarse right-hand side is
+// bit-identical to residual + full_weighting.
+constexpr int RX = TX + 1, RY = TY + 1, PR = align16(RX * RY);     // residual window
+constexpr int FUX = TX + 4, FUY = TY + 3, PFU = align16(FUX * FUY);  // u window
+constexpr int FBX = TX + 2, FBY = TY + 1, PFB = align16(FBX * FBY);  // b window
+constexpr int RFW_RU = 5, RFW_RB = 3;
+
+template <bool POW2>
+__global__ void __launch_bounds__(NTHR, 4) k_rfw(const __grid_constant__ CUtensorMap mu,
+                                                 const __grid_constant__ CUtensorMap mb,
+                                                 double* __restrict__ coarse, Geo gf, Geo gc,
+                                                 OpC c, double sigma, int zcc) {
+  extern __shared__ __align__(128) double sm[];
+  double* su = sm;                            // RFW_RU u windows
+  double* sb = su + RFW_RU * PFU;             // RFW_RB b windows
+  double* szb = sb + RFW_RB * PFB;            // z-weighted plane (RX x RY)
+  double* syx = szb + PR;                     // y-weighted rows (RX x TY/2)
+  unsigned long long* bu = (unsigned long long*)(syx + PR);
+  unsigned long long* bb = bu + RFW_RU;
+  const int tid = threadIdx.y * 32 + threadIdx.x;
+  const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TY;
+  const int jz0 = blockIdx.z * zcc, jz1 = min(jz0 + zcc, gc.nz);
+  const int p0 = 2 * jz0, p1 = 2 * jz1;       // residual planes p0 .. p1
+  const int ulo = p0 - 1, uhi = p1 + 1;       // u planes
+  if (tid == 0) {
+    for (int i = 0; i < RFW_RU; ++i) mbar_init(bu + i, 1);
+    for (int i = 0; i < RFW_RB; ++i) mbar_init(bb + i, 1);
+    fence_barrier_init();
+  }
+  __syncthreads();
+  auto issue_u = [&](int p) {
+    if (p > uhi) return;
+    const int s = (p - ulo) % RFW_RU;
+    mbar_expect(bu + s, FUX * FUY * 8u);
+    tma3(su + s * PFU, &mu, x0 - 2, y0 - 1, p, bu + s);
+  };
+  auto issue_b = [&](int p) {
+    if (p > p1) return;
+    const int s = (p - p0) % RFW_RB;
+    mbar_expect(bb + s, FBX * FBY * 8u);
+    tma3(sb + s * PFB, &mb, x0, y0, p, bb + s);
+  };
+  auto wait_u = [&](int p) {
+    const int k = p - ulo;
+    mbar_wait(bu + k % RFW_RU, (unsigned)((k / RFW_RU) & 1));
+  };
+  auto wait_b = [&](int p) {
+    const int k = p - p0;
+    mbar_wait(bb + k % RFW_RB, (unsigned)((k / RFW_RB) & 1));
+  };
+  if (tid == 0) {
+    for (int p = ulo; p < ulo + RFW_RU; ++p) issue_u(p);
+    for (int p = p0; p < p0 + RFW_RB; ++p) issue_b(p);
+  }
+  // owned residual points: window index k -> u / b window offsets
+  constexpr int PERR = (RX * RY + NTHR - 1) / NTHR;
+  int r_k[PERR], r_iu[PERR], r_ib[PERR];
+  bool r_ok[PERR];
+#pragma unroll
+  for (int q = 0; q < PERR; ++q) {
+    const int k = tid + q * NTHR;
+    const int ry = k / RX, rx = k - ry * RX;
+    r_k[q] = k < RX * RY ? k : -1;
+    r_iu[q] = (ry + 1) * FUX + rx + 2;
+    r_ib[q] = ry * FBX + rx;
+    r_ok[q] = k < RX * RY && x0 + rx < gf.nx && y0 + ry < gf.ny;
+  }
+  double acc[PERR];
+#pragma unroll
+  for (int q = 0; q < PERR; ++q) acc[q] = 0.0;
+  // coarse point of this thread (threads 0..127) in the 16 x 8 tile
+  const int cx = tid & 15, cy = tid >> 4;
+  const int gcx = x0 / 2 + cx, gcy = y0 / 2 + cy;
+  const bool c_ok = tid < (TX / 2) * (TY / 2) && gcx < gc.nx && gcy < gc.ny;
+  for (int p = p0; p <= p1 + 2; ++p) {
+    const int ph = p - p0;
+    if (p <= p1) {
+      // ---- residuals of plane p, folded into the z weights
+      if (ph == 0) { wait_u(p - 1); wait_u(p); }
+      wait_u(p + 1);
+      wait_b(p);
+      const double* pm = su + ((p - 1 - ulo) % RFW_RU) * PFU;
+      const double* pc = su + ((p - ulo) % RFW_RU) * PFU;
+      const double* pp = su + ((p + 1 - ulo) % RFW_RU) * PFU;
+      const double* pb = sb + ((p - p0) % RFW_RB) * PFB;
+#pragma unroll
+      for (int q = 0; q < PERR; ++q) {
+        if (r_k[q] < 0) continue;
+        double v = 0.0;
+        if (r_ok[q]) {
+          const int i = r_iu[q];
+          const double lap = lap7<POW2, FUX>(pm, pc, pp, i, c);
+          const double au = pc[i] - sigma * lap;
+          v = pb[r_ib[q]] - au;
+        }
+        if (ph == 0) {
+          acc[q] = v;                                  // a of coarse plane jz0
+        } else if (ph & 1) {
+          acc[q] = acc[q] + 2.0 * v;                   // t = a + 2 b
+        } else {
+          szb[r_k[q]] = 0.25 * (acc[q] + v);           // z weight of plane (p-2)/2
+          acc[q] = v;                                  // a of the next coarse plane
+        }
+      }
+    }
+    if ((ph & 1) == 1 && ph >= 3) {                    // y pass of jz = (p - 3) / 2
+      for (int k = tid; k < RX * (TY / 2); k += NTHR) {
+        const int yy = k / RX, xx = k - yy * RX;
+        const double* zc = szb + 2 * yy * RX + xx;
+        syx[k] = fw3(zc[0], zc[RX], zc[2 * RX]);
+      }
+    }
+    if ((ph & 1) == 0 && ph >= 4 && c_ok) {            // x pass of jz = (p - 4) / 2
+      const double* yr = syx + cy * RX + 2 * cx;
+      coarse[gc.at(gcx, gcy, (p - 4) / 2)] = fw3(yr[0], yr[1], yr[2]);
+    }
+    __syncthreads();
+    if (tid == 0 && p <= p1) {
+      issue_u(p - 1 + RFW_RU);    // u plane p-1 is free after the residuals of p
+      issue_b(p + RFW_RB);        // b plane p is free
+    }
+  }
+}
+
 // k_cubic4: k_cubic3's arithmetic (same passes, same FMA chains) as a skewed
 // three-stage pipeline with one barrier per fine plane: phase t runs the z
 // pass of fine plane z0+t (coarse ring -> zb[t&1]), the y pass of plane
@@ -1610,6 +1745,21 @@ int launch_zrb2(const double* u, const double* b, double* out, const Geo& g, con
 int g_cubic_variant = 1;    // 0: k_cubic3, 1: k_cubic4 (TMA ring, one barrier per plane)
 namespace {
 
+int launch_rfw(const double* u, const double* b, double* coarse, const Geo& g, const OpC& c,
+               double sigma, cudaStream_t s) {
+  Geo gc = make_geo(3, (g.N + 1) / 2);
+  CUtensorMap mu, mb;
+  PL_TRY(make_map(&mu, u, g, FUX, FUY));
+  PL_TRY(make_map(&mb, b, g, FBX, FBY));
+  const int zcc = pick_zc(g) / 2 < 4 ? 4 : pick_zc(g) / 2;
+  dim3 grid(ceil_div(g.nx, TX), ceil_div(g.ny, TY), ceil_div(gc.nz, zcc)), block(32, 8);
+  size_t smem = sizeof(double) * (RFW_RU * PFU + RFW_RB * PFB + 2 * PR) + 8 * (RFW_RU + RFW_RB);
+  auto kern = c.pow2 ? k_rfw<true> : k_rfw<false>;
+  raise_smem(kern, smem);
+  kern<<<grid, block, smem, s>>>(mu, mb, coarse, g, gc, c, sigma, zcc);
+  return 0;
+}
+
 int launch_cubic3(const double* coarse, double* fine, const Geo& gf, const int* cnt,
                   const int* idx, const double* w, int accumulate, cudaStream_t s) {
   Geo gc = make_geo(3, (gf.N + 1) / 2);
@@ -1666,6 +1816,19 @@ bool zmarch_ok(const Geo& g, const OpC& c) {
   // TMA needs 16-byte row and plane strides: the padded device layout
   return g_zmarch_enabled && g.dim == 3 && c.order == 2 && g.N >= g_zmarch_min_n && g.N >= 31 &&
          (g.sy % 2) == 0;
+}
+
+int g_rfw_enabled = 1;     // PL_OPT_RFW: fused residual + full weighting
+bool zmarch_rfw() { return g_rfw_enabled != 0; }
+
+int zlaunch_rfw(const double* u, const double* b, double* coarse, const Geo& g, const OpC& c,
+                double sigma, cudaStream_t s) {
+  Geo gc = make_geo(3, (g.N + 1) / 2);
+  PL_PRE(K_RESTRICT);
+  PL_TRY(launch_rfw(u, b, coarse, g, c, sigma, s));
+  // algorithmic bytes of the unfused pair (residual 24 B, FW 8 B + 8 B coarse)
+  PL_CHECK_LAUNCH(K_RESTRICT, 32.0 * g.npts + 8.0 * gc.npts);
+  return 0;
 }
 
 int zlaunch_apply(const double* u, double* f, const Geo& g, const OpC& c, cudaStream_t s) {

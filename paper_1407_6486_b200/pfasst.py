@@ -13,6 +13,14 @@ iteration, convergence freezing, block chaining.  Three executors:
     which time ranks n+1..P-1 of iteration k are still queued -- the GPU never
     drains waiting for the host.  ("threaded" is the reference's bitwise-
     identical alternative executor; here it is the same device schedule.)
+    With ``streams=True`` every time rank issues on its own CUDA
+    stream in wavefront order (anti-diagonals n + k): iteration k of rank n
+    depends only on iteration k of rank n-1 (its payloads, copied at the
+    start) and on iteration k-1 of itself, so latency-bound work of one rank
+    (coarse sweeps, small multigrid levels) overlaps the bandwidth-bound fine
+    sweeps of others.  Two events per rank order the hand-offs: "done"
+    (payload final) and "copied" (successor took its copy, the state may be
+    overwritten).  Results and traces are those of the serial order.
 ``"nccl"``
     one process per GPU (torch.distributed, NCCL over NVLink/NVSwitch), time
     rank n on process n mod G.  Fine / coarse hand-offs are NCCL send/recv of
@@ -79,13 +87,15 @@ class _PreCoarse(Hooks):
 class DeviceEngine:
     """Owns the TimeStep state of the time ranks of this process (one GPU)."""
 
-    def __init__(self, levels, dt, ranks):
+    def __init__(self, levels, dt, ranks, streams=False):
         self.levels = levels
         self.dt = dt
         self.L = len(levels)
         self.ranks = list(ranks)
         self.ts = {}
         self.spread_y = {}
+        self.streams = {n: torch.cuda.Stream() for n in self.ranks} if streams else None
+        self._coarse_in = {}
         self._res = zeros((max(self.ranks) + 1 if self.ranks else 1,))
         self._res_host = torch.zeros(self._res.shape, dtype=torch.float64,
                                      pin_memory=True)
@@ -139,6 +149,21 @@ class DeviceEngine:
         ts.set_y0(0, t)
         ts.states[0].y[0].copy_(t)
         self.levels[0].operator.apply_into(ts.states[0].y[0], ts.states[0].f[0])
+
+    def stream(self, n):
+        """Context issuing rank n's work (its own stream in wavefront mode)."""
+        import contextlib
+        return torch.cuda.stream(self.streams[n]) if self.streams else contextlib.nullcontext()
+
+    def stage_coarse(self, n, t):
+        """Copy of the predecessor's coarse payload, taken at the start of the
+        iteration (the predecessor may move on afterwards)."""
+        buf = self._coarse_in.get(n)
+        if buf is None:
+            buf = self._coarse_in[n] = clone_field(t)
+        else:
+            buf.copy_(t)
+        return buf
 
     # -- work ----------------------------------------------------------------
     def burn_in(self, n):
@@ -401,6 +426,57 @@ class _Block:
             self._resolve(n)
 
 
+    def iterations_wavefront(self):
+        """The iteration loop issued by anti-diagonals d = n + k (descending n
+        inside a diagonal), one CUDA stream per rank.  Convergence decisions
+        are taken exactly as in the serial loop; only the issue order and the
+        overlap on the device differ."""
+        e, p = self.e, self.p
+        caller = torch.cuda.current_stream()
+        for n in range(p):
+            e.streams[n].wait_stream(caller)
+        done_ev = [None] * p       # rank n's payload of its latest issued iteration is final
+        copied_ev = [None] * p     # rank n took its copies of rank n-1's payload
+        issued = [0] * p
+        stopped = [False] * p
+        for d in range(1, self.max_iter + p):
+            for n in range(p - 1, -1, -1):
+                k = d - n
+                if k < 1 or k > self.max_iter or stopped[n]:
+                    continue
+                self._resolve(n)
+                if self.frozen[n]:
+                    stopped[n] = True
+                    continue
+                st = e.streams[n]
+                with torch.cuda.stream(st):
+                    pre = None
+                    if n > 0:
+                        st.wait_event(done_ev[n - 1])
+                        e.set_fine_y0(n, e.fine_payload(n - 1))
+                        coarse = e.stage_coarse(n, e.coarse_payload(n - 1))
+                        pre = (lambda ts, n=n, c=coarse: e.set_coarse_y0(n, c))
+                        copied_ev[n] = torch.cuda.Event()
+                        copied_ev[n].record(st)
+                    # the successor's copy of this rank's previous payload
+                    if n + 1 < p and issued[n + 1] == k - 1 and copied_ev[n + 1] is not None:
+                        st.wait_event(copied_ev[n + 1])
+                    cyc = e.iteration(n, pre)
+                    handle = e.residual(n)
+                    done_ev[n] = torch.cuda.Event()
+                    done_ev[n].record(st)
+                    if self.record and n == p - 1:
+                        self.final_values.append(e.snapshot(e.fine_payload(n)))
+                self.vcycles[n] += cyc
+                self.iterations[n] = k
+                issued[n] = k
+                self.pending[n] = (k, cyc, handle)
+        for n in self.mine:
+            self._resolve(n)
+        for n in range(p):
+            caller.wait_stream(e.streams[n])
+
+
 def _gather_block(blk, exchange):
     """Combine per-process bookkeeping (nccl executor)."""
     if not isinstance(exchange, DistExchange):
@@ -425,11 +501,13 @@ def _world(group):
 
 def pfasst_run(levels, u0, t_end: float, p: int, blocks: int = 1, tol: float = 1e-9,
                max_iter: int = 20, executor: str = "serial", record_final_values: bool = False,
-               engine_factory=None, group=None) -> PfasstResult:
+               engine_factory=None, group=None, streams: bool = False) -> PfasstResult:
     """Run PFASST / IPFASST over ``blocks`` windows of ``p`` steps (pfasst.py:256-287).
 
     ``u0`` may be a numpy array (result returned on the host, drop-in) or an
-    fp64 CUDA tensor (result stays on the device)."""
+    fp64 CUDA tensor (result stays on the device).  ``streams`` (single
+    process only) issues each time rank on its own CUDA stream in wavefront
+    order; results are identical either way."""
     check_hierarchy(levels)
     if executor not in ("serial", "threaded", "nccl"):
         raise ValueError(f"unknown executor {executor!r}")
@@ -454,14 +532,19 @@ def pfasst_run(levels, u0, t_end: float, p: int, blocks: int = 1, tol: float = 1
             exchange = DistExchange(engine, group)
         else:
             if engine is None:
-                engine = engine_factory(levels, dt, range(p))
+                engine = (DeviceEngine(levels, dt, range(p), streams=streams)
+                          if engine_factory is DeviceEngine else
+                          engine_factory(levels, dt, range(p)))
             exchange = _LocalExchange(engine)
         for n in range(p):
             if exchange.owns(n):
                 engine.spread(n, u)
         blk = _Block(engine, exchange, p, tol, max_iter, block, record_final_values)
         blk.predictor()
-        blk.iterations_loop()
+        if isinstance(exchange, _LocalExchange) and getattr(engine, "streams", None):
+            blk.iterations_wavefront()
+        else:
+            blk.iterations_loop()
         if isinstance(exchange, DistExchange):
             exchange.finish()
             last = (p - 1) % exchange.world

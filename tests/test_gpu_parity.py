@@ -441,3 +441,69 @@ def test_zrb_variants_equal_plain_kernels(n, length, sigma, fuse):
     finally:
         _capi.set_option(_capi.OPT_ZRB_VARIANT, 4)
         _capi.set_option(_capi.OPT_FUSE_PROLONG, 0)
+
+
+@pytest.mark.parametrize("n", [32, 64, 128, 256])
+@pytest.mark.parametrize("pre,post,omega", [(1, 1, 1.0), (2, 0, 0.9), (0, 2, 1.0), (3, 2, 0.8)])
+def test_cooperative_mid_vcycle_equals_separate_launches(n, pre, post, omega):
+    """The cooperative launch that runs every V-cycle level below the TMA
+    threshold (and the one-CTA tail) reproduces the per-level launches bit for
+    bit: from a guess and from zero, for every tail split."""
+    rng = np.random.default_rng(7 * n + pre)
+    g = heat.Grid(3, n)
+    u = dev(rng.standard_normal(g.shape))
+    b = dev(rng.standard_normal(g.shape))
+    sop = mg.ShiftedOperator(heat.HeatOperator(g), 0.013)
+    cfg = mg.MgConfig("jor-rb", omega, pre, post)
+    _capi.set_option(_capi.OPT_MID, 0)
+    ref = mg.v_cycle(sop, u, b, cfg)
+    ref0 = mg.v_cycle(sop, torch.zeros_like(u), b, cfg)
+    try:
+        _capi.set_option(_capi.OPT_MID, 1)
+        for tail_n in (3, 7, 15):
+            _capi.set_option(_capi.OPT_MID_TAIL_N, tail_n)
+            assert torch.equal(mg.v_cycle(sop, u, b, cfg), ref), tail_n
+            assert torch.equal(mg.v_cycle(sop, torch.zeros_like(u), b, cfg), ref0), tail_n
+    finally:
+        _capi.set_option(_capi.OPT_MID, 1)
+        _capi.set_option(_capi.OPT_MID_TAIL_N, 7)
+
+
+@pytest.mark.parametrize("name", ["run_cfg1", "run_cfg2_small", "run_cfg3_small", "run_cfg4_small_tol"])
+def test_pfasst_rank_streams_identical(name):
+    """The wavefront schedule with one CUDA stream per time rank gives exactly
+    the single-stream results: final value, counts, convergence, trace."""
+    a, m = case(name)
+    levels = levels_from(m)
+    t_end = m["dt"] * m["p"] * m["blocks"]
+    kw = dict(blocks=m["blocks"], tol=m["tol"], max_iter=20, record_final_values=True)
+    r1 = pfasst.pfasst_run(levels, dev(a["u0"]), t_end, m["p"], streams=False, **kw)
+    r2 = pfasst.pfasst_run(levels, dev(a["u0"]), t_end, m["p"], streams=True, **kw)
+    assert torch.equal(r1.u, r2.u)
+    assert r1.rank_iterations == r2.rank_iterations
+    assert r1.rank_vcycles == r2.rank_vcycles
+    assert r1.converged == r2.converged
+    assert [(t.block, t.rank, t.iteration, t.residual, t.vcycles) for t in r1.trace] == \
+        [(t.block, t.rank, t.iteration, t.residual, t.vcycles) for t in r2.trace]
+    for b1, b2 in zip(r1.final_values, r2.final_values):
+        assert all(torch.equal(x, y) for x, y in zip(b1, b2))
+
+
+@pytest.mark.parametrize("n,length", [(128, 1.0), (256, 1.0), (128, 3.0)])
+def test_fused_residual_restriction(n, length):
+    """coarse b = FW(b - A_sigma u) in one pass equals residual + full weighting
+    (inside whole V-cycles, pre-sweeps 0..2)."""
+    rng = np.random.default_rng(n + 5)
+    g = heat.Grid(3, n, length)
+    u = dev(rng.standard_normal(g.shape))
+    b = dev(rng.standard_normal(g.shape))
+    sop = mg.ShiftedOperator(heat.HeatOperator(g), 0.021)
+    try:
+        for pre in (0, 1, 2):
+            cfg = mg.MgConfig("jor-rb", 1.0, pre, 1)
+            _capi.set_option(_capi.OPT_RFW, 0)
+            ref = mg.v_cycle(sop, u, b, cfg)
+            _capi.set_option(_capi.OPT_RFW, 1)
+            assert torch.equal(mg.v_cycle(sop, u, b, cfg), ref), pre
+    finally:
+        _capi.set_option(_capi.OPT_RFW, 1)
