@@ -76,8 +76,10 @@ const char* pl_last_error(void);
 #define PL_OPT_MID 6          /* 1 (default): V-cycle levels below the TMA threshold and the tail
                                  run as one cooperative launch (3-D order-2 jor-rb) */
 #define PL_OPT_MID_TAIL_N 7   /* largest n-1 the cooperative kernel leaves to its one-CTA tail
-                                 (default 7) */
+                                 (default 15) */
 #define PL_OPT_RFW 8          /* 1 (default): residual + full weighting fused (TMA levels) */
+#define PL_OPT_ZC_FLOOR 9     /* smallest z-chunk of the TMA kernels (power of two, default 16) */
+#define PL_OPT_FAST_TAIL 10   /* 1 (default): compile-time-sized 15^3/7^3 -> 3^3 jor-rb tail */
 int pl_set_option(int key, int value);
 
 /* storage elements of one field (incl. row pads) */

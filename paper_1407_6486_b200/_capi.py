@@ -20,7 +20,7 @@ PL_MAX_NODES = 17
 SMOOTHERS = {"jacobi": 0, "gauss-seidel": 1, "jor-rb": 2}
 RESTRICT = {"full-weighting": 0, "inject": 1, "copy": 2}
 STATUS = {0: "fixed", 1: "converged", 2: "stalled"}
-NUM_KINDS = 16
+NUM_KINDS = 17          # refreshed from the library by num_kinds()
 
 _lib = None
 _lock = threading.Lock()
@@ -108,6 +108,17 @@ def lib():
     return _lib
 
 
+def num_kinds():
+    """Number of kernel kinds the loaded library reports (pl_kind_name)."""
+    global NUM_KINDS
+    h = lib()
+    k = 0
+    while k < 64 and h.pl_kind_name(k).decode() != "?":
+        k += 1
+    NUM_KINDS = k
+    return k
+
+
 class MultigridErrorBase(RuntimeError):
     pass
 
@@ -121,6 +132,8 @@ OPT_CUBIC_VARIANT = 5
 OPT_MID = 6
 OPT_MID_TAIL_N = 7
 OPT_RFW = 8
+OPT_ZC_FLOOR = 9
+OPT_FAST_TAIL = 10
 
 
 def set_option(key, value):
@@ -144,11 +157,12 @@ def check(rc, what=""):
 
 def stats():
     """(launches, alg_bytes) per kernel kind since the last reset."""
-    n = (i64 * NUM_KINDS)()
-    b = (f64 * NUM_KINDS)()
-    lib().pl_stats_get(n, b, NUM_KINDS)
-    names = [lib().pl_kind_name(k).decode() for k in range(NUM_KINDS)]
-    return {names[k]: (int(n[k]), float(b[k])) for k in range(NUM_KINDS)}
+    nk = num_kinds()
+    n = (i64 * nk)()
+    b = (f64 * nk)()
+    lib().pl_stats_get(n, b, nk)
+    names = [lib().pl_kind_name(k).decode() for k in range(nk)]
+    return {names[k]: (int(n[k]), float(b[k])) for k in range(nk)}
 
 
 def stats_reset():
@@ -156,14 +170,14 @@ def stats_reset():
 
 
 def kind_index(name):
-    for k in range(NUM_KINDS):
+    for k in range(num_kinds()):
         if lib().pl_kind_name(k).decode() == name:
             return k
     raise KeyError(name)
 
 
 def kind_names():
-    return [lib().pl_kind_name(k).decode() for k in range(NUM_KINDS)]
+    return [lib().pl_kind_name(k).decode() for k in range(num_kinds())]
 
 
 def timing_enable(names):

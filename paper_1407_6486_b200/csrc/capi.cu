@@ -224,6 +224,8 @@ extern int g_cubic_variant;
 extern int g_mid_enabled;
 extern int g_mid_tail_n;
 extern int g_rfw_enabled;
+extern int g_zc_floor;
+extern int g_fast_tail;
 }
 
 extern "C" {
@@ -245,6 +247,18 @@ int pl_set_option(int key, int value) {
       return -1;
     }
     g_zrb_variant = value;
+    return 0;
+  }
+  if (key == PL_OPT_FAST_TAIL) {
+    g_fast_tail = value != 0;
+    return 0;
+  }
+  if (key == PL_OPT_ZC_FLOOR) {
+    if (value < 2 || (value & (value - 1))) {
+      set_error("z chunk floor must be a power of two >= 2");
+      return PL_ERR_ARG;
+    }
+    g_zc_floor = value;
     return 0;
   }
   if (key == PL_OPT_RFW) {

@@ -9,6 +9,7 @@
 // arithmetic (common.cuh / transfer_dev.cuh), so where a level runs does not
 // change a single bit of the result.
 #include <cmath>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <vector>
@@ -46,6 +47,8 @@ OpC make_opc(int n, double length, double nu, int order) {
 // ---------------------------------------------------------------------------
 // single-CTA tail
 
+int g_fast_tail = 1;   // PL_OPT_FAST_TAIL
+
 namespace {
 
 constexpr int TAIL_THREADS = 1024;
@@ -68,6 +71,7 @@ struct TailArgs {
   const double* lu;   // m*m factors + m pivots (global)
   int m;
   int lu_off;         // >= 0: factors staged in shared memory at this offset
+  int fast;           // 15 or 7: compile-time-sized 3-D order-2 jor-rb path (ft_*)
 };
 
 #define PL_FOR_SM_POINTS(g)                                                  \
@@ -203,11 +207,162 @@ __device__ void tail_lu(const TailArgs& a, const double* lu, const double* b, do
   __syncthreads();
 }
 
+// ---------------------------------------------------------------------------
+// fast tail: 3-D order-2 jor-rb tails 15^3 -> 7^3 -> 3^3 (LU, 27 unknowns) or
+// 7^3 -> 3^3 with compile-time level sizes (index arithmetic folds away),
+// colour-only sweeps and the LU solve as a register/shuffle chain in one
+// warp.  Per point it calls the generic tail's device functions
+// (shifted_point, shifted_diag, fw_point, lin_point) in the same order, so
+// the result is bit-identical to tail_run's generic path.
+
+template <int N>
+__device__ __forceinline__ Geo ct_geo() {
+  Geo g;
+  g.dim = 3;
+  g.N = N;
+  g.nx = N;
+  g.ny = N;
+  g.nz = N;
+  g.sy = N;
+  g.sz = N * N;
+  g.npts = N * N * N;
+  g.nstore = N * N * N;
+  return g;
+}
+
+template <int N>
+__device__ __forceinline__ void ft_colour(double* u, const double* b, const OpC& c, double sigma,
+                                          double omega, int red, bool zero) {
+  const Geo g = ct_geo<N>();
+  if (zero) {   // u == 0 on entry: red points 0 + (omega b) / d, black points 0
+    for (int p = threadIdx.x; p < N * N * N; p += blockDim.x) {
+      const int x = p % N, y = (p / N) % N, z = p / (N * N);
+      if (is_red<3>(x, y, z)) {
+        const double d = shifted_diag<3>(g, c, sigma, x, y, z);
+        u[p] = 0.0 + ((omega * b[p]) / d);
+      } else {
+        u[p] = 0.0;
+      }
+    }
+    return;
+  }
+  constexpr int H = (N + 1) / 2;
+  for (int t = threadIdx.x; t < H * N * N; t += blockDim.x) {
+    const int h = t % H, row = t / H;
+    const int y = row % N, z = row / N;
+    const int x = 2 * h + (((y + z + 3) & 1) ^ red ^ 1);
+    if (x >= N) continue;
+    const int p = (z * N + y) * N + x;
+    const double d = shifted_diag<3>(g, c, sigma, x, y, z);
+    const double r = b[p] - shifted_point<3>(u, g, c, sigma, x, y, z, p);
+    u[p] = u[p] + ((omega * r) / d);
+  }
+}
+
+// LAPACK getrs order (tail_lu) for m = 27: lane i of warp 0 holds u[i]
+__device__ __forceinline__ void ft_lu27(const double* A, const double* b, double* u) {
+  constexpr int m = 27;
+  if (threadIdx.x < 32) {
+    const int lane = threadIdx.x;
+    const double* piv = A + m * m;
+    // the sequential row interchanges, traced back to the source row
+    int q = lane;
+    for (int i = m - 1; i >= 0; --i) {
+      const int pi = (int)piv[i];
+      if (q == i) q = pi;
+      else if (q == pi) q = i;
+    }
+    double v = lane < m ? b[q] : 0.0;
+    for (int j = 0; j < m; ++j) {              // L y = P b (unit lower)
+      const double yj = __shfl_sync(0xffffffffu, v, j);
+      if (lane > j && lane < m) v = __fma_rn(-yj, A[lane * m + j], v);
+    }
+    for (int j = m - 1; j >= 0; --j) {          // U x = y
+      if (lane == j) v = v / A[j * m + j];
+      const double xj = __shfl_sync(0xffffffffu, v, j);
+      if (lane < j) v = __fma_rn(-xj, A[lane * m + j], v);
+    }
+    if (lane < m) u[lane] = v;
+  }
+  __syncthreads();
+}
+
+template <int N, int L>
+__device__ void ft_level(const TailArgs& a, double* sm, bool zero) {
+  const TailLevel& T = a.lv[L];
+  double* u = sm + T.off_u;
+  double* b = sm + T.off_b;
+  if constexpr (N == 3) {
+    ft_lu27(sm + a.lu_off, b, u);
+  } else {
+    constexpr int NC = (N - 1) / 2;
+    double* t = sm + T.off_t;
+    const Geo g = ct_geo<N>();
+    const Geo gc = ct_geo<NC>();
+    if (zero && a.pre == 0) {
+      for (int p = threadIdx.x; p < N * N * N; p += blockDim.x) u[p] = 0.0;
+      __syncthreads();
+    }
+    for (int k = 0; k < a.pre; ++k) {
+      ft_colour<N>(u, b, T.c, a.sigma, a.omega, 1, zero && k == 0);
+      __syncthreads();
+      ft_colour<N>(u, b, T.c, a.sigma, a.omega, 0, false);
+      __syncthreads();
+    }
+    for (int p = threadIdx.x; p < N * N * N; p += blockDim.x) {
+      const int x = p % N, y = (p / N) % N, z = p / (N * N);
+      t[p] = b[p] - shifted_point<3>(u, g, T.c, a.sigma, x, y, z, p);
+    }
+    __syncthreads();
+    const TailLevel& C = a.lv[L + 1];
+    double* bc = sm + C.off_b;
+    for (int p = threadIdx.x; p < NC * NC * NC; p += blockDim.x) {
+      const int x = p % NC, y = (p / NC) % NC, z = p / (NC * NC);
+      bc[p] = fw_point<3>(t, g, x, y, z);
+    }
+    __syncthreads();
+    ft_level<NC, L + 1>(a, sm, true);
+    const double* ec = sm + C.off_u;
+    for (int p = threadIdx.x; p < N * N * N; p += blockDim.x) {
+      const int x = p % N, y = (p / N) % N, z = p / (N * N);
+      u[p] = u[p] + lin_point<3>(ec, gc, x, y, z);
+    }
+    __syncthreads();
+    for (int k = 0; k < a.post; ++k) {
+      ft_colour<N>(u, b, T.c, a.sigma, a.omega, 1, false);
+      __syncthreads();
+      ft_colour<N>(u, b, T.c, a.sigma, a.omega, 0, false);
+      __syncthreads();
+    }
+  }
+}
+
 // the whole V-cycle of the tail levels by one CTA in shared memory
 template <int DIM>
 __device__ void tail_run(const TailArgs& a, const double* __restrict__ b_in, double* u_io,
                          int zero_guess, int ncycles, double* sm) {
   const TailLevel& L0 = a.lv[0];
+  if (DIM == 3 && a.fast) {
+    for (int i = threadIdx.x; i < a.m * a.m + a.m; i += blockDim.x) sm[a.lu_off + i] = a.lu[i];
+    PL_FOR_SM_POINTS(L0.g) {
+      int x, y, z;
+      decode(L0.g, p, x, y, z);
+      const long long gi = a.g0.at(x, y, z);
+      sm[L0.off_b + p] = b_in[gi];
+      if (!zero_guess) sm[L0.off_u + p] = u_io[gi];
+    }
+    __syncthreads();
+    for (int cyc = 0; cyc < ncycles; ++cyc) {
+      if (a.fast == 15) ft_level<15, 0>(a, sm, zero_guess && cyc == 0);
+      else ft_level<7, 0>(a, sm, zero_guess && cyc == 0);
+    }
+    PL_FOR_SM_POINTS(L0.g) {
+      int x, y, z;
+      decode(L0.g, p, x, y, z);
+      u_io[a.g0.at(x, y, z)] = sm[L0.off_u + p];
+    }
+    return;
+  }
   if (a.lu_off >= 0)
     for (int i = threadIdx.x; i < a.m * a.m + a.m; i += blockDim.x) sm[a.lu_off + i] = a.lu[i];
   PL_FOR_SM_POINTS(L0.g) {
@@ -298,6 +453,7 @@ struct MidLevel {
 };
 
 struct MidArgs {
+  unsigned long long* trace;   // PL_MID_TRACE diagnostics: %globaltimer per phase (or null)
   int nmid;                 // grid-wide levels 0 .. nmid-1; level nmid starts the tail
   MidLevel lv[MID_MAX + 1];
   int pre, post;
@@ -345,6 +501,21 @@ __device__ __forceinline__ void mid_colour(const MidLevel& L, const MidArgs& m, 
 template <int DIM>
 __global__ void __launch_bounds__(MID_THREADS) k_mid(MidArgs m, TailArgs ta) {
   cg::grid_group grid = cg::this_grid();
+  int ph = 0;
+#define MID_SYNC()                                                              \
+  do {                                                                          \
+    grid.sync();                                                                \
+    if (m.trace && blockIdx.x == 0 && threadIdx.x == 0) {                       \
+      unsigned long long t_;                                                    \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                    \
+      if (ph < 63) m.trace[1 + ph++] = t_;                                      \
+    }                                                                           \
+  } while (0)
+  if (m.trace && blockIdx.x == 0 && threadIdx.x == 0) {
+    unsigned long long t_;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));
+    m.trace[0] = t_;
+  }
   extern __shared__ double sm[];
   const long long gt = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   const long long gs = (long long)gridDim.x * blockDim.x;
@@ -354,13 +525,13 @@ __global__ void __launch_bounds__(MID_THREADS) k_mid(MidArgs m, TailArgs ta) {
     const bool zero = l == 0 ? m.zero != 0 : true;
     if (zero && m.pre == 0) {
       for (long long t = gt; t < L.g.nstore; t += gs) L.u[t] = 0.0;
-      grid.sync();
+      MID_SYNC();
     }
     for (int k = 0; k < m.pre; ++k) {
       mid_colour<DIM>(L, m, 1, zero && k == 0, gt, gs);
-      grid.sync();
+      MID_SYNC();
       mid_colour<DIM>(L, m, 0, false, gt, gs);
-      grid.sync();
+      MID_SYNC();
     }
     for (long long t = gt; t < L.g.npts; t += gs) {       // residual (k_residual)
       int x, y, z;
@@ -368,16 +539,16 @@ __global__ void __launch_bounds__(MID_THREADS) k_mid(MidArgs m, TailArgs ta) {
       const long long idx = L.g.at(x, y, z);
       L.t[idx] = L.b[idx] - shifted_point<DIM>(L.u, L.g, L.c, m.sigma, x, y, z, idx);
     }
-    grid.sync();
+    MID_SYNC();
     for (long long t = gt; t < C.g.npts; t += gs) {       // full weighting (k_fw)
       int x, y, z;
       decode_point(C.g, t, x, y, z);
       C.b[C.g.at(x, y, z)] = fw_point<DIM>(L.t, L.g, x, y, z);
     }
-    grid.sync();
+    MID_SYNC();
   }
   if (blockIdx.x == 0) tail_run<DIM>(ta, m.lv[m.nmid].b, m.lv[m.nmid].u, 1, 1, sm);
-  grid.sync();
+  MID_SYNC();
   for (int l = m.nmid - 1; l >= 0; --l) {
     const MidLevel& L = m.lv[l];
     const MidLevel& C = m.lv[l + 1];
@@ -387,15 +558,16 @@ __global__ void __launch_bounds__(MID_THREADS) k_mid(MidArgs m, TailArgs ta) {
       const long long idx = L.g.at(x, y, z);
       L.u[idx] = L.u[idx] + lin_point<DIM>(C.u, C.g, x, y, z);
     }
-    grid.sync();
+    MID_SYNC();
     for (int k = 0; k < m.post; ++k) {
       mid_colour<DIM>(L, m, 1, false, gt, gs);
-      grid.sync();
+      MID_SYNC();
       mid_colour<DIM>(L, m, 0, false, gt, gs);
-      if (l > 0 || k + 1 < m.post) grid.sync();
+      if (l > 0 || k + 1 < m.post) MID_SYNC();
     }
   }
 }
+#undef MID_SYNC
 
 }  // namespace
 
@@ -433,6 +605,16 @@ static int tail_args(MgPlan* P, int l0, double sigma, TailArgs& a, size_t* smem_
     a.lu_off = off;
     off += lu_n;
   }
+  // compile-time-sized path: 3-D order-2 jor-rb, levels 15 -> 7 -> 3 or 7 -> 3
+  a.fast = 0;
+  {
+    const int N0 = P->lv[l0].g.N;
+    bool chain = P->dim == 3 && P->order == 2 && P->smoother == SM_RB && a.lu_off >= 0 &&
+                 a.m == 27 && g_fast_tail && (N0 == 15 || N0 == 7);
+    for (int i = 0, n = N0; chain && i < a.nlev; ++i, n = (n - 1) / 2)
+      chain = P->lv[l0 + i].g.N == n && (P->lv[l0 + i].coarsest == (n == 3));
+    if (chain) a.fast = N0;
+  }
   *smem_out = sizeof(double) * off;
   return 0;
 }
@@ -458,7 +640,7 @@ static int launch_tail(MgPlan* P, int l0, double* u, const double* b, double sig
 }
 
 int g_mid_enabled = 1;      // PL_OPT_MID
-int g_mid_tail_n = 7;       // PL_OPT_MID_TAIL_N: largest N the mid kernel leaves to its tail
+int g_mid_tail_n = 15;      // PL_OPT_MID_TAIL_N: largest N the mid kernel leaves to its tail
 
 // first tail level of the mid kernel (>= the plan's tail_start)
 static int mid_tail_level(const MgPlan* P) {
@@ -515,11 +697,24 @@ static int launch_mid(MgPlan* P, int l0, double* u, const double* b, double sigm
       return 2;
     }
   }
+  static unsigned long long* trace = nullptr;
+  static const bool tracing = std::getenv("PL_MID_TRACE") != nullptr;
+  if (tracing && !trace) cudaMalloc(&trace, 64 * sizeof(unsigned long long));
+  m.trace = tracing ? trace : nullptr;
+  if (tracing) cudaMemsetAsync(trace, 0, 64 * sizeof(unsigned long long), s);
   void* args[] = {&m, &ta};
   PL_PRE(K_MID);
   cudaError_t e = cudaLaunchCooperativeKernel((void*)k_mid<3>, grid, MID_THREADS, args, smem, s);
   if (e != cudaSuccess) return cuda_status(e, "cooperative mid launch");
   bytes += 8.0 * P->lv[lt].g.npts * 3;
+  if (tracing) {   // diagnostics only: per-phase durations of this launch
+    unsigned long long h[64];
+    cudaMemcpyAsync(h, trace, sizeof(h), cudaMemcpyDeviceToHost, s);
+    cudaStreamSynchronize(s);
+    std::fprintf(stderr, "mid n=%d levels=%d:", P->lv[l0].g.N, m.nmid);
+    for (int i = 1; i < 64 && h[i]; ++i) std::fprintf(stderr, " %.2f", (h[i] - h[i - 1]) * 1e-3);
+    std::fprintf(stderr, " us\n");
+  }
   PL_CHECK_LAUNCH(K_MID, bytes);
   return 0;
 }

@@ -1620,12 +1620,17 @@ int make_map(CUtensorMap* m, const double* base, const Geo& g, int bw, int bh) {
   return 0;
 }
 
+}  // namespace
+int g_zc_floor = 16;  // PL_OPT_ZC_FLOOR (A/B): smallest z chunk (4 and 8 measured slower at 127^3)
+namespace {
 int pick_zc(const Geo& g) {
   // enough CTAs for several waves on 148 SMs; chunk halo planes cost
-  // (2 or 4)/zc extra L2 reads; zc even (the prolongation pairs planes)
+  // (2 or 4)/zc extra (L2) reads; zc even (the prolongation pairs planes).
+  // Grids below ~2^24 points are L2-resident: short chunks are cheap there
+  // and keep all SMs busy.
   long long tiles = (long long)ceil_div(g.nx, TX) * ceil_div(g.ny, TY);
   int zc = 64;
-  while (zc > 16 && tiles * ceil_div(g.nz, zc) < 148 * 8) zc /= 2;
+  while (zc > g_zc_floor && tiles * ceil_div(g.nz, zc) < 148 * 8) zc /= 2;
   return zc;
 }
 

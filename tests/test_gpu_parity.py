@@ -466,7 +466,7 @@ def test_cooperative_mid_vcycle_equals_separate_launches(n, pre, post, omega):
             assert torch.equal(mg.v_cycle(sop, torch.zeros_like(u), b, cfg), ref0), tail_n
     finally:
         _capi.set_option(_capi.OPT_MID, 1)
-        _capi.set_option(_capi.OPT_MID_TAIL_N, 7)
+        _capi.set_option(_capi.OPT_MID_TAIL_N, 15)
 
 
 @pytest.mark.parametrize("name", ["run_cfg1", "run_cfg2_small", "run_cfg3_small", "run_cfg4_small_tol"])
@@ -507,3 +507,29 @@ def test_fused_residual_restriction(n, length):
             assert torch.equal(mg.v_cycle(sop, u, b, cfg), ref), pre
     finally:
         _capi.set_option(_capi.OPT_RFW, 1)
+
+
+@pytest.mark.parametrize("n", [8, 16, 32, 64, 128])
+@pytest.mark.parametrize("pre,post,omega", [(1, 1, 1.0), (2, 0, 0.9), (0, 2, 1.0)])
+def test_fast_tail_equals_generic_tail(n, pre, post, omega):
+    """The compile-time-sized 15^3 / 7^3 -> 3^3 tail (warp-shuffle LU) equals
+    the generic one-CTA tail bit for bit, standalone and under the
+    cooperative kernel, from a guess and from zero."""
+    rng = np.random.default_rng(3 * n + pre)
+    g = heat.Grid(3, n)
+    u = dev(rng.standard_normal(g.shape))
+    b = dev(rng.standard_normal(g.shape))
+    sop = mg.ShiftedOperator(heat.HeatOperator(g), 0.07)
+    cfg = mg.MgConfig("jor-rb", omega, pre, post)
+    try:
+        _capi.set_option(_capi.OPT_FAST_TAIL, 0)
+        ref = mg.v_cycle(sop, u, b, cfg)
+        ref0 = mg.v_cycle(sop, torch.zeros_like(u), b, cfg)
+        _capi.set_option(_capi.OPT_FAST_TAIL, 1)
+        for tail_n in (7, 15):
+            _capi.set_option(_capi.OPT_MID_TAIL_N, tail_n)
+            assert torch.equal(mg.v_cycle(sop, u, b, cfg), ref), tail_n
+            assert torch.equal(mg.v_cycle(sop, torch.zeros_like(u), b, cfg), ref0), tail_n
+    finally:
+        _capi.set_option(_capi.OPT_FAST_TAIL, 1)
+        _capi.set_option(_capi.OPT_MID_TAIL_N, 15)
