@@ -13,7 +13,7 @@ iteration, convergence freezing, block chaining.  Three executors:
     which time ranks n+1..P-1 of iteration k are still queued -- the GPU never
     drains waiting for the host.  ("threaded" is the reference's bitwise-
     identical alternative executor; here it is the same device schedule.)
-    With ``streams=True`` every time rank issues on its own CUDA
+    With ``streams=True`` (default) every time rank issues on its own CUDA
     stream in wavefront order (anti-diagonals n + k): iteration k of rank n
     depends only on iteration k of rank n-1 (its payloads, copied at the
     start) and on iteration k-1 of itself, so latency-bound work of one rank
@@ -501,7 +501,7 @@ def _world(group):
 
 def pfasst_run(levels, u0, t_end: float, p: int, blocks: int = 1, tol: float = 1e-9,
                max_iter: int = 20, executor: str = "serial", record_final_values: bool = False,
-               engine_factory=None, group=None, streams: bool = False) -> PfasstResult:
+               engine_factory=None, group=None, streams: bool = True) -> PfasstResult:
     """Run PFASST / IPFASST over ``blocks`` windows of ``p`` steps (pfasst.py:256-287).
 
     ``u0`` may be a numpy array (result returned on the host, drop-in) or an

@@ -76,7 +76,10 @@ def main():
     os.makedirs(dst, exist_ok=True)
     if os.path.exists(os.path.join(OUT, "launches.csv")):
         launch_list(os.path.join(dst, "launch_list_summary.txt"))
-    caps = {"zrb255_full.ncu-rep": "dominant kernel: fused red-black sweep (TMA), 255^3 "
+    caps = {"top255_full.ncu-rep": "top kernels at 255^3 (k_zrb3 one-barrier red-black sweep, "
+                                   "k_rfw residual+restriction, k_cubic4 cubic correction, "
+                                   "k_mid cooperative small levels)",
+            "zrb255_full.ncu-rep": "dominant kernel: fused red-black sweep (TMA), 255^3 "
                                    "(first launch: with fused prolongation? see kernel name)",
             "jacobi512.ncu-rep": "round-1 baseline: one-point-per-thread Jacobi sweep, 511^3",
             "zmarch512.ncu-rep": "cp.async z-marching Jacobi sweep, 511^3 (before TMA)",
@@ -86,9 +89,11 @@ def main():
         p = os.path.join(OUT, rep)
         if os.path.exists(p):
             full_capture(p, os.path.join(dst, rep.replace(".ncu-rep", ".txt")), note)
-    b = os.path.join(OUT, "bench_full.json")
-    if os.path.exists(b):
-        json.dump(json.load(open(b)), open(os.path.join(dst, "bench.json"), "w"), indent=1)
+    for src, name in (("bench_full.json", "bench.json"),
+                      ("bench_nostreams.json", "bench_single_stream.json")):
+        b = os.path.join(OUT, src)
+        if os.path.exists(b) and os.path.getsize(b):
+            json.dump(json.load(open(b)), open(os.path.join(dst, name), "w"), indent=1)
 
 
 if __name__ == "__main__":
