@@ -207,6 +207,25 @@ int pl_timing_collect(int kind, long long* launches, double* total_ms, double* a
 int pl_timing_dump(int kind, long long nmax, double* bytes, float* ms, long long* n);
 const char* pl_kind_name(int kind);
 
+/* ---- time-rank communication (NCCL) ---------------
+   For non-Python hosts: the hand-offs of a multi-GPU PFASST run -- fine /
+   coarse payloads and the converged flag rank n -> n+1 (pfasst.py:107-118,
+   189-202 -> ncclSend/ncclRecv) and the block-boundary broadcast of the last
+   rank's value (pfasst.py:272-278 -> ncclBroadcast).  libnccl.so.2 is opened
+   at first use (no link-time dependency).  Byte counts; stream-ordered.
+   Pair a send with its matching recv inside pl_comm_group_start/end when one
+   process both sends and receives in the same step. */
+#define PL_COMM_ID_BYTES 128
+typedef struct pl_comm pl_comm;
+int pl_comm_unique_id(char* id /* PL_COMM_ID_BYTES */);
+int pl_comm_init(pl_comm** comm, const char* id, int rank, int nranks, int device);
+int pl_comm_destroy(pl_comm* comm);
+int pl_comm_group_start(void);
+int pl_comm_group_end(void);
+int pl_comm_send(pl_comm* comm, const void* buf, size_t bytes, int peer, void* stream);
+int pl_comm_recv(pl_comm* comm, void* buf, size_t bytes, int peer, void* stream);
+int pl_comm_bcast(pl_comm* comm, void* buf, size_t bytes, int root, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -81,6 +81,14 @@ _SIGS = {
     "pl_timing_collect": (i32, [i32, C.POINTER(i64), dp, dp]),
     "pl_timing_dump": (i32, [i32, i64, dp, C.POINTER(C.c_float), C.POINTER(i64)]),
     "pl_kind_name": (C.c_char_p, [i32]),
+    "pl_comm_unique_id": (i32, [C.c_char_p]),
+    "pl_comm_init": (i32, [C.POINTER(C.c_void_p), C.c_char_p, i32, i32, i32]),
+    "pl_comm_destroy": (i32, [C.c_void_p]),
+    "pl_comm_group_start": (i32, []),
+    "pl_comm_group_end": (i32, []),
+    "pl_comm_send": (i32, [C.c_void_p, C.c_void_p, C.c_size_t, i32, C.c_void_p]),
+    "pl_comm_recv": (i32, [C.c_void_p, C.c_void_p, C.c_size_t, i32, C.c_void_p]),
+    "pl_comm_bcast": (i32, [C.c_void_p, C.c_void_p, C.c_size_t, i32, C.c_void_p]),
 }
 
 EXPORTED = tuple(_SIGS)

@@ -83,6 +83,14 @@ def is_field(t, grid_dim):
     return all(g == w or s == 1 for g, w, s in zip(got, want, shape))
 
 
+def require_field(t, grid_dim, what):
+    """The *_into entry points take device fields in the library layout (no
+    copies); anything else is an error, never a silent out-of-bounds read."""
+    if not is_field(t, grid_dim):
+        raise ValueError(f"{what}: expected an fp64 CUDA field in the library's row-padded "
+                         "layout (use _device.to_device / new_field)")
+
+
 def to_device(x, grid_dim=None):
     """(field, was_host): x as a device field in the library layout (copied
     unless it already is one).  grid_dim defaults to x.ndim."""

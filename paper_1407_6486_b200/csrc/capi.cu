@@ -242,7 +242,7 @@ int pl_set_option(int key, int value) {
     return 0;
   }
   if (key == PL_OPT_ZRB_VARIANT) {
-    if (value < 0 || value > 4) {
+    if (value < 0 || value > 5) {
       set_error("zrb variant %d out of range", value);
       return -1;
     }

@@ -937,13 +937,13 @@ __device__ __forceinline__ void rb_phase(const RbCtx& k, int z, const double2& U
   else if (k.va) dst[0] = w.x;
 }
 
-template <bool POW2, int RU, int RB>
-__global__ void __launch_bounds__(NTHR_RB2, 3) k_zrb3(const __grid_constant__ CUtensorMap mu,
+template <bool POW2, int RU, int RB, int MINB>
+__global__ void __launch_bounds__(NTHR_RB2, MINB) k_zrb3(const __grid_constant__ CUtensorMap mu,
                                                       const __grid_constant__ CUtensorMap mb,
                                                       double* __restrict__ out, Geo g, OpC c,
                                                       double sigma, double omega, double dval,
                                                       double dinv, int zc) {
-  static_assert((RU & (RU - 1)) == 0 && (RB & (RB - 1)) == 0 && RU >= 8 && RB >= 4, "rings");
+  static_assert((RU & (RU - 1)) == 0 && (RB & (RB - 1)) == 0 && RU >= 8 && RB >= 2, "rings");
   extern __shared__ __align__(128) double sm[];
   RbCtx k;
   k.su = sm;
@@ -1021,7 +1021,7 @@ __global__ void __launch_bounds__(NTHR_RB2, 3) k_zrb3(const __grid_constant__ CU
 
   // ---- prologue: reds of planes z0-1 (if >= 0), z0, z0+1 (if <= R)
   for (int p = z0 - 2; p <= min(z0 + 2, uhi); ++p) wait_u(p);
-  for (int q = z0 - 1; q <= min(z0 + 1, bhi); ++q) wait_b(q);
+  for (int q = z0 - 1; q <= min(z0, bhi); ++q) wait_b(q);
   const double2 zero2 = make_double2(0.0, 0.0);
   double2 Um2 = lds2(rb_u<RU>(k, z0 - 2) + k.iu);
   double2 U0 = lds2(rb_u<RU>(k, z0 - 1) + k.iu);
@@ -1030,7 +1030,6 @@ __global__ void __launch_bounds__(NTHR_RB2, 3) k_zrb3(const __grid_constant__ CU
   double2 U3 = z0 + 2 <= uhi ? lds2(rb_u<RU>(k, z0 + 2) + k.iu) : zero2;
   const double2 Bm1 = lds2(rb_b<RB>(k, z0 - 1) + k.ib);
   double2 B0 = lds2(rb_b<RB>(k, z0) + k.ib);
-  double2 B1 = z0 + 1 <= bhi ? lds2(rb_b<RB>(k, z0 + 1) + k.ib) : zero2;
   // plane p red member: 1 - ((y + p) & 1); z0 even, so plane z0 has parity wpar
   auto pro_red = [&](int q, const double2& um, double2& uc, const double2& up,
                      const double2& bq, int par) {
@@ -1048,17 +1047,28 @@ __global__ void __launch_bounds__(NTHR_RB2, 3) k_zrb3(const __grid_constant__ CU
   };
   pro_red(z0 - 1, Um2, U0, U1, Bm1, 1 - wpar);
   pro_red(z0, U0, U1, U2, B0, wpar);
-  pro_red(z0 + 1, U1, U2, U3, B1, 1 - wpar);
   if (tid < 50) {
     rb_halo<POW2, RU, RB, 1>(k, z0 - 1);
     rb_halo<POW2, RU, RB, 0>(k, z0);
-    rb_halo<POW2, RU, RB, 1>(k, z0 + 1);
   }
+  if constexpr (RB == 2) {   // b plane z0+1 goes into the slot of z0-1
+    __syncthreads();
+    if (tid == 0) issue_b(z0 + 1);
+  }
+  if (z0 + 1 <= bhi) wait_b(z0 + 1);
+  double2 B1 = z0 + 1 <= bhi ? lds2(rb_b<RB>(k, z0 + 1) + k.ib) : zero2;
+  pro_red(z0 + 1, U1, U2, U3, B1, 1 - wpar);
+  if (tid < 50) rb_halo<POW2, RU, RB, 1>(k, z0 + 1);
   __syncthreads();
   if (tid == 0) {       // u planes z0-2, z0-1 and b planes z0-1 .. z0+1 are dead
     issue_u(z0 - 2 + RU);
     issue_u(z0 - 1 + RU);
-    for (int q = z0 - 1; q <= z0 + 1; ++q) issue_b(q + RB);
+    if constexpr (RB == 2) {
+      issue_b(z0 + 2);
+      issue_b(z0 + 3);
+    } else {
+      for (int q = z0 - 1; q <= z0 + 1; ++q) issue_b(q + RB);
+    }
   }
 
   // ---- main loop, two planes per trip: U0..U3 = own pair on z-1..z+2,
@@ -1732,7 +1742,12 @@ int launch_zrb2(const double* u, const double* b, double* out, const Geo& g, con
   } while (0)
   if (variant == 4) {
     size_t smem = ((size_t)8 * PU + (size_t)4 * PB) * 8 + 8 * (8 + 4);
-    auto kern = c.pow2 ? k_zrb3<true, 8, 4> : k_zrb3<false, 8, 4>;
+    auto kern = c.pow2 ? k_zrb3<true, 8, 4, 3> : k_zrb3<false, 8, 4, 3>;
+    raise_smem(kern, smem);
+    kern<<<grid, dim3(NTHR_RB2), smem, s>>>(mu, mb, out, g, c, sigma, omega, dval, dinv, zc);
+  } else if (variant == 5) {   // 2-plane b ring: 56.7 KB, 4 CTAs / SM (<= 64 registers)
+    size_t smem = ((size_t)8 * PU + (size_t)2 * PB) * 8 + 8 * (8 + 2);
+    auto kern = c.pow2 ? k_zrb3<true, 8, 2, 4> : k_zrb3<false, 8, 2, 4>;
     raise_smem(kern, smem);
     kern<<<grid, dim3(NTHR_RB2), smem, s>>>(mu, mb, out, g, c, sigma, omega, dval, dinv, zc);
   } else if (variant == 2) {

@@ -12,7 +12,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import _capi as capi
-from ._device import like_input, new_field, ptr, stream_ptr, to_device
+from ._device import like_input, new_field, ptr, require_field, stream_ptr, to_device
 
 
 @dataclass(frozen=True)
@@ -120,6 +120,8 @@ class HeatOperator:
 
     def apply_into(self, u, out):
         """out = nu Lap_h u for device tensors (no allocation)."""
+        require_field(u, self.grid.dim, "HeatOperator.apply_into(u)")
+        require_field(out, self.grid.dim, "HeatOperator.apply_into(out)")
         capi.check(capi.lib().pl_heat_apply(ptr(u), ptr(out), *self._args(), stream_ptr()),
                    "HeatOperator.apply")
         return out

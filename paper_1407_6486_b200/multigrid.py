@@ -16,7 +16,8 @@ import scipy.linalg
 import torch
 
 from . import _capi as capi
-from ._device import clone_field, device, like_input, new_field, ptr, stream_ptr, to_device
+from ._device import (clone_field, device, like_input, new_field, ptr, require_field,
+                      stream_ptr, to_device)
 from .heat import Grid, HeatOperator
 
 
@@ -235,6 +236,8 @@ def smooth(op: ShiftedOperator, u, b, cfg: MgConfig, count: int):
 
 def vcycles_into(op: ShiftedOperator, u, b, cfg: MgConfig, ncycles: int, zero_guess=False):
     """ncycles V-cycles in place on the device tensor u."""
+    require_field(u, op.grid.dim, "vcycles_into(u)")
+    require_field(b, op.grid.dim, "vcycles_into(b)")
     p = plan_for(op.base, cfg)
     p.ensure(op.sigma)
     capi.check(capi.lib().pl_mg_vcycles(p.handle.value, ptr(u), ptr(b), float(op.sigma),
@@ -264,6 +267,8 @@ class SolveResult:
 def solve_into(op: ShiftedOperator, u, b, cfg: MgConfig, policy) -> tuple:
     """In-place device solve; returns (cycles, status).  Raises MultigridError."""
     _check_policy(policy)
+    require_field(u, op.grid.dim, "solve_into(u)")
+    require_field(b, op.grid.dim, "solve_into(b)")
     if isinstance(policy, FixedCycles):
         vcycles_into(op, u, b, cfg, policy.cycles)
         return policy.cycles, "fixed"

@@ -6,7 +6,7 @@ at fine index 2j.  All four run as sm_100a kernels (csrc/transfer.cu).
 from __future__ import annotations
 
 from . import _capi as capi
-from ._device import like_input, new_field, ptr, scratch, stream_ptr, to_device
+from ._device import like_input, new_field, ptr, require_field, scratch, stream_ptr, to_device
 
 
 def _fine_n(shape):
@@ -37,6 +37,8 @@ def inject(u):
 
 
 def interp_linear_into(coarse, fine, accumulate):
+    require_field(coarse, coarse.dim(), "interp_linear_into(coarse)")
+    require_field(fine, coarse.dim(), "interp_linear_into(fine)")
     nf = 2 * (coarse.shape[0] + 1)
     capi.check(capi.lib().pl_interp_linear(ptr(coarse), ptr(fine), coarse.dim(), nf,
                                            int(accumulate), stream_ptr()), "interp_linear")
@@ -44,6 +46,8 @@ def interp_linear_into(coarse, fine, accumulate):
 
 
 def interp_cubic_into(coarse, fine, accumulate):
+    require_field(coarse, coarse.dim(), "interp_cubic_into(coarse)")
+    require_field(fine, coarse.dim(), "interp_cubic_into(fine)")
     nf = 2 * (coarse.shape[0] + 1)
     nb = capi.lib().pl_interp_cubic_scratch_bytes(coarse.dim(), nf)
     s = scratch("cubic", nb)

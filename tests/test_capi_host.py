@@ -110,3 +110,21 @@ def test_seeded_field_recipe_matches_oracle():
 def test_direct_policy_is_rejected_not_silently_replaced():
     with pytest.raises(NotImplementedError):
         mg._check_policy(mg.Direct())
+
+
+def test_comm_entry_points_validate_and_create_ids():
+    """pl_comm_*: NCCL is opened lazily (the library loads without it); ids are
+    128 bytes; argument errors are rejected before any device work."""
+    import ctypes as C
+    lib = _capi.lib()
+    buf = C.create_string_buffer(128)
+    assert lib.pl_comm_unique_id(buf) == 0
+    assert any(buf.raw)
+    assert lib.pl_comm_unique_id(None) < 0
+    h = C.c_void_p()
+    assert lib.pl_comm_init(C.byref(h), buf, 2, 1, 0) < 0          # rank >= nranks
+    assert lib.pl_comm_init(C.byref(h), buf, 0, 0, 0) < 0          # no ranks
+    assert lib.pl_comm_send(None, None, 0, 0, None) < 0
+    assert lib.pl_comm_recv(None, None, 0, 0, None) < 0
+    assert lib.pl_comm_bcast(None, None, 0, 0, None) < 0
+    assert lib.pl_comm_destroy(None) == 0

@@ -362,20 +362,22 @@ def test_fused_equals_unfused_at_127(sm, om, pre, post):
 def test_cubic_zmarch_equals_pass_kernels(nf):
     """The TMA-staged 3-D cubic interpolation equals the per-axis pass kernels
     (which are pinned to the reference by test_transfers_bitwise) bit for bit."""
+    from paper_1407_6486_b200._device import clone_field, to_device
     rng = np.random.default_rng(nf)
-    c = dev(rng.standard_normal((nf // 2 - 1,) * 3))
-    f = dev(rng.standard_normal((nf - 1,) * 3))
+    # the *_into entry points take fields in the library's row-padded layout
+    c = to_device(rng.standard_normal((nf // 2 - 1,) * 3))[0]
+    f = to_device(rng.standard_normal((nf - 1,) * 3))[0]
     _capi.set_option(_capi.OPT_ZMARCH_MIN_N, 31)
     try:
         _capi.set_option(_capi.OPT_ZMARCH, 0)
         ref = transfers.interp_cubic(c)
-        ref_acc = f.clone()
+        ref_acc = clone_field(f)
         transfers.interp_cubic_into(c, ref_acc, True)
         _capi.set_option(_capi.OPT_ZMARCH, 1)
         for variant in (0, 1):
             _capi.set_option(_capi.OPT_CUBIC_VARIANT, variant)
             assert torch.equal(transfers.interp_cubic(c), ref), variant
-            acc = f.clone()
+            acc = clone_field(f)
             transfers.interp_cubic_into(c, acc, True)
             assert torch.equal(acc, ref_acc), variant
     finally:
@@ -395,7 +397,7 @@ def test_pfasst_run_parity_tma_path(name):
         _capi.set_option(_capi.OPT_ZMARCH_MIN_N, 127)
 
 
-@pytest.mark.parametrize("variant", [0, 1, 2, 3, 4])
+@pytest.mark.parametrize("variant", [0, 1, 2, 3, 4, 5])
 def test_zrb_variants_bitwise_31cubed(variant):
     """Every jor-rb TMA sweep variant (three barriers per plane, and the
     register-pipelined one-barrier kernels with their ring sizes) reproduces
@@ -434,7 +436,7 @@ def test_zrb_variants_equal_plain_kernels(n, length, sigma, fuse):
     _capi.set_option(_capi.OPT_ZMARCH, 1)
     _capi.set_option(_capi.OPT_FUSE_PROLONG, fuse)
     try:
-        for variant in (0, 1, 2, 3, 4):
+        for variant in (0, 1, 2, 3, 4, 5):
             _capi.set_option(_capi.OPT_ZRB_VARIANT, variant)
             assert torch.equal(mg.v_cycle(sop, u, b, cfg), ref), variant
             assert torch.equal(mg.smooth(sop, u, b, cfg, 2), ref_s), variant
@@ -533,3 +535,31 @@ def test_fast_tail_equals_generic_tail(n, pre, post, omega):
     finally:
         _capi.set_option(_capi.OPT_FAST_TAIL, 1)
         _capi.set_option(_capi.OPT_MID_TAIL_N, 15)
+
+
+def test_comm_single_rank_roundtrip():
+    """A one-rank NCCL communicator through the C ABI: grouped self send/recv
+    and a broadcast move device bytes unchanged (multi-GPU hand-offs use the
+    same calls with peer = n +- 1)."""
+    import ctypes as C
+    lib = _capi.lib()
+    uid = C.create_string_buffer(128)
+    assert lib.pl_comm_unique_id(uid) == 0
+    h = C.c_void_p()
+    _capi.check(lib.pl_comm_init(C.byref(h), uid, 0, 1, torch.cuda.current_device()),
+                "comm init")
+    try:
+        src = torch.arange(1000, dtype=torch.float64, device="cuda") * 0.37
+        dst = torch.zeros_like(src)
+        s = torch.cuda.current_stream().cuda_stream
+        nb = src.numel() * 8
+        _capi.check(lib.pl_comm_group_start(), "group")
+        _capi.check(lib.pl_comm_send(h, src.data_ptr(), nb, 0, s), "send")
+        _capi.check(lib.pl_comm_recv(h, dst.data_ptr(), nb, 0, s), "recv")
+        _capi.check(lib.pl_comm_group_end(), "group")
+        b = src.clone()
+        _capi.check(lib.pl_comm_bcast(h, b.data_ptr(), nb, 0, s), "bcast")
+        torch.cuda.synchronize()
+        assert torch.equal(dst, src) and torch.equal(b, src)
+    finally:
+        lib.pl_comm_destroy(h)
