@@ -19,6 +19,7 @@ sample, extrapolated), clocks sampled during the timed region.
 from __future__ import annotations
 
 import argparse
+import faulthandler
 import json
 import os
 import statistics
@@ -153,6 +154,9 @@ def run_ours(args, w):
 
     rank, world, local = env_rank()
     torch.cuda.set_device(local)
+    for kv in filter(None, args.opts.split(",")):
+        k, v = kv.split("=")
+        _capi.set_option(int(k), int(v))
     if world > 1:
         dist.init_process_group("nccl", init_method="env://")
     executor = "nccl" if world > 1 else "serial"
@@ -246,7 +250,17 @@ def run_ours(args, w):
         peak, peak_src = peaks()
         steps_done = p * args.steps
         value = steps_done / (ms / 1e3)
-        achieved = (bytes_dom / n_dom) / ((ms_dom / n_dom) / 1e3) / 1e9 if n_dom else None
+        # the roofline is quoted on the dominant kind's fine-grid launches (the
+        # largest per-launch byte count): one kernel at one size, comparable
+        # with its ncu capture
+        if by_size:
+            b_top = max(by_size)
+            c_top, t_top = by_size[b_top]
+            achieved = b_top / ((t_top / c_top) / 1e3) / 1e9
+        else:
+            b_top = c_top = None
+            achieved = (bytes_dom / n_dom) / ((ms_dom / n_dom) / 1e3) / 1e9 if n_dom else None
+        traffic, traffic_src = ncu_traffic(dom)
         out = {
             "metric": "PFASST time-steps/s (MG V-cycle DOF-updates/s and HBM GB/s in "
                       "'vcycle' / 'roofline')",
@@ -260,6 +274,7 @@ def run_ours(args, w):
                        "vcycles_per_substep": w["cycles"], "time_ranks": p, "dt": dt,
                        "tol": w["tol"], "max_iter": 20, "executor": executor,
                        "rank_streams": streams,
+                       **({"options": args.opts} if args.opts else {}),
                        "parallelism": f"time{world}",
                        "l2": "fields (>=133 MB) exceed the 126 MB L2; no flush needed",
                        "rank_iterations": res.rank_iterations[0],
@@ -268,14 +283,19 @@ def run_ours(args, w):
                     "h2d_bytes_per_step": int(u0_host.nbytes),
                     "d2h_bytes_per_step": int(u0_host.nbytes)},
             "gpu_launches": launches,
-            "roofline": {"bound": "hbm", "kernel": dom,
+            "roofline": {"bound": "hbm", "kernel": f"{dom} @ {w['ns'][0] - 1}^{w['dim']}",
                          "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": (achieved / peak) if achieved else None,
+                         "alg_bytes_per_launch": b_top, "launches": c_top,
+                         "all_levels_achieved":
+                             (bytes_dom / n_dom) / ((ms_dom / n_dom) / 1e3) / 1e9
+                             if n_dom else None,
                          "per_level": {f"{b / 1e6:.1f}MB": {
                              "launches": c, "avg_us": 1e3 * t / c,
                              "gbs": b / (t / c / 1e3) / 1e9}
                              for b, (c, t) in sorted(by_size.items(), reverse=True)},
-                         "traffic": None, "peak_source": peak_src,
+                         "traffic": traffic, "traffic_source": traffic_src,
+                         "peak_source": peak_src,
                          "launches_timed": n_dom,
                          "kernel_share_of_step": ms_dom / ms_instr if ms_instr else None,
                          "instrumented_ms_per_step": ms_instr / args.steps,
@@ -290,6 +310,32 @@ def run_ours(args, w):
         dist.barrier()
         dist.destroy_process_group()
     return out
+
+
+NCU_KERNEL = {"jor_rb": "k_zrb3", "interp_cubic": "k_cubic4", "restrict": "k_rfw",
+              "mg_mid": "k_mid"}
+
+
+def ncu_traffic(kind):
+    """DRAM bytes (read + write) per launch of the kind's fine-grid kernel from
+    the latest committed ncu --set full capture (profiles/*/top255_full.txt),
+    or (None, reason)."""
+    import glob
+    import re
+    name = NCU_KERNEL.get(kind)
+    files = sorted(glob.glob(os.path.join(os.path.dirname(os.path.abspath(__file__)),
+                                          "profiles", "*", "top255_full.txt")))
+    if not name or not files:
+        return None, "no ncu capture committed for this kernel"
+    text = open(files[-1]).read()
+    blocks = text.split("\n\n")
+    for blk in blocks:
+        if re.search(r"::%s[<(]" % name, blk):
+            m = re.search(r"=> DRAM traffic ([0-9.]+) MB", blk)
+            if m:
+                rel = os.path.relpath(files[-1], os.path.dirname(os.path.abspath(__file__)))
+                return float(m.group(1)) * 1e6, f"{rel} (first {name} launch, 255^3)"
+    return None, f"{name} not in {os.path.basename(files[-1])}"
 
 
 def vcycle_rate(w, reps=10):
@@ -401,6 +447,7 @@ BLOCK_MODEL = {
 
 
 def main():
+    faulthandler.enable()
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
@@ -410,6 +457,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-streams", action="store_true",
                     help="issue all time ranks on one stream (A/B of the wavefront overlap)")
+    ap.add_argument("--opts", default="", help="pl_set_option pairs KEY=VAL,... (A/B only)")
     args = ap.parse_args()
     w = WORKLOADS[args.workload]
     if args.impl == "reference":

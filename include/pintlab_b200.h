@@ -80,6 +80,7 @@ const char* pl_last_error(void);
 #define PL_OPT_RFW 8          /* 1 (default): residual + full weighting fused (TMA levels) */
 #define PL_OPT_ZC_FLOOR 9     /* smallest z-chunk of the TMA kernels (power of two, default 16) */
 #define PL_OPT_FAST_TAIL 10   /* 1 (default): compile-time-sized 15^3/7^3 -> 3^3 jor-rb tail */
+#define PL_OPT_ZC_CTAS 11     /* CTA count the TMA kernels' z chunking aims for (default 1184) */
 int pl_set_option(int key, int value);
 
 /* storage elements of one field (incl. row pads) */

@@ -142,6 +142,7 @@ OPT_MID_TAIL_N = 7
 OPT_RFW = 8
 OPT_ZC_FLOOR = 9
 OPT_FAST_TAIL = 10
+OPT_ZC_CTAS = 11
 
 
 def set_option(key, value):

@@ -225,6 +225,7 @@ extern int g_mid_enabled;
 extern int g_mid_tail_n;
 extern int g_rfw_enabled;
 extern int g_zc_floor;
+extern int g_zc_ctas;
 extern int g_fast_tail;
 }
 
@@ -247,6 +248,14 @@ int pl_set_option(int key, int value) {
       return -1;
     }
     g_zrb_variant = value;
+    return 0;
+  }
+  if (key == PL_OPT_ZC_CTAS) {
+    if (value < 1) {
+      set_error("CTA target must be positive");
+      return PL_ERR_ARG;
+    }
+    g_zc_ctas = value;
     return 0;
   }
   if (key == PL_OPT_FAST_TAIL) {

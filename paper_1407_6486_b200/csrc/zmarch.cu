@@ -1632,6 +1632,7 @@ int make_map(CUtensorMap* m, const double* base, const Geo& g, int bw, int bh) {
 
 }  // namespace
 int g_zc_floor = 16;  // PL_OPT_ZC_FLOOR (A/B): smallest z chunk (4 and 8 measured slower at 127^3)
+int g_zc_ctas = 148 * 8;   // PL_OPT_ZC_CTAS (A/B): CTA count the z chunking aims for
 namespace {
 int pick_zc(const Geo& g) {
   // enough CTAs for several waves on 148 SMs; chunk halo planes cost
@@ -1640,7 +1641,7 @@ int pick_zc(const Geo& g) {
   // and keep all SMs busy.
   long long tiles = (long long)ceil_div(g.nx, TX) * ceil_div(g.ny, TY);
   int zc = 64;
-  while (zc > g_zc_floor && tiles * ceil_div(g.nz, zc) < 148 * 8) zc /= 2;
+  while (zc > g_zc_floor && tiles * ceil_div(g.nz, zc) < g_zc_ctas) zc /= 2;
   return zc;
 }
 
