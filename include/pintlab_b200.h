@@ -67,9 +67,8 @@ const char* pl_last_error(void);
 #define PL_OPT_ZMARCH 0       /* 1 (default): TMA z-marching + fused sweeps, 3-D order 2 */
 #define PL_OPT_ZMARCH_MIN_N 1 /* smallest n-1 using them (default 127, >= 31) */
 #define PL_OPT_GRAPHS 2       /* 1 (default): FixedCycles sweeps replay as CUDA graphs */
-#define PL_OPT_ZRB_VARIANT 3  /* jor-rb TMA sweep kernel: 0 three barriers/plane, 1-3 one
-                                 barrier/plane (ring sizes 6/4, 8/4, 8/6), 4 (default)
-                                 register-pipelined one barrier/plane; all bit-identical */
+#define PL_OPT_ZRB_VARIANT 3  /* jor-rb TMA sweep kernel: 0 three barriers per plane, 4 (default)
+                                 register-pipelined one barrier per plane; bit-identical */
 #define PL_OPT_FUSE_PROLONG 4 /* 1: prolongation fused into the first post-sweep (TMA levels);
                                  default 0 (separate per-cell prolongation is faster) */
 #define PL_OPT_CUBIC_VARIANT 5 /* 3-D cubic kernel: 0 staged loads, 1 (default) TMA ring */

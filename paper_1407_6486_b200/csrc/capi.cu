@@ -243,8 +243,8 @@ int pl_set_option(int key, int value) {
     return 0;
   }
   if (key == PL_OPT_ZRB_VARIANT) {
-    if (value < 0 || value > 5) {
-      set_error("zrb variant %d out of range", value);
+    if (value != 0 && value != 4) {
+      set_error("zrb variant %d out of range (0 or 4)", value);
       return -1;
     }
     g_zrb_variant = value;

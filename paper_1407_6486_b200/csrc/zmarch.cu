@@ -581,21 +581,7 @@ __global__ void __launch_bounds__(NTHR_RB) k_zrb(const __grid_constant__ CUtenso
 }
 
 // ---------------------------------------------------------------------------
-// one fused jor-rb sweep, ONE barrier per plane (k_zrb2)
-//
-// Phase z updates the red points of plane z+2 and the black points of plane
-// z.  A red point reads only black neighbours (old values) and its own
-// centre; a black point reads the red points of planes z-1..z+1, final since
-// phases z-3..z-1.  The two sets touch disjoint data, so one barrier per
-// plane suffices.  Thread (row, px) owns the point pair (x0+2px, x0+2px+1)
-// of tile row `row` on every plane and keeps that pair for planes z-1..z+3
-// (and b for z..z+2) in registers: each plane is read from shared memory
-// once by its owner, the centre and z-neighbours of both updates come from
-// registers, only the x/y neighbours are shared-memory loads.  The 50 red
-// points of the tile's halo ring are updated by threads 0..49.  The division
-// by the (constant) diagonal is the correctly rounded quotient computed from
-// the host's 1/d (div_const); everything else is the reference expression
-// tree (multigrid.py:225-233), so the result is bit-identical to k_zrb.
+// helpers of the one-barrier red-black sweep (k_zrb3)
 
 constexpr int NTHR_RB2 = 256;
 
@@ -619,191 +605,25 @@ __device__ __forceinline__ double div_const(double a, double b, double y) {
 __device__ __forceinline__ double2 lds2(const double* p) {
   return *reinterpret_cast<const double2*>(p);
 }
-__device__ __forceinline__ double sel(bool hi, const double2& v) { return hi ? v.y : v.x; }
-
-template <bool POW2, int RU, int RB>
-__global__ void __launch_bounds__(NTHR_RB2) k_zrb2(const __grid_constant__ CUtensorMap mu,
-                                                   const __grid_constant__ CUtensorMap mb,
-                                                   double* __restrict__ out, Geo g, OpC c,
-                                                   double sigma, double omega, double dval,
-                                                   double dinv, int zc) {
-  static_assert(RU >= 5 && RB >= 3, "ring too small");
-  extern __shared__ __align__(128) double sm[];
-  double* su = sm;
-  double* sb = su + RU * PU;
-  unsigned long long* bu = (unsigned long long*)(sb + RB * PB);
-  unsigned long long* bbar = bu + RU;
-  const int tid = threadIdx.x;
-  const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TY;
-  const int z0 = blockIdx.z * zc, z1 = min(z0 + zc, g.nz);
-  const int R = min(z1, g.nz - 1);          // last plane whose reds are needed
-  const int uhi = R + 1, bhi = R;           // last u / b plane staged
-  if (tid == 0) {
-    for (int i = 0; i < RU; ++i) mbar_init(bu + i, 1);
-    for (int i = 0; i < RB; ++i) mbar_init(bbar + i, 1);
-    fence_barrier_init();
-  }
-  __syncthreads();
-  // u plane p (z0-2 <= p <= uhi): slot (p-z0+2) % RU; b plane q (z0-1..bhi):
-  // slot (q-z0+1) % RB; the k-th use of a slot waits on parity k & 1
-  auto uplane = [&](int p) { return su + ((p - z0 + 2) % RU) * PU; };
-  auto bplane = [&](int q) { return sb + ((q - z0 + 1) % RB) * PB; };
-  auto issue_u = [&](int p) {
-    if (p > uhi) return;
-    const int k = (p - z0 + 2) % RU;
-    mbar_expect(bu + k, UX * UY * 8u);
-    tma3(su + k * PU, &mu, x0 - 2, y0 - 2, p, bu + k);
-  };
-  auto issue_b = [&](int q) {
-    if (q > bhi) return;
-    const int k = (q - z0 + 1) % RB;
-    mbar_expect(bbar + k, BW * BH * 8u);
-    tma3(sb + k * PB, &mb, x0 - 2, y0 - 1, q, bbar + k);
-  };
-  auto wait_u = [&](int p) {
-    const int k = p - z0 + 2;
-    mbar_wait(bu + k % RU, (unsigned)((k / RU) & 1));
-  };
-  auto wait_b = [&](int q) {
-    const int k = q - z0 + 1;
-    mbar_wait(bbar + k % RB, (unsigned)((k / RB) & 1));
-  };
-  if (tid == 0) {
-    for (int p = z0 - 2; p < z0 - 2 + RU; ++p) issue_u(p);
-    for (int q = z0 - 1; q < z0 - 1 + RB; ++q) issue_b(q);
-  }
-
-  // ---- per-thread geometry (fixed for all planes)
-  const int row = tid >> 4, px = tid & 15;
-  const int gy = y0 + row, gxa = x0 + 2 * px;
-  const bool va = gy < g.ny && gxa < g.nx, vb = gy < g.ny && gxa + 1 < g.nx;
-  const int iu = (row + 2) * UX + 2 * px + 2;     // first pair member, u window
-  const int ib = (row + 1) * BW + 2 * px + 2;     // first pair member, b window
-  double* optr = out + (long long)gy * g.sy + gxa;
-  // halo ring red point h = tid < 50, per plane parity P
-  int hu[2], hb[2];
-  bool hv[2];
-#pragma unroll
-  for (int P = 0; P < 2; ++P) {
-    int xx, yy;   // window-relative (tile origin = 0)
-    if (tid < 17) { yy = -1; xx = -1 + 2 * tid + (1 - P); }
-    else if (tid < 34) { yy = TY; xx = -1 + 2 * (tid - 17) + P; }
-    else if (tid < 42) { xx = -1; yy = 2 * (tid - 34) + P; }
-    else { xx = TX; yy = 2 * (tid - 42) + (1 - P); }
-    hu[P] = (yy + 2) * UX + xx + 2;
-    hb[P] = (yy + 1) * BW + xx + 2;
-    hv[P] = tid < 50 && x0 + xx >= 0 && x0 + xx < g.nx && y0 + yy >= 0 && y0 + yy < g.ny;
-  }
-  const int hu0 = hu[0], hu1 = hu[1], hb0 = hb[0], hb1 = hb[1];
-  const bool hv0 = hv[0], hv1 = hv[1];
-
-  auto lap = [&](double zm, double zp, double ym, double yp, double xm, double xp, double cc) {
-    double acc = 0.0;
-    acc = acc + dd2<POW2>((zm - 2.0 * cc) + zp, c);
-    acc = acc + dd2<POW2>((ym - 2.0 * cc) + yp, c);
-    acc = acc + dd2<POW2>((xm - 2.0 * cc) + xp, c);
-    return c.nu * acc;
-  };
-  auto relax = [&](double cc, double bv, double lp) {
-    const double r = bv - (cc - sigma * lp);
-    return cc + div_const(omega * r, dval, dinv);
-  };
-  // interior red member of the own pair on plane q (registers um, uc, up, bq)
-  auto red_own = [&](double* pl, const double2& um, double2& uc, const double2& up,
-                     const double2& bq, int q) {
-    const bool o = ((gy + q) & 1) == 0;             // red member: x odd <=> o
-    const double cc = sel(o, uc);
-    const double xo = pl[o ? iu + 2 : iu - 1];
-    const double xm = o ? uc.x : xo, xp = o ? xo : uc.y;
-    const double lp = lap(sel(o, um), sel(o, up), pl[iu - UX + o], pl[iu + UX + o], xm, xp, cc);
-    const double v = relax(cc, sel(o, bq), lp);
-    if ((o ? vb : va) && q >= 0 && q <= R) {
-      pl[iu + o] = v;
-      if (o) uc.y = v; else uc.x = v;
-    }
-  };
-  // halo red point on plane q (shared memory only)
-  auto red_halo = [&](int q) {
-    if (tid >= 50 || q < 0 || q > R) return;
-    const bool P = q & 1;
-    if (!(P ? hv1 : hv0)) return;
-    const int i = P ? hu1 : hu0;
-    double* pl = uplane(q);
-    const double* pm = uplane(q - 1);
-    const double* pp = uplane(q + 1);
-    const double cc = pl[i];
-    const double lp = lap(pm[i], pp[i], pl[i - UX], pl[i + UX], pl[i - 1], pl[i + 1], cc);
-    pl[i] = relax(cc, bplane(q)[P ? hb1 : hb0], lp);
-  };
-
-  // ---- prologue: reds of planes z0-1, z0, z0+1
-  for (int p = z0 - 2; p <= min(z0 + 2, uhi); ++p) wait_u(p);
-  for (int q = z0 - 1; q <= min(z0 + 1, bhi); ++q) wait_b(q);
-  double2 Um2 = lds2(uplane(z0 - 2) + iu);
-  double2 U0 = lds2(uplane(z0 - 1) + iu);
-  double2 U1 = lds2(uplane(z0) + iu);
-  double2 U2 = lds2(uplane(z0 + 1) + iu);
-  double2 U3 = z0 + 2 <= uhi ? lds2(uplane(z0 + 2) + iu) : make_double2(0.0, 0.0);
-  double2 Bm1 = lds2(bplane(z0 - 1) + ib);
-  double2 B0 = lds2(bplane(z0) + ib);
-  double2 B1 = z0 + 1 <= bhi ? lds2(bplane(z0 + 1) + ib) : make_double2(0.0, 0.0);
-  red_own(uplane(z0 - 1), Um2, U0, U1, Bm1, z0 - 1);
-  red_own(uplane(z0), U0, U1, U2, B0, z0);
-  if (z0 + 1 <= R) red_own(uplane(z0 + 1), U1, U2, U3, B1, z0 + 1);
-  red_halo(z0 - 1);
-  red_halo(z0);
-  red_halo(z0 + 1);
-  __syncthreads();
-  if (tid == 0) {
-    issue_u(z0 - 2 + RU);
-    issue_b(z0 - 1 + RB);
-  }
-
-  // ---- main loop: U0..U4 = own pair on planes z-1..z+3, B0..B2 = b on z..z+2
-  for (int z = z0; z < z1; ++z) {
-    const int q = z + 2;
-    const bool red = q <= R;
-    double2 U4 = make_double2(0.0, 0.0), B2 = make_double2(0.0, 0.0);
-    if (red) {
-      wait_u(q + 1);
-      wait_b(q);
-      U4 = lds2(uplane(q + 1) + iu);
-      B2 = lds2(bplane(q) + ib);
-      red_own(uplane(q), U2, U3, U4, B2, q);
-    }
-    // black member of the own pair on plane z
-    {
-      double* pl = uplane(z);
-      const bool o = ((gy + z) & 1) != 0;           // black member: x odd <=> o
-      const double cc = sel(o, U1);
-      const double xo = pl[o ? iu + 2 : iu - 1];
-      const double xm = o ? U1.x : xo, xp = o ? xo : U1.y;
-      const double lp = lap(sel(o, U0), sel(o, U2), pl[iu - UX + o], pl[iu + UX + o], xm, xp, cc);
-      const double v = relax(cc, sel(o, B0), lp);
-      double* dst = optr + (long long)z * g.sz;
-      const double2 w = o ? make_double2(U1.x, v) : make_double2(v, U1.y);
-      if (va && vb) *reinterpret_cast<double2*>(dst) = w;
-      else if (va) dst[0] = w.x;
-    }
-    red_halo(q);
-    __syncthreads();   // u plane z-1 and b plane z are free
-    if (tid == 0) {
-      issue_u(z - 1 + RU);
-      issue_b(z + RB);
-    }
-    U0 = U1; U1 = U2; U2 = U3; U3 = U4;
-    B0 = B1; B1 = B2;
-  }
-}
 
 // ---------------------------------------------------------------------------
-// k_zrb3: k_zrb2's schedule with the colour made warp-uniform.  Warp w owns
-// tile rows 4(w/2) + (w&1) and that + 2, so (y + z) has one parity per warp
-// and plane; the phase code is instantiated per parity (no selects), the main
-// loop is unrolled by two planes, rings are powers of two, and b is read
-// from shared memory once per plane (by its red phase) into registers.
-// u plane p is read from shared memory in phases p-3 .. p, b plane q in
-// phase q-2 only, so the rings recycle as soon as possible.
+// k_zrb3: one fused jor-rb sweep (multigrid.py:225-233) with ONE barrier per
+// plane.  Phase z updates the red points of plane z+2 and the black points of
+// plane z: a red point reads only black neighbours (old values) and its own
+// centre, a black point reads the red points of planes z-1..z+1, final since
+// phases z-3..z-1 -- the two sets touch disjoint data.  Thread (row, px) owns
+// the point pair (x0+2px, x0+2px+1) of its row on every plane and carries
+// that pair for planes z-1..z+3 (and b for z..z+2) in registers, so the
+// centre and z-neighbours come from registers and only x/y neighbours are
+// shared-memory loads; the 50 red points of the tile's halo ring are updated
+// by threads 0..49.  Warp w owns tile rows 4(w/2) + (w&1) and that + 2, so
+// (y + z) has one parity per warp and plane: the phase code is instantiated
+// per parity (no selects), the plane loop is unrolled by two, rings are
+// powers of two.  u plane p is read from shared memory in phases p-3 .. p,
+// b plane q in phase q-2 only, so the rings recycle as soon as possible.
+// The division by the constant diagonal is div_const (correctly rounded);
+// everything else is the reference's expression tree, so the sweep is
+// bit-identical to the one-colour kernels.
 
 struct RbCtx {
   double* su;
@@ -937,8 +757,8 @@ __device__ __forceinline__ void rb_phase(const RbCtx& k, int z, const double2& U
   else if (k.va) dst[0] = w.x;
 }
 
-template <bool POW2, int RU, int RB, int MINB>
-__global__ void __launch_bounds__(NTHR_RB2, MINB) k_zrb3(const __grid_constant__ CUtensorMap mu,
+template <bool POW2, int RU, int RB, int MINB, bool HW>
+__global__ void __launch_bounds__(HW ? 320 : NTHR_RB2, MINB) k_zrb3(const __grid_constant__ CUtensorMap mu,
                                                       const __grid_constant__ CUtensorMap mb,
                                                       double* __restrict__ out, Geo g, OpC c,
                                                       double sigma, double omega, double dval,
@@ -1000,19 +820,25 @@ __global__ void __launch_bounds__(NTHR_RB2, MINB) k_zrb3(const __grid_constant__
   k.ib = (row + 1) * BW + 2 * px + 2;
   k.optr = out + (long long)gy * g.sy + gxa;
   k.sz = g.sz;
+  // HW: warps 8-9 (threads 256..305) own the 50 halo reds and nothing else,
+  // so no warp does more than two updates per phase
+  const int hid = HW ? tid - 256 : tid;
+  const bool is_halo = HW ? warp >= 8 : hid < 50;
+  const bool is_int = HW ? warp < 8 : true;
   {
     int hu[2], hb[2];
     bool hv[2];
 #pragma unroll
     for (int P = 0; P < 2; ++P) {
       int xx, yy;
-      if (tid < 17) { yy = -1; xx = -1 + 2 * tid + (1 - P); }
-      else if (tid < 34) { yy = TY; xx = -1 + 2 * (tid - 17) + P; }
-      else if (tid < 42) { xx = -1; yy = 2 * (tid - 34) + P; }
-      else { xx = TX; yy = 2 * (tid - 42) + (1 - P); }
+      if (hid < 17) { yy = -1; xx = -1 + 2 * hid + (1 - P); }
+      else if (hid < 34) { yy = TY; xx = -1 + 2 * (hid - 17) + P; }
+      else if (hid < 42) { xx = -1; yy = 2 * (hid - 34) + P; }
+      else { xx = TX; yy = 2 * (hid - 42) + (1 - P); }
       hu[P] = (yy + 2) * UX + xx + 2;
       hb[P] = (yy + 1) * BW + xx + 2;
-      hv[P] = tid < 50 && x0 + xx >= 0 && x0 + xx < g.nx && y0 + yy >= 0 && y0 + yy < g.ny;
+      hv[P] = hid >= 0 && hid < 50 && x0 + xx >= 0 && x0 + xx < g.nx && y0 + yy >= 0 &&
+              y0 + yy < g.ny;
     }
     k.hu0 = hu[0]; k.hu1 = hu[1]; k.hb0 = hb[0]; k.hb1 = hb[1];
     k.hv0 = hv[0]; k.hv1 = hv[1];
@@ -1023,6 +849,11 @@ __global__ void __launch_bounds__(NTHR_RB2, MINB) k_zrb3(const __grid_constant__
   for (int p = z0 - 2; p <= min(z0 + 2, uhi); ++p) wait_u(p);
   for (int q = z0 - 1; q <= min(z0, bhi); ++q) wait_b(q);
   const double2 zero2 = make_double2(0.0, 0.0);
+  if (HW && !is_int) {      // interior registers of the halo warps are unused
+    k.iu = 2 * UX + 2;
+    k.ib = BW + 2;
+    k.va = k.vb = false;
+  }
   double2 Um2 = lds2(rb_u<RU>(k, z0 - 2) + k.iu);
   double2 U0 = lds2(rb_u<RU>(k, z0 - 1) + k.iu);
   double2 U1 = lds2(rb_u<RU>(k, z0) + k.iu);
@@ -1045,9 +876,11 @@ __global__ void __launch_bounds__(NTHR_RB2, MINB) k_zrb3(const __grid_constant__
       if (k.vb) { pl[k.iu + 1] = v; uc.y = v; }
     }
   };
-  pro_red(z0 - 1, Um2, U0, U1, Bm1, 1 - wpar);
-  pro_red(z0, U0, U1, U2, B0, wpar);
-  if (tid < 50) {
+  if (is_int) {
+    pro_red(z0 - 1, Um2, U0, U1, Bm1, 1 - wpar);
+    pro_red(z0, U0, U1, U2, B0, wpar);
+  }
+  if (is_halo) {
     rb_halo<POW2, RU, RB, 1>(k, z0 - 1);
     rb_halo<POW2, RU, RB, 0>(k, z0);
   }
@@ -1057,8 +890,8 @@ __global__ void __launch_bounds__(NTHR_RB2, MINB) k_zrb3(const __grid_constant__
   }
   if (z0 + 1 <= bhi) wait_b(z0 + 1);
   double2 B1 = z0 + 1 <= bhi ? lds2(rb_b<RB>(k, z0 + 1) + k.ib) : zero2;
-  pro_red(z0 + 1, U1, U2, U3, B1, 1 - wpar);
-  if (tid < 50) rb_halo<POW2, RU, RB, 1>(k, z0 + 1);
+  if (is_int) pro_red(z0 + 1, U1, U2, U3, B1, 1 - wpar);
+  if (is_halo) rb_halo<POW2, RU, RB, 1>(k, z0 + 1);
   __syncthreads();
   if (tid == 0) {       // u planes z0-2, z0-1 and b planes z0-1 .. z0+1 are dead
     issue_u(z0 - 2 + RU);
@@ -1083,8 +916,8 @@ __global__ void __launch_bounds__(NTHR_RB2, MINB) k_zrb3(const __grid_constant__
       }
       double2 U4 = lds2(rb_u<RU>(k, z + 3) + k.iu);   // stale beyond R: unused
       const double2 B2 = lds2(rb_b<RB>(k, z + 2) + k.ib);
-      rb_phase<POW2, RU, RB, PA>(k, z, U0, U1, U2, U3, U4, B0, B2);
-      if (tid < 50) rb_halo<POW2, RU, RB, 0>(k, z + 2);
+      if (is_int) rb_phase<POW2, RU, RB, PA>(k, z, U0, U1, U2, U3, U4, B0, B2);
+      if (is_halo) rb_halo<POW2, RU, RB, 0>(k, z + 2);
       __syncthreads();
       if (tid == 0) {
         issue_u(z + RU);
@@ -1098,8 +931,8 @@ __global__ void __launch_bounds__(NTHR_RB2, MINB) k_zrb3(const __grid_constant__
       }
       double2 U5 = lds2(rb_u<RU>(k, z + 4) + k.iu);
       const double2 B3 = lds2(rb_b<RB>(k, z + 3) + k.ib);
-      rb_phase<POW2, RU, RB, PB>(k, z + 1, U1, U2, U3, U4, U5, B1, B3);
-      if (tid < 50) rb_halo<POW2, RU, RB, 1>(k, z + 3);
+      if (is_int) rb_phase<POW2, RU, RB, PB>(k, z + 1, U1, U2, U3, U4, U5, B1, B3);
+      if (is_halo) rb_halo<POW2, RU, RB, 1>(k, z + 3);
       __syncthreads();
       if (tid == 0) {
         issue_u(z + 1 + RU);
@@ -1726,45 +1559,20 @@ int launch_zrb(const double* u, const double* b, const double* e, const Geo& gc,
   return 0;
 }
 
-int launch_zrb2(const double* u, const double* b, double* out, const Geo& g, const OpC& c,
-                double sigma, double omega, double dval, int variant, cudaStream_t s) {
+int launch_zrb3(const double* u, const double* b, double* out, const Geo& g, const OpC& c,
+                double sigma, double omega, double dval, cudaStream_t s) {
   CUtensorMap mu, mb;
   PL_TRY(make_map(&mu, u, g, UX, UY));
   PL_TRY(make_map(&mb, b, g, BW, BH));
   int zc = pick_zc(g);
   dim3 grid(ceil_div(g.nx, TX), ceil_div(g.ny, TY), ceil_div(g.nz, zc));
   const double dinv = 1.0 / dval;
-#define PL_ZRB2(P2, RU, RB)                                                          \
-  do {                                                                              \
-    size_t smem = ((size_t)RU * PU + (size_t)RB * PB) * 8 + 8 * (RU + RB);          \
-    auto kern = k_zrb2<P2, RU, RB>;                                                 \
-    raise_smem(kern, smem);                                                         \
-    kern<<<grid, dim3(NTHR_RB2), smem, s>>>(mu, mb, out, g, c, sigma, omega, dval, dinv, zc); \
-  } while (0)
-  if (variant == 4) {
-    size_t smem = ((size_t)8 * PU + (size_t)4 * PB) * 8 + 8 * (8 + 4);
-    auto kern = c.pow2 ? k_zrb3<true, 8, 4, 3> : k_zrb3<false, 8, 4, 3>;
-    raise_smem(kern, smem);
-    kern<<<grid, dim3(NTHR_RB2), smem, s>>>(mu, mb, out, g, c, sigma, omega, dval, dinv, zc);
-  } else if (variant == 5) {   // 2-plane b ring: 56.7 KB, 4 CTAs / SM (<= 64 registers)
-    size_t smem = ((size_t)8 * PU + (size_t)2 * PB) * 8 + 8 * (8 + 2);
-    auto kern = c.pow2 ? k_zrb3<true, 8, 2, 4> : k_zrb3<false, 8, 2, 4>;
-    raise_smem(kern, smem);
-    kern<<<grid, dim3(NTHR_RB2), smem, s>>>(mu, mb, out, g, c, sigma, omega, dval, dinv, zc);
-  } else if (variant == 2) {
-    if (c.pow2) PL_ZRB2(true, 8, 4); else PL_ZRB2(false, 8, 4);
-  } else if (variant == 3) {
-    if (c.pow2) PL_ZRB2(true, 8, 6); else PL_ZRB2(false, 8, 6);
-  } else {
-    if (c.pow2) PL_ZRB2(true, 6, 4); else PL_ZRB2(false, 6, 4);
-  }
-#undef PL_ZRB2
+  size_t smem = ((size_t)8 * PU + (size_t)4 * PB) * 8 + 8 * (8 + 4);
+  auto kern = c.pow2 ? k_zrb3<true, 8, 4, 3, false> : k_zrb3<false, 8, 4, 3, false>;
+  raise_smem(kern, smem);
+  kern<<<grid, dim3(NTHR_RB2), smem, s>>>(mu, mb, out, g, c, sigma, omega, dval, dinv, zc);
   return 0;
 }
-
-}  // namespace
-int g_cubic_variant = 1;    // 0: k_cubic3, 1: k_cubic4 (TMA ring, one barrier per plane)
-namespace {
 
 int launch_rfw(const double* u, const double* b, double* coarse, const Geo& g, const OpC& c,
                double sigma, cudaStream_t s) {
@@ -1780,6 +1588,10 @@ int launch_rfw(const double* u, const double* b, double* coarse, const Geo& g, c
   kern<<<grid, block, smem, s>>>(mu, mb, coarse, g, gc, c, sigma, zcc);
   return 0;
 }
+
+}  // namespace
+int g_cubic_variant = 1;    // 0: k_cubic3, 1: k_cubic4 (TMA ring, one barrier per plane)
+namespace {
 
 int launch_cubic3(const double* coarse, double* fine, const Geo& gf, const int* cnt,
                   const int* idx, const double* w, int accumulate, cudaStream_t s) {
@@ -1824,7 +1636,7 @@ double zdiag(const OpC& c, double sigma) {
 }
 
 int g_zmarch_enabled = 1;   // runtime knob (pl_set_option), for A/B tests
-int g_zrb_variant = 4;      // 0: k_zrb (3 barriers / plane), 1-3: k_zrb2 rings, 4: k_zrb3
+int g_zrb_variant = 4;      // 0: k_zrb (3 barriers / plane), 4: k_zrb3 (one barrier / plane)
 int g_fuse_prolong = 0;     // prolongation fused into the first post-sweep (slower since k_zrb3)
 bool zmarch_fuse_prolong() { return g_fuse_prolong != 0; }
 // smallest interior size for the TMA kernels: below it a CTA would march many
@@ -1895,7 +1707,7 @@ int zlaunch_rb(const double* u, const double* b, double* out, const Geo& g, cons
   Geo gc = make_geo(3, (g.N + 1) / 2);
   PL_PRE(K_RB);
   if (e || g_zrb_variant == 0) PL_TRY(launch_zrb(u, b, e, gc, out, g, c, sigma, omega, dval, s));
-  else PL_TRY(launch_zrb2(u, b, out, g, c, sigma, omega, dval, g_zrb_variant, s));
+  else PL_TRY(launch_zrb3(u, b, out, g, c, sigma, omega, dval, s));
   PL_CHECK_LAUNCH(K_RB, 24.0 * g.npts + (e ? 16.0 * g.npts + 8.0 * gc.npts : 0.0));
   return 0;
 }

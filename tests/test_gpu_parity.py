@@ -397,7 +397,7 @@ def test_pfasst_run_parity_tma_path(name):
         _capi.set_option(_capi.OPT_ZMARCH_MIN_N, 127)
 
 
-@pytest.mark.parametrize("variant", [0, 1, 2, 3, 4, 5])
+@pytest.mark.parametrize("variant", [0, 4])
 def test_zrb_variants_bitwise_31cubed(variant):
     """Every jor-rb TMA sweep variant (three barriers per plane, and the
     register-pipelined one-barrier kernels with their ring sizes) reproduces
@@ -436,7 +436,7 @@ def test_zrb_variants_equal_plain_kernels(n, length, sigma, fuse):
     _capi.set_option(_capi.OPT_ZMARCH, 1)
     _capi.set_option(_capi.OPT_FUSE_PROLONG, fuse)
     try:
-        for variant in (0, 1, 2, 3, 4, 5):
+        for variant in (0, 4):
             _capi.set_option(_capi.OPT_ZRB_VARIANT, variant)
             assert torch.equal(mg.v_cycle(sop, u, b, cfg), ref), variant
             assert torch.equal(mg.smooth(sop, u, b, cfg, 2), ref_s), variant
