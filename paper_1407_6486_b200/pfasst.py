@@ -477,6 +477,22 @@ class _Block:
             caller.wait_stream(e.streams[n])
 
 
+def _rank_streams_fit(levels, p) -> bool:
+    """Per-rank streams give each time rank its own sweep / multigrid scratch.
+    Use them only when that extra memory (a conservative 2x of the sweep and
+    multigrid workspaces per level) fits in half of the free device memory;
+    otherwise the single-stream schedule runs (same results)."""
+    from . import _capi as capi
+    lib = capi.lib()
+    per = 0
+    for lv in levels:
+        g = lv.operator.grid
+        per += 2 * (lib.pl_sweep_workspace_bytes(g.dim, g.n, lv.table.m) +
+                    lib.pl_mg_workspace_bytes(g.dim, g.n, lv.mg_cfg.coarsest_n))
+    free, _ = torch.cuda.mem_get_info()
+    return (p - 1) * per <= 0.5 * free
+
+
 def _gather_block(blk, exchange):
     """Combine per-process bookkeeping (nccl executor)."""
     if not isinstance(exchange, DistExchange):
@@ -507,7 +523,8 @@ def pfasst_run(levels, u0, t_end: float, p: int, blocks: int = 1, tol: float = 1
     ``u0`` may be a numpy array (result returned on the host, drop-in) or an
     fp64 CUDA tensor (result stays on the device).  ``streams`` (single
     process only) issues each time rank on its own CUDA stream in wavefront
-    order; results are identical either way."""
+    order when the per-stream scratch fits (``_rank_streams_fit``); results
+    are identical either way."""
     check_hierarchy(levels)
     if executor not in ("serial", "threaded", "nccl"):
         raise ValueError(f"unknown executor {executor!r}")
@@ -532,9 +549,11 @@ def pfasst_run(levels, u0, t_end: float, p: int, blocks: int = 1, tol: float = 1
             exchange = DistExchange(engine, group)
         else:
             if engine is None:
-                engine = (DeviceEngine(levels, dt, range(p), streams=streams)
-                          if engine_factory is DeviceEngine else
-                          engine_factory(levels, dt, range(p)))
+                if engine_factory is DeviceEngine:
+                    use = streams and p > 1 and _rank_streams_fit(levels, p)
+                    engine = DeviceEngine(levels, dt, range(p), streams=use)
+                else:
+                    engine = engine_factory(levels, dt, range(p))
             exchange = _LocalExchange(engine)
         for n in range(p):
             if exchange.owns(n):
