@@ -80,6 +80,12 @@ const char* pl_last_error(void);
 #define PL_OPT_ZC_FLOOR 9     /* smallest z-chunk of the TMA kernels (power of two, default 16) */
 #define PL_OPT_FAST_TAIL 10   /* 1 (default): compile-time-sized 15^3/7^3 -> 3^3 jor-rb tail */
 #define PL_OPT_ZC_CTAS 11     /* CTA count the TMA kernels' z chunking aims for (default 1184) */
+#define PL_OPT_MID2 12        /* 1: the cooperative small-level kernel runs one grid phase per
+                                 level and direction (overlapped shared-memory tiles, LU fused
+                                 into the last down phase); 0 (default, measured faster): one
+                                 phase per former kernel plus the one-CTA tail */
+#define PL_OPT_MID_CTAS 13    /* CTAs of the cooperative small-level kernels (default 32; 0: one
+                                 per SM); fewer leave SMs to other time ranks' streams */
 int pl_set_option(int key, int value);
 
 /* storage elements of one field (incl. row pads) */

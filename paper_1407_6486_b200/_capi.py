@@ -143,6 +143,8 @@ OPT_RFW = 8
 OPT_ZC_FLOOR = 9
 OPT_FAST_TAIL = 10
 OPT_ZC_CTAS = 11
+OPT_MID2 = 12
+OPT_MID_CTAS = 13
 
 
 def set_option(key, value):

@@ -227,6 +227,8 @@ extern int g_rfw_enabled;
 extern int g_zc_floor;
 extern int g_zc_ctas;
 extern int g_fast_tail;
+extern int g_mid2_enabled;
+extern int g_mid_ctas;
 }
 
 extern "C" {
@@ -276,6 +278,18 @@ int pl_set_option(int key, int value) {
   }
   if (key == PL_OPT_MID) {
     g_mid_enabled = value != 0;
+    return 0;
+  }
+  if (key == PL_OPT_MID_CTAS) {
+    if (value < 0) {
+      set_error("mid CTA count must be >= 0");
+      return PL_ERR_ARG;
+    }
+    g_mid_ctas = value;
+    return 0;
+  }
+  if (key == PL_OPT_MID2) {
+    g_mid2_enabled = value != 0;
     return 0;
   }
   if (key == PL_OPT_MID_TAIL_N) {

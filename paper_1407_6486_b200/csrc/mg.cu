@@ -641,6 +641,7 @@ static int launch_tail(MgPlan* P, int l0, double* u, const double* b, double sig
 
 int g_mid_enabled = 1;      // PL_OPT_MID
 int g_mid_tail_n = 15;      // PL_OPT_MID_TAIL_N: largest N the mid kernel leaves to its tail
+int g_mid_ctas = 32;        // PL_OPT_MID_CTAS: CTAs of the cooperative mid kernels (0: one per SM)
 
 // first tail level of the mid kernel (>= the plan's tail_start)
 static int mid_tail_level(const MgPlan* P) {
@@ -654,8 +655,20 @@ static bool mid_applies(const MgPlan* P, int l) {
          l < mid_tail_level(P) && mid_tail_level(P) - l <= MID_MAX;
 }
 
+bool mid2_applies(const MgPlan* P, int l0);
+int launch_mid2(MgPlan* P, int l0, double* u, const double* b, double sigma, int zero,
+                const double* lu_dev, cudaStream_t s);
+
 static int launch_mid(MgPlan* P, int l0, double* u, const double* b, double sigma, int zero,
                       cudaStream_t s) {
+  if (mid2_applies(P, l0)) {
+    auto it = P->lu.find(*(unsigned long long*)&sigma);
+    if (it == P->lu.end()) {
+      set_error("coarsest LU for sigma=%.17g not prepared", sigma);
+      return -3;
+    }
+    return launch_mid2(P, l0, u, b, sigma, zero, it->second.dev, s);
+  }
   const int lt = mid_tail_level(P);
   MidArgs m;
   std::memset(&m, 0, sizeof(m));
@@ -697,6 +710,7 @@ static int launch_mid(MgPlan* P, int l0, double* u, const double* b, double sigm
       return 2;
     }
   }
+  const int nblk = g_mid_ctas > 0 && g_mid_ctas < grid ? g_mid_ctas : grid;
   static unsigned long long* trace = nullptr;
   static const bool tracing = std::getenv("PL_MID_TRACE") != nullptr;
   if (tracing && !trace) cudaMalloc(&trace, 64 * sizeof(unsigned long long));
@@ -704,7 +718,7 @@ static int launch_mid(MgPlan* P, int l0, double* u, const double* b, double sigm
   if (tracing) cudaMemsetAsync(trace, 0, 64 * sizeof(unsigned long long), s);
   void* args[] = {&m, &ta};
   PL_PRE(K_MID);
-  cudaError_t e = cudaLaunchCooperativeKernel((void*)k_mid<3>, grid, MID_THREADS, args, smem, s);
+  cudaError_t e = cudaLaunchCooperativeKernel((void*)k_mid<3>, nblk, MID_THREADS, args, smem, s);
   if (e != cudaSuccess) return cuda_status(e, "cooperative mid launch");
   bytes += 8.0 * P->lv[lt].g.npts * 3;
   if (tracing) {   // diagnostics only: per-phase durations of this launch

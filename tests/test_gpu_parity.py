@@ -471,6 +471,48 @@ def test_cooperative_mid_vcycle_equals_separate_launches(n, pre, post, omega):
         _capi.set_option(_capi.OPT_MID_TAIL_N, 15)
 
 
+@pytest.mark.parametrize("n,length", [(16, 1.0), (32, 1.0), (64, 1.0), (64, 1.5), (128, 0.7),
+                                      (256, 1.0)])
+@pytest.mark.parametrize("pre,post,omega", [(1, 1, 1.0), (2, 1, 0.9), (1, 2, 1.0), (0, 1, 1.0),
+                                            (2, 0, 0.8)])
+def test_mid2_one_phase_per_level_equals_separate_launches(n, length, pre, post, omega):
+    """The overlapped-tile cooperative kernel (one grid phase per level and
+    direction, LU fused into the last down phase) reproduces the per-level
+    launches and the previous cooperative kernel bit for bit, from a guess and
+    from zero, for power-of-two and general dx^2."""
+    rng = np.random.default_rng(11 * n + 3 * pre + post)
+    g = heat.Grid(3, n, length)
+    u = dev(rng.standard_normal(g.shape))
+    b = dev(rng.standard_normal(g.shape))
+    sop = mg.ShiftedOperator(heat.HeatOperator(g), 0.0021)
+    cfg = mg.MgConfig("jor-rb", omega, pre, post)
+    try:
+        _capi.set_option(_capi.OPT_MID, 0)
+        ref = mg.v_cycle(sop, u, b, cfg)
+        ref0 = mg.v_cycle(sop, torch.zeros_like(u), b, cfg)
+        _capi.set_option(_capi.OPT_MID, 1)
+        _capi.set_option(_capi.OPT_MID2, 0)
+        assert torch.equal(mg.v_cycle(sop, u, b, cfg), ref)
+        _capi.set_option(_capi.OPT_MID2, 1)
+        for ctas in (0, 7, 32):
+            _capi.set_option(_capi.OPT_MID_CTAS, ctas)
+            assert torch.equal(mg.v_cycle(sop, u, b, cfg), ref), ctas
+        got = mg.v_cycle(sop, u, b, cfg)
+        assert torch.equal(got, ref), float((got - ref).abs().max())
+        assert torch.equal(mg.v_cycle(sop, torch.zeros_like(u), b, cfg), ref0)
+        two = mg.solve(sop, u, b, cfg, mg.FixedCycles(2)).u
+        _capi.set_option(_capi.OPT_MID2, 0)
+        assert torch.equal(mg.solve(sop, u, b, cfg, mg.FixedCycles(2)).u, two)
+        _capi.set_option(_capi.OPT_MID2, 0)
+        for ctas in (0, 5):
+            _capi.set_option(_capi.OPT_MID_CTAS, ctas)
+            assert torch.equal(mg.v_cycle(sop, u, b, cfg), ref), ctas
+    finally:
+        _capi.set_option(_capi.OPT_MID, 1)
+        _capi.set_option(_capi.OPT_MID2, 0)
+        _capi.set_option(_capi.OPT_MID_CTAS, 32)
+
+
 @pytest.mark.parametrize("name", ["run_cfg1", "run_cfg2_small", "run_cfg3_small", "run_cfg4_small_tol"])
 def test_pfasst_rank_streams_identical(name):
     """The wavefront schedule with one CUDA stream per time rank gives exactly
