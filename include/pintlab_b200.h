@@ -118,6 +118,8 @@ int pl_interp_cubic(const double* coarse, double* fine, int dim, int nf, int acc
 /* ---- geometric multigrid (multigrid.py) ---------------------------------- */
 size_t pl_mg_workspace_bytes(int dim, int n, int coarsest_n);
 /* MgConfig + the fine HeatOperator -> plan (multigrid.py:24-38, 178-201) */
+/* smoother: 0 jacobi, 1 gauss-seidel (lexicographic, hyperplane wavefront,
+   bit-identical to scipy solve_banded), 2 jor-rb */
 int pl_mg_plan_create(pl_mg_plan** plan, int dim, int n, double length, double nu, int order,
                       int smoother, double omega, int pre_sweeps, int post_sweeps,
                       int coarsest_n, void* workspace, size_t workspace_bytes);
@@ -145,6 +147,16 @@ int pl_mg_solve_tol(pl_mg_plan* plan, double* u, const double* b, double sigma, 
                     double stall, int max_cycles, int* cycles, int* status, double* residual,
                     void* stream);
 
+/* Direct policy (multigrid.py:63-65, 203-208, 263-264: SuperLU of the shifted
+   matrix) by fast diagonalisation: install T = V diag(lam) V^-1 of the plan's
+   1-D stencil matrix (host arrays, row-major (n-1) x (n-1): W = V^-1, W^T, V,
+   V^T, then lam), computed by the caller with numpy eigh/eig; then
+   u = (I - sigma nu Lap_h)^-1 b with dense cuBLAS GEMMs along each axis.
+   Agrees with SuperLU to rounding (tolerance, not bitwise). */
+int pl_mg_set_direct(pl_mg_plan* plan, const double* w, const double* wt, const double* v,
+                     const double* vt, const double* lam, void* stream);
+int pl_mg_direct(pl_mg_plan* plan, double* u, const double* b, double sigma, void* stream);
+
 /* ---- SDC sweeper (sdc.py) ------------------------------------------------ */
 #define PL_MAX_NODES 17 /* M + 1 <= 17 */
 
@@ -152,7 +164,7 @@ typedef struct pl_sweep_desc {
   int m;                                  /* sub-steps M */
   double qdelta[PL_MAX_NODES * PL_MAX_NODES]; /* rows m: Q[m+1,:] - Q[m,:], M x (M+1) */
   double gammas[PL_MAX_NODES];            /* float(gamma_m), sub-step fractions */
-  int policy;                             /* 0 FixedCycles, 1 ToTolerance */
+  int policy;                             /* 0 FixedCycles, 1 ToTolerance, 2 Direct */
   int fixed_cycles;
   double tol, stall;
   int max_cycles;

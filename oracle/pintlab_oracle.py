@@ -261,6 +261,57 @@ def shifted_matrix(op, sigma):
     return (scipy.sparse.identity(a.shape[0], format="csr") - sigma * a).tocsr()
 
 
+def gs_lower_solve_gbtrs(op, sigma, r):
+    """(D + L) y = r in the operation order of the reference's
+    scipy.linalg.solve_banded (multigrid.py:144-158, 219-224 -> LAPACK
+    dgbtrf/dgbtrs, no pivoting since the diagonal dominates each column):
+    l_ij = A_ij * RN(1/D_j) (dgbtrf DSCAL), y_i = fma(-y_j, l_ij, y_i) over the
+    lower neighbours j in increasing linear index (dgbtrs DGER), du = y / D
+    (DTBSV).  Pure-Python loops: the statement the CUDA wavefront
+    (csrc/gs.cuh) restates, checked bit for bit against solve_banded in
+    tests/test_oracle_golden.py; small grids only."""
+    a = shifted_matrix(op, sigma).tocsr()
+    d = a.diagonal()
+    y = r.ravel().astype(np.float64).copy()
+    for i in range(y.size):
+        row = a.getrow(i)
+        for j, aij in sorted(zip(row.indices, row.data)):
+            if j >= i:
+                break
+            l = aij * (1.0 / d[j])
+            y[i] = float(Fraction(-y[j]) * Fraction(l) + Fraction(y[i]))   # exact fma
+    return (y / d).reshape(r.shape)
+
+
+def direct_fast_diag(op, sigma, b):
+    """The GPU Direct algorithm (csrc/direct.cu) restated in numpy: T = V
+    diag(lam) V^-1 of the 1-D stencil matrix (eigh for order 2, eig + inv for
+    order 4), u = (V x..x V) diag(1/(1 - sigma nu sum lam)) (W x..x W) b.
+    Equal to the reference's SuperLU solve (multigrid.py:203-208) to
+    rounding, not bitwise."""
+    npts = op.n - 1
+    t = operator_matrix(Op(1, op.n, 1.0, op.order, op.length)).toarray()
+    if op.order == 2:
+        lam, v = np.linalg.eigh(t)
+        w = v.T
+    else:
+        lam, v = np.linalg.eig(t)
+        lam, v = lam.real, v.real
+        w = np.linalg.inv(v)
+    x = b.copy()
+    for ax in range(op.dim):
+        x = np.moveaxis(np.tensordot(w, np.moveaxis(x, ax, 0), axes=1), 0, ax)
+    s = np.zeros(op.shape)
+    for ax in range(op.dim):
+        shp = [1] * op.dim
+        shp[ax] = npts
+        s = s + lam.reshape(shp)
+    x = x / (1.0 - sigma * (op.nu * s))
+    for ax in range(op.dim):
+        x = np.moveaxis(np.tensordot(v, np.moveaxis(x, ax, 0), axes=1), 0, ax)
+    return x
+
+
 # ---------------------------------------------------------------------------
 # grid transfers  (transfers.py:19-97)
 

@@ -65,6 +65,8 @@ _SIGS = {
     "pl_mg_vcycles": (i32, [vp, vp, vp, f64, i32, i32, vp]),
     "pl_mg_solve_tol": (i32, [vp, vp, vp, f64, f64, f64, i32, ip, ip, dp, vp]),
     "pl_sweep_workspace_bytes": (sz, [i32, i32, i32]),
+    "pl_mg_set_direct": (i32, [vp, dp, dp, dp, dp, dp, vp]),
+    "pl_mg_direct": (i32, [vp, vp, vp, f64, vp]),
     "pl_sdc_sweep": (i32, [vp, C.POINTER(SweepDesc), vp, vp, vp, vp, f64, vp, sz, ip, ip, dp,
                            ip, vp]),
     "pl_sdc_residual": (i32, [vp, vp, vp, vp, dp, i32, f64, i64, vp, vp]),

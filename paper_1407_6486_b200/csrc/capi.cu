@@ -83,7 +83,7 @@ void timing_post(int kind, cudaStream_t s, double alg_bytes) {
 static const char* kKindNames[K_NUM_KINDS] = {
     "apply", "jacobi", "jor_rb", "residual", "restrict", "prolong", "mg_tail", "norm",
     "quadrature", "rhs", "residual_max", "fas", "correction_time", "interp_cubic", "copy",
-    "lu", "mg_mid"};
+    "lu", "mg_mid", "gauss_seidel", "direct"};
 
 // ---------------------------------------------------------------------------
 // SDC sweep (sdc.py:84-114)
@@ -139,6 +139,8 @@ static int sdc_sweep(MgPlan* P, const pl_sweep_desc* d, double* Y, double* F, co
     if (d->policy == 0) {
       PL_TRY(mg_cycles(P, ym1, R, dtm[m], d->fixed_cycles, 0, s));
       total += d->fixed_cycles;
+    } else if (d->policy == 2) {      // Direct: 0 cycles (multigrid.py:263-264)
+      PL_TRY(mg_direct(P, ym1, R, dtm[m], s));
     } else {
       int c = 0, st = 0;
       double res = 0;
@@ -410,6 +412,15 @@ int pl_mg_set_coarsest_lu(pl_mg_plan* plan, double sigma, const double* lu, cons
 }
 
 int pl_mg_coarsest_size(pl_mg_plan* plan) { return ((MgPlan*)plan)->m_lu; }
+
+int pl_mg_set_direct(pl_mg_plan* plan, const double* w, const double* wt, const double* v,
+                     const double* vt, const double* lam, void* stream) {
+  return mg_set_direct((MgPlan*)plan, w, wt, v, vt, lam, (cudaStream_t)stream);
+}
+
+int pl_mg_direct(pl_mg_plan* plan, double* u, const double* b, double sigma, void* stream) {
+  return mg_direct((MgPlan*)plan, u, b, sigma, (cudaStream_t)stream);
+}
 
 int pl_mg_smooth(pl_mg_plan* plan, double* u, const double* b, double sigma, int count,
                  void* stream) {

@@ -24,6 +24,12 @@ int launch_sumsq(const double* u, const double* b, const Geo& g, const OpC& c, d
                  double* partials, int npartials, double* out, cudaStream_t s);
 int sumsq_partials(const Geo& g);
 
+// ---- gs.cu -----------------------------------------------------------------
+// `count` lexicographic Gauss-Seidel sweeps in place on u (multigrid.py:219-224);
+// t is scratch of the field's size
+int launch_gs(double* u, const double* b, double* t, const Geo& g, const OpC& c, double sigma,
+              int count, cudaStream_t s);
+
 // ---- zmarch.cu: cp.async-pipelined 3-D order-2 versions (zmarch_ok) -------
 bool zmarch_ok(const Geo& g, const OpC& c);
 bool zmarch_enabled();

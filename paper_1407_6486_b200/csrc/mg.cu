@@ -17,6 +17,7 @@
 #include "kernels.cuh"
 #include "mg.h"
 #include "transfer_dev.cuh"
+#include "gs.cuh"
 
 #include <cooperative_groups.h>
 namespace cg = cooperative_groups;
@@ -117,6 +118,45 @@ __device__ void tail_smooth(const TailArgs& a, const TailLevel& L, double* sm, i
     if (count & 1) {
       PL_FOR_SM_POINTS(L.g) u[p] = t[p];
       __syncthreads();
+    }
+    return;
+  }
+  if (a.smoother == SM_GS) {
+    // lexicographic Gauss-Seidel (gs.cuh): residual into t, then the
+    // hyperplanes x + y + z = s in order (1-D: one thread), y over r in t
+    if (zero) {
+      PL_FOR_SM_POINTS(L.g) u[p] = 0.0;
+      __syncthreads();
+    }
+    const int smax = (L.g.nx - 1) + (DIM >= 2 ? L.g.ny - 1 : 0) + (DIM == 3 ? L.g.nz - 1 : 0);
+    for (int k = 0; k < count; ++k) {
+      PL_FOR_SM_POINTS(L.g) {
+        int x, y, z;
+        decode(L.g, p, x, y, z);
+        t[p] = b[p] - shifted_point<DIM>(u, L.g, L.c, a.sigma, x, y, z, p);
+      }
+      __syncthreads();
+      if (DIM == 1) {
+        if (threadIdx.x == 0)
+          for (int x = 0; x < L.g.nx; ++x) {
+            const double yi = gs_lower_point<DIM>(t, t[x], L.g, L.c, a.sigma, x, 0, 0, x);
+            t[x] = yi;
+            u[x] = u[x] + yi / shifted_diag<DIM>(L.g, L.c, a.sigma, x, 0, 0);
+          }
+        __syncthreads();
+        continue;
+      }
+      for (int s = 0; s <= smax; ++s) {
+        PL_FOR_SM_POINTS(L.g) {
+          int x, y, z;
+          decode(L.g, p, x, y, z);
+          if (x + y + z != s) continue;
+          const double yi = gs_lower_point<DIM>(t, t[p], L.g, L.c, a.sigma, x, y, z, p);
+          t[p] = yi;
+          u[p] = u[p] + yi / shifted_diag<DIM>(L.g, L.c, a.sigma, x, y, z);
+        }
+        __syncthreads();
+      }
     }
     return;
   }
@@ -769,7 +809,7 @@ int mg_plan_create(MgPlan** out, int dim, int n, double length, double nu, int o
     set_error("stencil order must be 2 or 4");
     return -1;
   }
-  if (smoother != SM_JACOBI && smoother != SM_RB) {
+  if (smoother != SM_JACOBI && smoother != SM_RB && smoother != SM_GS) {
     set_error("smoother %d is not implemented on the GPU path", smoother);
     return -2;
   }
@@ -850,6 +890,7 @@ void mg_plan_destroy(MgPlan* P) {
   }
   cudaFree(P->partials);
   cudaFreeHost(P->norm_host);
+  mg_direct_destroy(P);
   delete P;
 }
 
@@ -994,6 +1035,16 @@ static int level_smooth(MgPlan* P, MgLevel& L, double** cur, double* alt_u, cons
     return 0;
   }
   const bool fused = zmarch_ok(L.g, L.c);
+  if (P->smoother == SM_GS) {   // in place; t is the solve's scratch
+    if (zero) {
+      cudaError_t e = cudaMemsetAsync(u, 0, sizeof(double) * L.g.nstore, s);
+      if (e != cudaSuccess) return cuda_status(e, "memset");
+    }
+    double* scratch = (u == L.t) ? alt_u : L.t;
+    PL_TRY(launch_gs(u, b, scratch, L.g, L.c, sigma, count, s));
+    *cur = u;
+    return 0;
+  }
   if (P->smoother == SM_JACOBI) {
     int k = 0;
     if (fused) {             // pairs of sweeps in one pass (temporal blocking)

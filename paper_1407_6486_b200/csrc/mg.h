@@ -42,6 +42,12 @@ struct MgPlan {
   double* norm_host = nullptr;   // pinned, 2 doubles
   char* ws = nullptr;
   size_t ws_bytes = 0;
+  // Direct policy (direct.cu): W, W^T, V, V^T, lam on the device, two scratch
+  // fields, a cuBLAS handle
+  double* dir_mats = nullptr;
+  double* dir_work = nullptr;
+  void* cublas = nullptr;
+  int dir_ready = 0;
 };
 
 size_t mg_workspace_bytes(int dim, int n, int coarsest_n);
@@ -65,5 +71,14 @@ int mg_cycles(MgPlan* p, double* u, const double* b, double sigma, int ncycles,
 // when the cycle cap is hit (residual/cycles describe the failure).
 int mg_solve_tol(MgPlan* p, double* u, const double* b, double sigma, double tol, double stall,
                  int max_cycles, int* cycles, int* status, double* residual, cudaStream_t s);
+
+// Direct policy by fast diagonalisation (direct.cu): install the eigen-
+// decomposition T = V diag(lam) V^-1 of the level-0 1-D stencil matrix
+// (row-major N x N W = V^-1, W^T, V, V^T and lam, host arrays), then
+// u = (I - sigma nu Lap)^-1 b
+int mg_set_direct(MgPlan* P, const double* w, const double* wt, const double* v,
+                  const double* vt, const double* lam, cudaStream_t s);
+int mg_direct(MgPlan* P, double* u, const double* b, double sigma, cudaStream_t s);
+void mg_direct_destroy(MgPlan* P);
 
 }  // namespace pl

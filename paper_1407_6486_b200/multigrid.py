@@ -68,8 +68,10 @@ class ToTolerance:
 
 @dataclass(frozen=True)
 class Direct:
-    """Exact sparse solve (multigrid.py:63-65).  Not on the GPU path: no
-    BASELINE configuration uses it."""
+    """Exact solve (multigrid.py:63-65).  The reference factors the sparse
+    shifted matrix with SuperLU; the GPU path diagonalises the Kronecker sum
+    (pl_mg_direct: dense cuBLAS GEMMs along each axis and a point-wise scale),
+    equal to rounding."""
 
 
 SolvePolicy = Union[FixedCycles, ToTolerance, Direct]
@@ -120,6 +122,33 @@ class _Plan:
             self.handle.value, sigma, lu.ctypes.data_as(C.POINTER(C.c_double)),
             piv.ctypes.data_as(C.POINTER(C.c_int)), stream_ptr()), "coarsest LU")
         self._factored.add(sigma)
+
+    def ensure_direct(self):
+        """Install the eigen-decomposition T = V diag(lam) V^-1 of the 1-D
+        stencil matrix (the reference's entries, multigrid.py:86-107) for the
+        Direct policy: numpy eigh for the symmetric order-2 matrix, eig + inv
+        for order 4 (boundary rows make it non-symmetric).  Host setup, like
+        the coarsest LU; the solves run on the GPU."""
+        if getattr(self, "_direct", False):
+            return
+        g = self.op.grid
+        t = _laplacian_1d(g.n, g.length, self.op.order)
+        if self.op.order == 2:
+            lam, v = np.linalg.eigh(t)
+            w = v.T.copy()
+        else:
+            lam, v = np.linalg.eig(t)
+            if np.max(np.abs(lam.imag)) > 1e-9 * np.max(np.abs(lam.real)):
+                raise RuntimeError("order-4 stencil matrix has complex eigenvalues")
+            lam, v = lam.real.copy(), v.real.copy()
+            w = np.linalg.inv(v)
+        arrs = [np.ascontiguousarray(a, dtype=np.float64)
+                for a in (w, w.T, v, v.T, lam)]
+        dp = C.POINTER(C.c_double)
+        capi.check(capi.lib().pl_mg_set_direct(self.handle.value,
+                                               *[a.ctypes.data_as(dp) for a in arrs],
+                                               stream_ptr()), "direct factors")
+        self._direct = True
 
     def __del__(self):
         try:
@@ -210,13 +239,28 @@ class ShiftedOperator:
         return like_input(out, as_numpy)
 
     def solve_direct(self, b):
-        raise NotImplementedError("Direct solves are not on the GPU path")
+        """multigrid.py:203-208: (I - sigma A)^-1 b."""
+        g = self.base.grid
+        tb, host = to_device(b, g.dim)
+        out = new_field(g.shape)
+        direct_into(self, out, tb, MgConfig())
+        return like_input(out, host)
+
+
+def direct_into(op: "ShiftedOperator", u, b, cfg: MgConfig):
+    """u = (I - sigma A)^-1 b on the device (Direct policy)."""
+    require_field(u, op.grid.dim, "direct(u)")
+    require_field(b, op.grid.dim, "direct(b)")
+    p = plan_for(op.base, cfg)
+    p.ensure_direct()
+    capi.check(capi.lib().pl_mg_direct(p.handle.value, ptr(u), ptr(b), float(op.sigma),
+                                       stream_ptr()), "direct solve")
+    return u
 
 
 def _check_policy(policy):
-    if isinstance(policy, Direct):
-        raise NotImplementedError("Direct (sparse LU) is not on the B200 path; use "
-                                  "FixedCycles or ToTolerance")
+    if not isinstance(policy, (FixedCycles, ToTolerance, Direct)):
+        raise ValueError(f"unknown solve policy {policy!r}")
 
 
 def smooth(op: ShiftedOperator, u, b, cfg: MgConfig, count: int):
@@ -269,6 +313,9 @@ def solve_into(op: ShiftedOperator, u, b, cfg: MgConfig, policy) -> tuple:
     _check_policy(policy)
     require_field(u, op.grid.dim, "solve_into(u)")
     require_field(b, op.grid.dim, "solve_into(b)")
+    if isinstance(policy, Direct):            # multigrid.py:263-264
+        direct_into(op, u, b, cfg)
+        return 0, "direct"
     if isinstance(policy, FixedCycles):
         vcycles_into(op, u, b, cfg, policy.cycles)
         return policy.cycles, "fixed"

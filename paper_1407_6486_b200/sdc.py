@@ -89,6 +89,8 @@ def sweep_desc(table: QuadratureTable, policy) -> capi.SweepDesc:
         desc.gammas[i] = float(g)
     if isinstance(policy, FixedCycles):
         desc.policy, desc.fixed_cycles = 0, policy.cycles
+    elif isinstance(policy, Direct):
+        desc.policy = 2
     else:
         desc.policy = 1
         desc.tol, desc.stall, desc.max_cycles = policy.tol, policy.stall, policy.max_cycles
@@ -106,6 +108,8 @@ def sdc_sweep(states: NodeStates, y0, dt: float, op: HeatOperator, mg_cfg: MgCon
     ttau = to_device(tau, d)[0] if tau is not None else None
     desc = sweep_desc(states.table, policy)
     plan = plan_for(op, mg_cfg)
+    if isinstance(policy, Direct):
+        plan.ensure_direct()
     for gam in states.table.nodes.gammas:
         plan.ensure(float(gam) * dt)            # sdc.py:101 sigma of each sub-step
     g = op.grid

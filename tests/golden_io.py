@@ -11,8 +11,15 @@ GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
 
 @lru_cache(maxsize=None)
 def manifest():
+    """manifest.json (oracle/make_golden.py) merged with manifest_gsd.json
+    (oracle/make_golden_gs_direct.py: Gauss-Seidel and Direct cases)."""
     with open(os.path.join(GOLDEN, "manifest.json")) as fh:
-        return json.load(fh)
+        man = json.load(fh)
+    extra = os.path.join(GOLDEN, "manifest_gsd.json")
+    if os.path.exists(extra):
+        with open(extra) as fh:
+            man["cases"].update(json.load(fh)["cases"])
+    return man
 
 
 def case(name):

@@ -107,9 +107,13 @@ def test_seeded_field_recipe_matches_oracle():
         assert np.array_equal(product_field(Grid(d, n)), seeded_field(d, n))
 
 
-def test_direct_policy_is_rejected_not_silently_replaced():
-    with pytest.raises(NotImplementedError):
-        mg._check_policy(mg.Direct())
+def test_policies_accepted_and_unknown_rejected():
+    """Direct is on the GPU path now (pl_mg_direct); anything that is not a
+    reference policy is a ValueError, never a silent substitute."""
+    for pol in (mg.Direct(), mg.FixedCycles(1), mg.ToTolerance()):
+        mg._check_policy(pol)
+    with pytest.raises(ValueError):
+        mg._check_policy("direct")
 
 
 def test_comm_entry_points_validate_and_create_ids():

@@ -605,3 +605,63 @@ def test_comm_single_rank_roundtrip():
         assert torch.equal(dst, src) and torch.equal(b, src)
     finally:
         lib.pl_comm_destroy(h)
+
+
+# ------------------------------------- lexicographic Gauss-Seidel and Direct
+@pytest.mark.parametrize("name", names("gsd_k_"))
+def test_gauss_seidel_direct_kernels(name):
+    """GS sweeps and GS V-cycles are bit-identical to the reference's
+    scipy solve_banded (csrc/gs.cuh restates dgbtrf/dgbtrs's operation
+    order); Direct (fast diagonalisation on the GPU) agrees with SuperLU to
+    1e-12; ToTolerance with GS takes the reference's cycle count."""
+    a, m = case(name)
+    op = heat.HeatOperator(heat.Grid(m["dim"], m["n"], m["length"]), m["nu"], m["order"])
+    sop = mg.ShiftedOperator(op, m["sigma"])
+    cfg = mg.MgConfig("gauss-seidel")
+    u, b = dev(a["u"]), dev(a["b"])
+    bitwise(mg.smooth(sop, u, b, cfg, 1), a["gs1"])
+    bitwise(mg.smooth(sop, u, b, cfg, 2), a["gs2"])
+    close(mg.v_cycle(sop, u, b, cfg), a["vc22"], 1e-12)
+    close(mg.v_cycle(sop, torch.zeros_like(b), b, mg.MgConfig("gauss-seidel", 2 / 3, 1, 1)),
+          a["vc11z"], 1e-12)
+    res = mg.solve(sop, u, b, cfg, mg.Direct())
+    assert (res.cycles, res.status) == (0, "direct")
+    close(res.u, a["direct"], 1e-12)
+    close(sop.solve_direct(a["b"]), a["direct"], 1e-12)
+    res = mg.solve(sop, u, b, cfg, mg.ToTolerance(1e-10))
+    assert (res.cycles, res.status) == (m["tol_cycles"], m["tol_status"])
+    close(res.u, a["tol_u"])
+
+
+def test_gs_direct_serial_drivers():
+    a, m = case("gsd_sdc")
+    r = sdc.run_sdc(heat.HeatOperator(heat.Grid(1, 64)), quadrature.uniform_table(4),
+                    dev(a["u0"]), 0.25, 4, 1e-10, 20, mg.MgConfig("gauss-seidel"),
+                    mg.ToTolerance(1e-12))
+    assert r.iterations == m["gs"]["iterations"]
+    assert r.vcycles == m["gs"]["vcycles"]
+    for got, ref in zip(r.residuals, m["gs"]["residuals"]):
+        np.testing.assert_allclose(got, ref, rtol=1e-6, atol=1e-14)
+    close(r.u, a["gs_u"])
+    r = sdc.run_sdc(heat.HeatOperator(heat.Grid(2, 16), 1.0, 4), quadrature.uniform_table(4),
+                    dev(a["u02"]), 0.125, 2, 1e-11, 30, mg.MgConfig("gauss-seidel"),
+                    mg.Direct())
+    assert r.iterations == m["direct"]["iterations"]
+    assert r.vcycles == 0
+    close(r.u, a["direct_u"])
+
+
+@pytest.mark.parametrize("name", ["gsd_run_gs2d", "gsd_run_direct1d"])
+def test_pfasst_gauss_seidel_and_direct(name):
+    a, m = case(name)
+    pol = mg.Direct() if m["policy"] == "direct" else mg.FixedCycles(1)
+    levels = [hierarchy.Level(heat.HeatOperator(heat.Grid(m["d"], n)),
+                              quadrature.uniform_table(k - 1), mg.MgConfig("gauss-seidel"),
+                              pol, space_interp_order=4)
+              for n, k in zip(m["ns"], m["nodes"])]
+    res = pfasst.pfasst_run(levels, dev(a["u0"]), m["dt"] * m["p"], m["p"], tol=m["tol"],
+                            max_iter=20)
+    assert res.rank_iterations == m["rank_iterations"]
+    assert res.rank_vcycles == m["rank_vcycles"]
+    assert res.converged == m["converged"]
+    close(res.u, a["u"])

@@ -194,3 +194,68 @@ def test_serial_drivers():
 def test_seeded_field_matches_fixture():
     a, _ = case("run_cfg2_small")
     eq(O.seeded_field(2, 64), a["u0"])
+
+
+# ---- lexicographic Gauss-Seidel and the Direct policy (make_golden_gs_direct.py)
+@pytest.mark.parametrize("name", names("gsd_k_"))
+def test_gs_direct_kernels(name):
+    a, m = case(name)
+    op = O.Op(m["dim"], m["n"], m["nu"], m["order"], m["length"])
+    s = m["sigma"]
+    cfg = O.Mg("gauss-seidel")
+    eq(O.smooth(op, s, a["u"], a["b"], cfg, 1), a["gs1"])
+    eq(O.smooth(op, s, a["u"], a["b"], cfg, 2), a["gs2"])
+    eq(O.v_cycle(op, s, a["u"], a["b"], cfg), a["vc22"])
+    eq(O.v_cycle(op, s, np.zeros_like(a["b"]), a["b"], O.Mg("gauss-seidel", 2 / 3, 1, 1)),
+       a["vc11z"])
+    u, c, st = O.mg_solve(op, s, a["u"], a["b"], cfg, O.DirectSolve())
+    eq(u, a["direct"])
+    assert (c, st) == (0, "direct")
+    u, c, st = O.mg_solve(op, s, a["u"], a["b"], cfg, O.ToTol(1e-10))
+    eq(u, a["tol_u"])
+    assert (c, st) == (m["tol_cycles"], m["tol_status"])
+
+
+@pytest.mark.parametrize("dim,n,order", [(1, 16, 2), (1, 16, 4), (2, 8, 2), (2, 8, 4),
+                                         (3, 8, 2), (3, 8, 4)])
+def test_gs_gbtrs_order_is_solve_banded(dim, n, order):
+    """The GPU's Gauss-Seidel statement (fma chain over the lower neighbours
+    in linear-index order, multipliers A_ij * RN(1/D_j), division by D) is
+    bit-identical to the reference's scipy.linalg.solve_banded."""
+    op = O.Op(dim, n, 0.9, order, 1.3)
+    rng = np.random.default_rng(dim * 10 + order)
+    u = rng.standard_normal(op.shape)
+    b = rng.standard_normal(op.shape)
+    s = 0.017
+    ref = O.smooth(op, s, u, b, O.Mg("gauss-seidel"), 1)
+    r = b - O.shifted_apply(op, s, u)
+    eq(u + O.gs_lower_solve_gbtrs(op, s, r), ref)
+
+
+@pytest.mark.parametrize("dim,n,order", [(1, 64, 2), (1, 64, 4), (2, 32, 2), (2, 32, 4),
+                                         (3, 16, 2), (3, 16, 4)])
+def test_direct_fast_diagonalisation_matches_superlu(dim, n, order):
+    """The GPU Direct algorithm (eigen-decomposition of the 1-D stencil, dense
+    transforms per axis) agrees with the reference's SuperLU solve."""
+    op = O.Op(dim, n, 1.0, order)
+    b = np.random.default_rng(n + order).standard_normal(op.shape)
+    s = 0.01
+    ref, _, _ = O.mg_solve(op, s, np.zeros_like(b), b, O.Mg(), O.DirectSolve())
+    got = O.direct_fast_diag(op, s, b)
+    assert np.max(np.abs(got - ref)) <= 1e-12 * np.max(np.abs(ref))
+
+
+def test_gs_direct_drivers():
+    a, m = case("gsd_sdc")
+    op = O.Op(1, 64)
+    g = O.run_sdc(op, O.uniform_table(4), a["u0"], 0.25, 4, 1e-10, 20, O.Mg("gauss-seidel"),
+                  O.ToTol(1e-12))
+    assert g["iterations"] == m["gs"]["iterations"]
+    assert g["residuals"] == m["gs"]["residuals"]
+    assert g["vcycles"] == m["gs"]["vcycles"]
+    eq(g["u"], a["gs_u"])
+    d = O.run_sdc(O.Op(2, 16, 1.0, 4), O.uniform_table(4), a["u02"], 0.125, 2, 1e-11, 30,
+                  O.Mg("gauss-seidel"), O.DirectSolve())
+    assert d["iterations"] == m["direct"]["iterations"]
+    assert d["vcycles"] == m["direct"]["vcycles"] == 0
+    eq(d["u"], a["direct_u"])
