@@ -86,6 +86,12 @@ const char* pl_last_error(void);
                                  phase per former kernel plus the one-CTA tail */
 #define PL_OPT_MID_CTAS 13    /* CTAs of the cooperative small-level kernels (default 32; 0: one
                                  per SM); fewer leave SMs to other time ranks' streams */
+#define PL_OPT_ZRB_RING 14    /* one-barrier jor-rb sweep rings: 0 (default) 8 u + 4 b planes,
+                                 3 CTAs/SM; 1: 6 u + 3 b planes, 4 CTAs/SM; bit-identical */
+#define PL_OPT_RBRFW 15       /* 1: the last jor-rb pre-sweep, the residual and full weighting
+                                 run as one overlapped-tile pass (TMA levels); 0 (default,
+                                 measured faster): k_zrb3 then k_rfw; bit-identical */
+#define PL_OPT_RBRFW_ZCC 16   /* smallest coarse-plane z chunk of the fused pass (default 16) */
 int pl_set_option(int key, int value);
 
 /* storage elements of one field (incl. row pads) */

@@ -147,6 +147,9 @@ OPT_FAST_TAIL = 10
 OPT_ZC_CTAS = 11
 OPT_MID2 = 12
 OPT_MID_CTAS = 13
+OPT_ZRB_RING = 14
+OPT_RBRFW = 15
+OPT_RBRFW_ZCC = 16
 
 
 def set_option(key, value):

@@ -83,7 +83,7 @@ void timing_post(int kind, cudaStream_t s, double alg_bytes) {
 static const char* kKindNames[K_NUM_KINDS] = {
     "apply", "jacobi", "jor_rb", "residual", "restrict", "prolong", "mg_tail", "norm",
     "quadrature", "rhs", "residual_max", "fas", "correction_time", "interp_cubic", "copy",
-    "lu", "mg_mid", "gauss_seidel", "direct"};
+    "lu", "mg_mid", "gauss_seidel", "direct", "jor_rb_restrict"};
 
 // ---------------------------------------------------------------------------
 // SDC sweep (sdc.py:84-114)
@@ -231,6 +231,9 @@ extern int g_zc_ctas;
 extern int g_fast_tail;
 extern int g_mid2_enabled;
 extern int g_mid_ctas;
+extern int g_zrb_ring;
+extern int g_rbrfw_enabled;
+extern int g_rbrfw_zcc;
 }
 
 extern "C" {
@@ -288,6 +291,22 @@ int pl_set_option(int key, int value) {
       return PL_ERR_ARG;
     }
     g_mid_ctas = value;
+    return 0;
+  }
+  if (key == PL_OPT_RBRFW_ZCC) {
+    if (value < 1) {
+      set_error("z chunk must be positive");
+      return PL_ERR_ARG;
+    }
+    g_rbrfw_zcc = value;
+    return 0;
+  }
+  if (key == PL_OPT_RBRFW) {
+    g_rbrfw_enabled = value != 0;
+    return 0;
+  }
+  if (key == PL_OPT_ZRB_RING) {
+    g_zrb_ring = value != 0;
     return 0;
   }
   if (key == PL_OPT_MID2) {

@@ -52,6 +52,11 @@ bool zmarch_rfw();   // PL_OPT_RFW
 int zlaunch_rfw(const double* u, const double* b, double* coarse, const Geo& g, const OpC& c,
                 double sigma, cudaStream_t s);
 
+// last jor-rb pre-sweep u -> out (out != u) fused with coarse = FW(b - A out)
+extern int g_rbrfw_enabled;   // PL_OPT_RBRFW
+int zlaunch_rbrfw(const double* u, const double* b, double* out, double* coarse, const Geo& g,
+                  const OpC& c, double sigma, double omega, cudaStream_t s);
+
 // fine (+)= P_cubic coarse, 3-D, TMA-staged coarse planes (taps of cubic_taps)
 int zlaunch_cubic(const double* coarse, double* fine, const Geo& gf, const int* cnt,
                   const int* idx, const double* w, int accumulate, cudaStream_t s);

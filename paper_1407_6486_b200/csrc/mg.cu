@@ -1089,13 +1089,22 @@ static int vcycle(MgPlan* P, int l, double* u, const double* b, double sigma, bo
   MgLevel& L = P->lv[l];
   MgLevel& C = P->lv[l + 1];
   double* cur = u;
-  PL_TRY(level_smooth(P, L, &cur, u, b, sigma, P->pre, zero, s));
-  if (zmarch_ok(L.g, L.c) && zmarch_rfw()) {
-    PL_TRY(zlaunch_rfw(cur, b, C.b, L.g, L.c, sigma, s));
+  const bool zm = zmarch_ok(L.g, L.c);
+  if (zm && zmarch_rfw() && g_rbrfw_enabled && P->smoother == SM_RB && P->pre >= 1) {
+    // last pre-sweep + residual + full weighting in one pass (k_rbrfw)
+    PL_TRY(level_smooth(P, L, &cur, u, b, sigma, P->pre - 1, zero, s));
+    double* other = (cur == u) ? L.t : u;
+    PL_TRY(zlaunch_rbrfw(cur, b, other, C.b, L.g, L.c, sigma, P->omega, s));
+    cur = other;
   } else {
-    double* r = (cur == u) ? L.t : u;
-    PL_TRY(launch_residual(cur, b, r, L.g, L.c, sigma, s));
-    PL_TRY(launch_fw(r, C.b, L.g, s));
+    PL_TRY(level_smooth(P, L, &cur, u, b, sigma, P->pre, zero, s));
+    if (zm && zmarch_rfw()) {
+      PL_TRY(zlaunch_rfw(cur, b, C.b, L.g, L.c, sigma, s));
+    } else {
+      double* r = (cur == u) ? L.t : u;
+      PL_TRY(launch_residual(cur, b, r, L.g, L.c, sigma, s));
+      PL_TRY(launch_fw(r, C.b, L.g, s));
+    }
   }
   PL_TRY(vcycle(P, l + 1, C.u, C.b, sigma, true, s));
   // u += P e_c, then post-smoothing; fused into the first post-sweep pass

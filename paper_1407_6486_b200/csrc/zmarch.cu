@@ -26,6 +26,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <algorithm>
 #include <cstring>
 #include <mutex>
 #include <type_traits>
@@ -35,6 +36,9 @@
 #include "transfer_dev.cuh"
 
 namespace pl {
+
+extern int g_zrb_ring;   // PL_OPT_ZRB_RING: 0 8+4 plane rings (3 CTAs/SM), 1 6+3 (4 CTAs/SM)
+extern int g_rbrfw_zcc;  // PL_OPT_RBRFW_ZCC: smallest coarse z chunk of k_rbrfw
 
 namespace {
 
@@ -641,11 +645,11 @@ struct RbCtx {
 
 template <int RU>
 __device__ __forceinline__ double* rb_u(const RbCtx& k, int p) {
-  return k.su + ((p - k.z0 + 2) & (RU - 1)) * PU;
+  return k.su + ((unsigned)(p - k.z0 + 2) % RU) * PU;
 }
 template <int RB>
 __device__ __forceinline__ double* rb_b(const RbCtx& k, int q) {
-  return k.sb + ((q - k.z0 + 1) & (RB - 1)) * PB;
+  return k.sb + ((unsigned)(q - k.z0 + 1) % RB) * PB;
 }
 template <int O>
 __device__ __forceinline__ double mem(const double2& v) { return O ? v.y : v.x; }
@@ -763,7 +767,7 @@ __global__ void __launch_bounds__(HW ? 320 : NTHR_RB2, MINB) k_zrb3(const __grid
                                                       double* __restrict__ out, Geo g, OpC c,
                                                       double sigma, double omega, double dval,
                                                       double dinv, int zc) {
-  static_assert((RU & (RU - 1)) == 0 && (RB & (RB - 1)) == 0 && RU >= 8 && RB >= 2, "rings");
+  static_assert(RU >= 6 && RB >= 2, "rings");
   extern __shared__ __align__(128) double sm[];
   RbCtx k;
   k.su = sm;
@@ -789,23 +793,23 @@ __global__ void __launch_bounds__(HW ? 320 : NTHR_RB2, MINB) k_zrb3(const __grid
   __syncthreads();
   auto issue_u = [&](int p) {
     if (p > uhi) return;
-    const int s = (p - z0 + 2) & (RU - 1);
+    const int s = (unsigned)(p - z0 + 2) % RU;
     mbar_expect(bu + s, UX * UY * 8u);
     tma3(k.su + s * PU, &mu, x0 - 2, y0 - 2, p, bu + s);
   };
   auto issue_b = [&](int q) {
     if (q > bhi) return;
-    const int s = (q - z0 + 1) & (RB - 1);
+    const int s = (unsigned)(q - z0 + 1) % RB;
     mbar_expect(bbar + s, BW * BH * 8u);
     tma3(k.sb + s * PB, &mb, x0 - 2, y0 - 1, q, bbar + s);
   };
   auto wait_u = [&](int p) {
     const int i = p - z0 + 2;
-    mbar_wait(bu + (i & (RU - 1)), (unsigned)((i / RU) & 1));
+    mbar_wait(bu + (unsigned)i % RU, ((unsigned)i / RU) & 1u);
   };
   auto wait_b = [&](int q) {
     const int i = q - z0 + 1;
-    mbar_wait(bbar + (i & (RB - 1)), (unsigned)((i / RB) & 1));
+    mbar_wait(bbar + (unsigned)i % RB, ((unsigned)i / RB) & 1u);
   };
   if (tid == 0) {
     for (int p = z0 - 2; p < z0 - 2 + RU; ++p) issue_u(p);
@@ -1228,6 +1232,275 @@ __global__ void __launch_bounds__(NTHR, 4) k_rfw(const __grid_constant__ CUtenso
   }
 }
 
+// ---------------------------------------------------------------------------
+// k_rbrfw: the last pre-smoothing jor-rb sweep, the residual and full
+// weighting in ONE pass over u and b (multigrid.py:225-233, 245-246;
+// transfers.py:27-34).  k_zrb3 + k_rfw read u and b twice and write u once;
+// this kernel reads them once, writes the smoothed u and the coarse
+// right-hand side.  A CTA owns k_rfw's tile (16 x 8 coarse points, fine x0 ..
+// x0+31, y0 .. y0+15) and recomputes the halo it needs (overlapped tiling):
+//   R  = [x0, x0+32] x [y0, y0+16]        residuals (the FW footprint)
+//   F  = R + 1                            final u (black points updated)
+//   Rd = R + 2                            red points updated
+//   u window = [x0-4, x0+35] x [y0-3, y0+19] (old u, TMA, zero-filled ghosts)
+//   b window = [x0-2, x0+35] x [y0-2, y0+18]
+// Phase r (one barrier): red points of plane r (they read only old blacks),
+// black points of plane r-2 (reds of r-3 .. r-1 final), the residual of plane
+// r-4 (u final up to plane r-3) folded into k_rfw's z weights, the owned
+// points of plane r-3 to `out`, and k_rfw's y / x passes.  Residual points
+// carry their z-neighbour centres and b values in registers, so only planes
+// r-4 .. r+1 of u and r-2 .. r of b stay in shared memory.  Every update is
+// the reference's expression tree (rb_relax, the residual of k_z1, fw3), so
+// the smoothed u and the coarse right-hand side are bit-identical to k_zrb3 +
+// k_rfw.
+constexpr int QUX = TX + 8, QUY = TY + 7, PQU = align16(QUX * QUY);   // u window
+constexpr int QBX = TX + 6, QBY = TY + 5, PQB = align16(QBX * QBY);   // b window
+constexpr int RBF_RU = 8, RBF_RB = 5, RBF_NT = 384;
+constexpr int RBF_PERR = (RX * RY + RBF_NT - 1) / RBF_NT;             // residual points per thread
+
+template <bool POW2>
+__device__ __forceinline__ double rbf_relax(const double* sl, const double* slm,
+                                            const double* slp, int i, double bv, const OpC& c,
+                                            double sigma, double omega, double dval,
+                                            double dinv) {
+  const double cc = sl[i];
+  double acc = 0.0;
+  acc = acc + dd2<POW2>((slm[i] - 2.0 * cc) + slp[i], c);
+  acc = acc + dd2<POW2>((sl[i - QUX] - 2.0 * cc) + sl[i + QUX], c);
+  acc = acc + dd2<POW2>((sl[i - 1] - 2.0 * cc) + sl[i + 1], c);
+  const double lp = c.nu * acc;
+  const double r = bv - (cc - sigma * lp);
+  return cc + div_const(omega * r, dval, dinv);
+}
+
+// colour points of a box [xl, xh] x [yl, yh], statically dealt to threads:
+// slot s -> row s / w, k-th point of the colour; the x of the point depends on
+// the plane parity, so each slot keeps both window offsets and both validity
+// flags (domain clipping included) and a phase only selects by parity
+constexpr int RBF_RS = (21 * 19 + RBF_NT - 1) / RBF_NT;   // red slots per thread (Rd)
+constexpr int RBF_BS = (19 * 18 + RBF_NT - 1) / RBF_NT;   // black slots per thread (F)
+template <int NS>
+struct ColourSlots {
+  int iu0[NS], iu1[NS], ib0[NS], ib1[NS];   // window offsets for plane parity 0 / 1
+  bool ok0[NS], ok1[NS];
+  __device__ __forceinline__ void init(int xl, int xh, int yl, int yh, int red, int x0, int y0,
+                                       const Geo& g) {
+    const int w = (xh - xl) / 2 + 1, rows = yh - yl + 1;
+#pragma unroll
+    for (int j = 0; j < NS; ++j) {
+      const int sl = threadIdx.x + j * RBF_NT;
+      const int iy = sl / w, k = sl - iy * w;
+      const int y = yl + iy;
+#pragma unroll
+      for (int par = 0; par < 2; ++par) {   // par = plane & 1
+        // red: 1-based coordinate sum even <=> x + y + q odd (multigrid.py:167-175)
+        const int want = red ? ((y + par + 1) & 1) : ((y + par) & 1);
+        const int x = xl + ((want - xl) & 1) + 2 * k;
+        const int iu = (y - (y0 - 3)) * QUX + (x - (x0 - 4));
+        const int ib = (y - (y0 - 2)) * QBX + (x - (x0 - 2));
+        const bool ok = sl < rows * w && x <= xh && x >= 0 && x < g.nx && y >= 0 && y < g.ny;
+        if (par) { iu1[j] = iu; ib1[j] = ib; ok1[j] = ok; }
+        else { iu0[j] = iu; ib0[j] = ib; ok0[j] = ok; }
+      }
+    }
+  }
+  template <bool POW2>
+  __device__ __forceinline__ void run(double* sl, const double* slm, const double* slp,
+                                      const double* sbq, int par, const OpC& c, double sigma,
+                                      double omega, double dval, double dinv) const {
+#pragma unroll
+    for (int j = 0; j < NS; ++j) {
+      if (!(par ? ok1[j] : ok0[j])) continue;
+      const int i = par ? iu1[j] : iu0[j];
+      const int ib = par ? ib1[j] : ib0[j];
+      sl[i] = rbf_relax<POW2>(sl, slm, slp, i, sbq[ib], c, sigma, omega, dval, dinv);
+    }
+  }
+};
+
+template <bool POW2>
+__global__ void __launch_bounds__(RBF_NT, 2) k_rbrfw(const __grid_constant__ CUtensorMap mu,
+                                                    const __grid_constant__ CUtensorMap mb,
+                                                    double* __restrict__ out,
+                                                    double* __restrict__ coarse, Geo gf, Geo gc,
+                                                    OpC c, double sigma, double omega,
+                                                    double dval, double dinv, int zcc) {
+  extern __shared__ __align__(128) double sm[];
+  double* su = sm;                             // RBF_RU u windows
+  double* sb = su + RBF_RU * PQU;              // RBF_RB b windows
+  double* szb = sb + RBF_RB * PQB;             // z-weighted plane (RX x RY)
+  double* syx = szb + PR;                      // y-weighted rows (RX x TY/2)
+  unsigned long long* bu = (unsigned long long*)(syx + PR);
+  unsigned long long* bb = bu + RBF_RU;
+  const int tid = threadIdx.x;
+  const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TY;
+  const int jz0 = blockIdx.z * zcc, jz1 = min(jz0 + zcc, gc.nz);
+  const int p0 = 2 * jz0, p1 = 2 * jz1;        // residual planes p0 .. p1
+  const int ulo = p0 - 3, uhi = p1 + 3, blo = p0 - 2, bhi = p1 + 2;
+  // owned output planes: [p0, p1), the last chunk also p1
+  const int qhi = jz1 == gc.nz ? p1 : p1 - 1;
+  if (tid == 0) {
+    for (int i = 0; i < RBF_RU; ++i) mbar_init(bu + i, 1);
+    for (int i = 0; i < RBF_RB; ++i) mbar_init(bb + i, 1);
+    fence_barrier_init();
+  }
+  __syncthreads();
+  auto uslot = [&](int p) { return su + ((unsigned)(p - ulo) % RBF_RU) * PQU; };
+  auto bslot = [&](int p) { return sb + ((unsigned)(p - blo) % RBF_RB) * PQB; };
+  auto issue_u = [&](int p) {
+    if (p > uhi) return;
+    const int s = (unsigned)(p - ulo) % RBF_RU;
+    mbar_expect(bu + s, QUX * QUY * 8u);
+    tma3(su + s * PQU, &mu, x0 - 4, y0 - 3, p, bu + s);
+  };
+  auto issue_b = [&](int p) {
+    if (p > bhi) return;
+    const int s = (unsigned)(p - blo) % RBF_RB;
+    mbar_expect(bb + s, QBX * QBY * 8u);
+    tma3(sb + s * PQB, &mb, x0 - 2, y0 - 2, p, bb + s);
+  };
+  auto wait_u = [&](int p) {
+    const unsigned k = p - ulo;
+    mbar_wait(bu + k % RBF_RU, (k / RBF_RU) & 1u);
+  };
+  auto wait_b = [&](int p) {
+    const unsigned k = p - blo;
+    mbar_wait(bb + k % RBF_RB, (k / RBF_RB) & 1u);
+  };
+  if (tid == 0) {
+    for (int p = ulo; p < ulo + RBF_RU; ++p) issue_u(p);
+    for (int p = blo; p < blo + RBF_RB; ++p) issue_b(p);
+  }
+  // residual points of this thread (k_rfw's window order)
+  int r_iu[RBF_PERR], r_ib[RBF_PERR], r_k[RBF_PERR];
+  bool r_ok[RBF_PERR];
+#pragma unroll
+  for (int q = 0; q < RBF_PERR; ++q) {
+    const int k = tid + q * RBF_NT;
+    const int ry = k / RX, rx = k - ry * RX;
+    r_k[q] = k < RX * RY ? k : -1;
+    r_iu[q] = (ry + 3) * QUX + rx + 4;
+    r_ib[q] = (ry + 2) * QBX + rx + 2;
+    r_ok[q] = k < RX * RY && x0 + rx < gf.nx && y0 + ry < gf.ny;
+  }
+  double acc[RBF_PERR], ucm[RBF_PERR], ucc[RBF_PERR], bq1[RBF_PERR], bq2[RBF_PERR],
+      bq3[RBF_PERR], bq4[RBF_PERR];
+#pragma unroll
+  for (int q = 0; q < RBF_PERR; ++q) acc[q] = ucm[q] = ucc[q] = bq1[q] = bq2[q] = bq3[q] = bq4[q] = 0.0;
+  const int cx = tid & 15, cy = tid >> 4;     // coarse point (threads 0..127)
+  const int gcx = x0 / 2 + cx, gcy = y0 / 2 + cy;
+  const bool c_ok = tid < (TX / 2) * (TY / 2) && gcx < gc.nx && gcy < gc.ny;
+  ColourSlots<RBF_RS> reds;
+  ColourSlots<RBF_BS> blacks;
+  reds.init(x0 - 2, x0 + 34, y0 - 2, y0 + 18, 1, x0, y0, gf);
+  blacks.init(x0 - 1, x0 + 33, y0 - 1, y0 + 17, 0, x0, y0, gf);
+  wait_u(ulo);
+  wait_u(ulo + 1);
+  for (int r = p0 - 2; r <= p1 + 6; ++r) {
+    // ---- red points of plane r over Rd
+    if (r <= bhi) {
+      wait_u(r + 1);
+      wait_b(r);
+      if (r >= 0 && r < gf.nz)
+        reds.run<POW2>(uslot(r), uslot(r - 1), uslot(r + 1), bslot(r), r & 1, c, sigma, omega,
+                       dval, dinv);
+    }
+    // ---- black points of plane r-2 over F
+    const int qb = r - 2;
+    if (qb >= p0 - 1 && qb <= p1 + 1 && qb >= 0 && qb < gf.nz)
+      blacks.run<POW2>(uslot(qb), uslot(qb - 1), uslot(qb + 1), bslot(qb), qb & 1, c, sigma,
+                       omega, dval, dinv);
+    // ---- residual of plane p = r-4 (centres of planes p-1, p, p+1 in registers)
+    const int p = r - 4;
+    if (p >= p0 && p <= p1) {
+      const double* pc = uslot(p);
+      const double* pn = uslot(p + 1);
+      const int ph = p - p0;
+#pragma unroll
+      for (int q = 0; q < RBF_PERR; ++q) {
+        if (r_k[q] < 0) continue;
+        double v = 0.0;
+        const double zp = pn[r_iu[q]];
+        if (r_ok[q]) {
+          const int i = r_iu[q];
+          const double c0 = ucc[q];
+          double a = 0.0;
+          a = a + dd2<POW2>((ucm[q] - 2.0 * c0) + zp, c);
+          a = a + dd2<POW2>((pc[i - QUX] - 2.0 * c0) + pc[i + QUX], c);
+          a = a + dd2<POW2>((pc[i - 1] - 2.0 * c0) + pc[i + 1], c);
+          const double au = c0 - sigma * (c.nu * a);
+          v = bq4[q] - au;
+        }
+        ucm[q] = ucc[q];
+        ucc[q] = zp;
+        if (ph == 0) {
+          acc[q] = v;
+        } else if (ph & 1) {
+          acc[q] = acc[q] + 2.0 * v;
+        } else {
+          szb[r_k[q]] = 0.25 * (acc[q] + v);
+          acc[q] = v;
+        }
+      }
+    } else if (p == p0 - 1 || p == p0 - 2) {   // preload the centres of planes p0-1, p0
+#pragma unroll
+      for (int q = 0; q < RBF_PERR; ++q) {
+        if (r_k[q] < 0) continue;
+        ucm[q] = ucc[q];
+        ucc[q] = uslot(p + 1)[r_iu[q]];
+      }
+    }
+    // b values of this thread's residual points, four planes deep
+    if (r >= blo && r <= bhi) {
+#pragma unroll
+      for (int q = 0; q < RBF_PERR; ++q) {
+        bq4[q] = bq3[q];
+        bq3[q] = bq2[q];
+        bq2[q] = bq1[q];
+        bq1[q] = r_k[q] >= 0 ? bslot(r)[r_ib[q]] : 0.0;
+      }
+    } else {
+#pragma unroll
+      for (int q = 0; q < RBF_PERR; ++q) {
+        bq4[q] = bq3[q];
+        bq3[q] = bq2[q];
+        bq2[q] = bq1[q];
+      }
+    }
+    // ---- owned points of plane r-3 (final since phase r-1)
+    const int qo = r - 3;
+    if (qo >= p0 && qo <= qhi && tid < TX * TY / 2) {
+      const int oy = tid >> 4, ox = 2 * (tid & 15);
+      const int gx = x0 + ox, gy = y0 + oy;
+      if (gy < gf.ny && gx < gf.nx) {
+        const double2 v =
+            *reinterpret_cast<const double2*>(uslot(qo) + (oy + 3) * QUX + ox + 4);
+        double* dst = out + gf.at(gx, gy, qo);
+        if (gx + 1 < gf.nx) *reinterpret_cast<double2*>(dst) = v;
+        else dst[0] = v.x;
+      }
+    }
+    // ---- k_rfw's y and x passes (lagging the z weights by one and two planes)
+    const int fph = p - p0;
+    if (fph >= 3 && (fph & 1) == 1) {
+      for (int k = tid; k < RX * (TY / 2); k += RBF_NT) {
+        const int yy = k / RX, xx = k - yy * RX;
+        const double* zc = szb + 2 * yy * RX + xx;
+        syx[k] = fw3(zc[0], zc[RX], zc[2 * RX]);
+      }
+    }
+    if (fph >= 4 && (fph & 1) == 0 && c_ok) {
+      const double* yr = syx + cy * RX + 2 * cx;
+      coarse[gc.at(gcx, gcy, (p - 4) / 2)] = fw3(yr[0], yr[1], yr[2]);
+    }
+    __syncthreads();
+    if (tid == 0) {
+      if (r - 4 >= ulo) issue_u(r - 4 + RBF_RU);   // plane r-4 is dead
+      if (r - 2 >= blo) issue_b(r - 2 + RBF_RB);   // b plane r-2 is dead
+    }
+  }
+}
+
 // k_cubic4: k_cubic3's arithmetic (same passes, same FMA chains) as a skewed
 // three-stage pipeline with one barrier per fine plane: phase t runs the z
 // pass of fine plane z0+t (coarse ring -> zb[t&1]), the y pass of plane
@@ -1567,6 +1840,13 @@ int launch_zrb3(const double* u, const double* b, double* out, const Geo& g, con
   int zc = pick_zc(g);
   dim3 grid(ceil_div(g.nx, TX), ceil_div(g.ny, TY), ceil_div(g.nz, zc));
   const double dinv = 1.0 / dval;
+  if (g_zrb_ring == 1) {   // 6 u + 3 b planes, 4 CTAs per SM (register cap 64)
+    size_t smem = ((size_t)6 * PU + (size_t)3 * PB) * 8 + 8 * (6 + 3);
+    auto kern = c.pow2 ? k_zrb3<true, 6, 3, 4, false> : k_zrb3<false, 6, 3, 4, false>;
+    raise_smem(kern, smem);
+    kern<<<grid, dim3(NTHR_RB2), smem, s>>>(mu, mb, out, g, c, sigma, omega, dval, dinv, zc);
+    return 0;
+  }
   size_t smem = ((size_t)8 * PU + (size_t)4 * PB) * 8 + 8 * (8 + 4);
   auto kern = c.pow2 ? k_zrb3<true, 8, 4, 3, false> : k_zrb3<false, 8, 4, 3, false>;
   raise_smem(kern, smem);
@@ -1586,6 +1866,23 @@ int launch_rfw(const double* u, const double* b, double* coarse, const Geo& g, c
   auto kern = c.pow2 ? k_rfw<true> : k_rfw<false>;
   raise_smem(kern, smem);
   kern<<<grid, block, smem, s>>>(mu, mb, coarse, g, gc, c, sigma, zcc);
+  return 0;
+}
+
+int launch_rbrfw(const double* u, const double* b, double* out, double* coarse, const Geo& g,
+                 const OpC& c, double sigma, double omega, double dval, cudaStream_t s) {
+  Geo gc = make_geo(3, (g.N + 1) / 2);
+  CUtensorMap mu, mb;
+  PL_TRY(make_map(&mu, u, g, QUX, QUY));
+  PL_TRY(make_map(&mb, b, g, QBX, QBY));
+  // the pipeline fills over 9 phases: chunks of >= 16 coarse planes
+  const int zcc = std::max(g_rbrfw_zcc, pick_zc(g) / 2);
+  dim3 grid(ceil_div(g.nx, TX), ceil_div(g.ny, TY), ceil_div(gc.nz, zcc));
+  size_t smem = sizeof(double) * (RBF_RU * PQU + RBF_RB * PQB + 2 * PR) + 8 * (RBF_RU + RBF_RB);
+  auto kern = c.pow2 ? k_rbrfw<true> : k_rbrfw<false>;
+  raise_smem(kern, smem);
+  kern<<<grid, RBF_NT, smem, s>>>(mu, mb, out, coarse, g, gc, c, sigma, omega, dval, 1.0 / dval,
+                                  zcc);
   return 0;
 }
 
@@ -1637,6 +1934,7 @@ double zdiag(const OpC& c, double sigma) {
 
 int g_zmarch_enabled = 1;   // runtime knob (pl_set_option), for A/B tests
 int g_zrb_variant = 4;      // 0: k_zrb (3 barriers / plane), 4: k_zrb3 (one barrier / plane)
+int g_zrb_ring = 0;
 int g_fuse_prolong = 0;     // prolongation fused into the first post-sweep (slower since k_zrb3)
 bool zmarch_fuse_prolong() { return g_fuse_prolong != 0; }
 // smallest interior size for the TMA kernels: below it a CTA would march many
@@ -1661,6 +1959,21 @@ int zlaunch_rfw(const double* u, const double* b, double* coarse, const Geo& g, 
   PL_TRY(launch_rfw(u, b, coarse, g, c, sigma, s));
   // algorithmic bytes of the unfused pair (residual 24 B, FW 8 B + 8 B coarse)
   PL_CHECK_LAUNCH(K_RESTRICT, 32.0 * g.npts + 8.0 * gc.npts);
+  return 0;
+}
+
+int g_rbrfw_enabled = 0;   // PL_OPT_RBRFW: last pre-sweep + residual + FW fused (jor-rb);
+                           // measured slower than k_zrb3 + k_rfw (A/B only)
+int g_rbrfw_zcc = 16;
+
+int zlaunch_rbrfw(const double* u, const double* b, double* out, double* coarse, const Geo& g,
+                  const OpC& c, double sigma, double omega, cudaStream_t s) {
+  Geo gc = make_geo(3, (g.N + 1) / 2);
+  PL_PRE(K_RBRFW);
+  PL_TRY(launch_rbrfw(u, b, out, coarse, g, c, sigma, omega, zdiag(c, sigma), s));
+  // algorithmic bytes of the unfused kernels it replaces: one red-black
+  // sweep (24 B) plus residual + full weighting (32 B + 8 B per coarse point)
+  PL_CHECK_LAUNCH(K_RBRFW, 24.0 * g.npts + 32.0 * g.npts + 8.0 * gc.npts);
   return 0;
 }
 

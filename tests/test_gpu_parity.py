@@ -397,14 +397,15 @@ def test_pfasst_run_parity_tma_path(name):
         _capi.set_option(_capi.OPT_ZMARCH_MIN_N, 127)
 
 
-@pytest.mark.parametrize("variant", [0, 4])
+@pytest.mark.parametrize("variant", [0, 4, 5])
 def test_zrb_variants_bitwise_31cubed(variant):
     """Every jor-rb TMA sweep variant (three barriers per plane, and the
     register-pipelined one-barrier kernels with their ring sizes) reproduces
     the reference's red-black sweeps bit for bit on the 31^3 golden case."""
     a, m = case("mg32_d3")
     _capi.set_option(_capi.OPT_ZMARCH_MIN_N, 31)
-    _capi.set_option(_capi.OPT_ZRB_VARIANT, variant)
+    _capi.set_option(_capi.OPT_ZRB_VARIANT, min(variant, 4))
+    _capi.set_option(_capi.OPT_ZRB_RING, int(variant == 5))   # 5: the 6 + 3 plane rings
     try:
         sop = mg.ShiftedOperator(heat.HeatOperator(heat.Grid(3, 32)), m["sigma"])
         for om in (1.0, 0.8):
@@ -414,6 +415,7 @@ def test_zrb_variants_bitwise_31cubed(variant):
                         a[f"sm{cnt}_jor-rb_{om:.3f}"])
     finally:
         _capi.set_option(_capi.OPT_ZRB_VARIANT, 4)
+        _capi.set_option(_capi.OPT_ZRB_RING, 0)
         _capi.set_option(_capi.OPT_ZMARCH_MIN_N, 127)
 
 
@@ -436,12 +438,14 @@ def test_zrb_variants_equal_plain_kernels(n, length, sigma, fuse):
     _capi.set_option(_capi.OPT_ZMARCH, 1)
     _capi.set_option(_capi.OPT_FUSE_PROLONG, fuse)
     try:
-        for variant in (0, 4):
-            _capi.set_option(_capi.OPT_ZRB_VARIANT, variant)
+        for variant in (0, 4, 5):
+            _capi.set_option(_capi.OPT_ZRB_VARIANT, min(variant, 4))
+            _capi.set_option(_capi.OPT_ZRB_RING, int(variant == 5))
             assert torch.equal(mg.v_cycle(sop, u, b, cfg), ref), variant
             assert torch.equal(mg.smooth(sop, u, b, cfg, 2), ref_s), variant
     finally:
         _capi.set_option(_capi.OPT_ZRB_VARIANT, 4)
+        _capi.set_option(_capi.OPT_ZRB_RING, 0)
         _capi.set_option(_capi.OPT_FUSE_PROLONG, 0)
 
 
@@ -665,3 +669,33 @@ def test_pfasst_gauss_seidel_and_direct(name):
     assert res.rank_vcycles == m["rank_vcycles"]
     assert res.converged == m["converged"]
     close(res.u, a["u"])
+
+
+@pytest.mark.parametrize("n,length,sigma", [(32, 1.0, 0.01), (64, 1.0, 0.003), (128, 3.0, 0.01),
+                                            (256, 1.0, 1.0 / 512)])
+@pytest.mark.parametrize("pre", [1, 2])
+def test_fused_presweep_residual_restriction(n, length, sigma, pre):
+    """k_rbrfw (last jor-rb pre-sweep + residual + full weighting in one pass,
+    overlapped halo tiles, several z chunks, ragged edge tiles) gives the
+    separate sweep + k_rfw V-cycle bit for bit, from a guess and from zero."""
+    rng = np.random.default_rng(5 * n + pre)
+    g = heat.Grid(3, n, length)
+    u = dev(rng.standard_normal(g.shape))
+    b = dev(rng.standard_normal(g.shape))
+    sop = mg.ShiftedOperator(heat.HeatOperator(g), sigma)
+    cfg = mg.MgConfig("jor-rb", 1.0 if pre == 1 else 0.9, pre, 1)
+    _capi.set_option(_capi.OPT_ZMARCH_MIN_N, 31)
+    try:
+        _capi.set_option(_capi.OPT_RBRFW, 0)
+        ref = mg.v_cycle(sop, u, b, cfg)
+        ref0 = mg.v_cycle(sop, torch.zeros_like(u), b, cfg)
+        _capi.set_option(_capi.OPT_RBRFW, 1)
+        got = mg.v_cycle(sop, u, b, cfg)
+        assert torch.equal(got, ref), float((got - ref).abs().max())
+        assert torch.equal(mg.v_cycle(sop, torch.zeros_like(u), b, cfg), ref0)
+        _capi.set_option(_capi.OPT_ZMARCH, 0)
+        assert torch.equal(mg.v_cycle(sop, u, b, cfg), ref)
+    finally:
+        _capi.set_option(_capi.OPT_ZMARCH, 1)
+        _capi.set_option(_capi.OPT_RBRFW, 0)
+        _capi.set_option(_capi.OPT_ZMARCH_MIN_N, 127)
