@@ -761,7 +761,47 @@ __device__ __forceinline__ void rb_phase(const RbCtx& k, int z, const double2& U
   else if (k.va) dst[0] = w.x;
 }
 
-template <bool POW2, int RU, int RB, int MINB, bool HW>
+// rb_phase with this thread's halo red point (plane q = z+2, parity slot P)
+// evaluated in the same straight-line code: the 50 halo reds are dealt to
+// lanes 0..6 of every warp, so no warp carries a serial halo update after its
+// interior pair (the barrier then waits for the slowest of equal warps), and
+// the third chain adds instruction-level parallelism.  Lanes without a halo
+// point compute on a safe index and store nothing.
+template <bool POW2, int RU, int RB, int PAR, int P>
+__device__ __forceinline__ void rb_phase_h(const RbCtx& k, int z, const double2& U0, double2& U1,
+                                           const double2& U2, double2& U3, const double2& U4,
+                                           const double2& B0, const double2& B2) {
+  const int q = z + 2;
+  double* plr = rb_u<RU>(k, q);
+  const double* plb = rb_u<RU>(k, z);
+  const bool hv = (P ? k.hv1 : k.hv0) && q <= k.R;
+  const int hi = hv ? (P ? k.hu1 : k.hu0) : k.iu;
+  const int hb = hv ? (P ? k.hb1 : k.hb0) : k.ib;
+  const double* pm = rb_u<RU>(k, q - 1);
+  const double* pp = rb_u<RU>(k, q + 1);
+  const double* bq = rb_b<RB>(k, q);
+  Relax rr = rb_point_fast<POW2, 1 - PAR>(k, plr, U2, U3, U4, B2);
+  Relax rbk = rb_point_fast<POW2, PAR>(k, plb, U0, U1, U2, B0);
+  Relax rh = rb_fast<POW2>(k, pm[hi], pp[hi], plr[hi - UX], plr[hi + UX], plr[hi - 1],
+                           plr[hi + 1], plr[hi], bq[hb]);
+  if (__builtin_expect(!(quot_ok(rr.a) && quot_ok(rbk.a) && quot_ok(rh.a)), 0)) {
+    if (!quot_ok(rr.a)) rr.q = div_slow(rr.a, k.dval);
+    if (!quot_ok(rbk.a)) rbk.q = div_slow(rbk.a, k.dval);
+    if (!quot_ok(rh.a)) rh.q = div_slow(rh.a, k.dval);
+  }
+  const double vr = rr.cc + rr.q, vb = rbk.cc + rbk.q, vh = rh.cc + rh.q;
+  if (q <= k.R && (PAR ? k.va : k.vb)) {
+    plr[k.iu + 1 - PAR] = vr;
+    set_mem<1 - PAR>(U3, vr);
+  }
+  if (hv) plr[hi] = vh;
+  double* dst = k.optr + (long long)z * k.sz;
+  const double2 w = PAR ? make_double2(U1.x, vb) : make_double2(vb, U1.y);
+  if (k.va && k.vb) *reinterpret_cast<double2*>(dst) = w;
+  else if (k.va) dst[0] = w.x;
+}
+
+template <bool POW2, int RU, int RB, int MINB, bool HW, bool HM = false>
 __global__ void __launch_bounds__(HW ? 320 : NTHR_RB2, MINB) k_zrb3(const __grid_constant__ CUtensorMap mu,
                                                       const __grid_constant__ CUtensorMap mb,
                                                       double* __restrict__ out, Geo g, OpC c,
@@ -826,7 +866,8 @@ __global__ void __launch_bounds__(HW ? 320 : NTHR_RB2, MINB) k_zrb3(const __grid
   k.sz = g.sz;
   // HW: warps 8-9 (threads 256..305) own the 50 halo reds and nothing else,
   // so no warp does more than two updates per phase
-  const int hid = HW ? tid - 256 : tid;
+  // halo red ids: HW dedicated warps 8-9; HM lanes 0..6 of every warp; else threads 0..49
+  const int hid = HW ? tid - 256 : (HM ? (lane < 7 ? warp * 7 + lane : 99) : tid);
   const bool is_halo = HW ? warp >= 8 : hid < 50;
   const bool is_int = HW ? warp < 8 : true;
   {
@@ -920,8 +961,12 @@ __global__ void __launch_bounds__(HW ? 320 : NTHR_RB2, MINB) k_zrb3(const __grid
       }
       double2 U4 = lds2(rb_u<RU>(k, z + 3) + k.iu);   // stale beyond R: unused
       const double2 B2 = lds2(rb_b<RB>(k, z + 2) + k.ib);
-      if (is_int) rb_phase<POW2, RU, RB, PA>(k, z, U0, U1, U2, U3, U4, B0, B2);
-      if (is_halo) rb_halo<POW2, RU, RB, 0>(k, z + 2);
+      if (HM) {
+        rb_phase_h<POW2, RU, RB, PA, 0>(k, z, U0, U1, U2, U3, U4, B0, B2);
+      } else {
+        if (is_int) rb_phase<POW2, RU, RB, PA>(k, z, U0, U1, U2, U3, U4, B0, B2);
+        if (is_halo) rb_halo<POW2, RU, RB, 0>(k, z + 2);
+      }
       __syncthreads();
       if (tid == 0) {
         issue_u(z + RU);
@@ -935,8 +980,12 @@ __global__ void __launch_bounds__(HW ? 320 : NTHR_RB2, MINB) k_zrb3(const __grid
       }
       double2 U5 = lds2(rb_u<RU>(k, z + 4) + k.iu);
       const double2 B3 = lds2(rb_b<RB>(k, z + 3) + k.ib);
-      if (is_int) rb_phase<POW2, RU, RB, PB>(k, z + 1, U1, U2, U3, U4, U5, B1, B3);
-      if (is_halo) rb_halo<POW2, RU, RB, 1>(k, z + 3);
+      if (HM) {
+        rb_phase_h<POW2, RU, RB, PB, 1>(k, z + 1, U1, U2, U3, U4, U5, B1, B3);
+      } else {
+        if (is_int) rb_phase<POW2, RU, RB, PB>(k, z + 1, U1, U2, U3, U4, U5, B1, B3);
+        if (is_halo) rb_halo<POW2, RU, RB, 1>(k, z + 3);
+      }
       __syncthreads();
       if (tid == 0) {
         issue_u(z + 1 + RU);
@@ -1840,6 +1889,13 @@ int launch_zrb3(const double* u, const double* b, double* out, const Geo& g, con
   int zc = pick_zc(g);
   dim3 grid(ceil_div(g.nx, TX), ceil_div(g.ny, TY), ceil_div(g.nz, zc));
   const double dinv = 1.0 / dval;
+  if (g_zrb_ring == 2) {   // halo reds dealt to every warp, merged into the phase code
+    size_t smem = ((size_t)8 * PU + (size_t)4 * PB) * 8 + 8 * (8 + 4);
+    auto kern = c.pow2 ? k_zrb3<true, 8, 4, 3, false, true> : k_zrb3<false, 8, 4, 3, false, true>;
+    raise_smem(kern, smem);
+    kern<<<grid, dim3(NTHR_RB2), smem, s>>>(mu, mb, out, g, c, sigma, omega, dval, dinv, zc);
+    return 0;
+  }
   if (g_zrb_ring == 1) {   // 6 u + 3 b planes, 4 CTAs per SM (register cap 64)
     size_t smem = ((size_t)6 * PU + (size_t)3 * PB) * 8 + 8 * (6 + 3);
     auto kern = c.pow2 ? k_zrb3<true, 6, 3, 4, false> : k_zrb3<false, 6, 3, 4, false>;
