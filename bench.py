@@ -189,9 +189,17 @@ def run_ours(args, w):
     step(u0_dev, streams=False)       # per-launch events: no cross-rank overlap
     barrier()
     per_kind = {n: _capi.timing_collect(n) for n in names}
+    max_launch_bytes = {n: max(_capi.timing_by_size(n) or {0.0: None}) for n in names}
     _capi.timing_enable(None)
     total_ms = sum(v[1] for v in per_kind.values())
-    dom = max(per_kind, key=lambda n: per_kind[n][1])
+    dom_all = max(per_kind, key=lambda n: per_kind[n][1])
+    # the roofline is quoted on the dominant HBM-bound kind: one whose largest
+    # launch streams more than the L2 holds.  Kinds that only ever touch
+    # L2-resident fields (the cooperative small-level V-cycle on <= 63^3) are
+    # latency-bound; their share is reported beside, not against HBM.
+    l2 = torch.cuda.get_device_properties(local).L2_cache_size
+    hbm_kinds = [n for n in names if max_launch_bytes[n] > l2 and per_kind[n][0]]
+    dom = max(hbm_kinds, key=lambda n: per_kind[n][1]) if hbm_kinds else dom_all
 
     # ---- timed region: device-resident input (sweeps replay as CUDA graphs)
     stream = torch.cuda.current_stream()
@@ -283,6 +291,14 @@ def run_ours(args, w):
                     "h2d_bytes_per_step": int(u0_host.nbytes),
                     "d2h_bytes_per_step": int(u0_host.nbytes)},
             "gpu_launches": launches,
+            "dominant_kind": {"name": dom_all,
+                              "share_of_step": round(per_kind[dom_all][1] / total_ms, 4),
+                              "max_launch_mb": round(max_launch_bytes[dom_all] / 1e6, 1),
+                              "note": ("the roofline kernel" if dom_all == dom else
+                                       "latency-bound: every launch works on L2-resident "
+                                       "fields (< L2 = %.0f MB); reported by share, the "
+                                       "roofline is quoted on the dominant HBM-bound kind"
+                                       % (l2 / 1e6))},
             "roofline": {"bound": "hbm", "kernel": f"{dom} @ {w['ns'][0] - 1}^{w['dim']}",
                          "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": (achieved / peak) if achieved else None,

@@ -84,8 +84,9 @@ const char* pl_last_error(void);
                                  level and direction (overlapped shared-memory tiles, LU fused
                                  into the last down phase); 0 (default, measured faster): one
                                  phase per former kernel plus the one-CTA tail */
-#define PL_OPT_MID_CTAS 13    /* CTAs of the cooperative small-level kernels (default 32; 0: one
-                                 per SM); fewer leave SMs to other time ranks' streams */
+#define PL_OPT_MID_CTAS 13    /* CTAs of the cooperative small-level kernels (0, default: one per
+                                 SM); pfasst_run's rank-stream schedule sets 32 for its duration
+                                 so the other ranks' streams keep the remaining SMs */
 #define PL_OPT_ZRB_RING 14    /* one-barrier jor-rb sweep rings: 0 (default) 8 u + 4 b planes,
                                  3 CTAs/SM; 1: 6 u + 3 b planes, 4 CTAs/SM; bit-identical */
 #define PL_OPT_RBRFW 15       /* 1: the last jor-rb pre-sweep, the residual and full weighting

@@ -152,8 +152,29 @@ OPT_RBRFW = 15
 OPT_RBRFW_ZCC = 16
 
 
+_OPTION_VALUES = {}      # options set through this module (the library defaults otherwise)
+
+
 def set_option(key, value):
     check(lib().pl_set_option(key, int(value)), "set_option")
+    _OPTION_VALUES[key] = int(value)
+
+
+class option:
+    """Scoped pl_set_option: ``with option(OPT_MID_CTAS, 32): ...`` restores the
+    previous value (or ``default``) on exit."""
+
+    def __init__(self, key, value, default):
+        self.key, self.value, self.default = key, int(value), default
+
+    def __enter__(self):
+        self.prev = _OPTION_VALUES.get(self.key, self.default)
+        set_option(self.key, self.value)
+        return self
+
+    def __exit__(self, *exc):
+        set_option(self.key, self.prev)
+        return False
 
 
 def last_error():

@@ -681,7 +681,7 @@ static int launch_tail(MgPlan* P, int l0, double* u, const double* b, double sig
 
 int g_mid_enabled = 1;      // PL_OPT_MID
 int g_mid_tail_n = 15;      // PL_OPT_MID_TAIL_N: largest N the mid kernel leaves to its tail
-int g_mid_ctas = 32;        // PL_OPT_MID_CTAS: CTAs of the cooperative mid kernels (0: one per SM)
+int g_mid_ctas = 0;         // PL_OPT_MID_CTAS: CTAs of the cooperative mid kernels (0: one per SM)
 
 // first tail level of the mid kernel (>= the plan's tail_start)
 static int mid_tail_level(const MgPlan* P) {

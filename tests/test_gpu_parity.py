@@ -515,7 +515,7 @@ def test_mid2_one_phase_per_level_equals_separate_launches(n, length, pre, post,
     finally:
         _capi.set_option(_capi.OPT_MID, 1)
         _capi.set_option(_capi.OPT_MID2, 0)
-        _capi.set_option(_capi.OPT_MID_CTAS, 32)
+        _capi.set_option(_capi.OPT_MID_CTAS, 0)
 
 
 @pytest.mark.parametrize("name", ["run_cfg1", "run_cfg2_small", "run_cfg3_small", "run_cfg4_small_tol"])
