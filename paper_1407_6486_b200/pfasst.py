@@ -389,13 +389,39 @@ class _Block:
         if n + 1 < self.p and not self.x.owns(n + 1):
             self.x.send_flag(n, k, ok)
 
+    def _schedule(self):
+        """(k, n) issue order of this process's ranks.  One process (or one
+        owned rank): the reference's serial order, k-major.  Several owned
+        ranks on a process of the nccl executor (cyclic placement, G < P):
+        anti-diagonals d = n + k ascending, n descending -- rank n's iteration
+        k needs rank n-1's iteration k, which its owner issued on diagonal
+        d - 1, so no process waits inside a diagonal and the G processes run
+        concurrently instead of handing one iteration around the ring.  Every
+        process uses the same global order, so the messages between any pair
+        of processes are posted and matched in the same sequence on both
+        sides; convergence decisions are unchanged."""
+        if len(self.mine) <= 1 or isinstance(self.x, _LocalExchange):
+            for k in range(1, self.max_iter + 1):
+                yield k, None
+            return
+        for d in range(1, self.max_iter + self.p):
+            for n in sorted(self.mine, reverse=True):
+                k = d - n
+                if 1 <= k <= self.max_iter:
+                    yield k, n
+
     def iterations_loop(self):
         e, x, p = self.e, self.x, self.p
-        for k in range(1, self.max_iter + 1):
+        stopped = set()
+        for k, only in self._schedule():
             active = False
-            for n in self.mine:
+            for n in (self.mine if only is None else (only,)):
+                if n in stopped:
+                    continue
                 self._resolve(n)
                 if self.frozen[n]:
+                    if only is not None:
+                        stopped.add(n)
                     continue
                 active = True
                 if n > 0:
@@ -420,7 +446,7 @@ class _Block:
                 self.pending[n] = (k, cyc, handle)
                 if self.record and n == p - 1:
                     self.final_values.append(e.snapshot(e.fine_payload(n)))
-            if not active:
+            if not active and only is None:
                 break
         for n in self.mine:
             self._resolve(n)

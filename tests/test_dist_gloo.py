@@ -40,6 +40,8 @@ CASES = {
     "two_level_fixed": ((64, 32), (5, 3), mg.FixedCycles(1), 4, 1, 1e-10, 20),
     "three_level_tol_blocks": ((64, 32, 16), (5, 3, 2), mg.ToTolerance(1e-12), 5, 2, 1e-9, 12),
     "unconverged": ((32, 16), (3, 2), mg.FixedCycles(1), 3, 1, 1e-300, 3),
+    # several ranks per process (wavefront issue order), staggered freezing
+    "six_ranks_two_blocks": ((64, 32), (5, 3), mg.FixedCycles(1), 6, 2, 1e-9, 15),
 }
 
 
