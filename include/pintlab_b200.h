@@ -71,7 +71,8 @@ const char* pl_last_error(void);
                                  register-pipelined one barrier per plane; bit-identical */
 #define PL_OPT_FUSE_PROLONG 4 /* 1: prolongation fused into the first post-sweep (TMA levels);
                                  default 0 (separate per-cell prolongation is faster) */
-#define PL_OPT_CUBIC_VARIANT 5 /* 3-D cubic kernel: 0 staged loads, 1 (default) TMA ring */
+#define PL_OPT_CUBIC_VARIANT 5 /* 3-D cubic kernel: 0 staged loads, 1 TMA ring, 2 (default) TMA
+                                  ring with zero-padded branch-free tap chains; bit-identical */
 #define PL_OPT_MID 6          /* 1 (default): V-cycle levels below the TMA threshold and the tail
                                  run as one cooperative launch (3-D order-2 jor-rb) */
 #define PL_OPT_MID_TAIL_N 7   /* largest n-1 the cooperative kernel leaves to its one-CTA tail

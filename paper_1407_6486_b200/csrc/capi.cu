@@ -322,7 +322,11 @@ int pl_set_option(int key, int value) {
     return 0;
   }
   if (key == PL_OPT_CUBIC_VARIANT) {
-    g_cubic_variant = value != 0;
+    if (value < 0 || value > 2) {
+      set_error("cubic variant %d out of range (0..2)", value);
+      return PL_ERR_ARG;
+    }
+    g_cubic_variant = value;
     return 0;
   }
   if (key == PL_OPT_FUSE_PROLONG) {

@@ -1562,19 +1562,25 @@ __global__ void __launch_bounds__(RBF_NT, 2) k_rbrfw(const __grid_constant__ CUt
 constexpr int RQ4 = 8;
 constexpr int PY4 = align16(TY * QW);
 
-// acc = chain_{u < n} w[u] * v[u] in tap order (v loaded for every u)
+// acc = chain_{u < n} w[u] * v[u] in tap order (v loaded for every u).
+// g_cubic_pad: absent taps carry weight 0 and are chained too -- the
+// reference's dense tensordot adds those zero products as well, and for
+// finite values acc + 0 * v == acc (acc is never -0: the chain starts from
+// +0), so the result is the same bit for bit and the chain has no branches.
+template <bool PAD>
 __device__ __forceinline__ double tap_chain(int n, const double (&w)[4], double v0, double v1,
                                             double v2, double v3) {
   double acc = __fma_rn(w[0], v0, 0.0);
-  if (n > 1) acc = __fma_rn(w[1], v1, acc);
-  if (n > 2) acc = __fma_rn(w[2], v2, acc);
-  if (n > 3) acc = __fma_rn(w[3], v3, acc);
+  if (PAD || n > 1) acc = __fma_rn(w[1], v1, acc);
+  if (PAD || n > 2) acc = __fma_rn(w[2], v2, acc);
+  if (PAD || n > 3) acc = __fma_rn(w[3], v3, acc);
   return acc;
 }
 
 constexpr int RF4 = 8;                       // fine-tile ring (accumulate mode)
 constexpr int PF4 = TX * TY;
 
+template <bool PAD>
 __global__ void __launch_bounds__(NTHR, 3) k_cubic4(const __grid_constant__ CUtensorMap mc,
                                                  const __grid_constant__ CUtensorMap mf,
                                                  double* __restrict__ fine, Geo gf,
@@ -1706,7 +1712,7 @@ __global__ void __launch_bounds__(NTHR, 3) k_cubic4(const __grid_constant__ CUte
         const double* s1 = sc + ((zj[1] - jlo) & (RQ4 - 1)) * PQ + tid;
         const double* s2 = sc + ((zj[2] - jlo) & (RQ4 - 1)) * PQ + tid;
         const double* s3 = sc + ((zj[3] - jlo) & (RQ4 - 1)) * PQ + tid;
-        zb[(t & 1) * PQ + tid] = tap_chain(zn, zw, *s0, *s1, *s2, *s3);
+        zb[(t & 1) * PQ + tid] = tap_chain<PAD>(zn, zw, *s0, *s1, *s2, *s3);
       }
     }
     // ---- y pass of fine plane z0+t-1
@@ -1716,7 +1722,7 @@ __global__ void __launch_bounds__(NTHR, 3) k_cubic4(const __grid_constant__ CUte
 #pragma unroll
       for (int q = 0; q < 2; ++q)
         if (yk[q] >= 0)
-          yd[yk[q]] = tap_chain(yn[q], yw[q], zs[yi[q][0]], zs[yi[q][1]], zs[yi[q][2]],
+          yd[yk[q]] = tap_chain<PAD>(yn[q], yw[q], zs[yi[q][0]], zs[yi[q][1]], zs[yi[q][2]],
                                 zs[yi[q][3]]);
     }
     // ---- x pass (finish)
@@ -1724,8 +1730,8 @@ __global__ void __launch_bounds__(NTHR, 3) k_cubic4(const __grid_constant__ CUte
       const double* ys = yb + (t & 1) * PY4;      // (t - 2) & 1
       const double* ya = ys + fy0 * QW;
       const double* yc = ys + fy1 * QW;
-      const double a0 = tap_chain(xn, xw, ya[xi[0]], ya[xi[1]], ya[xi[2]], ya[xi[3]]);
-      const double a1 = tap_chain(xn, xw, yc[xi[0]], yc[xi[1]], yc[xi[2]], yc[xi[3]]);
+      const double a0 = tap_chain<PAD>(xn, xw, ya[xi[0]], ya[xi[1]], ya[xi[2]], ya[xi[3]]);
+      const double a1 = tap_chain<PAD>(xn, xw, yc[xi[0]], yc[xi[1]], yc[xi[2]], yc[xi[3]]);
       if (accumulate) {
         if (r0) *f0 = ftile[fy0 * TX + threadIdx.x] + a0;
         if (r1) *f1 = ftile[fy1 * TX + threadIdx.x] + a1;
@@ -1943,7 +1949,8 @@ int launch_rbrfw(const double* u, const double* b, double* out, double* coarse, 
 }
 
 }  // namespace
-int g_cubic_variant = 1;    // 0: k_cubic3, 1: k_cubic4 (TMA ring, one barrier per plane)
+int g_cubic_variant = 2;    // 0: k_cubic3, 1: k_cubic4 (TMA ring, one barrier per plane),
+                            // 2 (default): k_cubic4 with zero-padded branch-free tap chains
 namespace {
 
 int launch_cubic3(const double* coarse, double* fine, const Geo& gf, const int* cnt,
@@ -1951,15 +1958,16 @@ int launch_cubic3(const double* coarse, double* fine, const Geo& gf, const int* 
   Geo gc = make_geo(3, (gf.N + 1) / 2);
   const int zc = pick_zc(gf);
   dim3 grid(ceil_div(gf.nx, TX), ceil_div(gf.ny, TY), ceil_div(gf.nz, zc)), block(32, 8);
-  if (g_cubic_variant == 1) {
+  if (g_cubic_variant >= 1) {
     CUtensorMap mc;
     PL_TRY(make_map(&mc, coarse, gc, QW, QH));
     CUtensorMap mf;
     std::memset(&mf, 0, sizeof(mf));
     if (accumulate) PL_TRY(make_map(&mf, fine, gf, TX, TY));
     size_t smem = accumulate ? sizeof(double) * RF4 * PF4 : 0;
-    raise_smem(k_cubic4, smem);
-    k_cubic4<<<grid, block, smem, s>>>(mc, mf, fine, gf, cnt, idx, w, zc, accumulate);
+    auto kern = g_cubic_variant == 2 ? k_cubic4<true> : k_cubic4<false>;
+    raise_smem(kern, smem);
+    kern<<<grid, block, smem, s>>>(mc, mf, fine, gf, cnt, idx, w, zc, accumulate);
     return 0;
   }
   size_t smem = sizeof(double) * (RQ * PQ + align16(QW * QH) + align16(QW * TY));

@@ -374,14 +374,14 @@ def test_cubic_zmarch_equals_pass_kernels(nf):
         ref_acc = clone_field(f)
         transfers.interp_cubic_into(c, ref_acc, True)
         _capi.set_option(_capi.OPT_ZMARCH, 1)
-        for variant in (0, 1):
+        for variant in (0, 1, 2):
             _capi.set_option(_capi.OPT_CUBIC_VARIANT, variant)
             assert torch.equal(transfers.interp_cubic(c), ref), variant
             acc = clone_field(f)
             transfers.interp_cubic_into(c, acc, True)
             assert torch.equal(acc, ref_acc), variant
     finally:
-        _capi.set_option(_capi.OPT_CUBIC_VARIANT, 1)
+        _capi.set_option(_capi.OPT_CUBIC_VARIANT, 2)
         _capi.set_option(_capi.OPT_ZMARCH, 1)
         _capi.set_option(_capi.OPT_ZMARCH_MIN_N, 127)
 
