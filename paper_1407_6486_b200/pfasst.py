@@ -510,10 +510,10 @@ def _rank_stream_options():
     import os
 
     from . import _capi as capi
-    defaults = {capi.OPT_MID: 1, capi.OPT_MID_CTAS: 0}
+    defaults = {capi.OPT_MID: 1, capi.OPT_MID_CTAS: 0, capi.OPT_ZMARCH_MIN_N: 127}
     env = os.environ.get("PINTLAB_RANK_STREAM_OPTS")
-    if env is None:
-        return {capi.OPT_MID: (0, 1)}
+    if env is None:   # A/B on one box, 5 steps each: see DESIGN.md section 4
+        return {capi.OPT_MID: (0, 1), capi.OPT_ZMARCH_MIN_N: (63, 127)}
     out = {}
     for kv in filter(None, env.split(",")):
         k, v = (int(x) for x in kv.split("="))
@@ -607,10 +607,10 @@ def pfasst_run(levels, u0, t_end: float, p: int, blocks: int = 1, tol: float = 1
         if isinstance(exchange, _LocalExchange) and getattr(engine, "streams", None):
             # rank streams overlap each other's work: the small V-cycle
             # levels then run as ordinary per-level launches (no cooperative
-            # grid that must be co-resident on every SM) and interleave with
-            # the other ranks' kernels -- +15-20 % time-steps/s against the
-            # one-CTA-per-SM cooperative kernel, which a lone solve keeps
-            # (PL_OPT_MID; results are bit-identical either way)
+            # grid that must be co-resident on every SM; the TMA sweeps from
+            # 63^3 up) and interleave with the other ranks' kernels -- +15-25 %
+            # time-steps/s against the one-CTA-per-SM cooperative kernel,
+            # which a lone solve keeps (results are bit-identical either way)
             from contextlib import ExitStack
 
             from . import _capi as capi
