@@ -817,6 +817,9 @@ __global__ void __launch_bounds__(HW ? 320 : NTHR_RB2, MINB) k_zrb3(const __grid
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TY;
   const int z0 = blockIdx.z * zc, z1 = min(z0 + zc, g.nz);
+  // the in-loop TMA issues go to the first lane of warp 7, which owns no
+  // halo point, so the halo warps 0-1 are not delayed further after a barrier
+  constexpr int issuer = NTHR_RB2 - 32;
   k.z0 = z0;
   k.R = min(z1, g.nz - 1);
   const int uhi = k.R + 1, bhi = k.R;
@@ -968,7 +971,7 @@ __global__ void __launch_bounds__(HW ? 320 : NTHR_RB2, MINB) k_zrb3(const __grid
         if (is_halo) rb_halo<POW2, RU, RB, 0>(k, z + 2);
       }
       __syncthreads();
-      if (tid == 0) {
+      if (tid == issuer) {
         issue_u(z + RU);
         issue_b(z + 2 + RB);
       }
@@ -987,7 +990,7 @@ __global__ void __launch_bounds__(HW ? 320 : NTHR_RB2, MINB) k_zrb3(const __grid
         if (is_halo) rb_halo<POW2, RU, RB, 1>(k, z + 3);
       }
       __syncthreads();
-      if (tid == 0) {
+      if (tid == issuer) {
         issue_u(z + 1 + RU);
         issue_b(z + 3 + RB);
       }
@@ -1177,6 +1180,7 @@ __global__ void __launch_bounds__(NTHR, 4) k_rfw(const __grid_constant__ CUtenso
   unsigned long long* bu = (unsigned long long*)(syx + PR);
   unsigned long long* bb = bu + RFW_RU;
   const int tid = threadIdx.y * 32 + threadIdx.x;
+  constexpr int rfw_issuer = NTHR - 32;
   const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TY;
   const int jz0 = blockIdx.z * zcc, jz1 = min(jz0 + zcc, gc.nz);
   const int p0 = 2 * jz0, p1 = 2 * jz1;       // residual planes p0 .. p1
@@ -1274,7 +1278,7 @@ __global__ void __launch_bounds__(NTHR, 4) k_rfw(const __grid_constant__ CUtenso
       coarse[gc.at(gcx, gcy, (p - 4) / 2)] = fw3(yr[0], yr[1], yr[2]);
     }
     __syncthreads();
-    if (tid == 0 && p <= p1) {
+    if (tid == rfw_issuer && p <= p1) {   // warp 7: fewest residual points, no x pass
       issue_u(p - 1 + RFW_RU);    // u plane p-1 is free after the residuals of p
       issue_b(p + RFW_RB);        // b plane p is free
     }
@@ -1629,9 +1633,12 @@ __global__ void __launch_bounds__(NTHR, 3) k_cubic4(const __grid_constant__ CUte
     mbar_expect(fbar + sl, PF4 * 8u);
     tma3(sfine + sl * PF4, &mf, x0, y0, p, fbar + sl);
   };
-  if (tid == 0)
+  // one thread issues every TMA copy (issued is its private state): the
+  // first lane of warp 7, which has the fewest y-pass entries
+  constexpr int cissuer = NTHR - 32;
+  if (tid == cissuer)
     for (int p = z0; p < z0 + RF4; ++p) issue_fine(p);
-  int issued = jlo;     // thread 0: next coarse plane to issue
+  int issued = jlo;     // issuing thread: next coarse plane to issue
   auto issue_upto = [&](int live_lo) {   // thread 0
     for (; issued <= jtop && issued < live_lo + RQ4; ++issued) {
       const int sl = (issued - jlo) & (RQ4 - 1);
@@ -1639,7 +1646,7 @@ __global__ void __launch_bounds__(NTHR, 3) k_cubic4(const __grid_constant__ CUte
       tma3(sc + sl * PQ, &mc, cx0, cy0, issued, bar + sl);
     }
   };
-  if (tid == 0) issue_upto(jlo);
+  if (tid == cissuer) issue_upto(jlo);
   int waited = jlo;     // all threads: coarse planes [jlo, waited) have landed
   // ---- x taps of this thread's fine column
   const int gx = x0 + threadIdx.x;
@@ -1741,9 +1748,9 @@ __global__ void __launch_bounds__(NTHR, 3) k_cubic4(const __grid_constant__ CUte
       }
     }
     __syncthreads();
-    if (tid == 0 && t >= 2) issue_fine(ixp + RF4);   // x pass of ixp done: slot free
+    if (tid == cissuer && t >= 2) issue_fine(ixp + RF4);   // x pass of ixp done: slot free
     // coarse planes below the first taps of fine planes z0+t+1, z0+t+2 are dead
-    if (tid == 0) {
+    if (tid == cissuer) {
       int lo = jtop + 1;
       if (t + 1 < n) lo = min(lo, s_zj[(t + 1) * 4]);
       if (t + 2 < n) lo = min(lo, s_zj[(t + 2) * 4]);
