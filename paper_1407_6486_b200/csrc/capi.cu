@@ -306,8 +306,8 @@ int pl_set_option(int key, int value) {
     return 0;
   }
   if (key == PL_OPT_ZRB_RING) {
-    if (value < 0 || value > 2) {
-      set_error("zrb ring variant %d out of range (0..2)", value);
+    if (value < 0 || value > 3) {
+      set_error("zrb ring variant %d out of range (0..3)", value);
       return PL_ERR_ARG;
     }
     g_zrb_ring = value;

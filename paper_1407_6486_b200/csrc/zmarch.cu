@@ -819,7 +819,7 @@ __global__ void __launch_bounds__(HW ? 320 : NTHR_RB2, MINB) k_zrb3(const __grid
   const int z0 = blockIdx.z * zc, z1 = min(z0 + zc, g.nz);
   // the in-loop TMA issues go to the first lane of warp 7, which owns no
   // halo point, so the halo warps 0-1 are not delayed further after a barrier
-  constexpr int issuer = NTHR_RB2 - 32;
+  constexpr int issuer = HW ? 288 : NTHR_RB2 - 32;   // HW: halo warp 9 (one update per lane)
   k.z0 = z0;
   k.R = min(z1, g.nz - 1);
   const int uhi = k.R + 1, bhi = k.R;
@@ -1902,6 +1902,13 @@ int launch_zrb3(const double* u, const double* b, double* out, const Geo& g, con
   int zc = pick_zc(g);
   dim3 grid(ceil_div(g.nx, TX), ceil_div(g.ny, TY), ceil_div(g.nz, zc));
   const double dinv = 1.0 / dval;
+  if (g_zrb_ring == 3) {   // two dedicated halo warps (320 threads), 3 CTAs/SM
+    size_t smem = ((size_t)8 * PU + (size_t)4 * PB) * 8 + 8 * (8 + 4);
+    auto kern = c.pow2 ? k_zrb3<true, 8, 4, 3, true> : k_zrb3<false, 8, 4, 3, true>;
+    raise_smem(kern, smem);
+    kern<<<grid, dim3(320), smem, s>>>(mu, mb, out, g, c, sigma, omega, dval, dinv, zc);
+    return 0;
+  }
   if (g_zrb_ring == 2) {   // halo reds dealt to every warp, merged into the phase code
     size_t smem = ((size_t)8 * PU + (size_t)4 * PB) * 8 + 8 * (8 + 4);
     auto kern = c.pow2 ? k_zrb3<true, 8, 4, 3, false, true> : k_zrb3<false, 8, 4, 3, false, true>;
