@@ -11,14 +11,15 @@ GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
 
 @lru_cache(maxsize=None)
 def manifest():
-    """manifest.json (oracle/make_golden.py) merged with manifest_gsd.json
-    (oracle/make_golden_gs_direct.py: Gauss-Seidel and Direct cases)."""
+    """manifest.json (oracle/make_golden.py) merged with the manifest_*.json
+    of the other generators (make_golden_gs_direct.py: Gauss-Seidel and
+    Direct; make_golden_cfg3_full.py: full-size BASELINE config 3)."""
     with open(os.path.join(GOLDEN, "manifest.json")) as fh:
         man = json.load(fh)
-    extra = os.path.join(GOLDEN, "manifest_gsd.json")
-    if os.path.exists(extra):
-        with open(extra) as fh:
-            man["cases"].update(json.load(fh)["cases"])
+    for extra in sorted(os.listdir(GOLDEN)):   # manifest_gsd.json, manifest_cfg3_full.json
+        if extra.startswith("manifest_") and extra.endswith(".json"):
+            with open(os.path.join(GOLDEN, extra)) as fh:
+                man["cases"].update(json.load(fh)["cases"])
     return man
 
 

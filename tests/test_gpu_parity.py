@@ -11,6 +11,8 @@ bar (BASELINE.json north_star):
   * iteration counts, V-cycle counts (per run and per sub-step solve) and
     convergence flags are identical.
 """
+import math
+
 import numpy as np
 import pytest
 
@@ -701,3 +703,34 @@ def test_fused_presweep_residual_restriction(n, length, sigma, pre):
         _capi.set_option(_capi.OPT_ZMARCH, 1)
         _capi.set_option(_capi.OPT_RBRFW, 0)
         _capi.set_option(_capi.OPT_ZMARCH_MIN_N, 127)
+
+
+def test_cfg3_full_size_two_iterations():
+    """BASELINE config 3 at FULL size (255^3 / 127^3 / 63^3, 9 / 5 / 3 nodes,
+    jor-rb V(1,1), 8 time ranks) against the real reference's run with
+    max_iter = 2 (oracle/make_golden_cfg3_full.py; ~25 min and 47 GB on the
+    CPU): identical counts and convergence flags, fine residual trace and the
+    final field within the 1e-10 parity bound."""
+    import os
+    from tests.golden_io import GOLDEN
+    if not os.path.exists(os.path.join(GOLDEN, "cfg3_full_it2.npz")):
+        pytest.skip("full-size fixture not generated")
+    a, m = case("cfg3_full_it2")
+    cfg = mg.MgConfig("jor-rb", 1.0, 1, 1)
+    levels = [hierarchy.Level(heat.HeatOperator(heat.Grid(3, n)), quadrature.uniform_table(k - 1),
+                              cfg, mg.FixedCycles(1), space_interp_order=4)
+              for n, k in ((256, 9), (128, 5), (64, 3))]
+    u0 = heat.seeded_field(heat.Grid(3, 256))
+    res = pfasst.pfasst_run(levels, dev(u0), 8 / 64, 8, tol=1e-10, max_iter=2)
+    assert res.rank_iterations == m["rank_iterations"]
+    assert res.rank_vcycles == m["rank_vcycles"]
+    assert res.converged == m["converged"]
+    got = [[t.block, t.rank, t.iteration, t.level, t.vcycles] for t in res.trace]
+    assert got == [[r[0], r[1], r[2], r[3], r[5]] for r in m["trace"]]
+    floor = 1e-6 * float(np.max(np.abs(u0)))
+    for t, r in zip(res.trace, m["trace"]):
+        assert abs(t.residual - r[4]) <= 1e-10 * max(abs(r[4]), floor), (t, r)
+    u = res.u.cpu().numpy()
+    close(u[::16, ::16, ::16], a["sample"])
+    assert abs(float(np.max(np.abs(u))) - m["u_absmax"]) <= 1e-10 * m["u_absmax"]
+    assert abs(math.fsum(u.ravel().tolist()) - m["u_sum"]) <= 1e-10 * np.abs(u).sum()
