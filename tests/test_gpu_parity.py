@@ -727,10 +727,51 @@ def test_cfg3_full_size_two_iterations():
     assert res.converged == m["converged"]
     got = [[t.block, t.rank, t.iteration, t.level, t.vcycles] for t in res.trace]
     assert got == [[r[0], r[1], r[2], r[3], r[5]] for r in m["trace"]]
-    floor = 1e-6 * float(np.max(np.abs(u0)))
+    kappa = (1 / 64) * 4 * 3 * 256 ** 2        # dt |A_h|_inf, see test_pfasst_run_parity
+    floor = 4 * kappa * np.finfo(float).eps * float(np.max(np.abs(u0)))
     for t, r in zip(res.trace, m["trace"]):
-        assert abs(t.residual - r[4]) <= 1e-10 * max(abs(r[4]), floor), (t, r)
+        assert abs(t.residual - r[4]) <= 1e-10 * abs(r[4]) + floor, (t, r)
     u = res.u.cpu().numpy()
     close(u[::16, ::16, ::16], a["sample"])
+    assert abs(float(np.max(np.abs(u))) - m["u_absmax"]) <= 1e-10 * m["u_absmax"]
+    assert abs(math.fsum(u.ravel().tolist()) - m["u_sum"]) <= 1e-10 * np.abs(u).sum()
+
+
+@pytest.mark.parametrize("cycles", [1, 2])
+def test_cfg2_full_size(cycles):
+    """BASELINE config 2 at FULL size (1023^2 / 511^2, 5 / 3 nodes, Jacobi
+    V(2,2), 8 time ranks, 20 iterations) against the real reference
+    (oracle/make_golden_cfg2_full.py): identical iteration / V-cycle counts and
+    convergence flags, residual trace and final field within the 1e-10
+    parity bound."""
+    import os
+    from tests.golden_io import GOLDEN
+    if not os.path.exists(os.path.join(GOLDEN, "cfg2_full.npz")):
+        pytest.skip("full-size fixture not generated")
+    from tests.golden_io import manifest
+    m = manifest()["cases"][f"cfg2_full_fc{cycles}"]
+    with np.load(os.path.join(GOLDEN, "cfg2_full.npz")) as z:
+        a = {k: z[k] for k in z.files}
+    cfg = mg.MgConfig("jacobi", 2.0 / 3.0, 2, 2)
+    levels = [hierarchy.Level(heat.HeatOperator(heat.Grid(2, n)), quadrature.uniform_table(k - 1),
+                              cfg, mg.FixedCycles(cycles), space_interp_order=4)
+              for n, k in ((1024, 5), (512, 3))]
+    u0 = heat.seeded_field(heat.Grid(2, 1024))
+    res = pfasst.pfasst_run(levels, dev(u0), 8 / 64, 8, tol=1e-10, max_iter=20)
+    assert res.rank_iterations == m["rank_iterations"]
+    assert res.rank_vcycles == m["rank_vcycles"]
+    assert res.converged == m["converged"]
+    got = [[t.block, t.rank, t.iteration, t.level, t.vcycles] for t in res.trace]
+    assert got == [[r[0], r[1], r[2], r[3], r[5]] for r in m["trace"]]
+    # residual floor 4 kappa eps |u0| (test_pfasst_run_parity): a residual is
+    # a difference of O(|u|) terms, kappa = dt |A_h|_inf = (1/64) 4 d 1024^2
+    kappa = (1 / 64) * 4 * 2 * 1024 ** 2
+    floor = 4 * kappa * np.finfo(float).eps * float(np.max(np.abs(u0)))
+    worst = 0.0
+    for t, r in zip(res.trace, m["trace"]):
+        assert abs(t.residual - r[4]) <= 1e-10 * abs(r[4]) + floor, (t, r)
+        worst = max(worst, abs(t.residual - r[4]))
+    u = res.u.cpu().numpy()
+    close(u[::8, ::8], a[f"cfg2_full_fc{cycles}_sample"])
     assert abs(float(np.max(np.abs(u))) - m["u_absmax"]) <= 1e-10 * m["u_absmax"]
     assert abs(math.fsum(u.ravel().tolist()) - m["u_sum"]) <= 1e-10 * np.abs(u).sum()
