@@ -204,6 +204,10 @@ def test_gs_direct_kernels(name):
     s = m["sigma"]
     cfg = O.Mg("gauss-seidel")
     eq(O.smooth(op, s, a["u"], a["b"], cfg, 1), a["gs1"])
+    if m["dim"] == 3 and m["n"] >= 32:
+        # the scipy banded Gauss-Seidel at 31^3 takes ~1 min per case on the
+        # CPU; one sweep pins the oracle here, the GPU test checks every array
+        return
     eq(O.smooth(op, s, a["u"], a["b"], cfg, 2), a["gs2"])
     eq(O.v_cycle(op, s, a["u"], a["b"], cfg), a["vc22"])
     eq(O.v_cycle(op, s, np.zeros_like(a["b"]), a["b"], O.Mg("gauss-seidel", 2 / 3, 1, 1)),
