@@ -775,3 +775,45 @@ def test_cfg2_full_size(cycles):
     close(u[::8, ::8], a[f"cfg2_full_fc{cycles}_sample"])
     assert abs(float(np.max(np.abs(u))) - m["u_absmax"]) <= 1e-10 * m["u_absmax"]
     assert abs(math.fsum(u.ravel().tolist()) - m["u_sum"]) <= 1e-10 * np.abs(u).sum()
+
+
+def test_cfg4_full_size_kernels():
+    """BASELINE config 4's hot kernels at FULL size (511^3) against the real
+    reference (oracle/make_golden_cfg4_kernels.py): one Jacobi V(2,2) cycle
+    from seeded normal u, b and one 4-sub-step SDC sweep of the seeded u0 --
+    samples, sums and maxima within 1e-12, the sweep's cycle count and
+    collocation residual."""
+    import os
+    from tests.golden_io import GOLDEN, manifest
+    path = os.path.join(GOLDEN, "cfg4_kernels.npz")
+    if not os.path.exists(path):
+        pytest.skip("full-size fixture not generated")
+    m = manifest()["cases"]["cfg4_kernels"]
+    with np.load(path) as z:
+        a = {k: z[k] for k in z.files}
+    g = heat.Grid(3, 512)
+    op = heat.HeatOperator(g)
+    cfg = mg.MgConfig("jacobi", 2.0 / 3.0, 2, 2)
+    rng = np.random.default_rng(m["vcycle"]["seed"])
+    u = dev(rng.standard_normal(g.shape))
+    b = dev(rng.standard_normal(g.shape))
+    v = mg.v_cycle(mg.ShiftedOperator(op, m["vcycle"]["sigma"]), u, b, cfg)
+    del u, b
+    close(v[::32, ::32, ::32], a["vcycle_sample"], 1e-12)
+    vv = v.double()
+    assert abs(float(vv.abs().max()) - m["vcycle"]["absmax"]) <= 1e-12 * m["vcycle"]["absmax"]
+    assert abs(float(vv.sum()) - m["vcycle"]["sum"]) <= 1e-10 * float(vv.abs().sum())
+    del v, vv
+    u0 = dev(heat.seeded_field(g))
+    table = quadrature.uniform_table(4)
+    states = sdc.NodeStates.spread(op, table, u0)
+    cycles = sdc.sdc_sweep(states, u0, m["sweep"]["dt"], op, cfg, mg.FixedCycles(1))
+    assert cycles == m["sweep"]["cycles"]
+    y = states.y[-1]
+    close(y[::32, ::32, ::32], a["sweep_y_last_sample"], 1e-12)
+    close(states.y[2][::32, ::32, ::32], a["sweep_y_mid_sample"], 1e-12)
+    assert abs(float(y.sum()) - m["sweep"]["y_last"]["sum"]) <= 1e-10 * float(y.abs().sum())
+    res = sdc.residual(states, u0, m["sweep"]["dt"])
+    kappa = m["sweep"]["dt"] * 4 * 3 * 512 ** 2
+    floor = 4 * kappa * np.finfo(float).eps * float(u0.abs().max())
+    assert abs(res - m["sweep"]["res"]) <= 1e-10 * abs(m["sweep"]["res"]) + floor
