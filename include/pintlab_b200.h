@@ -94,6 +94,9 @@ const char* pl_last_error(void);
                                  run as one overlapped-tile pass (TMA levels); 0 (default,
                                  measured faster): k_zrb3 then k_rfw; bit-identical */
 #define PL_OPT_RBRFW_ZCC 16   /* smallest coarse-plane z chunk of the fused pass (default 16) */
+#define PL_OPT_FUSE_APPLY_RHS 17 /* 1 (default): the sweep's f refresh of node m and the next
+                                    sub-step's right-hand side share one pass over y[m] (TMA
+                                    levels); 0: separate apply and rhs launches; bit-identical */
 int pl_set_option(int key, int value);
 
 /* storage elements of one field (incl. row pads) */

@@ -150,6 +150,7 @@ OPT_MID_CTAS = 13
 OPT_ZRB_RING = 14
 OPT_RBRFW = 15
 OPT_RBRFW_ZCC = 16
+OPT_FUSE_APPLY_RHS = 17
 
 
 _OPTION_VALUES = {}      # options set through this module (the library defaults otherwise)

@@ -83,7 +83,7 @@ void timing_post(int kind, cudaStream_t s, double alg_bytes) {
 static const char* kKindNames[K_NUM_KINDS] = {
     "apply", "jacobi", "jor_rb", "residual", "restrict", "prolong", "mg_tail", "norm",
     "quadrature", "rhs", "residual_max", "fas", "correction_time", "interp_cubic", "copy",
-    "lu", "mg_mid", "gauss_seidel", "direct", "jor_rb_restrict"};
+    "lu", "mg_mid", "gauss_seidel", "direct", "jor_rb_restrict", "apply_rhs"};
 
 // ---------------------------------------------------------------------------
 // SDC sweep (sdc.py:84-114)
@@ -128,14 +128,18 @@ static int sdc_sweep(MgPlan* P, const pl_sweep_desc* d, double* Y, double* F, co
     if (e != cudaSuccess) return cuda_status(e, "y0 copy");
     count_launch(K_COPY, 16.0 * L.g.npts);
   }
-  PL_TRY(launch_apply(Y, F, L.g, L.c, s));
+  // f[m] = A y[m] fused with the right-hand side of sub-step m (sdc.py:102-104,
+  // 112): both read y[m]; rhs reads the OLD f[m+1], which the fusion leaves alone
+  auto refresh_rhs = [&](int m) {
+    return launch_apply_rhs(Y + (size_t)m * np, F + (size_t)m * np, F + (size_t)(m + 1) * np,
+                            S + (size_t)m * np, tau ? tau + (size_t)m * np : nullptr,
+                            tau ? tau + (size_t)(m + 1) * np : nullptr, dtm[m], R, np, L.g,
+                            L.c, s);
+  };
+  PL_TRY(refresh_rhs(0));
   int total = 0;
   for (int m = 0; m < M; ++m) {
-    double* ym = Y + (size_t)m * np;
     double* ym1 = Y + (size_t)(m + 1) * np;
-    PL_TRY(launch_rhs(ym, F + (size_t)(m + 1) * np, S + (size_t)m * np,
-                      tau ? tau + (size_t)m * np : nullptr,
-                      tau ? tau + (size_t)(m + 1) * np : nullptr, dtm[m], R, np, s));
     if (d->policy == 0) {
       PL_TRY(mg_cycles(P, ym1, R, dtm[m], d->fixed_cycles, 0, s));
       total += d->fixed_cycles;
@@ -155,7 +159,8 @@ static int sdc_sweep(MgPlan* P, const pl_sweep_desc* d, double* Y, double* F, co
       if (rc) return rc;
       total += c;
     }
-    PL_TRY(launch_apply(ym1, F + (size_t)(m + 1) * np, L.g, L.c, s));   // sdc.py:112
+    if (m + 1 < M) PL_TRY(refresh_rhs(m + 1));
+    else PL_TRY(launch_apply(ym1, F + (size_t)(m + 1) * np, L.g, L.c, s));   // sdc.py:112
   }
   *cycles = total;
   return 0;
@@ -331,6 +336,10 @@ int pl_set_option(int key, int value) {
   }
   if (key == PL_OPT_FUSE_PROLONG) {
     g_fuse_prolong = value != 0;
+    return 0;
+  }
+  if (key == PL_OPT_FUSE_APPLY_RHS) {
+    g_fuse_apply_rhs = value != 0;
     return 0;
   }
   if (key == PL_OPT_ZMARCH_MIN_N) {

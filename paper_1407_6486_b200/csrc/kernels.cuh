@@ -36,6 +36,15 @@ bool zmarch_enabled();
 bool zmarch_size_ok(int N);
 bool zmarch_fuse_prolong();   // PL_OPT_FUSE_PROLONG
 int zlaunch_apply(const double* u, double* f, const Geo& g, const OpC& c, cudaStream_t s);
+int zlaunch_apply_rhs(const double* u, double* f, const double* fnext, const double* sm,
+                      const double* tau0, const double* tau1, double dtm, double* rhs,
+                      const Geo& g, const OpC& c, cudaStream_t s);
+// f = A u, then rhs = (u - dtm fnext) + sm (+ (tau1 - tau0)): fused on TMA grids
+// (PL_OPT_FUSE_APPLY_RHS), two launches otherwise
+int launch_apply_rhs(const double* u, double* f, const double* fnext, const double* sm,
+                     const double* tau0, const double* tau1, double dtm, double* rhs,
+                     long long np, const Geo& g, const OpC& c, cudaStream_t s);
+extern int g_fuse_apply_rhs;
 int zlaunch_residual(const double* u, const double* b, double* r, const Geo& g, const OpC& c,
                      double sigma, cudaStream_t s);
 int zlaunch_jacobi(const double* u, const double* b, double* out, const Geo& g, const OpC& c,

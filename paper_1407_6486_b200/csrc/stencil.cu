@@ -172,6 +172,17 @@ int launch_apply(const double* u, double* f, const Geo& g, const OpC& c, cudaStr
   return 0;
 }
 
+int g_fuse_apply_rhs = 1;   // PL_OPT_FUSE_APPLY_RHS
+
+int launch_apply_rhs(const double* u, double* f, const double* fnext, const double* sm,
+                     const double* tau0, const double* tau1, double dtm, double* rhs,
+                     long long np, const Geo& g, const OpC& c, cudaStream_t s) {
+  if (g_fuse_apply_rhs && zmarch_ok(g, c))
+    return zlaunch_apply_rhs(u, f, fnext, sm, tau0, tau1, dtm, rhs, g, c, s);
+  PL_TRY(launch_apply(u, f, g, c, s));
+  return launch_rhs(u, fnext, sm, tau0, tau1, dtm, rhs, np, s);
+}
+
 int launch_residual(const double* u, const double* b, double* r, const Geo& g, const OpC& c,
                     double sigma, cudaStream_t s) {
   if (zmarch_ok(g, c)) return zlaunch_residual(u, b, r, g, c, sigma, s);

@@ -104,7 +104,18 @@ __device__ __forceinline__ double lap7(const double* pm, const double* pc, const
   return c.nu * acc;
 }
 
-enum { Z_APPLY = 0, Z_RESID = 1, Z_JAC = 2, Z_JAC0 = 3 };
+enum { Z_APPLY = 0, Z_RESID = 1, Z_JAC = 2, Z_JAC0 = 3, Z_APPLY_RHS = 4 };
+
+// Z_APPLY_RHS epilogue operands: the next sub-step's right-hand side
+// r = (y - dtm f_next) + s (+ (t1 - t0)) from the same u plane (sdc.py:102-104)
+struct RhsArgs {
+  const double* fn;
+  const double* s;
+  const double* t0;
+  const double* t1;
+  double* r;
+  double dtm;
+};
 
 // ---- shared machinery of the halo-2 kernels -------------------------------
 
@@ -212,11 +223,12 @@ template <int OP, bool POW2, int PREF>
 __global__ void __launch_bounds__(NTHR) k_z1(const __grid_constant__ CUtensorMap mu,
                                              const __grid_constant__ CUtensorMap mb,
                                              double* __restrict__ out, Geo g, OpC c,
-                                             double sigma, double omega, double dval, int zc) {
+                                             double sigma, double omega, double dval, int zc,
+                                             RhsArgs ra) {
   constexpr int HX = TX + 4, HY = TY + 2, P1 = align16(HX * HY), P0 = align16(TX * TY);
   constexpr int RING = PREF + 3;
   constexpr bool NEED_U = OP != Z_JAC0;
-  constexpr bool NEED_B = OP != Z_APPLY;
+  constexpr bool NEED_B = OP != Z_APPLY && OP != Z_APPLY_RHS;
   extern __shared__ __align__(128) double sm[];
   double* su = sm;
   double* sb = sm + (NEED_U ? RING * P1 : 0);
@@ -253,7 +265,28 @@ __global__ void __launch_bounds__(NTHR) k_z1(const __grid_constant__ CUtensorMap
   wait(z0 - 1);
   wait(z0);
   const int gx = x0 + threadIdx.x;
+  // Z_APPLY_RHS: f_next, s (and tau) of plane z+1 are loaded into registers
+  // while plane z computes, so their DRAM latency overlaps a whole plane
+  constexpr bool RHS = OP == Z_APPLY_RHS;
+  constexpr int NR = RHS ? 2 : 1;
+  double cf[NR], cs[NR], ct[NR];
+  auto rhs_load = [&](int z, double* f, double* sv, double* t) {
+#pragma unroll
+    for (int r = 0; r < NR; ++r) {
+      const int gy = y0 + threadIdx.y + 8 * r;
+      f[r] = sv[r] = t[r] = 0.0;
+      if (z < z1 && gx < g.nx && gy < g.ny) {
+        const long long gi = g.at(gx, gy, z);
+        f[r] = __ldcs(ra.fn + gi);
+        sv[r] = __ldcs(ra.s + gi);
+        if (ra.t0) t[r] = __ldcs(ra.t1 + gi) - __ldcs(ra.t0 + gi);
+      }
+    }
+  };
+  if constexpr (RHS) rhs_load(z0, cf, cs, ct);
   for (int z = z0; z < z1; ++z) {
+    double nf[NR], ns[NR], nt[NR];
+    if constexpr (RHS) rhs_load(z + 1, nf, ns, nt);
     wait(z + 1);
     const int sc = (z - z0 + 1) % RING;
     const double* pc = su + sc * P1;
@@ -266,8 +299,15 @@ __global__ void __launch_bounds__(NTHR) k_z1(const __grid_constant__ CUtensorMap
       const int gy = y0 + ly;
       if (gx < g.nx && gy < g.ny) {
         const int i = (ly + 1) * HX + threadIdx.x + 2;
+        const long long gi = g.at(gx, gy, z);
         double v;
-        if (OP == Z_JAC0) {
+        if constexpr (OP == Z_APPLY_RHS) {
+          // sdc.py:112 f refresh of this node, then sdc.py:102-104 for the next
+          double rr = (pc[i] - ra.dtm * cf[r & (NR - 1)]) + cs[r & (NR - 1)];
+          if (ra.t0) rr = rr + ct[r & (NR - 1)];
+          ra.r[gi] = rr;
+          v = lap7<POW2, HX>(pm, pc, pp, i, c);
+        } else if (OP == Z_JAC0) {
           v = 0.0 + ((omega * pb[ly * TX + threadIdx.x]) / dval);
         } else {
           double lap = lap7<POW2, HX>(pm, pc, pp, i, c);
@@ -279,11 +319,19 @@ __global__ void __launch_bounds__(NTHR) k_z1(const __grid_constant__ CUtensorMap
             v = OP == Z_RESID ? bb - au : pc[i] + ((omega * (bb - au)) / dval);
           }
         }
-        out[g.at(gx, gy, z)] = v;
+        out[gi] = v;
       }
     }
     __syncthreads();   // slot of plane z-1 is free
     if (tid == 0) issue(z + PREF + 1);
+    if constexpr (RHS) {
+#pragma unroll
+      for (int r = 0; r < NR; ++r) {
+        cf[r] = nf[r];
+        cs[r] = ns[r];
+        ct[r] = nt[r];
+      }
+    }
   }
 }
 
@@ -1820,22 +1868,23 @@ void raise_smem(K kern, size_t bytes) {
 
 template <int OP>
 int launch_z1(const double* u, const double* b, double* out, const Geo& g, const OpC& c,
-              double sigma, double omega, double dval, cudaStream_t s) {
+              double sigma, double omega, double dval, cudaStream_t s,
+              const RhsArgs& ra = RhsArgs{}) {
   constexpr int HX = TX + 4, HY = TY + 2, RING = PREF1 + 3;
   CUtensorMap mu, mb;
   std::memset(&mu, 0, sizeof(mu));
   std::memset(&mb, 0, sizeof(mb));
   if (OP != Z_JAC0) PL_TRY(make_map(&mu, u, g, HX, HY));
-  if (OP != Z_APPLY) PL_TRY(make_map(&mb, b, g, TX, TY));
+  constexpr bool NB = OP != Z_APPLY && OP != Z_APPLY_RHS;
+  if (NB) PL_TRY(make_map(&mb, b, g, TX, TY));
   size_t smem = sizeof(double) * RING *
-                    ((OP != Z_JAC0 ? align16(HX * HY) : 0) +
-                     (OP != Z_APPLY ? align16(TX * TY) : 0)) +
+                    ((OP != Z_JAC0 ? align16(HX * HY) : 0) + (NB ? align16(TX * TY) : 0)) +
                 8 * RING;
   int zc = pick_zc(g);
   dim3 grid(ceil_div(g.nx, TX), ceil_div(g.ny, TY), ceil_div(g.nz, zc)), block(32, 8);
   auto kern = c.pow2 ? k_z1<OP, true, PREF1> : k_z1<OP, false, PREF1>;
   raise_smem(kern, smem);
-  kern<<<grid, block, smem, s>>>(mu, mb, out, g, c, sigma, omega, dval, zc);
+  kern<<<grid, block, smem, s>>>(mu, mb, out, g, c, sigma, omega, dval, zc, ra);
   return 0;
 }
 
@@ -2059,6 +2108,18 @@ int zlaunch_apply(const double* u, double* f, const Geo& g, const OpC& c, cudaSt
   PL_PRE(K_APPLY);
   PL_TRY(launch_z1<Z_APPLY>(u, nullptr, f, g, c, 0.0, 0.0, 1.0, s));
   PL_CHECK_LAUNCH(K_APPLY, 16.0 * g.npts);
+  return 0;
+}
+
+int zlaunch_apply_rhs(const double* u, double* f, const double* fnext, const double* sm,
+                      const double* tau0, const double* tau1, double dtm, double* rhs,
+                      const Geo& g, const OpC& c, cudaStream_t s) {
+  RhsArgs ra{fnext, sm, tau0, tau1, rhs, dtm};
+  PL_PRE(K_APPLY_RHS);
+  PL_TRY(launch_z1<Z_APPLY_RHS>(u, nullptr, f, g, c, 0.0, 0.0, 1.0, s, ra));
+  // the unfused passes it replaces: apply (16 B) + rhs (32 B, 48 B with tau),
+  // minus the shared read of u
+  PL_CHECK_LAUNCH(K_APPLY_RHS, (tau0 ? 56.0 : 40.0) * g.npts);
   return 0;
 }
 

@@ -817,3 +817,34 @@ def test_cfg4_full_size_kernels():
     kappa = m["sweep"]["dt"] * 4 * 3 * 512 ** 2
     floor = 4 * kappa * np.finfo(float).eps * float(u0.abs().max())
     assert abs(res - m["sweep"]["res"]) <= 1e-10 * abs(m["sweep"]["res"]) + floor
+
+
+@pytest.mark.parametrize("n,with_tau", [(32, True), (128, False), (128, True), (256, False)])
+@pytest.mark.parametrize("policy", ["fixed", "tol"])
+def test_sweep_fused_apply_rhs_equals_separate(n, with_tau, policy):
+    """The sweep's f refresh fused with the next sub-step's right-hand side
+    (one pass over y[m], PL_OPT_FUSE_APPLY_RHS) leaves y, f and the V-cycle
+    count bit-identical to the separate apply and rhs launches."""
+    from paper_1407_6486_b200 import quadrature, sdc
+    rng = np.random.default_rng(n + 3 * with_tau)
+    g = heat.Grid(3, n)
+    op = heat.HeatOperator(g)
+    table = quadrature.uniform_table(4)
+    u0 = dev(rng.standard_normal(g.shape))
+    tau = dev(rng.standard_normal((5,) + g.shape) * 1e-3) if with_tau else None
+    cfg = mg.MgConfig("jor-rb", 1.0, 1, 1)
+    pol = mg.FixedCycles(1) if policy == "fixed" else mg.ToTolerance(1e-9, 0.75, 40)
+    outs = []
+    _capi.set_option(_capi.OPT_ZMARCH_MIN_N, 31)
+    try:
+        for fuse in (0, 1):
+            _capi.set_option(_capi.OPT_FUSE_APPLY_RHS, fuse)
+            st = sdc.NodeStates.spread(op, table, u0)
+            cyc = [sdc.sdc_sweep(st, u0, 1.0 / 64, op, cfg, pol, tau) for _ in range(2)]
+            outs.append((st.y, st.f, cyc))   # kept alive: distinct graph-cache keys
+    finally:
+        _capi.set_option(_capi.OPT_FUSE_APPLY_RHS, 1)
+        _capi.set_option(_capi.OPT_ZMARCH_MIN_N, 127)
+    assert outs[0][2] == outs[1][2]
+    assert torch.equal(outs[0][0], outs[1][0])
+    assert torch.equal(outs[0][1], outs[1][1])
