@@ -97,6 +97,8 @@ const char* pl_last_error(void);
 #define PL_OPT_FUSE_APPLY_RHS 17 /* 1 (default): the sweep's f refresh of node m and the next
                                     sub-step's right-hand side share one pass over y[m] (TMA
                                     levels); 0: separate apply and rhs launches; bit-identical */
+#define PL_OPT_RFW_THREADS 18  /* threads of the residual + full-weighting kernel: 288 (default;
+                                  at most two residual points per thread) or 256 */
 int pl_set_option(int key, int value);
 
 /* storage elements of one field (incl. row pads) */

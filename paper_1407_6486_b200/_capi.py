@@ -151,6 +151,7 @@ OPT_ZRB_RING = 14
 OPT_RBRFW = 15
 OPT_RBRFW_ZCC = 16
 OPT_FUSE_APPLY_RHS = 17
+OPT_RFW_THREADS = 18
 
 
 _OPTION_VALUES = {}      # options set through this module (the library defaults otherwise)

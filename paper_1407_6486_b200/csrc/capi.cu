@@ -239,6 +239,7 @@ extern int g_mid_ctas;
 extern int g_zrb_ring;
 extern int g_rbrfw_enabled;
 extern int g_rbrfw_zcc;
+extern int g_rfw_threads;
 }
 
 extern "C" {
@@ -336,6 +337,14 @@ int pl_set_option(int key, int value) {
   }
   if (key == PL_OPT_FUSE_PROLONG) {
     g_fuse_prolong = value != 0;
+    return 0;
+  }
+  if (key == PL_OPT_RFW_THREADS) {
+    if (value != 256 && value != 288) {
+      set_error("k_rfw threads must be 256 or 288");
+      return PL_ERR_ARG;
+    }
+    g_rfw_threads = value;
     return 0;
   }
   if (key == PL_OPT_FUSE_APPLY_RHS) {

@@ -742,9 +742,11 @@ __device__ __forceinline__ Relax rb_fast(const RbCtx& k, double zm, double zp, d
   o.q = __fma_rn(e, k.dinv, q);
   return o;
 }
+// 2^-960 <= |a| < 2^960 from the biased exponent (integer pipe; both paths
+// are correctly rounded, so the exact cut only picks the method)
 __device__ __forceinline__ bool quot_ok(double a) {
-  const double aa = fabs(a);
-  return aa >= 0x1p-960 && aa <= 0x1p960;
+  const unsigned e = ((unsigned)__double2hiint(a) >> 20) & 0x7ffu;
+  return e - 63u <= 1919u;
 }
 template <bool POW2, int O>
 __device__ __forceinline__ Relax rb_point_fast(const RbCtx& k, const double* pl,
@@ -788,7 +790,7 @@ __device__ __forceinline__ void rb_halo(const RbCtx& k, int q) {
 template <bool POW2, int RU, int RB, int PAR>
 __device__ __forceinline__ void rb_phase(const RbCtx& k, int z, const double2& U0, double2& U1,
                                          const double2& U2, double2& U3, const double2& U4,
-                                         const double2& B0, const double2& B2) {
+                                         const double2& B0, const double2& B2, double* dst) {
   const int q = z + 2;
   double* plr = rb_u<RU>(k, q);
   const double* plb = rb_u<RU>(k, z);
@@ -803,9 +805,8 @@ __device__ __forceinline__ void rb_phase(const RbCtx& k, int z, const double2& U
     plr[k.iu + 1 - PAR] = vr;
     set_mem<1 - PAR>(U3, vr);
   }
-  double* dst = k.optr + (long long)z * k.sz;
   const double2 w = PAR ? make_double2(U1.x, vb) : make_double2(vb, U1.y);
-  if (k.va && k.vb) *reinterpret_cast<double2*>(dst) = w;
+  if (k.vb) *reinterpret_cast<double2*>(dst) = w;   // vb implies va
   else if (k.va) dst[0] = w.x;
 }
 
@@ -1004,7 +1005,8 @@ __global__ void __launch_bounds__(HW ? 320 : NTHR_RB2, MINB) k_zrb3(const __grid
   // B0, B1 = b pair on z, z+1
   auto run = [&](auto par_tag) {
     constexpr int PA = decltype(par_tag)::value, PB = 1 - PA;
-    for (int z = z0; z < z1; z += 2) {
+    double* dst = k.optr + (long long)z0 * k.sz;   // own pair on plane z
+    for (int z = z0; z < z1; z += 2, dst += 2 * k.sz) {
       // plane z (parity PA)
       if (z + 2 <= k.R) {
         wait_u(z + 3);
@@ -1015,7 +1017,7 @@ __global__ void __launch_bounds__(HW ? 320 : NTHR_RB2, MINB) k_zrb3(const __grid
       if (HM) {
         rb_phase_h<POW2, RU, RB, PA, 0>(k, z, U0, U1, U2, U3, U4, B0, B2);
       } else {
-        if (is_int) rb_phase<POW2, RU, RB, PA>(k, z, U0, U1, U2, U3, U4, B0, B2);
+        if (is_int) rb_phase<POW2, RU, RB, PA>(k, z, U0, U1, U2, U3, U4, B0, B2, dst);
         if (is_halo) rb_halo<POW2, RU, RB, 0>(k, z + 2);
       }
       __syncthreads();
@@ -1034,7 +1036,7 @@ __global__ void __launch_bounds__(HW ? 320 : NTHR_RB2, MINB) k_zrb3(const __grid
       if (HM) {
         rb_phase_h<POW2, RU, RB, PB, 1>(k, z + 1, U1, U2, U3, U4, U5, B1, B3);
       } else {
-        if (is_int) rb_phase<POW2, RU, RB, PB>(k, z + 1, U1, U2, U3, U4, U5, B1, B3);
+        if (is_int) rb_phase<POW2, RU, RB, PB>(k, z + 1, U1, U2, U3, U4, U5, B1, B3, dst + k.sz);
         if (is_halo) rb_halo<POW2, RU, RB, 1>(k, z + 3);
       }
       __syncthreads();
@@ -1215,8 +1217,10 @@ constexpr int FUX = TX + 4, FUY = TY + 3, PFU = align16(FUX * FUY);  // u window
 constexpr int FBX = TX + 2, FBY = TY + 1, PFB = align16(FBX * FBY);  // b window
 constexpr int RFW_RU = 5, RFW_RB = 3;
 
-template <bool POW2>
-__global__ void __launch_bounds__(NTHR, 4) k_rfw(const __grid_constant__ CUtensorMap mu,
+// NT = 288 (nine warps): the 561 residual points of the window are at most
+// two per thread, so no warp carries a third residual chain per plane
+template <bool POW2, int NT>
+__global__ void __launch_bounds__(NT, 4) k_rfw(const __grid_constant__ CUtensorMap mu,
                                                  const __grid_constant__ CUtensorMap mb,
                                                  double* __restrict__ coarse, Geo gf, Geo gc,
                                                  OpC c, double sigma, int zcc) {
@@ -1228,7 +1232,7 @@ __global__ void __launch_bounds__(NTHR, 4) k_rfw(const __grid_constant__ CUtenso
   unsigned long long* bu = (unsigned long long*)(syx + PR);
   unsigned long long* bb = bu + RFW_RU;
   const int tid = threadIdx.y * 32 + threadIdx.x;
-  constexpr int rfw_issuer = NTHR - 32;
+  constexpr int rfw_issuer = NT - 32;
   const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TY;
   const int jz0 = blockIdx.z * zcc, jz1 = min(jz0 + zcc, gc.nz);
   const int p0 = 2 * jz0, p1 = 2 * jz1;       // residual planes p0 .. p1
@@ -1264,12 +1268,12 @@ __global__ void __launch_bounds__(NTHR, 4) k_rfw(const __grid_constant__ CUtenso
     for (int p = p0; p < p0 + RFW_RB; ++p) issue_b(p);
   }
   // owned residual points: window index k -> u / b window offsets
-  constexpr int PERR = (RX * RY + NTHR - 1) / NTHR;
+  constexpr int PERR = (RX * RY + NT - 1) / NT;
   int r_k[PERR], r_iu[PERR], r_ib[PERR];
   bool r_ok[PERR];
 #pragma unroll
   for (int q = 0; q < PERR; ++q) {
-    const int k = tid + q * NTHR;
+    const int k = tid + q * NT;
     const int ry = k / RX, rx = k - ry * RX;
     r_k[q] = k < RX * RY ? k : -1;
     r_iu[q] = (ry + 1) * FUX + rx + 2;
@@ -1315,7 +1319,7 @@ __global__ void __launch_bounds__(NTHR, 4) k_rfw(const __grid_constant__ CUtenso
       }
     }
     if ((ph & 1) == 1 && ph >= 3) {                    // y pass of jz = (p - 3) / 2
-      for (int k = tid; k < RX * (TY / 2); k += NTHR) {
+      for (int k = tid; k < RX * (TY / 2); k += NT) {
         const int yy = k / RX, xx = k - yy * RX;
         const double* zc = szb + 2 * yy * RX + xx;
         syx[k] = fw3(zc[0], zc[RX], zc[2 * RX]);
@@ -1847,6 +1851,7 @@ int make_map(CUtensorMap* m, const double* base, const Geo& g, int bw, int bh) {
 }
 
 }  // namespace
+int g_rfw_threads = 288;   // PL_OPT_RFW_THREADS: 256 (eight warps) or 288 (nine, default)
 int g_zc_floor = 16;  // PL_OPT_ZC_FLOOR (A/B): smallest z chunk (4 and 8 measured slower at 127^3)
 int g_zc_ctas = 148 * 8;   // PL_OPT_ZC_CTAS (A/B): CTA count the z chunking aims for
 namespace {
@@ -1986,9 +1991,11 @@ int launch_rfw(const double* u, const double* b, double* coarse, const Geo& g, c
   PL_TRY(make_map(&mu, u, g, FUX, FUY));
   PL_TRY(make_map(&mb, b, g, FBX, FBY));
   const int zcc = pick_zc(g) / 2 < 4 ? 4 : pick_zc(g) / 2;
-  dim3 grid(ceil_div(g.nx, TX), ceil_div(g.ny, TY), ceil_div(gc.nz, zcc)), block(32, 8);
+  const int nt = g_rfw_threads == 256 ? 256 : 288;
+  dim3 grid(ceil_div(g.nx, TX), ceil_div(g.ny, TY), ceil_div(gc.nz, zcc)), block(32, nt / 32);
   size_t smem = sizeof(double) * (RFW_RU * PFU + RFW_RB * PFB + 2 * PR) + 8 * (RFW_RU + RFW_RB);
-  auto kern = c.pow2 ? k_rfw<true> : k_rfw<false>;
+  auto kern = nt == 256 ? (c.pow2 ? k_rfw<true, 256> : k_rfw<false, 256>)
+                        : (c.pow2 ? k_rfw<true, 288> : k_rfw<false, 288>);
   raise_smem(kern, smem);
   kern<<<grid, block, smem, s>>>(mu, mb, coarse, g, gc, c, sigma, zcc);
   return 0;

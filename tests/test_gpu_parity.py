@@ -848,3 +848,24 @@ def test_sweep_fused_apply_rhs_equals_separate(n, with_tau, policy):
     assert outs[0][2] == outs[1][2]
     assert torch.equal(outs[0][0], outs[1][0])
     assert torch.equal(outs[0][1], outs[1][1])
+
+
+@pytest.mark.parametrize("n,sigma", [(128, 1.0 / 128), (256, 0.37)])
+@pytest.mark.parametrize("threads", [256, 288])
+def test_rfw_thread_layouts_equal_plain_kernels(n, sigma, threads):
+    """The fused residual + full-weighting kernel with eight or nine warps
+    gives the plain kernels' V-cycle (residual, then full weighting) bit for bit."""
+    rng = np.random.default_rng(n + threads)
+    g = heat.Grid(3, n)
+    u = dev(rng.standard_normal(g.shape))
+    b = dev(rng.standard_normal(g.shape))
+    sop = mg.ShiftedOperator(heat.HeatOperator(g), sigma)
+    cfg = mg.MgConfig("jor-rb", 1.0, 1, 1)
+    _capi.set_option(_capi.OPT_RFW, 0)
+    ref = mg.v_cycle(sop, u, b, cfg)
+    _capi.set_option(_capi.OPT_RFW, 1)
+    _capi.set_option(_capi.OPT_RFW_THREADS, threads)
+    try:
+        assert torch.equal(mg.v_cycle(sop, u, b, cfg), ref)
+    finally:
+        _capi.set_option(_capi.OPT_RFW_THREADS, 288)
