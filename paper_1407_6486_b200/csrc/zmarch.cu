@@ -1268,21 +1268,30 @@ __global__ void __launch_bounds__(NT, 4) k_rfw(const __grid_constant__ CUtensorM
     for (int p = p0; p < p0 + RFW_RB; ++p) issue_b(p);
   }
   // owned residual points: window index k -> u / b window offsets
+  // NT = 288: row-aligned ownership -- warp w owns row w (q = 0) and row w + 9
+  // (q = 1) of x0..x0+31, warp 8 lanes 0..16 the last column x0+32 -- so a
+  // warp's loads are 32 consecutive doubles (no bank conflicts at row wraps)
   constexpr int PERR = (RX * RY + NT - 1) / NT;
+  static_assert(NT != 288 || (PERR == 2 && RY == 17 && RX == 33), "row-aligned layout");
   int r_k[PERR], r_iu[PERR], r_ib[PERR];
   bool r_ok[PERR];
 #pragma unroll
   for (int q = 0; q < PERR; ++q) {
-    const int k = tid + q * NT;
+    int k = tid + q * NT;
+    if (NT == 288) {
+      const int w = tid >> 5, lane = tid & 31;
+      k = q == 0 ? w * RX + lane
+                 : (w < 8 ? (w + 9) * RX + lane : (lane < RY ? lane * RX + TX : RX * RY));
+    }
     const int ry = k / RX, rx = k - ry * RX;
     r_k[q] = k < RX * RY ? k : -1;
     r_iu[q] = (ry + 1) * FUX + rx + 2;
     r_ib[q] = ry * FBX + rx;
     r_ok[q] = k < RX * RY && x0 + rx < gf.nx && y0 + ry < gf.ny;
   }
-  double acc[PERR];
+  double acc[PERR], cm_[PERR], cc_[PERR];   // u of the own column at planes p-1, p
 #pragma unroll
-  for (int q = 0; q < PERR; ++q) acc[q] = 0.0;
+  for (int q = 0; q < PERR; ++q) acc[q] = cm_[q] = cc_[q] = 0.0;
   // coarse point of this thread (threads 0..127) in the 16 x 8 tile
   const int cx = tid & 15, cy = tid >> 4;
   const int gcx = x0 / 2 + cx, gcy = y0 / 2 + cy;
@@ -1301,13 +1310,26 @@ __global__ void __launch_bounds__(NT, 4) k_rfw(const __grid_constant__ CUtensorM
 #pragma unroll
       for (int q = 0; q < PERR; ++q) {
         if (r_k[q] < 0) continue;
+        const int i = r_iu[q];
+        if (ph == 0) {
+          cm_[q] = pm[i];
+          cc_[q] = pc[i];
+        }
+        const double zcp = pp[i];
         double v = 0.0;
         if (r_ok[q]) {
-          const int i = r_iu[q];
-          const double lap = lap7<POW2, FUX>(pm, pc, pp, i, c);
-          const double au = pc[i] - sigma * lap;
+          // lap7's expression tree with the column's centre values in registers
+          const double c0 = cc_[q];
+          double lacc = 0.0;
+          lacc = lacc + dd2<POW2>((cm_[q] - 2.0 * c0) + zcp, c);
+          lacc = lacc + dd2<POW2>((pc[i - FUX] - 2.0 * c0) + pc[i + FUX], c);
+          lacc = lacc + dd2<POW2>((pc[i - 1] - 2.0 * c0) + pc[i + 1], c);
+          const double lap = c.nu * lacc;
+          const double au = c0 - sigma * lap;
           v = pb[r_ib[q]] - au;
         }
+        cm_[q] = cc_[q];
+        cc_[q] = zcp;
         if (ph == 0) {
           acc[q] = v;                                  // a of coarse plane jz0
         } else if (ph & 1) {

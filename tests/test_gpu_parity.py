@@ -869,3 +869,25 @@ def test_rfw_thread_layouts_equal_plain_kernels(n, sigma, threads):
         assert torch.equal(mg.v_cycle(sop, u, b, cfg), ref)
     finally:
         _capi.set_option(_capi.OPT_RFW_THREADS, 288)
+
+
+@pytest.mark.parametrize("n,sigma", [(128, 1.0 / 128), (256, 0.37)])
+@pytest.mark.parametrize("threads", [256, 288])
+def test_rfw_thread_layouts_equal_plain_kernels(n, sigma, threads):
+    """The fused residual + full-weighting kernel (eight warps, or nine with
+    row-aligned residual ownership) gives the plain kernels' V-cycle
+    (residual, then full weighting) bit for bit."""
+    rng = np.random.default_rng(n + threads)
+    g = heat.Grid(3, n)
+    u = dev(rng.standard_normal(g.shape))
+    b = dev(rng.standard_normal(g.shape))
+    sop = mg.ShiftedOperator(heat.HeatOperator(g), sigma)
+    cfg = mg.MgConfig("jor-rb", 1.0, 1, 1)
+    _capi.set_option(_capi.OPT_RFW, 0)
+    ref = mg.v_cycle(sop, u, b, cfg)
+    _capi.set_option(_capi.OPT_RFW, 1)
+    _capi.set_option(_capi.OPT_RFW_THREADS, threads)
+    try:
+        assert torch.equal(mg.v_cycle(sop, u, b, cfg), ref)
+    finally:
+        _capi.set_option(_capi.OPT_RFW_THREADS, 288)

@@ -29,6 +29,7 @@ def main():
     ap.add_argument("--m", type=int, default=8)
     ap.add_argument("--sweeps", type=int, default=3)
     ap.add_argument("--tau", action="store_true")
+    ap.add_argument("--cubic", action="store_true", help="also time the cubic correction")
     ap.add_argument("--opts", default="")
     a = ap.parse_args()
     for kv in filter(None, a.opts.split(",")):
@@ -48,6 +49,12 @@ def main():
     _capi.timing_enable(names)
     for _ in range(a.sweeps):
         sdc_sweep(st, u0, 1.0 / 64, op, cfg, FixedCycles(1), tau)
+    if a.cubic:      # the coarse correction's cubic interpolation (accumulate)
+        from paper_1407_6486_b200 import transfers
+        from paper_1407_6486_b200._device import to_device
+        c = to_device(torch.randn(((a.n // 2) - 1,) * 3, dtype=torch.float64))[0]
+        for _ in range(a.sweeps * a.m):
+            transfers.interp_cubic_into(c, st.y[0], True)
     torch.cuda.synchronize()
     total = 0.0
     rows = []
