@@ -99,6 +99,9 @@ const char* pl_last_error(void);
                                     levels); 0: separate apply and rhs launches; bit-identical */
 #define PL_OPT_RFW_THREADS 18  /* threads of the residual + full-weighting kernel: 288 (default;
                                   at most two residual points per thread) or 256 */
+#define PL_OPT_ZREV 19        /* bit mask of TMA kernels that visit their z chunks top-down, so
+                                 they start on the planes the previous kernel left in L2:
+                                 1 apply (+ rhs), 2 residual + full weighting (default 3) */
 int pl_set_option(int key, int value);
 
 /* storage elements of one field (incl. row pads) */

@@ -240,6 +240,7 @@ extern int g_zrb_ring;
 extern int g_rbrfw_enabled;
 extern int g_rbrfw_zcc;
 extern int g_rfw_threads;
+extern int g_zrev_mask;
 }
 
 extern "C" {
@@ -337,6 +338,10 @@ int pl_set_option(int key, int value) {
   }
   if (key == PL_OPT_FUSE_PROLONG) {
     g_fuse_prolong = value != 0;
+    return 0;
+  }
+  if (key == PL_OPT_ZREV) {
+    g_zrev_mask = value;
     return 0;
   }
   if (key == PL_OPT_RFW_THREADS) {

@@ -87,6 +87,17 @@ __device__ __forceinline__ void fence_barrier_init() {
 
 __host__ __device__ constexpr int align16(int n) { return (n + 15) / 16 * 16; }  // 128 B
 
+// z-chunk of this CTA.  A negative chunk length asks for the reverse chunk
+// order: a kernel that streams a field right after another kernel streamed
+// it forwards then starts on the planes still resident in the 126 MB L2.
+__device__ __forceinline__ int zchunk_block(int& zc) {
+  if (zc < 0) {
+    zc = -zc;
+    return gridDim.z - 1 - blockIdx.z;
+  }
+  return blockIdx.z;
+}
+
 template <bool POW2>
 __device__ __forceinline__ double dd2(double x, const OpC& c) {
   return POW2 ? x * c.inv_dx2 : x / c.dx2;
@@ -235,7 +246,8 @@ __global__ void __launch_bounds__(NTHR) k_z1(const __grid_constant__ CUtensorMap
   unsigned long long* bar = (unsigned long long*)(sb + (NEED_B ? RING * P0 : 0));
   const int tid = threadIdx.y * 32 + threadIdx.x;
   const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TY;
-  const int z0 = blockIdx.z * zc, z1 = min(z0 + zc, g.nz);
+  const int bz = zchunk_block(zc);
+  const int z0 = bz * zc, z1 = min(z0 + zc, g.nz);
   if (tid == 0) {
     for (int i = 0; i < RING; ++i) mbar_init(bar + i, 1);
     fence_barrier_init();
@@ -1234,7 +1246,8 @@ __global__ void __launch_bounds__(NT, 4) k_rfw(const __grid_constant__ CUtensorM
   const int tid = threadIdx.y * 32 + threadIdx.x;
   constexpr int rfw_issuer = NT - 32;
   const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TY;
-  const int jz0 = blockIdx.z * zcc, jz1 = min(jz0 + zcc, gc.nz);
+  const int bz = zchunk_block(zcc);
+  const int jz0 = bz * zcc, jz1 = min(jz0 + zcc, gc.nz);
   const int p0 = 2 * jz0, p1 = 2 * jz1;       // residual planes p0 .. p1
   const int ulo = p0 - 1, uhi = p1 + 1;       // u planes
   if (tid == 0) {
@@ -1873,6 +1886,7 @@ int make_map(CUtensorMap* m, const double* base, const Geo& g, int bw, int bh) {
 }
 
 }  // namespace
+int g_zrev_mask = 3;   // PL_OPT_ZREV: reverse z-chunk order of 1 apply / apply+rhs, 2 k_rfw
 int g_rfw_threads = 288;   // PL_OPT_RFW_THREADS: 256 (eight warps) or 288 (nine, default)
 int g_zc_floor = 16;  // PL_OPT_ZC_FLOOR (A/B): smallest z chunk (4 and 8 measured slower at 127^3)
 int g_zc_ctas = 148 * 8;   // PL_OPT_ZC_CTAS (A/B): CTA count the z chunking aims for
@@ -1911,7 +1925,8 @@ int launch_z1(const double* u, const double* b, double* out, const Geo& g, const
   dim3 grid(ceil_div(g.nx, TX), ceil_div(g.ny, TY), ceil_div(g.nz, zc)), block(32, 8);
   auto kern = c.pow2 ? k_z1<OP, true, PREF1> : k_z1<OP, false, PREF1>;
   raise_smem(kern, smem);
-  kern<<<grid, block, smem, s>>>(mu, mb, out, g, c, sigma, omega, dval, zc, ra);
+  const bool rev = (OP == Z_APPLY || OP == Z_APPLY_RHS) && (g_zrev_mask & 1);
+  kern<<<grid, block, smem, s>>>(mu, mb, out, g, c, sigma, omega, dval, rev ? -zc : zc, ra);
   return 0;
 }
 
@@ -2019,7 +2034,7 @@ int launch_rfw(const double* u, const double* b, double* coarse, const Geo& g, c
   auto kern = nt == 256 ? (c.pow2 ? k_rfw<true, 256> : k_rfw<false, 256>)
                         : (c.pow2 ? k_rfw<true, 288> : k_rfw<false, 288>);
   raise_smem(kern, smem);
-  kern<<<grid, block, smem, s>>>(mu, mb, coarse, g, gc, c, sigma, zcc);
+  kern<<<grid, block, smem, s>>>(mu, mb, coarse, g, gc, c, sigma, (g_zrev_mask & 2) ? -zcc : zcc);
   return 0;
 }
 
