@@ -88,8 +88,10 @@ const char* pl_last_error(void);
 #define PL_OPT_MID_CTAS 13    /* CTAs of the cooperative small-level kernels (0, default: one per
                                  SM); pfasst_run's rank-stream schedule sets 32 for its duration
                                  so the other ranks' streams keep the remaining SMs */
-#define PL_OPT_ZRB_RING 14    /* one-barrier jor-rb sweep rings: 0 (default) 8 u + 4 b planes,
-                                 3 CTAs/SM; 1: 6 u + 3 b planes, 4 CTAs/SM; bit-identical */
+#define PL_OPT_ZRB_RING 14    /* one-barrier jor-rb sweep rings: 0 (default) 6 u + 3 b planes,
+                                 4 CTAs/SM, z chunks >= 32 from 255^3 up, else 8 u + 4 b planes,
+                                 3 CTAs/SM; 1: always 6 + 3; 4: always 8 + 4; 2, 3: halo-work
+                                 layouts (slower); bit-identical */
 #define PL_OPT_RBRFW 15       /* 1: the last jor-rb pre-sweep, the residual and full weighting
                                  run as one overlapped-tile pass (TMA levels); 0 (default,
                                  measured faster): k_zrb3 then k_rfw; bit-identical */

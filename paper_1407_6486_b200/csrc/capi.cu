@@ -313,8 +313,8 @@ int pl_set_option(int key, int value) {
     return 0;
   }
   if (key == PL_OPT_ZRB_RING) {
-    if (value < 0 || value > 3) {
-      set_error("zrb ring variant %d out of range (0..3)", value);
+    if (value < 0 || value > 4) {
+      set_error("zrb ring variant %d out of range (0..4)", value);
       return PL_ERR_ARG;
     }
     g_zrb_ring = value;

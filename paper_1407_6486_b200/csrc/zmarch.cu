@@ -2007,7 +2007,13 @@ int launch_zrb3(const double* u, const double* b, double* out, const Geo& g, con
     kern<<<grid, dim3(NTHR_RB2), smem, s>>>(mu, mb, out, g, c, sigma, omega, dval, dinv, zc);
     return 0;
   }
-  if (g_zrb_ring == 1) {   // 6 u + 3 b planes, 4 CTAs per SM (register cap 64)
+  // default (0): 6 u + 3 b planes from 255^3 up, in z chunks of >= 32 planes
+  // (1,024 CTAs at 255^3, 1.7 waves of 4 per SM: 91 vs 97 us); the 8 + 4
+  // rings at 3 CTAs per SM below, where they are faster (26 vs 27 us at 127^3)
+  const bool big = g_zrb_ring == 0 && g.N >= 255;
+  if (big) zc = zc < 32 ? 32 : zc;
+  if (g_zrb_ring == 1 || big) {   // 6 u + 3 b planes, 4 CTAs per SM (register cap 64)
+    grid.z = ceil_div(g.nz, zc);
     size_t smem = ((size_t)6 * PU + (size_t)3 * PB) * 8 + 8 * (6 + 3);
     auto kern = c.pow2 ? k_zrb3<true, 6, 3, 4, false> : k_zrb3<false, 6, 3, 4, false>;
     raise_smem(kern, smem);

@@ -399,7 +399,7 @@ def test_pfasst_run_parity_tma_path(name):
         _capi.set_option(_capi.OPT_ZMARCH_MIN_N, 127)
 
 
-@pytest.mark.parametrize("variant", [0, 4, 5, 6, 7])
+@pytest.mark.parametrize("variant", [0, 4, 5, 6, 7, 8])
 def test_zrb_variants_bitwise_31cubed(variant):
     """Every jor-rb TMA sweep variant (three barriers per plane, and the
     register-pipelined one-barrier kernels with their ring sizes) reproduces
@@ -409,7 +409,7 @@ def test_zrb_variants_bitwise_31cubed(variant):
     _capi.set_option(_capi.OPT_ZRB_VARIANT, min(variant, 4))
     # 5: the 6 + 3 plane rings, 6: halo reds merged into every warp's phase,
     # 7: two dedicated halo warps
-    _capi.set_option(_capi.OPT_ZRB_RING, {5: 1, 6: 2, 7: 3}.get(variant, 0))
+    _capi.set_option(_capi.OPT_ZRB_RING, {5: 1, 6: 2, 7: 3, 8: 4}.get(variant, 0))
     try:
         sop = mg.ShiftedOperator(heat.HeatOperator(heat.Grid(3, 32)), m["sigma"])
         for om in (1.0, 0.8):
@@ -442,9 +442,9 @@ def test_zrb_variants_equal_plain_kernels(n, length, sigma, fuse):
     _capi.set_option(_capi.OPT_ZMARCH, 1)
     _capi.set_option(_capi.OPT_FUSE_PROLONG, fuse)
     try:
-        for variant in (0, 4, 5, 6, 7):
+        for variant in (0, 4, 5, 6, 7, 8):
             _capi.set_option(_capi.OPT_ZRB_VARIANT, min(variant, 4))
-            _capi.set_option(_capi.OPT_ZRB_RING, {5: 1, 6: 2, 7: 3}.get(variant, 0))
+            _capi.set_option(_capi.OPT_ZRB_RING, {5: 1, 6: 2, 7: 3, 8: 4}.get(variant, 0))
             assert torch.equal(mg.v_cycle(sop, u, b, cfg), ref), variant
             assert torch.equal(mg.smooth(sop, u, b, cfg, 2), ref_s), variant
     finally:
