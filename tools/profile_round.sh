@@ -21,6 +21,6 @@ echo "launch list rc=$?"
 KB="python tools/kernel_bench.py --n 256 --reps 1 --only vcycle_jor-rb_V11,interp_cubic_add"
 timeout 120 $KB > /dev/null 2>&1 && \
 timeout 900 ncu --set full --clock-control none --import-source on \
-    -k regex:"k_zrb3|k_rfw|k_cubic4|k_mid" -c 5 -o gpurun_out/top255_full $KB \
+    -k regex:"k_zrb3|k_rfw|k_cubic4|k_mid|k_z1" -c 9 -o gpurun_out/top255_full $KB \
     > gpurun_out/ncu_full.log 2>&1
 echo "full capture rc=$?"
