@@ -340,6 +340,10 @@ int pl_set_option(int key, int value) {
     g_fuse_prolong = value != 0;
     return 0;
   }
+  if (key == PL_OPT_FUSE_FAS_FW) {
+    g_fuse_fas_fw = value != 0;
+    return 0;
+  }
   if (key == PL_OPT_ZREV) {
     g_zrev_mask = value;
     return 0;
@@ -662,12 +666,19 @@ int pl_compute_fas(const double* fineF, const double* fine_tau, int mf, const do
   Geo gf = make_geo(dim, nf), gc = make_geo(dim, nc);
   // fine integrals at the selected nodes: dt * (Q_f F_f)[idx] (+ tau_f[idx])
   Coef qf = coef_from(qf_rows, nsel, mf + 1);
-  PL_TRY(launch_chain_ex(fineF, gf.nstore, scratch, gf.nstore, qf, dt, gf.nstore, fine_tau,
-                         gf.nstore, idx, fine_tau ? 1 : 0, s));
-  // restrict each into tau_c (temporarily), then tau_c = R - dt (Q_c F_c)
-  for (int j = 0; j < nsel; ++j)
-    PL_TRY(restrict_field(scratch + (size_t)j * gf.nstore, tau_c + (size_t)j * gc.nstore, gf,
-                          restrict_kind, s));
+  if (restrict_kind == PL_RESTRICT_FULL_WEIGHTING && chain_fw_ok(qf, gf)) {
+    // integrals and full weighting in one pass: the fine integrals are never stored
+    PL_TRY(launch_chain_fw(fineF, gf.nstore, qf, dt, fine_tau, gf.nstore, idx, tau_c, gc.nstore,
+                           gf, s));
+  } else {
+    PL_TRY(launch_chain_ex(fineF, gf.nstore, scratch, gf.nstore, qf, dt, gf.nstore, fine_tau,
+                           gf.nstore, idx, fine_tau ? 1 : 0, s));
+    // restrict each into tau_c (temporarily)
+    for (int j = 0; j < nsel; ++j)
+      PL_TRY(restrict_field(scratch + (size_t)j * gf.nstore, tau_c + (size_t)j * gc.nstore, gf,
+                            restrict_kind, s));
+  }
+  // then tau_c = R - dt (Q_c F_c)
   Coef q = coef_from(qc, mc + 1, mc + 1);
   PL_TRY(launch_chain_ex(coarseF, gc.nstore, tau_c, gc.nstore, q, dt, gc.nstore, tau_c,
                          gc.nstore, nullptr, 2, s));

@@ -117,6 +117,13 @@ int launch_resmax(const double* Y, const double* F, long long stride, const doub
                   const double* tau, const Coef& q, double dt, long long npts,
                   double* out_dev, cudaStream_t s);
 // d = new - old  (coarse node deltas), then out[m] = chain(P_t[m], d)
+// FAS: coarse rows = FW(scale * chain(F) (+ add rows)) in one pass (3-D, >= 127^3,
+// 2..5 rows, <= 9 columns; chain_fw_ok); bit-identical to launch_chain_ex + launch_fw
+bool chain_fw_ok(const Coef& a, const Geo& gf);
+int launch_chain_fw(const double* F, long long stride, const Coef& a, double scale,
+                    const double* add, long long add_stride, const int* add_rows,
+                    double* coarse, long long cstride, const Geo& gf, cudaStream_t s);
+extern int g_fuse_fas_fw;
 int launch_delta_chain(const double* ynew, const double* yold, long long stride,
                        const Coef& pt, double* out, long long out_stride, long long npts,
                        cudaStream_t s);

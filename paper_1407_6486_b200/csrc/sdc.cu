@@ -17,6 +17,7 @@
 
 #include "common.cuh"
 #include "kernels.cuh"
+#include "transfer_dev.cuh"
 
 namespace pl {
 
@@ -172,6 +173,120 @@ bool compact(const Coef& a, NodeCoef& c, int& K) {
   return true;
 }
 
+
+// ---------------------------------------------------------------------------
+// FAS node integrals fused into full weighting (hierarchy.py:102-108 then
+// transfers.py:27-34): coarse[r] = FW(scale * chain_r(F) (+ add[addrow[r]]))
+// for R selected rows, without writing the R fine integrals.  Layout and
+// operation order are k_rfw's (zmarch.cu): a CTA owns a 16 x 8 coarse tile and
+// the 33 x 17 fine window of its footprint; warp w owns window rows w and w+9,
+// warp 8 also the last column; marching up the fine planes each thread
+// evaluates k_chain's arithmetic at its points and folds it into fw3's z
+// weights in registers (a, a + 2b, 0.25 (t + c)); the y pass runs one phase
+// later and the x pass two, one barrier per plane.  The result is bit-identical
+// to k_chain + k_fw.
+constexpr int CF_TX = 32, CF_TY = 16, CF_RX = CF_TX + 1, CF_RY = CF_TY + 1;
+constexpr int CF_PR = (CF_RX * CF_RY + 15) / 16 * 16;
+constexpr int CF_NT = 288;
+
+template <int K, int R>
+__global__ void __launch_bounds__(CF_NT, 3) k_chain_fw(const double* __restrict__ F,
+                                                      long long stride, NodeCoef c, double scale,
+                                                      const double* __restrict__ add,
+                                                      long long add_stride, int mode,
+                                                      double* __restrict__ coarse,
+                                                      long long cstride, Geo gf, Geo gc,
+                                                      int zcc) {
+  extern __shared__ __align__(16) double cf_sm[];
+  double* szb = cf_sm;                  // R z-weighted planes (CF_RX x CF_RY)
+  double* syx = cf_sm + R * CF_PR;      // R y-weighted row sets (CF_RX x CF_TY/2)
+  const int tid = threadIdx.y * 32 + threadIdx.x;
+  const int w = tid >> 5, lane = tid & 31;
+  const int x0 = blockIdx.x * CF_TX, y0 = blockIdx.y * CF_TY;
+  const int jz0 = blockIdx.z * zcc, jz1 = min(jz0 + zcc, gc.nz);
+  const int p0 = 2 * jz0, p1 = 2 * jz1;
+  int r_k[2];
+  bool r_ok[2];
+  long long r_g[2];
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    const int k = q == 0 ? w * CF_RX + lane
+                         : (w < 8 ? (w + 9) * CF_RX + lane
+                                  : (lane < CF_RY ? lane * CF_RX + CF_TX : CF_RX * CF_RY));
+    const int ry = k / CF_RX, rx = k - ry * CF_RX;
+    r_k[q] = k < CF_RX * CF_RY ? k : -1;
+    r_ok[q] = r_k[q] >= 0 && x0 + rx < gf.nx && y0 + ry < gf.ny;
+    r_g[q] = r_ok[q] ? gf.at(x0 + rx, y0 + ry, 0) : 0;
+  }
+  double acc[2][R];
+#pragma unroll
+  for (int q = 0; q < 2; ++q)
+#pragma unroll
+    for (int r = 0; r < R; ++r) acc[q][r] = 0.0;
+  const int cx = tid & 15, cy = (tid >> 4) & 7;
+  for (int p = p0; p <= p1 + 2; ++p) {
+    const int ph = p - p0;
+    if (p <= p1) {
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        if (r_k[q] < 0) continue;
+        double v[R];
+        if (r_ok[q]) {
+          const long long i = r_g[q] + (long long)p * gf.sz;
+          double f[K];
+#pragma unroll
+          for (int k = 0; k < K; ++k) f[k] = __ldcs(F + c.col[k] * stride + i);
+#pragma unroll
+          for (int r = 0; r < R; ++r) {          // k_chain's arithmetic
+            double a = 0.0;
+#pragma unroll
+            for (int k = 0; k < K; ++k) a = __fma_rn(c.a[r * K + k], f[k], a);
+            double t = scale * a;
+            if (mode == 1) t = t + add[c.addrow[r] * add_stride + i];
+            v[r] = t;
+          }
+        } else {
+#pragma unroll
+          for (int r = 0; r < R; ++r) v[r] = 0.0;
+        }
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          if (ph == 0) {
+            acc[q][r] = v[r];
+          } else if (ph & 1) {
+            acc[q][r] = acc[q][r] + 2.0 * v[r];
+          } else {
+            szb[r * CF_PR + r_k[q]] = 0.25 * (acc[q][r] + v[r]);
+            acc[q][r] = v[r];
+          }
+        }
+      }
+    }
+    if ((ph & 1) == 1 && ph >= 3) {          // y pass of jz = (p - 3) / 2
+      for (int e = tid; e < R * CF_RX * (CF_TY / 2); e += CF_NT) {
+        const int r = e / (CF_RX * (CF_TY / 2)), k = e - r * (CF_RX * (CF_TY / 2));
+        const int yy = k / CF_RX, xx = k - yy * CF_RX;
+        const double* zc = szb + r * CF_PR + 2 * yy * CF_RX + xx;
+        syx[r * CF_PR + k] = fw3(zc[0], zc[CF_RX], zc[2 * CF_RX]);
+      }
+    }
+    if ((ph & 1) == 0 && ph >= 4) {          // x pass of jz = (p - 4) / 2
+      for (int e = tid; e < R * (CF_TX / 2) * (CF_TY / 2); e += CF_NT) {
+        const int r = e >> 7, pt = e & 127;
+        const int ex = pt & 15, ey = pt >> 4;
+        const int gcx = x0 / 2 + ex, gcy = y0 / 2 + ey;
+        if (gcx < gc.nx && gcy < gc.ny) {
+          const double* yr = syx + r * CF_PR + ey * CF_RX + 2 * ex;
+          coarse[r * cstride + gc.at(gcx, gcy, (p - 4) / 2)] = fw3(yr[0], yr[1], yr[2]);
+        }
+      }
+    }
+    __syncthreads();
+  }
+  (void)cx;
+  (void)cy;
+}
+
 #define PL_K_DISPATCH(K, CALL)                                                    \
   switch (K) {                                                                    \
     case 1: CALL(1); break; case 2: CALL(2); break; case 3: CALL(3); break;      \
@@ -256,6 +371,57 @@ int launch_axpby(const double* a, const double* b, double* out, int sub, long lo
   PL_PRE(K_COPY);
   k_axpby<<<ceil_div(npts, 256), 256, 0, s>>>(a, b, out, sub, npts);
   PL_CHECK_LAUNCH(K_COPY, 24.0 * npts);
+  return 0;
+}
+
+
+int g_fuse_fas_fw = 1;   // PL_OPT_FUSE_FAS_FW
+
+bool chain_fw_ok(const Coef& a, const Geo& gf) {
+  return g_fuse_fas_fw && gf.dim == 3 && gf.N >= 127 && a.rows >= 2 && a.rows <= 5 &&
+         a.cols <= 9;
+}
+
+int launch_chain_fw(const double* F, long long stride, const Coef& a, double scale,
+                    const double* add, long long add_stride, const int* add_rows,
+                    double* coarse, long long cstride, const Geo& gf, cudaStream_t s) {
+  NodeCoef c;
+  int K;
+  if (!compact(a, c, K)) return -1;
+  if (add_rows)
+    for (int m = 0; m < a.rows; ++m) c.addrow[m] = add_rows[m];
+  Geo gc = make_geo(3, (gf.N + 1) / 2);
+  const int zcc = 8;
+  dim3 grid(ceil_div(gf.nx, CF_TX), ceil_div(gf.ny, CF_TY), ceil_div(gc.nz, zcc));
+  dim3 block(32, CF_NT / 32);
+  const int mode = add ? 1 : 0;
+  PL_PRE(K_FAS);
+#define CF_CALL(KK, RR)                                                                       \
+  do {                                                                                        \
+    size_t smem = sizeof(double) * 2 * RR * CF_PR;                                            \
+    cudaFuncSetAttribute(k_chain_fw<KK, RR>, cudaFuncAttributeMaxDynamicSharedMemorySize,     \
+                         (int)smem);                                                          \
+    k_chain_fw<KK, RR><<<grid, block, smem, s>>>(F, stride, c, scale, add, add_stride, mode,  \
+                                                 coarse, cstride, gf, gc, zcc);               \
+  } while (0)
+#define CF_R(KK)                                   \
+  switch (a.rows) {                                \
+    case 2: CF_CALL(KK, 2); break;                 \
+    case 3: CF_CALL(KK, 3); break;                 \
+    case 4: CF_CALL(KK, 4); break;                 \
+    default: CF_CALL(KK, 5); break;                \
+  }
+  switch (K) {
+    case 1: CF_R(1); break; case 2: CF_R(2); break; case 3: CF_R(3); break;
+    case 4: CF_R(4); break; case 5: CF_R(5); break; case 6: CF_R(6); break;
+    case 7: CF_R(7); break; case 8: CF_R(8); break; default: CF_R(9); break;
+  }
+#undef CF_R
+#undef CF_CALL
+  // the unfused passes it replaces: the chain (K + rows (+ rows) fields) and
+  // one full weighting per row (8 B per fine + 8 B per coarse point)
+  PL_CHECK_LAUNCH(K_FAS, 8.0 * gf.npts * (K + 2 * a.rows + (add ? a.rows : 0)) +
+                             8.0 * gc.npts * a.rows);
   return 0;
 }
 

@@ -891,3 +891,29 @@ def test_rfw_thread_layouts_equal_plain_kernels(n, sigma, threads):
         assert torch.equal(mg.v_cycle(sop, u, b, cfg), ref)
     finally:
         _capi.set_option(_capi.OPT_RFW_THREADS, 288)
+
+
+def test_fas_chain_fw_fused_equals_separate():
+    """The FAS node integrals full-weighted in the same pass (never stored;
+    PL_OPT_FUSE_FAS_FW) give a PFASST block bit-identical to the separate
+    chain and full-weighting launches: 3 levels 255^3 / 127^3 / 63^3, so both
+    the tau-free fine -> mid and the tau-carrying mid -> coarse restrictions
+    take the fused path."""
+    d = 3
+    cfg = mg.MgConfig("jor-rb", 1.0, 1, 1)
+    lv = [hierarchy.Level(heat.HeatOperator(heat.Grid(d, n)), quadrature.uniform_table(k - 1),
+                          cfg, mg.FixedCycles(1), space_interp_order=4)
+          for n, k in ((256, 5), (128, 3), (64, 2))]
+    u0 = dev(heat.seeded_field(heat.Grid(d, 256)))
+    outs = []
+    try:
+        for fuse in (0, 1):
+            _capi.set_option(_capi.OPT_FUSE_FAS_FW, fuse)
+            r = pfasst.pfasst_run(lv, u0, 3.0 / 64, 3, tol=1e-10, max_iter=3)
+            outs.append((r.u.clone(), r.rank_iterations, r.rank_vcycles,
+                         [row.residual for row in r.trace]))
+    finally:
+        _capi.set_option(_capi.OPT_FUSE_FAS_FW, 1)
+    assert outs[0][1] == outs[1][1] and outs[0][2] == outs[1][2]
+    assert outs[0][3] == outs[1][3]
+    assert torch.equal(outs[0][0], outs[1][0])
