@@ -60,7 +60,9 @@ __global__ void __launch_bounds__(256) k_chain(const double* __restrict__ in, lo
 
 // sdc.py:117-124, max-reduced as IEEE bit patterns (non-negative doubles
 // order like unsigned integers; NaN propagates like np.max).
-template <int K>
+// R > 0: the row count is a compile-time constant (R == q.rows), so every
+// load of the point is issued before the first chain; R == 0: runtime rows
+template <int K, int R = 0>
 __global__ void __launch_bounds__(256) k_resmax(const double* __restrict__ Y,
                                                 const double* __restrict__ F, long long stride,
                                                 const double* __restrict__ y0,
@@ -74,13 +76,19 @@ __global__ void __launch_bounds__(256) k_resmax(const double* __restrict__ Y,
 #pragma unroll
     for (int k = 0; k < K; ++k) f[k] = F[q.col[k] * stride + i];
     const double base = y0[i];
+    constexpr int NR = R > 0 ? R : MAXN;
+    double yv[R > 0 ? R : 1];
+    if constexpr (R > 0) {
 #pragma unroll
-    for (int m = 0; m < MAXN; ++m) {
-      if (m < q.rows) {
+      for (int m = 0; m < R; ++m) yv[m] = Y[m * stride + i];
+    }
+#pragma unroll
+    for (int m = 0; m < NR; ++m) {
+      if (R > 0 || m < q.rows) {
         double acc = 0.0;
 #pragma unroll
         for (int k = 0; k < K; ++k) acc = __fma_rn(q.a[m * K + k], f[k], acc);
-        double r = (base + dt * acc) - Y[m * stride + i];
+        double r = (base + dt * acc) - (R > 0 ? yv[R > 0 ? m : 0] : Y[m * stride + i]);
         if (tau) r = r + tau[m * stride + i];
         unsigned long long bits = (unsigned long long)__double_as_longlong(fabs(r));
         best = bits > best ? bits : best;
@@ -343,9 +351,20 @@ int launch_resmax(const double* Y, const double* F, long long stride, const doub
   const int blocks = ceil_div(npts, 256);
   unsigned long long* o = (unsigned long long*)out_dev;
   PL_PRE(K_RESMAX);
+  if (c.rows == K + 1 && K >= 1 && K <= 8) {   // Q of M+1 nodes: K = M used columns
+#define CALLR(KK) \
+  k_resmax<KK, KK + 1><<<blocks, 256, 0, s>>>(Y, F, stride, y0, tau, c, dt, npts, o)
+    switch (K) {
+      case 1: CALLR(1); break; case 2: CALLR(2); break; case 3: CALLR(3); break;
+      case 4: CALLR(4); break; case 5: CALLR(5); break; case 6: CALLR(6); break;
+      case 7: CALLR(7); break; default: CALLR(8); break;
+    }
+#undef CALLR
+  } else {
 #define CALL(KK) k_resmax<KK><<<blocks, 256, 0, s>>>(Y, F, stride, y0, tau, c, dt, npts, o)
-  PL_K_DISPATCH(K, CALL);
+    PL_K_DISPATCH(K, CALL);
 #undef CALL
+  }
   PL_CHECK_LAUNCH(K_RESMAX, 8.0 * npts * (K + q.rows + 1 + (tau ? q.rows : 0)));
   return 0;
 }

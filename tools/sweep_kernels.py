@@ -47,8 +47,10 @@ def main():
     torch.cuda.synchronize()
     names = _capi.kind_names()
     _capi.timing_enable(names)
+    from paper_1407_6486_b200.sdc import residual
     for _ in range(a.sweeps):
         sdc_sweep(st, u0, 1.0 / 64, op, cfg, FixedCycles(1), tau)
+        residual(st, u0, 1.0 / 64, tau)          # the collocation residual after each sweep
     if a.cubic:      # the coarse correction's cubic interpolation (accumulate)
         from paper_1407_6486_b200 import transfers
         from paper_1407_6486_b200._device import to_device
