@@ -78,6 +78,21 @@ __global__ void __launch_bounds__(256) k_prolong3_cell(const double* __restrict_
                           : 0.0;
       }
   const bool xo = jx < nc;   // fine 2j+1 exists along x
+  // accumulate: the (up to) four fine pairs are loaded before any store, so
+  // their DRAM latencies overlap (the compiler cannot prove the rows disjoint)
+  double2 old[2][2];
+#pragma unroll
+  for (int pz = 0; pz < 2; ++pz)
+#pragma unroll
+    for (int py = 0; py < 2; ++py) {
+      old[pz][py] = make_double2(0.0, 0.0);
+      if (accumulate && (pz == 0 || jz < nc) && (py == 0 || jy < nc)) {
+        const double* src = f + (long long)(2 * jz + pz) * gf.sz +
+                            (long long)(2 * jy + py) * gf.sy + 2 * jx;
+        if (xo) old[pz][py] = __ldcs(reinterpret_cast<const double2*>(src));
+        else old[pz][py].x = __ldcs(src);
+      }
+    }
 #pragma unroll
   for (int pz = 0; pz < 2; ++pz) {
     if (pz == 1 && jz >= nc) break;
@@ -98,13 +113,13 @@ __global__ void __launch_bounds__(256) k_prolong3_cell(const double* __restrict_
       if (xo) {
         double2 w = make_double2(ve, vo);
         if (accumulate) {
-          const double2 o = *reinterpret_cast<const double2*>(dst);
+          const double2 o = old[pz][py];
           w.x = o.x + w.x;
           w.y = o.y + w.y;
         }
         *reinterpret_cast<double2*>(dst) = w;
       } else {
-        dst[0] = accumulate ? dst[0] + ve : ve;
+        dst[0] = accumulate ? old[pz][py].x + ve : ve;
       }
     }
   }
