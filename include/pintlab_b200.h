@@ -104,7 +104,8 @@ const char* pl_last_error(void);
 #define PL_OPT_ZREV 19        /* bit mask of TMA kernels that visit their z chunks top-down, so
                                  they start on the planes the previous kernel left in L2:
                                  1 apply (+ rhs), 2 residual + full weighting (default 3) */
-#define PL_OPT_FUSE_FAS_FW 20 /* 1 (default): the FAS fine node integrals are full-weighted in
+#define PL_OPT_FUSE_FAS_FW 20 /* 1 (default): restrict_state full-weights all selected nodes in one
+                                 tiled launch, and the FAS fine node integrals are full-weighted in
                                  the same pass (3-D, >= 127^3), never stored; 0: separate
                                  chain and full-weighting launches; bit-identical */
 int pl_set_option(int key, int value);

@@ -642,9 +642,13 @@ int pl_restrict_state(const double* fineY, const int* idx, int nsel, double* coa
   cudaStream_t s = (cudaStream_t)stream;
   Geo gf = make_geo(dim, nf), gc = make_geo(dim, nc);
   OpC cc = make_opc(nc, length, nu_c, order_c);
+  // 3-D full weighting from 127^3 up: every selected node in one tiled launch
+  const bool batched = restrict_kind == PL_RESTRICT_FULL_WEIGHTING && fw_select_ok(gf, nsel);
+  if (batched) PL_TRY(launch_fw_select(fineY, gf.nstore, idx, nsel, coarseY, gc.nstore, gf, s));
   for (int j = 0; j < nsel; ++j) {
     double* cy = coarseY + (size_t)j * gc.nstore;
-    PL_TRY(restrict_field(fineY + (size_t)idx[j] * gf.nstore, cy, gf, restrict_kind, s));
+    if (!batched)
+      PL_TRY(restrict_field(fineY + (size_t)idx[j] * gf.nstore, cy, gf, restrict_kind, s));
     PL_TRY(launch_apply(cy, coarseF + (size_t)j * gc.nstore, gc, cc, s));
   }
   return 0;

@@ -124,6 +124,9 @@ int launch_chain_fw(const double* F, long long stride, const Coef& a, double sca
                     const double* add, long long add_stride, const int* add_rows,
                     double* coarse, long long cstride, const Geo& gf, cudaStream_t s);
 extern int g_fuse_fas_fw;
+bool fw_select_ok(const Geo& gf, int nsel);
+int launch_fw_select(const double* fine, long long stride, const int* idx, int nsel,
+                     double* coarse, long long cstride, const Geo& gf, cudaStream_t s);
 int launch_delta_chain(const double* ynew, const double* yold, long long stride,
                        const Coef& pt, double* out, long long out_stride, long long npts,
                        cudaStream_t s);

@@ -197,7 +197,9 @@ constexpr int CF_TX = 32, CF_TY = 16, CF_RX = CF_TX + 1, CF_RY = CF_TY + 1;
 constexpr int CF_PR = (CF_RX * CF_RY + 15) / 16 * 16;
 constexpr int CF_NT = 288;
 
-template <int K, int R>
+// IDENT (K == R): row r is input column r itself (restrict_state's full
+// weighting of the selected nodes, several fields in one launch)
+template <int K, int R, bool IDENT = false>
 __global__ void __launch_bounds__(CF_NT, 3) k_chain_fw(const double* __restrict__ F,
                                                       long long stride, NodeCoef c, double scale,
                                                       const double* __restrict__ add,
@@ -246,6 +248,10 @@ __global__ void __launch_bounds__(CF_NT, 3) k_chain_fw(const double* __restrict_
           for (int k = 0; k < K; ++k) f[k] = __ldcs(F + c.col[k] * stride + i);
 #pragma unroll
           for (int r = 0; r < R; ++r) {          // k_chain's arithmetic
+            if constexpr (IDENT) {
+              v[r] = f[r];
+              continue;
+            }
             double a = 0.0;
 #pragma unroll
             for (int k = 0; k < K; ++k) a = __fma_rn(c.a[r * K + k], f[k], a);
@@ -395,6 +401,39 @@ int launch_axpby(const double* a, const double* b, double* out, int sub, long lo
 
 
 int g_fuse_fas_fw = 1;   // PL_OPT_FUSE_FAS_FW
+
+bool fw_select_ok(const Geo& gf, int nsel) {
+  return g_fuse_fas_fw && gf.dim == 3 && gf.N >= 127 && nsel >= 1 && nsel <= 5;
+}
+
+// coarse[j] = FW(fine[idx[j]]) for j < nsel in one launch (k_chain_fw<IDENT>)
+int launch_fw_select(const double* fine, long long stride, const int* idx, int nsel,
+                     double* coarse, long long cstride, const Geo& gf, cudaStream_t s) {
+  NodeCoef c;
+  std::memset(&c, 0, sizeof(c));
+  c.rows = nsel;
+  for (int j = 0; j < nsel; ++j) c.col[j] = idx[j];
+  Geo gc = make_geo(3, (gf.N + 1) / 2);
+  const int zcc = 8;
+  dim3 grid(ceil_div(gf.nx, CF_TX), ceil_div(gf.ny, CF_TY), ceil_div(gc.nz, zcc));
+  dim3 block(32, CF_NT / 32);
+  PL_PRE(K_RESTRICT);
+#define FS_CALL(RR)                                                                         \
+  do {                                                                                      \
+    size_t smem = sizeof(double) * 2 * RR * CF_PR;                                          \
+    cudaFuncSetAttribute(k_chain_fw<RR, RR, true>,                                          \
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);           \
+    k_chain_fw<RR, RR, true><<<grid, block, smem, s>>>(fine, stride, c, 1.0, nullptr, 0, 0, \
+                                                       coarse, cstride, gf, gc, zcc);       \
+  } while (0)
+  switch (nsel) {
+    case 1: FS_CALL(1); break; case 2: FS_CALL(2); break; case 3: FS_CALL(3); break;
+    case 4: FS_CALL(4); break; default: FS_CALL(5); break;
+  }
+#undef FS_CALL
+  PL_CHECK_LAUNCH(K_RESTRICT, (8.0 * gf.npts + 8.0 * gc.npts) * nsel);
+  return 0;
+}
 
 bool chain_fw_ok(const Coef& a, const Geo& gf) {
   return g_fuse_fas_fw && gf.dim == 3 && gf.N >= 127 && a.rows >= 2 && a.rows <= 5 &&
