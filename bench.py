@@ -420,22 +420,29 @@ def run_reference(args, w, ratio=None):
     # algorithmic bytes of a whole block over those of one sample (the same
     # model the GPU arm counts): live from the GPU arm, else its recorded value
     model = {"block_over_sample": ratio} if ratio else BLOCK_MODEL[args.workload]
+    # one single-threaded worker PROCESS per core (spawned: numpy/scipy BLAS
+    # called from several threads of one process aborted once with a heap
+    # error); a round's time is its slowest worker's sample (they run together)
+    import concurrent.futures as cf
+    import multiprocessing as mp
+    saved = {k: os.environ.get(k) for k in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS",
+                                             "MKL_NUM_THREADS", "CUDA_VISIBLE_DEVICES")}
+    os.environ.update(OMP_NUM_THREADS="1", OPENBLAS_NUM_THREADS="1", MKL_NUM_THREADS="1",
+                      CUDA_VISIBLE_DEVICES="")
     vals = []
-    for i in range(args.warmup + args.steps):
-        ts = [None] * threads
-
-        def work(j):
-            ts[j] = oracle_sample(w)
-
-        t0 = time.perf_counter()
-        th = [threading.Thread(target=work, args=(j,)) for j in range(threads)]
-        for t in th:
-            t.start()
-        for t in th:
-            t.join()
-        wall = time.perf_counter() - t0
-        if i >= args.warmup:
-            vals.append(wall)
+    try:
+        with cf.ProcessPoolExecutor(max_workers=threads,
+                                    mp_context=mp.get_context("spawn")) as pool:
+            for i in range(args.warmup + args.steps):
+                wall = max(pool.map(oracle_sample, [w] * threads))
+                if i >= args.warmup:
+                    vals.append(wall)
+    finally:
+        for k, v in saved.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
     wall = sum(vals)
     samples = threads * len(vals)
     value = w["p"] / (wall / samples * model["block_over_sample"])
@@ -447,7 +454,8 @@ def run_reference(args, w, ratio=None):
                              "kind": "port",
                              "sample": f"{samples} fine sub-steps (rhs + {w['cycles']} V-cycle "
                                        f"+ f refresh at {w['ns'][0] - 1}^{w['dim']}) on "
-                                       f"{threads} threads; block time extrapolated x"
+                                       f"{threads} single-threaded processes; block time "
+                                       f"extrapolated x"
                                        f"{model['block_over_sample']:.1f} by algorithmic bytes"},
             "e2e": {"value": value, "unit": "time-steps/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
