@@ -464,9 +464,9 @@ def run_reference(args, w, ratio=None):
 # block / sample algorithmic-byte ratios measured by the GPU arm (the runtime's
 # byte counter over one block vs one fine sub-step); refreshed by --calibrate
 BLOCK_MODEL = {
-    "cfg3": {"block_over_sample": 2.0e3},
-    "cfg4": {"block_over_sample": 2.0e3},
-    "cfg2": {"block_over_sample": 2.0e3},
+    "cfg3": {"block_over_sample": 2230.4},     # profiles/r01/bench.json (GPU arm, live)
+    "cfg4": {"block_over_sample": 1048.1},
+    "cfg2": {"block_over_sample": 1124.9},
 }
 
 
