@@ -270,22 +270,38 @@ __device__ __forceinline__ Geo ct_geo() {
   return g;
 }
 
+// (I - sigma A) u at point p of a dense N^3 shared-memory level, order 2 with
+// a power-of-two dx^2: lap_point / shifted_point's operations in their order
+// (axes z, y, x accumulated from 0.0, x / dx2 == x * inv_dx2 exactly, zero
+// ghosts), with the order and pow2 branches folded away at compile time
+template <int N>
+__device__ __forceinline__ double ft_shifted(const double* u, double inv, double nu,
+                                            double sigma, int x, int y, int z, int p) {
+  const double c0 = u[p];
+  const double zm = z > 0 ? u[p - N * N] : 0.0, zp = z < N - 1 ? u[p + N * N] : 0.0;
+  const double ym = y > 0 ? u[p - N] : 0.0, yp = y < N - 1 ? u[p + N] : 0.0;
+  const double xm = x > 0 ? u[p - 1] : 0.0, xp = x < N - 1 ? u[p + 1] : 0.0;
+  double acc = 0.0;
+  acc = acc + ((zm - 2.0 * c0) + zp) * inv;
+  acc = acc + ((ym - 2.0 * c0) + yp) * inv;
+  acc = acc + ((xm - 2.0 * c0) + xp) * inv;
+  return c0 - sigma * (nu * acc);
+}
+
 template <int N>
 __device__ __forceinline__ void ft_colour(double* u, const double* b, const OpC& c, double sigma,
                                           double omega, int red, bool zero) {
   const Geo g = ct_geo<N>();
+  // order 2: the diagonal is the same at every point (shifted_diag's operations)
+  const double d = shifted_diag<3>(g, c, sigma, 1, 1, 1);
   if (zero) {   // u == 0 on entry: red points 0 + (omega b) / d, black points 0
     for (int p = threadIdx.x; p < N * N * N; p += blockDim.x) {
       const int x = p % N, y = (p / N) % N, z = p / (N * N);
-      if (is_red<3>(x, y, z)) {
-        const double d = shifted_diag<3>(g, c, sigma, x, y, z);
-        u[p] = 0.0 + ((omega * b[p]) / d);
-      } else {
-        u[p] = 0.0;
-      }
+      u[p] = is_red<3>(x, y, z) ? 0.0 + ((omega * b[p]) / d) : 0.0;
     }
     return;
   }
+  const double inv = c.inv_dx2, nu = c.nu;
   constexpr int H = (N + 1) / 2;
   for (int t = threadIdx.x; t < H * N * N; t += blockDim.x) {
     const int h = t % H, row = t / H;
@@ -293,8 +309,7 @@ __device__ __forceinline__ void ft_colour(double* u, const double* b, const OpC&
     const int x = 2 * h + (((y + z + 3) & 1) ^ red ^ 1);
     if (x >= N) continue;
     const int p = (z * N + y) * N + x;
-    const double d = shifted_diag<3>(g, c, sigma, x, y, z);
-    const double r = b[p] - shifted_point<3>(u, g, c, sigma, x, y, z, p);
+    const double r = b[p] - ft_shifted<N>(u, inv, nu, sigma, x, y, z, p);
     u[p] = u[p] + ((omega * r) / d);
   }
 }
@@ -351,7 +366,7 @@ __device__ void ft_level(const TailArgs& a, double* sm, bool zero) {
     }
     for (int p = threadIdx.x; p < N * N * N; p += blockDim.x) {
       const int x = p % N, y = (p / N) % N, z = p / (N * N);
-      t[p] = b[p] - shifted_point<3>(u, g, T.c, a.sigma, x, y, z, p);
+      t[p] = b[p] - ft_shifted<N>(u, T.c.inv_dx2, T.c.nu, a.sigma, x, y, z, p);
     }
     __syncthreads();
     const TailLevel& C = a.lv[L + 1];
@@ -490,7 +505,24 @@ struct MidLevel {
   double* t;
   Geo g;
   OpC c;
+  int pow2;   // order 2 with a power-of-two dx^2: mid_shifted / constant diagonal
 };
+
+// shifted_point's operations for order 2 and a power-of-two dx^2 (x / dx2 ==
+// x * inv_dx2 exactly): axes z, y, x accumulated from 0.0, zero ghosts
+__device__ __forceinline__ double mid_shifted(const double* __restrict__ u, const Geo& g,
+                                             const OpC& c, double sigma, int x, int y, int z,
+                                             long long idx) {
+  const double c0 = u[idx];
+  const double zm = z > 0 ? u[idx - g.sz] : 0.0, zp = z < g.nz - 1 ? u[idx + g.sz] : 0.0;
+  const double ym = y > 0 ? u[idx - g.sy] : 0.0, yp = y < g.ny - 1 ? u[idx + g.sy] : 0.0;
+  const double xm = x > 0 ? u[idx - 1] : 0.0, xp = x < g.nx - 1 ? u[idx + 1] : 0.0;
+  double acc = 0.0;
+  acc = acc + ((zm - 2.0 * c0) + zp) * c.inv_dx2;
+  acc = acc + ((ym - 2.0 * c0) + yp) * c.inv_dx2;
+  acc = acc + ((xm - 2.0 * c0) + xp) * c.inv_dx2;
+  return c0 - sigma * (c.nu * acc);
+}
 
 struct MidArgs {
   unsigned long long* trace;   // PL_MID_TRACE diagnostics: %globaltimer per phase (or null)
@@ -533,7 +565,9 @@ __device__ __forceinline__ void mid_colour(const MidLevel& L, const MidArgs& m, 
     if (x >= N) continue;
     const long long idx = g.at(x, y, z);
     const double d = shifted_diag<DIM>(g, L.c, m.sigma, x, y, z);
-    const double r = L.b[idx] - shifted_point<DIM>(L.u, g, L.c, m.sigma, x, y, z, idx);
+    const double r = L.b[idx] - (DIM == 3 && L.pow2
+                                     ? mid_shifted(L.u, g, L.c, m.sigma, x, y, z, idx)
+                                     : shifted_point<DIM>(L.u, g, L.c, m.sigma, x, y, z, idx));
     L.u[idx] = L.u[idx] + ((m.omega * r) / d);
   }
 }
@@ -577,7 +611,9 @@ __global__ void __launch_bounds__(MID_THREADS) k_mid(MidArgs m, TailArgs ta) {
       int x, y, z;
       decode_point(L.g, t, x, y, z);
       const long long idx = L.g.at(x, y, z);
-      L.t[idx] = L.b[idx] - shifted_point<DIM>(L.u, L.g, L.c, m.sigma, x, y, z, idx);
+      L.t[idx] = L.b[idx] - (DIM == 3 && L.pow2
+                                 ? mid_shifted(L.u, L.g, L.c, m.sigma, x, y, z, idx)
+                                 : shifted_point<DIM>(L.u, L.g, L.c, m.sigma, x, y, z, idx));
     }
     MID_SYNC();
     for (long long t = gt; t < C.g.npts; t += gs) {       // full weighting (k_fw)
@@ -651,8 +687,10 @@ static int tail_args(MgPlan* P, int l0, double sigma, TailArgs& a, size_t* smem_
     const int N0 = P->lv[l0].g.N;
     bool chain = P->dim == 3 && P->order == 2 && P->smoother == SM_RB && a.lu_off >= 0 &&
                  a.m == 27 && g_fast_tail && (N0 == 15 || N0 == 7);
+    // ft_shifted multiplies by 1 / dx^2: exact only for power-of-two dx^2
     for (int i = 0, n = N0; chain && i < a.nlev; ++i, n = (n - 1) / 2)
-      chain = P->lv[l0 + i].g.N == n && (P->lv[l0 + i].coarsest == (n == 3));
+      chain = P->lv[l0 + i].g.N == n && (P->lv[l0 + i].coarsest == (n == 3)) &&
+              P->lv[l0 + i].c.pow2;
     if (chain) a.fast = N0;
   }
   *smem_out = sizeof(double) * off;
@@ -727,6 +765,7 @@ static int launch_mid(MgPlan* P, int l0, double* u, const double* b, double sigm
     M.t = L.t;
     M.g = L.g;
     M.c = L.c;
+    M.pow2 = L.c.order == 2 && L.c.pow2;
     if (i < m.nmid) {   // the unfused kernels' algorithmic bytes
       const double np = (double)L.g.npts, nc = (double)P->lv[l0 + i + 1].g.npts;
       bytes += np * (24.0 * (P->pre + P->post) + 24.0 + 8.0 + 16.0) + nc * 16.0;
