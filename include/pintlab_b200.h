@@ -108,6 +108,10 @@ const char* pl_last_error(void);
                                  tiled launch, and the FAS fine node integrals are full-weighted in
                                  the same pass (3-D, >= 127^3), never stored; 0: separate
                                  chain and full-weighting launches; bit-identical */
+#define PL_OPT_MID_BAR 21     /* grid barrier of the cooperative small-level V-cycle: 0 (default)
+                                 cooperative_groups grid.sync(); 1: one arrive counter +
+                                 generation word (acquire/release at gpu scope, self-resetting;
+                                 measured slower); bit-identical */
 int pl_set_option(int key, int value);
 
 /* storage elements of one field (incl. row pads) */

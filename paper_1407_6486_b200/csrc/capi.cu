@@ -224,6 +224,7 @@ extern "C" int g_graphs_enabled;
 
 namespace pl {
 extern int g_zmarch_enabled;
+extern int g_mid_bar;
 extern int g_zmarch_min_n;
 extern int g_zrb_variant;
 extern int g_fuse_prolong;
@@ -342,6 +343,10 @@ int pl_set_option(int key, int value) {
   }
   if (key == PL_OPT_FUSE_FAS_FW) {
     g_fuse_fas_fw = value != 0;
+    return 0;
+  }
+  if (key == PL_OPT_MID_BAR) {
+    g_mid_bar = value != 0;
     return 0;
   }
   if (key == PL_OPT_ZREV) {

@@ -73,7 +73,18 @@ struct TailArgs {
   int m;
   int lu_off;         // >= 0: factors staged in shared memory at this offset
   int fast;           // 15 or 7: compile-time-sized 3-D order-2 jor-rb path (ft_*)
+  unsigned long long* trace;   // PL_MID_TRACE: [0] count, then %globaltimer per tail phase
 };
+
+// diagnostics only (PL_MID_TRACE): thread 0 stamps the end of a tail phase
+__device__ __forceinline__ void ft_stamp(const TailArgs& a) {
+  if (a.trace && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    const unsigned long long k = a.trace[0]++;
+    if (k < 62) a.trace[1 + k] = t;
+  }
+}
 
 #define PL_FOR_SM_POINTS(g)                                                  \
   for (int p = threadIdx.x; p < (int)(g).npts; p += blockDim.x)
@@ -349,6 +360,7 @@ __device__ void ft_level(const TailArgs& a, double* sm, bool zero) {
   double* b = sm + T.off_b;
   if constexpr (N == 3) {
     ft_lu27(sm + a.lu_off, b, u);
+    ft_stamp(a);
   } else {
     constexpr int NC = (N - 1) / 2;
     double* t = sm + T.off_t;
@@ -357,18 +369,22 @@ __device__ void ft_level(const TailArgs& a, double* sm, bool zero) {
     if (zero && a.pre == 0) {
       for (int p = threadIdx.x; p < N * N * N; p += blockDim.x) u[p] = 0.0;
       __syncthreads();
+      ft_stamp(a);
     }
     for (int k = 0; k < a.pre; ++k) {
       ft_colour<N>(u, b, T.c, a.sigma, a.omega, 1, zero && k == 0);
       __syncthreads();
+      ft_stamp(a);
       ft_colour<N>(u, b, T.c, a.sigma, a.omega, 0, false);
       __syncthreads();
+      ft_stamp(a);
     }
     for (int p = threadIdx.x; p < N * N * N; p += blockDim.x) {
       const int x = p % N, y = (p / N) % N, z = p / (N * N);
       t[p] = b[p] - ft_shifted<N>(u, T.c.inv_dx2, T.c.nu, a.sigma, x, y, z, p);
     }
     __syncthreads();
+      ft_stamp(a);
     const TailLevel& C = a.lv[L + 1];
     double* bc = sm + C.off_b;
     for (int p = threadIdx.x; p < NC * NC * NC; p += blockDim.x) {
@@ -376,6 +392,7 @@ __device__ void ft_level(const TailArgs& a, double* sm, bool zero) {
       bc[p] = fw_point<3>(t, g, x, y, z);
     }
     __syncthreads();
+      ft_stamp(a);
     ft_level<NC, L + 1>(a, sm, true);
     const double* ec = sm + C.off_u;
     for (int p = threadIdx.x; p < N * N * N; p += blockDim.x) {
@@ -383,11 +400,14 @@ __device__ void ft_level(const TailArgs& a, double* sm, bool zero) {
       u[p] = u[p] + lin_point<3>(ec, gc, x, y, z);
     }
     __syncthreads();
+      ft_stamp(a);
     for (int k = 0; k < a.post; ++k) {
       ft_colour<N>(u, b, T.c, a.sigma, a.omega, 1, false);
       __syncthreads();
+      ft_stamp(a);
       ft_colour<N>(u, b, T.c, a.sigma, a.omega, 0, false);
       __syncthreads();
+      ft_stamp(a);
     }
   }
 }
@@ -398,6 +418,7 @@ __device__ void tail_run(const TailArgs& a, const double* __restrict__ b_in, dou
                          int zero_guess, int ncycles, double* sm) {
   const TailLevel& L0 = a.lv[0];
   if (DIM == 3 && a.fast) {
+    ft_stamp(a);
     for (int i = threadIdx.x; i < a.m * a.m + a.m; i += blockDim.x) sm[a.lu_off + i] = a.lu[i];
     PL_FOR_SM_POINTS(L0.g) {
       int x, y, z;
@@ -407,6 +428,7 @@ __device__ void tail_run(const TailArgs& a, const double* __restrict__ b_in, dou
       if (!zero_guess) sm[L0.off_u + p] = u_io[gi];
     }
     __syncthreads();
+    ft_stamp(a);
     for (int cyc = 0; cyc < ncycles; ++cyc) {
       if (a.fast == 15) ft_level<15, 0>(a, sm, zero_guess && cyc == 0);
       else ft_level<7, 0>(a, sm, zero_guess && cyc == 0);
@@ -416,6 +438,7 @@ __device__ void tail_run(const TailArgs& a, const double* __restrict__ b_in, dou
       decode(L0.g, p, x, y, z);
       u_io[a.g0.at(x, y, z)] = sm[L0.off_u + p];
     }
+    ft_stamp(a);
     return;
   }
   if (a.lu_off >= 0)
@@ -531,6 +554,7 @@ struct MidArgs {
   int pre, post;
   double omega, sigma;
   int zero;                 // level 0 starts from a zero guess
+  int own_bar;              // mid_grid_bar instead of grid.sync (PL_OPT_MID_BAR)
 };
 
 // one colour of jor-rb, in place (k_rb arithmetic); zero: u == 0 on entry,
@@ -572,13 +596,44 @@ __device__ __forceinline__ void mid_colour(const MidLevel& L, const MidArgs& m, 
   }
 }
 
+// Grid barrier of k_mid (PL_OPT_MID_BAR): thread 0 of each CTA reads the
+// generation word, then arrives on the counter (acq_rel at gpu scope); the
+// last arriver resets the counter and publishes the next generation (release),
+// the others spin on it (acquire).  The counter is zero again after every
+// barrier, so consecutive launches share the words; cooperative launches are
+// fully co-resident, so no CTA of the next launch arrives before every CTA of
+// this one has left its last barrier.
+__device__ unsigned int g_mid_arrive = 0;
+__device__ unsigned int g_mid_gen = 0;
+
+__device__ __forceinline__ void mid_grid_bar() {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned int gen, old;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(gen) : "l"(&g_mid_gen) : "memory");
+    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;"
+                 : "=r"(old) : "l"(&g_mid_arrive) : "memory");
+    if (old == gridDim.x - 1) {
+      asm volatile("st.relaxed.gpu.global.u32 [%0], 0;" :: "l"(&g_mid_arrive) : "memory");
+      asm volatile("st.release.gpu.global.u32 [%0], %1;" :: "l"(&g_mid_gen), "r"(gen + 1) : "memory");
+    } else {
+      unsigned int cur;
+      do {
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(cur) : "l"(&g_mid_gen) : "memory");
+      } while (cur == gen);
+    }
+  }
+  __syncthreads();
+}
+
 template <int DIM>
 __global__ void __launch_bounds__(MID_THREADS) k_mid(MidArgs m, TailArgs ta) {
   cg::grid_group grid = cg::this_grid();
   int ph = 0;
 #define MID_SYNC()                                                              \
   do {                                                                          \
-    grid.sync();                                                                \
+    if (m.own_bar) mid_grid_bar();                                              \
+    else grid.sync();                                                           \
     if (m.trace && blockIdx.x == 0 && threadIdx.x == 0) {                       \
       unsigned long long t_;                                                    \
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                    \
@@ -720,6 +775,7 @@ static int launch_tail(MgPlan* P, int l0, double* u, const double* b, double sig
 int g_mid_enabled = 1;      // PL_OPT_MID
 int g_mid_tail_n = 15;      // PL_OPT_MID_TAIL_N: largest N the mid kernel leaves to its tail
 int g_mid_ctas = 0;         // PL_OPT_MID_CTAS: CTAs of the cooperative mid kernels (0: one per SM)
+int g_mid_bar = 0;          // PL_OPT_MID_BAR (A/B): k_mid's own grid barrier (slower: 98.6 vs 90.9 us at 63^3)
 
 // first tail level of the mid kernel (>= the plan's tail_start)
 static int mid_tail_level(const MgPlan* P) {
@@ -756,6 +812,7 @@ static int launch_mid(MgPlan* P, int l0, double* u, const double* b, double sigm
   m.omega = P->omega;
   m.sigma = sigma;
   m.zero = zero;
+  m.own_bar = g_mid_bar;
   double bytes = 0.0;
   for (int i = 0; i <= m.nmid; ++i) {
     const MgLevel& L = P->lv[l0 + i];
@@ -792,9 +849,10 @@ static int launch_mid(MgPlan* P, int l0, double* u, const double* b, double sigm
   const int nblk = g_mid_ctas > 0 && g_mid_ctas < grid ? g_mid_ctas : grid;
   static unsigned long long* trace = nullptr;
   static const bool tracing = std::getenv("PL_MID_TRACE") != nullptr;
-  if (tracing && !trace) cudaMalloc(&trace, 64 * sizeof(unsigned long long));
+  if (tracing && !trace) cudaMalloc(&trace, 128 * sizeof(unsigned long long));
   m.trace = tracing ? trace : nullptr;
-  if (tracing) cudaMemsetAsync(trace, 0, 64 * sizeof(unsigned long long), s);
+  ta.trace = tracing ? trace + 64 : nullptr;
+  if (tracing) cudaMemsetAsync(trace, 0, 128 * sizeof(unsigned long long), s);
   void* args[] = {&m, &ta};
   PL_PRE(K_MID);
   cudaError_t e = cudaLaunchCooperativeKernel((void*)k_mid<3>, nblk, MID_THREADS, args, smem, s);
@@ -806,6 +864,12 @@ static int launch_mid(MgPlan* P, int l0, double* u, const double* b, double sigm
     cudaStreamSynchronize(s);
     std::fprintf(stderr, "mid n=%d levels=%d:", P->lv[l0].g.N, m.nmid);
     for (int i = 1; i < 64 && h[i]; ++i) std::fprintf(stderr, " %.2f", (h[i] - h[i - 1]) * 1e-3);
+    std::fprintf(stderr, " us\n  tail phases:");
+    unsigned long long ht[64];
+    cudaMemcpyAsync(ht, trace + 64, sizeof(ht), cudaMemcpyDeviceToHost, s);
+    cudaStreamSynchronize(s);
+    for (int i = 2; i < 63 && i <= (int)ht[0]; ++i)
+      std::fprintf(stderr, " %.2f", (ht[i] - ht[i - 1]) * 1e-3);
     std::fprintf(stderr, " us\n");
   }
   PL_CHECK_LAUNCH(K_MID, bytes);

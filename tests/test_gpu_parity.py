@@ -470,12 +470,15 @@ def test_cooperative_mid_vcycle_equals_separate_launches(n, pre, post, omega):
     ref0 = mg.v_cycle(sop, torch.zeros_like(u), b, cfg)
     try:
         _capi.set_option(_capi.OPT_MID, 1)
-        for tail_n in (3, 7, 15):
-            _capi.set_option(_capi.OPT_MID_TAIL_N, tail_n)
-            assert torch.equal(mg.v_cycle(sop, u, b, cfg), ref), tail_n
-            assert torch.equal(mg.v_cycle(sop, torch.zeros_like(u), b, cfg), ref0), tail_n
+        for bar in (0, 1):   # grid.sync() (default) and k_mid's own grid barrier
+            _capi.set_option(_capi.OPT_MID_BAR, bar)
+            for tail_n in (3, 7, 15):
+                _capi.set_option(_capi.OPT_MID_TAIL_N, tail_n)
+                assert torch.equal(mg.v_cycle(sop, u, b, cfg), ref), (bar, tail_n)
+                assert torch.equal(mg.v_cycle(sop, torch.zeros_like(u), b, cfg), ref0), (bar, tail_n)
     finally:
         _capi.set_option(_capi.OPT_MID, 1)
+        _capi.set_option(_capi.OPT_MID_BAR, 0)
         _capi.set_option(_capi.OPT_MID_TAIL_N, 15)
 
 
