@@ -79,18 +79,25 @@ __device__ __forceinline__ double lin_point(const double* __restrict__ c, const 
     if (tx.two) b = lin_comb(ld(0, ty.j0, tx.j1), ty.two ? ld(0, ty.j1, tx.j1) : 0.0, ty.two);
     return lin_comb(a, b, tx.two);
   }
+  // 3-D: all eight taps loaded unconditionally (out-of-range ones read as 0.0)
+  // and combined by selects -- no lane-dependent loop trip counts, so a warp
+  // whose lanes alternate odd/even x does not serialise the two tap paths.
+  // lin_comb(a, b, false) == a for every b, so each result equals the
+  // reference-order evaluation above bit for bit.
   LinTap tz = lin_tap(iz);
-  double bx[2] = {0.0, 0.0};
-  for (int a = 0; a < (tx.two ? 2 : 1); ++a) {
-    int jx = a ? tx.j1 : tx.j0;
-    double by[2] = {0.0, 0.0};
-    for (int bidx = 0; bidx < (ty.two ? 2 : 1); ++bidx) {
-      int jy = bidx ? ty.j1 : ty.j0;
-      by[bidx] = lin_comb(ld(tz.j0, jy, jx), tz.two ? ld(tz.j1, jy, jx) : 0.0, tz.two);
+  double by[2][2];
+#pragma unroll
+  for (int a = 0; a < 2; ++a) {
+    const int jx = a ? tx.j1 : tx.j0;
+#pragma unroll
+    for (int bidx = 0; bidx < 2; ++bidx) {
+      const int jy = bidx ? ty.j1 : ty.j0;
+      by[a][bidx] = lin_comb(ld(tz.j0, jy, jx), ld(tz.j1, jy, jx), tz.two);
     }
-    bx[a] = lin_comb(by[0], by[1], ty.two);
   }
-  return lin_comb(bx[0], bx[1], tx.two);
+  const double bx0 = lin_comb(by[0][0], by[0][1], ty.two);
+  const double bx1 = lin_comb(by[1][0], by[1][1], ty.two);
+  return lin_comb(bx0, bx1, tx.two);
 }
 
 
