@@ -353,8 +353,15 @@ __device__ __forceinline__ void ft_lu27(const double* A, const double* b, double
   __syncthreads();
 }
 
+// ft_colour's zero-guess red pass at one point (u == 0 on entry)
+__device__ __forceinline__ double ft_red0(double bv, double omega, double d, int x, int y, int z) {
+  return is_red<3>(x, y, z) ? 0.0 + ((omega * bv) / d) : 0.0;
+}
+
+// fused: the zero-guess red pass (zero && pre > 0) was already applied by the
+// producer of b (the parent's full weighting or the tail's load loop)
 template <int N, int L>
-__device__ void ft_level(const TailArgs& a, double* sm, bool zero) {
+__device__ void ft_level(const TailArgs& a, double* sm, bool zero, bool fused = false) {
   const TailLevel& T = a.lv[L];
   double* u = sm + T.off_u;
   double* b = sm + T.off_b;
@@ -372,9 +379,11 @@ __device__ void ft_level(const TailArgs& a, double* sm, bool zero) {
       ft_stamp(a);
     }
     for (int k = 0; k < a.pre; ++k) {
-      ft_colour<N>(u, b, T.c, a.sigma, a.omega, 1, zero && k == 0);
-      __syncthreads();
-      ft_stamp(a);
+      if (!(fused && zero && k == 0)) {
+        ft_colour<N>(u, b, T.c, a.sigma, a.omega, 1, zero && k == 0);
+        __syncthreads();
+        ft_stamp(a);
+      }
       ft_colour<N>(u, b, T.c, a.sigma, a.omega, 0, false);
       __syncthreads();
       ft_stamp(a);
@@ -387,13 +396,21 @@ __device__ void ft_level(const TailArgs& a, double* sm, bool zero) {
       ft_stamp(a);
     const TailLevel& C = a.lv[L + 1];
     double* bc = sm + C.off_b;
+    // the coarse level starts from zero: its first red pass is fused here
+    // (NC == 3 is the LU, which has no sweeps)
+    constexpr bool FUSE = NC > 3;
+    const bool fz = FUSE && a.pre > 0;
+    double* uc = sm + C.off_u;
+    const double dc = shifted_diag<3>(gc, C.c, a.sigma, 1, 1, 1);
     for (int p = threadIdx.x; p < NC * NC * NC; p += blockDim.x) {
       const int x = p % NC, y = (p / NC) % NC, z = p / (NC * NC);
-      bc[p] = fw_point<3>(t, g, x, y, z);
+      const double v = fw_point<3>(t, g, x, y, z);
+      bc[p] = v;
+      if (fz) uc[p] = ft_red0(v, a.omega, dc, x, y, z);
     }
     __syncthreads();
       ft_stamp(a);
-    ft_level<NC, L + 1>(a, sm, true);
+    ft_level<NC, L + 1>(a, sm, true, fz);
     const double* ec = sm + C.off_u;
     for (int p = threadIdx.x; p < N * N * N; p += blockDim.x) {
       const int x = p % N, y = (p / N) % N, z = p / (N * N);
@@ -420,18 +437,23 @@ __device__ void tail_run(const TailArgs& a, const double* __restrict__ b_in, dou
   if (DIM == 3 && a.fast) {
     ft_stamp(a);
     for (int i = threadIdx.x; i < a.m * a.m + a.m; i += blockDim.x) sm[a.lu_off + i] = a.lu[i];
+    // zero guess: the first red pass of level 0 is fused into the load
+    const bool fz = zero_guess && a.pre > 0;
+    const double d0 = shifted_diag<3>(L0.g, L0.c, a.sigma, 1, 1, 1);
     PL_FOR_SM_POINTS(L0.g) {
       int x, y, z;
       decode(L0.g, p, x, y, z);
       const long long gi = a.g0.at(x, y, z);
-      sm[L0.off_b + p] = b_in[gi];
+      const double bv = b_in[gi];
+      sm[L0.off_b + p] = bv;
       if (!zero_guess) sm[L0.off_u + p] = u_io[gi];
+      else if (fz) sm[L0.off_u + p] = ft_red0(bv, a.omega, d0, x, y, z);
     }
     __syncthreads();
     ft_stamp(a);
     for (int cyc = 0; cyc < ncycles; ++cyc) {
-      if (a.fast == 15) ft_level<15, 0>(a, sm, zero_guess && cyc == 0);
-      else ft_level<7, 0>(a, sm, zero_guess && cyc == 0);
+      if (a.fast == 15) ft_level<15, 0>(a, sm, zero_guess && cyc == 0, fz && cyc == 0);
+      else ft_level<7, 0>(a, sm, zero_guess && cyc == 0, fz && cyc == 0);
     }
     PL_FOR_SM_POINTS(L0.g) {
       int x, y, z;
