@@ -34,7 +34,7 @@
 extern "C" {
 #endif
 
-#define PL_ABI_VERSION 1
+#define PL_ABI_VERSION 2
 
 #define PL_OK 0
 #define PL_ERR_MGCAP 1
@@ -45,13 +45,14 @@ extern "C" {
 
 /* smoother kinds (multigrid.py:26) */
 #define PL_SMOOTHER_JACOBI 0
-#define PL_SMOOTHER_GAUSS_SEIDEL 1 /* not on the GPU path: PL_ERR_UNSUPPORTED */
+#define PL_SMOOTHER_GAUSS_SEIDEL 1 /* lexicographic, hyperplane wavefront (gs.cu) */
 #define PL_SMOOTHER_JOR_RB 2
 
 /* solve status (multigrid.py:258) */
 #define PL_STATUS_FIXED 0
 #define PL_STATUS_CONVERGED 1
 #define PL_STATUS_STALLED 2
+#define PL_STATUS_DIRECT 3
 
 /* spatial restriction kinds (hierarchy.py:34, 66-71) */
 #define PL_RESTRICT_FULL_WEIGHTING 0
@@ -63,16 +64,14 @@ typedef struct pl_mg_plan pl_mg_plan;
 int pl_abi_version(void);
 const char* pl_last_error(void);
 
-/* runtime options (A/B testing of kernel variants; results are bit-identical) */
+/* runtime options (A/B testing of kernel variants; results are bit-identical).
+   Keys 3, 5, 12, 15, 16 and 21 belonged to removed dead-end variants and
+   are rejected. */
 #define PL_OPT_ZMARCH 0       /* 1 (default): TMA z-marching + fused sweeps, 3-D order 2 */
 #define PL_OPT_ZMARCH_MIN_N 1 /* smallest n-1 using them (default 127, >= 31) */
 #define PL_OPT_GRAPHS 2       /* 1 (default): FixedCycles sweeps replay as CUDA graphs */
-#define PL_OPT_ZRB_VARIANT 3  /* jor-rb TMA sweep kernel: 0 three barriers per plane, 4 (default)
-                                 register-pipelined one barrier per plane; bit-identical */
-#define PL_OPT_FUSE_PROLONG 4 /* 1: prolongation fused into the first post-sweep (TMA levels);
+#define PL_OPT_FUSE_PROLONG 4 /* 1: prolongation fused into the first Jacobi post-sweep pair (TMA levels);
                                  default 0 (separate per-cell prolongation is faster) */
-#define PL_OPT_CUBIC_VARIANT 5 /* 3-D cubic kernel: 0 staged loads, 1 TMA ring, 2 (default) TMA
-                                  ring with zero-padded branch-free tap chains; bit-identical */
 #define PL_OPT_MID 6          /* 1 (default): V-cycle levels below the TMA threshold and the tail
                                  run as one cooperative launch (3-D order-2 jor-rb) */
 #define PL_OPT_MID_TAIL_N 7   /* largest n-1 the cooperative kernel leaves to its one-CTA tail
@@ -81,21 +80,12 @@ const char* pl_last_error(void);
 #define PL_OPT_ZC_FLOOR 9     /* smallest z-chunk of the TMA kernels (power of two, default 16) */
 #define PL_OPT_FAST_TAIL 10   /* 1 (default): compile-time-sized 15^3/7^3 -> 3^3 jor-rb tail */
 #define PL_OPT_ZC_CTAS 11     /* CTA count the TMA kernels' z chunking aims for (default 1184) */
-#define PL_OPT_MID2 12        /* 1: the cooperative small-level kernel runs one grid phase per
-                                 level and direction (overlapped shared-memory tiles, LU fused
-                                 into the last down phase); 0 (default, measured faster): one
-                                 phase per former kernel plus the one-CTA tail */
 #define PL_OPT_MID_CTAS 13    /* CTAs of the cooperative small-level kernels (0, default: one per
                                  SM); pfasst_run's rank-stream schedule sets 32 for its duration
                                  so the other ranks' streams keep the remaining SMs */
 #define PL_OPT_ZRB_RING 14    /* one-barrier jor-rb sweep rings: 0 (default) 6 u + 3 b planes,
                                  4 CTAs/SM, z chunks >= 32 from 255^3 up, else 8 u + 4 b planes,
-                                 3 CTAs/SM; 1: always 6 + 3; 4: always 8 + 4; 2, 3: halo-work
-                                 layouts (slower); bit-identical */
-#define PL_OPT_RBRFW 15       /* 1: the last jor-rb pre-sweep, the residual and full weighting
-                                 run as one overlapped-tile pass (TMA levels); 0 (default,
-                                 measured faster): k_zrb3 then k_rfw; bit-identical */
-#define PL_OPT_RBRFW_ZCC 16   /* smallest coarse-plane z chunk of the fused pass (default 16) */
+                                 3 CTAs/SM; 1: always 6 + 3; 4: always 8 + 4; bit-identical */
 #define PL_OPT_FUSE_APPLY_RHS 17 /* 1 (default): the sweep's f refresh of node m and the next
                                     sub-step's right-hand side share one pass over y[m] (TMA
                                     levels); 0: separate apply and rhs launches; bit-identical */
@@ -108,10 +98,6 @@ const char* pl_last_error(void);
                                  tiled launch, and the FAS fine node integrals are full-weighted in
                                  the same pass (3-D, >= 127^3), never stored; 0: separate
                                  chain and full-weighting launches; bit-identical */
-#define PL_OPT_MID_BAR 21     /* grid barrier of the cooperative small-level V-cycle: 0 (default)
-                                 cooperative_groups grid.sync(); 1: one arrive counter +
-                                 generation word (acquire/release at gpu scope, self-resetting;
-                                 measured slower); bit-identical */
 int pl_set_option(int key, int value);
 
 /* storage elements of one field (incl. row pads) */
@@ -200,13 +186,17 @@ typedef struct pl_sweep_desc {
 size_t pl_sweep_workspace_bytes(int dim, int n, int m);
 /* sdc_sweep(states, y0, dt, op, mg_cfg, policy, tau) (sdc.py:84-114): Y, F are
    (M+1) x npts, in place; tau is (M+1) x npts or NULL.  Returns the V-cycles
-   in *cycles.  FixedCycles is asynchronous; ToTolerance synchronises per
-   solve.  On PL_ERR_MGCAP, *failed_substep (1-based), *fail_residual and
-   *fail_cycles describe the failed solve (SubStepError). */
+   in *cycles and, when substep_cycles / substep_status are non-NULL (host
+   arrays of M ints), the SolveResult.cycles and .status (PL_STATUS_*) of every
+   sub-step's solve (multigrid.py:261-288 as called at sdc.py:105-113).
+   FixedCycles is asynchronous; ToTolerance synchronises per solve.  On
+   PL_ERR_MGCAP, *failed_substep (1-based), *fail_residual and *fail_cycles
+   describe the failed solve (SubStepError) and the sub-step arrays hold the
+   solves before it. */
 int pl_sdc_sweep(pl_mg_plan* plan, const pl_sweep_desc* desc, double* Y, double* F,
                  const double* y0, const double* tau, double dt, void* workspace,
-                 size_t workspace_bytes, int* cycles, int* failed_substep,
-                 double* fail_residual, int* fail_cycles, void* stream);
+                 size_t workspace_bytes, int* cycles, int* substep_cycles, int* substep_status,
+                 int* failed_substep, double* fail_residual, int* fail_cycles, void* stream);
 /* residual(states, y0, dt, tau) (sdc.py:117-124): max-norm into out_dev
    (device double, asynchronous).  q is (M+1)x(M+1) row-major (host). */
 int pl_sdc_residual(const double* Y, const double* F, const double* y0, const double* tau,
@@ -238,7 +228,6 @@ int pl_coarse_correction(double* fineY, double* fineF, int mf, const double* coa
 size_t pl_coarse_correction_scratch_bytes(int dim, int nf, int nc, int mf, int interp_order);
 
 /* ---- runtime statistics (for bench.py / tests) -------------------------- */
-#define PL_NUM_KINDS 16
 /* counts and algorithmic bytes (SURVEY.md 8(d) model) of launched kernels */
 int pl_stats_reset(void);
 int pl_stats_get(long long* launches, double* alg_bytes, int nkinds);
@@ -250,25 +239,6 @@ int pl_timing_collect(int kind, long long* launches, double* total_ms, double* a
 /* the individual timed launches of one kind: algorithmic bytes and ms */
 int pl_timing_dump(int kind, long long nmax, double* bytes, float* ms, long long* n);
 const char* pl_kind_name(int kind);
-
-/* ---- time-rank communication (NCCL) ---------------
-   For non-Python hosts: the hand-offs of a multi-GPU PFASST run -- fine /
-   coarse payloads and the converged flag rank n -> n+1 (pfasst.py:107-118,
-   189-202 -> ncclSend/ncclRecv) and the block-boundary broadcast of the last
-   rank's value (pfasst.py:272-278 -> ncclBroadcast).  libnccl.so.2 is opened
-   at first use (no link-time dependency).  Byte counts; stream-ordered.
-   Pair a send with its matching recv inside pl_comm_group_start/end when one
-   process both sends and receives in the same step. */
-#define PL_COMM_ID_BYTES 128
-typedef struct pl_comm pl_comm;
-int pl_comm_unique_id(char* id /* PL_COMM_ID_BYTES */);
-int pl_comm_init(pl_comm** comm, const char* id, int rank, int nranks, int device);
-int pl_comm_destroy(pl_comm* comm);
-int pl_comm_group_start(void);
-int pl_comm_group_end(void);
-int pl_comm_send(pl_comm* comm, const void* buf, size_t bytes, int peer, void* stream);
-int pl_comm_recv(pl_comm* comm, void* buf, size_t bytes, int peer, void* stream);
-int pl_comm_bcast(pl_comm* comm, void* buf, size_t bytes, int root, void* stream);
 
 #ifdef __cplusplus
 }

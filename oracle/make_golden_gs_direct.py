@@ -33,6 +33,15 @@ def main():
 
     manifest = {"env": {"numpy": np.__version__, "python": platform.python_version(),
                         "reference": REF}, "cases": {}}
+    # per-solve log: multigrid.solve is looked up as a module attribute at
+    # sdc.py:107, so wrapping it records every sub-step solve in call order
+    log = []
+    real_solve = mg.solve
+
+    def logged_solve(op, u0, b, cfg, policy):
+        res = real_solve(op, u0, b, cfg, policy)
+        log.append([op.grid.n, op.sigma, res.cycles, res.status])
+        return res
     rng = np.random.default_rng(1407_0001)
 
     # ---- kernels: GS sweeps, GS V-cycles, Direct solves (multigrid.py:211-288)
@@ -62,16 +71,22 @@ def main():
     # ---- serial ISDC with GS + ToTolerance and with Direct (sdc.py:136-166)
     op = HeatOperator(Grid(1, 64), 1.0, 2)
     u0 = heat.initial_condition(op.grid, 1)
+    sdc.multigrid.solve = logged_solve
+    log.clear()
     r1 = sdc.run_sdc(op, quadrature.uniform_table(4), u0, 0.25, 4, 1e-10, 20,
                      mg.MgConfig(smoother="gauss-seidel"), mg.ToTolerance(1e-12))
+    solves_gs = [list(x) for x in log]
     op2 = HeatOperator(Grid(2, 16), 1.0, 4)
     u02 = seeded_field(2, 16)
+    log.clear()
     r2 = sdc.run_sdc(op2, quadrature.uniform_table(4), u02, 0.125, 2, 1e-11, 30,
                      mg.MgConfig(smoother="gauss-seidel"), mg.Direct())
+    solves_direct = [list(x) for x in log]
     manifest["cases"]["gsd_sdc"] = {
-        "gs": {"iterations": r1.iterations, "residuals": r1.residuals, "vcycles": r1.vcycles},
+        "gs": {"iterations": r1.iterations, "residuals": r1.residuals, "vcycles": r1.vcycles,
+               "solves": solves_gs},
         "direct": {"iterations": r2.iterations, "residuals": r2.residuals,
-                   "vcycles": r2.vcycles}}
+                   "vcycles": r2.vcycles, "solves": solves_direct}}
     np.savez_compressed(OUT / "gsd_sdc.npz", u0=u0, gs_u=r1.u, u02=u02, direct_u=r2.u)
 
     # ---- PFASST with the GS smoother (the reference's config default) and
@@ -89,6 +104,7 @@ def main():
                                   space_interp_order=4)
                   for n, m in zip(r["ns"], r["nodes"])]
         u0 = seeded_field(r["d"], r["ns"][0])
+        log.clear()
         res = pfasst.pfasst_run(levels, u0, r["dt"] * r["p"], r["p"], tol=r["tol"],
                                 max_iter=20, executor="serial")
         meta = {k: (list(v) if isinstance(v, tuple) else v) for k, v in r.items()
@@ -97,10 +113,12 @@ def main():
         meta.update(rank_iterations=res.rank_iterations, rank_vcycles=res.rank_vcycles,
                     converged=res.converged,
                     trace=[[t.block, t.rank, t.iteration, t.level, t.residual, t.vcycles]
-                           for t in res.trace])
+                           for t in res.trace],
+                    solves=[list(x) for x in log])
         manifest["cases"][f"gsd_run_{name}"] = meta
         np.savez_compressed(OUT / f"gsd_run_{name}.npz", u0=u0, u=res.u)
 
+    sdc.multigrid.solve = real_solve
     (OUT / "manifest_gsd.json").write_text(json.dumps(manifest, indent=1))
     print("wrote", len(manifest["cases"]), "cases")
 

@@ -592,7 +592,7 @@ def residual(st, y0, dt, tau=None):
     return float(np.max(np.abs(r)))
 
 
-def run_sdc(op, table, u0, t_end, n_steps, tol, max_iter, cfg, policy):
+def run_sdc(op, table, u0, t_end, n_steps, tol, max_iter, cfg, policy, solve_log=None):
     """sdc.py:136-166 -> dict(u, iterations, residuals, vcycles, exhausted)."""
     dt = t_end / n_steps
     u = u0
@@ -601,7 +601,7 @@ def run_sdc(op, table, u0, t_end, n_steps, tol, max_iter, cfg, policy):
         st = States.spread(op, table, u)
         hist = []
         for _ in range(max_iter):
-            out["vcycles"] += sdc_sweep(st, u, dt, op, cfg, policy)
+            out["vcycles"] += sdc_sweep(st, u, dt, op, cfg, policy, solve_log=solve_log)
             hist.append(residual(st, u, dt))
             if hist[-1] <= tol:
                 break

@@ -18,7 +18,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(PKG, "csrc")
 LIB_DIR = os.path.join(PKG, "lib")
 LIB = os.path.join(LIB_DIR, "libpintlab_b200.so")
-SOURCES = ["stencil.cu", "zmarch.cu", "transfer.cu", "sdc.cu", "mg.cu", "mid.cu", "gs.cu", "direct.cu", "capi.cu", "comm.cu"]
+SOURCES = ["stencil.cu", "zmarch.cu", "transfer.cu", "sdc.cu", "mg.cu", "gs.cu", "direct.cu", "capi.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-fmad=false", "-std=c++17", "-Xcompiler", "-fPIC",
          "-Xcompiler", "-O2", "-diag-suppress", "128"]

@@ -19,7 +19,7 @@ PL_ERR_ARG, PL_ERR_UNSUPPORTED, PL_ERR_STATE = -1, -2, -3
 PL_MAX_NODES = 17
 SMOOTHERS = {"jacobi": 0, "gauss-seidel": 1, "jor-rb": 2}
 RESTRICT = {"full-weighting": 0, "inject": 1, "copy": 2}
-STATUS = {0: "fixed", 1: "converged", 2: "stalled"}
+STATUS = {0: "fixed", 1: "converged", 2: "stalled", 3: "direct"}
 NUM_KINDS = 17          # refreshed from the library by num_kinds()
 
 _lib = None
@@ -46,6 +46,7 @@ _SIGS = {
     "pl_abi_version": (i32, []),
     "pl_last_error": (C.c_char_p, []),
     "pl_set_option": (i32, [i32, i32]),
+    "pl_field_elems": (i64, [i32, i32]),
     "pl_heat_apply": (i32, [vp, vp, i32, i32, f64, f64, i32, vp]),
     "pl_heat_diagonal": (i32, [vp, i32, i32, f64, f64, i32, f64, i32, vp]),
     "pl_shifted_apply": (i32, [vp, vp, i32, i32, f64, f64, i32, f64, vp]),
@@ -67,9 +68,9 @@ _SIGS = {
     "pl_sweep_workspace_bytes": (sz, [i32, i32, i32]),
     "pl_mg_set_direct": (i32, [vp, dp, dp, dp, dp, dp, vp]),
     "pl_mg_direct": (i32, [vp, vp, vp, f64, vp]),
-    "pl_sdc_sweep": (i32, [vp, C.POINTER(SweepDesc), vp, vp, vp, vp, f64, vp, sz, ip, ip, dp,
-                           ip, vp]),
-    "pl_sdc_residual": (i32, [vp, vp, vp, vp, dp, i32, f64, i64, vp, vp]),
+    "pl_sdc_sweep": (i32, [vp, C.POINTER(SweepDesc), vp, vp, vp, vp, f64, vp, sz, ip, ip, ip,
+                           ip, dp, ip, vp]),
+    "pl_sdc_residual": (i32, [vp, vp, vp, vp, dp, i32, f64, i32, i32, vp, vp]),
     "pl_restrict_state": (i32, [vp, ip, i32, vp, vp, i32, i32, i32, i32, f64, f64, i32, vp]),
     "pl_compute_fas": (i32, [vp, vp, i32, dp, ip, i32, vp, dp, i32, f64, vp, vp, i32, i32, i32,
                              i32, vp]),
@@ -83,14 +84,6 @@ _SIGS = {
     "pl_timing_collect": (i32, [i32, C.POINTER(i64), dp, dp]),
     "pl_timing_dump": (i32, [i32, i64, dp, C.POINTER(C.c_float), C.POINTER(i64)]),
     "pl_kind_name": (C.c_char_p, [i32]),
-    "pl_comm_unique_id": (i32, [C.c_char_p]),
-    "pl_comm_init": (i32, [C.POINTER(C.c_void_p), C.c_char_p, i32, i32, i32]),
-    "pl_comm_destroy": (i32, [C.c_void_p]),
-    "pl_comm_group_start": (i32, []),
-    "pl_comm_group_end": (i32, []),
-    "pl_comm_send": (i32, [C.c_void_p, C.c_void_p, C.c_size_t, i32, C.c_void_p]),
-    "pl_comm_recv": (i32, [C.c_void_p, C.c_void_p, C.c_size_t, i32, C.c_void_p]),
-    "pl_comm_bcast": (i32, [C.c_void_p, C.c_void_p, C.c_size_t, i32, C.c_void_p]),
 }
 
 EXPORTED = tuple(_SIGS)
@@ -112,7 +105,7 @@ def lib():
                 fn = getattr(h, name)
                 fn.restype = res
                 fn.argtypes = args
-            if h.pl_abi_version() != 1:
+            if h.pl_abi_version() != 2:
                 raise RuntimeError("ABI version mismatch")
             _lib = h
     return _lib
@@ -136,25 +129,19 @@ class MultigridErrorBase(RuntimeError):
 OPT_ZMARCH = 0
 OPT_ZMARCH_MIN_N = 1
 OPT_GRAPHS = 2
-OPT_ZRB_VARIANT = 3
 OPT_FUSE_PROLONG = 4
-OPT_CUBIC_VARIANT = 5
 OPT_MID = 6
 OPT_MID_TAIL_N = 7
 OPT_RFW = 8
 OPT_ZC_FLOOR = 9
 OPT_FAST_TAIL = 10
 OPT_ZC_CTAS = 11
-OPT_MID2 = 12
 OPT_MID_CTAS = 13
 OPT_ZRB_RING = 14
-OPT_RBRFW = 15
-OPT_RBRFW_ZCC = 16
 OPT_FUSE_APPLY_RHS = 17
 OPT_RFW_THREADS = 18
 OPT_ZREV = 19
 OPT_FUSE_FAS_FW = 20
-OPT_MID_BAR = 21
 
 
 _OPTION_VALUES = {}      # options set through this module (the library defaults otherwise)

@@ -1,6 +1,7 @@
 // extern "C" entry points (include/pintlab_b200.h), the SDC sweep and FAS
 // orchestration, and the runtime bookkeeping (errors, launch statistics,
 // per-kernel CUDA-event timing).
+#include <climits>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -83,7 +84,7 @@ void timing_post(int kind, cudaStream_t s, double alg_bytes) {
 static const char* kKindNames[K_NUM_KINDS] = {
     "apply", "jacobi", "jor_rb", "residual", "restrict", "prolong", "mg_tail", "norm",
     "quadrature", "rhs", "residual_max", "fas", "correction_time", "interp_cubic", "copy",
-    "lu", "mg_mid", "gauss_seidel", "direct", "jor_rb_restrict", "apply_rhs"};
+    "lu", "mg_mid", "gauss_seidel", "direct", "apply_rhs"};
 
 // ---------------------------------------------------------------------------
 // SDC sweep (sdc.py:84-114)
@@ -99,7 +100,8 @@ static Coef coef_from(const double* a, int rows, int cols) {
 
 static int sdc_sweep(MgPlan* P, const pl_sweep_desc* d, double* Y, double* F, const double* y0,
                      const double* tau, double dt, double* ws, size_t ws_bytes, int* cycles,
-                     int* failed, double* fres, int* fcyc, cudaStream_t s) {
+                     int* sub_cycles, int* sub_status, int* failed, double* fres, int* fcyc,
+                     cudaStream_t s) {
   const MgLevel& L = P->lv[0];
   const long long np = L.g.nstore;     // field stride / point-wise extent
   const int M = d->m;
@@ -143,8 +145,12 @@ static int sdc_sweep(MgPlan* P, const pl_sweep_desc* d, double* Y, double* F, co
     if (d->policy == 0) {
       PL_TRY(mg_cycles(P, ym1, R, dtm[m], d->fixed_cycles, 0, s));
       total += d->fixed_cycles;
+      if (sub_cycles) sub_cycles[m] = d->fixed_cycles;
+      if (sub_status) sub_status[m] = PL_STATUS_FIXED;
     } else if (d->policy == 2) {      // Direct: 0 cycles (multigrid.py:263-264)
       PL_TRY(mg_direct(P, ym1, R, dtm[m], s));
+      if (sub_cycles) sub_cycles[m] = 0;
+      if (sub_status) sub_status[m] = PL_STATUS_DIRECT;
     } else {
       int c = 0, st = 0;
       double res = 0;
@@ -158,6 +164,8 @@ static int sdc_sweep(MgPlan* P, const pl_sweep_desc* d, double* Y, double* F, co
       }
       if (rc) return rc;
       total += c;
+      if (sub_cycles) sub_cycles[m] = c;
+      if (sub_status) sub_status[m] = st;
     }
     if (m + 1 < M) PL_TRY(refresh_rhs(m + 1));
     else PL_TRY(launch_apply(ym1, F + (size_t)(m + 1) * np, L.g, L.c, s));   // sdc.py:112
@@ -224,22 +232,16 @@ extern "C" int g_graphs_enabled;
 
 namespace pl {
 extern int g_zmarch_enabled;
-extern int g_mid_bar;
 extern int g_zmarch_min_n;
-extern int g_zrb_variant;
 extern int g_fuse_prolong;
-extern int g_cubic_variant;
 extern int g_mid_enabled;
 extern int g_mid_tail_n;
 extern int g_rfw_enabled;
 extern int g_zc_floor;
 extern int g_zc_ctas;
 extern int g_fast_tail;
-extern int g_mid2_enabled;
 extern int g_mid_ctas;
 extern int g_zrb_ring;
-extern int g_rbrfw_enabled;
-extern int g_rbrfw_zcc;
 extern int g_rfw_threads;
 extern int g_zrev_mask;
 }
@@ -248,21 +250,29 @@ extern "C" {
 
 int pl_abi_version(void) { return PL_ABI_VERSION; }
 
+static int set_option_impl(int key, int value);
+// every option value accepted so far (INT_MIN: library default); part of the
+// CUDA-graph key, so a sweep captured under other options never replays
+static const int kMaxOptions = 64;
+static std::vector<int> g_opt_values(kMaxOptions, INT_MIN);
+static void drop_sweep_graphs(const void* plan);
+
 int pl_set_option(int key, int value) {
+  int rc = set_option_impl(key, value);
+  if (rc == 0 && key >= 0 && key < kMaxOptions) {
+    std::lock_guard<std::mutex> lk(g_stat_mu);
+    g_opt_values[key] = value;
+  }
+  return rc;
+}
+
+static int set_option_impl(int key, int value) {
   if (key == PL_OPT_ZMARCH) {
     g_zmarch_enabled = value != 0;
     return 0;
   }
   if (key == PL_OPT_GRAPHS) {
     g_graphs_enabled = value != 0;
-    return 0;
-  }
-  if (key == PL_OPT_ZRB_VARIANT) {
-    if (value != 0 && value != 4) {
-      set_error("zrb variant %d out of range (0 or 4)", value);
-      return -1;
-    }
-    g_zrb_variant = value;
     return 0;
   }
   if (key == PL_OPT_ZC_CTAS) {
@@ -301,40 +311,16 @@ int pl_set_option(int key, int value) {
     g_mid_ctas = value;
     return 0;
   }
-  if (key == PL_OPT_RBRFW_ZCC) {
-    if (value < 1) {
-      set_error("z chunk must be positive");
-      return PL_ERR_ARG;
-    }
-    g_rbrfw_zcc = value;
-    return 0;
-  }
-  if (key == PL_OPT_RBRFW) {
-    g_rbrfw_enabled = value != 0;
-    return 0;
-  }
   if (key == PL_OPT_ZRB_RING) {
-    if (value < 0 || value > 4) {
-      set_error("zrb ring variant %d out of range (0..4)", value);
+    if (value != 0 && value != 1 && value != 4) {
+      set_error("zrb ring variant %d must be 0, 1 or 4", value);
       return PL_ERR_ARG;
     }
     g_zrb_ring = value;
     return 0;
   }
-  if (key == PL_OPT_MID2) {
-    g_mid2_enabled = value != 0;
-    return 0;
-  }
   if (key == PL_OPT_MID_TAIL_N) {
     g_mid_tail_n = value;
-    return 0;
-  }
-  if (key == PL_OPT_CUBIC_VARIANT) {
-    if (value < 0 || value > 2) {
-      set_error("cubic variant %d out of range (0..2)", value);
-      return PL_ERR_ARG;
-    }
-    g_cubic_variant = value;
     return 0;
   }
   if (key == PL_OPT_FUSE_PROLONG) {
@@ -343,10 +329,6 @@ int pl_set_option(int key, int value) {
   }
   if (key == PL_OPT_FUSE_FAS_FW) {
     g_fuse_fas_fw = value != 0;
-    return 0;
-  }
-  if (key == PL_OPT_MID_BAR) {
-    g_mid_bar = value != 0;
     return 0;
   }
   if (key == PL_OPT_ZREV) {
@@ -457,6 +439,7 @@ int pl_mg_plan_create(pl_mg_plan** plan, int dim, int n, double length, double n
 }
 
 int pl_mg_plan_destroy(pl_mg_plan* plan) {
+  drop_sweep_graphs(plan);   // a recycled plan address must never replay a stale graph
   mg_plan_destroy((MgPlan*)plan);
   return 0;
 }
@@ -522,10 +505,11 @@ size_t pl_sweep_workspace_bytes(int dim, int n, int m) {
 struct SweepKey {
   const void *plan, *Y, *F, *y0, *tau, *ws;
   unsigned long long dt;
+  std::vector<int> opts;
   std::vector<double> coef;
   bool operator<(const SweepKey& o) const {
-    return std::tie(plan, Y, F, y0, tau, ws, dt, coef) <
-           std::tie(o.plan, o.Y, o.F, o.y0, o.tau, o.ws, o.dt, o.coef);
+    return std::tie(plan, Y, F, y0, tau, ws, dt, opts, coef) <
+           std::tie(o.plan, o.Y, o.F, o.y0, o.tau, o.ws, o.dt, o.opts, o.coef);
   }
 };
 struct SweepGraph {
@@ -534,35 +518,74 @@ struct SweepGraph {
   long long launches[K_NUM_KINDS];
   double bytes[K_NUM_KINDS];
 };
+// Bounded: a PFASST run uses one entry per (rank stream, level) buffer set;
+// past kMaxSweepGraphs the whole cache is dropped and recaptured on demand.
+static const size_t kMaxSweepGraphs = 512;
 static std::map<SweepKey, SweepGraph> g_sweep_graphs;
 static std::mutex g_graph_mu;
 static cudaStream_t g_capture_stream = nullptr;
 int g_graphs_enabled = 1;
 
+// destroy the captured sweeps of one plan (plan != NULL) or all of them;
+// callers must not hold g_graph_mu
+static void drop_sweep_graphs(const void* plan) {
+  std::lock_guard<std::mutex> lk(g_graph_mu);
+  for (auto it = g_sweep_graphs.begin(); it != g_sweep_graphs.end();) {
+    if (plan && it->first.plan != plan) {
+      ++it;
+      continue;
+    }
+    if (it->second.exec) cudaGraphExecDestroy(it->second.exec);
+    it = g_sweep_graphs.erase(it);
+  }
+}
+
+static void add_graph_stats(const SweepGraph& G) {
+  std::lock_guard<std::mutex> lk2(g_stat_mu);
+  for (int i = 0; i < K_NUM_KINDS; ++i) {
+    g_launches[i] += G.launches[i];
+    g_bytes[i] += G.bytes[i];
+  }
+}
+
+static void fixed_log(const pl_sweep_desc* d, int* sub_cycles, int* sub_status) {
+  for (int m = 0; m < d->m; ++m) {
+    if (sub_cycles) sub_cycles[m] = d->fixed_cycles;
+    if (sub_status) sub_status[m] = PL_STATUS_FIXED;
+  }
+}
+
 static int sweep_graphed(MgPlan* P, const pl_sweep_desc* d, double* Y, double* F,
                          const double* y0, const double* tau, double dt, double* ws,
-                         size_t ws_bytes, int* cycles, int* failed, double* fres, int* fcyc,
-                         cudaStream_t s) {
-  SweepKey k{P, Y, F, y0, tau, ws, 0, {}};
+                         size_t ws_bytes, int* cycles, int* sub_cycles, int* sub_status,
+                         int* failed, double* fres, int* fcyc, cudaStream_t s) {
+  SweepKey k{P, Y, F, y0, tau, ws, 0, {}, {}};
+  {
+    std::lock_guard<std::mutex> lk0(g_stat_mu);
+    k.opts = g_opt_values;
+  }
   std::memcpy(&k.dt, &dt, sizeof(dt));
   k.coef.assign(d->qdelta, d->qdelta + d->m * (d->m + 1));
   k.coef.insert(k.coef.end(), d->gammas, d->gammas + d->m);
   k.coef.push_back((double)d->fixed_cycles);
-  std::lock_guard<std::mutex> lk(g_graph_mu);
+  std::unique_lock<std::mutex> lk(g_graph_mu);
+  if (g_sweep_graphs.size() >= kMaxSweepGraphs && !g_sweep_graphs.count(k)) {
+    lk.unlock();
+    drop_sweep_graphs(nullptr);
+    lk.lock();
+  }
   SweepGraph& G = g_sweep_graphs[k];
   if (G.exec) {
     cudaError_t e = cudaGraphLaunch(G.exec, s);
     if (e != cudaSuccess) return cuda_status(e, "graph launch");
-    std::lock_guard<std::mutex> lk2(g_stat_mu);
-    for (int i = 0; i < K_NUM_KINDS; ++i) {
-      g_launches[i] += G.launches[i];
-      g_bytes[i] += G.bytes[i];
-    }
+    add_graph_stats(G);
     *cycles = d->m * d->fixed_cycles;
+    fixed_log(d, sub_cycles, sub_status);
     return 0;
   }
   if (++G.seen < 2)   // first use runs eagerly (lazy initialisation happens here)
-    return sdc_sweep(P, d, Y, F, y0, tau, dt, ws, ws_bytes, cycles, failed, fres, fcyc, s);
+    return sdc_sweep(P, d, Y, F, y0, tau, dt, ws, ws_bytes, cycles, sub_cycles, sub_status,
+                     failed, fres, fcyc, s);
   cudaError_t e;
   if (!g_capture_stream) {
     e = cudaStreamCreateWithFlags(&g_capture_stream, cudaStreamNonBlocking);
@@ -578,7 +601,8 @@ static int sweep_graphed(MgPlan* P, const pl_sweep_desc* d, double* Y, double* F
   cudaStream_t cs = g_capture_stream;
   e = cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal);
   if (e != cudaSuccess) return cuda_status(e, "begin capture");
-  int rc = sdc_sweep(P, d, Y, F, y0, tau, dt, ws, ws_bytes, cycles, failed, fres, fcyc, cs);
+  int rc = sdc_sweep(P, d, Y, F, y0, tau, dt, ws, ws_bytes, cycles, sub_cycles, sub_status,
+                     failed, fres, fcyc, cs);
   cudaGraph_t graph = nullptr;
   e = cudaStreamEndCapture(cs, &graph);
   if (rc) {
@@ -604,26 +628,23 @@ static int sweep_graphed(MgPlan* P, const pl_sweep_desc* d, double* Y, double* F
   // the capture stream is empty: order the replay after prior work on s
   e = cudaGraphLaunch(G.exec, s);
   if (e != cudaSuccess) return cuda_status(e, "graph launch");
-  std::lock_guard<std::mutex> lk2(g_stat_mu);
-  for (int i = 0; i < K_NUM_KINDS; ++i) {
-    g_launches[i] += G.launches[i];
-    g_bytes[i] += G.bytes[i];
-  }
+  add_graph_stats(G);
   return 0;
 }
 
 int pl_sdc_sweep(pl_mg_plan* plan, const pl_sweep_desc* desc, double* Y, double* F,
                  const double* y0, const double* tau, double dt, void* workspace,
-                 size_t workspace_bytes, int* cycles, int* failed_substep,
-                 double* fail_residual, int* fail_cycles, void* stream) {
+                 size_t workspace_bytes, int* cycles, int* substep_cycles, int* substep_status,
+                 int* failed_substep, double* fail_residual, int* fail_cycles, void* stream) {
   *failed_substep = 0;
   // per-launch event timing needs eager launches; ToTolerance syncs per solve
   if (g_graphs_enabled && desc->policy == 0 && g_time_mask == 0)
     return sweep_graphed((MgPlan*)plan, desc, Y, F, y0, tau, dt, (double*)workspace,
-                         workspace_bytes, cycles, failed_substep, fail_residual, fail_cycles,
-                         (cudaStream_t)stream);
+                         workspace_bytes, cycles, substep_cycles, substep_status, failed_substep,
+                         fail_residual, fail_cycles, (cudaStream_t)stream);
   return sdc_sweep((MgPlan*)plan, desc, Y, F, y0, tau, dt, (double*)workspace, workspace_bytes,
-                   cycles, failed_substep, fail_residual, fail_cycles, (cudaStream_t)stream);
+                   cycles, substep_cycles, substep_status, failed_substep, fail_residual,
+                   fail_cycles, (cudaStream_t)stream);
 }
 
 int pl_sdc_residual(const double* Y, const double* F, const double* y0, const double* tau,

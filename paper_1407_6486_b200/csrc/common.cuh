@@ -46,7 +46,7 @@ void timing_post(int kind, cudaStream_t s, double alg_bytes);
 enum KernelKind {
   K_APPLY = 0, K_JACOBI, K_RB, K_RESID, K_RESTRICT, K_PROLONG, K_TAIL,
   K_NORM, K_QUAD, K_RHS, K_RESMAX, K_FAS, K_CORR, K_INTERP, K_COPY, K_LU, K_MID, K_GS,
-  K_DIRECT, K_RBRFW, K_APPLY_RHS, K_NUM_KINDS
+  K_DIRECT, K_APPLY_RHS, K_NUM_KINDS
 };
 
 // ---------------------------------------------------------------------------

@@ -75,13 +75,20 @@ int launch_gs(double* u, const double* b, double* t, const Geo& g, const OpC& c,
       k_gs_line<<<1, 32, 0, s>>>(u, t, g, c, sigma);
     } else {
       void* kern = g.dim == 2 ? (void*)k_gs_wave<2> : (void*)k_gs_wave<3>;
-      static int grid[4] = {0, 0, 0, 0};
+      // resident grid, cached per device and dimension
+      static int grid_of[64][4] = {};
+      int dev = 0;
+      cudaGetDevice(&dev);
+      int* grid = grid_of[dev & 63];
       if (grid[g.dim] == 0) {
-        int dev = 0, sms = 0, per = 0;
-        cudaGetDevice(&dev);
+        int sms = 0, per = 0;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, GS_THREADS, 0);
-        grid[g.dim] = sms * (per < 2 ? (per < 1 ? 1 : per) : 2);
+        if (per < 1) {
+          set_error("gauss-seidel wavefront kernel does not fit one CTA per SM");
+          return 2;   // PL_ERR_CUDA
+        }
+        grid[g.dim] = sms * (per < 2 ? per : 2);
       }
       // enough threads for the widest hyperplane, at most the resident grid
       const long long width = g.dim == 2 ? g.ny : (long long)g.ny * g.nz;

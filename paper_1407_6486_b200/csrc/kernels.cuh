@@ -52,19 +52,15 @@ int zlaunch_jacobi(const double* u, const double* b, double* out, const Geo& g, 
 // two fused Jacobi sweeps u -> out (out != u); e non-null: u + P_lin e first
 int zlaunch_jacobi2(const double* u, const double* b, double* out, const Geo& g, const OpC& c,
                     double sigma, double omega, int zero_in, const double* e, cudaStream_t s);
-// one fused red+black jor-rb sweep u -> out (out != u); e non-null: u + P_lin e first
+// one fused red+black jor-rb sweep u -> out (out != u)
 int zlaunch_rb(const double* u, const double* b, double* out, const Geo& g, const OpC& c,
-               double sigma, double omega, const double* e, cudaStream_t s);
+               double sigma, double omega, cudaStream_t s);
 
 // coarse = FW(b - (I - sigma A) u) in one pass (residual never stored)
 bool zmarch_rfw();   // PL_OPT_RFW
 int zlaunch_rfw(const double* u, const double* b, double* coarse, const Geo& g, const OpC& c,
                 double sigma, cudaStream_t s);
 
-// last jor-rb pre-sweep u -> out (out != u) fused with coarse = FW(b - A out)
-extern int g_rbrfw_enabled;   // PL_OPT_RBRFW
-int zlaunch_rbrfw(const double* u, const double* b, double* out, double* coarse, const Geo& g,
-                  const OpC& c, double sigma, double omega, cudaStream_t s);
 
 // fine (+)= P_cubic coarse, 3-D, TMA-staged coarse planes (taps of cubic_taps)
 int zlaunch_cubic(const double* coarse, double* fine, const Geo& gf, const int* cnt,

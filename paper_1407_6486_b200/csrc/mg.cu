@@ -576,7 +576,6 @@ struct MidArgs {
   int pre, post;
   double omega, sigma;
   int zero;                 // level 0 starts from a zero guess
-  int own_bar;              // mid_grid_bar instead of grid.sync (PL_OPT_MID_BAR)
 };
 
 // one colour of jor-rb, in place (k_rb arithmetic); zero: u == 0 on entry,
@@ -618,44 +617,13 @@ __device__ __forceinline__ void mid_colour(const MidLevel& L, const MidArgs& m, 
   }
 }
 
-// Grid barrier of k_mid (PL_OPT_MID_BAR): thread 0 of each CTA reads the
-// generation word, then arrives on the counter (acq_rel at gpu scope); the
-// last arriver resets the counter and publishes the next generation (release),
-// the others spin on it (acquire).  The counter is zero again after every
-// barrier, so consecutive launches share the words; cooperative launches are
-// fully co-resident, so no CTA of the next launch arrives before every CTA of
-// this one has left its last barrier.
-__device__ unsigned int g_mid_arrive = 0;
-__device__ unsigned int g_mid_gen = 0;
-
-__device__ __forceinline__ void mid_grid_bar() {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    unsigned int gen, old;
-    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(gen) : "l"(&g_mid_gen) : "memory");
-    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;"
-                 : "=r"(old) : "l"(&g_mid_arrive) : "memory");
-    if (old == gridDim.x - 1) {
-      asm volatile("st.relaxed.gpu.global.u32 [%0], 0;" :: "l"(&g_mid_arrive) : "memory");
-      asm volatile("st.release.gpu.global.u32 [%0], %1;" :: "l"(&g_mid_gen), "r"(gen + 1) : "memory");
-    } else {
-      unsigned int cur;
-      do {
-        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(cur) : "l"(&g_mid_gen) : "memory");
-      } while (cur == gen);
-    }
-  }
-  __syncthreads();
-}
-
 template <int DIM>
 __global__ void __launch_bounds__(MID_THREADS) k_mid(MidArgs m, TailArgs ta) {
   cg::grid_group grid = cg::this_grid();
   int ph = 0;
 #define MID_SYNC()                                                              \
   do {                                                                          \
-    if (m.own_bar) mid_grid_bar();                                              \
-    else grid.sync();                                                           \
+    grid.sync();                                                                \
     if (m.trace && blockIdx.x == 0 && threadIdx.x == 0) {                       \
       unsigned long long t_;                                                    \
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                    \
@@ -797,7 +765,6 @@ static int launch_tail(MgPlan* P, int l0, double* u, const double* b, double sig
 int g_mid_enabled = 1;      // PL_OPT_MID
 int g_mid_tail_n = 15;      // PL_OPT_MID_TAIL_N: largest N the mid kernel leaves to its tail
 int g_mid_ctas = 0;         // PL_OPT_MID_CTAS: CTAs of the cooperative mid kernels (0: one per SM)
-int g_mid_bar = 0;          // PL_OPT_MID_BAR (A/B): k_mid's own grid barrier (slower: 98.6 vs 90.9 us at 63^3)
 
 // first tail level of the mid kernel (>= the plan's tail_start)
 static int mid_tail_level(const MgPlan* P) {
@@ -811,20 +778,8 @@ static bool mid_applies(const MgPlan* P, int l) {
          l < mid_tail_level(P) && mid_tail_level(P) - l <= MID_MAX;
 }
 
-bool mid2_applies(const MgPlan* P, int l0);
-int launch_mid2(MgPlan* P, int l0, double* u, const double* b, double sigma, int zero,
-                const double* lu_dev, cudaStream_t s);
-
 static int launch_mid(MgPlan* P, int l0, double* u, const double* b, double sigma, int zero,
                       cudaStream_t s) {
-  if (mid2_applies(P, l0)) {
-    auto it = P->lu.find(*(unsigned long long*)&sigma);
-    if (it == P->lu.end()) {
-      set_error("coarsest LU for sigma=%.17g not prepared", sigma);
-      return -3;
-    }
-    return launch_mid2(P, l0, u, b, sigma, zero, it->second.dev, s);
-  }
   const int lt = mid_tail_level(P);
   MidArgs m;
   std::memset(&m, 0, sizeof(m));
@@ -834,7 +789,6 @@ static int launch_mid(MgPlan* P, int l0, double* u, const double* b, double sigm
   m.omega = P->omega;
   m.sigma = sigma;
   m.zero = zero;
-  m.own_bar = g_mid_bar;
   double bytes = 0.0;
   for (int i = 0; i <= m.nmid; ++i) {
     const MgLevel& L = P->lv[l0 + i];
@@ -853,20 +807,23 @@ static int launch_mid(MgPlan* P, int l0, double* u, const double* b, double sigm
   TailArgs ta;
   size_t smem = 0;
   PL_TRY(tail_args(P, lt, sigma, ta, &smem));
-  static int grid = 0;
+  // one CTA per SM, cached per device once the occupancy check has passed
+  static int grid_of[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  int& grid = grid_of[dev & 63];
   if (grid == 0) {
-    int dev = 0, sms = 0, per = 0;
-    cudaGetDevice(&dev);
+    int sms = 0, per = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaFuncSetAttribute(k_mid<3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)TAIL_SMEM_BUDGET + 8192);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_mid<3>, MID_THREADS,
                                                   TAIL_SMEM_BUDGET + 8192);
-    grid = sms * (per > 0 ? 1 : 1);
     if (per < 1) {
       set_error("mid kernel does not fit one CTA per SM");
       return 2;
     }
+    grid = sms;
   }
   const int nblk = g_mid_ctas > 0 && g_mid_ctas < grid ? g_mid_ctas : grid;
   static unsigned long long* trace = nullptr;
@@ -1192,7 +1149,7 @@ static int level_smooth(MgPlan* P, MgLevel& L, double** cur, double* alt_u, cons
   }
   for (int k = 0; k < count; ++k) {
     if (fused) {            // red and black in one pass, out of place
-      PL_TRY(zlaunch_rb(u, b, other, L.g, L.c, sigma, P->omega, nullptr, s));
+      PL_TRY(zlaunch_rb(u, b, other, L.g, L.c, sigma, P->omega, s));
       std::swap(u, other);
     } else if (P->order == 2) {    // same-colour points never neighbour: in place
       PL_TRY(launch_rb(u, b, u, L.g, L.c, sigma, P->omega, 1, s));
@@ -1215,32 +1172,19 @@ static int vcycle(MgPlan* P, int l, double* u, const double* b, double sigma, bo
   MgLevel& C = P->lv[l + 1];
   double* cur = u;
   const bool zm = zmarch_ok(L.g, L.c);
-  if (zm && zmarch_rfw() && g_rbrfw_enabled && P->smoother == SM_RB && P->pre >= 1) {
-    // last pre-sweep + residual + full weighting in one pass (k_rbrfw)
-    PL_TRY(level_smooth(P, L, &cur, u, b, sigma, P->pre - 1, zero, s));
-    double* other = (cur == u) ? L.t : u;
-    PL_TRY(zlaunch_rbrfw(cur, b, other, C.b, L.g, L.c, sigma, P->omega, s));
-    cur = other;
+  PL_TRY(level_smooth(P, L, &cur, u, b, sigma, P->pre, zero, s));
+  if (zm && zmarch_rfw()) {
+    PL_TRY(zlaunch_rfw(cur, b, C.b, L.g, L.c, sigma, s));
   } else {
-    PL_TRY(level_smooth(P, L, &cur, u, b, sigma, P->pre, zero, s));
-    if (zm && zmarch_rfw()) {
-      PL_TRY(zlaunch_rfw(cur, b, C.b, L.g, L.c, sigma, s));
-    } else {
-      double* r = (cur == u) ? L.t : u;
-      PL_TRY(launch_residual(cur, b, r, L.g, L.c, sigma, s));
-      PL_TRY(launch_fw(r, C.b, L.g, s));
-    }
+    double* r = (cur == u) ? L.t : u;
+    PL_TRY(launch_residual(cur, b, r, L.g, L.c, sigma, s));
+    PL_TRY(launch_fw(r, C.b, L.g, s));
   }
   PL_TRY(vcycle(P, l + 1, C.u, C.b, sigma, true, s));
-  // u += P e_c, then post-smoothing; fused into the first post-sweep pass
-  // when the TMA kernels cover this level (multigrid.py:250-251)
+  // u += P e_c, then post-smoothing (multigrid.py:250-251); with
+  // PL_OPT_FUSE_PROLONG the Jacobi pair on the TMA levels does both
   int post = P->post;
-  if (zmarch_ok(L.g, L.c) && zmarch_fuse_prolong() && P->smoother == SM_RB && post >= 1) {
-    double* other = (cur == u) ? L.t : u;
-    PL_TRY(zlaunch_rb(cur, b, other, L.g, L.c, sigma, P->omega, C.u, s));
-    cur = other;
-    post -= 1;
-  } else if (zmarch_ok(L.g, L.c) && zmarch_fuse_prolong() && P->smoother == SM_JACOBI &&
+  if (zmarch_ok(L.g, L.c) && zmarch_fuse_prolong() && P->smoother == SM_JACOBI &&
              post >= 2) {
     double* other = (cur == u) ? L.t : u;
     PL_TRY(zlaunch_jacobi2(cur, b, other, L.g, L.c, sigma, P->omega, 0, C.u, s));

@@ -38,13 +38,11 @@
 namespace pl {
 
 extern int g_zrb_ring;   // PL_OPT_ZRB_RING: 0 8+4 plane rings (3 CTAs/SM), 1 6+3 (4 CTAs/SM)
-extern int g_rbrfw_zcc;  // PL_OPT_RBRFW_ZCC: smallest coarse z chunk of k_rbrfw
 
 namespace {
 
 constexpr int TX = 32, TY = 16;           // output tile
 constexpr int NTHR = 256;                 // k_z1 / k_z2: 32 x 8 threads, 2 rows each
-constexpr int NTHR_RB = 320;              // k_zrb: one red point of the halo-1 window each
 
 // ---- TMA / mbarrier primitives --------------------------------------------
 
@@ -548,102 +546,6 @@ __global__ void __launch_bounds__(NTHR) k_z2(const __grid_constant__ CUtensorMap
   }
 }
 
-// one fused jor-rb sweep (optionally after the prolongation)
-template <bool POW2, bool PRO, int PREF>
-__global__ void __launch_bounds__(NTHR_RB) k_zrb(const __grid_constant__ CUtensorMap mu,
-                                                 const __grid_constant__ CUtensorMap mb,
-                                                 const __grid_constant__ CUtensorMap me,
-                                                 double* __restrict__ out, Geo g, OpC c,
-                                                 double sigma, double omega, double dval,
-                                                 int zc) {
-  using S = Stager<NTHR_RB, PRO, PREF>;
-  constexpr int NRED = (TX + 2) / 2 * (TY + 2);                     // red points of halo-1
-  constexpr int PERR = (NRED + NTHR_RB - 1) / NTHR_RB;
-  extern __shared__ __align__(128) double sm[];
-  const int tid = threadIdx.x;
-  S st;
-  st.setup(sm, &mu, &mb, &me, zc, g, tid);
-  const int x0 = st.x0, y0 = st.y0, z0 = st.z0, z1 = st.z1;
-  // red list: window point j -> (yy, xx) with xx = 2 (j % 17) + ((yy + zz + 1) & 1)
-  // (x0, y0 even); per plane parity: u-window index, b-window index, in-domain
-  int r_iu[2][PERR], r_ib[2][PERR];
-  bool r_in[2][PERR];
-#pragma unroll
-  for (int par = 0; par < 2; ++par)
-#pragma unroll
-    for (int q = 0; q < PERR; ++q) {
-      int j = tid + q * NTHR_RB;
-      int yy = j / ((TX + 2) / 2), xr = j - yy * ((TX + 2) / 2);
-      int xx = 2 * xr + ((yy + par + 1) & 1);
-      int gx = x0 - 1 + xx, gy = y0 - 1 + yy;
-      r_iu[par][q] = (yy + 1) * UX + xx + 1;
-      r_ib[par][q] = yy * BW + xx + 1;
-      r_in[par][q] = j < NRED && gx >= 0 && gx < g.nx && gy >= 0 && gy < g.ny;
-    }
-  // black pair: tile row `row`, x = 2 px + {0, 1}; black x has (x + row + z) even
-  const int px = tid & 15, row = tid >> 4;
-  const int gy = y0 + row;
-  auto red_update = [&](int zz) {
-    if (zz < 0 || zz >= g.nz) return;       // ghost planes stay zero
-    const int par = zz & 1;
-    double* pc = st.uplane(zz);
-    const double* pm = st.uplane(zz - 1);
-    const double* pp = st.uplane(zz + 1);
-    const double* pb = st.bplane(zz);
-#pragma unroll
-    for (int q = 0; q < PERR; ++q) {
-      if (r_in[par][q]) {
-        const int i = r_iu[par][q];
-        const double r = pb[r_ib[par][q]] - (pc[i] - sigma * lap7<POW2, UX>(pm, pc, pp, i, c));
-        pc[i] = pc[i] + ((omega * r) / dval);
-      }
-    }
-  };
-
-  if (tid == 0)
-    for (int p = z0 - 2; p <= z0 + PREF; ++p) st.issue(p, false);
-  for (int p = z0 - 2; p <= z0 + 1; ++p) {
-    st.wait_u(p);
-    __syncthreads();
-    st.prolong(p, g);
-  }
-  st.wait_b(z0 - 1);
-  st.wait_b(z0);
-  __syncthreads();
-  red_update(z0 - 1);
-  __syncthreads();
-  red_update(z0);
-  for (int z = z0; z < z1; ++z) {
-    st.wait_u(z + 2);
-    st.wait_b(z + 1);
-    if (PRO) {
-      st.prolong(z + 2, g);
-      __syncthreads();
-    }
-    // red(z+1) reads only black points of planes z..z+2 and its own centre
-    red_update(z + 1);
-    __syncthreads();
-    const int par = (row + z) & 1;
-    const int xb = 2 * px + par, xr = 2 * px + 1 - par;
-    const double* pm = st.uplane(z - 1);
-    const double* pc = st.uplane(z);
-    const double* pp = st.uplane(z + 1);
-    const double* pb = st.bplane(z);
-    if (tid < 16 * TY && gy < g.ny) {
-      const int gxb = x0 + xb, gxr = x0 + xr;
-      const int ib = (row + 2) * UX + xb + 2;
-      if (gxb < g.nx) {
-        const double rr =
-            pb[(row + 1) * BW + xb + 2] - (pc[ib] - sigma * lap7<POW2, UX>(pm, pc, pp, ib, c));
-        out[g.at(gxb, gy, z)] = pc[ib] + ((omega * rr) / dval);
-      }
-      if (gxr < g.nx) out[g.at(gxr, gy, z)] = pc[(row + 2) * UX + xr + 2];
-    }
-    __syncthreads();   // u plane z-1 and b plane z are free
-    if (tid == 0) st.issue(z + PREF + 1, false);
-  }
-}
-
 // ---------------------------------------------------------------------------
 // helpers of the one-barrier red-black sweep (k_zrb3)
 
@@ -822,48 +724,8 @@ __device__ __forceinline__ void rb_phase(const RbCtx& k, int z, const double2& U
   else if (k.va) dst[0] = w.x;
 }
 
-// rb_phase with this thread's halo red point (plane q = z+2, parity slot P)
-// evaluated in the same straight-line code: the 50 halo reds are dealt to
-// lanes 0..6 of every warp, so no warp carries a serial halo update after its
-// interior pair (the barrier then waits for the slowest of equal warps), and
-// the third chain adds instruction-level parallelism.  Lanes without a halo
-// point compute on a safe index and store nothing.
-template <bool POW2, int RU, int RB, int PAR, int P>
-__device__ __forceinline__ void rb_phase_h(const RbCtx& k, int z, const double2& U0, double2& U1,
-                                           const double2& U2, double2& U3, const double2& U4,
-                                           const double2& B0, const double2& B2) {
-  const int q = z + 2;
-  double* plr = rb_u<RU>(k, q);
-  const double* plb = rb_u<RU>(k, z);
-  const bool hv = (P ? k.hv1 : k.hv0) && q <= k.R;
-  const int hi = hv ? (P ? k.hu1 : k.hu0) : k.iu;
-  const int hb = hv ? (P ? k.hb1 : k.hb0) : k.ib;
-  const double* pm = rb_u<RU>(k, q - 1);
-  const double* pp = rb_u<RU>(k, q + 1);
-  const double* bq = rb_b<RB>(k, q);
-  Relax rr = rb_point_fast<POW2, 1 - PAR>(k, plr, U2, U3, U4, B2);
-  Relax rbk = rb_point_fast<POW2, PAR>(k, plb, U0, U1, U2, B0);
-  Relax rh = rb_fast<POW2>(k, pm[hi], pp[hi], plr[hi - UX], plr[hi + UX], plr[hi - 1],
-                           plr[hi + 1], plr[hi], bq[hb]);
-  if (__builtin_expect(!(quot_ok(rr.a) && quot_ok(rbk.a) && quot_ok(rh.a)), 0)) {
-    if (!quot_ok(rr.a)) rr.q = div_slow(rr.a, k.dval);
-    if (!quot_ok(rbk.a)) rbk.q = div_slow(rbk.a, k.dval);
-    if (!quot_ok(rh.a)) rh.q = div_slow(rh.a, k.dval);
-  }
-  const double vr = rr.cc + rr.q, vb = rbk.cc + rbk.q, vh = rh.cc + rh.q;
-  if (q <= k.R && (PAR ? k.va : k.vb)) {
-    plr[k.iu + 1 - PAR] = vr;
-    set_mem<1 - PAR>(U3, vr);
-  }
-  if (hv) plr[hi] = vh;
-  double* dst = k.optr + (long long)z * k.sz;
-  const double2 w = PAR ? make_double2(U1.x, vb) : make_double2(vb, U1.y);
-  if (k.va && k.vb) *reinterpret_cast<double2*>(dst) = w;
-  else if (k.va) dst[0] = w.x;
-}
-
-template <bool POW2, int RU, int RB, int MINB, bool HW, bool HM = false>
-__global__ void __launch_bounds__(HW ? 320 : NTHR_RB2, MINB) k_zrb3(const __grid_constant__ CUtensorMap mu,
+template <bool POW2, int RU, int RB, int MINB>
+__global__ void __launch_bounds__(NTHR_RB2, MINB) k_zrb3(const __grid_constant__ CUtensorMap mu,
                                                       const __grid_constant__ CUtensorMap mb,
                                                       double* __restrict__ out, Geo g, OpC c,
                                                       double sigma, double omega, double dval,
@@ -880,7 +742,7 @@ __global__ void __launch_bounds__(HW ? 320 : NTHR_RB2, MINB) k_zrb3(const __grid
   const int z0 = blockIdx.z * zc, z1 = min(z0 + zc, g.nz);
   // the in-loop TMA issues go to the first lane of warp 7, which owns no
   // halo point, so the halo warps 0-1 are not delayed further after a barrier
-  constexpr int issuer = HW ? 288 : NTHR_RB2 - 32;   // HW: halo warp 9 (one update per lane)
+  constexpr int issuer = NTHR_RB2 - 32;
   k.z0 = z0;
   k.R = min(z1, g.nz - 1);
   const int uhi = k.R + 1, bhi = k.R;
@@ -928,12 +790,9 @@ __global__ void __launch_bounds__(HW ? 320 : NTHR_RB2, MINB) k_zrb3(const __grid
   k.ib = (row + 1) * BW + 2 * px + 2;
   k.optr = out + (long long)gy * g.sy + gxa;
   k.sz = g.sz;
-  // HW: warps 8-9 (threads 256..305) own the 50 halo reds and nothing else,
-  // so no warp does more than two updates per phase
-  // halo red ids: HW dedicated warps 8-9; HM lanes 0..6 of every warp; else threads 0..49
-  const int hid = HW ? tid - 256 : (HM ? (lane < 7 ? warp * 7 + lane : 99) : tid);
-  const bool is_halo = HW ? warp >= 8 : hid < 50;
-  const bool is_int = HW ? warp < 8 : true;
+  // halo red ids: threads 0..49
+  const int hid = tid;
+  const bool is_halo = hid < 50;
   {
     int hu[2], hb[2];
     bool hv[2];
@@ -958,11 +817,6 @@ __global__ void __launch_bounds__(HW ? 320 : NTHR_RB2, MINB) k_zrb3(const __grid
   for (int p = z0 - 2; p <= min(z0 + 2, uhi); ++p) wait_u(p);
   for (int q = z0 - 1; q <= min(z0, bhi); ++q) wait_b(q);
   const double2 zero2 = make_double2(0.0, 0.0);
-  if (HW && !is_int) {      // interior registers of the halo warps are unused
-    k.iu = 2 * UX + 2;
-    k.ib = BW + 2;
-    k.va = k.vb = false;
-  }
   double2 Um2 = lds2(rb_u<RU>(k, z0 - 2) + k.iu);
   double2 U0 = lds2(rb_u<RU>(k, z0 - 1) + k.iu);
   double2 U1 = lds2(rb_u<RU>(k, z0) + k.iu);
@@ -985,10 +839,8 @@ __global__ void __launch_bounds__(HW ? 320 : NTHR_RB2, MINB) k_zrb3(const __grid
       if (k.vb) { pl[k.iu + 1] = v; uc.y = v; }
     }
   };
-  if (is_int) {
-    pro_red(z0 - 1, Um2, U0, U1, Bm1, 1 - wpar);
-    pro_red(z0, U0, U1, U2, B0, wpar);
-  }
+  pro_red(z0 - 1, Um2, U0, U1, Bm1, 1 - wpar);
+  pro_red(z0, U0, U1, U2, B0, wpar);
   if (is_halo) {
     rb_halo<POW2, RU, RB, 1>(k, z0 - 1);
     rb_halo<POW2, RU, RB, 0>(k, z0);
@@ -999,7 +851,7 @@ __global__ void __launch_bounds__(HW ? 320 : NTHR_RB2, MINB) k_zrb3(const __grid
   }
   if (z0 + 1 <= bhi) wait_b(z0 + 1);
   double2 B1 = z0 + 1 <= bhi ? lds2(rb_b<RB>(k, z0 + 1) + k.ib) : zero2;
-  if (is_int) pro_red(z0 + 1, U1, U2, U3, B1, 1 - wpar);
+  pro_red(z0 + 1, U1, U2, U3, B1, 1 - wpar);
   if (is_halo) rb_halo<POW2, RU, RB, 1>(k, z0 + 1);
   __syncthreads();
   if (tid == 0) {       // u planes z0-2, z0-1 and b planes z0-1 .. z0+1 are dead
@@ -1026,12 +878,8 @@ __global__ void __launch_bounds__(HW ? 320 : NTHR_RB2, MINB) k_zrb3(const __grid
       }
       double2 U4 = lds2(rb_u<RU>(k, z + 3) + k.iu);   // stale beyond R: unused
       const double2 B2 = lds2(rb_b<RB>(k, z + 2) + k.ib);
-      if (HM) {
-        rb_phase_h<POW2, RU, RB, PA, 0>(k, z, U0, U1, U2, U3, U4, B0, B2);
-      } else {
-        if (is_int) rb_phase<POW2, RU, RB, PA>(k, z, U0, U1, U2, U3, U4, B0, B2, dst);
-        if (is_halo) rb_halo<POW2, RU, RB, 0>(k, z + 2);
-      }
+      rb_phase<POW2, RU, RB, PA>(k, z, U0, U1, U2, U3, U4, B0, B2, dst);
+      if (is_halo) rb_halo<POW2, RU, RB, 0>(k, z + 2);
       __syncthreads();
       if (tid == issuer) {
         issue_u(z + RU);
@@ -1045,12 +893,8 @@ __global__ void __launch_bounds__(HW ? 320 : NTHR_RB2, MINB) k_zrb3(const __grid
       }
       double2 U5 = lds2(rb_u<RU>(k, z + 4) + k.iu);
       const double2 B3 = lds2(rb_b<RB>(k, z + 3) + k.ib);
-      if (HM) {
-        rb_phase_h<POW2, RU, RB, PB, 1>(k, z + 1, U1, U2, U3, U4, U5, B1, B3);
-      } else {
-        if (is_int) rb_phase<POW2, RU, RB, PB>(k, z + 1, U1, U2, U3, U4, U5, B1, B3, dst + k.sz);
-        if (is_halo) rb_halo<POW2, RU, RB, 1>(k, z + 3);
-      }
+      rb_phase<POW2, RU, RB, PB>(k, z + 1, U1, U2, U3, U4, U5, B1, B3, dst + k.sz);
+      if (is_halo) rb_halo<POW2, RU, RB, 1>(k, z + 3);
       __syncthreads();
       if (tid == issuer) {
         issue_u(z + 1 + RU);
@@ -1072,145 +916,6 @@ __global__ void __launch_bounds__(HW ? 320 : NTHR_RB2, MINB) k_zrb3(const __grid
 // increasing tap order, exactly the per-axis dgemm order of the reference.
 
 constexpr int QW = TX / 2 + 4, QH = TY / 2 + 4, PQ = align16(QW * QH);   // coarse window
-constexpr int RQ = 6;                                                     // coarse ring
-
-__device__ __forceinline__ void cpa8(double* smem, const double* gmem, bool valid) {
-  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem),
-               "r"(valid ? 8 : 0));
-}
-__device__ __forceinline__ void cpa_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-template <int N>
-__device__ __forceinline__ void cpa_wait() {
-  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
-}
-
-__global__ void __launch_bounds__(NTHR) k_cubic3(const double* __restrict__ coarse, Geo gc,
-                                                 double* __restrict__ fine, Geo gf,
-                                                 const int* __restrict__ tcnt,
-                                                 const int* __restrict__ tidx,
-                                                 const double* __restrict__ tw, int zc,
-                                                 int accumulate) {
-  extern __shared__ __align__(128) double sm[];
-  double* sc = sm;                       // RQ * PQ coarse planes
-  double* zb = sc + RQ * PQ;             // QH x QW  z-interpolated window
-  double* yb = zb + align16(QW * QH);    // TY x QW  y-interpolated rows
-  const int tid = threadIdx.y * 32 + threadIdx.x;
-  const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TY;
-  const int z0 = blockIdx.z * zc, z1 = min(z0 + zc, gf.nz);
-  const int cx0 = x0 / 2 - 2, cy0 = y0 / 2 - 2;
-  const int jlo = tidx[z0 * 4];
-  const int jtop = tidx[(z1 - 1) * 4 + tcnt[z1 - 1] - 1];   // last coarse plane needed
-  int loaded = jlo;      // coarse planes [jlo, loaded) are staged
-  // coarse window element (per thread fixed): in-plane offset or -1 (zero)
-  constexpr int PERQ = (QW * QH + NTHR - 1) / NTHR;
-  int qoff[PERQ];
-#pragma unroll
-  for (int q = 0; q < PERQ; ++q) {
-    const int k = tid + q * NTHR;
-    const int yy = k / QW, xx = k - yy * QW;
-    const int cx = cx0 + xx, cy = cy0 + yy;
-    qoff[q] = (k < QW * QH && cx >= 0 && cx < gc.nx && cy >= 0 && cy < gc.ny)
-                  ? cy * (int)gc.sy + cx : -1;
-  }
-  // per-thread tap registers: x taps of the thread's column, y taps of its
-  // pass-y entries (the (x, y) geometry is the same on every plane)
-  const int gx = x0 + threadIdx.x;
-  (void)jtop;
-  int xn = 0, xi[4] = {0, 0, 0, 0};
-  double xw[4] = {0.0, 0.0, 0.0, 0.0};
-  if (gx < gf.nx) {
-    xn = tcnt[gx];
-#pragma unroll
-    for (int t = 0; t < 4; ++t)
-      if (t < xn) { xi[t] = tidx[gx * 4 + t] - cx0; xw[t] = tw[gx * 4 + t]; }
-  }
-  constexpr int PERY = (TY * QW + NTHR - 1) / NTHR;
-  int yn[PERY], yk[PERY], yi[PERY][4];
-  double yw[PERY][4];
-#pragma unroll
-  for (int q = 0; q < PERY; ++q) {
-    const int k = tid + q * NTHR;
-    const int fy = k / QW, cx = k - fy * QW;
-    const int gy = y0 + fy;
-    yk[q] = k;
-    yn[q] = (k < TY * QW && gy < gf.ny) ? tcnt[gy] : 0;
-#pragma unroll
-    for (int t = 0; t < 4; ++t) {
-      yi[q][t] = 0;
-      yw[q][t] = 0.0;
-      if (t < yn[q]) { yi[q][t] = (tidx[gy * 4 + t] - cy0) * QW + cx; yw[q][t] = tw[gy * 4 + t]; }
-    }
-  }
-  for (int iz = z0; iz < z1; ++iz) {
-    const int nt = tcnt[iz];
-    int zs[4] = {0, 0, 0, 0};
-    double zw[4] = {0.0, 0.0, 0.0, 0.0};
-#pragma unroll
-    for (int t = 0; t < 4; ++t)
-      if (t < nt) { zs[t] = ((tidx[iz * 4 + t] - jlo) % RQ) * PQ; zw[t] = tw[iz * 4 + t]; }
-    const int jmax = tidx[iz * 4 + nt - 1];
-    // fine values to accumulate into: load now, use after the passes
-    double fin[2] = {0.0, 0.0};
-    if (accumulate && gx < gf.nx) {
-#pragma unroll
-      for (int r = 0; r < 2; ++r) {
-        const int gy = y0 + threadIdx.y + 8 * r;
-        if (gy < gf.ny) fin[r] = fine[gf.at(gx, gy, iz)];
-      }
-    }
-    // stage the coarse planes this fine plane adds (planes below its first
-    // tap are dead; the ring holds RQ >= 4 live planes)
-    for (; loaded <= jmax; ++loaded) {
-      double* dst = sc + ((loaded - jlo) % RQ) * PQ;
-      const double* src = coarse + (long long)loaded * gc.sz;
-#pragma unroll
-      for (int q = 0; q < PERQ; ++q) {
-        const int k = tid + q * NTHR;
-        if (k < QW * QH) dst[k] = qoff[q] >= 0 ? __ldg(src + qoff[q]) : 0.0;
-      }
-    }
-    __syncthreads();
-    // pass z over the coarse window
-    for (int k = tid; k < QW * QH; k += NTHR) {
-      double acc = 0.0;
-#pragma unroll
-      for (int t = 0; t < 4; ++t)
-        if (t < nt) acc = __fma_rn(zw[t], sc[zs[t] + k], acc);
-      zb[k] = acc;
-    }
-    __syncthreads();
-    // pass y onto the tile rows
-#pragma unroll
-    for (int q = 0; q < PERY; ++q) {
-      if (yk[q] < TY * QW) {
-        double acc = 0.0;
-#pragma unroll
-        for (int t = 0; t < 4; ++t)
-          if (t < yn[q]) acc = __fma_rn(yw[q][t], zb[yi[q][t]], acc);
-        yb[yk[q]] = acc;
-      }
-    }
-    __syncthreads();
-    // pass x onto the tile, accumulate into the fine field
-    if (gx < gf.nx) {
-#pragma unroll
-      for (int r = 0; r < 2; ++r) {
-        const int fy = threadIdx.y + 8 * r;
-        const int gy = y0 + fy;
-        if (gy < gf.ny) {
-          const double* row = yb + fy * QW;
-          double acc = 0.0;
-#pragma unroll
-          for (int t = 0; t < 4; ++t)
-            if (t < xn) acc = __fma_rn(xw[t], row[xi[t]], acc);
-          fine[gf.at(gx, gy, iz)] = accumulate ? fin[r] + acc : acc;
-        }
-      }
-    }
-    __syncthreads();
-  }
-}
 
 // k_rfw: coarse b = FW(b - (I - sigma A) u) in one pass (multigrid.py:245-246;
 // transfers.py:27-34).  A CTA owns a 16 x 8 coarse tile; each thread owns up
@@ -1368,275 +1073,6 @@ __global__ void __launch_bounds__(NT, 4) k_rfw(const __grid_constant__ CUtensorM
     if (tid == rfw_issuer && p <= p1) {   // warp 7: fewest residual points, no x pass
       issue_u(p - 1 + RFW_RU);    // u plane p-1 is free after the residuals of p
       issue_b(p + RFW_RB);        // b plane p is free
-    }
-  }
-}
-
-// ---------------------------------------------------------------------------
-// k_rbrfw: the last pre-smoothing jor-rb sweep, the residual and full
-// weighting in ONE pass over u and b (multigrid.py:225-233, 245-246;
-// transfers.py:27-34).  k_zrb3 + k_rfw read u and b twice and write u once;
-// this kernel reads them once, writes the smoothed u and the coarse
-// right-hand side.  A CTA owns k_rfw's tile (16 x 8 coarse points, fine x0 ..
-// x0+31, y0 .. y0+15) and recomputes the halo it needs (overlapped tiling):
-//   R  = [x0, x0+32] x [y0, y0+16]        residuals (the FW footprint)
-//   F  = R + 1                            final u (black points updated)
-//   Rd = R + 2                            red points updated
-//   u window = [x0-4, x0+35] x [y0-3, y0+19] (old u, TMA, zero-filled ghosts)
-//   b window = [x0-2, x0+35] x [y0-2, y0+18]
-// Phase r (one barrier): red points of plane r (they read only old blacks),
-// black points of plane r-2 (reds of r-3 .. r-1 final), the residual of plane
-// r-4 (u final up to plane r-3) folded into k_rfw's z weights, the owned
-// points of plane r-3 to `out`, and k_rfw's y / x passes.  Residual points
-// carry their z-neighbour centres and b values in registers, so only planes
-// r-4 .. r+1 of u and r-2 .. r of b stay in shared memory.  Every update is
-// the reference's expression tree (rb_relax, the residual of k_z1, fw3), so
-// the smoothed u and the coarse right-hand side are bit-identical to k_zrb3 +
-// k_rfw.
-constexpr int QUX = TX + 8, QUY = TY + 7, PQU = align16(QUX * QUY);   // u window
-constexpr int QBX = TX + 6, QBY = TY + 5, PQB = align16(QBX * QBY);   // b window
-constexpr int RBF_RU = 8, RBF_RB = 5, RBF_NT = 384;
-constexpr int RBF_PERR = (RX * RY + RBF_NT - 1) / RBF_NT;             // residual points per thread
-
-template <bool POW2>
-__device__ __forceinline__ double rbf_relax(const double* sl, const double* slm,
-                                            const double* slp, int i, double bv, const OpC& c,
-                                            double sigma, double omega, double dval,
-                                            double dinv) {
-  const double cc = sl[i];
-  double acc = 0.0;
-  acc = acc + dd2<POW2>((slm[i] - 2.0 * cc) + slp[i], c);
-  acc = acc + dd2<POW2>((sl[i - QUX] - 2.0 * cc) + sl[i + QUX], c);
-  acc = acc + dd2<POW2>((sl[i - 1] - 2.0 * cc) + sl[i + 1], c);
-  const double lp = c.nu * acc;
-  const double r = bv - (cc - sigma * lp);
-  return cc + div_const(omega * r, dval, dinv);
-}
-
-// colour points of a box [xl, xh] x [yl, yh], statically dealt to threads:
-// slot s -> row s / w, k-th point of the colour; the x of the point depends on
-// the plane parity, so each slot keeps both window offsets and both validity
-// flags (domain clipping included) and a phase only selects by parity
-constexpr int RBF_RS = (21 * 19 + RBF_NT - 1) / RBF_NT;   // red slots per thread (Rd)
-constexpr int RBF_BS = (19 * 18 + RBF_NT - 1) / RBF_NT;   // black slots per thread (F)
-template <int NS>
-struct ColourSlots {
-  int iu0[NS], iu1[NS], ib0[NS], ib1[NS];   // window offsets for plane parity 0 / 1
-  bool ok0[NS], ok1[NS];
-  __device__ __forceinline__ void init(int xl, int xh, int yl, int yh, int red, int x0, int y0,
-                                       const Geo& g) {
-    const int w = (xh - xl) / 2 + 1, rows = yh - yl + 1;
-#pragma unroll
-    for (int j = 0; j < NS; ++j) {
-      const int sl = threadIdx.x + j * RBF_NT;
-      const int iy = sl / w, k = sl - iy * w;
-      const int y = yl + iy;
-#pragma unroll
-      for (int par = 0; par < 2; ++par) {   // par = plane & 1
-        // red: 1-based coordinate sum even <=> x + y + q odd (multigrid.py:167-175)
-        const int want = red ? ((y + par + 1) & 1) : ((y + par) & 1);
-        const int x = xl + ((want - xl) & 1) + 2 * k;
-        const int iu = (y - (y0 - 3)) * QUX + (x - (x0 - 4));
-        const int ib = (y - (y0 - 2)) * QBX + (x - (x0 - 2));
-        const bool ok = sl < rows * w && x <= xh && x >= 0 && x < g.nx && y >= 0 && y < g.ny;
-        if (par) { iu1[j] = iu; ib1[j] = ib; ok1[j] = ok; }
-        else { iu0[j] = iu; ib0[j] = ib; ok0[j] = ok; }
-      }
-    }
-  }
-  template <bool POW2>
-  __device__ __forceinline__ void run(double* sl, const double* slm, const double* slp,
-                                      const double* sbq, int par, const OpC& c, double sigma,
-                                      double omega, double dval, double dinv) const {
-#pragma unroll
-    for (int j = 0; j < NS; ++j) {
-      if (!(par ? ok1[j] : ok0[j])) continue;
-      const int i = par ? iu1[j] : iu0[j];
-      const int ib = par ? ib1[j] : ib0[j];
-      sl[i] = rbf_relax<POW2>(sl, slm, slp, i, sbq[ib], c, sigma, omega, dval, dinv);
-    }
-  }
-};
-
-template <bool POW2>
-__global__ void __launch_bounds__(RBF_NT, 2) k_rbrfw(const __grid_constant__ CUtensorMap mu,
-                                                    const __grid_constant__ CUtensorMap mb,
-                                                    double* __restrict__ out,
-                                                    double* __restrict__ coarse, Geo gf, Geo gc,
-                                                    OpC c, double sigma, double omega,
-                                                    double dval, double dinv, int zcc) {
-  extern __shared__ __align__(128) double sm[];
-  double* su = sm;                             // RBF_RU u windows
-  double* sb = su + RBF_RU * PQU;              // RBF_RB b windows
-  double* szb = sb + RBF_RB * PQB;             // z-weighted plane (RX x RY)
-  double* syx = szb + PR;                      // y-weighted rows (RX x TY/2)
-  unsigned long long* bu = (unsigned long long*)(syx + PR);
-  unsigned long long* bb = bu + RBF_RU;
-  const int tid = threadIdx.x;
-  const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TY;
-  const int jz0 = blockIdx.z * zcc, jz1 = min(jz0 + zcc, gc.nz);
-  const int p0 = 2 * jz0, p1 = 2 * jz1;        // residual planes p0 .. p1
-  const int ulo = p0 - 3, uhi = p1 + 3, blo = p0 - 2, bhi = p1 + 2;
-  // owned output planes: [p0, p1), the last chunk also p1
-  const int qhi = jz1 == gc.nz ? p1 : p1 - 1;
-  if (tid == 0) {
-    for (int i = 0; i < RBF_RU; ++i) mbar_init(bu + i, 1);
-    for (int i = 0; i < RBF_RB; ++i) mbar_init(bb + i, 1);
-    fence_barrier_init();
-  }
-  __syncthreads();
-  auto uslot = [&](int p) { return su + ((unsigned)(p - ulo) % RBF_RU) * PQU; };
-  auto bslot = [&](int p) { return sb + ((unsigned)(p - blo) % RBF_RB) * PQB; };
-  auto issue_u = [&](int p) {
-    if (p > uhi) return;
-    const int s = (unsigned)(p - ulo) % RBF_RU;
-    mbar_expect(bu + s, QUX * QUY * 8u);
-    tma3(su + s * PQU, &mu, x0 - 4, y0 - 3, p, bu + s);
-  };
-  auto issue_b = [&](int p) {
-    if (p > bhi) return;
-    const int s = (unsigned)(p - blo) % RBF_RB;
-    mbar_expect(bb + s, QBX * QBY * 8u);
-    tma3(sb + s * PQB, &mb, x0 - 2, y0 - 2, p, bb + s);
-  };
-  auto wait_u = [&](int p) {
-    const unsigned k = p - ulo;
-    mbar_wait(bu + k % RBF_RU, (k / RBF_RU) & 1u);
-  };
-  auto wait_b = [&](int p) {
-    const unsigned k = p - blo;
-    mbar_wait(bb + k % RBF_RB, (k / RBF_RB) & 1u);
-  };
-  if (tid == 0) {
-    for (int p = ulo; p < ulo + RBF_RU; ++p) issue_u(p);
-    for (int p = blo; p < blo + RBF_RB; ++p) issue_b(p);
-  }
-  // residual points of this thread (k_rfw's window order)
-  int r_iu[RBF_PERR], r_ib[RBF_PERR], r_k[RBF_PERR];
-  bool r_ok[RBF_PERR];
-#pragma unroll
-  for (int q = 0; q < RBF_PERR; ++q) {
-    const int k = tid + q * RBF_NT;
-    const int ry = k / RX, rx = k - ry * RX;
-    r_k[q] = k < RX * RY ? k : -1;
-    r_iu[q] = (ry + 3) * QUX + rx + 4;
-    r_ib[q] = (ry + 2) * QBX + rx + 2;
-    r_ok[q] = k < RX * RY && x0 + rx < gf.nx && y0 + ry < gf.ny;
-  }
-  double acc[RBF_PERR], ucm[RBF_PERR], ucc[RBF_PERR], bq1[RBF_PERR], bq2[RBF_PERR],
-      bq3[RBF_PERR], bq4[RBF_PERR];
-#pragma unroll
-  for (int q = 0; q < RBF_PERR; ++q) acc[q] = ucm[q] = ucc[q] = bq1[q] = bq2[q] = bq3[q] = bq4[q] = 0.0;
-  const int cx = tid & 15, cy = tid >> 4;     // coarse point (threads 0..127)
-  const int gcx = x0 / 2 + cx, gcy = y0 / 2 + cy;
-  const bool c_ok = tid < (TX / 2) * (TY / 2) && gcx < gc.nx && gcy < gc.ny;
-  ColourSlots<RBF_RS> reds;
-  ColourSlots<RBF_BS> blacks;
-  reds.init(x0 - 2, x0 + 34, y0 - 2, y0 + 18, 1, x0, y0, gf);
-  blacks.init(x0 - 1, x0 + 33, y0 - 1, y0 + 17, 0, x0, y0, gf);
-  wait_u(ulo);
-  wait_u(ulo + 1);
-  for (int r = p0 - 2; r <= p1 + 6; ++r) {
-    // ---- red points of plane r over Rd
-    if (r <= bhi) {
-      wait_u(r + 1);
-      wait_b(r);
-      if (r >= 0 && r < gf.nz)
-        reds.run<POW2>(uslot(r), uslot(r - 1), uslot(r + 1), bslot(r), r & 1, c, sigma, omega,
-                       dval, dinv);
-    }
-    // ---- black points of plane r-2 over F
-    const int qb = r - 2;
-    if (qb >= p0 - 1 && qb <= p1 + 1 && qb >= 0 && qb < gf.nz)
-      blacks.run<POW2>(uslot(qb), uslot(qb - 1), uslot(qb + 1), bslot(qb), qb & 1, c, sigma,
-                       omega, dval, dinv);
-    // ---- residual of plane p = r-4 (centres of planes p-1, p, p+1 in registers)
-    const int p = r - 4;
-    if (p >= p0 && p <= p1) {
-      const double* pc = uslot(p);
-      const double* pn = uslot(p + 1);
-      const int ph = p - p0;
-#pragma unroll
-      for (int q = 0; q < RBF_PERR; ++q) {
-        if (r_k[q] < 0) continue;
-        double v = 0.0;
-        const double zp = pn[r_iu[q]];
-        if (r_ok[q]) {
-          const int i = r_iu[q];
-          const double c0 = ucc[q];
-          double a = 0.0;
-          a = a + dd2<POW2>((ucm[q] - 2.0 * c0) + zp, c);
-          a = a + dd2<POW2>((pc[i - QUX] - 2.0 * c0) + pc[i + QUX], c);
-          a = a + dd2<POW2>((pc[i - 1] - 2.0 * c0) + pc[i + 1], c);
-          const double au = c0 - sigma * (c.nu * a);
-          v = bq4[q] - au;
-        }
-        ucm[q] = ucc[q];
-        ucc[q] = zp;
-        if (ph == 0) {
-          acc[q] = v;
-        } else if (ph & 1) {
-          acc[q] = acc[q] + 2.0 * v;
-        } else {
-          szb[r_k[q]] = 0.25 * (acc[q] + v);
-          acc[q] = v;
-        }
-      }
-    } else if (p == p0 - 1 || p == p0 - 2) {   // preload the centres of planes p0-1, p0
-#pragma unroll
-      for (int q = 0; q < RBF_PERR; ++q) {
-        if (r_k[q] < 0) continue;
-        ucm[q] = ucc[q];
-        ucc[q] = uslot(p + 1)[r_iu[q]];
-      }
-    }
-    // b values of this thread's residual points, four planes deep
-    if (r >= blo && r <= bhi) {
-#pragma unroll
-      for (int q = 0; q < RBF_PERR; ++q) {
-        bq4[q] = bq3[q];
-        bq3[q] = bq2[q];
-        bq2[q] = bq1[q];
-        bq1[q] = r_k[q] >= 0 ? bslot(r)[r_ib[q]] : 0.0;
-      }
-    } else {
-#pragma unroll
-      for (int q = 0; q < RBF_PERR; ++q) {
-        bq4[q] = bq3[q];
-        bq3[q] = bq2[q];
-        bq2[q] = bq1[q];
-      }
-    }
-    // ---- owned points of plane r-3 (final since phase r-1)
-    const int qo = r - 3;
-    if (qo >= p0 && qo <= qhi && tid < TX * TY / 2) {
-      const int oy = tid >> 4, ox = 2 * (tid & 15);
-      const int gx = x0 + ox, gy = y0 + oy;
-      if (gy < gf.ny && gx < gf.nx) {
-        const double2 v =
-            *reinterpret_cast<const double2*>(uslot(qo) + (oy + 3) * QUX + ox + 4);
-        double* dst = out + gf.at(gx, gy, qo);
-        if (gx + 1 < gf.nx) *reinterpret_cast<double2*>(dst) = v;
-        else dst[0] = v.x;
-      }
-    }
-    // ---- k_rfw's y and x passes (lagging the z weights by one and two planes)
-    const int fph = p - p0;
-    if (fph >= 3 && (fph & 1) == 1) {
-      for (int k = tid; k < RX * (TY / 2); k += RBF_NT) {
-        const int yy = k / RX, xx = k - yy * RX;
-        const double* zc = szb + 2 * yy * RX + xx;
-        syx[k] = fw3(zc[0], zc[RX], zc[2 * RX]);
-      }
-    }
-    if (fph >= 4 && (fph & 1) == 0 && c_ok) {
-      const double* yr = syx + cy * RX + 2 * cx;
-      coarse[gc.at(gcx, gcy, (p - 4) / 2)] = fw3(yr[0], yr[1], yr[2]);
-    }
-    __syncthreads();
-    if (tid == 0) {
-      if (r - 4 >= ulo) issue_u(r - 4 + RBF_RU);   // plane r-4 is dead
-      if (r - 2 >= blo) issue_b(r - 2 + RBF_RB);   // b plane r-2 is dead
     }
   }
 }
@@ -1959,32 +1395,6 @@ int launch_z2(const double* u, const double* b, const double* e, const Geo& gc, 
   return 0;
 }
 
-int launch_zrb(const double* u, const double* b, const double* e, const Geo& gc, double* out,
-               const Geo& g, const OpC& c, double sigma, double omega, double dval,
-               cudaStream_t s) {
-  CUtensorMap mu, mb, me;
-  std::memset(&me, 0, sizeof(me));
-  PL_TRY(make_map(&mu, u, g, UX, UY));
-  PL_TRY(make_map(&mb, b, g, BW, BH));
-  if (e) PL_TRY(make_map(&me, e, gc, CW, CH));
-  int zc = pick_zc(g);
-  dim3 grid(ceil_div(g.nx, TX), ceil_div(g.ny, TY), ceil_div(g.nz, zc));
-#define PL_ZRB(P2, PRO)                                                             \
-  do {                                                                             \
-    size_t smem = Stager<NTHR_RB, PRO, PREF2>::smem_bytes();                       \
-    auto kern = k_zrb<P2, PRO, PREF2>;                                             \
-    raise_smem(kern, smem);                                                        \
-    kern<<<grid, dim3(NTHR_RB), smem, s>>>(mu, mb, me, out, g, c, sigma, omega, dval, zc); \
-  } while (0)
-  if (c.pow2) {
-    if (e) PL_ZRB(true, true); else PL_ZRB(true, false);
-  } else {
-    if (e) PL_ZRB(false, true); else PL_ZRB(false, false);
-  }
-#undef PL_ZRB
-  return 0;
-}
-
 int launch_zrb3(const double* u, const double* b, double* out, const Geo& g, const OpC& c,
                 double sigma, double omega, double dval, cudaStream_t s) {
   CUtensorMap mu, mb;
@@ -1993,20 +1403,6 @@ int launch_zrb3(const double* u, const double* b, double* out, const Geo& g, con
   int zc = pick_zc(g);
   dim3 grid(ceil_div(g.nx, TX), ceil_div(g.ny, TY), ceil_div(g.nz, zc));
   const double dinv = 1.0 / dval;
-  if (g_zrb_ring == 3) {   // two dedicated halo warps (320 threads), 3 CTAs/SM
-    size_t smem = ((size_t)8 * PU + (size_t)4 * PB) * 8 + 8 * (8 + 4);
-    auto kern = c.pow2 ? k_zrb3<true, 8, 4, 3, true> : k_zrb3<false, 8, 4, 3, true>;
-    raise_smem(kern, smem);
-    kern<<<grid, dim3(320), smem, s>>>(mu, mb, out, g, c, sigma, omega, dval, dinv, zc);
-    return 0;
-  }
-  if (g_zrb_ring == 2) {   // halo reds dealt to every warp, merged into the phase code
-    size_t smem = ((size_t)8 * PU + (size_t)4 * PB) * 8 + 8 * (8 + 4);
-    auto kern = c.pow2 ? k_zrb3<true, 8, 4, 3, false, true> : k_zrb3<false, 8, 4, 3, false, true>;
-    raise_smem(kern, smem);
-    kern<<<grid, dim3(NTHR_RB2), smem, s>>>(mu, mb, out, g, c, sigma, omega, dval, dinv, zc);
-    return 0;
-  }
   // default (0): 6 u + 3 b planes from 255^3 up, in z chunks of >= 32 planes
   // (1,024 CTAs at 255^3, 1.7 waves of 4 per SM: 91 vs 97 us); the 8 + 4
   // rings at 3 CTAs per SM below, where they are faster (26 vs 27 us at 127^3)
@@ -2015,13 +1411,13 @@ int launch_zrb3(const double* u, const double* b, double* out, const Geo& g, con
   if (g_zrb_ring == 1 || big) {   // 6 u + 3 b planes, 4 CTAs per SM (register cap 64)
     grid.z = ceil_div(g.nz, zc);
     size_t smem = ((size_t)6 * PU + (size_t)3 * PB) * 8 + 8 * (6 + 3);
-    auto kern = c.pow2 ? k_zrb3<true, 6, 3, 4, false> : k_zrb3<false, 6, 3, 4, false>;
+    auto kern = c.pow2 ? k_zrb3<true, 6, 3, 4> : k_zrb3<false, 6, 3, 4>;
     raise_smem(kern, smem);
     kern<<<grid, dim3(NTHR_RB2), smem, s>>>(mu, mb, out, g, c, sigma, omega, dval, dinv, zc);
     return 0;
   }
   size_t smem = ((size_t)8 * PU + (size_t)4 * PB) * 8 + 8 * (8 + 4);
-  auto kern = c.pow2 ? k_zrb3<true, 8, 4, 3, false> : k_zrb3<false, 8, 4, 3, false>;
+  auto kern = c.pow2 ? k_zrb3<true, 8, 4, 3> : k_zrb3<false, 8, 4, 3>;
   raise_smem(kern, smem);
   kern<<<grid, dim3(NTHR_RB2), smem, s>>>(mu, mb, out, g, c, sigma, omega, dval, dinv, zc);
   return 0;
@@ -2044,48 +1440,22 @@ int launch_rfw(const double* u, const double* b, double* coarse, const Geo& g, c
   return 0;
 }
 
-int launch_rbrfw(const double* u, const double* b, double* out, double* coarse, const Geo& g,
-                 const OpC& c, double sigma, double omega, double dval, cudaStream_t s) {
-  Geo gc = make_geo(3, (g.N + 1) / 2);
-  CUtensorMap mu, mb;
-  PL_TRY(make_map(&mu, u, g, QUX, QUY));
-  PL_TRY(make_map(&mb, b, g, QBX, QBY));
-  // the pipeline fills over 9 phases: chunks of >= 16 coarse planes
-  const int zcc = std::max(g_rbrfw_zcc, pick_zc(g) / 2);
-  dim3 grid(ceil_div(g.nx, TX), ceil_div(g.ny, TY), ceil_div(gc.nz, zcc));
-  size_t smem = sizeof(double) * (RBF_RU * PQU + RBF_RB * PQB + 2 * PR) + 8 * (RBF_RU + RBF_RB);
-  auto kern = c.pow2 ? k_rbrfw<true> : k_rbrfw<false>;
-  raise_smem(kern, smem);
-  kern<<<grid, RBF_NT, smem, s>>>(mu, mb, out, coarse, g, gc, c, sigma, omega, dval, 1.0 / dval,
-                                  zcc);
-  return 0;
-}
-
 }  // namespace
-int g_cubic_variant = 2;    // 0: k_cubic3, 1: k_cubic4 (TMA ring, one barrier per plane),
-                            // 2 (default): k_cubic4 with zero-padded branch-free tap chains
 namespace {
 
-int launch_cubic3(const double* coarse, double* fine, const Geo& gf, const int* cnt,
+int launch_cubic4(const double* coarse, double* fine, const Geo& gf, const int* cnt,
                   const int* idx, const double* w, int accumulate, cudaStream_t s) {
   Geo gc = make_geo(3, (gf.N + 1) / 2);
   const int zc = pick_zc(gf);
   dim3 grid(ceil_div(gf.nx, TX), ceil_div(gf.ny, TY), ceil_div(gf.nz, zc)), block(32, 8);
-  if (g_cubic_variant >= 1) {
-    CUtensorMap mc;
-    PL_TRY(make_map(&mc, coarse, gc, QW, QH));
-    CUtensorMap mf;
-    std::memset(&mf, 0, sizeof(mf));
-    if (accumulate) PL_TRY(make_map(&mf, fine, gf, TX, TY));
-    size_t smem = accumulate ? sizeof(double) * RF4 * PF4 : 0;
-    auto kern = g_cubic_variant == 2 ? k_cubic4<true> : k_cubic4<false>;
-    raise_smem(kern, smem);
-    kern<<<grid, block, smem, s>>>(mc, mf, fine, gf, cnt, idx, w, zc, accumulate);
-    return 0;
-  }
-  size_t smem = sizeof(double) * (RQ * PQ + align16(QW * QH) + align16(QW * TY));
-  raise_smem(k_cubic3, smem);
-  k_cubic3<<<grid, block, smem, s>>>(coarse, gc, fine, gf, cnt, idx, w, zc, accumulate);
+  CUtensorMap mc;
+  PL_TRY(make_map(&mc, coarse, gc, QW, QH));
+  CUtensorMap mf;
+  std::memset(&mf, 0, sizeof(mf));
+  if (accumulate) PL_TRY(make_map(&mf, fine, gf, TX, TY));
+  size_t smem = accumulate ? sizeof(double) * RF4 * PF4 : 0;
+  raise_smem(k_cubic4<true>, smem);
+  k_cubic4<true><<<grid, block, smem, s>>>(mc, mf, fine, gf, cnt, idx, w, zc, accumulate);
   return 0;
 }
 
@@ -2094,7 +1464,7 @@ int launch_cubic3(const double* coarse, double* fine, const Geo& gf, const int* 
 int zlaunch_cubic(const double* coarse, double* fine, const Geo& gf, const int* cnt,
                   const int* idx, const double* w, int accumulate, cudaStream_t s) {
   PL_PRE(K_INTERP);
-  PL_TRY(launch_cubic3(coarse, fine, gf, cnt, idx, w, accumulate, s));
+  PL_TRY(launch_cubic4(coarse, fine, gf, cnt, idx, w, accumulate, s));
   Geo gc = make_geo(3, (gf.N + 1) / 2);
   PL_CHECK_LAUNCH(K_INTERP, (accumulate ? 16.0 : 8.0) * gf.npts + 8.0 * gc.npts);
   return 0;
@@ -2110,9 +1480,8 @@ double zdiag(const OpC& c, double sigma) {
 }
 
 int g_zmarch_enabled = 1;   // runtime knob (pl_set_option), for A/B tests
-int g_zrb_variant = 4;      // 0: k_zrb (3 barriers / plane), 4: k_zrb3 (one barrier / plane)
 int g_zrb_ring = 0;
-int g_fuse_prolong = 0;     // prolongation fused into the first post-sweep (slower since k_zrb3)
+int g_fuse_prolong = 0;     // Jacobi: prolongation fused into the first post-sweep pair (k_z2)
 bool zmarch_fuse_prolong() { return g_fuse_prolong != 0; }
 // smallest interior size for the TMA kernels: below it a CTA would march many
 // planes for few CTAs (latency-bound); the one-point-per-thread kernels win
@@ -2136,21 +1505,6 @@ int zlaunch_rfw(const double* u, const double* b, double* coarse, const Geo& g, 
   PL_TRY(launch_rfw(u, b, coarse, g, c, sigma, s));
   // algorithmic bytes of the unfused pair (residual 24 B, FW 8 B + 8 B coarse)
   PL_CHECK_LAUNCH(K_RESTRICT, 32.0 * g.npts + 8.0 * gc.npts);
-  return 0;
-}
-
-int g_rbrfw_enabled = 0;   // PL_OPT_RBRFW: last pre-sweep + residual + FW fused (jor-rb);
-                           // measured slower than k_zrb3 + k_rfw (A/B only)
-int g_rbrfw_zcc = 16;
-
-int zlaunch_rbrfw(const double* u, const double* b, double* out, double* coarse, const Geo& g,
-                  const OpC& c, double sigma, double omega, cudaStream_t s) {
-  Geo gc = make_geo(3, (g.N + 1) / 2);
-  PL_PRE(K_RBRFW);
-  PL_TRY(launch_rbrfw(u, b, out, coarse, g, c, sigma, omega, zdiag(c, sigma), s));
-  // algorithmic bytes of the unfused kernels it replaces: one red-black
-  // sweep (24 B) plus residual + full weighting (32 B + 8 B per coarse point)
-  PL_CHECK_LAUNCH(K_RBRFW, 24.0 * g.npts + 32.0 * g.npts + 8.0 * gc.npts);
   return 0;
 }
 
@@ -2204,13 +1558,11 @@ int zlaunch_jacobi2(const double* u, const double* b, double* out, const Geo& g,
 }
 
 int zlaunch_rb(const double* u, const double* b, double* out, const Geo& g, const OpC& c,
-               double sigma, double omega, const double* e, cudaStream_t s) {
+               double sigma, double omega, cudaStream_t s) {
   double dval = zdiag(c, sigma);
-  Geo gc = make_geo(3, (g.N + 1) / 2);
   PL_PRE(K_RB);
-  if (e || g_zrb_variant == 0) PL_TRY(launch_zrb(u, b, e, gc, out, g, c, sigma, omega, dval, s));
-  else PL_TRY(launch_zrb3(u, b, out, g, c, sigma, omega, dval, s));
-  PL_CHECK_LAUNCH(K_RB, 24.0 * g.npts + (e ? 16.0 * g.npts + 8.0 * gc.npts : 0.0));
+  PL_TRY(launch_zrb3(u, b, out, g, c, sigma, omega, dval, s));
+  PL_CHECK_LAUNCH(K_RB, 24.0 * g.npts);
   return 0;
 }
 

@@ -81,27 +81,6 @@ def seeded_field(grid: Grid, seed: int = 1407, modes: int = 16, kmax: int = 32,
     return u
 
 
-def discrete_symbol(grid: Grid, k: int) -> float:
-    """heat.py:65-72."""
-    if grid.dim != 1:
-        raise ValueError("discrete symbol is defined for 1D grids only")
-    if not 1 <= k <= grid.n - 1:
-        raise ValueError(f"mode number k must be in [1, {grid.n - 1}], got {k}")
-    dx = grid.dx
-    return (-2.0 + 2.0 * np.cos(k * np.pi * dx / grid.length)) / dx ** 2
-
-
-def exact_pde(grid: Grid, k: int, nu: float, t: float) -> np.ndarray:
-    """heat.py:75-78."""
-    rate = grid.dim * nu * (k * np.pi / grid.length) ** 2
-    return np.exp(-rate * t) * initial_condition(grid, k)
-
-
-def exact_ode(grid: Grid, k: int, nu: float, t: float) -> np.ndarray:
-    """heat.py:81-86."""
-    return np.exp(nu * discrete_symbol(grid, k) * t) * initial_condition(grid, k)
-
-
 @dataclass(frozen=True)
 class HeatOperator:
     """nu times the order-2 / order-4 discrete Laplacian (heat.py:95-158)."""

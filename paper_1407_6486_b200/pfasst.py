@@ -84,6 +84,21 @@ class _PreCoarse(Hooks):
             self.fn(ts)
 
 
+_RANK_STREAMS: dict = {}
+
+
+def _rank_stream(n):
+    """The CUDA stream of time rank n on the current device, created once per
+    process: the per-stream multigrid plans and scratch (multigrid.plan_for,
+    _device.scratch) are keyed by the stream, so reusing the streams across
+    pfasst_run calls reuses those workspaces instead of growing them."""
+    key = (torch.cuda.current_device(), n)
+    st = _RANK_STREAMS.get(key)
+    if st is None:
+        st = _RANK_STREAMS[key] = torch.cuda.Stream()
+    return st
+
+
 class DeviceEngine:
     """Owns the TimeStep state of the time ranks of this process (one GPU)."""
 
@@ -94,7 +109,7 @@ class DeviceEngine:
         self.ranks = list(ranks)
         self.ts = {}
         self.spread_y = {}
-        self.streams = {n: torch.cuda.Stream() for n in self.ranks} if streams else None
+        self.streams = {n: _rank_stream(n) for n in self.ranks} if streams else None
         self._coarse_in = {}
         self._res = zeros((max(self.ranks) + 1 if self.ranks else 1,))
         self._res_host = torch.zeros(self._res.shape, dtype=torch.float64,
@@ -146,8 +161,8 @@ class DeviceEngine:
     def set_fine_y0(self, n, t):
         """pfasst.py:196-198 for level 0."""
         ts = self.ts[n]
-        ts.set_y0(0, t)
         ts.states[0].y[0].copy_(t)
+        ts.set_y0(0, ts.states[0].y[0], alias=True)
         self.levels[0].operator.apply_into(ts.states[0].y[0], ts.states[0].f[0])
 
     def stream(self, n):
@@ -347,6 +362,18 @@ class _Block:
         self.frozen = [False] * p
         self.pending = {}        # n -> (k, cycles, residual handle)
         self.status = [dict() for _ in range(p)]   # n -> {k: converged}
+        self.solves = []         # ((stage, k or phase, rank, seq), record) when logging
+        self.tag = None
+
+    def sink(self, recs):
+        """sdc._solve_sink while this block logs solves: tags each record with
+        its position in the reference's serial order (predictor phase-major,
+        then iteration-major, rank-minor; pfasst.py:213-228)."""
+        for r in recs:
+            self.solves.append(((*self.tag, len(self.solves)), r))
+
+    def serial_solves(self):
+        return [r for _, r in sorted(self.solves, key=lambda t: t[0])]
 
     def predictor(self):
         """pfasst.py:166-181, phase-major (serial order)."""
@@ -357,6 +384,7 @@ class _Block:
                     continue
                 if n > 0:
                     e.set_coarse_y0(n, x.recv_pred(n, ph))
+                self.tag = (0, ph, n)
                 self.vcycles[n] += e.burn_in(n)
                 if n + 1 < p and not x.owns(n + 1):
                     x.send_pred(n, ph)
@@ -434,6 +462,7 @@ class _Block:
                 # the local exchange hands over the predecessor's coarse value
                 # by reading its state inside the pre-coarse hook (same as the
                 # reference's blocking coarse recv, pfasst.py:107-112)
+                self.tag = (1, k, n)
                 cyc = e.iteration(n, pre)
                 if n + 1 < p and not x.owns(n + 1):
                     # coarse payload was produced by the coarse sweep; the fine
@@ -487,6 +516,7 @@ class _Block:
                     # the successor's copy of this rank's previous payload
                     if n + 1 < p and issued[n + 1] == k - 1 and copied_ev[n + 1] is not None:
                         st.wait_event(copied_ev[n + 1])
+                    self.tag = (1, k, n)
                     cyc = e.iteration(n, pre)
                     handle = e.residual(n)
                     done_ev[n] = torch.cuda.Event()
@@ -537,21 +567,43 @@ def _rank_streams_fit(levels, p) -> bool:
     return (p - 1) * per <= 0.5 * free
 
 
+def _run_block(blk, engine, exchange):
+    """Predictor and iterations of one block (pfasst.py:213-228)."""
+    blk.predictor()
+    if isinstance(exchange, _LocalExchange) and getattr(engine, "streams", None):
+        # rank streams overlap each other's work: the small V-cycle levels
+        # then run as ordinary per-level launches (no cooperative grid that
+        # must be co-resident on every SM; the TMA sweeps from 63^3 up) and
+        # interleave with the other ranks' kernels -- +15-25 % time-steps/s
+        # against the one-CTA-per-SM cooperative kernel, which a lone solve
+        # keeps (results are bit-identical either way)
+        from contextlib import ExitStack
+
+        from . import _capi as capi
+        with ExitStack() as scope:
+            for key, (value, default) in _rank_stream_options().items():
+                scope.enter_context(capi.option(key, value, default))
+            blk.iterations_wavefront()
+    else:
+        blk.iterations_loop()
+
+
 def _gather_block(blk, exchange):
     """Combine per-process bookkeeping (nccl executor)."""
     if not isinstance(exchange, DistExchange):
-        return blk.iterations, blk.vcycles, blk.converged, blk.trace
+        return blk.iterations, blk.vcycles, blk.converged, blk.trace, blk.serial_solves()
     dist = exchange.dist
     mine = {n: (blk.iterations[n], blk.vcycles[n], blk.converged[n]) for n in blk.mine}
     rows = [(r.block, r.rank, r.iteration, r.level, r.residual, r.vcycles) for r in blk.trace]
     gathered = [None] * exchange.world
-    dist.all_gather_object(gathered, (mine, rows), group=exchange.group)
-    it, vc, cv, tr = [0] * blk.p, [0] * blk.p, [False] * blk.p, []
-    for m, rws in gathered:
+    dist.all_gather_object(gathered, (mine, rows, blk.solves), group=exchange.group)
+    it, vc, cv, tr, sv = [0] * blk.p, [0] * blk.p, [False] * blk.p, [], []
+    for m, rws, solves in gathered:
         for n, (a, b, c) in m.items():
             it[n], vc[n], cv[n] = a, b, c
         tr.extend(TraceRow(*r) for r in rws)
-    return it, vc, cv, tr
+        sv.extend(solves)
+    return it, vc, cv, tr, [r for _, r in sorted(sv, key=lambda t: t[0])]
 
 
 def _world(group):
@@ -561,14 +613,20 @@ def _world(group):
 
 def pfasst_run(levels, u0, t_end: float, p: int, blocks: int = 1, tol: float = 1e-9,
                max_iter: int = 20, executor: str = "serial", record_final_values: bool = False,
-               engine_factory=None, group=None, streams: bool = True) -> PfasstResult:
+               engine_factory=None, group=None, streams: bool = True,
+               solve_log: list | None = None) -> PfasstResult:
     """Run PFASST / IPFASST over ``blocks`` windows of ``p`` steps (pfasst.py:256-287).
 
     ``u0`` may be a numpy array (result returned on the host, drop-in) or an
     fp64 CUDA tensor (result stays on the device).  ``streams`` (single
     process only) issues each time rank on its own CUDA stream in wavefront
     order when the per-stream scratch fits (``_rank_streams_fit``); results
-    are identical either way."""
+    are identical either way.
+
+    ``solve_log`` (optional list) receives, per block, the list of
+    ``[n, sigma, cycles, status]`` records of every sub-step solve in the
+    reference's serial order (predictor, then iterations; the parity aid of
+    the oracle's per-solve log), whatever the executor or issue order."""
     check_hierarchy(levels)
     if executor not in ("serial", "threaded", "nccl"):
         raise ValueError(f"unknown executor {executor!r}")
@@ -603,23 +661,14 @@ def pfasst_run(levels, u0, t_end: float, p: int, blocks: int = 1, tol: float = 1
             if exchange.owns(n):
                 engine.spread(n, u)
         blk = _Block(engine, exchange, p, tol, max_iter, block, record_final_values)
-        blk.predictor()
-        if isinstance(exchange, _LocalExchange) and getattr(engine, "streams", None):
-            # rank streams overlap each other's work: the small V-cycle
-            # levels then run as ordinary per-level launches (no cooperative
-            # grid that must be co-resident on every SM; the TMA sweeps from
-            # 63^3 up) and interleave with the other ranks' kernels -- +15-25 %
-            # time-steps/s against the one-CTA-per-SM cooperative kernel,
-            # which a lone solve keeps (results are bit-identical either way)
-            from contextlib import ExitStack
-
-            from . import _capi as capi
-            with ExitStack() as scope:
-                for key, (value, default) in _rank_stream_options().items():
-                    scope.enter_context(capi.option(key, value, default))
-                blk.iterations_wavefront()
-        else:
-            blk.iterations_loop()
+        if solve_log is not None:
+            from . import sdc as _sdc
+            _sdc._solve_sink = blk.sink
+        try:
+            _run_block(blk, engine, exchange)
+        finally:
+            if solve_log is not None:
+                _sdc._solve_sink = None
         if isinstance(exchange, DistExchange):
             exchange.finish()
             last = (p - 1) % exchange.world
@@ -636,7 +685,9 @@ def pfasst_run(levels, u0, t_end: float, p: int, blocks: int = 1, tol: float = 1
                 blk.final_values = holder[0]
         else:
             u = engine.snapshot(engine.fine_payload(p - 1))
-        it, vc, cv, tr = _gather_block(blk, exchange)
+        it, vc, cv, tr, sv = _gather_block(blk, exchange)
+        if solve_log is not None:
+            solve_log.append(sv)
         result.rank_iterations.append(list(it))
         result.rank_vcycles.append(list(vc))
         result.converged.append(list(cv))

@@ -98,10 +98,20 @@ def sweep_desc(table: QuadratureTable, policy) -> capi.SweepDesc:
     return desc
 
 
+# Receiver of per-solve records while a PFASST run logs them (pfasst_run's
+# ``solve_log``): called with the list of records of one sweep.
+_solve_sink = None
+
+
 def sdc_sweep(states: NodeStates, y0, dt: float, op: HeatOperator, mg_cfg: MgConfig,
-              policy: SolvePolicy, tau=None) -> int:
+              policy: SolvePolicy, tau=None, solve_log: list | None = None) -> int:
     """One sweep through the sub-steps, in place; returns V-cycles used
-    (sdc.py:84-114)."""
+    (sdc.py:84-114).
+
+    ``solve_log`` (optional list) receives one ``[n, sigma, cycles, status]``
+    record per sub-step solve -- the grid size, sigma = float(gamma_m) * dt and
+    the ``SolveResult.cycles`` / ``.status`` the reference's ``multigrid.solve``
+    returns for it (multigrid.py:261-288, called at sdc.py:105-113)."""
     _check_policy(policy)
     d = op.grid.dim
     ty0, _ = to_device(y0, d)
@@ -116,14 +126,24 @@ def sdc_sweep(states: NodeStates, y0, dt: float, op: HeatOperator, mg_cfg: MgCon
     nb = capi.lib().pl_sweep_workspace_bytes(g.dim, g.n, states.table.m)
     ws = scratch("sweep", nb)
     cyc, fsub, fres, fcyc = C.c_int(0), C.c_int(0), C.c_double(0), C.c_int(0)
+    m = states.table.m
+    sub_c, sub_s = (C.c_int * m)(), (C.c_int * m)()
     rc = capi.lib().pl_sdc_sweep(plan.handle.value, C.byref(desc), ptr(states.y),
                                  ptr(states.f), ptr(ty0), ptr(ttau), float(dt), ws.data_ptr(),
-                                 ws.numel(), C.byref(cyc), C.byref(fsub), C.byref(fres),
-                                 C.byref(fcyc), stream_ptr())
+                                 ws.numel(), C.byref(cyc), sub_c, sub_s, C.byref(fsub),
+                                 C.byref(fres), C.byref(fcyc), stream_ptr())
     if rc == capi.PL_ERR_MGCAP:
         cause = MultigridError(capi.last_error(), fres.value, fcyc.value)
         raise SubStepError(fsub.value, cause) from cause
     capi.check(rc, "sdc_sweep")
+    if solve_log is not None or _solve_sink is not None:
+        gam = states.table.nodes.gammas
+        recs = [[g.n, float(gam[i]) * dt, int(sub_c[i]), capi.STATUS[sub_s[i]]]
+                for i in range(m)]
+        if solve_log is not None:
+            solve_log.extend(recs)
+        if _solve_sink is not None:
+            _solve_sink(recs)
     return cyc.value
 
 
@@ -161,8 +181,10 @@ class RunResult:
 
 
 def run_sdc(op: HeatOperator, table: QuadratureTable, u0, t_end: float, n_steps: int,
-            tol: float, max_iter: int, mg_cfg: MgConfig, policy: SolvePolicy) -> RunResult:
-    """Serial SDC / ISDC over n_steps steps (sdc.py:136-166)."""
+            tol: float, max_iter: int, mg_cfg: MgConfig, policy: SolvePolicy,
+            solve_log: list | None = None) -> RunResult:
+    """Serial SDC / ISDC over n_steps steps (sdc.py:136-166); ``solve_log``
+    as in sdc_sweep."""
     if n_steps < 1:
         raise ValueError("need at least one time step")
     dt = t_end / n_steps
@@ -173,7 +195,7 @@ def run_sdc(op: HeatOperator, table: QuadratureTable, u0, t_end: float, n_steps:
         history = []
         sweeps = 0
         for _ in range(max_iter):
-            result.vcycles += sdc_sweep(states, u, dt, op, mg_cfg, policy)
+            result.vcycles += sdc_sweep(states, u, dt, op, mg_cfg, policy, solve_log=solve_log)
             sweeps += 1
             res = residual(states, u, dt)
             history.append(res)

@@ -14,10 +14,52 @@ from paper_1407_6486_b200.heat import Grid, HeatOperator
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-def header_functions():
+def header_prototypes():
+    """{name: (return type, [parameter types])} of every function declared in
+    include/pintlab_b200.h (comments stripped, prototypes may span lines)."""
     src = open(os.path.join(ROOT, "include", "pintlab_b200.h")).read()
-    return sorted(set(re.findall(r"^\s*(?:int|size_t|const char\*)\s+(pl_\w+)\s*\(", src,
-                                 re.M)))
+    src = re.sub(r"/\*.*?\*/", " ", src, flags=re.S)
+    src = re.sub(r"^\s*#.*$", " ", src, flags=re.M)
+    out = {}
+    for m in re.finditer(r"((?:const\s+)?[A-Za-z_][\w ]*?[\s*]+)(pl_\w+)\s*\(([^)]*)\)\s*;",
+                         src, re.S):
+        ret, name, params = m.group(1), m.group(2), m.group(3)
+        ret = " ".join(ret.replace("*", " * ").split())
+        plist = []
+        for prm in params.split(","):
+            prm = " ".join(prm.replace("*", " * ").split())
+            if prm in ("", "void"):
+                continue
+            # drop the parameter name (the last identifier) when one is given
+            toks = prm.split()
+            if len(toks) > 1 and re.fullmatch(r"[A-Za-z_]\w*", toks[-1]) and \
+                    toks[-1] not in ("int", "double", "char", "void", "size_t", "unsigned",
+                                     "long"):
+                toks = toks[:-1]
+            plist.append(" ".join(toks))
+        out[name] = (ret, plist)
+    return out
+
+
+def header_functions():
+    return sorted(header_prototypes())
+
+
+def _ctypes_kind(t):
+    """The ctypes type a C type must be bound with (pointers -> void* or a
+    typed pointer; width matters for integers and floats)."""
+    t = t.replace("const ", "")
+    if t.endswith("*"):
+        return "ptr"
+    return {"int": ctypes.c_int, "unsigned": ctypes.c_uint, "double": ctypes.c_double,
+            "size_t": ctypes.c_size_t, "long long": ctypes.c_longlong}[t]
+
+
+def _bound_kind(ct):
+    if ct in (ctypes.c_void_p, ctypes.c_char_p) or (isinstance(ct, type) and
+                                                    issubclass(ct, ctypes._Pointer)):
+        return "ptr"
+    return ct
 
 
 def test_library_builds_and_exports_header():
@@ -28,7 +70,29 @@ def test_library_builds_and_exports_header():
     for name in decl:
         assert hasattr(lib, name), f"{name} declared in the header but not exported"
     assert set(decl) == set(_capi.EXPORTED)
-    assert _capi.lib().pl_abi_version() == 1
+    assert _capi.lib().pl_abi_version() == 2
+
+
+def test_ctypes_signatures_match_header_prototypes():
+    """Arity and argument widths of every binding equal the C prototype: a
+    missing argument would let ctypes truncate a trailing 64-bit stream
+    handle to a C int."""
+    protos = header_prototypes()
+    for name, (ret, params) in protos.items():
+        res, args = _capi._SIGS[name]
+        assert len(args) == len(params), (name, params, args)
+        for i, (c_t, bound) in enumerate(zip(params, args)):
+            assert _ctypes_kind(c_t) == _bound_kind(bound), (name, i, c_t, bound)
+        want = None if ret == "void" else _ctypes_kind(ret)
+        assert want == _bound_kind(res), (name, ret, res)
+
+
+def test_header_parser_sees_multiline_and_long_long():
+    protos = header_prototypes()
+    assert protos["pl_field_elems"] == ("long long", ["int", "int"])
+    assert len(protos["pl_sdc_sweep"][1]) == 16
+    assert protos["pl_sdc_residual"][1][7:9] == ["int", "int"]
+    assert protos["pl_last_error"] == ("const char *", [])
 
 
 def test_kind_names_and_stats_without_gpu():
@@ -114,21 +178,3 @@ def test_policies_accepted_and_unknown_rejected():
         mg._check_policy(pol)
     with pytest.raises(ValueError):
         mg._check_policy("direct")
-
-
-def test_comm_entry_points_validate_and_create_ids():
-    """pl_comm_*: NCCL is opened lazily (the library loads without it); ids are
-    128 bytes; argument errors are rejected before any device work."""
-    import ctypes as C
-    lib = _capi.lib()
-    buf = C.create_string_buffer(128)
-    assert lib.pl_comm_unique_id(buf) == 0
-    assert any(buf.raw)
-    assert lib.pl_comm_unique_id(None) < 0
-    h = C.c_void_p()
-    assert lib.pl_comm_init(C.byref(h), buf, 2, 1, 0) < 0          # rank >= nranks
-    assert lib.pl_comm_init(C.byref(h), buf, 0, 0, 0) < 0          # no ranks
-    assert lib.pl_comm_send(None, None, 0, 0, None) < 0
-    assert lib.pl_comm_recv(None, None, 0, 0, None) < 0
-    assert lib.pl_comm_bcast(None, None, 0, 0, None) < 0
-    assert lib.pl_comm_destroy(None) == 0

@@ -159,8 +159,13 @@ def test_sweep_and_residual(name):
     st = sdc.NodeStates(table, y, f)
     pol = mg.FixedCycles(1) if m["policy"] == "fixed1" else mg.ToTolerance(1e-12)
     tau = dev(a["tau"]) if "tau" in a else None
-    cyc = sdc.sdc_sweep(st, dev(a["y0"]), m["dt"], op, mg.MgConfig(), pol, tau=tau)
+    log = []
+    cyc = sdc.sdc_sweep(st, dev(a["y0"]), m["dt"], op, mg.MgConfig(), pol, tau=tau,
+                        solve_log=log)
     assert cyc == m["cycles"]
+    # one [n, sigma, cycles, status] per sub-step solve, as multigrid.solve
+    # returned them inside the reference's sweep (sdc.py:105-113)
+    assert log == m["solves"]
     close(st.y, a["y_out"], 1e-12)
     close(st.f, a["f_out"], 1e-10)
     res = sdc.residual(st, dev(a["y0"]), m["dt"], tau=tau)
@@ -232,12 +237,21 @@ RUNS = ["run_cfg0", "run_cfg0_interp2", "run_cfg1", "run_cfg1_fc2", "run_cfg2_sm
 
 
 @pytest.mark.parametrize("name", RUNS)
-def test_pfasst_run_parity(name):
+def test_pfasst_run_parity(name, streams=True):
     a, m = case(name)
     levels = levels_from(m)
     t_end = m["dt"] * m["p"] * m["blocks"]
+    log = []
     res = pfasst.pfasst_run(levels, dev(a["u0"]), t_end, m["p"], blocks=m["blocks"],
-                            tol=m["tol"], max_iter=20, record_final_values=True)
+                            tol=m["tol"], max_iter=20, record_final_values=True,
+                            solve_log=log, streams=streams)
+    # every sub-step solve of the run -- predictor and iterations, every rank
+    # and level -- in the reference's serial order: grid, sigma, V-cycles and
+    # SolveResult status identical (multigrid.py:261-288 via sdc.py:105-113)
+    got_solves = [r for blk in log for r in blk]
+    assert len(got_solves) == len(m["solves"])
+    bad = [(i, g, r) for i, (g, r) in enumerate(zip(got_solves, m["solves"])) if g != r]
+    assert not bad, bad[:5]
     assert res.rank_iterations == m["rank_iterations"]
     assert res.rank_vcycles == m["rank_vcycles"]
     assert res.converged == m["converged"]
@@ -376,14 +390,11 @@ def test_cubic_zmarch_equals_pass_kernels(nf):
         ref_acc = clone_field(f)
         transfers.interp_cubic_into(c, ref_acc, True)
         _capi.set_option(_capi.OPT_ZMARCH, 1)
-        for variant in (0, 1, 2):
-            _capi.set_option(_capi.OPT_CUBIC_VARIANT, variant)
-            assert torch.equal(transfers.interp_cubic(c), ref), variant
-            acc = clone_field(f)
-            transfers.interp_cubic_into(c, acc, True)
-            assert torch.equal(acc, ref_acc), variant
+        assert torch.equal(transfers.interp_cubic(c), ref)
+        acc = clone_field(f)
+        transfers.interp_cubic_into(c, acc, True)
+        assert torch.equal(acc, ref_acc)
     finally:
-        _capi.set_option(_capi.OPT_CUBIC_VARIANT, 2)
         _capi.set_option(_capi.OPT_ZMARCH, 1)
         _capi.set_option(_capi.OPT_ZMARCH_MIN_N, 127)
 
@@ -399,17 +410,14 @@ def test_pfasst_run_parity_tma_path(name):
         _capi.set_option(_capi.OPT_ZMARCH_MIN_N, 127)
 
 
-@pytest.mark.parametrize("variant", [0, 4, 5, 6, 7, 8])
-def test_zrb_variants_bitwise_31cubed(variant):
-    """Every jor-rb TMA sweep variant (three barriers per plane, and the
-    register-pipelined one-barrier kernels with their ring sizes) reproduces
-    the reference's red-black sweeps bit for bit on the 31^3 golden case."""
+@pytest.mark.parametrize("ring", [0, 1, 4])
+def test_zrb_variants_bitwise_31cubed(ring):
+    """The jor-rb TMA sweep with each of its ring layouts (6 + 3 planes at 4
+    CTAs/SM, 8 + 4 at 3) reproduces the reference's red-black sweeps bit for
+    bit on the 31^3 golden case."""
     a, m = case("mg32_d3")
     _capi.set_option(_capi.OPT_ZMARCH_MIN_N, 31)
-    _capi.set_option(_capi.OPT_ZRB_VARIANT, min(variant, 4))
-    # 5: the 6 + 3 plane rings, 6: halo reds merged into every warp's phase,
-    # 7: two dedicated halo warps
-    _capi.set_option(_capi.OPT_ZRB_RING, {5: 1, 6: 2, 7: 3, 8: 4}.get(variant, 0))
+    _capi.set_option(_capi.OPT_ZRB_RING, ring)
     try:
         sop = mg.ShiftedOperator(heat.HeatOperator(heat.Grid(3, 32)), m["sigma"])
         for om in (1.0, 0.8):
@@ -418,18 +426,16 @@ def test_zrb_variants_bitwise_31cubed(variant):
                 bitwise(mg.smooth(sop, dev(a["u"]), dev(a["b"]), cfg, cnt),
                         a[f"sm{cnt}_jor-rb_{om:.3f}"])
     finally:
-        _capi.set_option(_capi.OPT_ZRB_VARIANT, 4)
         _capi.set_option(_capi.OPT_ZRB_RING, 0)
         _capi.set_option(_capi.OPT_ZMARCH_MIN_N, 127)
 
 
 @pytest.mark.parametrize("n,length,sigma", [(128, 1.0, 1.0 / 128), (256, 1.0, 0.37),
                                             (128, 3.0, 0.01)])
-@pytest.mark.parametrize("fuse", [1, 0])
-def test_zrb_variants_equal_plain_kernels(n, length, sigma, fuse):
+def test_zrb_variants_equal_plain_kernels(n, length, sigma):
     """At 127^3 / 255^3 (several z chunks, ragged last tiles, a non-power-of-two
-    dx^2) every sweep variant, with and without the fused prolongation, gives
-    the plain one-colour kernels' V-cycle bit for bit."""
+    dx^2) every ring layout of the sweep gives the plain one-colour kernels'
+    V-cycle bit for bit."""
     rng = np.random.default_rng(n + int(length))
     g = heat.Grid(3, n, length)
     u = dev(rng.standard_normal(g.shape))
@@ -440,17 +446,13 @@ def test_zrb_variants_equal_plain_kernels(n, length, sigma, fuse):
     ref = mg.v_cycle(sop, u, b, cfg)
     ref_s = mg.smooth(sop, u, b, cfg, 2)
     _capi.set_option(_capi.OPT_ZMARCH, 1)
-    _capi.set_option(_capi.OPT_FUSE_PROLONG, fuse)
     try:
-        for variant in (0, 4, 5, 6, 7, 8):
-            _capi.set_option(_capi.OPT_ZRB_VARIANT, min(variant, 4))
-            _capi.set_option(_capi.OPT_ZRB_RING, {5: 1, 6: 2, 7: 3, 8: 4}.get(variant, 0))
-            assert torch.equal(mg.v_cycle(sop, u, b, cfg), ref), variant
-            assert torch.equal(mg.smooth(sop, u, b, cfg, 2), ref_s), variant
+        for ring in (0, 1, 4):
+            _capi.set_option(_capi.OPT_ZRB_RING, ring)
+            assert torch.equal(mg.v_cycle(sop, u, b, cfg), ref), ring
+            assert torch.equal(mg.smooth(sop, u, b, cfg, 2), ref_s), ring
     finally:
-        _capi.set_option(_capi.OPT_ZRB_VARIANT, 4)
         _capi.set_option(_capi.OPT_ZRB_RING, 0)
-        _capi.set_option(_capi.OPT_FUSE_PROLONG, 0)
 
 
 @pytest.mark.parametrize("n", [32, 64, 128, 256])
@@ -470,58 +472,17 @@ def test_cooperative_mid_vcycle_equals_separate_launches(n, pre, post, omega):
     ref0 = mg.v_cycle(sop, torch.zeros_like(u), b, cfg)
     try:
         _capi.set_option(_capi.OPT_MID, 1)
-        for bar in (0, 1):   # grid.sync() (default) and k_mid's own grid barrier
-            _capi.set_option(_capi.OPT_MID_BAR, bar)
+        for ctas in (0, 32):
+            _capi.set_option(_capi.OPT_MID_CTAS, ctas)
             for tail_n in (3, 7, 15):
                 _capi.set_option(_capi.OPT_MID_TAIL_N, tail_n)
-                assert torch.equal(mg.v_cycle(sop, u, b, cfg), ref), (bar, tail_n)
-                assert torch.equal(mg.v_cycle(sop, torch.zeros_like(u), b, cfg), ref0), (bar, tail_n)
+                assert torch.equal(mg.v_cycle(sop, u, b, cfg), ref), (ctas, tail_n)
+                assert torch.equal(mg.v_cycle(sop, torch.zeros_like(u), b, cfg), ref0), \
+                    (ctas, tail_n)
     finally:
         _capi.set_option(_capi.OPT_MID, 1)
-        _capi.set_option(_capi.OPT_MID_BAR, 0)
-        _capi.set_option(_capi.OPT_MID_TAIL_N, 15)
-
-
-@pytest.mark.parametrize("n,length", [(16, 1.0), (32, 1.0), (64, 1.0), (64, 1.5), (128, 0.7),
-                                      (256, 1.0)])
-@pytest.mark.parametrize("pre,post,omega", [(1, 1, 1.0), (2, 1, 0.9), (1, 2, 1.0), (0, 1, 1.0),
-                                            (2, 0, 0.8)])
-def test_mid2_one_phase_per_level_equals_separate_launches(n, length, pre, post, omega):
-    """The overlapped-tile cooperative kernel (one grid phase per level and
-    direction, LU fused into the last down phase) reproduces the per-level
-    launches and the previous cooperative kernel bit for bit, from a guess and
-    from zero, for power-of-two and general dx^2."""
-    rng = np.random.default_rng(11 * n + 3 * pre + post)
-    g = heat.Grid(3, n, length)
-    u = dev(rng.standard_normal(g.shape))
-    b = dev(rng.standard_normal(g.shape))
-    sop = mg.ShiftedOperator(heat.HeatOperator(g), 0.0021)
-    cfg = mg.MgConfig("jor-rb", omega, pre, post)
-    try:
-        _capi.set_option(_capi.OPT_MID, 0)
-        ref = mg.v_cycle(sop, u, b, cfg)
-        ref0 = mg.v_cycle(sop, torch.zeros_like(u), b, cfg)
-        _capi.set_option(_capi.OPT_MID, 1)
-        _capi.set_option(_capi.OPT_MID2, 0)
-        assert torch.equal(mg.v_cycle(sop, u, b, cfg), ref)
-        _capi.set_option(_capi.OPT_MID2, 1)
-        for ctas in (0, 7, 32):
-            _capi.set_option(_capi.OPT_MID_CTAS, ctas)
-            assert torch.equal(mg.v_cycle(sop, u, b, cfg), ref), ctas
-        got = mg.v_cycle(sop, u, b, cfg)
-        assert torch.equal(got, ref), float((got - ref).abs().max())
-        assert torch.equal(mg.v_cycle(sop, torch.zeros_like(u), b, cfg), ref0)
-        two = mg.solve(sop, u, b, cfg, mg.FixedCycles(2)).u
-        _capi.set_option(_capi.OPT_MID2, 0)
-        assert torch.equal(mg.solve(sop, u, b, cfg, mg.FixedCycles(2)).u, two)
-        _capi.set_option(_capi.OPT_MID2, 0)
-        for ctas in (0, 5):
-            _capi.set_option(_capi.OPT_MID_CTAS, ctas)
-            assert torch.equal(mg.v_cycle(sop, u, b, cfg), ref), ctas
-    finally:
-        _capi.set_option(_capi.OPT_MID, 1)
-        _capi.set_option(_capi.OPT_MID2, 0)
         _capi.set_option(_capi.OPT_MID_CTAS, 0)
+        _capi.set_option(_capi.OPT_MID_TAIL_N, 15)
 
 
 @pytest.mark.parametrize("name", ["run_cfg1", "run_cfg2_small", "run_cfg3_small", "run_cfg4_small_tol"])
@@ -532,8 +493,12 @@ def test_pfasst_rank_streams_identical(name):
     levels = levels_from(m)
     t_end = m["dt"] * m["p"] * m["blocks"]
     kw = dict(blocks=m["blocks"], tol=m["tol"], max_iter=20, record_final_values=True)
-    r1 = pfasst.pfasst_run(levels, dev(a["u0"]), t_end, m["p"], streams=False, **kw)
-    r2 = pfasst.pfasst_run(levels, dev(a["u0"]), t_end, m["p"], streams=True, **kw)
+    log1, log2 = [], []
+    r1 = pfasst.pfasst_run(levels, dev(a["u0"]), t_end, m["p"], streams=False, solve_log=log1,
+                           **kw)
+    r2 = pfasst.pfasst_run(levels, dev(a["u0"]), t_end, m["p"], streams=True, solve_log=log2,
+                           **kw)
+    assert log1 == log2 and [r for blk in log1 for r in blk] == m["solves"]
     assert torch.equal(r1.u, r2.u)
     assert r1.rank_iterations == r2.rank_iterations
     assert r1.rank_vcycles == r2.rank_vcycles
@@ -590,34 +555,6 @@ def test_fast_tail_equals_generic_tail(n, pre, post, omega):
         _capi.set_option(_capi.OPT_MID_TAIL_N, 15)
 
 
-def test_comm_single_rank_roundtrip():
-    """A one-rank NCCL communicator through the C ABI: grouped self send/recv
-    and a broadcast move device bytes unchanged (multi-GPU hand-offs use the
-    same calls with peer = n +- 1)."""
-    import ctypes as C
-    lib = _capi.lib()
-    uid = C.create_string_buffer(128)
-    assert lib.pl_comm_unique_id(uid) == 0
-    h = C.c_void_p()
-    _capi.check(lib.pl_comm_init(C.byref(h), uid, 0, 1, torch.cuda.current_device()),
-                "comm init")
-    try:
-        src = torch.arange(1000, dtype=torch.float64, device="cuda") * 0.37
-        dst = torch.zeros_like(src)
-        s = torch.cuda.current_stream().cuda_stream
-        nb = src.numel() * 8
-        _capi.check(lib.pl_comm_group_start(), "group")
-        _capi.check(lib.pl_comm_send(h, src.data_ptr(), nb, 0, s), "send")
-        _capi.check(lib.pl_comm_recv(h, dst.data_ptr(), nb, 0, s), "recv")
-        _capi.check(lib.pl_comm_group_end(), "group")
-        b = src.clone()
-        _capi.check(lib.pl_comm_bcast(h, b.data_ptr(), nb, 0, s), "bcast")
-        torch.cuda.synchronize()
-        assert torch.equal(dst, src) and torch.equal(b, src)
-    finally:
-        lib.pl_comm_destroy(h)
-
-
 # ------------------------------------- lexicographic Gauss-Seidel and Direct
 @pytest.mark.parametrize("name", names("gsd_k_"))
 def test_gauss_seidel_direct_kernels(name):
@@ -646,17 +583,21 @@ def test_gauss_seidel_direct_kernels(name):
 
 def test_gs_direct_serial_drivers():
     a, m = case("gsd_sdc")
+    log = []
     r = sdc.run_sdc(heat.HeatOperator(heat.Grid(1, 64)), quadrature.uniform_table(4),
                     dev(a["u0"]), 0.25, 4, 1e-10, 20, mg.MgConfig("gauss-seidel"),
-                    mg.ToTolerance(1e-12))
+                    mg.ToTolerance(1e-12), solve_log=log)
+    assert log == m["gs"]["solves"]     # per sub-step V-cycles and status
     assert r.iterations == m["gs"]["iterations"]
     assert r.vcycles == m["gs"]["vcycles"]
     for got, ref in zip(r.residuals, m["gs"]["residuals"]):
         np.testing.assert_allclose(got, ref, rtol=1e-6, atol=1e-14)
     close(r.u, a["gs_u"])
+    log = []
     r = sdc.run_sdc(heat.HeatOperator(heat.Grid(2, 16), 1.0, 4), quadrature.uniform_table(4),
                     dev(a["u02"]), 0.125, 2, 1e-11, 30, mg.MgConfig("gauss-seidel"),
-                    mg.Direct())
+                    mg.Direct(), solve_log=log)
+    assert log == m["direct"]["solves"]
     assert r.iterations == m["direct"]["iterations"]
     assert r.vcycles == 0
     close(r.u, a["direct_u"])
@@ -670,42 +611,14 @@ def test_pfasst_gauss_seidel_and_direct(name):
                               quadrature.uniform_table(k - 1), mg.MgConfig("gauss-seidel"),
                               pol, space_interp_order=4)
               for n, k in zip(m["ns"], m["nodes"])]
+    log = []
     res = pfasst.pfasst_run(levels, dev(a["u0"]), m["dt"] * m["p"], m["p"], tol=m["tol"],
-                            max_iter=20)
+                            max_iter=20, solve_log=log)
+    assert [r for blk in log for r in blk] == m["solves"]
     assert res.rank_iterations == m["rank_iterations"]
     assert res.rank_vcycles == m["rank_vcycles"]
     assert res.converged == m["converged"]
     close(res.u, a["u"])
-
-
-@pytest.mark.parametrize("n,length,sigma", [(32, 1.0, 0.01), (64, 1.0, 0.003), (128, 3.0, 0.01),
-                                            (256, 1.0, 1.0 / 512)])
-@pytest.mark.parametrize("pre", [1, 2])
-def test_fused_presweep_residual_restriction(n, length, sigma, pre):
-    """k_rbrfw (last jor-rb pre-sweep + residual + full weighting in one pass,
-    overlapped halo tiles, several z chunks, ragged edge tiles) gives the
-    separate sweep + k_rfw V-cycle bit for bit, from a guess and from zero."""
-    rng = np.random.default_rng(5 * n + pre)
-    g = heat.Grid(3, n, length)
-    u = dev(rng.standard_normal(g.shape))
-    b = dev(rng.standard_normal(g.shape))
-    sop = mg.ShiftedOperator(heat.HeatOperator(g), sigma)
-    cfg = mg.MgConfig("jor-rb", 1.0 if pre == 1 else 0.9, pre, 1)
-    _capi.set_option(_capi.OPT_ZMARCH_MIN_N, 31)
-    try:
-        _capi.set_option(_capi.OPT_RBRFW, 0)
-        ref = mg.v_cycle(sop, u, b, cfg)
-        ref0 = mg.v_cycle(sop, torch.zeros_like(u), b, cfg)
-        _capi.set_option(_capi.OPT_RBRFW, 1)
-        got = mg.v_cycle(sop, u, b, cfg)
-        assert torch.equal(got, ref), float((got - ref).abs().max())
-        assert torch.equal(mg.v_cycle(sop, torch.zeros_like(u), b, cfg), ref0)
-        _capi.set_option(_capi.OPT_ZMARCH, 0)
-        assert torch.equal(mg.v_cycle(sop, u, b, cfg), ref)
-    finally:
-        _capi.set_option(_capi.OPT_ZMARCH, 1)
-        _capi.set_option(_capi.OPT_RBRFW, 0)
-        _capi.set_option(_capi.OPT_ZMARCH_MIN_N, 127)
 
 
 def test_cfg3_full_size_two_iterations():
@@ -851,27 +764,6 @@ def test_sweep_fused_apply_rhs_equals_separate(n, with_tau, policy):
     assert outs[0][2] == outs[1][2]
     assert torch.equal(outs[0][0], outs[1][0])
     assert torch.equal(outs[0][1], outs[1][1])
-
-
-@pytest.mark.parametrize("n,sigma", [(128, 1.0 / 128), (256, 0.37)])
-@pytest.mark.parametrize("threads", [256, 288])
-def test_rfw_thread_layouts_equal_plain_kernels(n, sigma, threads):
-    """The fused residual + full-weighting kernel with eight or nine warps
-    gives the plain kernels' V-cycle (residual, then full weighting) bit for bit."""
-    rng = np.random.default_rng(n + threads)
-    g = heat.Grid(3, n)
-    u = dev(rng.standard_normal(g.shape))
-    b = dev(rng.standard_normal(g.shape))
-    sop = mg.ShiftedOperator(heat.HeatOperator(g), sigma)
-    cfg = mg.MgConfig("jor-rb", 1.0, 1, 1)
-    _capi.set_option(_capi.OPT_RFW, 0)
-    ref = mg.v_cycle(sop, u, b, cfg)
-    _capi.set_option(_capi.OPT_RFW, 1)
-    _capi.set_option(_capi.OPT_RFW_THREADS, threads)
-    try:
-        assert torch.equal(mg.v_cycle(sop, u, b, cfg), ref)
-    finally:
-        _capi.set_option(_capi.OPT_RFW_THREADS, 288)
 
 
 @pytest.mark.parametrize("n,sigma", [(128, 1.0 / 128), (256, 0.37)])

@@ -252,14 +252,18 @@ def test_direct_fast_diagonalisation_matches_superlu(dim, n, order):
 def test_gs_direct_drivers():
     a, m = case("gsd_sdc")
     op = O.Op(1, 64)
+    log = []
     g = O.run_sdc(op, O.uniform_table(4), a["u0"], 0.25, 4, 1e-10, 20, O.Mg("gauss-seidel"),
-                  O.ToTol(1e-12))
+                  O.ToTol(1e-12), solve_log=log)
+    assert [list(x) for x in log] == m["gs"]["solves"]
     assert g["iterations"] == m["gs"]["iterations"]
     assert g["residuals"] == m["gs"]["residuals"]
     assert g["vcycles"] == m["gs"]["vcycles"]
     eq(g["u"], a["gs_u"])
+    log = []
     d = O.run_sdc(O.Op(2, 16, 1.0, 4), O.uniform_table(4), a["u02"], 0.125, 2, 1e-11, 30,
-                  O.Mg("gauss-seidel"), O.DirectSolve())
+                  O.Mg("gauss-seidel"), O.DirectSolve(), solve_log=log)
+    assert [list(x) for x in log] == m["direct"]["solves"]
     assert d["iterations"] == m["direct"]["iterations"]
     assert d["vcycles"] == m["direct"]["vcycles"] == 0
     eq(d["u"], a["direct_u"])
