@@ -121,29 +121,6 @@ def build_levels(w):
             for n, k in zip(w["ns"], w["nodes"])]
 
 
-def alg_bytes_of_one_substep(w):
-    """Algorithmic bytes (SURVEY.md 8(d) model, counted by the runtime) of one
-    fine-level sub-step: rhs + V-cycles + f refresh."""
-    import torch
-    from paper_1407_6486_b200 import _capi
-    from paper_1407_6486_b200.heat import Grid, HeatOperator, seeded_field
-    from paper_1407_6486_b200.multigrid import MgConfig, ShiftedOperator, vcycles_into
-    from paper_1407_6486_b200._device import clone_field, to_device
-    g = Grid(w["dim"], w["ns"][0])
-    op = HeatOperator(g)
-    u = to_device(seeded_field(g))[0]
-    b = clone_field(u)
-    cfg = MgConfig(w["smoother"], w["omega"], w["pre"], w["post"])
-    sop = ShiftedOperator(op, w["dt"] / (w["nodes"][0] - 1))
-    vcycles_into(sop, u, b, cfg, w["cycles"])        # warm (plans, LU)
-    torch.cuda.synchronize()
-    _capi.stats_reset()
-    vcycles_into(sop, u, b, cfg, w["cycles"])
-    torch.cuda.synchronize()
-    st = _capi.stats()
-    return sum(v[1] for v in st.values()) + (32.0 + 16.0) * g.dof
-
-
 def run_ours(args, w):
     import numpy as np
     import torch
@@ -270,8 +247,7 @@ def run_ours(args, w):
             achieved = (bytes_dom / n_dom) / ((ms_dom / n_dom) / 1e3) / 1e9 if n_dom else None
         traffic, traffic_src = ncu_traffic(dom)
         out = {
-            "metric": "PFASST time-steps/s (MG V-cycle DOF-updates/s and HBM GB/s in "
-                      "'vcycle' / 'roofline')",
+            "metric": "PFASST time-steps/s",
             "value": value, "unit": "time-steps/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64",
@@ -321,7 +297,6 @@ def run_ours(args, w):
             "clocks": clk.summary(),
         }
         out["vcycle"] = vcycle_rate(w)
-        out["block_over_sample"] = (alg_total / args.steps) / alg_bytes_of_one_substep(w)
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
@@ -384,90 +359,267 @@ def vcycle_rate(w, reps=10):
 
 # ---------------------------------------------------------------------------
 # reference arm: the reference's CPU algorithm (oracle port, numpy)
+#
+# A PFASST block is (K + P - 1) rank-iterations deep on the reference's
+# threaded executor (one thread per time rank; rank n's iteration k waits for
+# rank n-1's, pfasst.py:231-253), after a predictor of P coarsest sweeps and
+# one interpolate_up (pfasst.py:166-181).  One rank-iteration at full size is
+# split into units -- restrict + FAS per level, the coarsest sweep, per level
+# the coarse correction and the sweep, and the finest sweep as its quadrature,
+# one sub-step (x M) and the hand-off + residual -- and every unit is timed at
+# full size on min(P, cores) single-threaded worker processes running it
+# concurrently (each process is one time rank with its own state), so the
+# memory-bandwidth contention is that of P concurrent ranks.  Then
+#   block = (K + P - 1) * sum(units) + P * sweep_coarsest + sum(corrections)
+# with K the GPU run's iteration count (20 for cfg3: no rank converges).
 
 
-def oracle_sample(w):
-    """One fine-level sub-step of the workload via the oracle: rhs build,
-    FixedCycles V-cycles, f refresh (sdc.py:102-112).  Returns seconds."""
-    import numpy as np
-    from oracle import pintlab_oracle as O
-    op = O.Op(w["dim"], w["ns"][0])
-    u = O.seeded_field(w["dim"], w["ns"][0])
-    f = O.heat_apply(op, u)
-    s = np.zeros_like(u)
-    dtm = w["dt"] / (w["nodes"][0] - 1)
-    cfg = O.Mg(w["smoother"], w["omega"], w["pre"], w["post"])
+def cpu_units(w):
+    """Unit names of one rank-iteration, in the order mlsdc_iteration runs
+    them (hierarchy.py:166-203), and how often each occurs."""
+    L = len(w["ns"])
+    units = [f"down{l}" for l in range(L - 1)] + [f"sweep{L - 1}"]
+    for l in range(L - 2, -1, -1):
+        units.append(f"corr{l}")
+        if l > 0:
+            units.append(f"sweep{l}")
+    units += ["quad0", "sub0", "resid0"]
+    mult = {u: 1 for u in units}
+    mult["sub0"] = w["nodes"][0] - 1
+    return units, mult
+
+
+class _CpuRank:
+    """One time rank's full-size state on the oracle, and the units of a
+    rank-iteration restated from oracle primitives (mlsdc_iteration and
+    sdc_sweep split where the units cut them)."""
+
+    def __init__(self, w):
+        import numpy as np
+        from oracle import pintlab_oracle as O
+        self.O, self.np, self.w = O, np, w
+        self.dt = w["dt"]
+        self.lv = [O.Lvl(O.Op(w["dim"], n), O.uniform_table(k - 1),
+                         O.Mg(w["smoother"], w["omega"], w["pre"], w["post"]),
+                         O.Fixed(w["cycles"]), w["interp"])
+                   for n, k in zip(w["ns"], w["nodes"])]
+        self.ts = O.Step.spread(self.lv, O.seeded_field(w["dim"], w["ns"][0]))
+        self.old = [s.copy() for s in self.ts.states]
+        self.s = None
+
+    def run(self, unit):
+        O, np, ts, lv, dt = self.O, self.np, self.ts, self.lv, self.dt
+        kind, l = unit[:-1], int(unit[-1])
+        if kind == "down":               # hierarchy.py:177-186
+            r = O.restrict_state(ts.states[l], lv[l], lv[l + 1])
+            ts.tau[l + 1] = O.compute_fas(ts.states[l], r, lv[l], lv[l + 1], dt,
+                                          fine_tau=ts.tau[l])
+            self.old[l + 1] = r.copy()
+            ts.states[l + 1] = r
+            ts.y0[l + 1] = r.y[0].copy()
+        elif kind == "sweep":            # sdc.py:84-114
+            O._sweep_level(ts, l, dt, None)
+        elif kind == "corr":             # hierarchy.py:196-198
+            O.coarse_correction(ts.states[l], self.old[l + 1], ts.states[l + 1], lv[l],
+                                lv[l + 1])
+            ts.y0[l] = ts.states[l].y[0].copy()
+        elif kind == "quad":             # sdc.py:93-97
+            st, q = ts.states[0], ts.states[0].table.q
+            self.s = dt * np.tensordot(q[1:] - q[:-1], st.f, axes=(1, 0))
+            st.y[0] = ts.y0[0]
+            st.f[0] = O.heat_apply(lv[0].op, ts.y0[0])
+        elif kind == "sub":              # sdc.py:98-113, a middle sub-step
+            st, m = ts.states[0], (self.w["nodes"][0] - 1) // 2
+            if self.s is None:
+                self.run("quad0")
+            dtm = float(st.table.gammas[m]) * dt
+            rhs = st.y[m] - dtm * st.f[m + 1] + self.s[m]
+            if ts.tau[0] is not None:
+                rhs = rhs + (ts.tau[0][m + 1] - ts.tau[0][m])
+            u, _, _ = O.mg_solve(lv[0].op, dtm, st.y[m + 1].copy(), rhs, lv[0].cfg,
+                                 lv[0].policy)
+            st.y[m + 1] = u
+            st.f[m + 1] = O.heat_apply(lv[0].op, u)
+        elif kind == "resid":            # pfasst.py:189-200: hand-off + residual
+            st = ts.states[0]
+            st.y[0] = ts.y0[0]
+            st.f[0] = O.heat_apply(lv[0].op, ts.y0[0])
+            O.residual(st, ts.y0[0], dt)
+        else:
+            raise ValueError(unit)
+
+
+def _cpu_worker(conn, w):
     t0 = time.perf_counter()
-    rhs = u - dtm * f + s
-    v, _, _ = O.mg_solve(op, dtm, u.copy(), rhs, cfg, O.Fixed(w["cycles"]))
-    O.heat_apply(op, v)
-    return time.perf_counter() - t0
+    rank = _CpuRank(w)
+    conn.send(time.perf_counter() - t0)
+    while True:
+        unit = conn.recv()
+        if unit is None:
+            break
+        t0 = time.perf_counter()
+        rank.run(unit)
+        conn.send(time.perf_counter() - t0)
+    conn.close()
 
 
-def cpu_extrapolate(w, sample_s, threads, samples, block_alg_bytes, sample_alg_bytes):
-    """Time-steps/s of the reference algorithm on this host, extrapolated from
-    the measured sub-step samples by algorithmic bytes."""
-    per_sample = sample_s / samples * threads      # seconds per sample per thread
-    block_s = per_sample * block_alg_bytes / sample_alg_bytes / threads
-    return w["p"] / block_s
+def _mem_available():
+    try:
+        with open("/proc/meminfo") as fh:
+            for line in fh:
+                if line.startswith("MemAvailable:"):
+                    return int(line.split()[1]) * 1024
+    except OSError:
+        pass
+    return None
 
 
-def run_reference(args, w, ratio=None):
+class CpuRanks:
+    """min(P, cores) worker processes (spawned, single-threaded BLAS), each
+    holding one time rank's state; ``time(unit)`` runs the unit on all of
+    them at once and returns the wall time."""
+
+    def __init__(self, w, max_procs=None):
+        import multiprocessing as mp
+        self.cores = os.cpu_count() or 1
+        n = max(1, min(w["p"], self.cores, max_procs or w["p"]))
+        # bound by memory: about 3 (M+1) + 8 fine fields per process
+        per = 8.0 * (w["ns"][0] - 1) ** w["dim"] * (3 * w["nodes"][0] + 8)
+        avail = _mem_available()
+        if avail:
+            n = max(1, min(n, int(0.7 * avail // per)))
+        self.procs_n = n
+        saved = {k: os.environ.get(k) for k in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS",
+                                                 "MKL_NUM_THREADS", "CUDA_VISIBLE_DEVICES")}
+        os.environ.update(OMP_NUM_THREADS="1", OPENBLAS_NUM_THREADS="1", MKL_NUM_THREADS="1",
+                          CUDA_VISIBLE_DEVICES="")
+        ctx = mp.get_context("spawn")
+        self.conns, self.procs = [], []
+        try:
+            for _ in range(n):
+                a, b = ctx.Pipe()
+                pr = ctx.Process(target=_cpu_worker, args=(b, w), daemon=True)
+                pr.start()
+                self.conns.append(a)
+                self.procs.append(pr)
+        finally:
+            for k, v in saved.items():
+                if v is None:
+                    os.environ.pop(k, None)
+                else:
+                    os.environ[k] = v
+        self.setup_s = max(c.recv() for c in self.conns)
+
+    def time(self, unit):
+        t0 = time.perf_counter()
+        for c in self.conns:
+            c.send(unit)
+        for c in self.conns:
+            c.recv()
+        return time.perf_counter() - t0
+
+    def close(self):
+        for c in self.conns:
+            try:
+                c.send(None)
+            except Exception:
+                pass
+        for pr in self.procs:
+            pr.join(timeout=10)
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+
+def host_info():
+    import numpy as np
+    model = None
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    try:
+        import scipy
+        sv = scipy.__version__
+    except Exception:
+        sv = None
+    return {"cpu_model": model, "os_cpu_count": os.cpu_count(), "blas_threads": 1,
+            "numpy": np.__version__, "scipy": sv}
+
+
+def cpu_block_estimate(w, unit_s, iters):
+    """(seconds per block, seconds per rank-iteration) from the per-unit
+    concurrent wall times."""
+    units, mult = cpu_units(w)
+    t_ri = sum(unit_s[u] * mult[u] for u in units)
+    L = len(w["ns"])
+    predictor = w["p"] * unit_s[f"sweep{L - 1}"] + sum(unit_s[f"corr{l}"]
+                                                        for l in range(L - 1))
+    return (iters + w["p"] - 1) * t_ri + predictor, t_ri
+
+
+def run_reference(args, w, iters=None, passes=None, max_procs=None):
+    """The reference's algorithm (oracle port) on this host's cores: each
+    step times one unit of a rank-iteration (round robin) on the concurrent
+    rank processes; ``passes`` (the cpu_baseline leg) times every unit that
+    many times instead."""
     rank, world, _ = env_rank()
     if rank != 0:
         return None
-    threads = max(1, min(8, os.cpu_count() or 1))
-    # algorithmic bytes of a whole block over those of one sample (the same
-    # model the GPU arm counts): live from the GPU arm, else its recorded value
-    model = {"block_over_sample": ratio} if ratio else BLOCK_MODEL[args.workload]
-    # one single-threaded worker PROCESS per core (spawned: numpy/scipy BLAS
-    # called from several threads of one process aborted once with a heap
-    # error); a round's time is its slowest worker's sample (they run together)
-    import concurrent.futures as cf
-    import multiprocessing as mp
-    saved = {k: os.environ.get(k) for k in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS",
-                                             "MKL_NUM_THREADS", "CUDA_VISIBLE_DEVICES")}
-    os.environ.update(OMP_NUM_THREADS="1", OPENBLAS_NUM_THREADS="1", MKL_NUM_THREADS="1",
-                      CUDA_VISIBLE_DEVICES="")
-    vals = []
-    try:
-        with cf.ProcessPoolExecutor(max_workers=threads,
-                                    mp_context=mp.get_context("spawn")) as pool:
+    iters = iters or 20
+    units, _ = cpu_units(w)
+    samples = {u: [] for u in units}
+    with CpuRanks(w, max_procs) as pool:
+        if passes:
+            for _ in range(passes):
+                for u in units:
+                    samples[u].append(pool.time(u))
+            steps_note = f"{passes} pass(es) over the {len(units)} units"
+        else:
             for i in range(args.warmup + args.steps):
-                wall = max(pool.map(oracle_sample, [w] * threads))
+                u = units[i % len(units)]
+                t = pool.time(u)
                 if i >= args.warmup:
-                    vals.append(wall)
-    finally:
-        for k, v in saved.items():
-            if v is None:
-                os.environ.pop(k, None)
-            else:
-                os.environ[k] = v
-    wall = sum(vals)
-    samples = threads * len(vals)
-    value = w["p"] / (wall / samples * model["block_over_sample"])
+                    samples[u].append(t)
+            missing = [u for u in units if not samples[u]]
+            for u in missing:          # fewer timed steps than units
+                samples[u].append(pool.time(u))
+            steps_note = (f"{args.steps} timed steps, one unit each (round robin)" +
+                          (f"; {len(missing)} units timed after the loop" if missing else ""))
+        nproc, setup_s = pool.procs_n, pool.setup_s
+    all_t = [t for v in samples.values() for t in v]
+    unit_s = {u: statistics.mean(v) for u, v in samples.items()}
+    block_s, t_ri = cpu_block_estimate(w, unit_s, iters)
+    value = w["p"] / block_s
+    grid = f"{w['ns'][0] - 1}^{w['dim']}"
+    sample = (f"full-size ({grid}) units of one rank-iteration of the oracle port, each run "
+              f"concurrently on {nproc} single-threaded processes (one time rank each): "
+              f"{steps_note}; rank-iteration {t_ri:.1f} s; block = (K + P - 1) = "
+              f"{iters + w['p'] - 1} rank-iterations + predictor = {block_s:.0f} s "
+              f"(threaded-executor wavefront bound, pfasst.py:231-253)")
     return {"impl": "reference", "metric": "PFASST time-steps/s", "value": value,
             "unit": "time-steps/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "higher_is_better": True, "dtype": "f64",
+            "warmup": args.warmup,
+            # wall time of one timed step (one unit on every rank process);
+            # ``value`` is P / the block time those units add up to
+            "ms_per_step": 1e3 * statistics.mean(all_t),
+            "higher_is_better": True, "dtype": "f64",
+            "data": "synthetic (seeded Fourier-mode u0, SURVEY.md 8(d))",
             "config": {"workload": args.workload},
-            "cpu_baseline": {"value": value, "unit": "time-steps/s", "cores": threads,
-                             "kind": "port",
-                             "sample": f"{samples} fine sub-steps (rhs + {w['cycles']} V-cycle "
-                                       f"+ f refresh at {w['ns'][0] - 1}^{w['dim']}) on "
-                                       f"{threads} single-threaded processes; block time "
-                                       f"extrapolated x"
-                                       f"{model['block_over_sample']:.1f} by algorithmic bytes"},
+            "cpu_baseline": {"value": value, "unit": "time-steps/s", "cores": nproc,
+                             "kind": "port", "sample": sample,
+                             "unit_seconds": {u: round(t, 3) for u, t in unit_s.items()},
+                             "rank_iteration_s": t_ri, "block_s": block_s,
+                             "setup_s": setup_s, "host": host_info()},
             "e2e": {"value": value, "unit": "time-steps/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
-
-
-# block / sample algorithmic-byte ratios measured by the GPU arm (the runtime's
-# byte counter over one block vs one fine sub-step); refreshed by --calibrate
-BLOCK_MODEL = {
-    "cfg3": {"block_over_sample": 2230.4},     # profiles/r01/bench.json (GPU arm, live)
-    "cfg4": {"block_over_sample": 1048.1},
-    "cfg2": {"block_over_sample": 1124.9},
-}
 
 
 def main():
@@ -492,10 +644,9 @@ def main():
     out = run_ours(args, w)
     if out is not None:
         if not args.no_cpu_baseline and out["n_gpus"] == 1:
-            ref = run_reference(argparse.Namespace(warmup=0, steps=1, workload=args.workload),
-                                w, out["block_over_sample"])
-            cb = dict(ref["cpu_baseline"])
-            out["cpu_baseline"] = cb
+            ref = run_reference(argparse.Namespace(warmup=0, steps=0, workload=args.workload),
+                                w, iters=max(out["config"]["rank_iterations"]), passes=1)
+            out["cpu_baseline"] = dict(ref["cpu_baseline"])
         print(json.dumps(out))
 
 

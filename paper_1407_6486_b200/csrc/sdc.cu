@@ -476,10 +476,9 @@ int launch_chain_fw(const double* F, long long stride, const Coef& a, double sca
   }
 #undef CF_R
 #undef CF_CALL
-  // the unfused passes it replaces: the chain (K + rows (+ rows) fields) and
-  // one full weighting per row (8 B per fine + 8 B per coarse point)
-  PL_CHECK_LAUNCH(K_FAS, 8.0 * gf.npts * (K + 2 * a.rows + (add ? a.rows : 0)) +
-                             8.0 * gc.npts * a.rows);
+  // SURVEY 8(d) K13 for the fine part: read the K fine F fields (+ the
+  // selected fine tau rows), write one coarse field per selected row
+  PL_CHECK_LAUNCH(K_FAS, 8.0 * gf.npts * (K + (add ? a.rows : 0)) + 8.0 * gc.npts * a.rows);
   return 0;
 }
 

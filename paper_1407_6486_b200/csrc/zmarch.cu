@@ -1503,8 +1503,8 @@ int zlaunch_rfw(const double* u, const double* b, double* coarse, const Geo& g, 
   Geo gc = make_geo(3, (g.N + 1) / 2);
   PL_PRE(K_RESTRICT);
   PL_TRY(launch_rfw(u, b, coarse, g, c, sigma, s));
-  // algorithmic bytes of the unfused pair (residual 24 B, FW 8 B + 8 B coarse)
-  PL_CHECK_LAUNCH(K_RESTRICT, 32.0 * g.npts + 8.0 * gc.npts);
+  // read u, b (16 B per fine point), write the coarse rhs
+  PL_CHECK_LAUNCH(K_RESTRICT, 16.0 * g.npts + 8.0 * gc.npts);
   return 0;
 }
 

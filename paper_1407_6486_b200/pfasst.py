@@ -207,9 +207,12 @@ class DeviceEngine:
     def snapshot(self, t):
         return clone_field(t)
 
-    # wire format of the NCCL hand-offs: the field's flat padded storage
+    on_device = True
+
+    # wire format of the hand-offs: the field's flat padded storage, sent
+    # straight from the state (DistExchange.fence orders later overwrites)
     def to_wire(self, t):
-        return flat_storage(t).clone()
+        return flat_storage(t)
 
     def wire_buffer(self, like):
         return torch.empty(field_elems(tuple(like.shape)), dtype=torch.float64,
@@ -254,6 +257,9 @@ class _LocalExchange:
     def recv_flag(self, n, k):
         return None        # resolved from this process's own bookkeeping
 
+    def fence(self, n):
+        pass
+
 
 class DistExchange:
     """torch.distributed point-to-point hand-offs between processes (NCCL on
@@ -263,7 +269,15 @@ class DistExchange:
     receives are posted when the receiving rank starts its iteration (and
     waited on at once), sends are posted as soon as the payload is final,
     and the 8-byte converged flag is received lazily, right before the host
-    needs it."""
+    needs it.
+
+    No payload is copied for sending: a send reads the sender's live state
+    (its flat padded storage), and ``fence(n)`` -- called before rank n's
+    next sweep can overwrite that state -- makes the compute stream wait for
+    rank n's outstanding sends (a device-side wait under NCCL).  Receives land
+    in per-(rank, level) buffers reused across iterations.  With device
+    fields on a gloo group (two processes sharing one GPU in the tests) the
+    wire is staged through host memory."""
 
     def __init__(self, engine, group=None):
         import torch.distributed as dist
@@ -272,10 +286,13 @@ class DistExchange:
         self.group = group
         self.world = dist.get_world_size(group)
         self.me = dist.get_rank(group)
-        self._pending = []       # outstanding send works (+ their buffers)
+        self._pending = {}       # rank n -> outstanding send works (+ their buffers)
         self._cache = {}         # n -> (fine, coarse) once the predecessor froze
         self._last = {}          # n -> last (fine, coarse) received
         self._last_pred = {}
+        self._rbuf = {}          # (n, tag) -> receive buffer
+        self.host_wire = dist.get_backend(group) == "gloo" and getattr(engine, "on_device",
+                                                                       False)
 
     def proc(self, n):
         return n % self.world
@@ -283,62 +300,91 @@ class DistExchange:
     def owns(self, n):
         return self.proc(n) == self.me
 
-    def _send(self, t, dst_rank):
-        buf = self.e.to_wire(t)
-        w = self.dist.isend(buf, self.proc(dst_rank), group=self.group)
-        self._pending.append((w, buf))
-        if len(self._pending) > 16:
-            w0, _ = self._pending.pop(0)
-            w0.wait()
+    def fence(self, n):
+        """Rank n's state may be overwritten after this (its sends are done)."""
+        for w, _ in self._pending.pop(n, ()):
+            w.wait()
 
-    def _recv(self, like, src_rank):
-        buf = self.e.wire_buffer(like)
-        self.dist.irecv(buf, self.proc(src_rank), group=self.group).wait()
+    def _send(self, n, t, dst_rank):
+        buf = self.e.to_wire(t)
+        if self.host_wire:
+            buf = buf.cpu()
+        w = self.dist.isend(buf, self.proc(dst_rank), group=self.group)
+        self._pending.setdefault(n, []).append((w, buf))
+
+    def _recv(self, like, src_rank, n, tag):
+        key = (n, tag)
+        buf = self._rbuf.get(key)
+        if buf is None:
+            buf = self._rbuf[key] = self.e.wire_buffer(like)
+        if self.host_wire:
+            hb = torch.empty(buf.shape, dtype=buf.dtype)
+            self.dist.irecv(hb, self.proc(src_rank), group=self.group).wait()
+            buf.copy_(hb)
+        else:
+            self.dist.irecv(buf, self.proc(src_rank), group=self.group).wait()
         return self.e.from_wire(buf, like)
 
     def send_pred(self, n, ph):
-        self._send(self.e.coarse_payload(n), n + 1)
+        self._send(n, self.e.coarse_payload(n), n + 1)
 
     def recv_pred(self, n, ph):
         # rank n-1 took part in phases 0..n-1; phase n re-reads phase n-1
         if ph < n:
-            self._last_pred[n] = self._recv(self.e.coarse_payload(n), n - 1)
+            self._last_pred[n] = self._recv(self.e.coarse_payload(n), n - 1, n, "pred")
         return self._last_pred[n]
 
     def send_coarse(self, n, k):
-        self._send(self.e.coarse_payload(n), n + 1)
+        self._send(n, self.e.coarse_payload(n), n + 1)
 
     def recv_iteration(self, n, k):
         if n in self._cache:
             return self._cache[n]
-        coarse = self._recv(self.e.coarse_payload(n), n - 1)
-        fine = self._recv(self.e.fine_payload(n), n - 1)
+        coarse = self._recv(self.e.coarse_payload(n), n - 1, n, "coarse")
+        fine = self._recv(self.e.fine_payload(n), n - 1, n, "fine")
         self._last[n] = (fine, coarse)
         return fine, coarse
 
     def send_fine(self, n, k):
-        self._send(self.e.fine_payload(n), n + 1)
+        self._send(n, self.e.fine_payload(n), n + 1)
 
     def send_flag(self, n, k, flag):
-        dev = self.e.fine_payload(n).device
-        buf = torch.tensor([1.0 if flag else 0.0], dtype=torch.float64, device=dev)
+        buf = torch.tensor([1.0 if flag else 0.0], dtype=torch.float64)
+        if not self.host_wire:
+            buf = buf.to(self.e.fine_payload(n).device)
         w = self.dist.isend(buf, self.proc(n + 1), group=self.group)
-        self._pending.append((w, buf))
+        self._pending.setdefault(-1, []).append((w, buf))
 
     def recv_flag(self, n, k):
         if n in self._cache:
             return True
-        flag = torch.empty(1, dtype=torch.float64, device=self.e.fine_payload(n).device)
+        flag = torch.empty(1, dtype=torch.float64)
+        if not self.host_wire:
+            flag = flag.to(self.e.fine_payload(n).device)
         self.dist.irecv(flag, self.proc(n - 1), group=self.group).wait()
         ok = bool(flag.item() != 0.0)
         if ok:                   # predecessor frozen: keep its final payloads
             self._cache[n] = self._last[n]
         return ok
 
+    def broadcast_final(self, p, like):
+        """The last rank's fine value of the block, on every process
+        (pfasst.py:272-278)."""
+        last = (p - 1) % self.world
+        wire = self.e.to_wire(self.e.fine_payload(p - 1)) if self.owns(p - 1) \
+            else self.e.wire_buffer(like)
+        if self.host_wire:
+            host = wire.cpu()
+            self.dist.broadcast(host, last, group=self.group)
+            if not self.owns(p - 1):
+                wire.copy_(host)
+        else:
+            self.dist.broadcast(wire, last, group=self.group)
+        return self.e.snapshot(self.e.from_wire(wire, like))
+
     def finish(self):
-        for w, _ in self._pending:
-            w.wait()
-        self._pending.clear()
+        for n in list(self._pending):
+            self.fence(n)
         self._cache.clear()
         self._last.clear()
         self._last_pred.clear()
@@ -384,6 +430,7 @@ class _Block:
                     continue
                 if n > 0:
                     e.set_coarse_y0(n, x.recv_pred(n, ph))
+                x.fence(n)          # the sweep overwrites the last coarse payload
                 self.tag = (0, ph, n)
                 self.vcycles[n] += e.burn_in(n)
                 if n + 1 < p and not x.owns(n + 1):
@@ -452,6 +499,7 @@ class _Block:
                         stopped.add(n)
                     continue
                 active = True
+                x.fence(n)          # this iteration overwrites the payloads sent
                 if n > 0:
                     fine, coarse = x.recv_iteration(n, k)
                     e.set_fine_y0(n, fine)
@@ -673,10 +721,7 @@ def pfasst_run(levels, u0, t_end: float, p: int, blocks: int = 1, tol: float = 1
             exchange.finish()
             last = (p - 1) % exchange.world
             like = engine.fine_payload(engine.ranks[0]) if engine.ranks else u
-            wire = engine.to_wire(engine.fine_payload(p - 1)) if exchange.owns(p - 1) \
-                else engine.wire_buffer(like)
-            exchange.dist.broadcast(wire, last, group=group)
-            u = engine.from_wire(wire, like)
+            u = exchange.broadcast_final(p, like)
             if record_final_values:
                 fv = [v.contiguous().cpu().numpy() for v in blk.final_values] \
                     if exchange.owns(p - 1) else None
