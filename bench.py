@@ -135,7 +135,11 @@ def run_ours(args, w):
         k, v = kv.split("=")
         _capi.set_option(int(k), int(v))
     if world > 1:
-        dist.init_process_group("nccl", init_method="env://")
+        # communicator set-up lines (ranks, NVLink/NVLS transport) on stderr
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        dist.init_process_group("nccl", init_method="env://",
+                                device_id=torch.device("cuda", local))
     executor = "nccl" if world > 1 else "serial"
     levels = build_levels(w)
     p, dt = w["p"], w["dt"]

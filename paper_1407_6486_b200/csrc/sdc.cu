@@ -403,7 +403,8 @@ int launch_axpby(const double* a, const double* b, double* out, int sub, long lo
 int g_fuse_fas_fw = 1;   // PL_OPT_FUSE_FAS_FW
 
 bool fw_select_ok(const Geo& gf, int nsel) {
-  return g_fuse_fas_fw && gf.dim == 3 && gf.N >= 127 && nsel >= 1 && nsel <= 5;
+  return g_fuse_fas_fw && gf.dim == 3 && gf.N >= 31 && zmarch_size_ok(gf.N) && nsel >= 1 &&
+         nsel <= 5;
 }
 
 // coarse[j] = FW(fine[idx[j]]) for j < nsel in one launch (k_chain_fw<IDENT>)
@@ -436,7 +437,8 @@ int launch_fw_select(const double* fine, long long stride, const int* idx, int n
 }
 
 bool chain_fw_ok(const Coef& a, const Geo& gf) {
-  return g_fuse_fas_fw && gf.dim == 3 && gf.N >= 127 && a.rows >= 2 && a.rows <= 5 &&
+  return g_fuse_fas_fw && gf.dim == 3 && gf.N >= 31 && zmarch_size_ok(gf.N) && a.rows >= 2 &&
+         a.rows <= 5 &&
          a.cols <= 9;
 }
 
