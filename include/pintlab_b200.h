@@ -98,6 +98,9 @@ const char* pl_last_error(void);
                                  tiled launch, and the FAS fine node integrals are full-weighted in
                                  the same pass (3-D, >= 127^3), never stored; 0: separate
                                  chain and full-weighting launches; bit-identical */
+#define PL_OPT_ZC_FIT 22       /* 1 (default): z chunks of the jor-rb sweep and the cubic kernel
+                                  chosen by a wave-quantisation model of the device's resident
+                                  CTA slots; 0: power-of-two chunks aiming at PL_OPT_ZC_CTAS */
 int pl_set_option(int key, int value);
 
 /* storage elements of one field (incl. row pads) */

@@ -239,6 +239,7 @@ extern int g_mid_tail_n;
 extern int g_rfw_enabled;
 extern int g_zc_floor;
 extern int g_zc_ctas;
+extern int g_zc_fit;
 extern int g_fast_tail;
 extern int g_mid_ctas;
 extern int g_zrb_ring;
@@ -281,6 +282,10 @@ static int set_option_impl(int key, int value) {
       return PL_ERR_ARG;
     }
     g_zc_ctas = value;
+    return 0;
+  }
+  if (key == PL_OPT_ZC_FIT) {
+    g_zc_fit = value != 0;
     return 0;
   }
   if (key == PL_OPT_FAST_TAIL) {

@@ -27,8 +27,13 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
+#include <map>
 #include <mutex>
+#include <queue>
+#include <tuple>
+#include <vector>
 #include <type_traits>
 
 #include "common.cuh"
@@ -1282,6 +1287,176 @@ __global__ void __launch_bounds__(NTHR, 3) k_cubic4(const __grid_constant__ CUte
   }
 }
 
+// ---------------------------------------------------------------------------
+// k_cubic5: fine (+)= P_cubic coarse for 3-D (transfers.py:82-89) with the
+// coincident rows, columns and planes specialised.  A fine index on a coarse
+// point has the single weight 1 in the reference's dense interpolation
+// matrix, so its dgemm chain fma(1, v, 0) + 0 * ... is exactly v + 0.0 for
+// finite v; the other fine indices keep k_cubic4's 4-tap FMA chain in tap
+// order.  Fine x columns and y rows alternate between the two kinds, so every
+// thread owns one of each -- an x task is one column pair of one row, a y
+// task one row pair of one coarse column -- and no warp diverges; fine z
+// planes alternate too, and a coincident plane skips the z pass (its y pass
+// reads the coarse window straight from the TMA ring).  Skewed three-stage
+// pipeline as k_cubic4 (z pass of plane t, y pass of t-1, x pass of t-2), one
+// barrier per plane; coarse windows (20 x 12) and, in accumulate mode, the
+// old fine tiles arrive by TMA.  Bit-identical to k_cubic4.
+constexpr int PYB5 = align16(QW * TY);
+constexpr int NT5 = 256;
+constexpr int RF5 = 6;                       // fine-tile ring (accumulate mode)
+static_assert((TX / 2) * TY == NT5 && (TY / 2) * QW <= NT5 && QW * QH <= NT5, "task layout");
+
+__global__ void __launch_bounds__(NT5, 4) k_cubic5(const __grid_constant__ CUtensorMap mc,
+                                                   const __grid_constant__ CUtensorMap mf,
+                                                   double* __restrict__ fine, Geo gf,
+                                                   const int* __restrict__ tcnt,
+                                                   const int* __restrict__ tidx,
+                                                   const double* __restrict__ tw, int zc,
+                                                   int accumulate) {
+  __shared__ __align__(128) double sc[RQ4 * PQ];
+  __shared__ __align__(128) double zb[2 * PQ];
+  __shared__ __align__(128) double yb[2 * PYB5];
+  __shared__ __align__(8) unsigned long long bar[RQ4];
+  __shared__ __align__(8) unsigned long long fbar[RF5];
+  __shared__ double s_zw[64 * 4];
+  __shared__ int s_zj[64 * 4], s_zn[64];
+  extern __shared__ __align__(128) double sfine[];   // RF4 fine tiles (accumulate)
+  const int tid = threadIdx.x;
+  const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TY;
+  const int z0 = blockIdx.z * zc, z1 = min(z0 + zc, gf.nz);
+  const int n = z1 - z0;
+  const int cx0 = x0 / 2 - 2, cy0 = y0 / 2 - 2;
+  auto first_tap = [&](int iz) { return __ldg(tidx + iz * 4); };
+  auto last_tap = [&](int iz) { return __ldg(tidx + iz * 4 + __ldg(tcnt + iz) - 1); };
+  const int jlo = n > 1 ? min(first_tap(z0), first_tap(z0 + 1)) : first_tap(z0);
+  const int jtop = n > 1 ? max(last_tap(z1 - 1), last_tap(z1 - 2)) : last_tap(z1 - 1);
+  if (tid == 0) {
+    for (int i = 0; i < RQ4; ++i) mbar_init(bar + i, 1);
+    for (int i = 0; i < RF5; ++i) mbar_init(fbar + i, 1);
+    fence_barrier_init();
+  }
+  if (tid < n) {
+    const int iz = z0 + tid, nt = __ldg(tcnt + iz);
+    s_zn[tid] = nt;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      s_zj[tid * 4 + u] = __ldg(tidx + iz * 4 + min(u, nt - 1));
+      s_zw[tid * 4 + u] = u < nt ? __ldg(tw + iz * 4 + u) : 0.0;
+    }
+  }
+  __syncthreads();
+  constexpr int cissuer = NT5 - 32;
+  auto issue_fine = [&](int p) {
+    if (!accumulate || p >= z1) return;
+    const int sl = (p - z0) % RF5;
+    mbar_expect(fbar + sl, PF4 * 8u);
+    tma3(sfine + sl * PF4, &mf, x0, y0, p, fbar + sl);
+  };
+  if (tid == cissuer)
+    for (int p = z0; p < z0 + RF5; ++p) issue_fine(p);
+  int issued = jlo;
+  auto issue_upto = [&](int live_lo) {
+    for (; issued <= jtop && issued < live_lo + RQ4; ++issued) {
+      const int sl = (issued - jlo) & (RQ4 - 1);
+      mbar_expect(bar + sl, QW * QH * 8u);
+      tma3(sc + sl * PQ, &mc, cx0, cy0, issued, bar + sl);
+    }
+  };
+  if (tid == cissuer) issue_upto(jlo);
+  int waited = jlo;
+  // ---- y task: coarse column ycx; fine rows y0+2q (4-tap, table taps) and
+  // y0+2q+1 (coincident with coarse row y0/2+q, window row q+2)
+  const bool yt = tid < (TY / 2) * QW;
+  const int yq = tid / QW, ycx = tid - (tid / QW) * QW;
+  int yi[4];
+  double yw[4];
+  {
+    const int gy = y0 + 2 * yq;
+    const bool ok = yt && gy < gf.ny;
+    const int yn = ok ? __ldg(tcnt + gy) : 1;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      yi[u] = ok ? (__ldg(tidx + gy * 4 + min(u, yn - 1)) - cy0) * QW + ycx : ycx;
+      yw[u] = ok && u < yn ? __ldg(tw + gy * 4 + u) : 0.0;
+    }
+  }
+  const int yci = (yq + 2) * QW + ycx;
+  const int yo = (2 * yq) * QW + ycx;
+  // ---- x task: row xr, columns x0+2xp (4-tap) and x0+2xp+1 (coincident with
+  // coarse column x0/2+xp, window column xp+2)
+  const int xr = tid >> 4, xp = tid & 15;
+  const int gx = x0 + 2 * xp, gy = y0 + xr;
+  int xi[4];
+  double xw[4];
+  {
+    const bool ok = gx < gf.nx;
+    const int xn = ok ? __ldg(tcnt + gx) : 1;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      xi[u] = xr * QW + (ok ? __ldg(tidx + gx * 4 + min(u, xn - 1)) - cx0 : 0);
+      xw[u] = ok && u < xn ? __ldg(tw + gx * 4 + u) : 0.0;
+    }
+  }
+  const int xci = xr * QW + xp + 2;
+  const bool in0 = gx < gf.nx && gy < gf.ny, in1 = gx + 1 < gf.nx && gy < gf.ny;
+  const int fo = xr * TX + 2 * xp;
+  double* fp = fine + (in0 ? gf.at(gx, gy, 0) : 0) + (long long)(z0 - 2) * gf.sz;
+  for (int t = 0; t < n + 2; ++t, fp += gf.sz) {
+    // ---- z pass of fine plane z0+t (4-tap planes only)
+    if (t < n) {
+      const int zn = s_zn[t];
+      int zj[4];
+      double zw[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) { zj[u] = s_zj[t * 4 + u]; zw[u] = s_zw[t * 4 + u]; }
+      for (; waited <= zj[3]; ++waited) {
+        const int k = waited - jlo;
+        mbar_wait(bar + (k & (RQ4 - 1)), (unsigned)((k / RQ4) & 1));
+      }
+      if (zn > 1 && tid < QW * QH) {
+        const double* s0 = sc + ((zj[0] - jlo) & (RQ4 - 1)) * PQ + tid;
+        const double* s1 = sc + ((zj[1] - jlo) & (RQ4 - 1)) * PQ + tid;
+        const double* s2 = sc + ((zj[2] - jlo) & (RQ4 - 1)) * PQ + tid;
+        const double* s3 = sc + ((zj[3] - jlo) & (RQ4 - 1)) * PQ + tid;
+        zb[(t & 1) * PQ + tid] = tap_chain<true>(4, zw, *s0, *s1, *s2, *s3);
+      }
+    }
+    // ---- y pass of fine plane z0+t-1
+    const int t2 = t - 1;
+    if (t2 >= 0 && t2 < n && yt) {
+      const double* zs = s_zn[t2] > 1 ? zb + (t2 & 1) * PQ
+                                      : sc + ((s_zj[t2 * 4] - jlo) & (RQ4 - 1)) * PQ;
+      double* yd = yb + (t2 & 1) * PYB5;
+      yd[yo] = tap_chain<true>(4, yw, zs[yi[0]], zs[yi[1]], zs[yi[2]], zs[yi[3]]);
+      yd[yo + QW] = zs[yci] + 0.0;
+    }
+    // ---- x pass of fine plane z0+t-2
+    const int t3 = t - 2;
+    if (t3 >= 0) {
+      const double* ys = yb + (t3 & 1) * PYB5;
+      double a0 = tap_chain<true>(4, xw, ys[xi[0]], ys[xi[1]], ys[xi[2]], ys[xi[3]]);
+      double a1 = ys[xci] + 0.0;
+      if (accumulate) {
+        mbar_wait(fbar + t3 % RF5, (unsigned)((t3 / RF5) & 1));
+        const double2 o = *reinterpret_cast<const double2*>(sfine + (t3 % RF5) * PF4 + fo);
+        a0 = o.x + a0;
+        a1 = o.y + a1;
+      }
+      if (in1) *reinterpret_cast<double2*>(fp) = make_double2(a0, a1);
+      else if (in0) fp[0] = a0;
+    }
+    __syncthreads();
+    if (tid == cissuer) {
+      if (t3 >= 0) issue_fine(z0 + t3 + RF5);   // x pass of plane t-2 done: slot free
+      int lo = jtop + 1;                     // coarse planes still read: z pass of
+      if (t < n && s_zn[t] == 1) lo = min(lo, s_zj[t * 4]);   // t+1, t+2; y pass of t
+      if (t + 1 < n) lo = min(lo, s_zj[(t + 1) * 4]);
+      if (t + 2 < n) lo = min(lo, s_zj[(t + 2) * 4]);
+      issue_upto(lo);
+    }
+  }
+}
+
 constexpr int PREF1 = 3;
 constexpr int PREF2 = 3;
 
@@ -1326,6 +1501,7 @@ int g_zrev_mask = 3;   // PL_OPT_ZREV: reverse z-chunk order of 1 apply / apply+
 int g_rfw_threads = 288;   // PL_OPT_RFW_THREADS: 256 (eight warps) or 288 (nine, default)
 int g_zc_floor = 16;  // PL_OPT_ZC_FLOOR (A/B): smallest z chunk (4 and 8 measured slower at 127^3)
 int g_zc_ctas = 148 * 8;   // PL_OPT_ZC_CTAS (A/B): CTA count the z chunking aims for
+int g_zc_fit = 1;          // PL_OPT_ZC_FIT: wave-aware z chunks (pick_zc_fit)
 namespace {
 int pick_zc(const Geo& g) {
   // enough CTAs for several waves on 148 SMs; chunk halo planes cost
@@ -1341,6 +1517,66 @@ int pick_zc(const Geo& g) {
 template <typename K>
 void raise_smem(K kern, size_t bytes) {
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+}
+
+// resident CTAs of one kernel configuration on the whole device (cached)
+template <typename K>
+int resident_ctas(K kern, int threads, size_t smem) {
+  static std::mutex mu;
+  static std::map<std::tuple<const void*, int, size_t, int>, int> cache;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  auto key = std::make_tuple((const void*)kern, threads, smem, dev);
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = cache.find(key);
+  if (it != cache.end()) return it->second;
+  int sms = 0, per = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, threads, smem);
+  const int r = sms * (per > 0 ? per : 1);
+  cache[key] = r;
+  return r;
+}
+
+// Wave-aware z chunk (PL_OPT_ZC_FIT): the CTAs of a z-marching kernel (tiles
+// x chunks, dispatched in blockIdx order) are list-scheduled on the device's
+// resident slots, each taking (planes + extra) plane-phases, where extra is
+// the pipeline fill and the per-CTA prologue; the chunk length in [zmin, zmax]
+// (a multiple of step) with the shortest makespan wins, ties to the longer
+// chunk.  At 255^3 with 4 CTAs per SM the power-of-two chunks give 1.7 or 3.5
+// waves; e.g. 30-plane chunks give 1,152 CTAs = 1.95 waves.
+int pick_zc_fit(const Geo& g, int slots, int step, int extra, int zmin, int zmax) {
+  if (!g_zc_fit) return pick_zc(g);
+  static std::mutex mu;
+  static std::map<std::tuple<int, int, int, int, int, int, int>, int> cache;
+  const long long tiles = (long long)ceil_div(g.nx, TX) * ceil_div(g.ny, TY);
+  auto key = std::make_tuple(g.nz, (int)tiles, slots, step, extra, zmin, zmax);
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = cache.find(key);
+  if (it != cache.end()) return it->second;
+  int best = zmax;
+  long long best_t = -1;
+  std::vector<long long> fin;
+  for (int zc = zmax; zc >= zmin; zc -= step) {
+    fin.assign(slots, 0);
+    std::make_heap(fin.begin(), fin.end(), std::greater<long long>());
+    long long end = 0;
+    for (int z = 0; z < g.nz; z += zc) {
+      const long long d = std::min(zc, g.nz - z) + extra;
+      for (long long t = 0; t < tiles; ++t) {
+        std::pop_heap(fin.begin(), fin.end(), std::greater<long long>());
+        fin.back() += d;
+        end = std::max(end, fin.back());
+        std::push_heap(fin.begin(), fin.end(), std::greater<long long>());
+      }
+    }
+    if (best_t < 0 || end < best_t) {
+      best_t = end;
+      best = zc;
+    }
+  }
+  cache[key] = best;
+  return best;
 }
 
 template <int OP>
@@ -1409,10 +1645,12 @@ int launch_zrb3(const double* u, const double* b, double* out, const Geo& g, con
   const bool big = g_zrb_ring == 0 && g.N >= 255;
   if (big) zc = zc < 32 ? 32 : zc;
   if (g_zrb_ring == 1 || big) {   // 6 u + 3 b planes, 4 CTAs per SM (register cap 64)
-    grid.z = ceil_div(g.nz, zc);
     size_t smem = ((size_t)6 * PU + (size_t)3 * PB) * 8 + 8 * (6 + 3);
     auto kern = c.pow2 ? k_zrb3<true, 6, 3, 4> : k_zrb3<false, 6, 3, 4>;
     raise_smem(kern, smem);
+    // even chunks (the phase code assumes an even z0)
+    if (g_zc_fit) zc = pick_zc_fit(g, resident_ctas(kern, NTHR_RB2, smem), 2, 5, 16, 64);
+    grid.z = ceil_div(g.nz, zc);
     kern<<<grid, dim3(NTHR_RB2), smem, s>>>(mu, mb, out, g, c, sigma, omega, dval, dinv, zc);
     return 0;
   }
@@ -1454,8 +1692,17 @@ int launch_cubic4(const double* coarse, double* fine, const Geo& gf, const int* 
   std::memset(&mf, 0, sizeof(mf));
   if (accumulate) PL_TRY(make_map(&mf, fine, gf, TX, TY));
   size_t smem = accumulate ? sizeof(double) * RF4 * PF4 : 0;
-  raise_smem(k_cubic4<true>, smem);
-  k_cubic4<true><<<grid, block, smem, s>>>(mc, mf, fine, gf, cnt, idx, w, zc, accumulate);
+  static const bool use4 = std::getenv("PL_CUBIC4") != nullptr;   // dev A/B only
+  if (use4) {
+    raise_smem(k_cubic4<true>, smem);
+    k_cubic4<true><<<grid, block, smem, s>>>(mc, mf, fine, gf, cnt, idx, w, zc, accumulate);
+    return 0;
+  }
+  const size_t smem5 = accumulate ? sizeof(double) * RF5 * PF4 : 0;
+  raise_smem(k_cubic5, smem5);
+  const int zc5 = pick_zc_fit(gf, resident_ctas(k_cubic5, NT5, smem5), 1, 5, 8, 64);
+  grid.z = ceil_div(gf.nz, zc5);
+  k_cubic5<<<grid, NT5, smem5, s>>>(mc, mf, fine, gf, cnt, idx, w, zc5, accumulate);
   return 0;
 }
 
