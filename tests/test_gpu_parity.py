@@ -430,9 +430,9 @@ def test_zrb_variants_bitwise_31cubed(ring):
         _capi.set_option(_capi.OPT_ZMARCH_MIN_N, 127)
 
 
-@pytest.mark.parametrize("n,length,sigma", [(128, 1.0, 1.0 / 128), (256, 1.0, 0.37),
-                                            (128, 3.0, 0.01)])
-def test_zrb_variants_equal_plain_kernels(n, length, sigma):
+@pytest.mark.parametrize("n,length,sigma,nu", [(128, 1.0, 1.0 / 128, 1.0), (256, 1.0, 0.37, 1.0),
+                                               (128, 3.0, 0.01, 0.7), (128, 1.0, 0.02, 0.7)])
+def test_zrb_variants_equal_plain_kernels(n, length, sigma, nu):
     """At 127^3 / 255^3 (several z chunks, ragged last tiles, a non-power-of-two
     dx^2) every ring layout of the sweep gives the plain one-colour kernels'
     V-cycle bit for bit."""
@@ -440,17 +440,23 @@ def test_zrb_variants_equal_plain_kernels(n, length, sigma):
     g = heat.Grid(3, n, length)
     u = dev(rng.standard_normal(g.shape))
     b = dev(rng.standard_normal(g.shape))
-    sop = mg.ShiftedOperator(heat.HeatOperator(g), sigma)
+    sop = mg.ShiftedOperator(heat.HeatOperator(g, nu), sigma)
     cfg = mg.MgConfig("jor-rb", 1.0, 1, 1)
     _capi.set_option(_capi.OPT_ZMARCH, 0)
     ref = mg.v_cycle(sop, u, b, cfg)
     ref_s = mg.smooth(sop, u, b, cfg, 2)
+    c9 = mg.MgConfig("jor-rb", 0.9, 1, 1)
+    ref_om = (mg.v_cycle(sop, u, b, c9), mg.smooth(sop, u, b, c9, 2))
     _capi.set_option(_capi.OPT_ZMARCH, 1)
     try:
         for ring in (0, 1, 4):
             _capi.set_option(_capi.OPT_ZRB_RING, ring)
-            assert torch.equal(mg.v_cycle(sop, u, b, cfg), ref), ring
-            assert torch.equal(mg.smooth(sop, u, b, cfg, 2), ref_s), ring
+            for om in (1.0, 0.9):
+                c = mg.MgConfig("jor-rb", om, 1, 1)
+                r1 = ref if om == 1.0 else ref_om[0]
+                r2 = ref_s if om == 1.0 else ref_om[1]
+                assert torch.equal(mg.v_cycle(sop, u, b, c), r1), (ring, om)
+                assert torch.equal(mg.smooth(sop, u, b, c, 2), r2), (ring, om)
     finally:
         _capi.set_option(_capi.OPT_ZRB_RING, 0)
 
