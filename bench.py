@@ -32,7 +32,13 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 WORKLOADS = {
-    # name: (dim, ns, nodes, smoother, omega, pre, post, cycles, P, dt, tol)
+    # BASELINE.json configs: grids, nodes, smoother, sweeps,
+    # V-cycles per sub-step (or a ToTolerance policy), time ranks, dt, PFASST tol
+    "cfg0": dict(dim=1, ns=(256, 128), nodes=(5, 3), smoother="jacobi", omega=2.0 / 3.0,
+                 pre=2, post=2, cycles=None, policy=("tol", 1e-12), p=4, dt=1.0 / 32,
+                 tol=1e-10, interp=4, u0="sine"),
+    "cfg1": dict(dim=1, ns=(256, 128), nodes=(5, 3), smoother="jacobi", omega=2.0 / 3.0,
+                 pre=2, post=2, cycles=1, p=4, dt=1.0 / 32, tol=1e-10, interp=4, u0="sine"),
     "cfg3": dict(dim=3, ns=(256, 128, 64), nodes=(9, 5, 3), smoother="jor-rb", omega=1.0,
                  pre=1, post=1, cycles=1, p=8, dt=1.0 / 64, tol=1e-10, interp=4),
     "cfg4": dict(dim=3, ns=(512, 256), nodes=(5, 3), smoother="jacobi", omega=2.0 / 3.0,
@@ -113,12 +119,68 @@ class ClockSampler:
 def build_levels(w):
     from paper_1407_6486_b200.heat import Grid, HeatOperator
     from paper_1407_6486_b200.hierarchy import Level
-    from paper_1407_6486_b200.multigrid import FixedCycles, MgConfig
+    from paper_1407_6486_b200.multigrid import FixedCycles, MgConfig, ToTolerance
     from paper_1407_6486_b200.quadrature import uniform_table
     cfg = MgConfig(w["smoother"], w["omega"], w["pre"], w["post"])
-    return [Level(HeatOperator(Grid(w["dim"], n)), uniform_table(k - 1), cfg,
-                  FixedCycles(w["cycles"]), space_interp_order=w["interp"])
+    pol = ToTolerance(w["policy"][1]) if w.get("policy") else FixedCycles(w["cycles"])
+    return [Level(HeatOperator(Grid(w["dim"], n)), uniform_table(k - 1), cfg, pol,
+                  space_interp_order=w["interp"])
             for n, k in zip(w["ns"], w["nodes"])]
+
+
+def initial_field(w):
+    """u0 of the workload: sin(pi x) for the 1-D configs, the
+    seeded Fourier-mode field otherwise."""
+    from paper_1407_6486_b200.heat import Grid, initial_condition, seeded_field
+    g = Grid(w["dim"], w["ns"][0])
+    return initial_condition(g, 1) if w.get("u0") == "sine" else seeded_field(g)
+
+
+def release_device_caches():
+    """Drop the multigrid plans and scratch of the previous workload."""
+    import gc
+
+    import torch
+    from paper_1407_6486_b200 import _device, multigrid
+    multigrid._plans.clear()
+    _device.release_scratch()
+    gc.collect()
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
+
+
+def measure_workload(name, steps=3, warmup=2):
+    """PFASST time-steps/s of another BASELINE configuration on this GPU
+    (device-resident u0, rank streams where they fit; CUDA events)."""
+    import torch
+    from paper_1407_6486_b200._device import to_device
+    from paper_1407_6486_b200.pfasst import pfasst_run
+    w = WORKLOADS[name]
+    levels = build_levels(w)
+    u0 = to_device(initial_field(w))[0]
+    p, dt = w["p"], w["dt"]
+    res = None
+    for _ in range(warmup):
+        res = pfasst_run(levels, u0, dt * p, p, tol=w["tol"], max_iter=20)
+    torch.cuda.synchronize()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record()
+    for _ in range(steps):
+        res = pfasst_run(levels, u0, dt * p, p, tol=w["tol"], max_iter=20)
+    t1.record()
+    torch.cuda.synchronize()
+    ms = t0.elapsed_time(t1) / steps
+    out = {"value": p / (ms / 1e3), "unit": "time-steps/s", "ms_per_step": ms, "steps": steps,
+           "warmup": warmup, "grids": [n - 1 for n in w["ns"]], "dim": w["dim"],
+           "nodes": list(w["nodes"]), "smoother": w["smoother"],
+           "policy": (f"ToTolerance({w['policy'][1]:g})" if w.get("policy")
+                      else f"FixedCycles({w['cycles']})"),
+           "time_ranks": p, "rank_iterations": res.rank_iterations[0],
+           "rank_vcycles": res.rank_vcycles[0]}
+    del levels, u0, res
+    release_device_caches()
+    return out
 
 
 def run_ours(args, w):
@@ -144,7 +206,7 @@ def run_ours(args, w):
     levels = build_levels(w)
     p, dt = w["p"], w["dt"]
     from paper_1407_6486_b200._device import to_device
-    u0_host = seeded_field(Grid(w["dim"], w["ns"][0]))
+    u0_host = initial_field(w)
     u0_dev = to_device(u0_host)[0]            # device field in the library layout
     u0_pinned = torch.from_numpy(u0_host).pin_memory()
 
@@ -301,6 +363,19 @@ def run_ours(args, w):
             "clocks": clk.summary(),
         }
         out["vcycle"] = vcycle_rate(w)
+    if world == 1 and not args.no_other_configs:
+        # the other BASELINE configurations, a few blocks each (not the headline)
+        release_device_caches()
+        others = {}
+        for name in ("cfg0", "cfg1", "cfg2", "cfg4"):
+            if name == args.workload:
+                continue
+            try:
+                others[name] = measure_workload(name)
+            except Exception as exc:           # report, never hide the headline
+                others[name] = {"error": repr(exc)[:200]}
+        if out is not None:
+            out["other_configs"] = others
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
@@ -403,11 +478,14 @@ class _CpuRank:
         from oracle import pintlab_oracle as O
         self.O, self.np, self.w = O, np, w
         self.dt = w["dt"]
+        pol = O.ToTol(w["policy"][1]) if w.get("policy") else O.Fixed(w["cycles"])
         self.lv = [O.Lvl(O.Op(w["dim"], n), O.uniform_table(k - 1),
-                         O.Mg(w["smoother"], w["omega"], w["pre"], w["post"]),
-                         O.Fixed(w["cycles"]), w["interp"])
+                         O.Mg(w["smoother"], w["omega"], w["pre"], w["post"]), pol,
+                         w["interp"])
                    for n, k in zip(w["ns"], w["nodes"])]
-        self.ts = O.Step.spread(self.lv, O.seeded_field(w["dim"], w["ns"][0]))
+        u0 = (O.sine_mode(w["dim"], w["ns"][0], 1) if w.get("u0") == "sine"
+              else O.seeded_field(w["dim"], w["ns"][0]))
+        self.ts = O.Step.spread(self.lv, u0)
         self.old = [s.copy() for s in self.ts.states]
         self.s = None
 
@@ -635,6 +713,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="cfg3", choices=sorted(WORKLOADS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-other-configs", action="store_true",
+                    help="skip the short runs of the other BASELINE configurations")
     ap.add_argument("--no-streams", action="store_true",
                     help="issue all time ranks on one stream (A/B of the wavefront overlap)")
     ap.add_argument("--opts", default="", help="pl_set_option pairs KEY=VAL,... (A/B only)")

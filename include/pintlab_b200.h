@@ -101,6 +101,10 @@ const char* pl_last_error(void);
 #define PL_OPT_ZC_FIT 22       /* 1 (default): z chunks of the jor-rb sweep and the cubic kernel
                                   chosen by a wave-quantisation model of the device's resident
                                   CTA slots; 0: power-of-two chunks aiming at PL_OPT_ZC_CTAS */
+#define PL_OPT_TOL_DEVICE 24   /* 1 (default): ToTolerance solves whose whole hierarchy fits the
+                                  one-CTA tail kernel (1-D, small grids) run their norm / cycle
+                                  loop on the device, one launch and one readback per solve;
+                                  0: host loop with a readback per V-cycle */
 int pl_set_option(int key, int value);
 
 /* storage elements of one field (incl. row pads) */

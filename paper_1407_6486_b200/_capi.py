@@ -143,6 +143,7 @@ OPT_RFW_THREADS = 18
 OPT_ZREV = 19
 OPT_FUSE_FAS_FW = 20
 OPT_ZC_FIT = 22
+OPT_TOL_DEVICE = 24
 
 
 _OPTION_VALUES = {}      # options set through this module (the library defaults otherwise)

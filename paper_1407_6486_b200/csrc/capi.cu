@@ -240,6 +240,7 @@ extern int g_rfw_enabled;
 extern int g_zc_floor;
 extern int g_zc_ctas;
 extern int g_zc_fit;
+extern int g_tol_device;
 extern int g_fast_tail;
 extern int g_mid_ctas;
 extern int g_zrb_ring;
@@ -282,6 +283,10 @@ static int set_option_impl(int key, int value) {
       return PL_ERR_ARG;
     }
     g_zc_ctas = value;
+    return 0;
+  }
+  if (key == PL_OPT_TOL_DEVICE) {
+    g_tol_device = value != 0;
     return 0;
   }
   if (key == PL_OPT_ZC_FIT) {

@@ -76,6 +76,18 @@ struct TailArgs {
   unsigned long long* trace;   // PL_MID_TRACE: [0] count, then %globaltimer per tail phase
 };
 
+// ToTolerance loop run inside the tail kernel (multigrid.py:270-288) when the
+// whole hierarchy fits one CTA: norms are block reductions, the loop control
+// is on the device, and the outcome goes to out[0] = residual, out[1] =
+// 4 * cycles + (status + 1) with status -1 for the cycle cap.  u is written
+// back only when the solve succeeds (the reference solves on a copy).
+struct TolArgs {
+  int on;
+  double tol, stall;
+  int max_cycles;
+  double* out;
+};
+
 // diagnostics only (PL_MID_TRACE): thread 0 stamps the end of a tail phase
 __device__ __forceinline__ void ft_stamp(const TailArgs& a) {
   if (a.trace && threadIdx.x == 0) {
@@ -429,10 +441,87 @@ __device__ void ft_level(const TailArgs& a, double* sm, bool zero, bool fused = 
   }
 }
 
+// one V-cycle of the tail levels on the shared-memory state (level 0 u, b)
+template <int DIM>
+__device__ void tail_vcycle(const TailArgs& a, double* sm, bool zero0) {
+  int l = 0;
+  // ---- down: pre-smooth, residual, full weighting
+  for (; !a.lv[l].coarsest; ++l) {
+    const TailLevel& L = a.lv[l];
+    const TailLevel& C = a.lv[l + 1];
+    tail_smooth<DIM>(a, L, sm, a.pre, l == 0 ? zero0 : true);
+    double* u = sm + L.off_u;
+    double* b = sm + L.off_b;
+    double* t = sm + L.off_t;
+    PL_FOR_SM_POINTS(L.g) {
+      int x, y, z;
+      decode(L.g, p, x, y, z);
+      t[p] = b[p] - shifted_point<DIM>(u, L.g, L.c, a.sigma, x, y, z, p);
+    }
+    __syncthreads();
+    double* bc = sm + C.off_b;
+    PL_FOR_SM_POINTS(C.g) {
+      int x, y, z;
+      decode(C.g, p, x, y, z);
+      bc[p] = fw_point<DIM>(t, L.g, x, y, z);
+    }
+    __syncthreads();
+  }
+  // ---- coarsest: dense LU (ignores the initial guess, multigrid.py:240-243)
+  tail_lu(a, a.lu_off >= 0 ? sm + a.lu_off : a.lu, sm + a.lv[l].off_b, sm + a.lv[l].off_u);
+  // ---- up: prolongate, correct, post-smooth
+  for (--l; l >= 0; --l) {
+    const TailLevel& L = a.lv[l];
+    const TailLevel& C = a.lv[l + 1];
+    double* u = sm + L.off_u;
+    const double* ec = sm + C.off_u;
+    PL_FOR_SM_POINTS(L.g) {
+      int x, y, z;
+      decode(L.g, p, x, y, z);
+      u[p] = u[p] + lin_point<DIM>(ec, C.g, x, y, z);
+    }
+    __syncthreads();
+    tail_smooth<DIM>(a, L, sm, a.post, false);
+  }
+}
+
+// sum of squares over level 0 of b (u == nullptr) or of b - A_sigma u, in a
+// fixed order (per-thread strided sums, warp shuffles, then warp 0)
+template <int DIM>
+__device__ double tail_sumsq(const TailArgs& a, const double* sm, bool resid) {
+  __shared__ double part[TAIL_THREADS / 32];
+  const TailLevel& L = a.lv[0];
+  const double* u = sm + L.off_u;
+  const double* b = sm + L.off_b;
+  double acc = 0.0;
+  PL_FOR_SM_POINTS(L.g) {
+    double v = b[p];
+    if (resid) {
+      int x, y, z;
+      decode(L.g, p, x, y, z);
+      v = v - shifted_point<DIM>(u, L.g, L.c, a.sigma, x, y, z, p);
+    }
+    acc = acc + v * v;
+  }
+  for (int o = 16; o > 0; o >>= 1) acc = acc + __shfl_down_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  double tot = 0.0;
+  if (threadIdx.x < 32) {
+    double v = threadIdx.x < blockDim.x / 32 ? part[threadIdx.x] : 0.0;
+    for (int o = 16; o > 0; o >>= 1) v = v + __shfl_down_sync(0xffffffffu, v, o);
+    if (threadIdx.x == 0) part[0] = v;
+  }
+  __syncthreads();
+  tot = part[0];
+  __syncthreads();
+  return tot;
+}
+
 // the whole V-cycle of the tail levels by one CTA in shared memory
 template <int DIM>
 __device__ void tail_run(const TailArgs& a, const double* __restrict__ b_in, double* u_io,
-                         int zero_guess, int ncycles, double* sm) {
+                         int zero_guess, int ncycles, double* sm, const TolArgs& tol) {
   const TailLevel& L0 = a.lv[0];
   if (DIM == 3 && a.fast) {
     ft_stamp(a);
@@ -473,47 +562,40 @@ __device__ void tail_run(const TailArgs& a, const double* __restrict__ b_in, dou
     if (!zero_guess) sm[L0.off_u + p] = u_io[gi];
   }
   __syncthreads();
-  for (int cyc = 0; cyc < ncycles; ++cyc) {
-    bool zero0 = zero_guess && cyc == 0;
-    int l = 0;
-    // ---- down: pre-smooth, residual, full weighting
-    for (; !a.lv[l].coarsest; ++l) {
-      const TailLevel& L = a.lv[l];
-      const TailLevel& C = a.lv[l + 1];
-      tail_smooth<DIM>(a, L, sm, a.pre, l == 0 ? zero0 : true);
-      double* u = sm + L.off_u;
-      double* b = sm + L.off_b;
-      double* t = sm + L.off_t;
-      PL_FOR_SM_POINTS(L.g) {
-        int x, y, z;
-        decode(L.g, p, x, y, z);
-        t[p] = b[p] - shifted_point<DIM>(u, L.g, L.c, a.sigma, x, y, z, p);
-      }
+  if (tol.on) {
+    // ToTolerance (multigrid.py:270-288), entirely on the device
+    const double bn = sqrt(tail_sumsq<DIM>(a, sm, false));
+    int c = 0, st = 1;
+    double res = 0.0;
+    if (bn == 0.0) {
+      PL_FOR_SM_POINTS(L0.g) sm[L0.off_u + p] = 0.0;
       __syncthreads();
-      double* bc = sm + C.off_b;
-      PL_FOR_SM_POINTS(C.g) {
-        int x, y, z;
-        decode(C.g, p, x, y, z);
-        bc[p] = fw_point<DIM>(t, L.g, x, y, z);
+    } else {
+      res = sqrt(tail_sumsq<DIM>(a, sm, true));
+      while (res > tol.tol * bn) {
+        if (c >= tol.max_cycles) {
+          st = -1;
+          break;
+        }
+        tail_vcycle<DIM>(a, sm, false);
+        ++c;
+        const double nres = sqrt(tail_sumsq<DIM>(a, sm, true));
+        if (nres > tol.tol * bn && nres >= tol.stall * res) {
+          st = 2;
+          res = nres;
+          break;
+        }
+        res = nres;
       }
-      __syncthreads();
     }
-    // ---- coarsest: dense LU (ignores the initial guess, multigrid.py:240-243)
-    tail_lu(a, a.lu_off >= 0 ? sm + a.lu_off : a.lu, sm + a.lv[l].off_b, sm + a.lv[l].off_u);
-    // ---- up: prolongate, correct, post-smooth
-    for (--l; l >= 0; --l) {
-      const TailLevel& L = a.lv[l];
-      const TailLevel& C = a.lv[l + 1];
-      double* u = sm + L.off_u;
-      const double* ec = sm + C.off_u;
-      PL_FOR_SM_POINTS(L.g) {
-        int x, y, z;
-        decode(L.g, p, x, y, z);
-        u[p] = u[p] + lin_point<DIM>(ec, C.g, x, y, z);
-      }
-      __syncthreads();
-      tail_smooth<DIM>(a, L, sm, a.post, false);
+    if (threadIdx.x == 0) {
+      tol.out[0] = res;
+      tol.out[1] = 4.0 * c + (st + 1);
+      tol.out[2] = bn;
     }
+    if (st == -1) return;          // the failed solve leaves u untouched
+  } else {
+    for (int cyc = 0; cyc < ncycles; ++cyc) tail_vcycle<DIM>(a, sm, zero_guess && cyc == 0);
   }
   PL_FOR_SM_POINTS(L0.g) {
     int x, y, z;
@@ -526,9 +608,9 @@ template <int DIM>
 __global__ void __launch_bounds__(TAIL_THREADS) k_tail(TailArgs a,
                                                        const double* __restrict__ b_in,
                                                        double* u_io, int zero_guess,
-                                                       int ncycles) {
+                                                       int ncycles, TolArgs tol) {
   extern __shared__ double sm[];
-  tail_run<DIM>(a, b_in, u_io, zero_guess, ncycles, sm);
+  tail_run<DIM>(a, b_in, u_io, zero_guess, ncycles, sm, tol);
 }
 
 // ---------------------------------------------------------------------------
@@ -668,7 +750,7 @@ __global__ void __launch_bounds__(MID_THREADS) k_mid(MidArgs m, TailArgs ta) {
     }
     MID_SYNC();
   }
-  if (blockIdx.x == 0) tail_run<DIM>(ta, m.lv[m.nmid].b, m.lv[m.nmid].u, 1, 1, sm);
+  if (blockIdx.x == 0) tail_run<DIM>(ta, m.lv[m.nmid].b, m.lv[m.nmid].u, 1, 1, sm, TolArgs{});
   MID_SYNC();
   for (int l = m.nmid - 1; l >= 0; --l) {
     const MidLevel& L = m.lv[l];
@@ -743,11 +825,13 @@ static int tail_args(MgPlan* P, int l0, double sigma, TailArgs& a, size_t* smem_
 }
 
 static int launch_tail(MgPlan* P, int l0, double* u, const double* b, double sigma,
-                       int zero_guess, int ncycles, cudaStream_t s) {
+                       int zero_guess, int ncycles, cudaStream_t s,
+                       const TolArgs& tol = TolArgs{}) {
   TailArgs a;
   size_t smem = 0;
   PL_TRY(tail_args(P, l0, sigma, a, &smem));
-  void (*kern)(TailArgs, const double*, double*, int, int) =
+  if (tol.on) a.fast = 0;    // the device ToTolerance loop runs the generic levels
+  void (*kern)(TailArgs, const double*, double*, int, int, TolArgs) =
       P->dim == 1 ? k_tail<1> : (P->dim == 2 ? k_tail<2> : k_tail<3>);
   static bool attr_set[4] = {false, false, false, false};
   if (!attr_set[P->dim]) {
@@ -756,7 +840,7 @@ static int launch_tail(MgPlan* P, int l0, double* u, const double* b, double sig
     attr_set[P->dim] = true;
   }
   PL_PRE(K_TAIL);
-  kern<<<1, TAIL_THREADS, smem, s>>>(a, b, u, zero_guess, ncycles);
+  kern<<<1, TAIL_THREADS, smem, s>>>(a, b, u, zero_guess, ncycles, tol);
   double bytes = 8.0 * P->lv[l0].g.npts * (zero_guess ? 2 : 3);
   PL_CHECK_LAUNCH(K_TAIL, bytes);
   return 0;
@@ -948,13 +1032,13 @@ int mg_plan_create(MgPlan** out, int dim, int n, double length, double nu, int o
   P->tail_smem = acc;
   // norms
   P->npartials = sumsq_partials(P->lv[0].g);
-  cudaError_t e = cudaMalloc(&P->partials, sizeof(double) * (P->npartials + 2));
+  cudaError_t e = cudaMalloc(&P->partials, sizeof(double) * (P->npartials + 4));
   if (e != cudaSuccess) {
     delete P;
     return cuda_status(e, "cudaMalloc partials");
   }
   P->norm_dev = P->partials + P->npartials;
-  e = cudaMallocHost(&P->norm_host, 2 * sizeof(double));
+  e = cudaMallocHost(&P->norm_host, 4 * sizeof(double));
   if (e != cudaSuccess) {
     cudaFree(P->partials);
     delete P;
@@ -1237,10 +1321,34 @@ static int norm2(MgPlan* P, const double* u, const double* b, double sigma, doub
   return 0;
 }
 
+int g_tol_device = 1;   // PL_OPT_TOL_DEVICE
+
 int mg_solve_tol(MgPlan* P, double* u, const double* b, double sigma, double tol, double stall,
                  int max_cycles, int* cycles, int* status, double* residual, cudaStream_t s) {
   PL_TRY(mg_prepare(P, sigma, s));
   MgLevel& L = P->lv[0];
+  if (g_tol_device && P->tail_start == 0) {
+    // the whole solve in one single-CTA launch, one readback
+    TolArgs ta{1, tol, stall, max_cycles, P->norm_dev};
+    PL_TRY(launch_tail(P, 0, u, b, sigma, 0, 0, s, ta));
+    cudaError_t e = cudaMemcpyAsync(P->norm_host, P->norm_dev, 3 * sizeof(double),
+                                    cudaMemcpyDeviceToHost, s);
+    if (e != cudaSuccess) return cuda_status(e, "tolerance readback");
+    e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) return cuda_status(e, "sync");
+    const long long code = (long long)P->norm_host[1];
+    const int st = (int)(code & 3) - 1;
+    *cycles = (int)(code >> 2);
+    *residual = P->norm_host[0];
+    if (st < 0) {
+      *status = -1;
+      set_error("no convergence after %d V-cycles (relative residual %.3e)", *cycles,
+                *residual / P->norm_host[2]);
+      return 1;
+    }
+    *status = st == 2 ? ST_STALLED : ST_CONVERGED;
+    return 0;
+  }
   double bnorm;
   PL_TRY(norm2(P, nullptr, b, sigma, &bnorm, s));
   *cycles = 0;
