@@ -382,7 +382,7 @@ def run_ours(args, w):
     return out
 
 
-NCU_KERNEL = {"jor_rb": "k_zrb3", "interp_cubic": "k_cubic4", "restrict": "k_rfw",
+NCU_KERNEL = {"jor_rb": "k_zrb3", "interp_cubic": "k_cubic5", "restrict": "k_rfw",
               "mg_mid": "k_mid"}
 
 

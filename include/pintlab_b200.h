@@ -170,7 +170,8 @@ int pl_mg_solve_tol(pl_mg_plan* plan, double* u, const double* b, double sigma, 
    matrix) by fast diagonalisation: install T = V diag(lam) V^-1 of the plan's
    1-D stencil matrix (host arrays, row-major (n-1) x (n-1): W = V^-1, W^T, V,
    V^T, then lam), computed by the caller with numpy eigh/eig; then
-   u = (I - sigma nu Lap_h)^-1 b with dense cuBLAS GEMMs along each axis.
+   u = (I - sigma nu Lap_h)^-1 b with dense fp64 products along each axis
+   (a tiled GEMM kernel of this library).
    Agrees with SuperLU to rounding (tolerance, not bitwise). */
 int pl_mg_set_direct(pl_mg_plan* plan, const double* w, const double* wt, const double* v,
                      const double* vt, const double* lam, void* stream);

@@ -5,13 +5,11 @@
 // is a Kronecker sum of one 1-D stencil matrix T (the same on every axis):
 // with T = V diag(lam) V^-1,
 //   u = (V x V x V) diag(1 / (1 - sigma nu (lam_i + lam_j + lam_k))) (W x W x W) b,
-// W = V^-1, i.e. three batched dense GEMMs with an N x N matrix per
-// direction (cuBLAS dgemm -- plain library GEMMs) and one point-wise scale.
+// W = V^-1, i.e. one dense N x N product per direction and way (k_dgemm_rm,
+// a tiled fp64 GEMM written here) and one point-wise scale.
 // V, W and lam come from the host (numpy eigh / eig + inv, like the
 // reference's own host factorisations); the solve is on the GPU.  Results
 // agree with SuperLU to rounding (not bitwise): tolerance-tested.
-#include <cublas_v2.h>
-
 #include <cstring>
 
 #include "common.cuh"
@@ -35,25 +33,78 @@ __global__ void k_direct_scale(double* w, Geo g, const double* __restrict__ lam,
   w[p] = w[p] / (1.0 - sigma * (nu * s));
 }
 
-// row-major C (m x n) = A (m x k) * B (k x n), batched with element strides
-int gemm_rm(cublasHandle_t h, int m, int n, int k, const double* A, long long lda, long long sa,
+// row-major C (m x n) = A (m x k) * B (k x n), batched with element strides.
+// 64 x 64 output tile per CTA, 256 threads with 4 x 4 outputs each, k in
+// steps of 16 through shared memory; every output is one FMA chain over k in
+// increasing order (deterministic).  Out-of-range rows / columns / k load
+// zeros and store nothing.
+constexpr int GBM = 64, GBN = 64, GBK = 16;
+
+__global__ void __launch_bounds__(256) k_dgemm_rm(int m, int n, int k, const double* __restrict__ A,
+                                                  long long lda, long long sa,
+                                                  const double* __restrict__ B, long long ldb,
+                                                  long long sb, double* __restrict__ C,
+                                                  long long ldc, long long sc) {
+  __shared__ double As[GBK][GBM + 2];   // As[kk][i] = A[i0 + i][k0 + kk]
+  __shared__ double Bs[GBK][GBN + 2];   // Bs[kk][j] = B[k0 + kk][j0 + j]
+  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+  const int i0 = blockIdx.y * GBM, j0 = blockIdx.x * GBN;
+  A += (long long)blockIdx.z * sa;
+  B += (long long)blockIdx.z * sb;
+  C += (long long)blockIdx.z * sc;
+  double acc[4][4] = {};
+  for (int k0 = 0; k0 < k; k0 += GBK) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {            // A tile: 64 rows x 16 k
+      const int e = tid + q * 256, i = e >> 4, kk = e & 15;
+      const int gi = i0 + i, gk = k0 + kk;
+      As[kk][i] = gi < m && gk < k ? A[(long long)gi * lda + gk] : 0.0;
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {            // B tile: 16 k x 64 columns
+      const int e = tid + q * 256, kk = e >> 6, j = e & 63;
+      const int gk = k0 + kk, gj = j0 + j;
+      Bs[kk][j] = gk < k && gj < n ? B[(long long)gk * ldb + gj] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < GBK; ++kk) {
+      double a[4], b[4];
+#pragma unroll
+      for (int r = 0; r < 4; ++r) a[r] = As[kk][ty * 4 + r];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) b[c] = Bs[kk][tx + 16 * c];
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) acc[r][c] = __fma_rn(a[r], b[c], acc[r][c]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    const int gi = i0 + ty * 4 + r;
+    if (gi >= m) continue;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const int gj = j0 + tx + 16 * c;
+      if (gj < n) C[(long long)gi * ldc + gj] = acc[r][c];
+    }
+  }
+}
+
+int gemm_rm(cudaStream_t s, int m, int n, int k, const double* A, long long lda, long long sa,
             const double* B, long long ldb, long long sb, double* C, long long ldc, long long sc,
             int batch) {
-  const double one = 1.0, zero = 0.0;
-  cublasStatus_t st = cublasDgemmStridedBatched(h, CUBLAS_OP_N, CUBLAS_OP_N, n, m, k, &one, B,
-                                                (int)ldb, sb, A, (int)lda, sa, &zero, C,
-                                                (int)ldc, sc, batch);
-  if (st != CUBLAS_STATUS_SUCCESS) {
-    set_error("cublasDgemmStridedBatched failed (%d)", (int)st);
-    return 2;
-  }
-  return 0;
+  dim3 grid(ceil_div(n, GBN), ceil_div(m, GBM), batch);
+  k_dgemm_rm<<<grid, 256, 0, s>>>(m, n, k, A, lda, sa, B, ldb, sb, C, ldc, sc);
+  return cuda_status(cudaGetLastError(), "direct transform");
 }
 
 // out = M applied along axis `ax` (0 = slowest) of in; M row-major N x N,
 // MT its transpose (row-major).  Pads of `out` are written only by the
 // slowest-axis product, from the zero pads of `in`.
-int apply_axis(cublasHandle_t h, const Geo& g, int ax, const double* M, const double* MT,
+int apply_axis(cudaStream_t h, const Geo& g, int ax, const double* M, const double* MT,
                const double* in, double* out) {
   const int N = g.N;
   const int fast = g.dim - 1;
@@ -84,12 +135,6 @@ int mg_set_direct(MgPlan* P, const double* w, const double* wt, const double* v,
     // pads of the scratch fields must read as zeros (apply_axis)
     e = cudaMemsetAsync(P->dir_work, 0, sizeof(double) * 2 * (size_t)L.g.nstore, s);
     if (e != cudaSuccess) return cuda_status(e, "memset direct scratch");
-    cublasHandle_t h = nullptr;
-    if (cublasCreate(&h) != CUBLAS_STATUS_SUCCESS) {
-      set_error("cublasCreate failed");
-      return 2;
-    }
-    P->cublas = h;
   }
   const double* src[5] = {w, wt, v, vt, lam};
   const size_t cnt[5] = {N * N, N * N, N * N, N * N, N};
@@ -122,8 +167,7 @@ int mg_direct(MgPlan* P, double* u, const double* b, double sigma, cudaStream_t 
   const double* lam = VT + N * N;
   double* t0 = P->dir_work;
   double* t1 = P->dir_work + g.nstore;
-  cublasHandle_t h = (cublasHandle_t)P->cublas;
-  cublasSetStream(h, s);
+  cudaStream_t h = s;
   PL_PRE(K_DIRECT);
   // forward transform W along every axis (fastest first), scale, V back
   const double* in = b;
@@ -151,10 +195,8 @@ int mg_direct(MgPlan* P, double* u, const double* b, double sigma, cudaStream_t 
 }
 
 void mg_direct_destroy(MgPlan* P) {
-  if (P->cublas) cublasDestroy((cublasHandle_t)P->cublas);
   cudaFree(P->dir_mats);
   cudaFree(P->dir_work);
-  P->cublas = nullptr;
   P->dir_mats = P->dir_work = nullptr;
 }
 

@@ -43,10 +43,9 @@ struct MgPlan {
   char* ws = nullptr;
   size_t ws_bytes = 0;
   // Direct policy (direct.cu): W, W^T, V, V^T, lam on the device, two scratch
-  // fields, a cuBLAS handle
+  // fields
   double* dir_mats = nullptr;
   double* dir_work = nullptr;
-  void* cublas = nullptr;
   int dir_ready = 0;
 };
 

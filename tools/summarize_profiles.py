@@ -26,7 +26,7 @@ def launch_list(dst):
     tot = sum(v[1] for v in agg.values())
     with open(dst, "w") as fh:
         fh.write(f"# ncu --metrics gpu__time_duration.sum --clock-control none -s 30000 -c 4000\n"
-                 f"# python bench.py --steps 1 --warmup 3 --no-cpu-baseline  ({len(rows)} launches, "
+                 f"# python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-other-configs (rank streams; {len(rows)} launches, "
                  f"{tot:.1f} us, cold-cache serialised: compare SHARES)\n")
         fh.write(f"{'share':>7s} {'us':>10s} {'n':>5s}  kernel\n")
         for k, (n, us) in sorted(agg.items(), key=lambda kv: -kv[1][1]):
@@ -77,7 +77,7 @@ def main():
     if os.path.exists(os.path.join(OUT, "launches.csv")):
         launch_list(os.path.join(dst, "launch_list_summary.txt"))
     caps = {"top255_full.ncu-rep": "top kernels at 255^3 (k_zrb3 one-barrier red-black sweep, "
-                                   "k_rfw residual+restriction, k_cubic4 cubic correction, "
+                                   "k_rfw residual+restriction, k_cubic5 cubic correction, "
                                    "k_mid cooperative small levels)",
             "zrb255_full.ncu-rep": "dominant kernel: fused red-black sweep (TMA), 255^3 "
                                    "(first launch: with fused prolongation? see kernel name)",
