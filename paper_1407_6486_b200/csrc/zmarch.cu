@@ -642,18 +642,19 @@ __device__ __forceinline__ double rb_relax(const RbCtx& k, double zm, double zp,
 struct Relax {
   double cc, a, q;
 };
-template <bool POW2>
+// UNIT: nu = omega = 1, whose multiplications are exact and skipped
+template <bool POW2, bool UNIT = false>
 __device__ __forceinline__ Relax rb_fast(const RbCtx& k, double zm, double zp, double ym,
                                          double yp, double xm, double xp, double cc, double bv) {
   double acc = 0.0;
   acc = acc + dd2<POW2>((zm - 2.0 * cc) + zp, k.c);
   acc = acc + dd2<POW2>((ym - 2.0 * cc) + yp, k.c);
   acc = acc + dd2<POW2>((xm - 2.0 * cc) + xp, k.c);
-  const double lp = k.c.nu * acc;
+  const double lp = UNIT ? acc : k.c.nu * acc;
   const double r = bv - (cc - k.sigma * lp);
   Relax o;
   o.cc = cc;
-  o.a = k.omega * r;
+  o.a = UNIT ? r : k.omega * r;
   double q = o.a * k.dinv;
   double e = __fma_rn(-k.dval, q, o.a);
   q = __fma_rn(e, k.dinv, q);
@@ -667,13 +668,13 @@ __device__ __forceinline__ bool quot_ok(double a) {
   const unsigned e = ((unsigned)__double2hiint(a) >> 20) & 0x7ffu;
   return e - 63u <= 1919u;
 }
-template <bool POW2, int O>
+template <bool POW2, int O, bool UNIT = false>
 __device__ __forceinline__ Relax rb_point_fast(const RbCtx& k, const double* pl,
                                                const double2& um, const double2& uc,
                                                const double2& up, const double2& bq) {
   const double xm = O ? uc.x : pl[k.iu - 1];
   const double xp = O ? pl[k.iu + 2] : uc.y;
-  return rb_fast<POW2>(k, mem<O>(um), mem<O>(up), pl[k.iu - UX + O], pl[k.iu + UX + O], xm, xp,
+  return rb_fast<POW2, UNIT>(k, mem<O>(um), mem<O>(up), pl[k.iu - UX + O], pl[k.iu + UX + O], xm, xp,
                        mem<O>(uc), mem<O>(bq));
 }
 
@@ -706,15 +707,15 @@ __device__ __forceinline__ void rb_halo(const RbCtx& k, int q) {
 // of this warp's rows: red member 1 - PAR, black member PAR.  Both updates
 // are evaluated branch-free (independent chains the scheduler interleaves);
 // one warp-wide test sends out-of-range quotients to the IEEE division.
-template <bool POW2, int RU, int RB, int PAR>
+template <bool POW2, int RU, int RB, int PAR, bool UNIT>
 __device__ __forceinline__ void rb_phase(const RbCtx& k, int z, const double2& U0, double2& U1,
                                          const double2& U2, double2& U3, const double2& U4,
                                          const double2& B0, const double2& B2, double* dst) {
   const int q = z + 2;
   double* plr = rb_u<RU>(k, q);
   const double* plb = rb_u<RU>(k, z);
-  Relax rr = rb_point_fast<POW2, 1 - PAR>(k, plr, U2, U3, U4, B2);
-  Relax rbk = rb_point_fast<POW2, PAR>(k, plb, U0, U1, U2, B0);
+  Relax rr = rb_point_fast<POW2, 1 - PAR, UNIT>(k, plr, U2, U3, U4, B2);
+  Relax rbk = rb_point_fast<POW2, PAR, UNIT>(k, plb, U0, U1, U2, B0);
   if (__builtin_expect(!(quot_ok(rr.a) && quot_ok(rbk.a)), 0)) {
     if (!quot_ok(rr.a)) rr.q = div_slow(rr.a, k.dval);
     if (!quot_ok(rbk.a)) rbk.q = div_slow(rbk.a, k.dval);
@@ -729,7 +730,7 @@ __device__ __forceinline__ void rb_phase(const RbCtx& k, int z, const double2& U
   else if (k.va) dst[0] = w.x;
 }
 
-template <bool POW2, int RU, int RB, int MINB>
+template <bool POW2, int RU, int RB, int MINB, bool UNIT>
 __global__ void __launch_bounds__(NTHR_RB2, MINB) k_zrb3(const __grid_constant__ CUtensorMap mu,
                                                       const __grid_constant__ CUtensorMap mb,
                                                       double* __restrict__ out, Geo g, OpC c,
@@ -883,7 +884,7 @@ __global__ void __launch_bounds__(NTHR_RB2, MINB) k_zrb3(const __grid_constant__
       }
       double2 U4 = lds2(rb_u<RU>(k, z + 3) + k.iu);   // stale beyond R: unused
       const double2 B2 = lds2(rb_b<RB>(k, z + 2) + k.ib);
-      rb_phase<POW2, RU, RB, PA>(k, z, U0, U1, U2, U3, U4, B0, B2, dst);
+      rb_phase<POW2, RU, RB, PA, UNIT>(k, z, U0, U1, U2, U3, U4, B0, B2, dst);
       if (is_halo) rb_halo<POW2, RU, RB, 0>(k, z + 2);
       __syncthreads();
       if (tid == issuer) {
@@ -898,7 +899,7 @@ __global__ void __launch_bounds__(NTHR_RB2, MINB) k_zrb3(const __grid_constant__
       }
       double2 U5 = lds2(rb_u<RU>(k, z + 4) + k.iu);
       const double2 B3 = lds2(rb_b<RB>(k, z + 3) + k.ib);
-      rb_phase<POW2, RU, RB, PB>(k, z + 1, U1, U2, U3, U4, U5, B1, B3, dst + k.sz);
+      rb_phase<POW2, RU, RB, PB, UNIT>(k, z + 1, U1, U2, U3, U4, U5, B1, B3, dst + k.sz);
       if (is_halo) rb_halo<POW2, RU, RB, 1>(k, z + 3);
       __syncthreads();
       if (tid == issuer) {
@@ -1639,6 +1640,7 @@ int launch_zrb3(const double* u, const double* b, double* out, const Geo& g, con
   int zc = pick_zc(g);
   dim3 grid(ceil_div(g.nx, TX), ceil_div(g.ny, TY), ceil_div(g.nz, zc));
   const double dinv = 1.0 / dval;
+  const bool unit = c.nu == 1.0 && omega == 1.0;   // exact multiplications skipped
   // default (0): 6 u + 3 b planes from 255^3 up, in z chunks of >= 32 planes
   // (1,024 CTAs at 255^3, 1.7 waves of 4 per SM: 91 vs 97 us); the 8 + 4
   // rings at 3 CTAs per SM below, where they are faster (26 vs 27 us at 127^3)
@@ -1646,7 +1648,8 @@ int launch_zrb3(const double* u, const double* b, double* out, const Geo& g, con
   if (big) zc = zc < 32 ? 32 : zc;
   if (g_zrb_ring == 1 || big) {   // 6 u + 3 b planes, 4 CTAs per SM (register cap 64)
     size_t smem = ((size_t)6 * PU + (size_t)3 * PB) * 8 + 8 * (6 + 3);
-    auto kern = c.pow2 ? k_zrb3<true, 6, 3, 4> : k_zrb3<false, 6, 3, 4>;
+    auto kern = c.pow2 ? (unit ? k_zrb3<true, 6, 3, 4, true> : k_zrb3<true, 6, 3, 4, false>)
+                       : (unit ? k_zrb3<false, 6, 3, 4, true> : k_zrb3<false, 6, 3, 4, false>);
     raise_smem(kern, smem);
     // even chunks (the phase code assumes an even z0)
     if (g_zc_fit) zc = pick_zc_fit(g, resident_ctas(kern, NTHR_RB2, smem), 2, 5, 16, 64);
@@ -1655,7 +1658,8 @@ int launch_zrb3(const double* u, const double* b, double* out, const Geo& g, con
     return 0;
   }
   size_t smem = ((size_t)8 * PU + (size_t)4 * PB) * 8 + 8 * (8 + 4);
-  auto kern = c.pow2 ? k_zrb3<true, 8, 4, 3> : k_zrb3<false, 8, 4, 3>;
+  auto kern = c.pow2 ? (unit ? k_zrb3<true, 8, 4, 3, true> : k_zrb3<true, 8, 4, 3, false>)
+                     : (unit ? k_zrb3<false, 8, 4, 3, true> : k_zrb3<false, 8, 4, 3, false>);
   raise_smem(kern, smem);
   kern<<<grid, dim3(NTHR_RB2), smem, s>>>(mu, mb, out, g, c, sigma, omega, dval, dinv, zc);
   return 0;
