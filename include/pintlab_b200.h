@@ -65,8 +65,8 @@ int pl_abi_version(void);
 const char* pl_last_error(void);
 
 /* runtime options (A/B testing of kernel variants; results are bit-identical).
-   Keys 3, 5, 12, 15, 16 and 21 belonged to removed dead-end variants and
-   are rejected. */
+   Keys 3, 5, 12, 15, 16, 18 and 21 belonged to removed variants and are
+   rejected. */
 #define PL_OPT_ZMARCH 0       /* 1 (default): TMA z-marching + fused sweeps, 3-D order 2 */
 #define PL_OPT_ZMARCH_MIN_N 1 /* smallest n-1 using them (default 127, >= 31) */
 #define PL_OPT_GRAPHS 2       /* 1 (default): FixedCycles sweeps replay as CUDA graphs */
@@ -89,8 +89,6 @@ const char* pl_last_error(void);
 #define PL_OPT_FUSE_APPLY_RHS 17 /* 1 (default): the sweep's f refresh of node m and the next
                                     sub-step's right-hand side share one pass over y[m] (TMA
                                     levels); 0: separate apply and rhs launches; bit-identical */
-#define PL_OPT_RFW_THREADS 18  /* threads of the residual + full-weighting kernel: 288 (default;
-                                  at most two residual points per thread) or 256 */
 #define PL_OPT_ZREV 19        /* bit mask of TMA kernels that visit their z chunks top-down, so
                                  they start on the planes the previous kernel left in L2:
                                  1 apply (+ rhs), 2 residual + full weighting (default 3) */

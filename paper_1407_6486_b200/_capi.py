@@ -139,7 +139,6 @@ OPT_ZC_CTAS = 11
 OPT_MID_CTAS = 13
 OPT_ZRB_RING = 14
 OPT_FUSE_APPLY_RHS = 17
-OPT_RFW_THREADS = 18
 OPT_ZREV = 19
 OPT_FUSE_FAS_FW = 20
 OPT_ZC_FIT = 22

@@ -244,7 +244,6 @@ extern int g_tol_device;
 extern int g_fast_tail;
 extern int g_mid_ctas;
 extern int g_zrb_ring;
-extern int g_rfw_threads;
 extern int g_zrev_mask;
 }
 
@@ -343,14 +342,6 @@ static int set_option_impl(int key, int value) {
   }
   if (key == PL_OPT_ZREV) {
     g_zrev_mask = value;
-    return 0;
-  }
-  if (key == PL_OPT_RFW_THREADS) {
-    if (value != 256 && value != 288) {
-      set_error("k_rfw threads must be 256 or 288");
-      return PL_ERR_ARG;
-    }
-    g_rfw_threads = value;
     return 0;
   }
   if (key == PL_OPT_FUSE_APPLY_RHS) {

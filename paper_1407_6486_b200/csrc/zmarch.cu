@@ -924,29 +924,35 @@ __global__ void __launch_bounds__(NTHR_RB2, MINB) k_zrb3(const __grid_constant__
 constexpr int QW = TX / 2 + 4, QH = TY / 2 + 4, PQ = align16(QW * QH);   // coarse window
 
 // k_rfw: coarse b = FW(b - (I - sigma A) u) in one pass (multigrid.py:245-246;
-// transfers.py:27-34).  A CTA owns a 16 x 8 coarse tile; each thread owns up
-// to three fine (x, y) points of the 33 x 17 residual window (fine x0..x0+32,
-// y0..y0+16).  Marching up the fine planes it evaluates its residuals from
-// TMA-staged u (halo 1) and b windows and folds them into the z weights in
-// registers in fw3's operation order (0.25 * ((a + 2 b) + c): a at plane 2jz,
-// t = a + 2 b at 2jz+1, 0.25 * (t + c) at 2jz+2, which is also the next
-// coarse plane's a).  The z-weighted plane goes to shared memory; the y pass
-// runs in the next phase and the x pass in the one after -- one barrier per
-// fine plane, and the fine residual is never stored.  Residual arithmetic is
-// k_z1<Z_RESID>'s and the weights fw_point's: the coarse right-hand side is
-// bit-identical to residual + full_weighting.
+// transfers.py:27-34).  A CTA owns a 16 x 8 coarse tile and marches up the
+// fine planes of its z chunk; each fine residual of the 33 x 17 window (fine
+// x0..x0+32, y0..y0+16) is evaluated from TMA-staged u (halo 1) and b windows
+// and folded into the z weights in registers in fw3's operation order
+// (0.25 * ((a + 2 b) + c): a at plane 2jz, t = a + 2 b at 2jz+1,
+// 0.25 * (t + c) at 2jz+2, which is also the next coarse plane's a).  The
+// z-weighted plane goes to shared memory; its y pass runs in the next phase
+// and the x pass in the one after -- one barrier per fine plane, and the fine
+// residual is never stored.  Nine warps: warp w owns residual rows w and w+9
+// of x0..x0+31, warp 8 also the column x0+32, so each thread evaluates at
+// most two residuals per plane and a warp's loads are 32 consecutive doubles.
+// The plane loop is unrolled by two (odd and even planes of the chunk carry
+// different z weights and passes), the u / b ring slots and their mbarrier
+// phases advance incrementally, and every per-thread index is precomputed:
+// the integer work per plane is a few adds.  ν = 1 has its own instantiation.
+// Residual arithmetic is k_z1<Z_RESID>'s and the weights fw_point's: the
+// coarse right-hand side is bit-identical to residual + full_weighting.
 constexpr int RX = TX + 1, RY = TY + 1, PR = align16(RX * RY);     // residual window
 constexpr int FUX = TX + 4, FUY = TY + 3, PFU = align16(FUX * FUY);  // u window
 constexpr int FBX = TX + 2, FBY = TY + 1, PFB = align16(FBX * FBY);  // b window
-constexpr int RFW_RU = 5, RFW_RB = 3;
+constexpr int RFW_RU = 5, RFW_RB = 3, RFW_NT = 288;
+constexpr int RFW_SMEM = sizeof(double) * (RFW_RU * PFU + RFW_RB * PFB + 2 * PR) +
+                         8 * (RFW_RU + RFW_RB);
 
-// NT = 288 (nine warps): the 561 residual points of the window are at most
-// two per thread, so no warp carries a third residual chain per plane
-template <bool POW2, int NT>
-__global__ void __launch_bounds__(NT, 4) k_rfw(const __grid_constant__ CUtensorMap mu,
-                                                 const __grid_constant__ CUtensorMap mb,
-                                                 double* __restrict__ coarse, Geo gf, Geo gc,
-                                                 OpC c, double sigma, int zcc) {
+template <bool POW2, bool UNIT>
+__global__ void __launch_bounds__(RFW_NT, 4) k_rfw(const __grid_constant__ CUtensorMap mu,
+                                                    const __grid_constant__ CUtensorMap mb,
+                                                    double* __restrict__ coarse, Geo gf, Geo gc,
+                                                    OpC c, double sigma, int zcc) {
   extern __shared__ __align__(128) double sm[];
   double* su = sm;                            // RFW_RU u windows
   double* sb = su + RFW_RU * PFU;             // RFW_RB b windows
@@ -954,8 +960,8 @@ __global__ void __launch_bounds__(NT, 4) k_rfw(const __grid_constant__ CUtensorM
   double* syx = szb + PR;                     // y-weighted rows (RX x TY/2)
   unsigned long long* bu = (unsigned long long*)(syx + PR);
   unsigned long long* bb = bu + RFW_RU;
-  const int tid = threadIdx.y * 32 + threadIdx.x;
-  constexpr int rfw_issuer = NT - 32;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  constexpr int rfw_issuer = RFW_NT - 32;     // warp 8: fewest residual points, no x pass
   const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TY;
   const int bz = zchunk_block(zcc);
   const int jz0 = bz * zcc, jz1 = min(jz0 + zcc, gc.nz);
@@ -967,6 +973,7 @@ __global__ void __launch_bounds__(NT, 4) k_rfw(const __grid_constant__ CUtensorM
     fence_barrier_init();
   }
   __syncthreads();
+  // the issuing thread's own ring counters (only it issues)
   auto issue_u = [&](int p) {
     if (p > uhi) return;
     const int s = (p - ulo) % RFW_RU;
@@ -979,107 +986,118 @@ __global__ void __launch_bounds__(NT, 4) k_rfw(const __grid_constant__ CUtensorM
     mbar_expect(bb + s, FBX * FBY * 8u);
     tma3(sb + s * PFB, &mb, x0, y0, p, bb + s);
   };
-  auto wait_u = [&](int p) {
-    const int k = p - ulo;
-    mbar_wait(bu + k % RFW_RU, (unsigned)((k / RFW_RU) & 1));
-  };
-  auto wait_b = [&](int p) {
-    const int k = p - p0;
-    mbar_wait(bb + k % RFW_RB, (unsigned)((k / RFW_RB) & 1));
-  };
   if (tid == 0) {
     for (int p = ulo; p < ulo + RFW_RU; ++p) issue_u(p);
     for (int p = p0; p < p0 + RFW_RB; ++p) issue_b(p);
   }
-  // owned residual points: window index k -> u / b window offsets
-  // NT = 288: row-aligned ownership -- warp w owns row w (q = 0) and row w + 9
-  // (q = 1) of x0..x0+31, warp 8 lanes 0..16 the last column x0+32 -- so a
-  // warp's loads are 32 consecutive doubles (no bank conflicts at row wraps)
-  constexpr int PERR = (RX * RY + NT - 1) / NT;
-  static_assert(NT != 288 || (PERR == 2 && RY == 17 && RX == 33), "row-aligned layout");
-  int r_k[PERR], r_iu[PERR], r_ib[PERR];
-  bool r_ok[PERR];
+  // ---- owned residual points (q = 0: row w; q = 1: row w + 9, or for warp 8
+  // the column x0 + 32 of rows 0..16)
+  int r_iu[2], r_ib[2], r_k[2];
+  bool r_ok[2], r_on[2];
 #pragma unroll
-  for (int q = 0; q < PERR; ++q) {
-    int k = tid + q * NT;
-    if (NT == 288) {
-      const int w = tid >> 5, lane = tid & 31;
-      k = q == 0 ? w * RX + lane
-                 : (w < 8 ? (w + 9) * RX + lane : (lane < RY ? lane * RX + TX : RX * RY));
-    }
+  for (int q = 0; q < 2; ++q) {
+    const int k = q == 0 ? warp * RX + lane
+                         : (warp < 8 ? (warp + 9) * RX + lane : (lane < RY ? lane * RX + TX : 0));
     const int ry = k / RX, rx = k - ry * RX;
-    r_k[q] = k < RX * RY ? k : -1;
+    r_on[q] = q == 0 || warp < 8 || lane < RY;
+    r_k[q] = k;
     r_iu[q] = (ry + 1) * FUX + rx + 2;
     r_ib[q] = ry * FBX + rx;
-    r_ok[q] = k < RX * RY && x0 + rx < gf.nx && y0 + ry < gf.ny;
+    r_ok[q] = r_on[q] && x0 + rx < gf.nx && y0 + ry < gf.ny;
   }
-  double acc[PERR], cm_[PERR], cc_[PERR];   // u of the own column at planes p-1, p
-#pragma unroll
-  for (int q = 0; q < PERR; ++q) acc[q] = cm_[q] = cc_[q] = 0.0;
-  // coarse point of this thread (threads 0..127) in the 16 x 8 tile
+  double acc[2], cm_[2], cc_[2];             // z fold; u of the own column at p-1, p
+  // ---- y pass entry (threads < RX * TY/2): syx[yy][xx] from szb rows 2yy..2yy+2
+  const bool ytask = tid < RX * (TY / 2);
+  const int yy = tid / RX, xx = tid - (tid / RX) * RX;
+  const int yo = ytask ? 2 * yy * RX + xx : 0, yd = ytask ? tid : 0;
+  // ---- x pass entry (threads < 128): coarse point (cx, cy) of the tile
   const int cx = tid & 15, cy = tid >> 4;
   const int gcx = x0 / 2 + cx, gcy = y0 / 2 + cy;
   const bool c_ok = tid < (TX / 2) * (TY / 2) && gcx < gc.nx && gcy < gc.ny;
-  for (int p = p0; p <= p1 + 2; ++p) {
-    const int ph = p - p0;
-    if (p <= p1) {
-      // ---- residuals of plane p, folded into the z weights
-      if (ph == 0) { wait_u(p - 1); wait_u(p); }
-      wait_u(p + 1);
-      wait_b(p);
-      const double* pm = su + ((p - 1 - ulo) % RFW_RU) * PFU;
-      const double* pc = su + ((p - ulo) % RFW_RU) * PFU;
-      const double* pp = su + ((p + 1 - ulo) % RFW_RU) * PFU;
-      const double* pb = sb + ((p - p0) % RFW_RB) * PFB;
+  const int xo = cy * RX + 2 * cx;
+  double* cdst = coarse + (c_ok ? gc.at(gcx, gcy, jz0) : 0);
+  // ---- u / b ring position of plane p+1 (u) and p (b), advanced per plane
+  int us = 2, up_ = 0;          // slot and phase bit of u plane p+1 (= ulo + 2 at p = p0)
+  int bs = 0, bp = 0;           // of b plane p
+  const double* pm = su;        // u planes p-1, p (slots 0, 1 at p = p0)
+  const double* pc = su + PFU;
+  // residual of plane p folded into the weights; FIRST: the chunk's first
+  // plane (a := v), ODD: t = a + 2 v, else 0.25 (t + v) -> szb, a := v
+  auto resid = [&](auto mode_tag, int p) {
+    constexpr int MODE = decltype(mode_tag)::value;   // 0 first, 1 odd, 2 even
+    mbar_wait(bu + us, (unsigned)up_);
+    mbar_wait(bb + bs, (unsigned)bp);
+    const double* pp = su + us * PFU;
+    const double* pb = sb + bs * PFB;
 #pragma unroll
-      for (int q = 0; q < PERR; ++q) {
-        if (r_k[q] < 0) continue;
-        const int i = r_iu[q];
-        if (ph == 0) {
-          cm_[q] = pm[i];
-          cc_[q] = pc[i];
-        }
-        const double zcp = pp[i];
-        double v = 0.0;
-        if (r_ok[q]) {
-          // lap7's expression tree with the column's centre values in registers
-          const double c0 = cc_[q];
-          double lacc = 0.0;
-          lacc = lacc + dd2<POW2>((cm_[q] - 2.0 * c0) + zcp, c);
-          lacc = lacc + dd2<POW2>((pc[i - FUX] - 2.0 * c0) + pc[i + FUX], c);
-          lacc = lacc + dd2<POW2>((pc[i - 1] - 2.0 * c0) + pc[i + 1], c);
-          const double lap = c.nu * lacc;
-          const double au = c0 - sigma * lap;
-          v = pb[r_ib[q]] - au;
-        }
-        cm_[q] = cc_[q];
-        cc_[q] = zcp;
-        if (ph == 0) {
-          acc[q] = v;                                  // a of coarse plane jz0
-        } else if (ph & 1) {
-          acc[q] = acc[q] + 2.0 * v;                   // t = a + 2 b
-        } else {
-          szb[r_k[q]] = 0.25 * (acc[q] + v);           // z weight of plane (p-2)/2
-          acc[q] = v;                                  // a of the next coarse plane
-        }
+    for (int q = 0; q < 2; ++q) {
+      if (!r_on[q]) continue;
+      const int i = r_iu[q];
+      if (MODE == 0) {
+        cm_[q] = pm[i];
+        cc_[q] = pc[i];
+      }
+      const double zcp = pp[i];
+      double v = 0.0;
+      if (r_ok[q]) {
+        // lap7's expression tree with the column's centre values in registers
+        const double c0 = cc_[q];
+        double lacc = 0.0;
+        lacc = lacc + dd2<POW2>((cm_[q] - 2.0 * c0) + zcp, c);
+        lacc = lacc + dd2<POW2>((pc[i - FUX] - 2.0 * c0) + pc[i + FUX], c);
+        lacc = lacc + dd2<POW2>((pc[i - 1] - 2.0 * c0) + pc[i + 1], c);
+        const double lap = UNIT ? lacc : c.nu * lacc;
+        const double au = c0 - sigma * lap;
+        v = pb[r_ib[q]] - au;
+      }
+      cm_[q] = cc_[q];
+      cc_[q] = zcp;
+      if (MODE == 0) {
+        acc[q] = v;
+      } else if (MODE == 1) {
+        acc[q] = acc[q] + 2.0 * v;
+      } else {
+        szb[r_k[q]] = 0.25 * (acc[q] + v);
+        acc[q] = v;
       }
     }
-    if ((ph & 1) == 1 && ph >= 3) {                    // y pass of jz = (p - 3) / 2
-      for (int k = tid; k < RX * (TY / 2); k += NT) {
-        const int yy = k / RX, xx = k - yy * RX;
-        const double* zc = szb + 2 * yy * RX + xx;
-        syx[k] = fw3(zc[0], zc[RX], zc[2 * RX]);
-      }
+    pm = pc;
+    pc = pp;
+    if (++us == RFW_RU) { us = 0; up_ ^= 1; }
+    if (++bs == RFW_RB) { bs = 0; bp ^= 1; }
+  };
+  auto ypass = [&]() {
+    if (ytask) syx[yd] = fw3(szb[yo], szb[yo + RX], szb[yo + 2 * RX]);
+  };
+  auto xpass = [&]() {
+    if (c_ok) {
+      *cdst = fw3(syx[xo], syx[xo + 1], syx[xo + 2]);
+      cdst += gc.sz;
     }
-    if ((ph & 1) == 0 && ph >= 4 && c_ok) {            // x pass of jz = (p - 4) / 2
-      const double* yr = syx + cy * RX + 2 * cx;
-      coarse[gc.at(gcx, gcy, (p - 4) / 2)] = fw3(yr[0], yr[1], yr[2]);
-    }
+  };
+  auto after = [&](int p) {    // plane p's residuals done: u plane p-1 and b plane p are free
     __syncthreads();
-    if (tid == rfw_issuer && p <= p1) {   // warp 7: fewest residual points, no x pass
-      issue_u(p - 1 + RFW_RU);    // u plane p-1 is free after the residuals of p
-      issue_b(p + RFW_RB);        // b plane p is free
+    if (tid == rfw_issuer && p <= p1) {
+      issue_u(p - 1 + RFW_RU);
+      issue_b(p + RFW_RB);
     }
+  };
+  // phase p0: a of coarse plane jz0
+  mbar_wait(bu + 0, 0u);
+  mbar_wait(bu + 1, 0u);
+  resid(std::integral_constant<int, 0>{}, p0);
+  after(p0);
+  // phases (p0 + 2i + 1, p0 + 2i + 2): odd plane (t, y pass of the coarse
+  // plane finished two phases ago), even plane (c and the next a, x pass)
+  for (int p = p0 + 1; p <= p1 + 2; p += 2) {
+    const int ph = p - p0;                         // odd
+    if (p <= p1) resid(std::integral_constant<int, 1>{}, p);
+    if (ph >= 3) ypass();                          // y pass of jz = (p - 3) / 2
+    after(p);
+    if (p + 1 > p1 + 2) break;
+    if (p + 1 <= p1) resid(std::integral_constant<int, 2>{}, p + 1);
+    if (ph + 1 >= 4) xpass();                      // x pass of jz = (p - 3) / 2
+    after(p + 1);
   }
 }
 
@@ -1499,7 +1517,6 @@ int make_map(CUtensorMap* m, const double* base, const Geo& g, int bw, int bh) {
 
 }  // namespace
 int g_zrev_mask = 3;   // PL_OPT_ZREV: reverse z-chunk order of 1 apply / apply+rhs, 2 k_rfw
-int g_rfw_threads = 288;   // PL_OPT_RFW_THREADS: 256 (eight warps) or 288 (nine, default)
 int g_zc_floor = 16;  // PL_OPT_ZC_FLOOR (A/B): smallest z chunk (4 and 8 measured slower at 127^3)
 int g_zc_ctas = 148 * 8;   // PL_OPT_ZC_CTAS (A/B): CTA count the z chunking aims for
 int g_zc_fit = 1;          // PL_OPT_ZC_FIT: wave-aware z chunks (pick_zc_fit)
@@ -1672,13 +1689,12 @@ int launch_rfw(const double* u, const double* b, double* coarse, const Geo& g, c
   PL_TRY(make_map(&mu, u, g, FUX, FUY));
   PL_TRY(make_map(&mb, b, g, FBX, FBY));
   const int zcc = pick_zc(g) / 2 < 4 ? 4 : pick_zc(g) / 2;
-  const int nt = g_rfw_threads == 256 ? 256 : 288;
-  dim3 grid(ceil_div(g.nx, TX), ceil_div(g.ny, TY), ceil_div(gc.nz, zcc)), block(32, nt / 32);
-  size_t smem = sizeof(double) * (RFW_RU * PFU + RFW_RB * PFB + 2 * PR) + 8 * (RFW_RU + RFW_RB);
-  auto kern = nt == 256 ? (c.pow2 ? k_rfw<true, 256> : k_rfw<false, 256>)
-                        : (c.pow2 ? k_rfw<true, 288> : k_rfw<false, 288>);
-  raise_smem(kern, smem);
-  kern<<<grid, block, smem, s>>>(mu, mb, coarse, g, gc, c, sigma, (g_zrev_mask & 2) ? -zcc : zcc);
+  dim3 grid(ceil_div(g.nx, TX), ceil_div(g.ny, TY), ceil_div(gc.nz, zcc));
+  auto kern = c.pow2 ? (c.nu == 1.0 ? k_rfw<true, true> : k_rfw<true, false>)
+                     : (c.nu == 1.0 ? k_rfw<false, true> : k_rfw<false, false>);
+  raise_smem(kern, RFW_SMEM);
+  kern<<<grid, RFW_NT, RFW_SMEM, s>>>(mu, mb, coarse, g, gc, c, sigma,
+                                      (g_zrev_mask & 2) ? -zcc : zcc);
   return 0;
 }
 

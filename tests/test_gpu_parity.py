@@ -772,26 +772,27 @@ def test_sweep_fused_apply_rhs_equals_separate(n, with_tau, policy):
     assert torch.equal(outs[0][1], outs[1][1])
 
 
-@pytest.mark.parametrize("n,sigma", [(128, 1.0 / 128), (256, 0.37)])
-@pytest.mark.parametrize("threads", [256, 288])
-def test_rfw_thread_layouts_equal_plain_kernels(n, sigma, threads):
-    """The fused residual + full-weighting kernel (eight warps, or nine with
-    row-aligned residual ownership) gives the plain kernels' V-cycle
-    (residual, then full weighting) bit for bit."""
-    rng = np.random.default_rng(n + threads)
+@pytest.mark.parametrize("n,sigma,nu", [(128, 1.0 / 128, 1.0), (256, 0.37, 1.0),
+                                        (128, 0.02, 0.7), (64, 0.05, 1.0)])
+def test_rfw_equals_plain_kernels(n, sigma, nu):
+    """The fused residual + full-weighting kernel (both nu instantiations,
+    several z chunks, ragged tiles) gives the plain kernels' V-cycle (residual,
+    then full weighting) bit for bit."""
+    rng = np.random.default_rng(n + int(100 * nu))
     g = heat.Grid(3, n)
     u = dev(rng.standard_normal(g.shape))
     b = dev(rng.standard_normal(g.shape))
-    sop = mg.ShiftedOperator(heat.HeatOperator(g), sigma)
+    sop = mg.ShiftedOperator(heat.HeatOperator(g, nu), sigma)
     cfg = mg.MgConfig("jor-rb", 1.0, 1, 1)
-    _capi.set_option(_capi.OPT_RFW, 0)
-    ref = mg.v_cycle(sop, u, b, cfg)
-    _capi.set_option(_capi.OPT_RFW, 1)
-    _capi.set_option(_capi.OPT_RFW_THREADS, threads)
+    _capi.set_option(_capi.OPT_ZMARCH_MIN_N, 63)
     try:
+        _capi.set_option(_capi.OPT_RFW, 0)
+        ref = mg.v_cycle(sop, u, b, cfg)
+        _capi.set_option(_capi.OPT_RFW, 1)
         assert torch.equal(mg.v_cycle(sop, u, b, cfg), ref)
     finally:
-        _capi.set_option(_capi.OPT_RFW_THREADS, 288)
+        _capi.set_option(_capi.OPT_RFW, 1)
+        _capi.set_option(_capi.OPT_ZMARCH_MIN_N, 127)
 
 
 def test_fas_chain_fw_fused_equals_separate():
