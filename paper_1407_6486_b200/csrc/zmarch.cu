@@ -1333,7 +1333,7 @@ __global__ void __launch_bounds__(NT5, 4) k_cubic5(const __grid_constant__ CUten
                                                    const double* __restrict__ tw, int zc,
                                                    int accumulate) {
   __shared__ __align__(128) double sc[RQ4 * PQ];
-  __shared__ __align__(128) double zb[2 * PQ];
+  __shared__ __align__(128) double zb[PQ];
   __shared__ __align__(128) double yb[2 * PYB5];
   __shared__ __align__(8) unsigned long long bar[RQ4];
   __shared__ __align__(8) unsigned long long fbar[RF5];
@@ -1419,60 +1419,81 @@ __global__ void __launch_bounds__(NT5, 4) k_cubic5(const __grid_constant__ CUten
   const int xci = xr * QW + xp + 2;
   const bool in0 = gx < gf.nx && gy < gf.ny, in1 = gx + 1 < gf.nx && gy < gf.ny;
   const int fo = xr * TX + 2 * xp;
-  double* fp = fine + (in0 ? gf.at(gx, gy, 0) : 0) + (long long)(z0 - 2) * gf.sz;
-  for (int t = 0; t < n + 2; ++t, fp += gf.sz) {
-    // ---- z pass of fine plane z0+t (4-tap planes only)
+  double* fp = fine + (in0 ? gf.at(gx, gy, 0) : 0) + (long long)z0 * gf.sz;
+  // z0 is even (even chunks): window planes t alternate 4-tap (t even: fine
+  // array index even) and coincident (t odd).  Phase t runs the z pass of
+  // plane t (4-tap planes only), the y pass of t-1 and the x pass of t-2, so
+  // an even phase writes yb[1] and reads yb[0], an odd phase the reverse, and
+  // one z buffer suffices (written in even phases, read in the next odd one).
+  int fslot = 0, fphase = 0;   // fine-tile ring slot / phase of the x-pass plane
+  auto wait_coarse = [&](int jmax) {
+    for (; waited <= jmax; ++waited) {
+      const int k = waited - jlo;
+      mbar_wait(bar + (k & (RQ4 - 1)), (unsigned)((k / RQ4) & 1));
+    }
+  };
+  auto xpass = [&](const double* ys, bool coincident_plane) {
+    double a0 = tap_chain<true>(4, xw, ys[xi[0]], ys[xi[1]], ys[xi[2]], ys[xi[3]]);
+    double a1 = ys[xci] + 0.0;
+    (void)coincident_plane;
+    if (accumulate) {
+      mbar_wait(fbar + fslot, (unsigned)fphase);
+      const double2 o = *reinterpret_cast<const double2*>(sfine + fslot * PF4 + fo);
+      a0 = o.x + a0;
+      a1 = o.y + a1;
+    }
+    if (++fslot == RF5) { fslot = 0; fphase ^= 1; }
+    if (in1) *reinterpret_cast<double2*>(fp) = make_double2(a0, a1);
+    else if (in0) fp[0] = a0;
+    fp += gf.sz;
+  };
+  auto issue_after = [&](int t) {   // phase t done
+    if (tid != cissuer) return;
+    if (t >= 2) issue_fine(z0 + t - 2 + RF5);   // x pass of plane t-2 done: slot free
+    int lo = jtop + 1;                  // coarse planes still read: z pass of t+1, t+2,
+    if (t < n && s_zn[t] == 1) lo = min(lo, s_zj[t * 4]);   // y pass of a coincident t
+    if (t + 1 < n) lo = min(lo, s_zj[(t + 1) * 4]);
+    if (t + 2 < n) lo = min(lo, s_zj[(t + 2) * 4]);
+    issue_upto(lo);
+  };
+  for (int t = 0; t < n + 2; t += 2) {
+    // ---- even phase: z pass of 4-tap plane t, y pass of coincident t-1,
+    // x pass of 4-tap t-2
     if (t < n) {
-      const int zn = s_zn[t];
       int zj[4];
       double zw[4];
 #pragma unroll
       for (int u = 0; u < 4; ++u) { zj[u] = s_zj[t * 4 + u]; zw[u] = s_zw[t * 4 + u]; }
-      for (; waited <= zj[3]; ++waited) {
-        const int k = waited - jlo;
-        mbar_wait(bar + (k & (RQ4 - 1)), (unsigned)((k / RQ4) & 1));
-      }
-      if (zn > 1 && tid < QW * QH) {
+      wait_coarse(zj[3]);
+      if (tid < QW * QH) {
         const double* s0 = sc + ((zj[0] - jlo) & (RQ4 - 1)) * PQ + tid;
         const double* s1 = sc + ((zj[1] - jlo) & (RQ4 - 1)) * PQ + tid;
         const double* s2 = sc + ((zj[2] - jlo) & (RQ4 - 1)) * PQ + tid;
         const double* s3 = sc + ((zj[3] - jlo) & (RQ4 - 1)) * PQ + tid;
-        zb[(t & 1) * PQ + tid] = tap_chain<true>(4, zw, *s0, *s1, *s2, *s3);
+        zb[tid] = tap_chain<true>(4, zw, *s0, *s1, *s2, *s3);
       }
     }
-    // ---- y pass of fine plane z0+t-1
-    const int t2 = t - 1;
-    if (t2 >= 0 && t2 < n && yt) {
-      const double* zs = s_zn[t2] > 1 ? zb + (t2 & 1) * PQ
-                                      : sc + ((s_zj[t2 * 4] - jlo) & (RQ4 - 1)) * PQ;
-      double* yd = yb + (t2 & 1) * PYB5;
+    if (t >= 1 && t - 1 < n && yt) {
+      const double* zs = sc + ((s_zj[(t - 1) * 4] - jlo) & (RQ4 - 1)) * PQ;
+      double* yd = yb + PYB5;
       yd[yo] = tap_chain<true>(4, yw, zs[yi[0]], zs[yi[1]], zs[yi[2]], zs[yi[3]]);
       yd[yo + QW] = zs[yci] + 0.0;
     }
-    // ---- x pass of fine plane z0+t-2
-    const int t3 = t - 2;
-    if (t3 >= 0) {
-      const double* ys = yb + (t3 & 1) * PYB5;
-      double a0 = tap_chain<true>(4, xw, ys[xi[0]], ys[xi[1]], ys[xi[2]], ys[xi[3]]);
-      double a1 = ys[xci] + 0.0;
-      if (accumulate) {
-        mbar_wait(fbar + t3 % RF5, (unsigned)((t3 / RF5) & 1));
-        const double2 o = *reinterpret_cast<const double2*>(sfine + (t3 % RF5) * PF4 + fo);
-        a0 = o.x + a0;
-        a1 = o.y + a1;
-      }
-      if (in1) *reinterpret_cast<double2*>(fp) = make_double2(a0, a1);
-      else if (in0) fp[0] = a0;
-    }
+    if (t >= 2) xpass(yb, false);
     __syncthreads();
-    if (tid == cissuer) {
-      if (t3 >= 0) issue_fine(z0 + t3 + RF5);   // x pass of plane t-2 done: slot free
-      int lo = jtop + 1;                     // coarse planes still read: z pass of
-      if (t < n && s_zn[t] == 1) lo = min(lo, s_zj[t * 4]);   // t+1, t+2; y pass of t
-      if (t + 1 < n) lo = min(lo, s_zj[(t + 1) * 4]);
-      if (t + 2 < n) lo = min(lo, s_zj[(t + 2) * 4]);
-      issue_upto(lo);
+    issue_after(t);
+    if (t + 1 >= n + 2) break;
+    // ---- odd phase: (coincident plane t+1 needs its coarse plane next
+    // phase), y pass of 4-tap plane t, x pass of coincident t-1
+    if (t + 1 < n) wait_coarse(s_zj[(t + 1) * 4]);
+    if (t < n && yt) {
+      double* yd = yb;
+      yd[yo] = tap_chain<true>(4, yw, zb[yi[0]], zb[yi[1]], zb[yi[2]], zb[yi[3]]);
+      yd[yo + QW] = zb[yci] + 0.0;
     }
+    if (t >= 1) xpass(yb + PYB5, true);
+    __syncthreads();
+    issue_after(t + 1);
   }
 }
 
@@ -1720,7 +1741,7 @@ int launch_cubic4(const double* coarse, double* fine, const Geo& gf, const int* 
   }
   const size_t smem5 = accumulate ? sizeof(double) * RF5 * PF4 : 0;
   raise_smem(k_cubic5, smem5);
-  const int zc5 = pick_zc_fit(gf, resident_ctas(k_cubic5, NT5, smem5), 1, 5, 8, 64);
+  const int zc5 = pick_zc_fit(gf, resident_ctas(k_cubic5, NT5, smem5), 2, 5, 8, 64);
   grid.z = ceil_div(gf.nz, zc5);
   k_cubic5<<<grid, NT5, smem5, s>>>(mc, mf, fine, gf, cnt, idx, w, zc5, accumulate);
   return 0;
