@@ -215,6 +215,136 @@ __global__ void __launch_bounds__(CF_NT, 3) k_chain_fw(const double* __restrict_
   const int x0 = blockIdx.x * CF_TX, y0 = blockIdx.y * CF_TY;
   const int jz0 = blockIdx.z * zcc, jz1 = min(jz0 + zcc, gc.nz);
   const int p0 = 2 * jz0, p1 = 2 * jz1;
+  // ---- owned fine points: row w (q = 0), row w + 9 or (warp 8) the last column
+  int r_k[2];
+  bool r_on[2], r_ok[2];
+  const double* r_f[2];                 // F at the point on plane p (column 0 of F)
+  const double* r_a[2];                 // add (tau) at the point on plane p
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    const int k = q == 0 ? w * CF_RX + lane
+                         : (w < 8 ? (w + 9) * CF_RX + lane : (lane < CF_RY ? lane * CF_RX + CF_TX : 0));
+    const int ry = k / CF_RX, rx = k - ry * CF_RX;
+    r_on[q] = q == 0 || w < 8 || lane < CF_RY;
+    r_k[q] = k;
+    r_ok[q] = r_on[q] && x0 + rx < gf.nx && y0 + ry < gf.ny;
+    const long long g0 = r_ok[q] ? gf.at(x0 + rx, y0 + ry, p0) : 0;
+    r_f[q] = F + g0;
+    r_a[q] = add ? add + g0 : nullptr;
+  }
+  double acc[2][R];
+  // ---- y pass: thread tid < 264 owns window entry (yy, xx) of every row set r
+  constexpr int NYE = CF_RX * (CF_TY / 2);
+  const bool ytask = tid < NYE;
+  const int yy = tid / CF_RX, xx = tid - (tid / CF_RX) * CF_RX;
+  const int y_src = 2 * yy * CF_RX + xx;
+  // ---- x pass: entries e = tid + 288 i (< R * 128), coarse plane advanced per pass
+  constexpr int NX = R * (CF_TX / 2) * (CF_TY / 2), NXI = (NX + CF_NT - 1) / CF_NT;
+  // the chain values of plane p at the owned points (k_chain's arithmetic)
+  auto values = [&](int q, long long off, double* v) {
+    if (!r_ok[q]) {
+#pragma unroll
+      for (int r = 0; r < R; ++r) v[r] = 0.0;
+      return;
+    }
+    double f[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) f[k] = __ldcs(r_f[q] + c.col[k] * stride + off);
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      if constexpr (IDENT) {
+        v[r] = f[r];
+      } else {
+        double a = 0.0;
+#pragma unroll
+        for (int k = 0; k < K; ++k) a = __fma_rn(c.a[r * K + k], f[k], a);
+        double t = scale * a;
+        if (mode == 1) t = t + r_a[q][c.addrow[r] * add_stride + off];
+        v[r] = t;
+      }
+    }
+  };
+  // MODE 0: first plane of the chunk (a := v); 1: odd plane (t = a + 2 v);
+  // 2: even plane (0.25 (t + v) -> szb, a := v)
+  auto fold = [&](auto mode_tag, long long off) {
+    constexpr int MODE = decltype(mode_tag)::value;
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      if (!r_on[q]) continue;
+      double v[R];
+      values(q, off, v);
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        if (MODE == 0) {
+          acc[q][r] = v[r];
+        } else if (MODE == 1) {
+          acc[q][r] = acc[q][r] + 2.0 * v[r];
+        } else {
+          szb[r * CF_PR + r_k[q]] = 0.25 * (acc[q][r] + v[r]);
+          acc[q][r] = v[r];
+        }
+      }
+    }
+  };
+  auto ypass = [&]() {
+    if (!ytask) return;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const double* zc = szb + r * CF_PR + y_src;
+      syx[r * CF_PR + tid] = fw3(zc[0], zc[CF_RX], zc[2 * CF_RX]);
+    }
+  };
+  int jz = jz0;
+  auto xpass = [&]() {
+#pragma unroll
+    for (int it = 0; it < NXI; ++it) {
+      const int e = tid + it * CF_NT;
+      const int r = e >> 7, pt = e & 127;
+      const int ex = pt & 15, ey = pt >> 4;
+      const int gcx = x0 / 2 + ex, gcy = y0 / 2 + ey;
+      if (e < NX && gcx < gc.nx && gcy < gc.ny) {
+        const double* yr = syx + r * CF_PR + ey * CF_RX + 2 * ex;
+        coarse[r * cstride + gc.at(gcx, gcy, jz)] = fw3(yr[0], yr[1], yr[2]);
+      }
+    }
+    ++jz;
+  };
+  // phase p0, then pairs (odd plane: y pass of the coarse plane finished two
+  // phases ago; even plane: x pass)
+  long long off = 0;
+  fold(std::integral_constant<int, 0>{}, off);
+  __syncthreads();
+  for (int p = p0 + 1; p <= p1 + 2; p += 2) {
+    const int ph = p - p0;                     // odd
+    off += gf.sz;
+    if (p <= p1) fold(std::integral_constant<int, 1>{}, off);
+    if (ph >= 3) ypass();                      // y pass of jz = (p - 3) / 2
+    __syncthreads();
+    off += gf.sz;
+    if (p + 1 <= p1) fold(std::integral_constant<int, 2>{}, off);
+    if (ph + 1 >= 4) xpass();                  // x pass of jz = (p - 3) / 2
+    __syncthreads();
+  }
+}
+
+// the same operation for many input fields (K x R large): the runtime plane
+// loop keeps fewer values live (no spills at 72 registers)
+template <int K, int R, bool IDENT = false>
+__global__ void __launch_bounds__(CF_NT, 3) k_chain_fw_wide(const double* __restrict__ F,
+                                                      long long stride, NodeCoef c, double scale,
+                                                      const double* __restrict__ add,
+                                                      long long add_stride, int mode,
+                                                      double* __restrict__ coarse,
+                                                      long long cstride, Geo gf, Geo gc,
+                                                      int zcc) {
+  extern __shared__ __align__(16) double cf_sm[];
+  double* szb = cf_sm;                  // R z-weighted planes (CF_RX x CF_RY)
+  double* syx = cf_sm + R * CF_PR;      // R y-weighted row sets (CF_RX x CF_TY/2)
+  const int tid = threadIdx.y * 32 + threadIdx.x;
+  const int w = tid >> 5, lane = tid & 31;
+  const int x0 = blockIdx.x * CF_TX, y0 = blockIdx.y * CF_TY;
+  const int jz0 = blockIdx.z * zcc, jz1 = min(jz0 + zcc, gc.nz);
+  const int p0 = 2 * jz0, p1 = 2 * jz1;
   int r_k[2];
   bool r_ok[2];
   long long r_g[2];
@@ -456,13 +586,15 @@ int launch_chain_fw(const double* F, long long stride, const Coef& a, double sca
   dim3 block(32, CF_NT / 32);
   const int mode = add ? 1 : 0;
   PL_PRE(K_FAS);
+  // up to 25 chain coefficients per point the unrolled kernel keeps every
+  // value in registers; wider FAS chains (K x R > 25) take the plane-loop form
 #define CF_CALL(KK, RR)                                                                       \
   do {                                                                                        \
     size_t smem = sizeof(double) * 2 * RR * CF_PR;                                            \
-    cudaFuncSetAttribute(k_chain_fw<KK, RR>, cudaFuncAttributeMaxDynamicSharedMemorySize,     \
-                         (int)smem);                                                          \
-    k_chain_fw<KK, RR><<<grid, block, smem, s>>>(F, stride, c, scale, add, add_stride, mode,  \
-                                                 coarse, cstride, gf, gc, zcc);               \
+    auto kern = KK * RR <= 25 ? k_chain_fw<KK, RR> : k_chain_fw_wide<KK, RR>;                 \
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);       \
+    kern<<<grid, block, smem, s>>>(F, stride, c, scale, add, add_stride, mode, coarse,        \
+                                   cstride, gf, gc, zcc);                                     \
   } while (0)
 #define CF_R(KK)                                   \
   switch (a.rows) {                                \

@@ -94,6 +94,24 @@ def main():
                                                     s), 8.0 * N * (2 + 2.0 ** -g.dim))
     run("interp_cubic_add", lambda: transfers.interp_cubic_into(c, u, True),
         8.0 * N * (2 + 2.0 ** -g.dim))
+    if args.dim == 3:   # FAS machinery of a 9/5-node, n/n/2 level pair (BASELINE config 3)
+        from paper_1407_6486_b200 import hierarchy
+        from paper_1407_6486_b200.hierarchy import Level
+        cfgm = MgConfig("jor-rb", 1.0, 1, 1)
+        fl = Level(op, uniform_table(8), cfgm, FixedCycles(1), space_interp_order=4)
+        cl = Level(HeatOperator(Grid(3, g.n // 2)), uniform_table(4), cfgm, FixedCycles(1),
+                   space_interp_order=4)
+        fst = NodeStates.spread(op, fl.table, u)
+        rs = hierarchy.restrict_state(fst, fl, cl)
+        nc = (g.n // 2 - 1) ** 3
+        run("restrict_state", lambda: hierarchy.restrict_state(fst, fl, cl, out=rs),
+            8.0 * N * 5 + 24.0 * 5 * nc)
+        tau = hierarchy.compute_fas(fst, rs, fl, cl, 1 / 64)
+        run("compute_fas", lambda: hierarchy.compute_fas(fst, rs, fl, cl, 1 / 64, out=tau),
+            8.0 * N * 9 + 8.0 * 9 * nc)
+        old = rs.copy()
+        run("coarse_correction", lambda: hierarchy.coarse_correction(fst, old, rs, fl, cl),
+            (8.0 * 2 + 16.0) * 9 * N)
     for M in (4, 8):
         table = uniform_table(M)
         st = NodeStates.spread(op, table, u)
