@@ -141,7 +141,8 @@ def release_device_caches():
     import gc
 
     import torch
-    from paper_1407_6486_b200 import _device, multigrid
+    from paper_1407_6486_b200 import _device, multigrid, pfasst
+    pfasst.release_engines()
     multigrid._plans.clear()
     _device.release_scratch()
     gc.collect()

@@ -636,6 +636,31 @@ def _run_block(blk, engine, exchange):
         blk.iterations_loop()
 
 
+_ENGINE_CACHE: list = []     # [(key, engine)] of the most recent pfasst_run
+
+
+def _device_engine(levels, dt, ranks, streams):
+    """The DeviceEngine of the previous pfasst_run when it ran the same level
+    objects, dt, ranks and stream mode on this device: its per-rank state
+    buffers are re-spread rather than reallocated, so repeated runs keep their
+    device addresses (and the captured sweep graphs keyed by them).  One
+    engine is kept; a run with other levels replaces it."""
+    key = (tuple(id(lv) for lv in levels), float(dt), tuple(ranks), bool(streams),
+           torch.cuda.current_device())
+    if _ENGINE_CACHE and _ENGINE_CACHE[0][0] == key and \
+            all(a is b for a, b in zip(_ENGINE_CACHE[0][1].levels, levels)):
+        return _ENGINE_CACHE[0][1]
+    _ENGINE_CACHE.clear()
+    engine = DeviceEngine(levels, dt, ranks, streams=streams)
+    _ENGINE_CACHE.append((key, engine))
+    return engine
+
+
+def release_engines():
+    """Drop the cached engine (its device buffers)."""
+    _ENGINE_CACHE.clear()
+
+
 def _gather_block(blk, exchange):
     """Combine per-process bookkeeping (nccl executor)."""
     if not isinstance(exchange, DistExchange):
@@ -695,13 +720,15 @@ def pfasst_run(levels, u0, t_end: float, p: int, blocks: int = 1, tol: float = 1
             me = dist.get_rank(group)
             ranks = [n for n in range(p) if n % world == me]
             if engine is None:
-                engine = engine_factory(levels, dt, ranks)
+                engine = (_device_engine(levels, dt, ranks, False)
+                          if engine_factory is DeviceEngine else
+                          engine_factory(levels, dt, ranks))
             exchange = DistExchange(engine, group)
         else:
             if engine is None:
                 if engine_factory is DeviceEngine:
                     use = streams and p > 1 and _rank_streams_fit(levels, p)
-                    engine = DeviceEngine(levels, dt, range(p), streams=use)
+                    engine = _device_engine(levels, dt, range(p), use)
                 else:
                     engine = engine_factory(levels, dt, range(p))
             exchange = _LocalExchange(engine)
