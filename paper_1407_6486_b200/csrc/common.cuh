@@ -199,4 +199,54 @@ __host__ __device__ inline int ceil_div(long long a, long long b) {
   return (int)((a + b - 1) / b);
 }
 
+// correctly rounded a / b given y = RN(1/b): q0 = RN(a y) is within 1.5 ulp,
+// one Markstein correction makes it faithful, the second exact (Markstein's
+// theorem: y within half an ulp of 1/b, q faithful, remainder exact by FMA).
+// Zeros (sign), subnormals, huge values and non-finite a take the IEEE
+// division.  (The coarsest LU's reciprocals come from the host; every other
+// y is RN(1/b) computed once per thread for a constant diagonal.)
+static __device__ __noinline__ double div_slow(double a, double b) { return a / b; }
+static __device__ __forceinline__ double div_const(double a, double b, double y) {
+  double q = a * y;
+  double r = __fma_rn(-b, q, a);
+  q = __fma_rn(r, y, q);
+  r = __fma_rn(-b, q, a);
+  q = __fma_rn(r, y, q);
+  const double aa = fabs(a);
+  if (__builtin_expect(!(aa >= 0x1p-960 && aa <= 0x1p960), 0)) q = div_slow(a, b);
+  return q;
+}
+
+// div_const's preconditions for a divisor d used across a whole level: RN(1/d)
+// normal and every quotient of an in-range a normal.  Otherwise the IEEE
+// division is used (rd = 0 marks it).
+__host__ __device__ inline bool diag_div_ok(double d) {
+  const double ad = fabs(d);
+  return ad >= 0x1p-64 && ad <= 0x1p64;
+}
+__device__ __forceinline__ double rcp_diag(double d) { return diag_div_ok(d) ? 1.0 / d : 0.0; }
+__device__ __forceinline__ double div_diag(double a, double d, double rd) {
+  return rd != 0.0 ? div_const(a, d, rd) : a / d;
+}
+
+// a / d for the shifted diagonal d of an order-2 level, which is one value for
+// the whole level: dc and its reciprocal rc = RN(1/dc) are computed once per
+// thread (ConstDiag) and the quotient is div_const's correctly rounded one --
+// the same bits as the IEEE division.  Order 4 (boundary rows differ) divides.
+struct ConstDiag {
+  bool on;
+  double d, r;
+  template <int DIM>
+  __device__ __forceinline__ void init(const Geo& g, const OpC& c, double sigma) {
+    d = c.order == 2 ? shifted_diag<DIM>(g, c, sigma, 0, 0, 0) : 1.0;
+    on = c.order == 2 && diag_div_ok(d);
+    r = 1.0 / d;
+  }
+  template <int DIM>
+  __device__ __forceinline__ double div(double a, const Geo& g, const OpC& c, double sigma,
+                                        int x, int y, int z) const {
+    return on ? div_const(a, d, r) : a / shifted_diag<DIM>(g, c, sigma, x, y, z);
+  }
+};
+
 }  // namespace pl

@@ -119,6 +119,8 @@ __device__ void tail_smooth(const TailArgs& a, const TailLevel& L, double* sm, i
     }
     return;
   }
+  ConstDiag cd;
+  cd.init<DIM>(L.g, L.c, a.sigma);
   if (a.smoother == SM_JACOBI) {
     // ping-pong u <-> t; one copy back only for an odd sweep count
     for (int k = 0; k < count; ++k) {
@@ -128,12 +130,11 @@ __device__ void tail_smooth(const TailArgs& a, const TailLevel& L, double* sm, i
       PL_FOR_SM_POINTS(L.g) {
         int x, y, z;
         decode(L.g, p, x, y, z);
-        double d = shifted_diag<DIM>(L.g, L.c, a.sigma, x, y, z);
         if (z0) {
-          dst[p] = 0.0 + ((a.omega * b[p]) / d);
+          dst[p] = 0.0 + cd.div<DIM>(a.omega * b[p], L.g, L.c, a.sigma, x, y, z);
         } else {
           double au = shifted_point<DIM>(src, L.g, L.c, a.sigma, x, y, z, p);
-          dst[p] = src[p] + ((a.omega * (b[p] - au)) / d);
+          dst[p] = src[p] + cd.div<DIM>(a.omega * (b[p] - au), L.g, L.c, a.sigma, x, y, z);
         }
       }
       __syncthreads();
@@ -204,9 +205,8 @@ __device__ void tail_smooth(const TailArgs& a, const TailLevel& L, double* sm, i
           const int x = 2 * h + (((y + z + DIM) & 1) ^ colour ^ 1);
           if (x >= N) continue;
           const int p = (z * L.g.ny + y) * N + x;
-          double d = shifted_diag<DIM>(L.g, L.c, a.sigma, x, y, z);
           double r = b[p] - shifted_point<DIM>(u, L.g, L.c, a.sigma, x, y, z, p);
-          u[p] = u[p] + ((a.omega * r) / d);
+          u[p] = u[p] + cd.div<DIM>(a.omega * r, L.g, L.c, a.sigma, x, y, z);
         }
         __syncthreads();
         continue;
@@ -259,8 +259,9 @@ __device__ void tail_lu(const TailArgs& a, const double* lu, const double* b, do
       for (int i = j + 1 + threadIdx.x; i < m; i += 32) u[i] = __fma_rn(-yj, A[i * m + j], u[i]);
       __syncwarp();
     }
+    const double* rcp = A + (size_t)m * m + m;   // RN(1 / U_jj), host-computed
     for (int j = m - 1; j >= 0; --j) {       // U x = y
-      if (threadIdx.x == 0) u[j] = u[j] / A[j * m + j];
+      if (threadIdx.x == 0) u[j] = div_diag(u[j], A[j * m + j], rcp[j]);
       __syncwarp();
       double xj = u[j];
       for (int i = threadIdx.x; i < j; i += 32) u[i] = __fma_rn(-xj, A[i * m + j], u[i]);
@@ -317,10 +318,11 @@ __device__ __forceinline__ void ft_colour(double* u, const double* b, const OpC&
   const Geo g = ct_geo<N>();
   // order 2: the diagonal is the same at every point (shifted_diag's operations)
   const double d = shifted_diag<3>(g, c, sigma, 1, 1, 1);
+  const double dr = rcp_diag(d);  // the quotients below are div_const's (exact RN)
   if (zero) {   // u == 0 on entry: red points 0 + (omega b) / d, black points 0
     for (int p = threadIdx.x; p < N * N * N; p += blockDim.x) {
       const int x = p % N, y = (p / N) % N, z = p / (N * N);
-      u[p] = is_red<3>(x, y, z) ? 0.0 + ((omega * b[p]) / d) : 0.0;
+      u[p] = is_red<3>(x, y, z) ? 0.0 + div_diag(omega * b[p], d, dr) : 0.0;
     }
     return;
   }
@@ -333,7 +335,7 @@ __device__ __forceinline__ void ft_colour(double* u, const double* b, const OpC&
     if (x >= N) continue;
     const int p = (z * N + y) * N + x;
     const double r = b[p] - ft_shifted<N>(u, inv, nu, sigma, x, y, z, p);
-    u[p] = u[p] + ((omega * r) / d);
+    u[p] = u[p] + div_diag(omega * r, d, dr);
   }
 }
 
@@ -355,8 +357,9 @@ __device__ __forceinline__ void ft_lu27(const double* A, const double* b, double
       const double yj = __shfl_sync(0xffffffffu, v, j);
       if (lane > j && lane < m) v = __fma_rn(-yj, A[lane * m + j], v);
     }
+    const double* rcp = A + m * m + m;        // RN(1 / U_jj), host-computed
     for (int j = m - 1; j >= 0; --j) {          // U x = y
-      if (lane == j) v = v / A[j * m + j];
+      if (lane == j) v = div_diag(v, A[j * m + j], rcp[j]);
       const double xj = __shfl_sync(0xffffffffu, v, j);
       if (lane < j) v = __fma_rn(-xj, A[lane * m + j], v);
     }
@@ -366,8 +369,9 @@ __device__ __forceinline__ void ft_lu27(const double* A, const double* b, double
 }
 
 // ft_colour's zero-guess red pass at one point (u == 0 on entry)
-__device__ __forceinline__ double ft_red0(double bv, double omega, double d, int x, int y, int z) {
-  return is_red<3>(x, y, z) ? 0.0 + ((omega * bv) / d) : 0.0;
+__device__ __forceinline__ double ft_red0(double bv, double omega, double d, double dr, int x,
+                                          int y, int z) {
+  return is_red<3>(x, y, z) ? 0.0 + div_diag(omega * bv, d, dr) : 0.0;
 }
 
 // fused: the zero-guess red pass (zero && pre > 0) was already applied by the
@@ -413,12 +417,12 @@ __device__ void ft_level(const TailArgs& a, double* sm, bool zero, bool fused = 
     constexpr bool FUSE = NC > 3;
     const bool fz = FUSE && a.pre > 0;
     double* uc = sm + C.off_u;
-    const double dc = shifted_diag<3>(gc, C.c, a.sigma, 1, 1, 1);
+    const double dc = shifted_diag<3>(gc, C.c, a.sigma, 1, 1, 1), dcr = rcp_diag(dc);
     for (int p = threadIdx.x; p < NC * NC * NC; p += blockDim.x) {
       const int x = p % NC, y = (p / NC) % NC, z = p / (NC * NC);
       const double v = fw_point<3>(t, g, x, y, z);
       bc[p] = v;
-      if (fz) uc[p] = ft_red0(v, a.omega, dc, x, y, z);
+      if (fz) uc[p] = ft_red0(v, a.omega, dc, dcr, x, y, z);
     }
     __syncthreads();
       ft_stamp(a);
@@ -525,10 +529,10 @@ __device__ void tail_run(const TailArgs& a, const double* __restrict__ b_in, dou
   const TailLevel& L0 = a.lv[0];
   if (DIM == 3 && a.fast) {
     ft_stamp(a);
-    for (int i = threadIdx.x; i < a.m * a.m + a.m; i += blockDim.x) sm[a.lu_off + i] = a.lu[i];
+    for (int i = threadIdx.x; i < a.m * a.m + 2 * a.m; i += blockDim.x) sm[a.lu_off + i] = a.lu[i];
     // zero guess: the first red pass of level 0 is fused into the load
     const bool fz = zero_guess && a.pre > 0;
-    const double d0 = shifted_diag<3>(L0.g, L0.c, a.sigma, 1, 1, 1);
+    const double d0 = shifted_diag<3>(L0.g, L0.c, a.sigma, 1, 1, 1), d0r = rcp_diag(d0);
     PL_FOR_SM_POINTS(L0.g) {
       int x, y, z;
       decode(L0.g, p, x, y, z);
@@ -536,7 +540,7 @@ __device__ void tail_run(const TailArgs& a, const double* __restrict__ b_in, dou
       const double bv = b_in[gi];
       sm[L0.off_b + p] = bv;
       if (!zero_guess) sm[L0.off_u + p] = u_io[gi];
-      else if (fz) sm[L0.off_u + p] = ft_red0(bv, a.omega, d0, x, y, z);
+      else if (fz) sm[L0.off_u + p] = ft_red0(bv, a.omega, d0, d0r, x, y, z);
     }
     __syncthreads();
     ft_stamp(a);
@@ -553,7 +557,7 @@ __device__ void tail_run(const TailArgs& a, const double* __restrict__ b_in, dou
     return;
   }
   if (a.lu_off >= 0)
-    for (int i = threadIdx.x; i < a.m * a.m + a.m; i += blockDim.x) sm[a.lu_off + i] = a.lu[i];
+    for (int i = threadIdx.x; i < a.m * a.m + 2 * a.m; i += blockDim.x) sm[a.lu_off + i] = a.lu[i];
   PL_FOR_SM_POINTS(L0.g) {
     int x, y, z;
     decode(L0.g, p, x, y, z);
@@ -666,14 +670,15 @@ template <int DIM>
 __device__ __forceinline__ void mid_colour(const MidLevel& L, const MidArgs& m, int red,
                                            bool zero, long long gt, long long gs) {
   const Geo& g = L.g;
+  ConstDiag cd;
+  cd.init<DIM>(g, L.c, m.sigma);
   if (zero) {
     for (long long t = gt; t < g.npts; t += gs) {
       int x, y, z;
       decode_point(g, t, x, y, z);
       const long long idx = g.at(x, y, z);
       if (is_red<DIM>(x, y, z)) {
-        const double d = shifted_diag<DIM>(g, L.c, m.sigma, x, y, z);
-        L.u[idx] = 0.0 + ((m.omega * L.b[idx]) / d);
+        L.u[idx] = 0.0 + cd.div<DIM>(m.omega * L.b[idx], g, L.c, m.sigma, x, y, z);
       } else {
         L.u[idx] = 0.0;
       }
@@ -691,11 +696,10 @@ __device__ __forceinline__ void mid_colour(const MidLevel& L, const MidArgs& m, 
     const int x = 2 * h + (((y + z + DIM) & 1) ^ red ^ 1);
     if (x >= N) continue;
     const long long idx = g.at(x, y, z);
-    const double d = shifted_diag<DIM>(g, L.c, m.sigma, x, y, z);
     const double r = L.b[idx] - (DIM == 3 && L.pow2
                                      ? mid_shifted(L.u, g, L.c, m.sigma, x, y, z, idx)
                                      : shifted_point<DIM>(L.u, g, L.c, m.sigma, x, y, z, idx));
-    L.u[idx] = L.u[idx] + ((m.omega * r) / d);
+    L.u[idx] = L.u[idx] + cd.div<DIM>(m.omega * r, g, L.c, m.sigma, x, y, z);
   }
 }
 
@@ -803,7 +807,7 @@ static int tail_args(MgPlan* P, int l0, double sigma, TailArgs& a, size_t* smem_
     T.off_t = off; off += np;
   }
   a.lu_off = -1;
-  const int lu_n = a.m * a.m + a.m;
+  const int lu_n = a.m * a.m + 2 * a.m;
   if (sizeof(double) * (off + lu_n) <= TAIL_SMEM_BUDGET + 8192) {
     a.lu_off = off;
     off += lu_n;
@@ -1134,6 +1138,16 @@ static void coarsest_lu_host(const MgPlan* P, double sigma, double* out) {
   std::memcpy(out + (size_t)m * m, piv.data(), sizeof(double) * m);
 }
 
+// RN(1 / U_jj) after the m x m factors and the m pivots (0: IEEE division):
+// the device solves divide by the diagonal with div_diag, whose quotient is
+// the IEEE one
+static void lu_reciprocals(int m, double* e) {
+  for (int j = 0; j < m; ++j) {
+    const double d = e[(size_t)j * m + j];
+    e[(size_t)m * m + m + j] = diag_div_ok(d) ? 1.0 / d : 0.0;
+  }
+}
+
 static int lu_entry(MgPlan* P, double sigma, LuEntry** out) {
   unsigned long long key = *(unsigned long long*)&sigma;
   auto it = P->lu.find(key);
@@ -1141,7 +1155,7 @@ static int lu_entry(MgPlan* P, double sigma, LuEntry** out) {
     *out = &it->second;
     return 0;
   }
-  size_t count = (size_t)P->m_lu * P->m_lu + P->m_lu;
+  size_t count = (size_t)P->m_lu * P->m_lu + 2 * (size_t)P->m_lu;
   LuEntry E;
   cudaError_t e = cudaMallocHost(&E.host, count * sizeof(double));
   if (e != cudaSuccess) return cuda_status(e, "cudaMallocHost lu");
@@ -1159,8 +1173,9 @@ int mg_prepare(MgPlan* P, double sigma, cudaStream_t s) {
   LuEntry* E = nullptr;
   int rc = lu_entry(P, sigma, &E);
   if (rc <= 0) return rc;
-  size_t count = (size_t)P->m_lu * P->m_lu + P->m_lu;
+  size_t count = (size_t)P->m_lu * P->m_lu + 2 * (size_t)P->m_lu;
   coarsest_lu_host(P, sigma, E->host);
+  lu_reciprocals(P->m_lu, E->host);
   cudaError_t e = cudaMemcpyAsync(E->dev, E->host, count * sizeof(double),
                                   cudaMemcpyHostToDevice, s);
   if (e != cudaSuccess) return cuda_status(e, "upload lu");
@@ -1179,7 +1194,8 @@ int mg_set_coarsest_lu(MgPlan* P, double sigma, const double* lu, const int* piv
   if (e != cudaSuccess) return cuda_status(e, "sync");
   std::memcpy(E->host, lu, sizeof(double) * mm);
   for (int i = 0; i < P->m_lu; ++i) E->host[mm + i] = (double)piv[i];
-  e = cudaMemcpyAsync(E->dev, E->host, (mm + P->m_lu) * sizeof(double),
+  lu_reciprocals(P->m_lu, E->host);
+  e = cudaMemcpyAsync(E->dev, E->host, (mm + 2 * P->m_lu) * sizeof(double),
                       cudaMemcpyHostToDevice, s);
   if (e != cudaSuccess) return cuda_status(e, "upload lu");
   return 0;

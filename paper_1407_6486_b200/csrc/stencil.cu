@@ -76,14 +76,15 @@ __global__ void __launch_bounds__(256) k_jacobi(const double* __restrict__ u,
                                                 const double* __restrict__ b,
                                                 double* __restrict__ out, Geo g, OpC c,
                                                 double sigma, double omega, int zero_in, int zc) {
+  ConstDiag cd;
+  cd.init<DIM>(g, c, sigma);
   PL_FOR_POINTS(g) {
     long long idx = (long long)z * g.sz + (long long)y * g.sy + x;
-    double d = shifted_diag<DIM>(g, c, sigma, x, y, z);
     if (zero_in) {
-      out[idx] = 0.0 + ((omega * b[idx]) / d);
+      out[idx] = 0.0 + cd.div<DIM>(omega * b[idx], g, c, sigma, x, y, z);
     } else {
       double au = shifted_point<DIM>(u, g, c, sigma, x, y, z, idx);
-      out[idx] = u[idx] + ((omega * (b[idx] - au)) / d);
+      out[idx] = u[idx] + cd.div<DIM>(omega * (b[idx] - au), g, c, sigma, x, y, z);
     }
   }
 }
@@ -93,13 +94,14 @@ template <int DIM>
 __global__ void __launch_bounds__(256) k_rb(const double* in, const double* __restrict__ b,
                                             double* out, Geo g, OpC c, double sigma,
                                             double omega, int red, int inplace, int zc) {
+  ConstDiag cd;
+  cd.init<DIM>(g, c, sigma);
   PL_FOR_POINTS(g) {
     long long idx = (long long)z * g.sz + (long long)y * g.sy + x;
     bool mine = is_red<DIM>(x, y, z) == (red != 0);
     if (mine) {
-      double d = shifted_diag<DIM>(g, c, sigma, x, y, z);
       double r = b[idx] - shifted_point<DIM>(in, g, c, sigma, x, y, z, idx);
-      out[idx] = in[idx] + ((omega * r) / d);
+      out[idx] = in[idx] + cd.div<DIM>(omega * r, g, c, sigma, x, y, z);
     } else if (!inplace) {
       out[idx] = in[idx];
     }

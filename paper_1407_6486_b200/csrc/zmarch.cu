@@ -556,22 +556,6 @@ __global__ void __launch_bounds__(NTHR) k_z2(const __grid_constant__ CUtensorMap
 
 constexpr int NTHR_RB2 = 256;
 
-// correctly rounded a / b given y = RN(1/b): q0 = RN(a y) is within 1.5 ulp,
-// one Markstein correction makes it faithful, the second exact (Markstein's
-// theorem: y within half an ulp of 1/b, q faithful, remainder exact by FMA).
-// Zeros (sign), subnormals, huge values and non-finite a take the IEEE
-// division.
-__device__ __noinline__ double div_slow(double a, double b) { return a / b; }
-__device__ __forceinline__ double div_const(double a, double b, double y) {
-  double q = a * y;
-  double r = __fma_rn(-b, q, a);
-  q = __fma_rn(r, y, q);
-  r = __fma_rn(-b, q, a);
-  q = __fma_rn(r, y, q);
-  const double aa = fabs(a);
-  if (__builtin_expect(!(aa >= 0x1p-960 && aa <= 0x1p960), 0)) q = div_slow(a, b);
-  return q;
-}
 
 __device__ __forceinline__ double2 lds2(const double* p) {
   return *reinterpret_cast<const double2*>(p);
@@ -1848,6 +1832,10 @@ int zlaunch_jacobi2(const double* u, const double* b, double* out, const Geo& g,
 int zlaunch_rb(const double* u, const double* b, double* out, const Geo& g, const OpC& c,
                double sigma, double omega, cudaStream_t s) {
   double dval = zdiag(c, sigma);
+  if (!diag_div_ok(dval)) {   // outside div_const's range: the one-colour kernels
+    PL_TRY(launch_rb(u, b, out, g, c, sigma, omega, 1, s));
+    return launch_rb(out, b, out, g, c, sigma, omega, 0, s);
+  }
   PL_PRE(K_RB);
   PL_TRY(launch_zrb3(u, b, out, g, c, sigma, omega, dval, s));
   PL_CHECK_LAUNCH(K_RB, 24.0 * g.npts);
