@@ -35,7 +35,9 @@ OpC make_opc(int n, double length, double nu, int order) {
   c.dx2 = powp(dx, 2.0);
   int e;
   double mant = std::frexp(c.dx2, &e);
-  c.pow2 = (mant == 0.5);
+  // a power of two no larger than one: scaling by 1 / dx^2 is then exact and
+  // cannot underflow, which the FMA folds of the stencil kernels rely on
+  c.pow2 = (mant == 0.5) && c.dx2 <= 1.0;
   c.inv_dx2 = 1.0 / c.dx2;
   c.d12 = 12.0 * c.dx2;
   c.nu = nu;

@@ -101,9 +101,17 @@ __device__ __forceinline__ int zchunk_block(int& zc) {
   return blockIdx.z;
 }
 
+// acc + ((m - 2 c0) + p) / dx^2, one axis of the order-2 Laplacian.  For a
+// power-of-two dx^2 <= 1 (OpC::pow2) the scaling by 1 / dx^2 is exact, hence
+// fma(t, 1 / dx^2, acc) == acc + t / dx^2 bit for bit (short of overflow):
+// the reference's value with one dependent operation less per axis.  (Folding
+// m - 2 c0 into an FMA as well is just as exact but costs the red-black sweep
+// registers: 116 instead of 24 bytes of spill loads.)
 template <bool POW2>
-__device__ __forceinline__ double dd2(double x, const OpC& c) {
-  return POW2 ? x * c.inv_dx2 : x / c.dx2;
+__device__ __forceinline__ double axis_acc(double acc, double m, double c0, double p,
+                                           const OpC& c) {
+  const double t = (m - 2.0 * c0) + p;
+  return POW2 ? __fma_rn(t, c.inv_dx2, acc) : acc + t / c.dx2;
 }
 
 // nu * Lap at smem point: planes pm (z-1), pc (z), pp (z+1), row stride W
@@ -112,9 +120,9 @@ __device__ __forceinline__ double lap7(const double* pm, const double* pc, const
                                        int i, const OpC& c) {
   const double c0 = pc[i];
   double acc = 0.0;
-  acc = acc + dd2<POW2>((pm[i] - 2.0 * c0) + pp[i], c);
-  acc = acc + dd2<POW2>((pc[i - W] - 2.0 * c0) + pc[i + W], c);
-  acc = acc + dd2<POW2>((pc[i - 1] - 2.0 * c0) + pc[i + 1], c);
+  acc = axis_acc<POW2>(acc, pm[i], c0, pp[i], c);
+  acc = axis_acc<POW2>(acc, pc[i - W], c0, pc[i + W], c);
+  acc = axis_acc<POW2>(acc, pc[i - 1], c0, pc[i + 1], c);
   return c.nu * acc;
 }
 
@@ -560,6 +568,35 @@ constexpr int NTHR_RB2 = 256;
 __device__ __forceinline__ double2 lds2(const double* p) {
   return *reinterpret_cast<const double2*>(p);
 }
+// shared-window (32-bit) addressing for the sweep's plane loop: address
+// arithmetic stays one integer add and the offsets fold into the instruction
+template <int OFF>
+__device__ __forceinline__ double sld1(unsigned a) {
+  double v;
+  asm volatile("ld.shared.f64 %0, [%1+%2];" : "=d"(v) : "r"(a), "n"(OFF));
+  return v;
+}
+template <int OFF>
+__device__ __forceinline__ double2 sld2(unsigned a) {
+  double2 v;
+  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2+%3];" : "=d"(v.x), "=d"(v.y) : "r"(a), "n"(OFF));
+  return v;
+}
+template <int OFF>
+__device__ __forceinline__ void sst1(unsigned a, double v) {
+  asm volatile("st.shared.f64 [%0+%1], %2;" ::"r"(a), "n"(OFF), "d"(v) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_s(unsigned bar, unsigned parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
 
 // ---------------------------------------------------------------------------
 // k_zrb3: one fused jor-rb sweep (multigrid.py:225-233) with ONE barrier per
@@ -580,6 +617,13 @@ __device__ __forceinline__ double2 lds2(const double* p) {
 // everything else is the reference's expression tree, so the sweep is
 // bit-identical to the one-colour kernels.
 
+// Ring slots carry their own mbarrier: slot s of the u ring is the USL doubles
+// at su + s * USL, the window first and the barrier word at element PU, so a
+// slot offset is all a phase needs (no slot index, no modulo).  The b ring
+// (half as many slots, same stride) follows the u ring.
+constexpr int USL = PU + 16;              // slot stride (a multiple of 128 bytes)
+static_assert(BW == UX && PB <= PU, "the b window shares the u window's row pitch and slot");
+
 struct RbCtx {
   double* su;
   double* sb;
@@ -588,7 +632,7 @@ struct RbCtx {
   bool va, vb;          // pair members in the domain
   double* optr;         // global address of the pair on plane 0
   long long sz;
-  int hu0, hu1, hb0, hb1;   // halo red point per plane parity
+  int hu0, hu1;         // halo red point per plane parity (b: the same - UX)
   bool hv0, hv1;
   OpC c;
   double sigma, omega, dval, dinv;
@@ -596,11 +640,11 @@ struct RbCtx {
 
 template <int RU>
 __device__ __forceinline__ double* rb_u(const RbCtx& k, int p) {
-  return k.su + ((unsigned)(p - k.z0 + 2) % RU) * PU;
+  return k.su + ((unsigned)(p - k.z0 + 2) % RU) * USL;
 }
 template <int RB>
 __device__ __forceinline__ double* rb_b(const RbCtx& k, int q) {
-  return k.sb + ((unsigned)(q - k.z0 + 1) % RB) * PB;
+  return k.sb + ((unsigned)(q - k.z0 + 3) % RB) * USL;   // the slot of u plane q+1, mod RB
 }
 template <int O>
 __device__ __forceinline__ double mem(const double2& v) { return O ? v.y : v.x; }
@@ -613,9 +657,9 @@ __device__ __forceinline__ double rb_relax(const RbCtx& k, double zm, double zp,
                                            double yp, double xm, double xp, double cc,
                                            double bv) {
   double acc = 0.0;
-  acc = acc + dd2<POW2>((zm - 2.0 * cc) + zp, k.c);
-  acc = acc + dd2<POW2>((ym - 2.0 * cc) + yp, k.c);
-  acc = acc + dd2<POW2>((xm - 2.0 * cc) + xp, k.c);
+  acc = axis_acc<POW2>(acc, zm, cc, zp, k.c);
+  acc = axis_acc<POW2>(acc, ym, cc, yp, k.c);
+  acc = axis_acc<POW2>(acc, xm, cc, xp, k.c);
   const double lp = k.c.nu * acc;
   const double r = bv - (cc - k.sigma * lp);
   return cc + div_const(k.omega * r, k.dval, k.dinv);
@@ -631,9 +675,9 @@ template <bool POW2, bool UNIT = false>
 __device__ __forceinline__ Relax rb_fast(const RbCtx& k, double zm, double zp, double ym,
                                          double yp, double xm, double xp, double cc, double bv) {
   double acc = 0.0;
-  acc = acc + dd2<POW2>((zm - 2.0 * cc) + zp, k.c);
-  acc = acc + dd2<POW2>((ym - 2.0 * cc) + yp, k.c);
-  acc = acc + dd2<POW2>((xm - 2.0 * cc) + xp, k.c);
+  acc = axis_acc<POW2>(acc, zm, cc, zp, k.c);
+  acc = axis_acc<POW2>(acc, ym, cc, yp, k.c);
+  acc = axis_acc<POW2>(acc, xm, cc, xp, k.c);
   const double lp = UNIT ? acc : k.c.nu * acc;
   const double r = bv - (cc - k.sigma * lp);
   Relax o;
@@ -652,15 +696,6 @@ __device__ __forceinline__ bool quot_ok(double a) {
   const unsigned e = ((unsigned)__double2hiint(a) >> 20) & 0x7ffu;
   return e - 63u <= 1919u;
 }
-template <bool POW2, int O, bool UNIT = false>
-__device__ __forceinline__ Relax rb_point_fast(const RbCtx& k, const double* pl,
-                                               const double2& um, const double2& uc,
-                                               const double2& up, const double2& bq) {
-  const double xm = O ? uc.x : pl[k.iu - 1];
-  const double xp = O ? pl[k.iu + 2] : uc.y;
-  return rb_fast<POW2, UNIT>(k, mem<O>(um), mem<O>(up), pl[k.iu - UX + O], pl[k.iu + UX + O], xm, xp,
-                       mem<O>(uc), mem<O>(bq));
-}
 
 // update member O of the own pair on plane q (pl); um/uc/up = own pair on
 // planes q-1, q, q+1 (uc updated), bq = b pair on q.  Returns the new value.
@@ -673,6 +708,15 @@ __device__ __forceinline__ double rb_point(const RbCtx& k, const double* pl, con
   return rb_relax<POW2>(k, mem<O>(um), mem<O>(up), pl[k.iu - UX + O], pl[k.iu + UX + O], xm, xp,
                         mem<O>(uc), mem<O>(bq));
 }
+// the same from the thread's own pair address `own` on that plane, with the z
+// neighbours and b as scalars; branch-free part only
+template <bool POW2, int O, bool UNIT>
+__device__ __forceinline__ Relax rb_own(const RbCtx& k, const double* own, double zm, double zp,
+                                        const double2& uc, double bq) {
+  const double xm = O ? uc.x : own[-1];
+  const double xp = O ? own[2] : uc.y;
+  return rb_fast<POW2, UNIT>(k, zm, zp, own[-UX + O], own[UX + O], xm, xp, mem<O>(uc), bq);
+}
 
 // halo red point (threads < 50) on plane q of parity P, shared memory only
 template <bool POW2, int RU, int RB, int P>
@@ -684,55 +728,30 @@ __device__ __forceinline__ void rb_halo(const RbCtx& k, int q) {
   const double* pm = rb_u<RU>(k, q - 1);
   const double* pp = rb_u<RU>(k, q + 1);
   pl[i] = rb_relax<POW2>(k, pm[i], pp[i], pl[i - UX], pl[i + UX], pl[i - 1], pl[i + 1], pl[i],
-                         rb_b<RB>(k, q)[P ? k.hb1 : k.hb0]);
+                         rb_b<RB>(k, q)[i - UX]);
 }
 
-// one phase: red of plane z+2 (if <= R), black of plane z.  PAR = (y + z) & 1
-// of this warp's rows: red member 1 - PAR, black member PAR.  Both updates
-// are evaluated branch-free (independent chains the scheduler interleaves);
-// one warp-wide test sends out-of-range quotients to the IEEE division.
-template <bool POW2, int RU, int RB, int PAR, bool UNIT>
-__device__ __forceinline__ void rb_phase(const RbCtx& k, int z, const double2& U0, double2& U1,
-                                         const double2& U2, double2& U3, const double2& U4,
-                                         const double2& B0, const double2& B2, double* dst) {
-  const int q = z + 2;
-  double* plr = rb_u<RU>(k, q);
-  const double* plb = rb_u<RU>(k, z);
-  Relax rr = rb_point_fast<POW2, 1 - PAR, UNIT>(k, plr, U2, U3, U4, B2);
-  Relax rbk = rb_point_fast<POW2, PAR, UNIT>(k, plb, U0, U1, U2, B0);
-  if (__builtin_expect(!(quot_ok(rr.a) && quot_ok(rbk.a)), 0)) {
-    if (!quot_ok(rr.a)) rr.q = div_slow(rr.a, k.dval);
-    if (!quot_ok(rbk.a)) rbk.q = div_slow(rbk.a, k.dval);
-  }
-  const double vr = rr.cc + rr.q, vb = rbk.cc + rbk.q;
-  if (q <= k.R && (PAR ? k.va : k.vb)) {
-    plr[k.iu + 1 - PAR] = vr;
-    set_mem<1 - PAR>(U3, vr);
-  }
-  const double2 w = PAR ? make_double2(U1.x, vb) : make_double2(vb, U1.y);
-  if (k.vb) *reinterpret_cast<double2*>(dst) = w;   // vb implies va
-  else if (k.va) dst[0] = w.x;
+// both quotient numerators in [2^-960, 2^960): one unsigned compare of the
+// shifted high words (sign dropped, biased exponent 63 .. 1982)
+__device__ __forceinline__ bool quots_ok(double a, double b) {
+  const unsigned ha = ((unsigned)__double2hiint(a) << 1) - (63u << 21);
+  const unsigned hb = ((unsigned)__double2hiint(b) << 1) - (63u << 21);
+  return max(ha, hb) <= ((1919u << 21) | 0x1fffffu);
 }
-
 template <bool POW2, int RU, int RB, int MINB, bool UNIT>
 __global__ void __launch_bounds__(NTHR_RB2, MINB) k_zrb3(const __grid_constant__ CUtensorMap mu,
                                                       const __grid_constant__ CUtensorMap mb,
                                                       double* __restrict__ out, Geo g, OpC c,
                                                       double sigma, double omega, double dval,
                                                       double dinv, int zc) {
-  static_assert(RU >= 6 && RB >= 2, "rings");
+  static_assert(RU >= 6 && RU == 2 * RB, "rings");
   extern __shared__ __align__(128) double sm[];
   RbCtx k;
   k.su = sm;
-  k.sb = sm + RU * PU;
-  unsigned long long* bu = (unsigned long long*)(k.sb + RB * PB);
-  unsigned long long* bbar = bu + RU;
+  k.sb = sm + RU * USL;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TY;
   const int z0 = blockIdx.z * zc, z1 = min(z0 + zc, g.nz);
-  // the in-loop TMA issues go to the first lane of warp 7, which owns no
-  // halo point, so the halo warps 0-1 are not delayed further after a barrier
-  constexpr int issuer = NTHR_RB2 - 32;
   k.z0 = z0;
   k.R = min(z1, g.nz - 1);
   const int uhi = k.R + 1, bhi = k.R;
@@ -741,31 +760,42 @@ __global__ void __launch_bounds__(NTHR_RB2, MINB) k_zrb3(const __grid_constant__
   k.omega = omega;
   k.dval = dval;
   k.dinv = dinv;
+  auto ubar = [&](int s) { return (unsigned long long*)(k.su + s * USL + PU); };
+  auto bbar = [&](int s) { return (unsigned long long*)(k.sb + s * USL + PB); };
   if (tid == 0) {
-    for (int i = 0; i < RU; ++i) mbar_init(bu + i, 1);
-    for (int i = 0; i < RB; ++i) mbar_init(bbar + i, 1);
+    for (int i = 0; i < RU; ++i) mbar_init(ubar(i), 1);
+    for (int i = 0; i < RB; ++i) mbar_init(bbar(i), 1);
     fence_barrier_init();
+    // b plane q rides with u plane q+1: index i = q - z0 + 3, slot i % RB,
+    // barrier parity (i / RB) & 1.  The first b plane (z0-1) has i = 2, so
+    // slots 0 and 1 are first used in their "second" round: complete their
+    // first phase here.
+    mbar_arrive(bbar(0));
+    mbar_arrive(bbar(1));
   }
   __syncthreads();
-  auto issue_u = [&](int p) {
+  // TMA copy of u plane p / b plane q into the slot at element offset o
+  auto load_u = [&](int p, int o) {
     if (p > uhi) return;
-    const int s = (unsigned)(p - z0 + 2) % RU;
-    mbar_expect(bu + s, UX * UY * 8u);
-    tma3(k.su + s * PU, &mu, x0 - 2, y0 - 2, p, bu + s);
+    unsigned long long* bar = (unsigned long long*)(k.su + o + PU);
+    mbar_expect(bar, UX * UY * 8u);
+    tma3(k.su + o, &mu, x0 - 2, y0 - 2, p, bar);
   };
-  auto issue_b = [&](int q) {
+  auto load_b = [&](int q, int o) {
     if (q > bhi) return;
-    const int s = (unsigned)(q - z0 + 1) % RB;
-    mbar_expect(bbar + s, BW * BH * 8u);
-    tma3(k.sb + s * PB, &mb, x0 - 2, y0 - 1, q, bbar + s);
+    unsigned long long* bar = (unsigned long long*)(k.sb + o + PB);
+    mbar_expect(bar, BW * BH * 8u);
+    tma3(k.sb + o, &mb, x0 - 2, y0 - 1, q, bar);
   };
+  auto issue_u = [&](int p) { load_u(p, (int)((unsigned)(p - z0 + 2) % RU) * USL); };
+  auto issue_b = [&](int q) { load_b(q, (int)((unsigned)(q - z0 + 3) % RB) * USL); };
   auto wait_u = [&](int p) {
     const int i = p - z0 + 2;
-    mbar_wait(bu + (unsigned)i % RU, ((unsigned)i / RU) & 1u);
+    mbar_wait(ubar((unsigned)i % RU), ((unsigned)i / RU) & 1u);
   };
   auto wait_b = [&](int q) {
-    const int i = q - z0 + 1;
-    mbar_wait(bbar + (unsigned)i % RB, ((unsigned)i / RB) & 1u);
+    const int i = q - z0 + 3;
+    mbar_wait(bbar((unsigned)i % RB), ((unsigned)i / RB) & 1u);
   };
   if (tid == 0) {
     for (int p = z0 - 2; p < z0 - 2 + RU; ++p) issue_u(p);
@@ -784,7 +814,7 @@ __global__ void __launch_bounds__(NTHR_RB2, MINB) k_zrb3(const __grid_constant__
   const int hid = tid;
   const bool is_halo = hid < 50;
   {
-    int hu[2], hb[2];
+    int hu[2];
     bool hv[2];
 #pragma unroll
     for (int P = 0; P < 2; ++P) {
@@ -794,11 +824,10 @@ __global__ void __launch_bounds__(NTHR_RB2, MINB) k_zrb3(const __grid_constant__
       else if (hid < 42) { xx = -1; yy = 2 * (hid - 34) + P; }
       else { xx = TX; yy = 2 * (hid - 42) + (1 - P); }
       hu[P] = (yy + 2) * UX + xx + 2;
-      hb[P] = (yy + 1) * BW + xx + 2;
       hv[P] = hid >= 0 && hid < 50 && x0 + xx >= 0 && x0 + xx < g.nx && y0 + yy >= 0 &&
               y0 + yy < g.ny;
     }
-    k.hu0 = hu[0]; k.hu1 = hu[1]; k.hb0 = hb[0]; k.hb1 = hb[1];
+    k.hu0 = hu[0]; k.hu1 = hu[1];
     k.hv0 = hv[0]; k.hv1 = hv[1];
   }
   const int wpar = (y0 + row) & 1;   // = warp & 1 (y0 even)
@@ -808,12 +837,12 @@ __global__ void __launch_bounds__(NTHR_RB2, MINB) k_zrb3(const __grid_constant__
   for (int q = z0 - 1; q <= min(z0, bhi); ++q) wait_b(q);
   const double2 zero2 = make_double2(0.0, 0.0);
   double2 Um2 = lds2(rb_u<RU>(k, z0 - 2) + k.iu);
-  double2 U0 = lds2(rb_u<RU>(k, z0 - 1) + k.iu);
-  double2 U1 = lds2(rb_u<RU>(k, z0) + k.iu);
-  double2 U2 = lds2(rb_u<RU>(k, z0 + 1) + k.iu);
-  double2 U3 = z0 + 2 <= uhi ? lds2(rb_u<RU>(k, z0 + 2) + k.iu) : zero2;
+  double2 W0 = lds2(rb_u<RU>(k, z0 - 1) + k.iu);
+  double2 W1 = lds2(rb_u<RU>(k, z0) + k.iu);
+  double2 W2 = lds2(rb_u<RU>(k, z0 + 1) + k.iu);
+  double2 W3 = z0 + 2 <= uhi ? lds2(rb_u<RU>(k, z0 + 2) + k.iu) : zero2;
   const double2 Bm1 = lds2(rb_b<RB>(k, z0 - 1) + k.ib);
-  double2 B0 = lds2(rb_b<RB>(k, z0) + k.ib);
+  const double2 B0 = lds2(rb_b<RB>(k, z0) + k.ib);
   // plane p red member: 1 - ((y + p) & 1); z0 even, so plane z0 has parity wpar
   auto pro_red = [&](int q, const double2& um, double2& uc, const double2& up,
                      const double2& bq, int par) {
@@ -829,69 +858,146 @@ __global__ void __launch_bounds__(NTHR_RB2, MINB) k_zrb3(const __grid_constant__
       if (k.vb) { pl[k.iu + 1] = v; uc.y = v; }
     }
   };
-  pro_red(z0 - 1, Um2, U0, U1, Bm1, 1 - wpar);
-  pro_red(z0, U0, U1, U2, B0, wpar);
+  pro_red(z0 - 1, Um2, W0, W1, Bm1, 1 - wpar);
+  pro_red(z0, W0, W1, W2, B0, wpar);
   if (is_halo) {
     rb_halo<POW2, RU, RB, 1>(k, z0 - 1);
     rb_halo<POW2, RU, RB, 0>(k, z0);
   }
-  if constexpr (RB == 2) {   // b plane z0+1 goes into the slot of z0-1
-    __syncthreads();
-    if (tid == 0) issue_b(z0 + 1);
-  }
   if (z0 + 1 <= bhi) wait_b(z0 + 1);
-  double2 B1 = z0 + 1 <= bhi ? lds2(rb_b<RB>(k, z0 + 1) + k.ib) : zero2;
-  pro_red(z0 + 1, U1, U2, U3, B1, 1 - wpar);
+  const double2 B1 = z0 + 1 <= bhi ? lds2(rb_b<RB>(k, z0 + 1) + k.ib) : zero2;
+  pro_red(z0 + 1, W1, W2, W3, B1, 1 - wpar);
   if (is_halo) rb_halo<POW2, RU, RB, 1>(k, z0 + 1);
   __syncthreads();
   if (tid == 0) {       // u planes z0-2, z0-1 and b planes z0-1 .. z0+1 are dead
     issue_u(z0 - 2 + RU);
     issue_u(z0 - 1 + RU);
-    if constexpr (RB == 2) {
-      issue_b(z0 + 2);
-      issue_b(z0 + 3);
-    } else {
-      for (int q = z0 - 1; q <= z0 + 1; ++q) issue_b(q + RB);
-    }
+    for (int q = z0 - 1; q <= z0 + 1; ++q) issue_b(q + RB);
   }
 
-  // ---- main loop, two planes per trip: U0..U3 = own pair on z-1..z+2,
-  // B0, B1 = b pair on z, z+1
+  // ---- main loop, four planes per trip.  In phase z the registers A, B, C, D
+  // hold the own pair on planes z-1 .. z+2 and plane z+3 is loaded over A once
+  // A's last use is done; four phases rotate the four names back, so no
+  // register moves.  The ring offsets (bytes) of planes z .. z+3 rotate the
+  // same way (advanced by one slot with a compare for the wrap); b plane z+2
+  // sits in the b slot "u slot of z+3, mod RB", whose barrier parity is which
+  // half of the u ring that slot is in.  The b plane's black member waits two
+  // phases in ba / bb.
+  constexpr int SB = USL * 8;                          // slot stride in bytes
+  constexpr int HB = (RU * USL - UX) * 8;              // u-ring point -> same point of the b ring
+  const unsigned smb = saddr(sm);
+  const unsigned tub = smb + k.iu * 8;                 // own pair in slot 0 of the u ring
+  // halo point per plane parity
+  const unsigned hb0 = smb + k.hu0 * 8, hb1 = smb + k.hu1 * 8;
+  // bit 0: the thread that issues the copies (first lane of warp 7, which owns
+  // no halo point); bit 1 / 2: halo thread with a point on even / odd planes
+  const int flags = (tid == NTHR_RB2 - 32 ? 1 : 0) | (is_halo && k.hv0 ? 2 : 0) |
+                    (is_halo && k.hv1 ? 4 : 0);
   auto run = [&](auto par_tag) {
-    constexpr int PA = decltype(par_tag)::value, PB = 1 - PA;
+    constexpr int PA = decltype(par_tag)::value, PB_ = 1 - PA;
+    int o0 = 2 * SB, o1 = 3 * SB, o2 = 4 * SB, o3 = 5 * SB;   // planes z0 .. z0+3
+    unsigned pu = 0;                               // mbarrier parity of plane z+3's copy
     double* dst = k.optr + (long long)z0 * k.sz;   // own pair on plane z
-    for (int z = z0; z < z1; z += 2, dst += 2 * k.sz) {
-      // plane z (parity PA)
-      if (z + 2 <= k.R) {
-        wait_u(z + 3);
-        wait_b(z + 2);
+    double ba = mem<PA>(B0), bb = mem<PB_>(B1);    // black members of b on z, z+1
+    // one phase: red of plane z+2 (if <= R), black of plane z.  PAR = (y + z) & 1
+    // of this warp's rows: red member 1 - PAR, black member PAR.  Both updates
+    // are evaluated branch-free (independent chains the scheduler interleaves);
+    // one warp-wide test sends out-of-range quotients to the IEEE division.
+    //
+    // SYNC: the phase ends with the CTA barrier and the refill of the slots the
+    // last two phases freed.  Reds written in phase z are first read by other
+    // threads in phase z+2, so one barrier per two phases orders every
+    // shared-memory dependence.
+    auto next_u = [](int o) { return o == (RU - 1) * SB ? 0 : o + SB; };
+    auto phase = [&](auto ptag, auto sync_tag, int z, double2& A, double2& B, const double2& C,
+                     double2& D, double& bk, int& oa, int o_b, int o_c, int o_d) {
+      constexpr int PAR = decltype(ptag)::value;
+      constexpr bool SYNC = decltype(sync_tag)::value;
+      constexpr int ZP = PAR ^ PA;                   // parity of plane z (z0 is even)
+      const int q = z + 2;
+      const bool hi = o_d >= RB * SB;                // b slot round = half of the u ring
+      const int ob = (hi ? o_d - RB * SB : o_d);     // b plane z+2's slot
+      if (q <= k.R) {
+        mbar_wait_s(smb + o_d + PU * 8, pu);
+        mbar_wait_s(smb + ob + (RU * USL + PB) * 8, hi ? 1u : 0u);
       }
-      double2 U4 = lds2(rb_u<RU>(k, z + 3) + k.iu);   // stale beyond R: unused
-      const double2 B2 = lds2(rb_b<RB>(k, z + 2) + k.ib);
-      rb_phase<POW2, RU, RB, PA, UNIT>(k, z, U0, U1, U2, U3, U4, B0, B2, dst);
-      if (is_halo) rb_halo<POW2, RU, RB, 0>(k, z + 2);
-      __syncthreads();
-      if (tid == issuer) {
-        issue_u(z + RU);
-        issue_b(z + 2 + RB);
+      const double2 N = sld2<0>(tub + o_d);          // plane z+3 (stale beyond R: unused)
+      const double2 B2 = sld2<HB>(tub + ob);         // b on plane z+2
+      const unsigned ar = tub + o_c, ak = tub + oa;  // own pair on planes z+2, z
+      Relax rr, rk;
+      {
+        constexpr int O = 1 - PAR;
+        const double xm = O ? D.x : sld1<-8>(ar);
+        const double xp = O ? sld1<16>(ar) : D.y;
+        rr = rb_fast<POW2, UNIT>(k, mem<O>(C), mem<O>(N), sld1<(O - UX) * 8>(ar),
+                                 sld1<(O + UX) * 8>(ar), xm, xp, mem<O>(D), mem<O>(B2));
       }
+      {
+        constexpr int O = PAR;
+        const double xm = O ? B.x : sld1<-8>(ak);
+        const double xp = O ? sld1<16>(ak) : B.y;
+        rk = rb_fast<POW2, UNIT>(k, mem<O>(A), mem<O>(C), sld1<(O - UX) * 8>(ak),
+                                 sld1<(O + UX) * 8>(ak), xm, xp, mem<O>(B), bk);
+      }
+      if (__builtin_expect(!quots_ok(rr.a, rk.a), 0)) {
+        if (!quot_ok(rr.a)) rr.q = div_slow(rr.a, k.dval);
+        if (!quot_ok(rk.a)) rk.q = div_slow(rk.a, k.dval);
+      }
+      const double vr = rr.cc + rr.q, vk = rk.cc + rk.q;
+      if (q <= k.R && (PAR ? k.va : k.vb)) {
+        sst1<(1 - PAR) * 8>(ar, vr);
+        set_mem<1 - PAR>(D, vr);
+      }
+      set_mem<PAR>(B, vk);
+      if (k.vb) *reinterpret_cast<double2*>(dst) = B;   // vb implies va
+      else if (k.va) dst[0] = B.x;
+      dst += k.sz;
+      A = N;
+      bk = mem<PAR>(B2);
+      if ((flags & (ZP ? 4 : 2)) && q <= k.R) {      // halo reds of plane z+2
+        const unsigned h = ZP ? hb1 : hb0;
+        const unsigned hc = h + o_c;
+        const double cc = sld1<0>(hc);
+        sst1<0>(hc, rb_relax<POW2>(k, sld1<0>(h + o_b), sld1<0>(h + o_d), sld1<-UX * 8>(hc),
+                                   sld1<UX * 8>(hc), sld1<-8>(hc), sld1<8>(hc), cc,
+                                   sld1<HB>(h + ob)));
+      }
+      // plane z+4 takes the slot after plane z+3's
+      const bool wu = o_d == (RU - 1) * SB;
+      oa = wu ? 0 : o_d + SB;
+      pu ^= wu ? 1u : 0u;
+      if (SYNC) {
+        __syncthreads();
+        if (flags & 1) {
+          // u planes z-1, z and b planes z+1, z+2 are dead.  oa is the slot
+          // of u plane z+4; plane z-1+RU follows it RU-5 slots on.  b plane
+          // q sits in the b slot "u slot of q+1, mod RB".
+          auto half = [](int o) { return (o >= RB * SB ? o - RB * SB : o) >> 3; };
+          int u1 = oa, t = oa;
+#pragma unroll
+          for (int i = 0; i < RU - 5; ++i) u1 = next_u(u1);
+#pragma unroll
+          for (int i = 0; i < RB - 2; ++i) t = next_u(t);   // u plane z+2+RB
+          load_u(z - 1 + RU, u1 >> 3);
+          load_u(z + RU, next_u(u1) >> 3);
+          load_b(z + 1 + RB, half(t));
+          load_b(z + 2 + RB, half(next_u(t)));
+        }
+      }
+    };
+    using TA = std::integral_constant<int, PA>;
+    using TB = std::integral_constant<int, PB_>;
+    using S0 = std::false_type;
+    using S1 = std::true_type;
+    for (int z = z0;; z += 4) {
+      phase(TA{}, S0{}, z, W0, W1, W2, W3, ba, o0, o1, o2, o3);
       if (z + 1 >= z1) break;
-      // plane z+1 (parity PB)
-      if (z + 3 <= k.R) {
-        wait_u(z + 4);
-        wait_b(z + 3);
-      }
-      double2 U5 = lds2(rb_u<RU>(k, z + 4) + k.iu);
-      const double2 B3 = lds2(rb_b<RB>(k, z + 3) + k.ib);
-      rb_phase<POW2, RU, RB, PB, UNIT>(k, z + 1, U1, U2, U3, U4, U5, B1, B3, dst + k.sz);
-      if (is_halo) rb_halo<POW2, RU, RB, 1>(k, z + 3);
-      __syncthreads();
-      if (tid == issuer) {
-        issue_u(z + 1 + RU);
-        issue_b(z + 3 + RB);
-      }
-      U0 = U2; U1 = U3; U2 = U4; U3 = U5;
-      B0 = B2; B1 = B3;
+      phase(TB{}, S1{}, z + 1, W1, W2, W3, W0, bb, o1, o2, o3, o0);
+      if (z + 2 >= z1) break;
+      phase(TA{}, S0{}, z + 2, W2, W3, W0, W1, ba, o2, o3, o0, o1);
+      if (z + 3 >= z1) break;
+      phase(TB{}, S1{}, z + 3, W3, W0, W1, W2, bb, o3, o0, o1, o2);
+      if (z + 4 >= z1) break;
     }
   };
   if (wpar) run(std::integral_constant<int, 1>{});
@@ -1027,9 +1133,9 @@ __global__ void __launch_bounds__(RFW_NT, 4) k_rfw(const __grid_constant__ CUten
         // lap7's expression tree with the column's centre values in registers
         const double c0 = cc_[q];
         double lacc = 0.0;
-        lacc = lacc + dd2<POW2>((cm_[q] - 2.0 * c0) + zcp, c);
-        lacc = lacc + dd2<POW2>((pc[i - FUX] - 2.0 * c0) + pc[i + FUX], c);
-        lacc = lacc + dd2<POW2>((pc[i - 1] - 2.0 * c0) + pc[i + 1], c);
+        lacc = axis_acc<POW2>(lacc, cm_[q], c0, zcp, c);
+        lacc = axis_acc<POW2>(lacc, pc[i - FUX], c0, pc[i + FUX], c);
+        lacc = axis_acc<POW2>(lacc, pc[i - 1], c0, pc[i + 1], c);
         const double lap = UNIT ? lacc : c.nu * lacc;
         const double au = c0 - sigma * lap;
         v = pb[r_ib[q]] - au;
@@ -1669,7 +1775,7 @@ int launch_zrb3(const double* u, const double* b, double* out, const Geo& g, con
   const bool big = g_zrb_ring == 0 && g.N >= 255;
   if (big) zc = zc < 32 ? 32 : zc;
   if (g_zrb_ring == 1 || big) {   // 6 u + 3 b planes, 4 CTAs per SM (register cap 64)
-    size_t smem = ((size_t)6 * PU + (size_t)3 * PB) * 8 + 8 * (6 + 3);
+    size_t smem = (size_t)(6 + 3) * USL * 8;
     auto kern = c.pow2 ? (unit ? k_zrb3<true, 6, 3, 4, true> : k_zrb3<true, 6, 3, 4, false>)
                        : (unit ? k_zrb3<false, 6, 3, 4, true> : k_zrb3<false, 6, 3, 4, false>);
     raise_smem(kern, smem);
@@ -1679,7 +1785,7 @@ int launch_zrb3(const double* u, const double* b, double* out, const Geo& g, con
     kern<<<grid, dim3(NTHR_RB2), smem, s>>>(mu, mb, out, g, c, sigma, omega, dval, dinv, zc);
     return 0;
   }
-  size_t smem = ((size_t)8 * PU + (size_t)4 * PB) * 8 + 8 * (8 + 4);
+  size_t smem = (size_t)(8 + 4) * USL * 8;
   auto kern = c.pow2 ? (unit ? k_zrb3<true, 8, 4, 3, true> : k_zrb3<true, 8, 4, 3, false>)
                      : (unit ? k_zrb3<false, 8, 4, 3, true> : k_zrb3<false, 8, 4, 3, false>);
   raise_smem(kern, smem);
