@@ -1789,6 +1789,9 @@ int launch_zrb3(const double* u, const double* b, double* out, const Geo& g, con
   auto kern = c.pow2 ? (unit ? k_zrb3<true, 8, 4, 3, true> : k_zrb3<true, 8, 4, 3, false>)
                      : (unit ? k_zrb3<false, 8, 4, 3, true> : k_zrb3<false, 8, 4, 3, false>);
   raise_smem(kern, smem);
+  // (wave-fitted shorter chunks are faster for a lone sweep on the L2-resident
+  // levels -- 35 vs 38 us at 127^3 with 10 planes, 25 vs 30 us at 63^3 with 2 --
+  // but not inside the rank-stream wavefront: 7.04-7.18 vs 7.20-7.23 time-steps/s)
   kern<<<grid, dim3(NTHR_RB2), smem, s>>>(mu, mb, out, g, c, sigma, omega, dval, dinv, zc);
   return 0;
 }
