@@ -1191,17 +1191,12 @@ __global__ void __launch_bounds__(RFW_NT, 4) k_rfw(const __grid_constant__ CUten
   }
 }
 
-// k_cubic4: k_cubic3's arithmetic (same passes, same FMA chains) as a skewed
-// three-stage pipeline with one barrier per fine plane: phase t runs the z
-// pass of fine plane z0+t (coarse ring -> zb[t&1]), the y pass of plane
-// z0+t-1 (zb -> yb[(t-1)&1]) and the x pass of plane z0+t-2 (yb -> fine).
-// Coarse windows arrive by TMA (zero-filled outside the domain) into an
-// 8-slot ring, issued as soon as a slot's plane is no longer needed.  Shared
-// memory is static (compile-time addresses); every tap is loaded from a safe
-// index and accumulated by a predicated FMA, so the chains are branch-free
-// and skip absent taps exactly like the reference's sparse rows.
+// Shared pieces of the 3-D cubic interpolation kernel: coarse windows arrive
+// by TMA (zero-filled outside the domain) into an 8-slot ring, issued as soon
+// as a slot's plane is no longer needed; every tap is loaded from a safe index
+// and accumulated by a predicated FMA, so the chains are branch-free and skip
+// absent taps exactly like the reference's sparse rows.
 constexpr int RQ4 = 8;
-constexpr int PY4 = align16(TY * QW);
 
 // acc = chain_{u < n} w[u] * v[u] in tap order (v loaded for every u).
 // g_cubic_pad: absent taps carry weight 0 and are chained too -- the
@@ -1218,198 +1213,21 @@ __device__ __forceinline__ double tap_chain(int n, const double (&w)[4], double 
   return acc;
 }
 
-constexpr int RF4 = 8;                       // fine-tile ring (accumulate mode)
 constexpr int PF4 = TX * TY;
 
-template <bool PAD>
-__global__ void __launch_bounds__(NTHR, 3) k_cubic4(const __grid_constant__ CUtensorMap mc,
-                                                 const __grid_constant__ CUtensorMap mf,
-                                                 double* __restrict__ fine, Geo gf,
-                                                 const int* __restrict__ tcnt,
-                                                 const int* __restrict__ tidx,
-                                                 const double* __restrict__ tw, int zc,
-                                                 int accumulate) {
-  __shared__ __align__(128) double sc[RQ4 * PQ];
-  __shared__ __align__(128) double zb[2 * PQ];
-  __shared__ __align__(128) double yb[2 * PY4];
-  __shared__ __align__(8) unsigned long long bar[RQ4];
-  __shared__ __align__(8) unsigned long long fbar[RF4];
-  __shared__ double s_zw[64 * 4];        // z taps of the chunk's fine planes (zc <= 64)
-  __shared__ int s_zj[64 * 4], s_zn[64];
-  extern __shared__ __align__(128) double sfine[];   // RF4 fine tiles (accumulate)
-  const int tid = threadIdx.y * 32 + threadIdx.x;
-  const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TY;
-  const int z0 = blockIdx.z * zc, z1 = min(z0 + zc, gf.nz);
-  const int n = z1 - z0;
-  const int cx0 = x0 / 2 - 2, cy0 = y0 / 2 - 2;
-  // tap windows are not monotone in the fine index (an odd row reaches one
-  // coarse plane below the even row before it and one above the even row
-  // after it): bounds take the last two planes into account
-  auto first_tap = [&](int iz) { return __ldg(tidx + iz * 4); };
-  auto last_tap = [&](int iz) { return __ldg(tidx + iz * 4 + __ldg(tcnt + iz) - 1); };
-  const int jlo = n > 1 ? min(first_tap(z0), first_tap(z0 + 1)) : first_tap(z0);
-  const int jtop = n > 1 ? max(last_tap(z1 - 1), last_tap(z1 - 2)) : last_tap(z1 - 1);
-  if (tid == 0) {
-    for (int i = 0; i < RQ4; ++i) mbar_init(bar + i, 1);
-    for (int i = 0; i < RF4; ++i) mbar_init(fbar + i, 1);
-    fence_barrier_init();
-  }
-  if (tid < n) {
-    const int iz = z0 + tid, nt = __ldg(tcnt + iz);
-    s_zn[tid] = nt;
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      s_zj[tid * 4 + u] = __ldg(tidx + iz * 4 + min(u, nt - 1));   // absent: last tap
-      s_zw[tid * 4 + u] = u < nt ? __ldg(tw + iz * 4 + u) : 0.0;
-    }
-  }
-  __syncthreads();
-  auto issue_fine = [&](int p) {   // thread 0
-    if (!accumulate || p >= z1) return;
-    const int sl = (p - z0) & (RF4 - 1);
-    mbar_expect(fbar + sl, PF4 * 8u);
-    tma3(sfine + sl * PF4, &mf, x0, y0, p, fbar + sl);
-  };
-  // one thread issues every TMA copy (issued is its private state): the
-  // first lane of warp 7, which has the fewest y-pass entries
-  constexpr int cissuer = NTHR - 32;
-  if (tid == cissuer)
-    for (int p = z0; p < z0 + RF4; ++p) issue_fine(p);
-  int issued = jlo;     // issuing thread: next coarse plane to issue
-  auto issue_upto = [&](int live_lo) {   // thread 0
-    for (; issued <= jtop && issued < live_lo + RQ4; ++issued) {
-      const int sl = (issued - jlo) & (RQ4 - 1);
-      mbar_expect(bar + sl, QW * QH * 8u);
-      tma3(sc + sl * PQ, &mc, cx0, cy0, issued, bar + sl);
-    }
-  };
-  if (tid == cissuer) issue_upto(jlo);
-  int waited = jlo;     // all threads: coarse planes [jlo, waited) have landed
-  // ---- x taps of this thread's fine column
-  const int gx = x0 + threadIdx.x;
-  const bool xin = gx < gf.nx;
-  int xn = 1, xi[4] = {0, 0, 0, 0};
-  double xw[4] = {0.0, 0.0, 0.0, 0.0};
-  if (xin) {
-    xn = __ldg(tcnt + gx);
-#pragma unroll
-    for (int u = 0; u < 4; ++u)
-      if (u < xn) { xi[u] = __ldg(tidx + gx * 4 + u) - cx0; xw[u] = __ldg(tw + gx * 4 + u); }
-#pragma unroll
-    for (int u = 1; u < 4; ++u)
-      if (u >= xn) xi[u] = xi[0];
-  }
-  // ---- y taps of this thread's (up to two) y-pass entries
-  constexpr int PERY = (TY * QW + NTHR - 1) / NTHR;
-  static_assert(PERY == 2, "y pass layout");
-  int yn[2], yk[2], yi[2][4];
-  double yw[2][4];
-#pragma unroll
-  for (int q = 0; q < 2; ++q) {
-    const int k = tid + q * NTHR;
-    const int fy = k / QW, cx = k - fy * QW;
-    const int gy = y0 + fy;
-    yk[q] = k < TY * QW ? k : -1;
-    const bool ok = k < TY * QW && gy < gf.ny;
-    yn[q] = ok ? __ldg(tcnt + gy) : 1;
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      yi[q][u] = cx;
-      yw[q][u] = 0.0;
-      if (ok && u < yn[q]) {
-        yi[q][u] = (__ldg(tidx + gy * 4 + u) - cy0) * QW + cx;
-        yw[q][u] = __ldg(tw + gy * 4 + u);
-      }
-    }
-#pragma unroll
-    for (int u = 1; u < 4; ++u)
-      if (u >= yn[q]) yi[q][u] = yi[q][0];
-  }
-  const bool zent = tid < QW * QH;
-  const int fy0 = threadIdx.y, fy1 = threadIdx.y + 8;
-  const bool r0 = xin && y0 + fy0 < gf.ny, r1 = xin && y0 + fy1 < gf.ny;
-  // fine addresses of the x pass, advanced one plane per phase
-  double* f0 = fine + gf.at(xin ? gx : 0, r0 ? y0 + fy0 : 0, 0) + (long long)(z0 - 2) * gf.sz;
-  double* f1 = fine + gf.at(xin ? gx : 0, r1 ? y0 + fy1 : 0, 0) + (long long)(z0 - 2) * gf.sz;
-  for (int t = 0; t < n + 2; ++t, f0 += gf.sz, f1 += gf.sz) {
-    // ---- x pass of fine plane z0+t-2: fine values first
-    const int ixp = z0 + t - 2;
-    const bool xpass = t >= 2;
-    const double* ftile = sfine + ((ixp - z0) & (RF4 - 1)) * PF4;
-    if (xpass && accumulate) {
-      const int k = ixp - z0;
-      mbar_wait(fbar + (k & (RF4 - 1)), (unsigned)((k / RF4) & 1));
-    }
-    // ---- z pass of fine plane z0+t
-    if (t < n) {
-      const int zn = s_zn[t];
-      int zj[4];
-      double zw[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) { zj[u] = s_zj[t * 4 + u]; zw[u] = s_zw[t * 4 + u]; }
-      for (; waited <= zj[3]; ++waited) {     // zj[3] = last tap (clamped)
-        const int k = waited - jlo;
-        mbar_wait(bar + (k & (RQ4 - 1)), (unsigned)((k / RQ4) & 1));
-      }
-      if (zent) {
-        const double* s0 = sc + ((zj[0] - jlo) & (RQ4 - 1)) * PQ + tid;
-        const double* s1 = sc + ((zj[1] - jlo) & (RQ4 - 1)) * PQ + tid;
-        const double* s2 = sc + ((zj[2] - jlo) & (RQ4 - 1)) * PQ + tid;
-        const double* s3 = sc + ((zj[3] - jlo) & (RQ4 - 1)) * PQ + tid;
-        zb[(t & 1) * PQ + tid] = tap_chain<PAD>(zn, zw, *s0, *s1, *s2, *s3);
-      }
-    }
-    // ---- y pass of fine plane z0+t-1
-    if (t >= 1 && t <= n) {
-      const double* zs = zb + ((t - 1) & 1) * PQ;
-      double* yd = yb + ((t - 1) & 1) * PY4;
-#pragma unroll
-      for (int q = 0; q < 2; ++q)
-        if (yk[q] >= 0)
-          yd[yk[q]] = tap_chain<PAD>(yn[q], yw[q], zs[yi[q][0]], zs[yi[q][1]], zs[yi[q][2]],
-                                zs[yi[q][3]]);
-    }
-    // ---- x pass (finish)
-    if (xpass) {
-      const double* ys = yb + (t & 1) * PY4;      // (t - 2) & 1
-      const double* ya = ys + fy0 * QW;
-      const double* yc = ys + fy1 * QW;
-      const double a0 = tap_chain<PAD>(xn, xw, ya[xi[0]], ya[xi[1]], ya[xi[2]], ya[xi[3]]);
-      const double a1 = tap_chain<PAD>(xn, xw, yc[xi[0]], yc[xi[1]], yc[xi[2]], yc[xi[3]]);
-      if (accumulate) {
-        if (r0) *f0 = ftile[fy0 * TX + threadIdx.x] + a0;
-        if (r1) *f1 = ftile[fy1 * TX + threadIdx.x] + a1;
-      } else {
-        if (r0) *f0 = a0;
-        if (r1) *f1 = a1;
-      }
-    }
-    __syncthreads();
-    if (tid == cissuer && t >= 2) issue_fine(ixp + RF4);   // x pass of ixp done: slot free
-    // coarse planes below the first taps of fine planes z0+t+1, z0+t+2 are dead
-    if (tid == cissuer) {
-      int lo = jtop + 1;
-      if (t + 1 < n) lo = min(lo, s_zj[(t + 1) * 4]);
-      if (t + 2 < n) lo = min(lo, s_zj[(t + 2) * 4]);
-      issue_upto(lo);
-    }
-  }
-}
-
-// ---------------------------------------------------------------------------
 // k_cubic5: fine (+)= P_cubic coarse for 3-D (transfers.py:82-89) with the
 // coincident rows, columns and planes specialised.  A fine index on a coarse
 // point has the single weight 1 in the reference's dense interpolation
 // matrix, so its dgemm chain fma(1, v, 0) + 0 * ... is exactly v + 0.0 for
-// finite v; the other fine indices keep k_cubic4's 4-tap FMA chain in tap
+// finite v; the other fine indices keep the 4-tap FMA chain in tap
 // order.  Fine x columns and y rows alternate between the two kinds, so every
 // thread owns one of each -- an x task is one column pair of one row, a y
 // task one row pair of one coarse column -- and no warp diverges; fine z
 // planes alternate too, and a coincident plane skips the z pass (its y pass
 // reads the coarse window straight from the TMA ring).  Skewed three-stage
-// pipeline as k_cubic4 (z pass of plane t, y pass of t-1, x pass of t-2), one
+// pipeline (z pass of plane t, y pass of t-1, x pass of t-2), one
 // barrier per plane; coarse windows (20 x 12) and, in accumulate mode, the
-// old fine tiles arrive by TMA.  Bit-identical to k_cubic4.
+// old fine tiles arrive by TMA.  Bit-identical to the per-axis pass kernels.
 constexpr int PYB5 = align16(QW * TY);
 constexpr int NT5 = 256;
 constexpr int RF5 = 6;                       // fine-tile ring (accumulate mode)
@@ -1429,7 +1247,7 @@ __global__ void __launch_bounds__(NT5, 4) k_cubic5(const __grid_constant__ CUten
   __shared__ __align__(8) unsigned long long fbar[RF5];
   __shared__ double s_zw[64 * 4];
   __shared__ int s_zj[64 * 4], s_zn[64];
-  extern __shared__ __align__(128) double sfine[];   // RF4 fine tiles (accumulate)
+  extern __shared__ __align__(128) double sfine[];   // RF5 fine tiles (accumulate)
   const int tid = threadIdx.x;
   const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TY;
   const int z0 = blockIdx.z * zc, z1 = min(z0 + zc, gf.nz);
@@ -1815,23 +1633,16 @@ int launch_rfw(const double* u, const double* b, double* coarse, const Geo& g, c
 }  // namespace
 namespace {
 
-int launch_cubic4(const double* coarse, double* fine, const Geo& gf, const int* cnt,
+int launch_cubic5(const double* coarse, double* fine, const Geo& gf, const int* cnt,
                   const int* idx, const double* w, int accumulate, cudaStream_t s) {
   Geo gc = make_geo(3, (gf.N + 1) / 2);
   const int zc = pick_zc(gf);
-  dim3 grid(ceil_div(gf.nx, TX), ceil_div(gf.ny, TY), ceil_div(gf.nz, zc)), block(32, 8);
+  dim3 grid(ceil_div(gf.nx, TX), ceil_div(gf.ny, TY), ceil_div(gf.nz, zc));
   CUtensorMap mc;
   PL_TRY(make_map(&mc, coarse, gc, QW, QH));
   CUtensorMap mf;
   std::memset(&mf, 0, sizeof(mf));
   if (accumulate) PL_TRY(make_map(&mf, fine, gf, TX, TY));
-  size_t smem = accumulate ? sizeof(double) * RF4 * PF4 : 0;
-  static const bool use4 = std::getenv("PL_CUBIC4") != nullptr;   // dev A/B only
-  if (use4) {
-    raise_smem(k_cubic4<true>, smem);
-    k_cubic4<true><<<grid, block, smem, s>>>(mc, mf, fine, gf, cnt, idx, w, zc, accumulate);
-    return 0;
-  }
   const size_t smem5 = accumulate ? sizeof(double) * RF5 * PF4 : 0;
   raise_smem(k_cubic5, smem5);
   const int zc5 = pick_zc_fit(gf, resident_ctas(k_cubic5, NT5, smem5), 2, 5, 8, 64);
@@ -1845,7 +1656,7 @@ int launch_cubic4(const double* coarse, double* fine, const Geo& gf, const int* 
 int zlaunch_cubic(const double* coarse, double* fine, const Geo& gf, const int* cnt,
                   const int* idx, const double* w, int accumulate, cudaStream_t s) {
   PL_PRE(K_INTERP);
-  PL_TRY(launch_cubic4(coarse, fine, gf, cnt, idx, w, accumulate, s));
+  PL_TRY(launch_cubic5(coarse, fine, gf, cnt, idx, w, accumulate, s));
   Geo gc = make_geo(3, (gf.N + 1) / 2);
   PL_CHECK_LAUNCH(K_INTERP, (accumulate ? 16.0 : 8.0) * gf.npts + 8.0 * gc.npts);
   return 0;

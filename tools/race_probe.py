@@ -15,7 +15,7 @@ runs under compute-sanitizer where that tool is available.
 Exercises, at sizes the sanitizer finishes in minutes: the TMA z-marching
 kernels with their mbarrier rings and in-place shared-memory red/black
 updates (k_zrb3 with both ring layouts, k_z1 apply / apply+rhs / residual /
-Jacobi, k_z2, k_rfw, k_cubic4, k_chain_fw, engaged from 31^3 by
+Jacobi, k_z2, k_rfw, k_cubic5, k_chain_fw, engaged from 31^3 by
 PL_OPT_ZMARCH_MIN_N), the cooperative small-level V-cycle (k_mid with its
 grid.sync phases and the one-CTA shared-memory tail) at 63^3, and one
 PFASST block of the same structure.  Each result is compared against the
