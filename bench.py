@@ -284,12 +284,15 @@ def run_ours(args, w):
     _capi.timing_enable(None)
 
     # ---- e2e: host (pinned) buffers through the public API
+    # (input from pinned host memory, result into a reused pinned host buffer:
+    # both copies are inside the timed region, every step)
+    out_pinned = torch.empty(tuple(u0_pinned.shape), dtype=torch.float64).pin_memory()
     barrier()
     te0 = time.perf_counter()
     for _ in range(args.steps):
         r = pfasst_run(levels, u0_pinned, dt * p, p, tol=w["tol"], max_iter=20,
-                       executor=executor, streams=streams)
-        _ = r.u if isinstance(r.u, np.ndarray) else r.u.cpu()
+                       executor=executor, streams=streams, out=out_pinned)
+        assert r.u is out_pinned
     barrier()
     e2e_s = time.perf_counter() - te0
     if world > 1:

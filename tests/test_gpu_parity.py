@@ -298,6 +298,28 @@ def test_pfasst_numpy_drop_in_and_executors():
         pfasst.pfasst_run(levels, a["u0"], t_end, 0)
 
 
+def test_pfasst_out_buffer():
+    """``out=``: the final value lands in a caller-owned host buffer (numpy or
+    a pinned tensor), bit-identical to the array returned without it."""
+    a, m = case("run_cfg3_small")
+    levels = levels_from(m)
+    t_end = m["dt"] * m["p"] * m["blocks"]
+    kw = dict(blocks=m["blocks"], tol=m["tol"], max_iter=20)
+    ref = pfasst.pfasst_run(levels, a["u0"], t_end, m["p"], **kw).u
+    out_np = np.empty_like(a["u0"])
+    r = pfasst.pfasst_run(levels, a["u0"], t_end, m["p"], out=out_np, **kw)
+    assert r.u is out_np and np.array_equal(out_np, ref)
+    out_pin = torch.empty(a["u0"].shape, dtype=torch.float64).pin_memory()
+    r = pfasst.pfasst_run(levels, torch.from_numpy(a["u0"]).pin_memory(), t_end, m["p"],
+                          out=out_pin, **kw)
+    assert r.u is out_pin and np.array_equal(out_pin.numpy(), ref)
+    with pytest.raises(ValueError):
+        pfasst.pfasst_run(levels, a["u0"], t_end, m["p"], out=np.empty(3), **kw)
+    with pytest.raises(ValueError):
+        pfasst.pfasst_run(levels, a["u0"], t_end, m["p"],
+                          out=np.empty(a["u0"].shape, dtype=np.float32), **kw)
+
+
 def test_serial_drivers_and_p1_equivalence():
     a, m = case("serial_drivers")
     lv = [hierarchy.Level(heat.HeatOperator(heat.Grid(1, n)), quadrature.uniform_table(k - 1),
