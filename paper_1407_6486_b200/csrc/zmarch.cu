@@ -760,42 +760,36 @@ __global__ void __launch_bounds__(NTHR_RB2, MINB) k_zrb3(const __grid_constant__
   k.omega = omega;
   k.dval = dval;
   k.dinv = dinv;
+  // b plane q rides with u plane q+1: it sits in the b slot "u slot of plane
+  // q+1, mod RB" and completes on that u slot's barrier, which is armed for the
+  // bytes of both copies -- one wait per phase covers the two planes it needs
   auto ubar = [&](int s) { return (unsigned long long*)(k.su + s * USL + PU); };
-  auto bbar = [&](int s) { return (unsigned long long*)(k.sb + s * USL + PB); };
   if (tid == 0) {
     for (int i = 0; i < RU; ++i) mbar_init(ubar(i), 1);
-    for (int i = 0; i < RB; ++i) mbar_init(bbar(i), 1);
     fence_barrier_init();
-    // b plane q rides with u plane q+1: index i = q - z0 + 3, slot i % RB,
-    // barrier parity (i / RB) & 1.  The first b plane (z0-1) has i = 2, so
-    // slots 0 and 1 are first used in their "second" round: complete their
-    // first phase here.
-    mbar_arrive(bbar(0));
-    mbar_arrive(bbar(1));
   }
   __syncthreads();
   // TMA copy of u plane p / b plane q into the slot at element offset o
+  // TMA copy of u plane p into the slot at element offset o; its barrier also
+  // expects b plane p-1 when that plane exists (p >= z0; p <= uhi <=> p-1 <= bhi)
   auto load_u = [&](int p, int o) {
     if (p > uhi) return;
     unsigned long long* bar = (unsigned long long*)(k.su + o + PU);
-    mbar_expect(bar, UX * UY * 8u);
+    mbar_expect(bar, UX * UY * 8u + (p >= z0 ? BW * BH * 8u : 0u));
     tma3(k.su + o, &mu, x0 - 2, y0 - 2, p, bar);
   };
+  // TMA copy of b plane q into the b slot of the u slot at element offset o
+  // (the slot of u plane q+1), completing on that u slot's barrier
   auto load_b = [&](int q, int o) {
     if (q > bhi) return;
-    unsigned long long* bar = (unsigned long long*)(k.sb + o + PB);
-    mbar_expect(bar, BW * BH * 8u);
-    tma3(k.sb + o, &mb, x0 - 2, y0 - 1, q, bar);
+    unsigned long long* bar = (unsigned long long*)(k.su + o + PU);
+    tma3(k.sb + (o >= RB * USL ? o - RB * USL : o), &mb, x0 - 2, y0 - 1, q, bar);
   };
   auto issue_u = [&](int p) { load_u(p, (int)((unsigned)(p - z0 + 2) % RU) * USL); };
-  auto issue_b = [&](int q) { load_b(q, (int)((unsigned)(q - z0 + 3) % RB) * USL); };
-  auto wait_u = [&](int p) {
+  auto issue_b = [&](int q) { load_b(q, (int)((unsigned)(q - z0 + 3) % RU) * USL); };
+  auto wait_u = [&](int p) {      // u plane p and b plane p-1
     const int i = p - z0 + 2;
     mbar_wait(ubar((unsigned)i % RU), ((unsigned)i / RU) & 1u);
-  };
-  auto wait_b = [&](int q) {
-    const int i = q - z0 + 3;
-    mbar_wait(bbar((unsigned)i % RB), ((unsigned)i / RB) & 1u);
   };
   if (tid == 0) {
     for (int p = z0 - 2; p < z0 - 2 + RU; ++p) issue_u(p);
@@ -834,7 +828,6 @@ __global__ void __launch_bounds__(NTHR_RB2, MINB) k_zrb3(const __grid_constant__
 
   // ---- prologue: reds of planes z0-1 (if >= 0), z0, z0+1 (if <= R)
   for (int p = z0 - 2; p <= min(z0 + 2, uhi); ++p) wait_u(p);
-  for (int q = z0 - 1; q <= min(z0, bhi); ++q) wait_b(q);
   const double2 zero2 = make_double2(0.0, 0.0);
   double2 Um2 = lds2(rb_u<RU>(k, z0 - 2) + k.iu);
   double2 W0 = lds2(rb_u<RU>(k, z0 - 1) + k.iu);
@@ -864,7 +857,6 @@ __global__ void __launch_bounds__(NTHR_RB2, MINB) k_zrb3(const __grid_constant__
     rb_halo<POW2, RU, RB, 1>(k, z0 - 1);
     rb_halo<POW2, RU, RB, 0>(k, z0);
   }
-  if (z0 + 1 <= bhi) wait_b(z0 + 1);
   const double2 B1 = z0 + 1 <= bhi ? lds2(rb_b<RB>(k, z0 + 1) + k.ib) : zero2;
   pro_red(z0 + 1, W1, W2, W3, B1, 1 - wpar);
   if (is_halo) rb_halo<POW2, RU, RB, 1>(k, z0 + 1);
@@ -917,10 +909,7 @@ __global__ void __launch_bounds__(NTHR_RB2, MINB) k_zrb3(const __grid_constant__
       const int q = z + 2;
       const bool hi = o_d >= RB * SB;                // b slot round = half of the u ring
       const int ob = (hi ? o_d - RB * SB : o_d);     // b plane z+2's slot
-      if (q <= k.R) {
-        mbar_wait_s(smb + o_d + PU * 8, pu);
-        mbar_wait_s(smb + ob + (RU * USL + PB) * 8, hi ? 1u : 0u);
-      }
+      if (q <= k.R) mbar_wait_s(smb + o_d + PU * 8, pu);
       const double2 N = sld2<0>(tub + o_d);          // plane z+3 (stale beyond R: unused)
       const double2 B2 = sld2<HB>(tub + ob);         // b on plane z+2
       const unsigned ar = tub + o_c, ak = tub + oa;  // own pair on planes z+2, z
@@ -972,7 +961,6 @@ __global__ void __launch_bounds__(NTHR_RB2, MINB) k_zrb3(const __grid_constant__
           // u planes z-1, z and b planes z+1, z+2 are dead.  oa is the slot
           // of u plane z+4; plane z-1+RU follows it RU-5 slots on.  b plane
           // q sits in the b slot "u slot of q+1, mod RB".
-          auto half = [](int o) { return (o >= RB * SB ? o - RB * SB : o) >> 3; };
           int u1 = oa, t = oa;
 #pragma unroll
           for (int i = 0; i < RU - 5; ++i) u1 = next_u(u1);
@@ -980,8 +968,8 @@ __global__ void __launch_bounds__(NTHR_RB2, MINB) k_zrb3(const __grid_constant__
           for (int i = 0; i < RB - 2; ++i) t = next_u(t);   // u plane z+2+RB
           load_u(z - 1 + RU, u1 >> 3);
           load_u(z + RU, next_u(u1) >> 3);
-          load_b(z + 1 + RB, half(t));
-          load_b(z + 2 + RB, half(next_u(t)));
+          load_b(z + 1 + RB, t >> 3);
+          load_b(z + 2 + RB, next_u(t) >> 3);
         }
       }
     };
