@@ -966,9 +966,9 @@ __global__ void __launch_bounds__(NTHR_RB2, MINB) k_zrb3(const __grid_constant__
           for (int i = 0; i < RU - 5; ++i) u1 = next_u(u1);
 #pragma unroll
           for (int i = 0; i < RB - 2; ++i) t = next_u(t);   // u plane z+2+RB
-          load_u(z - 1 + RU, u1 >> 3);
-          load_u(z + RU, next_u(u1) >> 3);
+          load_u(z - 1 + RU, u1 >> 3);        // the planes phase z+2 waits for first
           load_b(z + 1 + RB, t >> 3);
+          load_u(z + RU, next_u(u1) >> 3);
           load_b(z + 2 + RB, next_u(t) >> 3);
         }
       }
