@@ -1023,8 +1023,7 @@ constexpr int RX = TX + 1, RY = TY + 1, PR = align16(RX * RY);     // residual w
 constexpr int FUX = TX + 4, FUY = TY + 3, PFU = align16(FUX * FUY);  // u window
 constexpr int FBX = TX + 2, FBY = TY + 1, PFB = align16(FBX * FBY);  // b window
 constexpr int RFW_RU = 5, RFW_RB = 3, RFW_NT = 288;
-constexpr int RFW_SMEM = sizeof(double) * (RFW_RU * PFU + RFW_RB * PFB + 2 * PR) +
-                         8 * (RFW_RU + RFW_RB);
+constexpr int RFW_SMEM = sizeof(double) * (RFW_RU * PFU + RFW_RB * PFB + 2 * PR) + 8 * RFW_RU;
 
 template <bool POW2, bool UNIT>
 __global__ void __launch_bounds__(RFW_NT, 4) k_rfw(const __grid_constant__ CUtensorMap mu,
@@ -1037,7 +1036,6 @@ __global__ void __launch_bounds__(RFW_NT, 4) k_rfw(const __grid_constant__ CUten
   double* szb = sb + RFW_RB * PFB;            // z-weighted plane (RX x RY)
   double* syx = szb + PR;                     // y-weighted rows (RX x TY/2)
   unsigned long long* bu = (unsigned long long*)(syx + PR);
-  unsigned long long* bb = bu + RFW_RU;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   constexpr int rfw_issuer = RFW_NT - 32;     // warp 8: fewest residual points, no x pass
   const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TY;
@@ -1047,22 +1045,22 @@ __global__ void __launch_bounds__(RFW_NT, 4) k_rfw(const __grid_constant__ CUten
   const int ulo = p0 - 1, uhi = p1 + 1;       // u planes
   if (tid == 0) {
     for (int i = 0; i < RFW_RU; ++i) mbar_init(bu + i, 1);
-    for (int i = 0; i < RFW_RB; ++i) mbar_init(bb + i, 1);
     fence_barrier_init();
   }
   __syncthreads();
-  // the issuing thread's own ring counters (only it issues)
+  // b plane p is needed in the same phase as u plane p+1 and completes on
+  // that u slot's barrier, armed for the bytes of both copies: one wait per
+  // plane.  (Only the issuing thread computes slots by modulo.)
   auto issue_u = [&](int p) {
     if (p > uhi) return;
     const int s = (p - ulo) % RFW_RU;
-    mbar_expect(bu + s, FUX * FUY * 8u);
+    mbar_expect(bu + s, FUX * FUY * 8u + (p > p0 ? FBX * FBY * 8u : 0u));
     tma3(su + s * PFU, &mu, x0 - 2, y0 - 1, p, bu + s);
   };
   auto issue_b = [&](int p) {
     if (p > p1) return;
     const int s = (p - p0) % RFW_RB;
-    mbar_expect(bb + s, FBX * FBY * 8u);
-    tma3(sb + s * PFB, &mb, x0, y0, p, bb + s);
+    tma3(sb + s * PFB, &mb, x0, y0, p, bu + (p + 1 - ulo) % RFW_RU);
   };
   if (tid == 0) {
     for (int p = ulo; p < ulo + RFW_RU; ++p) issue_u(p);
@@ -1096,15 +1094,14 @@ __global__ void __launch_bounds__(RFW_NT, 4) k_rfw(const __grid_constant__ CUten
   double* cdst = coarse + (c_ok ? gc.at(gcx, gcy, jz0) : 0);
   // ---- u / b ring position of plane p+1 (u) and p (b), advanced per plane
   int us = 2, up_ = 0;          // slot and phase bit of u plane p+1 (= ulo + 2 at p = p0)
-  int bs = 0, bp = 0;           // of b plane p
+  int bs = 0;                   // slot of b plane p
   const double* pm = su;        // u planes p-1, p (slots 0, 1 at p = p0)
   const double* pc = su + PFU;
   // residual of plane p folded into the weights; FIRST: the chunk's first
   // plane (a := v), ODD: t = a + 2 v, else 0.25 (t + v) -> szb, a := v
   auto resid = [&](auto mode_tag, int p) {
     constexpr int MODE = decltype(mode_tag)::value;   // 0 first, 1 odd, 2 even
-    mbar_wait(bu + us, (unsigned)up_);
-    mbar_wait(bb + bs, (unsigned)bp);
+    mbar_wait(bu + us, (unsigned)up_);   // u plane p+1 and b plane p
     const double* pp = su + us * PFU;
     const double* pb = sb + bs * PFB;
 #pragma unroll
@@ -1142,7 +1139,7 @@ __global__ void __launch_bounds__(RFW_NT, 4) k_rfw(const __grid_constant__ CUten
     pm = pc;
     pc = pp;
     if (++us == RFW_RU) { us = 0; up_ ^= 1; }
-    if (++bs == RFW_RB) { bs = 0; bp ^= 1; }
+    if (++bs == RFW_RB) bs = 0;
   };
   auto ypass = [&]() {
     if (ytask) syx[yd] = fw3(szb[yo], szb[yo + RX], szb[yo + 2 * RX]);
