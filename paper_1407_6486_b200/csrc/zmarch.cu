@@ -1157,9 +1157,9 @@ __global__ void __launch_bounds__(RFW_NT, 4) k_rfw(const __grid_constant__ CUten
   };
   auto after = [&](int p) {    // plane p's residuals done: u plane p-1 and b plane p are free
     __syncthreads();
-    if (tid == rfw_issuer && p <= p1) {
-      issue_u(p - 1 + RFW_RU);
-      issue_b(p + RFW_RB);
+    if (p <= p1) {      // the two copies start together: warp 8 issues u, warp 7 b
+      if (tid == rfw_issuer) issue_u(p - 1 + RFW_RU);
+      else if (tid == rfw_issuer - 32) issue_b(p + RFW_RB);
     }
   };
   // phase p0: a of coarse plane jz0
