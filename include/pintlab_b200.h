@@ -83,7 +83,7 @@ const char* pl_last_error(void);
 #define PL_OPT_MID_CTAS 13    /* CTAs of the cooperative small-level kernels (0, default: one per
                                  SM); pfasst_run's rank-stream schedule sets 32 for its duration
                                  so the other ranks' streams keep the remaining SMs */
-#define PL_OPT_ZRB_RING 14    /* one-barrier jor-rb sweep rings: 0 (default) 6 u + 3 b planes,
+#define PL_OPT_ZRB_RING 14    /* fused jor-rb sweep rings: 0 (default) 6 u + 3 b planes,
                                  4 CTAs/SM, z chunks >= 32 from 255^3 up, else 8 u + 4 b planes,
                                  3 CTAs/SM; 1: always 6 + 3; 4: always 8 + 4; bit-identical */
 #define PL_OPT_FUSE_APPLY_RHS 17 /* 1 (default): the sweep's f refresh of node m and the next

@@ -560,7 +560,7 @@ __global__ void __launch_bounds__(NTHR) k_z2(const __grid_constant__ CUtensorMap
 }
 
 // ---------------------------------------------------------------------------
-// helpers of the one-barrier red-black sweep (k_zrb3)
+// helpers of the fused red-black sweep (k_zrb3)
 
 constexpr int NTHR_RB2 = 256;
 
@@ -599,23 +599,25 @@ __device__ __forceinline__ void mbar_wait_s(unsigned bar, unsigned parity) {
 }
 
 // ---------------------------------------------------------------------------
-// k_zrb3: one fused jor-rb sweep (multigrid.py:225-233) with ONE barrier per
-// plane.  Phase z updates the red points of plane z+2 and the black points of
-// plane z: a red point reads only black neighbours (old values) and its own
-// centre, a black point reads the red points of planes z-1..z+1, final since
-// phases z-3..z-1 -- the two sets touch disjoint data.  Thread (row, px) owns
-// the point pair (x0+2px, x0+2px+1) of its row on every plane and carries
-// that pair for planes z-1..z+3 (and b for z..z+2) in registers, so the
-// centre and z-neighbours come from registers and only x/y neighbours are
-// shared-memory loads; the 50 red points of the tile's halo ring are updated
-// by threads 0..49.  Warp w owns tile rows 4(w/2) + (w&1) and that + 2, so
-// (y + z) has one parity per warp and plane: the phase code is instantiated
-// per parity (no selects), the plane loop is unrolled by two, rings are
-// powers of two.  u plane p is read from shared memory in phases p-3 .. p,
-// b plane q in phase q-2 only, so the rings recycle as soon as possible.
-// The division by the constant diagonal is div_const (correctly rounded);
-// everything else is the reference's expression tree, so the sweep is
-// bit-identical to the one-colour kernels.
+// k_zrb3: one fused jor-rb sweep (multigrid.py:225-233) with one CTA barrier
+// per TWO planes.  Phase z updates the red points of plane z+2 and the black
+// points of plane z: a red point reads only black neighbours (old values) and
+// its own centre, a black point reads the red points of planes z-1..z+1,
+// final since phases z-3..z-1 -- the two sets touch disjoint data, and a red
+// value written in phase z is first read by another thread in phase z+2.
+// Thread (row, px) owns the point pair (x0+2px, x0+2px+1) of its row on every
+// plane and carries that pair for planes z-1..z+2 (plus the plane it loads)
+// and the black member of b for z, z+1 in registers, so the centre and
+// z-neighbours come from registers and only x/y neighbours are shared-memory
+// loads; the 50 red points of the tile's halo ring are updated by threads
+// 0..49.  Warp w owns tile rows 4(w/2) + (w&1) and that + 2, so (y + z) has
+// one parity per warp and plane: the phase code is instantiated per parity
+// (no selects) and the plane loop is unrolled by four, which rotates the four
+// register pairs and the four ring offsets by name.  u plane p is read from
+// shared memory in phases p-3 .. p, b plane q in phase q-2 only.  The
+// division by the constant diagonal is the correctly rounded Markstein
+// quotient (div_const's); everything else is the reference's expression tree,
+// so the sweep is bit-identical to the one-colour kernels.
 
 // Ring slots carry their own mbarrier: slot s of the u ring is the USL doubles
 // at su + s * USL, the window first and the barrier word at element PU, so a
