@@ -483,6 +483,35 @@ def test_zrb_variants_equal_plain_kernels(n, length, sigma, nu):
         _capi.set_option(_capi.OPT_ZRB_RING, 0)
 
 
+@pytest.mark.parametrize("n,length", [(32, 1.7), (64, 1.0), (64, 2.5)])
+def test_tma_kernels_small_grids_equal_plain_kernels(n, length):
+    """The smallest grids the TMA kernels accept (one or two ragged tiles per
+    axis, one to four z chunks), with and without a power-of-two dx^2 and
+    nu != 1: the sweeps and the stencil give the plain one-point kernels'
+    results bit for bit, for every ring layout."""
+    rng = np.random.default_rng(n)
+    g = heat.Grid(3, n, length)
+    u = dev(rng.standard_normal(g.shape))
+    b = dev(rng.standard_normal(g.shape))
+    sop = mg.ShiftedOperator(heat.HeatOperator(g, 0.8), 0.03)
+    cfgs = [mg.MgConfig("jor-rb", 1.0, 1, 1), mg.MgConfig("jor-rb", 0.9, 2, 1),
+            mg.MgConfig("jacobi", 2.0 / 3.0, 2, 2)]
+    _capi.set_option(_capi.OPT_ZMARCH, 0)
+    ref = [(mg.smooth(sop, u, b, c, 2), mg.smooth(sop, u, b, c, 3), sop.apply(u)) for c in cfgs]
+    _capi.set_option(_capi.OPT_ZMARCH, 1)
+    _capi.set_option(_capi.OPT_ZMARCH_MIN_N, 31)
+    try:
+        for ring in (0, 1, 4):
+            _capi.set_option(_capi.OPT_ZRB_RING, ring)
+            for c, (r2, r3, ra) in zip(cfgs, ref):
+                assert torch.equal(mg.smooth(sop, u, b, c, 2), r2), (n, ring, c.smoother)
+                assert torch.equal(mg.smooth(sop, u, b, c, 3), r3), (n, ring, c.smoother)
+                assert torch.equal(sop.apply(u), ra)
+    finally:
+        _capi.set_option(_capi.OPT_ZRB_RING, 0)
+        _capi.set_option(_capi.OPT_ZMARCH_MIN_N, 127)
+
+
 @pytest.mark.parametrize("n", [32, 64, 128, 256])
 @pytest.mark.parametrize("pre,post,omega", [(1, 1, 1.0), (2, 0, 0.9), (0, 2, 1.0), (3, 2, 0.8)])
 def test_cooperative_mid_vcycle_equals_separate_launches(n, pre, post, omega):
