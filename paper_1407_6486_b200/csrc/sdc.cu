@@ -193,6 +193,15 @@ bool compact(const Coef& a, NodeCoef& c, int& K) {
 // weights in registers (a, a + 2b, 0.25 (t + c)); the y pass runs one phase
 // later and the x pass two, one barrier per plane.  The result is bit-identical
 // to k_chain + k_fw.
+// next-plane prefetch into L1: the plane loop issues its loads, waits for them
+// and only then meets the barrier, so without it a CTA has one DRAM round trip
+// per plane on its critical path (long scoreboard 10 warp-cycles per issued
+// instruction).  restrict_state 272 -> 244 us, compute_fas 351 -> 341 us at
+// 255^3; prefetching a second plane ahead into L2 as well is slower (261 /
+// 375 us).
+__device__ __forceinline__ void prefetch_plane(const double* p) {
+  asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
+}
 constexpr int CF_TX = 32, CF_TY = 16, CF_RX = CF_TX + 1, CF_RY = CF_TY + 1;
 constexpr int CF_PR = (CF_RX * CF_RY + 15) / 16 * 16;
 constexpr int CF_NT = 288;
@@ -241,7 +250,7 @@ __global__ void __launch_bounds__(CF_NT, 3) k_chain_fw(const double* __restrict_
   // ---- x pass: entries e = tid + 288 i (< R * 128), coarse plane advanced per pass
   constexpr int NX = R * (CF_TX / 2) * (CF_TY / 2), NXI = (NX + CF_NT - 1) / CF_NT;
   // the chain values of plane p at the owned points (k_chain's arithmetic)
-  auto values = [&](int q, long long off, double* v) {
+  auto values = [&](int q, long long off, double* v, bool pf) {
     if (!r_ok[q]) {
 #pragma unroll
       for (int r = 0; r < R; ++r) v[r] = 0.0;
@@ -250,6 +259,10 @@ __global__ void __launch_bounds__(CF_NT, 3) k_chain_fw(const double* __restrict_
     double f[K];
 #pragma unroll
     for (int k = 0; k < K; ++k) f[k] = __ldcs(r_f[q] + c.col[k] * stride + off);
+    if (pf) {
+#pragma unroll
+      for (int k = 0; k < K; ++k) prefetch_plane(r_f[q] + c.col[k] * stride + off + gf.sz);
+    }
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       if constexpr (IDENT) {
@@ -266,13 +279,13 @@ __global__ void __launch_bounds__(CF_NT, 3) k_chain_fw(const double* __restrict_
   };
   // MODE 0: first plane of the chunk (a := v); 1: odd plane (t = a + 2 v);
   // 2: even plane (0.25 (t + v) -> szb, a := v)
-  auto fold = [&](auto mode_tag, long long off) {
+  auto fold = [&](auto mode_tag, long long off, bool pf) {
     constexpr int MODE = decltype(mode_tag)::value;
 #pragma unroll
     for (int q = 0; q < 2; ++q) {
       if (!r_on[q]) continue;
       double v[R];
-      values(q, off, v);
+      values(q, off, v, pf);
 #pragma unroll
       for (int r = 0; r < R; ++r) {
         if (MODE == 0) {
@@ -312,16 +325,16 @@ __global__ void __launch_bounds__(CF_NT, 3) k_chain_fw(const double* __restrict_
   // phase p0, then pairs (odd plane: y pass of the coarse plane finished two
   // phases ago; even plane: x pass)
   long long off = 0;
-  fold(std::integral_constant<int, 0>{}, off);
+  fold(std::integral_constant<int, 0>{}, off, p0 + 1 <= p1);
   __syncthreads();
   for (int p = p0 + 1; p <= p1 + 2; p += 2) {
     const int ph = p - p0;                     // odd
     off += gf.sz;
-    if (p <= p1) fold(std::integral_constant<int, 1>{}, off);
+    if (p <= p1) fold(std::integral_constant<int, 1>{}, off, p + 1 <= p1);
     if (ph >= 3) ypass();                      // y pass of jz = (p - 3) / 2
     __syncthreads();
     off += gf.sz;
-    if (p + 1 <= p1) fold(std::integral_constant<int, 2>{}, off);
+    if (p + 1 <= p1) fold(std::integral_constant<int, 2>{}, off, p + 2 <= p1);
     if (ph + 1 >= 4) xpass();                  // x pass of jz = (p - 3) / 2
     __syncthreads();
   }
@@ -376,6 +389,10 @@ __global__ void __launch_bounds__(CF_NT, 3) k_chain_fw_wide(const double* __rest
           double f[K];
 #pragma unroll
           for (int k = 0; k < K; ++k) f[k] = __ldcs(F + c.col[k] * stride + i);
+          if (p < p1) {
+#pragma unroll
+            for (int k = 0; k < K; ++k) prefetch_plane(F + c.col[k] * stride + i + gf.sz);
+          }
 #pragma unroll
           for (int r = 0; r < R; ++r) {          // k_chain's arithmetic
             if constexpr (IDENT) {
