@@ -710,6 +710,28 @@ def test_cfg3_full_size_two_iterations():
     assert abs(math.fsum(u.ravel().tolist()) - m["u_sum"]) <= 1e-10 * np.abs(u).sum()
 
 
+def test_cfg3_full_size_schedules_and_repeats_identical():
+    """BASELINE config 3 at FULL size, four iterations: the rank-stream
+    wavefront (eight streams of TMA kernels in flight at 255^3 / 127^3 / 63^3),
+    the single-stream schedule and a repeat of the wavefront give the same
+    bits -- final field, residual trace, counts.  A shared-memory race in a
+    fused kernel under load would show here as a differing value."""
+    cfg = mg.MgConfig("jor-rb", 1.0, 1, 1)
+    levels = [hierarchy.Level(heat.HeatOperator(heat.Grid(3, n)), quadrature.uniform_table(k - 1),
+                              cfg, mg.FixedCycles(1), space_interp_order=4)
+              for n, k in ((256, 9), (128, 5), (64, 3))]
+    u0 = dev(heat.seeded_field(heat.Grid(3, 256)))
+    runs = [pfasst.pfasst_run(levels, u0, 8 / 64, 8, tol=1e-10, max_iter=4, streams=st)
+            for st in (True, False, True)]
+    ref = runs[0]
+    assert ref.rank_iterations == [[4] * 8]
+    for r in runs[1:]:
+        assert torch.equal(r.u, ref.u)
+        assert r.rank_iterations == ref.rank_iterations and r.rank_vcycles == ref.rank_vcycles
+        assert [(t.rank, t.iteration, t.level, t.residual) for t in r.trace] == \
+            [(t.rank, t.iteration, t.level, t.residual) for t in ref.trace]
+
+
 @pytest.mark.parametrize("cycles", [1, 2])
 def test_cfg2_full_size(cycles):
     """BASELINE config 2 at FULL size (1023^2 / 511^2, 5 / 3 nodes, Jacobi
