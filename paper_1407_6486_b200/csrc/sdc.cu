@@ -32,6 +32,21 @@ struct NodeCoef {
   double a[MAXN * MAXN];   // R x K, row-major over compacted columns
 };
 
+// byte offsets of the compacted input columns and of the `add` rows, computed
+// on the host (col[k] * stride * 8): a load address is one 64-bit add away
+// from the point's base instead of a multiply by the field stride per load
+struct ColOfs {
+  long long f[MAXN];
+  long long a[MAXN];
+};
+inline ColOfs col_offsets(const NodeCoef& c, int K, long long stride, long long add_stride) {
+  ColOfs o;
+  std::memset(&o, 0, sizeof(o));
+  for (int k = 0; k < K && k < MAXN; ++k) o.f[k] = (long long)c.col[k] * stride * 8;
+  for (int m = 0; m < MAXN; ++m) o.a[m] = (long long)c.addrow[m] * add_stride * 8;
+  return o;
+}
+
 // mode 0: out = scale*chain ; 1: out = scale*chain + add ; 2: out = add - scale*chain
 template <int K>
 __global__ void __launch_bounds__(256) k_chain(const double* __restrict__ in, long long in_stride,
@@ -210,9 +225,8 @@ constexpr int CF_NT = 288;
 // weighting of the selected nodes, several fields in one launch)
 template <int K, int R, bool IDENT = false>
 __global__ void __launch_bounds__(CF_NT, 3) k_chain_fw(const double* __restrict__ F,
-                                                      long long stride, NodeCoef c, double scale,
-                                                      const double* __restrict__ add,
-                                                      long long add_stride, int mode,
+                                                      ColOfs o, NodeCoef c, double scale,
+                                                      const double* __restrict__ add, int mode,
                                                       double* __restrict__ coarse,
                                                       long long cstride, Geo gf, Geo gc,
                                                       int zcc) {
@@ -257,11 +271,13 @@ __global__ void __launch_bounds__(CF_NT, 3) k_chain_fw(const double* __restrict_
       return;
     }
     double f[K];
+    const char* base = reinterpret_cast<const char*>(r_f[q] + off);
 #pragma unroll
-    for (int k = 0; k < K; ++k) f[k] = __ldcs(r_f[q] + c.col[k] * stride + off);
+    for (int k = 0; k < K; ++k) f[k] = __ldcs(reinterpret_cast<const double*>(base + o.f[k]));
     if (pf) {
+      const char* nxt = base + gf.sz * 8;
 #pragma unroll
-      for (int k = 0; k < K; ++k) prefetch_plane(r_f[q] + c.col[k] * stride + off + gf.sz);
+      for (int k = 0; k < K; ++k) prefetch_plane(reinterpret_cast<const double*>(nxt + o.f[k]));
     }
 #pragma unroll
     for (int r = 0; r < R; ++r) {
@@ -272,7 +288,9 @@ __global__ void __launch_bounds__(CF_NT, 3) k_chain_fw(const double* __restrict_
 #pragma unroll
         for (int k = 0; k < K; ++k) a = __fma_rn(c.a[r * K + k], f[k], a);
         double t = scale * a;
-        if (mode == 1) t = t + r_a[q][c.addrow[r] * add_stride + off];
+        if (mode == 1)
+          t = t + *reinterpret_cast<const double*>(reinterpret_cast<const char*>(r_a[q] + off) +
+                                                   o.a[r]);
         v[r] = t;
       }
     }
@@ -344,9 +362,8 @@ __global__ void __launch_bounds__(CF_NT, 3) k_chain_fw(const double* __restrict_
 // loop keeps fewer values live (no spills at 72 registers)
 template <int K, int R, bool IDENT = false>
 __global__ void __launch_bounds__(CF_NT, 3) k_chain_fw_wide(const double* __restrict__ F,
-                                                      long long stride, NodeCoef c, double scale,
-                                                      const double* __restrict__ add,
-                                                      long long add_stride, int mode,
+                                                      ColOfs o, NodeCoef c, double scale,
+                                                      const double* __restrict__ add, int mode,
                                                       double* __restrict__ coarse,
                                                       long long cstride, Geo gf, Geo gc,
                                                       int zcc) {
@@ -376,8 +393,11 @@ __global__ void __launch_bounds__(CF_NT, 3) k_chain_fw_wide(const double* __rest
   for (int q = 0; q < 2; ++q)
 #pragma unroll
     for (int r = 0; r < R; ++r) acc[q][r] = 0.0;
-  const int cx = tid & 15, cy = (tid >> 4) & 7;
-  for (int p = p0; p <= p1 + 2; ++p) {
+  // y pass: thread tid < 264 owns window entry (yy, xx) of every row set r
+  const bool ytask = tid < CF_RX * (CF_TY / 2);
+  const int y_src = 2 * (tid / CF_RX) * CF_RX + (tid - (tid / CF_RX) * CF_RX);
+  long long pofs = (long long)p0 * gf.sz * 8;      // byte offset of plane p
+  for (int p = p0; p <= p1 + 2; ++p, pofs += gf.sz * 8) {
     const int ph = p - p0;
     if (p <= p1) {
 #pragma unroll
@@ -385,14 +405,11 @@ __global__ void __launch_bounds__(CF_NT, 3) k_chain_fw_wide(const double* __rest
         if (r_k[q] < 0) continue;
         double v[R];
         if (r_ok[q]) {
-          const long long i = r_g[q] + (long long)p * gf.sz;
+          const char* base = reinterpret_cast<const char*>(F + r_g[q]) + pofs;
           double f[K];
 #pragma unroll
-          for (int k = 0; k < K; ++k) f[k] = __ldcs(F + c.col[k] * stride + i);
-          if (p < p1) {
-#pragma unroll
-            for (int k = 0; k < K; ++k) prefetch_plane(F + c.col[k] * stride + i + gf.sz);
-          }
+          for (int k = 0; k < K; ++k)
+            f[k] = __ldcs(reinterpret_cast<const double*>(base + o.f[k]));
 #pragma unroll
           for (int r = 0; r < R; ++r) {          // k_chain's arithmetic
             if constexpr (IDENT) {
@@ -403,7 +420,9 @@ __global__ void __launch_bounds__(CF_NT, 3) k_chain_fw_wide(const double* __rest
 #pragma unroll
             for (int k = 0; k < K; ++k) a = __fma_rn(c.a[r * K + k], f[k], a);
             double t = scale * a;
-            if (mode == 1) t = t + add[c.addrow[r] * add_stride + i];
+            if (mode == 1)
+              t = t + *reinterpret_cast<const double*>(
+                          reinterpret_cast<const char*>(add + r_g[q]) + pofs + o.a[r]);
             v[r] = t;
           }
         } else {
@@ -423,12 +442,11 @@ __global__ void __launch_bounds__(CF_NT, 3) k_chain_fw_wide(const double* __rest
         }
       }
     }
-    if ((ph & 1) == 1 && ph >= 3) {          // y pass of jz = (p - 3) / 2
-      for (int e = tid; e < R * CF_RX * (CF_TY / 2); e += CF_NT) {
-        const int r = e / (CF_RX * (CF_TY / 2)), k = e - r * (CF_RX * (CF_TY / 2));
-        const int yy = k / CF_RX, xx = k - yy * CF_RX;
-        const double* zc = szb + r * CF_PR + 2 * yy * CF_RX + xx;
-        syx[r * CF_PR + k] = fw3(zc[0], zc[CF_RX], zc[2 * CF_RX]);
+    if ((ph & 1) == 1 && ph >= 3 && ytask) {          // y pass of jz = (p - 3) / 2
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const double* zc = szb + r * CF_PR + y_src;
+        syx[r * CF_PR + tid] = fw3(zc[0], zc[CF_RX], zc[2 * CF_RX]);
       }
     }
     if ((ph & 1) == 0 && ph >= 4) {          // x pass of jz = (p - 4) / 2
@@ -444,8 +462,6 @@ __global__ void __launch_bounds__(CF_NT, 3) k_chain_fw_wide(const double* __rest
     }
     __syncthreads();
   }
-  (void)cx;
-  (void)cy;
 }
 
 #define PL_K_DISPATCH(K, CALL)                                                    \
@@ -561,6 +577,7 @@ int launch_fw_select(const double* fine, long long stride, const int* idx, int n
   std::memset(&c, 0, sizeof(c));
   c.rows = nsel;
   for (int j = 0; j < nsel; ++j) c.col[j] = idx[j];
+  const ColOfs ofs = col_offsets(c, nsel, stride, 0);
   Geo gc = make_geo(3, (gf.N + 1) / 2);
   const int zcc = 8;
   dim3 grid(ceil_div(gf.nx, CF_TX), ceil_div(gf.ny, CF_TY), ceil_div(gc.nz, zcc));
@@ -571,8 +588,8 @@ int launch_fw_select(const double* fine, long long stride, const int* idx, int n
     size_t smem = sizeof(double) * 2 * RR * CF_PR;                                          \
     cudaFuncSetAttribute(k_chain_fw<RR, RR, true>,                                          \
                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);           \
-    k_chain_fw<RR, RR, true><<<grid, block, smem, s>>>(fine, stride, c, 1.0, nullptr, 0, 0, \
-                                                       coarse, cstride, gf, gc, zcc);       \
+    k_chain_fw<RR, RR, true><<<grid, block, smem, s>>>(fine, ofs, c, 1.0, nullptr, 0, coarse,  \
+                                                       cstride, gf, gc, zcc);               \
   } while (0)
   switch (nsel) {
     case 1: FS_CALL(1); break; case 2: FS_CALL(2); break; case 3: FS_CALL(3); break;
@@ -597,6 +614,7 @@ int launch_chain_fw(const double* F, long long stride, const Coef& a, double sca
   if (!compact(a, c, K)) return -1;
   if (add_rows)
     for (int m = 0; m < a.rows; ++m) c.addrow[m] = add_rows[m];
+  const ColOfs ofs = col_offsets(c, K, stride, add_stride);
   Geo gc = make_geo(3, (gf.N + 1) / 2);
   const int zcc = 8;
   dim3 grid(ceil_div(gf.nx, CF_TX), ceil_div(gf.ny, CF_TY), ceil_div(gc.nz, zcc));
@@ -610,8 +628,7 @@ int launch_chain_fw(const double* F, long long stride, const Coef& a, double sca
     size_t smem = sizeof(double) * 2 * RR * CF_PR;                                            \
     auto kern = KK * RR <= 25 ? k_chain_fw<KK, RR> : k_chain_fw_wide<KK, RR>;                 \
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);       \
-    kern<<<grid, block, smem, s>>>(F, stride, c, scale, add, add_stride, mode, coarse,        \
-                                   cstride, gf, gc, zcc);                                     \
+    kern<<<grid, block, smem, s>>>(F, ofs, c, scale, add, mode, coarse, cstride, gf, gc, zcc); \
   } while (0)
 #define CF_R(KK)                                   \
   switch (a.rows) {                                \
