@@ -410,6 +410,11 @@ __global__ void __launch_bounds__(CF_NT, 3) k_chain_fw_wide(const double* __rest
 #pragma unroll
           for (int k = 0; k < K; ++k)
             f[k] = __ldcs(reinterpret_cast<const double*>(base + o.f[k]));
+          if (p < p1) {
+            const char* nxt = base + gf.sz * 8;
+#pragma unroll
+            for (int k = 0; k < K; ++k) prefetch_plane(reinterpret_cast<const double*>(nxt + o.f[k]));
+          }
 #pragma unroll
           for (int r = 0; r < R; ++r) {          // k_chain's arithmetic
             if constexpr (IDENT) {
