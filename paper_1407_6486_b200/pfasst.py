@@ -636,24 +636,38 @@ def _run_block(blk, engine, exchange):
         blk.iterations_loop()
 
 
-_ENGINE_CACHE: list = []     # [(key, engine)] of the most recent pfasst_run
+_ENGINE_CACHE: list = []     # [(key, engine)] of the most recent pfasst_run configuration
 
 
 def _device_engine(levels, dt, ranks, streams):
-    """The DeviceEngine of the previous pfasst_run when it ran the same level
+    """The DeviceEngine of a previous pfasst_run when it ran the same level
     objects, dt, ranks and stream mode on this device: its per-rank state
     buffers are re-spread rather than reallocated, so repeated runs keep their
     device addresses (and the captured sweep graphs keyed by them).  One
-    engine is kept; a run with other levels replaces it."""
-    key = (tuple(id(lv) for lv in levels), float(dt), tuple(ranks), bool(streams),
-           torch.cuda.current_device())
-    if _ENGINE_CACHE and _ENGINE_CACHE[0][0] == key and \
-            all(a is b for a, b in zip(_ENGINE_CACHE[0][1].levels, levels)):
-        return _ENGINE_CACHE[0][1]
-    _ENGINE_CACHE.clear()
+    engine per schedule (rank streams / single stream) of the most recent
+    configuration is kept, the second only while more than a quarter of the
+    device memory stays free; a run with other levels, dt or ranks replaces
+    them."""
+    base = (tuple(id(lv) for lv in levels), float(dt), tuple(ranks),
+            torch.cuda.current_device())
+    key = base + (bool(streams),)
+    for k, eng in _ENGINE_CACHE:
+        if k == key and all(a is b for a, b in zip(eng.levels, levels)):
+            return eng
+    if any(k[:-1] != base or not all(a is b for a, b in zip(e.levels, levels))
+           for k, e in _ENGINE_CACHE):
+        _ENGINE_CACHE.clear()
     engine = DeviceEngine(levels, dt, ranks, streams=streams)
     _ENGINE_CACHE.append((key, engine))
     return engine
+
+
+def _trim_engines():
+    """Keep the other schedule's engine only while memory is plentiful."""
+    if len(_ENGINE_CACHE) > 1:
+        free, total = torch.cuda.mem_get_info()
+        if free < 0.25 * total:
+            del _ENGINE_CACHE[0]
 
 
 def release_engines():
@@ -777,6 +791,8 @@ def pfasst_run(levels, u0, t_end: float, p: int, blocks: int = 1, tol: float = 1
         result.trace.extend(sorted(tr, key=lambda r: (r.iteration, r.rank, r.level)))
         result.final_values.append([like_input(v, host) if isinstance(v, torch.Tensor)
                                     else v for v in blk.final_values])
+    if engine_factory is DeviceEngine:
+        _trim_engines()
     if out is not None and isinstance(u, torch.Tensor) and u.is_cuda:
         out_t.copy_(u)             # synchronous: the caller may read out right away
         result.u = out
