@@ -287,66 +287,100 @@ __global__ void __launch_bounds__(NTHR) k_z1(const __grid_constant__ CUtensorMap
     for (int p = z0 - 1; p <= z0 + PREF; ++p) issue(p);
   wait(z0 - 1);
   wait(z0);
+  // ---- per-thread constants: two points (rows ty and ty + 8) of column tx.
+  // Window indices, validity and the 32-bit element offset of the point on
+  // plane z (every field here has fewer than 2^31 elements: checked at launch)
+  // are computed once; the plane loop advances them by additions only, the
+  // ring slot of plane z+1 and its barrier parity incrementally, and carries
+  // the points' own z column (u on planes z-1, z) in registers.
   const int gx = x0 + threadIdx.x;
+  const int i0 = (threadIdx.y + 1) * HX + threadIdx.x + 2;
+  constexpr int DI = 8 * HX;                          // second point: 8 rows down
+  const bool ok0 = gx < g.nx && y0 + (int)threadIdx.y < g.ny;
+  const bool ok1 = gx < g.nx && y0 + (int)threadIdx.y + 8 < g.ny;
+  unsigned gi = (unsigned)g.at(gx < g.nx ? gx : 0, min(y0 + (int)threadIdx.y, g.ny - 1), z0);
+  const unsigned dgi = 8u * (unsigned)g.sy, gsz = (unsigned)g.sz;
+  const int ib0 = threadIdx.y * TX + threadIdx.x;     // b window (no halo)
+  int sn = 2;                                         // slot of plane z+1 (z = z0: plane z0+1)
+  unsigned pn = 0;                                    // its barrier parity
+  const double* pm = su;                              // planes z-1, z: slots 0, 1
+  const double* pc = su + P1;
+  const double* pbc = sb + P0;                        // b of plane z
+  double um0 = 0.0, um1 = 0.0, uc0 = 0.0, uc1 = 0.0;
+  if constexpr (NEED_U) {
+    um0 = pm[i0]; um1 = pm[i0 + DI];
+    uc0 = pc[i0]; uc1 = pc[i0 + DI];
+  }
   // Z_APPLY_RHS: f_next, s (and tau) of plane z+1 are loaded into registers
   // while plane z computes, so their DRAM latency overlaps a whole plane
   constexpr bool RHS = OP == Z_APPLY_RHS;
   constexpr int NR = RHS ? 2 : 1;
   double cf[NR], cs[NR], ct[NR];
-  auto rhs_load = [&](int z, double* f, double* sv, double* t) {
+  auto rhs_load = [&](bool live, unsigned o, double* f, double* sv, double* t) {
 #pragma unroll
     for (int r = 0; r < NR; ++r) {
-      const int gy = y0 + threadIdx.y + 8 * r;
       f[r] = sv[r] = t[r] = 0.0;
-      if (z < z1 && gx < g.nx && gy < g.ny) {
-        const long long gi = g.at(gx, gy, z);
-        f[r] = __ldcs(ra.fn + gi);
-        sv[r] = __ldcs(ra.s + gi);
-        if (ra.t0) t[r] = __ldcs(ra.t1 + gi) - __ldcs(ra.t0 + gi);
+      if (live && (r ? ok1 : ok0)) {
+        const unsigned q = o + (r ? dgi : 0u);
+        f[r] = __ldcs(ra.fn + q);
+        sv[r] = __ldcs(ra.s + q);
+        if (ra.t0) t[r] = __ldcs(ra.t1 + q) - __ldcs(ra.t0 + q);
       }
     }
   };
-  if constexpr (RHS) rhs_load(z0, cf, cs, ct);
-  for (int z = z0; z < z1; ++z) {
+  if constexpr (RHS) rhs_load(true, gi, cf, cs, ct);
+  // lap7's expression tree with the own column from registers
+  auto lap = [&](const double* qc, const double* qp, int i, double m, double c0) {
+    double acc = 0.0;
+    acc = axis_acc<POW2>(acc, m, c0, qp[i], c);
+    acc = axis_acc<POW2>(acc, qc[i - HX], c0, qc[i + HX], c);
+    acc = axis_acc<POW2>(acc, qc[i - 1], c0, qc[i + 1], c);
+    return c.nu * acc;
+  };
+  for (int z = z0; z < z1; ++z, gi += gsz) {
     double nf[NR], ns[NR], nt[NR];
-    if constexpr (RHS) rhs_load(z + 1, nf, ns, nt);
-    wait(z + 1);
-    const int sc = (z - z0 + 1) % RING;
-    const double* pc = su + sc * P1;
-    const double* pm = su + ((z - z0) % RING) * P1;
-    const double* pp = su + ((z - z0 + 2) % RING) * P1;
-    const double* pb = sb + sc * P0;
+    if constexpr (RHS) rhs_load(z + 1 < z1, gi + gsz, nf, ns, nt);
+    mbar_wait(bar + sn, pn);
+    const double* pp = su + sn * P1;
 #pragma unroll
     for (int r = 0; r < 2; ++r) {
-      const int ly = threadIdx.y + 8 * r;
-      const int gy = y0 + ly;
-      if (gx < g.nx && gy < g.ny) {
-        const int i = (ly + 1) * HX + threadIdx.x + 2;
-        const long long gi = g.at(gx, gy, z);
+      const int i = i0 + r * DI;
+      double& um = r ? um1 : um0;
+      double& uc = r ? uc1 : uc0;
+      double up = 0.0;
+      if constexpr (NEED_U) up = pp[i];
+      if (r ? ok1 : ok0) {
+        const unsigned q = gi + (r ? dgi : 0u);
         double v;
         if constexpr (OP == Z_APPLY_RHS) {
           // sdc.py:112 f refresh of this node, then sdc.py:102-104 for the next
-          double rr = (pc[i] - ra.dtm * cf[r & (NR - 1)]) + cs[r & (NR - 1)];
+          double rr = (uc - ra.dtm * cf[r & (NR - 1)]) + cs[r & (NR - 1)];
           if (ra.t0) rr = rr + ct[r & (NR - 1)];
-          ra.r[gi] = rr;
-          v = lap7<POW2, HX>(pm, pc, pp, i, c);
+          ra.r[q] = rr;
+          v = lap(pc, pp, i, um, uc);
         } else if (OP == Z_JAC0) {
-          v = 0.0 + ((omega * pb[ly * TX + threadIdx.x]) / dval);
+          v = 0.0 + ((omega * pbc[ib0 + r * 8 * TX]) / dval);
         } else {
-          double lap = lap7<POW2, HX>(pm, pc, pp, i, c);
+          const double l = lap(pc, pp, i, um, uc);
           if (OP == Z_APPLY) {
-            v = lap;
+            v = l;
           } else {
-            double au = pc[i] - sigma * lap;
-            double bb = pb[ly * TX + threadIdx.x];
-            v = OP == Z_RESID ? bb - au : pc[i] + ((omega * (bb - au)) / dval);
+            const double au = uc - sigma * l;
+            const double bb = pbc[ib0 + r * 8 * TX];
+            v = OP == Z_RESID ? bb - au : uc + ((omega * (bb - au)) / dval);
           }
         }
-        out[gi] = v;
+        out[q] = v;
       }
+      um = uc;
+      uc = up;
     }
     __syncthreads();   // slot of plane z-1 is free
     if (tid == 0) issue(z + PREF + 1);
+    pm = pc;
+    pc = pp;
+    pbc = sb + sn * P0;
+    if (++sn == RING) { sn = 0; pn ^= 1u; }
     if constexpr (RHS) {
 #pragma unroll
       for (int r = 0; r < NR; ++r) {
@@ -1523,6 +1557,10 @@ int launch_z1(const double* u, const double* b, double* out, const Geo& g, const
               double sigma, double omega, double dval, cudaStream_t s,
               const RhsArgs& ra = RhsArgs{}) {
   constexpr int HX = TX + 4, HY = TY + 2, RING = PREF1 + 3;
+  if (g.nstore >= (1LL << 31)) {     // the kernel indexes a field with 32-bit element offsets
+    set_error("k_z1: field of %lld elements exceeds 2^31", g.nstore);
+    return 2;
+  }
   CUtensorMap mu, mb;
   std::memset(&mu, 0, sizeof(mu));
   std::memset(&mb, 0, sizeof(mb));
