@@ -47,29 +47,42 @@ inline ColOfs col_offsets(const NodeCoef& c, int K, long long stride, long long 
   return o;
 }
 
+// the chain kernels index a field's points with 32 bits
+inline bool small_field(long long npts) {
+  if (npts < (1LL << 31)) return true;
+  set_error("chain kernel: %lld points exceed 2^31", npts);
+  return false;
+}
+
 // mode 0: out = scale*chain ; 1: out = scale*chain + add ; 2: out = add - scale*chain
 template <int K>
-__global__ void __launch_bounds__(256) k_chain(const double* __restrict__ in, long long in_stride,
+__global__ void __launch_bounds__(256) k_chain(const double* __restrict__ in, ColOfs o,
                                                double* out, long long out_stride,
                                                NodeCoef c, double scale, long long npts,
                                                const double* add,   // may alias out
-                                               long long add_stride, int mode) {
-  long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= npts) return;
+                                               int mode) {
+  // fields have fewer than 2^31 elements (checked at launch): one 32-bit point
+  // index, column / row addresses by 64-bit adds of host-computed byte offsets
+  const unsigned i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (unsigned)npts) return;
+  const char* pin = reinterpret_cast<const char*>(in + i);
   double v[K];
 #pragma unroll
-  for (int k = 0; k < K; ++k) v[k] = in[c.col[k] * in_stride + i];
+  for (int k = 0; k < K; ++k) v[k] = *reinterpret_cast<const double*>(pin + o.f[k]);
+  char* po = reinterpret_cast<char*>(out + i);
+  const char* pa = reinterpret_cast<const char*>(add + i);
+  const long long ob = out_stride * 8;
 #pragma unroll
   for (int m = 0; m < MAXN; ++m) {
-    if (m < c.rows) {
-      double acc = 0.0;
+    if (m >= c.rows) break;
+    double acc = 0.0;
 #pragma unroll
-      for (int k = 0; k < K; ++k) acc = __fma_rn(c.a[m * K + k], v[k], acc);
-      double r = scale * acc;
-      if (mode == 1) r = r + add[c.addrow[m] * add_stride + i];
-      else if (mode == 2) r = add[c.addrow[m] * add_stride + i] - r;
-      out[m * out_stride + i] = r;
-    }
+    for (int k = 0; k < K; ++k) acc = __fma_rn(c.a[m * K + k], v[k], acc);
+    double r = scale * acc;
+    if (mode == 1) r = r + *reinterpret_cast<const double*>(pa + o.a[m]);
+    else if (mode == 2) r = *reinterpret_cast<const double*>(pa + o.a[m]) - r;
+    *reinterpret_cast<double*>(po) = r;
+    po += ob;
   }
 }
 
@@ -79,23 +92,28 @@ __global__ void __launch_bounds__(256) k_chain(const double* __restrict__ in, lo
 // load of the point is issued before the first chain; R == 0: runtime rows
 template <int K, int R = 0>
 __global__ void __launch_bounds__(256) k_resmax(const double* __restrict__ Y,
-                                                const double* __restrict__ F, long long stride,
+                                                const double* __restrict__ F, ColOfs o,
+                                                long long stride,
                                                 const double* __restrict__ y0,
                                                 const double* __restrict__ tau, NodeCoef q,
                                                 double dt, long long npts,
                                                 unsigned long long* out) {
-  long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const unsigned i = blockIdx.x * blockDim.x + threadIdx.x;   // < 2^31 (checked at launch)
   unsigned long long best = 0ull;
-  if (i < npts) {
+  if (i < (unsigned)npts) {
+    const char* pf = reinterpret_cast<const char*>(F + i);
     double f[K];
 #pragma unroll
-    for (int k = 0; k < K; ++k) f[k] = F[q.col[k] * stride + i];
+    for (int k = 0; k < K; ++k) f[k] = *reinterpret_cast<const double*>(pf + o.f[k]);
     const double base = y0[i];
     constexpr int NR = R > 0 ? R : MAXN;
+    const long long sb = stride * 8;
+    const char* py = reinterpret_cast<const char*>(Y + i);
+    const char* pt = reinterpret_cast<const char*>(tau + i);
     double yv[R > 0 ? R : 1];
     if constexpr (R > 0) {
 #pragma unroll
-      for (int m = 0; m < R; ++m) yv[m] = Y[m * stride + i];
+      for (int m = 0; m < R; ++m) yv[m] = *reinterpret_cast<const double*>(py + m * sb);
     }
 #pragma unroll
     for (int m = 0; m < NR; ++m) {
@@ -103,8 +121,9 @@ __global__ void __launch_bounds__(256) k_resmax(const double* __restrict__ Y,
         double acc = 0.0;
 #pragma unroll
         for (int k = 0; k < K; ++k) acc = __fma_rn(q.a[m * K + k], f[k], acc);
-        double r = (base + dt * acc) - (R > 0 ? yv[R > 0 ? m : 0] : Y[m * stride + i]);
-        if (tau) r = r + tau[m * stride + i];
+        double r = (base + dt * acc) -
+                   (R > 0 ? yv[R > 0 ? m : 0] : *reinterpret_cast<const double*>(py + m * sb));
+        if (tau) r = r + *reinterpret_cast<const double*>(pt + m * sb);
         unsigned long long bits = (unsigned long long)__double_as_longlong(fabs(r));
         best = bits > best ? bits : best;
       }
@@ -127,25 +146,28 @@ __global__ void __launch_bounds__(256) k_resmax(const double* __restrict__ Y,
 template <int K>
 __global__ void __launch_bounds__(256) k_delta_chain(const double* __restrict__ ynew,
                                                      const double* __restrict__ yold,
-                                                     long long stride, NodeCoef pt,
+                                                     ColOfs o, NodeCoef pt,
                                                      double* __restrict__ out,
                                                      long long out_stride, long long npts) {
-  long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= npts) return;
+  const unsigned i = blockIdx.x * blockDim.x + threadIdx.x;   // < 2^31 (checked at launch)
+  if (i >= (unsigned)npts) return;
+  const char* pn = reinterpret_cast<const char*>(ynew + i);
+  const char* po = reinterpret_cast<const char*>(yold + i);
   double d[K];
 #pragma unroll
-  for (int k = 0; k < K; ++k) {
-    long long o = pt.col[k] * stride + i;
-    d[k] = ynew[o] - yold[o];
-  }
+  for (int k = 0; k < K; ++k)
+    d[k] = *reinterpret_cast<const double*>(pn + o.f[k]) -
+           *reinterpret_cast<const double*>(po + o.f[k]);
+  char* pout = reinterpret_cast<char*>(out + i);
+  const long long ob = out_stride * 8;
 #pragma unroll
   for (int m = 0; m < MAXN; ++m) {
-    if (m < pt.rows) {
-      double acc = 0.0;
+    if (m >= pt.rows) break;
+    double acc = 0.0;
 #pragma unroll
-      for (int k = 0; k < K; ++k) acc = __fma_rn(pt.a[m * K + k], d[k], acc);
-      out[m * out_stride + i] = acc;
-    }
+    for (int k = 0; k < K; ++k) acc = __fma_rn(pt.a[m * K + k], d[k], acc);
+    *reinterpret_cast<double*>(pout) = acc;
+    pout += ob;
   }
 }
 
@@ -489,11 +511,12 @@ int launch_chain_ex(const double* in, long long in_stride, double* out, long lon
   if (!compact(a, c, K)) return -1;
   if (add_rows)
     for (int m = 0; m < a.rows; ++m) c.addrow[m] = add_rows[m];
+  if (!small_field(npts)) return -1;
+  const ColOfs ofs = col_offsets(c, K, in_stride, add_stride);
   const int blocks = ceil_div(npts, 256);
   PL_PRE(K_QUAD);
-#define CALL(KK)                                                                          \
-  k_chain<KK><<<blocks, 256, 0, s>>>(in, in_stride, out, out_stride, c, scale, npts, add, \
-                                     add_stride, mode)
+#define CALL(KK) \
+  k_chain<KK><<<blocks, 256, 0, s>>>(in, ofs, out, out_stride, c, scale, npts, add, mode)
   PL_K_DISPATCH(K, CALL);
 #undef CALL
   PL_CHECK_LAUNCH(K_QUAD, 8.0 * npts * (K + a.rows + (mode ? a.rows : 0)));
@@ -519,7 +542,8 @@ int launch_resmax(const double* Y, const double* F, long long stride, const doub
                   double* out_dev, cudaStream_t s) {
   NodeCoef c;
   int K;
-  if (!compact(q, c, K)) return -1;
+  if (!compact(q, c, K) || !small_field(npts)) return -1;
+  const ColOfs ofs = col_offsets(c, K, stride, 0);
   cudaError_t e = cudaMemsetAsync(out_dev, 0, sizeof(double), s);
   if (e != cudaSuccess) return cuda_status(e, "memset");
   const int blocks = ceil_div(npts, 256);
@@ -527,7 +551,7 @@ int launch_resmax(const double* Y, const double* F, long long stride, const doub
   PL_PRE(K_RESMAX);
   if (c.rows == K + 1 && K >= 1 && K <= 8) {   // Q of M+1 nodes: K = M used columns
 #define CALLR(KK) \
-  k_resmax<KK, KK + 1><<<blocks, 256, 0, s>>>(Y, F, stride, y0, tau, c, dt, npts, o)
+  k_resmax<KK, KK + 1><<<blocks, 256, 0, s>>>(Y, F, ofs, stride, y0, tau, c, dt, npts, o)
     switch (K) {
       case 1: CALLR(1); break; case 2: CALLR(2); break; case 3: CALLR(3); break;
       case 4: CALLR(4); break; case 5: CALLR(5); break; case 6: CALLR(6); break;
@@ -535,7 +559,8 @@ int launch_resmax(const double* Y, const double* F, long long stride, const doub
     }
 #undef CALLR
   } else {
-#define CALL(KK) k_resmax<KK><<<blocks, 256, 0, s>>>(Y, F, stride, y0, tau, c, dt, npts, o)
+#define CALL(KK) \
+  k_resmax<KK><<<blocks, 256, 0, s>>>(Y, F, ofs, stride, y0, tau, c, dt, npts, o)
     PL_K_DISPATCH(K, CALL);
 #undef CALL
   }
@@ -548,11 +573,12 @@ int launch_delta_chain(const double* ynew, const double* yold, long long stride,
                        cudaStream_t s) {
   NodeCoef c;
   int K;
-  if (!compact(pt, c, K)) return -1;
+  if (!compact(pt, c, K) || !small_field(npts)) return -1;
+  const ColOfs ofs = col_offsets(c, K, stride, 0);
   const int blocks = ceil_div(npts, 256);
   PL_PRE(K_CORR);
 #define CALL(KK) \
-  k_delta_chain<KK><<<blocks, 256, 0, s>>>(ynew, yold, stride, c, out, out_stride, npts)
+  k_delta_chain<KK><<<blocks, 256, 0, s>>>(ynew, yold, ofs, c, out, out_stride, npts)
   PL_K_DISPATCH(K, CALL);
 #undef CALL
   PL_CHECK_LAUNCH(K_CORR, 8.0 * npts * (2 * K + pt.rows));
