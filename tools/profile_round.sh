@@ -24,3 +24,10 @@ timeout 900 ncu --set full --clock-control none --import-source on \
     -k regex:"k_zrb3|k_rfw|k_cubic5|k_mid|k_z1" -c 10 -o gpurun_out/top255_full $KB \
     > gpurun_out/ncu_full.log 2>&1
 echo "full capture rc=$?"
+# the other fine-level kernels (one launch each): an SDC sweep, the residual, the FAS machinery
+KO="python tools/kernel_bench.py --n 256 --reps 1 --only sweep_M8_jorrb_V11,residual_max_M8,restrict_state,compute_fas,coarse_correction"
+timeout 200 $KO > /dev/null 2>&1 && \
+timeout 900 ncu --set full --clock-control none --import-source on \
+    -k regex:"k_z1|k_cubic5|k_prolong3_cell|k_chain|k_resmax|k_delta_chain" -c 160 -o gpurun_out/other255_full $KO \
+    > gpurun_out/ncu_other.log 2>&1
+echo "other kernels capture rc=$?"

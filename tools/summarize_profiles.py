@@ -79,6 +79,10 @@ def main():
     caps = {"top255_full.ncu-rep": "top kernels at 255^3 (k_zrb3 one-barrier red-black sweep, "
                                    "k_rfw residual+restriction, k_cubic5 cubic correction, "
                                    "k_mid cooperative small levels)",
+            "other255_full.ncu-rep": "the other fine-level kernels at 255^3 in kernel_bench's order "
+                                     "(restrict_state: k_chain_fw + coarse k_z1 applies; FAS: "
+                                     "k_chain_fw_wide + k_chain; then the correction, the residual and "
+                                     "one SDC sweep as far as the launch count reaches)",
             "zrb255_full.ncu-rep": "dominant kernel: fused red-black sweep (TMA), 255^3 "
                                    "(first launch: with fused prolongation? see kernel name)",
             "jacobi512.ncu-rep": "round-1 baseline: one-point-per-thread Jacobi sweep, 511^3",
